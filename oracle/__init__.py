@@ -1,0 +1,196 @@
+"""ctypes wrapper of the fp64 CPU oracle (oracle/pget_oracle.c).
+
+TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs may import this package.  The product
+path (paper_2604_26745_b200) never imports it and shares no code with it.
+
+Every function takes the geometry descriptor as a dict with the fields of
+pget_geometry_desc and numpy arrays (any float dtype; widened to fp64 exactly).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "pget_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+ST_CG = 16  # offset of the CG residual norms in the stats vector
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (fp64, OpenMP, no FMA contraction)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math",
+                               "-fPIC", "-shared", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+class _Desc(C.Structure):
+    _fields_ = [("n_px", C.c_int), ("n_angles", C.c_int), ("n_banks", C.c_int),
+                ("n_det", C.c_int), ("n_subrays", C.c_int), ("subray_sigma", C.c_double),
+                ("step_px", C.c_double), ("bank1_shift", C.c_double), ("batch", C.c_int)]
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        _lib = C.CDLL(_LIB)
+        P = C.c_void_p
+        for name, args in [
+            ("orc_tables", [P] * 8), ("orc_forward", [P] * 4), ("orc_forward_naive", [P] * 4),
+            ("orc_jvp", [P] * 7), ("orc_vjp", [P] * 6), ("orc_n_t", [P]),
+            ("orc_gn_cg_step", [P, P, P, P, C.c_double, C.c_double, C.c_int, P, P, P]),
+            ("orc_apply_H", [P, P, P, C.c_double, C.c_double, P, P]),
+        ]:
+            f = getattr(_lib, name)
+            f.argtypes = args
+            f.restype = C.c_int
+        _lib.orc_laplacian.argtypes = [C.c_int, C.c_int, P, P]
+        _lib.orc_laplacian.restype = None
+        _lib.orc_ray_quadrature.argtypes = [C.c_int, P, P, C.c_double]
+        _lib.orc_ray_quadrature.restype = C.c_double
+        _lib.orc_ray_adjoint.argtypes = [C.c_int, P, P, C.c_double, P, P]
+        _lib.orc_ray_adjoint.restype = None
+        _lib.orc_threads.restype = C.c_int
+    return _lib
+
+
+def _desc(g: dict) -> _Desc:
+    return _Desc(int(g["n_px"]), int(g["n_angles"]), int(g.get("n_banks", 2)), int(g.get("n_det", 91)),
+                 int(g.get("n_subrays", 1)), float(g.get("subray_sigma", 0.4)),
+                 float(g.get("step_px", 0.5)), float(g.get("bank1_shift", 0.0)), int(g.get("batch", 1)))
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def threads() -> int:
+    return _load().orc_threads()
+
+
+def sino_shape(g):
+    d = _desc(g)
+    return (d.batch, d.n_angles, d.n_banks, d.n_det)
+
+
+def img_shape(g):
+    d = _desc(g)
+    return (d.batch, d.n_px, d.n_px)
+
+
+def tables(g: dict) -> dict:
+    """All O1 tables: angles, dirs (cos,sin), offsets, weights, tlat (h, Delta, T), n_t, clip."""
+    lib = _load()
+    d = _desc(g)
+    nA, nB, nd, J = d.n_angles, d.n_banks, d.n_det, d.n_subrays
+    out = dict(angles=np.zeros(nA), dirs=np.zeros((nA, nB, 2)), offsets=np.zeros((nB, nd, J)),
+               weights=np.zeros(J), tlat=np.zeros(3), clip=np.zeros((nA, nB, nd, J, 2), np.int32))
+    nt = C.c_int(0)
+    lib.orc_tables(C.byref(d), _p(out["angles"]), _p(out["dirs"]), _p(out["offsets"]),
+                   _p(out["weights"]), _p(out["tlat"]), C.byref(nt), _p(out["clip"]))
+    out["n_t"] = nt.value
+    return out
+
+
+def forward(g, lam, mu, naive=False):
+    lib = _load()
+    d = _desc(g)
+    lam, mu = _f64(lam), _f64(mu)
+    y = np.zeros(sino_shape(g))
+    rc = (lib.orc_forward_naive if naive else lib.orc_forward)(C.byref(d), _p(lam), _p(mu), _p(y))
+    assert rc == 0, rc
+    return y
+
+
+def jvp(g, lam, mu, dlam, dmu, with_y=False):
+    lib = _load()
+    d = _desc(g)
+    a = [_f64(x) for x in (lam, mu, dlam, dmu)]
+    y = np.zeros(sino_shape(g))
+    dy = np.zeros(sino_shape(g))
+    rc = lib.orc_jvp(C.byref(d), *[_p(x) for x in a], _p(y), _p(dy))
+    assert rc == 0, rc
+    return (y, dy) if with_y else dy
+
+
+def vjp(g, lam, mu, w):
+    lib = _load()
+    d = _desc(g)
+    lam, mu, w = _f64(lam), _f64(mu), _f64(w)
+    gl = np.zeros(img_shape(g))
+    gm = np.zeros(img_shape(g))
+    rc = lib.orc_vjp(C.byref(d), _p(lam), _p(mu), _p(w), _p(gl), _p(gm))
+    assert rc == 0, rc
+    return gl, gm
+
+
+def laplacian(u):
+    lib = _load()
+    u = _f64(u)
+    if u.ndim == 2:
+        u = u[None]
+    out = np.zeros_like(u)
+    lib.orc_laplacian(u.shape[-1], u.shape[0], _p(u), _p(out))
+    return out
+
+
+def apply_H(g, lam, mu, alpha, beta, p_lam, p_mu):
+    lib = _load()
+    d = _desc(g)
+    lam, mu = _f64(lam), _f64(mu)
+    p = np.concatenate([_f64(p_lam).ravel(), _f64(p_mu).ravel()])
+    out = np.zeros_like(p)
+    rc = lib.orc_apply_H(C.byref(d), _p(lam), _p(mu), alpha, beta, _p(p), _p(out))
+    assert rc == 0
+    n = p.size // 2
+    return out[:n].reshape(img_shape(g)), out[n:].reshape(img_shape(g))
+
+
+def gn_cg_step(g, lam, mu, y, alpha, beta, n_cg):
+    """One LM iteration (O7).  Returns (s_lam, s_mu, stats dict)."""
+    lib = _load()
+    d = _desc(g)
+    lam, mu, y = _f64(lam), _f64(mu), _f64(y)
+    sl = np.zeros(img_shape(g))
+    sm = np.zeros(img_shape(g))
+    st = np.zeros(ST_CG + n_cg + 1)
+    rc = lib.orc_gn_cg_step(C.byref(d), _p(lam), _p(mu), _p(y), float(alpha), float(beta), int(n_cg),
+                            _p(sl), _p(sm), _p(st))
+    assert rc == 0, rc
+    return sl, sm, stats_dict(st, n_cg)
+
+
+def stats_dict(st, n_cg):
+    return dict(f=st[0], misfit=st[1], reg=st[2], grad_norm=st[3], pred=st[4], f_trial=st[5],
+                rho=st[6], accepted=bool(st[7]), beta_next=st[8], n_cg_done=int(st[9]),
+                breakdown=int(st[10]), beta_min=st[11], js2=st[12], als2=st[13], bs=st[14],
+                cg_res=np.array(st[ST_CG:ST_CG + n_cg + 1]))
+
+
+def ray_quadrature(lam_s, mu_s, delta):
+    lib = _load()
+    l, m = _f64(lam_s), _f64(mu_s)
+    return lib.orc_ray_quadrature(len(l), _p(l), _p(m), float(delta))
+
+
+def ray_adjoint(lam_s, mu_s, delta):
+    lib = _load()
+    l, m = _f64(lam_s), _f64(mu_s)
+    dl = np.zeros_like(l)
+    dm = np.zeros_like(l)
+    lib.orc_ray_adjoint(len(l), _p(l), _p(m), float(delta), _p(dl), _p(dm))
+    return dl, dm

@@ -1,0 +1,607 @@
+/*
+ * pget_oracle.c -- plain, slow, fp64 CPU oracle of the PGET hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no
+ * code, header, table or constant generator with the CUDA product path
+ * (paper_2604_26745_b200/csrc); it is written directly from the definitions
+ * below, with direct loops over rays and samples and no blocking or fusion.
+ *
+ * Definitions (which restate the paper):
+ *   F(lam,mu)(s,th) = int lam(s th_perp + t th) exp(-B mu(s th_perp + t th, th)) dt,
+ *   B mu(x,th)      = int_0^inf mu(x + tau th) dtau
+ *       -- PAPER.md:48-54, Sec. 2.1, eq:fwd_model (ray-sampled quadrature, readings Q7-Q9)
+ *   D_lam F[dlam] = F(dlam, mu);  D_mu F[dmu] = -F(lam B(dmu), mu)
+ *       -- PAPER.md:55-59, eq:frechet
+ *   adjoint F'^*[w]  -- used at PAPER.md:231, 277 (Thm 10.3, proof of Prop. 1)
+ *   f(u) = 1/2 ||F(u)-y||^2 + alpha/2 (||L lam||^2 + ||L mu||^2)
+ *       -- PAPER.md:144-148 eq:lma_objective with reading Q10
+ *   LM step (J^T J + alpha L^T L + beta I) s = -grad f, m_k, rho_k
+ *       -- PAPER.md:160-180 eq:m-function, eq:LMA-step; PAPER.md:248 eq:rho_agreement
+ *       -- inner solver: plain CG (reading Q12) instead of the paper's SGP.
+ *
+ * Parity pins: see tests/test_oracle_*.py (P1-P12 of SURVEY.md §8(c.4)).
+ * Compile: gcc -O2 -fopenmp -ffp-contract=off -fPIC -shared (no fast-math).
+ */
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+typedef struct {
+    int n_px, n_angles, n_banks, n_det, n_subrays;
+    double subray_sigma, step_px, bank1_shift;
+    int batch;
+} orc_desc;
+
+/* ------------------------------------------------------------------ O1 geometry */
+typedef struct {
+    double h, delta, T;
+    int n_t;
+} orc_lattice;
+
+static orc_lattice o1_lattice(const orc_desc* g)
+{
+    orc_lattice L;
+    L.h = 2.0 / g->n_px;                               /* h = 2/N            */
+    L.delta = g->step_px * L.h;                        /* Delta = step_px*h  */
+    double m = ceil((sqrt(2.0) + L.h) / L.delta);      /* T = Delta*ceil((sqrt2+h)/Delta) */
+    L.T = L.delta * m;
+    L.n_t = 2 * (int)m;                                /* n_t = 2T/Delta     */
+    return L;
+}
+
+static double o1_theta(const orc_desc* g, int a) { return 2.0 * M_PI * a / g->n_angles; }
+
+/* direction of bank b at angle a: phi = theta_a + b*pi; omega = (cos phi, sin phi) */
+static void o1_dir(const orc_desc* g, int a, int b, double* c, double* s)
+{
+    double phi = o1_theta(g, a) + b * M_PI;
+    *c = cos(phi);
+    *s = sin(phi);
+}
+
+/* offset sigma_{b,d,j} = s_d (+ bank1_shift*p for bank 1) + delta_j */
+static double o1_offset(const orc_desc* g, int b, int d, int j)
+{
+    int nd = g->n_det, J = g->n_subrays;
+    double p = 2.0 / (nd - 1);
+    double s = (double)(2 * d - (nd - 1)) / (double)(nd - 1);
+    if (b == 1) s = s + g->bank1_shift * p;
+    double dj = (double)(2 * j + 1 - J) / (double)(2 * J) * p;
+    return s + dj;
+}
+
+static void o1_weights(const orc_desc* g, double* w)
+{
+    int J = g->n_subrays;
+    double p = 2.0 / (g->n_det - 1);
+    double sp = g->subray_sigma * p;
+    double sum = 0.0;
+    for (int j = 0; j < J; ++j) {
+        double dj = (double)(2 * j + 1 - J) / (double)(2 * J) * p;
+        w[j] = exp(-(dj * dj) / (2.0 * sp * sp));
+        sum += w[j];
+    }
+    for (int j = 0; j < J; ++j) w[j] = w[j] / sum;
+}
+
+/* slab clip of x(t) = sigma*omega_perp + t*omega against |x|,|y| <= 1 + h/2 */
+static void o1_clip(const orc_desc* g, const orc_lattice* L, double c, double s, double sigma,
+                    int* ilo, int* ihi)
+{
+    double bb = 1.0 + L->h / 2.0;
+    double om[2] = {c, s};
+    double op[2] = {-s, c};
+    double tin = -INFINITY, tout = INFINITY;
+    for (int k = 0; k < 2; ++k) {
+        double base = sigma * op[k];
+        if (om[k] == 0.0) {
+            if (fabs(base) > bb) { tin = INFINITY; tout = -INFINITY; }
+        } else {
+            double t1 = (-bb - base) / om[k];
+            double t2 = (bb - base) / om[k];
+            double lo = t1 < t2 ? t1 : t2, hi = t1 < t2 ? t2 : t1;
+            if (lo > tin) tin = lo;
+            if (hi < tout) tout = hi;
+        }
+    }
+    if (!(tin <= tout)) { *ilo = 0; *ihi = -1; return; }
+    double lo = ceil((tin + L->T) / L->delta - 0.5);
+    double hi = floor((tout + L->T) / L->delta - 0.5);
+    if (lo < 0.0) lo = 0.0;
+    if (hi > (double)(L->n_t - 1)) hi = (double)(L->n_t - 1);
+    if (lo > hi) { *ilo = 0; *ihi = -1; return; }
+    *ilo = (int)lo;
+    *ihi = (int)hi;
+}
+
+int orc_n_t(const orc_desc* g) { return o1_lattice(g).n_t; }
+
+/* Export every O1 table (for the bit-exact comparison with the library, pin P1). */
+int orc_tables(const orc_desc* g, double* angles, double* dirs, double* offsets, double* weights,
+               double* tlat, int* n_t, int* clip)
+{
+    orc_lattice L = o1_lattice(g);
+    int nA = g->n_angles, nB = g->n_banks, nd = g->n_det, J = g->n_subrays;
+    for (int a = 0; a < nA; ++a) angles[a] = o1_theta(g, a);
+    for (int a = 0; a < nA; ++a)
+        for (int b = 0; b < nB; ++b) o1_dir(g, a, b, &dirs[(a * nB + b) * 2], &dirs[(a * nB + b) * 2 + 1]);
+    for (int b = 0; b < nB; ++b)
+        for (int d = 0; d < nd; ++d)
+            for (int j = 0; j < J; ++j) offsets[(b * nd + d) * J + j] = o1_offset(g, b, d, j);
+    o1_weights(g, weights);
+    tlat[0] = L.h; tlat[1] = L.delta; tlat[2] = L.T;
+    *n_t = L.n_t;
+    for (int a = 0; a < nA; ++a)
+        for (int b = 0; b < nB; ++b) {
+            double c, s;
+            o1_dir(g, a, b, &c, &s);
+            for (int d = 0; d < nd; ++d)
+                for (int j = 0; j < J; ++j) {
+                    size_t r = (((size_t)a * nB + b) * nd + d) * J + j;
+                    o1_clip(g, &L, c, s, o1_offset(g, b, d, j), &clip[2 * r], &clip[2 * r + 1]);
+                }
+        }
+    return 0;
+}
+
+/* ------------------------------------------------------------------ O2 sampling */
+/* pixel-index coordinates of sample i: u = (x+1)/h - 1/2, v = (y+1)/h - 1/2 */
+static void o2_pos(const orc_lattice* L, double c, double s, double sigma, int i, double* u, double* v)
+{
+    double t = -L->T + (i + 0.5) * L->delta;
+    double x = sigma * (-s) + t * c;
+    double y = sigma * c + t * s;
+    *u = (x + 1.0) / L->h - 0.5;
+    *v = (y + 1.0) / L->h - 0.5;
+}
+
+static double o2_pix(const double* img, int N, int j, int i)
+{
+    if (i < 0 || i >= N || j < 0 || j >= N) return 0.0;
+    return img[(size_t)j * N + i];
+}
+
+/* bilinear interpolation with zero outside the grid */
+static double o2_sample(const double* img, int N, double u, double v)
+{
+    double fi = floor(u), fj = floor(v);
+    int i0 = (int)fi, j0 = (int)fj;
+    double fu = u - fi, fv = v - fj;
+    return (1.0 - fu) * (1.0 - fv) * o2_pix(img, N, j0, i0) + fu * (1.0 - fv) * o2_pix(img, N, j0, i0 + 1)
+         + (1.0 - fu) * fv * o2_pix(img, N, j0 + 1, i0) + fu * fv * o2_pix(img, N, j0 + 1, i0 + 1);
+}
+
+/* transpose of o2_sample: scatter val to the 4 neighbours, dropping out-of-grid ones */
+static void o2_scatter(double* img, int N, double u, double v, double val)
+{
+    double fi = floor(u), fj = floor(v);
+    int i0 = (int)fi, j0 = (int)fj;
+    double fu = u - fi, fv = v - fj;
+    double wts[4] = {(1.0 - fu) * (1.0 - fv), fu * (1.0 - fv), (1.0 - fu) * fv, fu * fv};
+    int di[4] = {0, 1, 0, 1}, dj[4] = {0, 0, 1, 1};
+    for (int k = 0; k < 4; ++k) {
+        int ii = i0 + di[k], jj = j0 + dj[k];
+        if (ii < 0 || ii >= N || jj < 0 || jj >= N) continue;
+        img[(size_t)jj * N + ii] += wts[k] * val;
+    }
+}
+
+/* ------------------------------------------------------------------ per-ray work */
+typedef struct {
+    orc_lattice L;
+    double w[64];
+} orc_ctx;
+
+static int ctx_init(const orc_desc* g, orc_ctx* cx)
+{
+    if (g->n_subrays > 64 || g->n_subrays < 1 || g->n_det < 2 || g->n_px < 2 || g->n_angles < 1 ||
+        g->n_banks < 1 || g->n_banks > 2 || g->step_px <= 0.0)
+        return -1;
+    cx->L = o1_lattice(g);
+    o1_weights(g, cx->w);
+    return 0;
+}
+
+/* O3/O4 for one ray.  Returns g_ray; *dg_ray (if dlam) gets the JVP.
+ * A_i = Delta*(1/2 mu_i + sum_{k>i} mu_k);  g = Delta * sum_i lam_i exp(-A_i)
+ * dA_i = Delta*(1/2 dmu_i + sum_{k>i} dmu_k); dg = Delta * sum_i (dlam_i - lam_i dA_i) exp(-A_i) */
+static double ray_fwd(const orc_lattice* L, int N, const double* lam, const double* mu,
+                      const double* dlam, const double* dmu, double c, double s, double sigma,
+                      int ilo, int ihi, double* dg_ray)
+{
+    double g = 0.0, dg = 0.0;
+    double sum_mu = 0.0, sum_dmu = 0.0;      /* sum_{k>i} over samples nearer the detector */
+    for (int i = ihi; i >= ilo; --i) {
+        double u, v;
+        o2_pos(L, c, s, sigma, i, &u, &v);
+        double li = o2_sample(lam, N, u, v), mi = o2_sample(mu, N, u, v);
+        double A = L->delta * (0.5 * mi + sum_mu);
+        double E = exp(-A);
+        g += li * E;
+        if (dlam) {
+            double dli = o2_sample(dlam, N, u, v), dmi = o2_sample(dmu, N, u, v);
+            double dA = L->delta * (0.5 * dmi + sum_dmu);
+            dg += (dli - li * dA) * E;
+            sum_dmu += dmi;
+        }
+        sum_mu += mi;
+    }
+    if (dg_ray) *dg_ray = L->delta * dg;
+    return L->delta * g;
+}
+
+/* Same value as ray_fwd's g, by the O(n^2) double loop written straight from the
+ * definition (used only by the brute-force pin on tiny inputs). */
+static double ray_fwd_naive(const orc_lattice* L, int N, const double* lam, const double* mu,
+                            double c, double s, double sigma, int ilo, int ihi)
+{
+    double g = 0.0;
+    for (int i = ilo; i <= ihi; ++i) {
+        double u, v;
+        o2_pos(L, c, s, sigma, i, &u, &v);
+        double A = 0.5 * o2_sample(mu, N, u, v);
+        for (int k = i + 1; k <= ihi; ++k) {
+            double uk, vk;
+            o2_pos(L, c, s, sigma, k, &uk, &vk);
+            A += o2_sample(mu, N, uk, vk);
+        }
+        g += o2_sample(lam, N, u, v) * exp(-L->delta * A);
+    }
+    return L->delta * g;
+}
+
+/* O5 for one ray with adjoint weight wr:
+ * a_lam(i) = wr*Delta*E_i; a_mu(i) = -wr*Delta^2*(sum_{k<i} lam_k E_k + 1/2 lam_i E_i) */
+static void ray_vjp(const orc_lattice* L, int N, const double* lam, const double* mu, double wr,
+                    double c, double s, double sigma, int ilo, int ihi, double* glam, double* gmu,
+                    double* buf)
+{
+    int n = ihi - ilo + 1;
+    if (n <= 0) return;
+    double* ls = buf;          /* lam_i */
+    double* E = buf + n;       /* E_i   */
+    double sum_mu = 0.0;
+    for (int i = ihi; i >= ilo; --i) {
+        double u, v;
+        o2_pos(L, c, s, sigma, i, &u, &v);
+        double mi = o2_sample(mu, N, u, v);
+        ls[i - ilo] = o2_sample(lam, N, u, v);
+        E[i - ilo] = exp(-L->delta * (0.5 * mi + sum_mu));
+        sum_mu += mi;
+    }
+    double prefix = 0.0;       /* sum_{k<i} lam_k E_k (samples farther from the detector) */
+    for (int i = ilo; i <= ihi; ++i) {
+        double u, v;
+        o2_pos(L, c, s, sigma, i, &u, &v);
+        double le = ls[i - ilo] * E[i - ilo];
+        double al = wr * L->delta * E[i - ilo];
+        double am = -wr * L->delta * L->delta * (prefix + 0.5 * le);
+        o2_scatter(glam, N, u, v, al);
+        o2_scatter(gmu, N, u, v, am);
+        prefix += le;
+    }
+}
+
+static int num_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
+
+int orc_threads(void) { return num_threads(); }
+
+/* ------------------------------------------------------------------ O3 / O4 */
+/* lam, mu, dlam, dmu: [B][N][N]; y, dy: [B][n_A][n_banks][n_det].  dlam==NULL -> forward only.
+ * naive != 0 selects the O(n^2) quadrature (forward only). */
+static int fwd_impl(const orc_desc* g, const double* lam, const double* mu, const double* dlam,
+                    const double* dmu, double* y, double* dy, int naive)
+{
+    orc_ctx cx;
+    if (ctx_init(g, &cx)) return -1;
+    int N = g->n_px, nA = g->n_angles, nB = g->n_banks, nd = g->n_det, J = g->n_subrays;
+    long n_ab = (long)g->batch * nA * nB;
+    size_t npx = (size_t)N * N;
+#pragma omp parallel for schedule(static)
+    for (long q = 0; q < n_ab; ++q) {
+        int b = (int)(q % nB), a = (int)((q / nB) % nA);
+        long m = q / ((long)nA * nB);
+        const double* l = lam + m * npx;
+        const double* u = mu + m * npx;
+        const double* dl = dlam ? dlam + m * npx : NULL;
+        const double* du = dmu ? dmu + m * npx : NULL;
+        double c, s;
+        o1_dir(g, a, b, &c, &s);
+        for (int d = 0; d < nd; ++d) {
+            double acc = 0.0, dacc = 0.0;
+            for (int j = 0; j < J; ++j) {
+                double sigma = o1_offset(g, b, d, j);
+                int ilo, ihi;
+                o1_clip(g, &cx.L, c, s, sigma, &ilo, &ihi);
+                double gj, dgj = 0.0;
+                if (naive)
+                    gj = ray_fwd_naive(&cx.L, N, l, u, c, s, sigma, ilo, ihi);
+                else
+                    gj = ray_fwd(&cx.L, N, l, u, dl, du, c, s, sigma, ilo, ihi, dl ? &dgj : NULL);
+                acc += cx.w[j] * gj;                 /* y = sum_j w_j g_ray */
+                dacc += cx.w[j] * dgj;
+            }
+            if (y) y[q * nd + d] = acc;
+            if (dy) dy[q * nd + d] = dacc;
+        }
+    }
+    return 0;
+}
+
+int orc_forward(const orc_desc* g, const double* lam, const double* mu, double* y)
+{
+    return fwd_impl(g, lam, mu, NULL, NULL, y, NULL, 0);
+}
+
+int orc_forward_naive(const orc_desc* g, const double* lam, const double* mu, double* y)
+{
+    return fwd_impl(g, lam, mu, NULL, NULL, y, NULL, 1);
+}
+
+int orc_jvp(const orc_desc* g, const double* lam, const double* mu, const double* dlam,
+            const double* dmu, double* y, double* dy)
+{
+    return fwd_impl(g, lam, mu, dlam, dmu, y, dy, 0);
+}
+
+/* ------------------------------------------------------------------ O5 */
+int orc_vjp(const orc_desc* g, const double* lam, const double* mu, const double* w, double* glam,
+            double* gmu)
+{
+    orc_ctx cx;
+    if (ctx_init(g, &cx)) return -1;
+    int N = g->n_px, nA = g->n_angles, nB = g->n_banks, nd = g->n_det, J = g->n_subrays;
+    size_t npx = (size_t)N * N;
+    int nth = num_threads();
+    memset(glam, 0, sizeof(double) * npx * g->batch);
+    memset(gmu, 0, sizeof(double) * npx * g->batch);
+    for (int m = 0; m < g->batch; ++m) {
+        double* priv = (double*)calloc((size_t)nth * 2 * npx, sizeof(double));
+        if (!priv) return -2;
+        const double* l = lam + m * npx;
+        const double* u = mu + m * npx;
+#pragma omp parallel
+        {
+            int tid = 0;
+#ifdef _OPENMP
+            tid = omp_get_thread_num();
+#endif
+            double* gl = priv + (size_t)tid * 2 * npx;
+            double* gm = gl + npx;
+            double* buf = (double*)malloc(sizeof(double) * 2 * (cx.L.n_t + 1));
+#pragma omp for schedule(static)
+            for (int q = 0; q < nA * nB; ++q) {
+                int b = q % nB, a = q / nB;
+                double c, s;
+                o1_dir(g, a, b, &c, &s);
+                for (int d = 0; d < nd; ++d) {
+                    double wd = w[((size_t)m * nA * nB + q) * nd + d];
+                    for (int j = 0; j < J; ++j) {
+                        double sigma = o1_offset(g, b, d, j);
+                        int ilo, ihi;
+                        o1_clip(g, &cx.L, c, s, sigma, &ilo, &ihi);
+                        ray_vjp(&cx.L, N, l, u, cx.w[j] * wd, c, s, sigma, ilo, ihi, gl, gm, buf);
+                    }
+                }
+            }
+            free(buf);
+        }
+        for (int t = 0; t < nth; ++t)
+            for (size_t k = 0; k < npx; ++k) {
+                glam[m * npx + k] += priv[(size_t)t * 2 * npx + k];
+                gmu[m * npx + k] += priv[(size_t)t * 2 * npx + npx + k];
+            }
+        free(priv);
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------------ O6 regulariser */
+/* (Lu)[j][i] = 4u[j][i] - u[j][i-1] - u[j][i+1] - u[j-1][i] - u[j+1][i], zero outside */
+void orc_laplacian(int N, int batch, const double* u, double* Lu)
+{
+    for (int m = 0; m < batch; ++m) {
+        const double* x = u + (size_t)m * N * N;
+        double* o = Lu + (size_t)m * N * N;
+        for (int j = 0; j < N; ++j)
+            for (int i = 0; i < N; ++i)
+                o[j * N + i] = 4.0 * x[j * N + i] - o2_pix(x, N, j, i - 1) - o2_pix(x, N, j, i + 1)
+                             - o2_pix(x, N, j - 1, i) - o2_pix(x, N, j + 1, i);
+    }
+}
+
+static double dot(const double* a, const double* b, size_t n)
+{
+    double s = 0.0;
+    for (size_t k = 0; k < n; ++k) s += a[k] * b[k];
+    return s;
+}
+
+/* ------------------------------------------------------------------ O7 GN-CG step + LM wrap */
+/* Stats layout (double[16 + n_cg + 1]):
+ *  0 f(u)   1 1/2||r||^2   2 R(u)   3 ||b||   4 pred = m(0)-m(s)   5 f(u+s)   6 rho
+ *  7 accepted   8 beta_next   9 CG steps done   10 breakdown   11 beta_min   12 ||Js||^2
+ *  13 alpha||Ls||^2   14 <b,s>   15 (unused)   16.. ||z_k|| for k = 0..n_cg            */
+#define ST_CG 16
+
+typedef struct {
+    const orc_desc* g;
+    const double *lam, *mu;
+    double alpha, beta;
+    size_t npx;
+    double *tmp_y, *tl, *tm;
+} hctx;
+
+/* H p = J^T(J p) + alpha L^T L p + beta p  (p, out stacked [lam-part | mu-part]) */
+static int apply_H(hctx* H, const double* p, double* out)
+{
+    size_t n = H->npx;
+    if (orc_jvp(H->g, H->lam, H->mu, p, p + n, NULL, H->tmp_y)) return -1;
+    if (orc_vjp(H->g, H->lam, H->mu, H->tmp_y, out, out + n)) return -1;
+    for (int f = 0; f < 2; ++f) {
+        orc_laplacian(H->g->n_px, H->g->batch, p + f * n, H->tl);
+        orc_laplacian(H->g->n_px, H->g->batch, H->tl, H->tm);
+        for (size_t k = 0; k < n; ++k) out[f * n + k] += H->alpha * H->tm[k] + H->beta * p[f * n + k];
+    }
+    return 0;
+}
+
+static double objective(const orc_desc* g, const double* lam, const double* mu, const double* y,
+                        double alpha, double* misfit, double* reg, double* r_out, double* tl)
+{
+    size_t ns = (size_t)g->batch * g->n_angles * g->n_banks * g->n_det;
+    size_t npx = (size_t)g->batch * g->n_px * g->n_px;
+    double* r = r_out;
+    orc_forward(g, lam, mu, r);
+    for (size_t k = 0; k < ns; ++k) r[k] = r[k] - y[k];           /* r = F(u) - y */
+    *misfit = 0.5 * dot(r, r, ns);
+    orc_laplacian(g->n_px, g->batch, lam, tl);
+    double q = dot(tl, tl, npx);
+    orc_laplacian(g->n_px, g->batch, mu, tl);
+    q += dot(tl, tl, npx);
+    *reg = 0.5 * alpha * q;                                       /* R(u) = alpha/2 (||L lam||^2 + ||L mu||^2) */
+    return *misfit + *reg;
+}
+
+int orc_gn_cg_step(const orc_desc* g, const double* lam, const double* mu, const double* y,
+                   double alpha, double beta, int n_cg, double* s_lam, double* s_mu, double* stats)
+{
+    size_t npx = (size_t)g->batch * g->n_px * g->n_px;
+    size_t ns = (size_t)g->batch * g->n_angles * g->n_banks * g->n_det;
+    size_t n2 = 2 * npx;
+    double* r = (double*)malloc(sizeof(double) * ns);
+    double* ys = (double*)malloc(sizeof(double) * ns);
+    double* bvec = (double*)malloc(sizeof(double) * n2);
+    double* s = (double*)calloc(n2, sizeof(double));
+    double* z = (double*)malloc(sizeof(double) * n2);
+    double* p = (double*)malloc(sizeof(double) * n2);
+    double* q = (double*)malloc(sizeof(double) * n2);
+    double* tl = (double*)malloc(sizeof(double) * npx);
+    double* tm = (double*)malloc(sizeof(double) * npx);
+    double* ut = (double*)malloc(sizeof(double) * n2);
+    if (!r || !ys || !bvec || !s || !z || !p || !q || !tl || !tm || !ut) return -2;
+    for (int k = 0; k < ST_CG + n_cg + 1; ++k) stats[k] = 0.0;
+
+    /* 1-2: r = F(u) - y, f(u) = 1/2||r||^2 + R(u) */
+    double misfit, reg;
+    double f0 = objective(g, lam, mu, y, alpha, &misfit, &reg, r, tl);
+    /* 3: b = -(J^T r + alpha L^T L u) */
+    orc_vjp(g, lam, mu, r, bvec, bvec + npx);
+    for (int f = 0; f < 2; ++f) {
+        const double* uf = f ? mu : lam;
+        orc_laplacian(g->n_px, g->batch, uf, tl);
+        orc_laplacian(g->n_px, g->batch, tl, tm);
+        for (size_t k = 0; k < npx; ++k) bvec[f * npx + k] = -(bvec[f * npx + k] + alpha * tm[k]);
+    }
+    stats[0] = f0; stats[1] = misfit; stats[2] = reg; stats[3] = sqrt(dot(bvec, bvec, n2));
+
+    /* 5: CG from s0 = 0 on H s = b */
+    hctx H = {g, lam, mu, alpha, beta, npx, ys, tl, tm};
+    memcpy(z, bvec, sizeof(double) * n2);
+    memcpy(p, bvec, sizeof(double) * n2);
+    double zeta = dot(z, z, n2);
+    stats[ST_CG + 0] = sqrt(zeta);
+    double beta_min = 0.0;
+    int k;
+    for (k = 0; k < n_cg; ++k) {
+        if (zeta == 0.0) { stats[10] = 1.0; break; }
+        apply_H(&H, p, q);
+        double gam = dot(p, q, n2);
+        if (k == 0) beta_min = 1e-3 * gam / zeta;          /* 1e-3 <b,Hb>/<b,b> */
+        if (gam <= 0.0) { stats[10] = 2.0; break; }
+        double al = zeta / gam;
+        for (size_t i = 0; i < n2; ++i) { s[i] += al * p[i]; z[i] -= al * q[i]; }
+        double zeta2 = dot(z, z, n2);
+        double bt = zeta2 / zeta;
+        for (size_t i = 0; i < n2; ++i) p[i] = z[i] + bt * p[i];
+        zeta = zeta2;
+        stats[ST_CG + k + 1] = sqrt(zeta);
+    }
+    stats[9] = k;
+    stats[11] = beta_min;
+
+    /* 6: pred = <b,s> - 1/2(||Js||^2 + alpha||Ls||^2) */
+    orc_jvp(g, lam, mu, s, s + npx, NULL, ys);
+    double js2 = dot(ys, ys, ns);
+    double ls2 = 0.0;
+    for (int f = 0; f < 2; ++f) {
+        orc_laplacian(g->n_px, g->batch, s + f * npx, tl);
+        ls2 += dot(tl, tl, npx);
+    }
+    double bs = dot(bvec, s, n2);
+    double pred = bs - 0.5 * (js2 + alpha * ls2);
+    stats[4] = pred; stats[12] = js2; stats[13] = alpha * ls2; stats[14] = bs;
+
+    /* 7: f(u+s), rho */
+    for (size_t i = 0; i < npx; ++i) { ut[i] = lam[i] + s[i]; ut[npx + i] = mu[i] + s[npx + i]; }
+    double mis2, reg2;
+    double f1 = objective(g, ut, ut + npx, y, alpha, &mis2, &reg2, r, tl);
+    double rho = (f0 - f1) / pred;
+    stats[5] = f1; stats[6] = rho;
+    /* 8: accept iff rho > eta = 0.1; beta update x10 (reject) / x0.2 (rho > 0.75) */
+    int acc = rho > 0.1;
+    double bn = beta;
+    if (!acc) bn = (10.0 * beta > beta_min) ? 10.0 * beta : beta_min;
+    else if (rho > 0.75) bn = 0.2 * beta;
+    stats[7] = acc; stats[8] = bn;
+
+    memcpy(s_lam, s, sizeof(double) * npx);
+    memcpy(s_mu, s + npx, sizeof(double) * npx);
+    free(r); free(ys); free(bvec); free(s); free(z); free(p); free(q); free(tl); free(tm); free(ut);
+    return 0;
+}
+
+/* H applied to a given p (operator-level parity pin of the GN product). */
+int orc_apply_H(const orc_desc* g, const double* lam, const double* mu, double alpha, double beta,
+                const double* p, double* out)
+{
+    size_t npx = (size_t)g->batch * g->n_px * g->n_px;
+    size_t ns = (size_t)g->batch * g->n_angles * g->n_banks * g->n_det;
+    double* ys = (double*)malloc(sizeof(double) * ns);
+    double* tl = (double*)malloc(sizeof(double) * npx);
+    double* tm = (double*)malloc(sizeof(double) * npx);
+    hctx H = {g, lam, mu, alpha, beta, npx, ys, tl, tm};
+    int rc = apply_H(&H, p, out);
+    free(ys); free(tl); free(tm);
+    return rc;
+}
+
+/* Per-ray quadrature on explicit sample values (pin P3 / P9 use it directly). */
+double orc_ray_quadrature(int n, const double* lam_s, const double* mu_s, double delta)
+{
+    double g = 0.0, sum_mu = 0.0;
+    for (int i = n - 1; i >= 0; --i) {
+        g += lam_s[i] * exp(-delta * (0.5 * mu_s[i] + sum_mu));
+        sum_mu += mu_s[i];
+    }
+    return delta * g;
+}
+
+/* Per-ray adjoint coefficients on explicit sample values: dg/dlam_i, dg/dmu_i (pin P9). */
+void orc_ray_adjoint(int n, const double* lam_s, const double* mu_s, double delta, double* dl,
+                     double* dm)
+{
+    double sum_mu = 0.0;
+    for (int i = n - 1; i >= 0; --i) {
+        dl[i] = exp(-delta * (0.5 * mu_s[i] + sum_mu));   /* E_i, scaled below */
+        sum_mu += mu_s[i];
+    }
+    double prefix = 0.0;
+    for (int i = 0; i < n; ++i) {
+        double le = lam_s[i] * dl[i];
+        dm[i] = -delta * delta * (prefix + 0.5 * le);
+        prefix += le;
+        dl[i] = delta * dl[i];
+    }
+}

@@ -1,0 +1,413 @@
+"""Pins of the fp64 oracle against what the paper and the mathematics fix
+(SURVEY.md §8(c.4) P1-P12).  CPU only.  None of these re-types an oracle formula:
+each compares it with a closed form, a symmetry, brute force, finite differences,
+a library routine or an algebraic identity of a different function.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle as O
+import pget_data as P
+from tests.metrics import max_rel, rel_l2
+
+
+def small(n_px=16, n_angles=8, n_det=9, J=3, batch=1, **kw):
+    d = dict(n_px=n_px, n_angles=n_angles, n_banks=2, n_det=n_det, n_subrays=J,
+             subray_sigma=0.4, step_px=0.5, bank1_shift=0.0, batch=batch)
+    d.update(kw)
+    return d
+
+
+def rand_img(g, seed, lo=0.0, hi=1.0):
+    rng = np.random.default_rng(seed)
+    return rng.uniform(lo, hi, size=O.img_shape(g))
+
+
+# ----------------------------------------------------------------------------- P1 geometry
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+def test_p1_tables_closed_form(cid):
+    g = P.geometry_desc(cid)
+    t = O.tables(g)
+    N, nA, nd, J = g["n_px"], g["n_angles"], g["n_det"], g["n_subrays"]
+    h = 2.0 / N
+    # angles 2*pi*a/n_A, cos/sin of theta (+pi for bank 1)
+    assert np.allclose(t["angles"], 2 * np.pi * np.arange(nA) / nA, rtol=0, atol=1e-15)
+    assert np.allclose(t["dirs"][:, 0, 0], np.cos(t["angles"]), atol=1e-15)
+    assert np.allclose(t["dirs"][:, 1, 0], -np.cos(t["angles"]), atol=1e-15)
+    assert np.allclose(t["dirs"][:, 1, 1], -np.sin(t["angles"]), atol=1e-15)
+    # offsets: endpoints +-1 at the outer sub-ray centres, mirror symmetry bitwise
+    off = t["offsets"]
+    for b in range(2):
+        assert np.array_equal(off[b, ::-1, ::-1], -off[b])
+    assert np.array_equal(off[0], off[1])
+    pitch = 2.0 / (nd - 1)
+    assert np.allclose(np.diff(off[0].ravel()), pitch / J, atol=1e-14)   # uniform sub-ray lattice
+    # weights: normalised Gaussian, sigma = 0.4 pitch
+    w = t["weights"]
+    assert abs(w.sum() - 1.0) <= 2 ** -52 * J
+    dj = (np.arange(J) + 0.5) / J - 0.5
+    ref = np.exp(-dj ** 2 / (2 * 0.4 ** 2))
+    assert np.allclose(w, ref / ref.sum(), rtol=1e-14, atol=0)
+    # t-lattice
+    hh, delta, T = t["tlat"]
+    assert hh == h and delta == 0.5 * h
+    m = math.ceil((math.sqrt(2) + h) / delta)
+    assert T == delta * m and t["n_t"] == 2 * m
+
+
+@pytest.mark.parametrize("gd", [small(), small(n_px=33, n_angles=12, J=2, n_det=7),
+                                P.geometry_desc(1)])
+def test_p1_clip_is_exact_support(gd):
+    """Brute force: sample i lies in [i_lo, i_hi] iff its position is inside the
+    support box |x|,|y| <= 1 + h/2 of the zero-padded bilinear interpolant."""
+    t = O.tables(gd)
+    h, delta, T = t["tlat"]
+    i = np.arange(t["n_t"])
+    tt = -T + (i + 0.5) * delta
+    bb = 1 + h / 2
+    for a in range(gd["n_angles"]):
+        for b in range(2):
+            c, s = t["dirs"][a, b]
+            for d in range(gd["n_det"]):
+                for j in range(gd["n_subrays"]):
+                    sig = t["offsets"][b, d, j]
+                    x = sig * (-s) + tt * c
+                    y = sig * c + tt * s
+                    inside = (np.abs(x) <= bb * (1 + 1e-12)) & (np.abs(y) <= bb * (1 + 1e-12))
+                    strict = (np.abs(x) <= bb * (1 - 1e-12)) & (np.abs(y) <= bb * (1 - 1e-12))
+                    lo, hi = t["clip"][a, b, d, j]
+                    sel = (i >= lo) & (i <= hi)
+                    assert np.all(inside[sel]) and np.all(sel[strict])
+
+
+# ----------------------------------------------------------------------------- P2 / P4 closed forms
+def _disk_geom(N, nA=4):
+    return dict(n_px=N, n_angles=nA, n_banks=2, n_det=91, n_subrays=1, subray_sigma=0.4,
+                step_px=0.5, bank1_shift=0.0, batch=1)
+
+
+def _disk_errors(N, mu0):
+    g = _disk_geom(N)
+    lam, mu = P.disk_phantom(N, 0.5, 1.0, mu0)
+    y = O.forward(g, lam, mu)[0]                    # [nA][2][91]
+    s = O.tables(g)["offsets"][0, :, 0]
+    R = 0.5
+    sel = np.abs(s) <= 0.9 * R
+    chord = 2 * np.sqrt(np.maximum(R * R - s ** 2, 0))
+    ref = chord if mu0 == 0 else (1 - np.exp(-mu0 * chord)) / mu0
+    err = np.abs(y[:, 0, sel] - ref[sel]) / ref[sel]
+    return err, y
+
+
+def test_p2_radon_disk():
+    """mu = 0: the plain Radon transform, g(s) = 2 lam0 sqrt(R^2 - s^2) (north star)."""
+    err, y = _disk_errors(128, 0.0)
+    assert err.max() <= 1e-2
+    # bank duality at mu = 0: bank 1 sees the same lines reversed
+    assert np.abs(y[:, 1, :] - y[:, 0, ::-1]).max() <= 1e-13 * np.abs(y).max()
+
+
+def test_p4_attenuated_disk_closed_form_and_convergence():
+    """Uniform disk lam0 = 1, mu0 = 0.5, R = 0.5: g(s) = (1 - e^{-mu0 2 sqrt(R^2-s^2)})/mu0
+    (north star; PAPER.md:48-54 eq:fwd_model); first-order convergence in h."""
+    means = []
+    for N in (128, 256):
+        err, _ = _disk_errors(N, 0.5)
+        assert err.max() <= 1.5e-2
+        assert err.mean() <= 0.15 * (2.0 / N)
+        means.append(err.mean())
+    assert means[0] / means[1] >= 1.5
+
+
+# ----------------------------------------------------------------------------- P3 quadrature closed form
+@pytest.mark.parametrize("n,lam0,mu0,delta", [(1, 1.0, 0.5, 0.01), (37, 0.8, 0.5, 0.015625),
+                                              (400, 1.3, 2.0, 0.0078125), (730, 1.0, 0.05, 0.00390625)])
+def test_p3_geometric_series(n, lam0, mu0, delta):
+    g = O.ray_quadrature(np.full(n, lam0), np.full(n, mu0), delta)
+    x = mu0 * delta
+    ref = lam0 * delta * math.exp(-x / 2) * math.expm1(-n * x) / math.expm1(-x)
+    assert abs(g - ref) <= 1e-14 * ref
+
+
+def test_p3_recurrence_equals_double_loop():
+    """Brute force: the O(n) suffix recurrence equals the O(n^2) double loop of the definition."""
+    g = small(n_px=12, n_angles=6, J=2, n_det=7)
+    lam, mu = rand_img(g, 1), rand_img(g, 2, 0, 2.0)
+    a = O.forward(g, lam, mu)
+    b = O.forward(g, lam, mu, naive=True)
+    assert np.abs(a - b).max() <= 1e-13 * np.abs(b).max()
+
+
+# ----------------------------------------------------------------------------- P5 invariants
+def test_p5_invariants():
+    g = small(n_px=20, n_angles=8)
+    lam, mu = rand_img(g, 3), rand_img(g, 4, 0, 0.6)
+    lam2 = rand_img(g, 5)
+    y1 = O.forward(g, lam, mu)
+    y2 = O.forward(g, lam2, mu)
+    y12 = O.forward(g, 2.0 * lam - 0.5 * lam2, mu)
+    assert rel_l2(y12, 2 * y1 - 0.5 * y2) <= 1e-13                 # linear in lambda
+    assert np.all(O.forward(g, np.zeros_like(lam), mu) == 0.0)      # lambda = 0 -> y = 0
+    for k in range(5):                                              # monotone in every mu pixel
+        mu_up = mu.copy()
+        j, i = np.random.default_rng(k).integers(0, 20, size=2)
+        mu_up[0, j, i] += 0.3
+        assert np.all(O.forward(g, lam, mu_up) <= y1 + 1e-15)
+    # bank identity: y[a][1][d] = y[(a + nA/2) mod nA][0][d]
+    nA = g["n_angles"]
+    sh = np.roll(y1[0, :, 0, :], -nA // 2, axis=0)
+    assert np.abs(y1[0, :, 1, :] - sh).max() <= 1e-13 * np.abs(y1).max()
+
+
+# ----------------------------------------------------------------------------- P6 rotation
+@pytest.mark.parametrize("cid", [1, 2])
+def test_p6_rotation_invariance(cid):
+    cfg = P.CONFIGS[cid]
+    lam, mu = P.make_phantom(cid)
+    lam, mu = lam.astype(np.float64), mu.astype(np.float64)
+    g = P.geometry_desc(cid, n_angles=40 if cid == 2 else cfg.n_angles)
+    nA = g["n_angles"]
+    y = O.forward(g, lam, mu)
+    # 180 degrees: lam'[iy][ix] = lam[N-1-iy][N-1-ix]  ->  y'[a] = y[a - nA/2]
+    y180 = O.forward(g, lam[:, ::-1, ::-1], mu[:, ::-1, ::-1])
+    assert rel_l2(y180, np.roll(y, nA // 2, axis=1)) <= 1e-12
+    if nA % 4 == 0:
+        # +90 degrees: lam'[iy][ix] = lam[N-1-ix][iy]  ->  y'[a] = y[a - nA/4]
+        r90 = lambda im: np.transpose(im, (0, 2, 1))[:, :, ::-1]
+        y90 = O.forward(g, r90(lam), r90(mu))
+        assert rel_l2(y90, np.roll(y, nA // 4, axis=1)) <= 1e-12
+        # the wrong sign must fail (confirms the orientation once)
+        assert rel_l2(y90, np.roll(y, -nA // 4, axis=1)) > 1e-3
+
+
+def test_p6_single_pixel_orientation():
+    g = small(n_px=16, n_angles=4, J=1, n_det=31)
+    lam = np.zeros((1, 16, 16))
+    lam[0, 3, 12] = 1.0                     # x = -1 + 12.5h > 0, y = -1 + 3.5h < 0
+    mu = np.zeros_like(lam)
+    y = O.forward(g, lam, mu)[0]
+    s = O.tables(g)["offsets"][0, :, 0]
+    h = 2 / 16
+    x0, y0 = -1 + 12.5 * h, -1 + 3.5 * h
+    # theta = 0: omega = (1, 0), omega_perp = (0, 1) -> the pixel projects to s = y0
+    assert abs(s[np.argmax(y[0, 0])] - y0) <= 2 / 30
+    # theta = pi/2: omega_perp = (-1, 0) -> s = -x0
+    assert abs(s[np.argmax(y[1, 0])] + x0) <= 2 / 30
+
+
+# ----------------------------------------------------------------------------- P7 JVP
+def test_p7_jvp_central_differences():
+    g = small(n_px=24, n_angles=10, J=3, n_det=11)
+    lam, mu = rand_img(g, 10, 0, 1.5), rand_img(g, 11, 0, 0.6)
+    un = math.sqrt(np.sum(lam ** 2) + np.sum(mu ** 2))
+    for k in range(20):
+        rng = np.random.default_rng(100 + k)
+        dl = rng.uniform(-1, 1, lam.shape)
+        dm = rng.uniform(-0.1, 0.1, mu.shape)
+        eps = 1e-6 * un / math.sqrt(np.sum(dl ** 2) + np.sum(dm ** 2))
+        fd = (O.forward(g, lam + eps * dl, mu + eps * dm) - O.forward(g, lam - eps * dl, mu - eps * dm)) / (2 * eps)
+        jv = O.jvp(g, lam, mu, dl, dm)
+        assert rel_l2(jv, fd) <= 1e-7
+
+
+def test_p7_jvp_lambda_part_is_forward():
+    """D_lam F[dlam] = F(dlam, mu) (PAPER.md:56 eq:frechet) and lam = 0, dlam = 0 -> 0."""
+    g = small(n_px=20)
+    lam, mu, dl = rand_img(g, 1), rand_img(g, 2, 0, 0.6), rand_img(g, 3, -1, 1)
+    jv = O.jvp(g, lam, mu, dl, np.zeros_like(mu))
+    assert rel_l2(jv, O.forward(g, dl, mu)) <= 1e-14
+    assert np.all(O.jvp(g, np.zeros_like(lam), mu, np.zeros_like(lam), rand_img(g, 4)) == 0)
+
+
+# ----------------------------------------------------------------------------- P8 adjoint
+def test_p8_adjoint_identity_100_triples():
+    g = small(n_px=12, n_angles=6, J=2, n_det=9)
+    for k in range(100):
+        rng = np.random.default_rng(1000 + k)
+        lam = rng.uniform(0, 1.5, O.img_shape(g))
+        mu = rng.uniform(0, 0.6, O.img_shape(g))
+        vl = rng.standard_normal(O.img_shape(g))
+        vm = rng.standard_normal(O.img_shape(g))
+        w = rng.standard_normal(O.sino_shape(g))
+        jv = O.jvp(g, lam, mu, vl, vm)
+        gl, gm = O.vjp(g, lam, mu, w)
+        lhs = np.sum(jv * w)
+        rhs = np.sum(vl * gl) + np.sum(vm * gm)
+        assert abs(lhs - rhs) <= 1e-10 * np.linalg.norm(jv) * np.linalg.norm(w)
+
+
+def test_p8_dense_jacobian_transpose():
+    g = dict(n_px=8, n_angles=4, n_banks=2, n_det=5, n_subrays=2, subray_sigma=0.4, step_px=0.5,
+             bank1_shift=0.0, batch=1)
+    rng = np.random.default_rng(5)
+    lam = rng.uniform(0.2, 1.5, (1, 8, 8))
+    mu = rng.uniform(0.1, 0.6, (1, 8, 8))
+    npx = 64
+    cols = []
+    for k in range(2 * npx):
+        e = np.zeros(2 * npx)
+        e[k] = 1.0
+        cols.append(O.jvp(g, lam, mu, e[:npx].reshape(1, 8, 8), e[npx:].reshape(1, 8, 8)).ravel())
+    Jd = np.stack(cols, axis=1)                       # [n_sino, 2 npx]
+    ns = Jd.shape[0]
+    rows = []
+    for r in range(ns):
+        w = np.zeros(ns)
+        w[r] = 1.0
+        gl, gm = O.vjp(g, lam, mu, w.reshape(O.sino_shape(g)))
+        rows.append(np.concatenate([gl.ravel(), gm.ravel()]))
+    JT = np.stack(rows, axis=0)                       # [n_sino, 2 npx] should equal Jd
+    assert np.abs(JT - Jd).max() <= 1e-12 * np.abs(Jd).max()
+
+
+def test_p8_vjp_zero_weights():
+    g = small()
+    gl, gm = O.vjp(g, rand_img(g, 1), rand_img(g, 2), np.zeros(O.sino_shape(g)))
+    assert np.all(gl == 0) and np.all(gm == 0)
+
+
+# ----------------------------------------------------------------------------- P9 per-ray adjoint
+def test_p9_per_ray_adjoint_fd():
+    rng = np.random.default_rng(9)
+    n, delta = 60, 0.01
+    ls, ms = rng.uniform(0, 1.5, n), rng.uniform(0, 3, n)
+    dl, dm = O.ray_adjoint(ls, ms, delta)
+    eps = 1e-3          # g is linear in lam and smooth in mu: truncation O(eps^2 delta^2) << roundoff
+    for i in range(0, n, 7):
+        e = np.zeros(n)
+        e[i] = eps
+        fl = (O.ray_quadrature(ls + e, ms, delta) - O.ray_quadrature(ls - e, ms, delta)) / (2 * eps)
+        fm = (O.ray_quadrature(ls, ms + e, delta) - O.ray_quadrature(ls, ms - e, delta)) / (2 * eps)
+        assert abs(fl - dl[i]) <= 1e-8 * abs(dl[i])
+        assert abs(fm - dm[i]) <= 1e-8 * abs(dm[i])
+
+
+# ----------------------------------------------------------------------------- P10 regulariser
+def test_p10_laplacian():
+    rng = np.random.default_rng(3)
+    x, y = rng.standard_normal((1, 11, 11)), rng.standard_normal((1, 11, 11))
+    LLx = O.laplacian(O.laplacian(x))
+    LLy = O.laplacian(O.laplacian(y))
+    assert abs(np.sum(x * LLy) - np.sum(LLx * y)) <= 1e-12 * np.abs(LLx).max()
+    assert np.sum(x * LLx) >= 0
+    c = O.laplacian(np.full((1, 11, 11), 2.5))[0]
+    assert np.all(c[1:-1, 1:-1] == 0) and c[0, 5] == 2.5 and c[0, 0] == 5.0
+    d = np.zeros((1, 7, 7))
+    d[0, 3, 3] = 1.0
+    Ld = O.laplacian(d)[0]
+    ref = np.zeros((7, 7))
+    ref[3, 3] = 4
+    ref[2, 3] = ref[4, 3] = ref[3, 2] = ref[3, 4] = -1
+    assert np.array_equal(Ld, ref)
+
+
+# ----------------------------------------------------------------------------- P11 / P12 GN-CG and LM
+def _dense_H(g, lam, mu, alpha, beta):
+    npx = g["n_px"] ** 2
+    N = g["n_px"]
+    Jc, Lc = [], []
+    for k in range(2 * npx):
+        e = np.zeros(2 * npx)
+        e[k] = 1.0
+        Jc.append(O.jvp(g, lam, mu, e[:npx].reshape(1, N, N), e[npx:].reshape(1, N, N)).ravel())
+        Lc.append(np.concatenate([O.laplacian(e[:npx].reshape(1, N, N)).ravel(),
+                                  O.laplacian(e[npx:].reshape(1, N, N)).ravel()]))
+    Jd, Ld = np.stack(Jc, 1), np.stack(Lc, 1)
+    return Jd, Ld, Jd.T @ Jd + alpha * Ld.T @ Ld + beta * np.eye(2 * npx)
+
+
+def test_p11_cg_equals_dense_solve():
+    N = 6
+    g = dict(n_px=N, n_angles=6, n_banks=2, n_det=9, n_subrays=2, subray_sigma=0.4, step_px=0.5,
+             bank1_shift=0.0, batch=1)
+    rng = np.random.default_rng(2)
+    lam, mu = rng.uniform(0.3, 1.2, (1, N, N)), rng.uniform(0.1, 0.5, (1, N, N))
+    y = O.forward(g, rng.uniform(0.3, 1.2, (1, N, N)), rng.uniform(0.1, 0.5, (1, N, N)))
+    alpha, beta = 1e-2, 0.05
+    Jd, Ld, H = _dense_H(g, lam, mu, alpha, beta)
+    r = (O.forward(g, lam, mu) - y).ravel()
+    u = np.concatenate([lam.ravel(), mu.ravel()])
+    b = -(Jd.T @ r + alpha * Ld.T @ (Ld @ u))
+    s_ref = np.linalg.solve(H, b)
+    sl, sm, st = O.gn_cg_step(g, lam, mu, y, alpha, beta, 200)
+    s = np.concatenate([sl.ravel(), sm.ravel()])
+    assert rel_l2(s, s_ref) <= 1e-8
+    assert abs(st["grad_norm"] - np.linalg.norm(b)) <= 1e-10 * np.linalg.norm(b)
+    # operator level: oracle H p (J^T via the VJP) equals the dense H built from JVP columns
+    p = rng.standard_normal(2 * N * N)
+    hl, hm = O.apply_H(g, lam, mu, alpha, beta, p[:N * N].reshape(1, N, N), p[N * N:].reshape(1, N, N))
+    assert rel_l2(np.concatenate([hl.ravel(), hm.ravel()]), H @ p) <= 1e-12
+    # model: pred = m(0) - m(s) with m(s) = 1/2||r + Js||^2 + alpha/2 ||L(u+s)||^2 (eq:m-function)
+    def m(sv):
+        return 0.5 * np.sum((r + Jd @ sv) ** 2) + 0.5 * alpha * np.sum((Ld @ (u + sv)) ** 2)
+    assert abs(st["f"] - m(np.zeros_like(s))) <= 1e-12 * st["f"]          # m(0) = f(u)
+    assert abs(st["pred"] - (m(np.zeros_like(s)) - m(s))) <= 1e-9 * abs(st["pred"])
+
+
+def test_p11_cg_recurrence_residuals():
+    N = 8
+    g = dict(n_px=N, n_angles=8, n_banks=2, n_det=11, n_subrays=2, subray_sigma=0.4, step_px=0.5,
+             bank1_shift=0.0, batch=1)
+    rng = np.random.default_rng(4)
+    lam, mu = rng.uniform(0.3, 1.2, (1, N, N)), rng.uniform(0.1, 0.5, (1, N, N))
+    y = O.forward(g, *P.disk_phantom(N, 0.6, 1.0, 0.4))
+    alpha, beta = 1e-3, 0.0
+    preds = []
+    for k in (1, 3, 6):
+        sl, sm, st = O.gn_cg_step(g, lam, mu, y, alpha, beta, k)
+        hl, hm = O.apply_H(g, lam, mu, alpha, beta, sl, sm)
+        # b = -(J^T r + alpha L^T L u): rebuild from the first CG residual norm and H s
+        _, _, st0 = O.gn_cg_step(g, lam, mu, y, alpha, beta, 0)
+        r = O.forward(g, lam, mu) - y
+        gl, gm = O.vjp(g, lam, mu, r)
+        bl = -(gl + alpha * O.laplacian(O.laplacian(lam)))
+        bm = -(gm + alpha * O.laplacian(O.laplacian(mu)))
+        res = np.sqrt(np.sum((bl - hl) ** 2) + np.sum((bm - hm) ** 2))
+        assert abs(res - st["cg_res"][k]) <= 1e-8 * st["cg_res"][0]
+        preds.append(st["pred"])
+        assert st["pred"] > 0
+    assert preds[0] < preds[1] < preds[2]           # quadratic model decreases monotonically
+
+
+def test_p11_linear_case_rho_one():
+    """lam = 0, alpha = 0: J_mu = 0 so s_mu = 0, and F is linear in lam -> rho = 1."""
+    N = 10
+    g = dict(n_px=N, n_angles=8, n_banks=2, n_det=11, n_subrays=1, subray_sigma=0.4, step_px=0.5,
+             bank1_shift=0.0, batch=1)
+    lt, mt = P.disk_phantom(N, 0.6, 1.0, 0.4)
+    y = O.forward(g, lt, mt)
+    lam = np.zeros((1, N, N))
+    sl, sm, st = O.gn_cg_step(g, lam, mt, y, 0.0, 0.0, 15)
+    assert np.all(sm == 0)
+    assert abs(st["rho"] - 1.0) <= 1e-10
+    assert st["accepted"]
+
+
+def test_p12_lm_wrap():
+    cfg = P.CONFIGS[2]
+    g = P.geometry_desc(2, n_px=32, n_angles=24)
+    lt, mt = P.make_phantom(2, n_px=32)
+    y = P.poisson_noise(O.forward(g, lt, mt), 1e4, 2)
+    l0, m0 = P.initial_guess(32)
+    sl, sm, st = O.gn_cg_step(g, l0, m0, y, cfg.alpha, 0.0, 8)
+    assert st["pred"] > 0
+    r = O.forward(g, l0, m0) - y
+    reg = 0.5 * cfg.alpha * (np.sum(O.laplacian(l0) ** 2) + np.sum(O.laplacian(m0) ** 2))
+    assert abs(st["f"] - (0.5 * np.sum(r ** 2) + reg)) <= 1e-12 * st["f"]
+    assert np.all(np.diff(st["cg_res"]) != 0)
+    if st["accepted"]:
+        assert st["f_trial"] < st["f"]
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+def test_p1_sample_counts_golden(cid):
+    import json, os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "sample_counts.json")))[str(cid)]
+    g = P.geometry_desc(cid)
+    t = O.tables(g)
+    cl = t["clip"]
+    assert int(np.clip(cl[..., 1] - cl[..., 0] + 1, 0, None).sum()) * g["batch"] == gold["samples"]
+    assert cl[..., 0].size * g["batch"] == gold["rays"]
+    assert t["n_t"] == gold["n_t"]
