@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""Benchmark of the PGET hot path on B200 (BASELINE.json metric:
+"ray-samples/s for fwd/JVP/VJP and ms per LM iteration at 1 B200 vs roofline").
+
+One step = one pass of the whole hot path over one
+batch of synthetic config-2 input (BASELINE.json configs[1]: 9x9 lattice, N=128,
+360 angles, 2x91 detectors, J=5, Poisson noise at 1e4 peak):
+    forward(u) + JVP(u; du) + VJP(u; w) + one LM iteration (20 CG steps, alpha=1e-3,
+    beta=0, trial evaluation)
+value = nominal ray-sample passes per step x steps x ranks / max-over-ranks device time.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Multi-GPU (torchrun): every rank runs an independent replica (the assemblies are
+independent problems; no data-path collective) -> "scaling": "weak".
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ray-samples/s for fwd/JVP/VJP and ms per LM iteration at 1 B200 vs roofline"
+SMEM_B_PER_CLK_SM = 128          # guide: smem/L1 crossbar bytes per clock per SM
+N_SM = 148
+# algorithmic shared-memory bytes per nominal ray-sample
+ALG_BYTES = {"forward": 32, "jvp": 64, "vjp": 32 + 32 + 64, "gn": 64 + 32 + 64}
+
+
+def lm_passes(n_cg):
+    # forward(u) + VJP(r) + n_cg GN products (JVP+VJP each) + JVP(s) + forward(u+s)
+    return {"forward": 2, "vjp": 1, "jvp": 1, "gn": n_cg}
+
+
+class Clocks:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for k, n in enumerate(names):
+                if len(r) > 3 + k and r[3 + k].lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the fp64 oracle (the paper has no code; the oracle is the reference
+    arm for this tier) on a bounded sample of the same workload, on the host cores."""
+    if rank != 0:
+        return 0
+    import oracle as O
+    import pget_data as P
+    cfg = P.CONFIGS[args.config]
+    sample = cpu_sample(cfg, args.ref_angles)
+    times = []
+    for k in range(args.warmup + args.steps):
+        dt, n = run_oracle_step(O, P, cfg, sample)
+        if k >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    value = sample["samples_per_step"] * len(times) / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "ray-samples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"config {cfg.cid} (bounded sample: {sample['desc']})"},
+        "cpu_baseline": {"value": value, "unit": "ray-samples/s", "cores": O.threads(), "kind": "oracle",
+                         "sample": sample["desc"]},
+        "e2e": {"value": value, "unit": "ray-samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_sample(cfg, n_angles):
+    import oracle as O
+    import pget_data as P
+    gd = P.geometry_desc(cfg.cid, n_angles=n_angles, batch=1)
+    t = O.tables(gd)
+    cl = t["clip"]
+    nominal = int(np.clip(cl[..., 1] - cl[..., 0] + 1, 0, None).sum())
+    lam, mu = P.make_phantom(cfg.cid)
+    lam, mu = lam[:1], mu[:1]
+    dl, dm = P.rod_directions(cfg.cid)
+    dl, dm = dl[:1], dm[:1]
+    l0, m0 = P.initial_guess(cfg.n_px)
+    y = P.poisson_noise(O.forward(gd, lam, mu), cfg.noise_peak or 1e4, cfg.seed)
+    w = (O.forward(gd, lam * 1.05, mu) - O.forward(gd, lam, mu)).astype(np.float32)
+    passes = 3 + sum(v * (2 if k == "gn" else 1) for k, v in lm_passes(cfg.n_cg).items())
+    return dict(gd=gd, lam=lam, mu=mu, dl=dl, dm=dm, l0=l0, m0=m0, y=y, w=w, nominal=nominal,
+                samples_per_step=nominal * passes,
+                desc=f"one step (fwd+JVP+VJP+1 LM iteration, {cfg.n_cg} CG) of config {cfg.cid} restricted to "
+                     f"{n_angles} of {cfg.n_angles} angles ({nominal} nominal samples/pass, {passes} passes)")
+
+
+def run_oracle_step(O, P, cfg, s):
+    t0 = time.perf_counter()
+    O.forward(s["gd"], s["lam"], s["mu"])
+    O.jvp(s["gd"], s["lam"], s["mu"], s["dl"], s["dm"])
+    O.vjp(s["gd"], s["lam"], s["mu"], s["w"])
+    O.gn_cg_step(s["gd"], s["l0"], s["m0"], s["y"], cfg.alpha, 0.0, cfg.n_cg)
+    return time.perf_counter() - t0, s["samples_per_step"]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--ref-angles", type=int, default=36)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return reference_arm(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_26745_b200 as pg
+    import pget_data as P
+
+    if args.warmup < 3:
+        args.warmup = 3
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    cfg = P.CONFIGS[args.config]
+    gd = P.geometry_desc(cfg.cid)
+    g = pg.Geometry(gd, device=local)
+    nominal = g.info["n_samples_nominal"]
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x, np.float32)).cuda()
+
+    # ---- synthetic inputs (seeded; per-rank replica), resident in HBM before timing
+    lam_h, mu_h = P.make_phantom(cfg.cid)
+    dl_h, dm_h = P.rod_directions(cfg.cid)
+    lp_h, mp_h = P.make_phantom_prime(cfg.cid)
+    l0_h, m0_h = P.initial_guess(cfg.n_px, cfg.batch)
+    lam, mu, dl, dm, lp, mp, l0, m0 = map(dev, (lam_h, mu_h, dl_h, dm_h, lp_h, mp_h, l0_h, m0_h))
+    y_clean = pg.forward(g, lam, mu)
+    w = (pg.forward(g, lp, mp) - y_clean).contiguous()
+    y_meas = dev(P.poisson_noise(y_clean.cpu().numpy(), cfg.noise_peak or 1e4, cfg.seed))
+    torch.cuda.synchronize()
+
+    # outputs / workspaces preallocated (the library never allocates)
+    y = torch.empty(g.sino_shape, device="cuda")
+    dy = torch.empty_like(y)
+    gl = torch.empty(g.img_shape, device="cuda")
+    gm = torch.empty_like(gl)
+    sl = torch.empty_like(gl)
+    sm = torch.empty_like(gl)
+    stats = pg.stats_buffer(g)
+    ws = {op: g.workspace(op) for op in ("forward", "jvp", "vjp", "gn_cg_step")}
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+
+    def step(ev=None):
+        if ev: ev[0].record()
+        pg.forward(g, lam, mu, y=y, ws=ws["forward"])
+        if ev: ev[1].record()
+        pg.jvp(g, lam, mu, dl, dm, dy=dy, ws=ws["jvp"])
+        if ev: ev[2].record()
+        pg.vjp(g, lam, mu, w, g_lam=gl, g_mu=gm, ws=ws["vjp"])
+        if ev: ev[3].record()
+        pg.gn_cg_step(g, l0, m0, y_meas, cfg.alpha, 0.0, cfg.n_cg, pg.PGET_GN_EVAL_TRIAL, s_lam=sl, s_mu=sm,
+                      stats=stats, ws=ws["gn_cg_step"])
+        if ev: ev[4].record()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    passes = {"forward": 1, "jvp": 1, "vjp": 1}
+    lmp = lm_passes(cfg.n_cg)
+    sample_passes = 3 + sum(v * (2 if k == "gn" else 1) for k, v in lmp.items())
+    samples_per_step = nominal * sample_passes
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    clocks = Clocks(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    pg.profile_begin(args.steps * (8 + 2 * cfg.n_cg) + 64)
+    for k in range(args.steps):
+        flush.zero_()                       # L2 flush between timed steps (outside the events)
+        step(evs[k])
+    torch.cuda.synchronize()
+    prof = pg.profile_end()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    phase = {"forward": 0.0, "jvp": 0.0, "vjp": 0.0, "lm": 0.0}
+    for e in evs:
+        phase["forward"] += e[0].elapsed_time(e[1])
+        phase["jvp"] += e[1].elapsed_time(e[2])
+        phase["vjp"] += e[2].elapsed_time(e[3])
+        phase["lm"] += e[3].elapsed_time(e[4])
+    total_ms = sum(phase.values())
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+
+    # ---- end to end through the public API with host buffers (pinned), copies timed
+    e2e = None
+    if not args.no_e2e:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a, np.float32)).pin_memory()
+        h_in = [pin(a) for a in (lam_h, mu_h, dl_h, dm_h, l0_h, m0_h)] + [pin(w.cpu().numpy()),
+                                                                          pin(y_meas.cpu().numpy())]
+        d_in = [torch.empty(x.shape, device="cuda") for x in h_in]
+        h_out = [torch.empty(x.shape, dtype=x.dtype).pin_memory() for x in (y, dy, gl, gm, sl, sm, stats)]
+        bi = sum(x.numel() * x.element_size() for x in h_in)
+        bo = sum(x.numel() * x.element_size() for x in h_out)
+
+        def e2e_step():
+            for hh, dd in zip(h_in, d_in):
+                dd.copy_(hh, non_blocking=True)
+            L, M, DL, DM, L0, M0, W, Y = d_in
+            pg.forward(g, L, M, y=y, ws=ws["forward"])
+            pg.jvp(g, L, M, DL, DM, dy=dy, ws=ws["jvp"])
+            pg.vjp(g, L, M, W, g_lam=gl, g_mu=gm, ws=ws["vjp"])
+            pg.gn_cg_step(g, L0, M0, Y, cfg.alpha, 0.0, cfg.n_cg, pg.PGET_GN_EVAL_TRIAL, s_lam=sl, s_mu=sm,
+                          stats=stats, ws=ws["gn_cg_step"])
+            for hh, dd in zip(h_out, (y, dy, gl, gm, sl, sm, stats)):
+                hh.copy_(dd, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        tot = 0.0
+        for _ in range(args.steps):
+            flush.zero_()
+            a.record()
+            e2e_step()
+            b.record()
+            b.synchronize()
+            tot += a.elapsed_time(b)
+        te = torch.tensor([tot], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": world * samples_per_step * args.steps / (float(te.item()) * 1e-3), "unit": "ray-samples/s",
+               "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo}
+
+    # ---- roofline of the dominant kernel (GN normal product projector) from live CUDA events
+    dom = max(prof["ms"], key=lambda k: prof["ms"][k])
+    n_launch = max(prof["launches"][dom], 1)
+    per_launch_ms = prof["ms"][dom] / n_launch
+    units = nominal                                     # nominal samples per launch (one pass over all rays)
+    achieved_gbs = ALG_BYTES[dom] * units / (per_launch_ms * 1e-3) / 1e9
+    sm_mhz = (clk or {}).get("sm_mhz") or 1965.0
+    peak_gbs = SMEM_B_PER_CLK_SM * N_SM * sm_mhz * 1e6 / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(f"cfg{cfg.cid}", {}).get(dom)
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle as O
+        s = cpu_sample(cfg, args.ref_angles)
+        dt, n = run_oracle_step(O, P, cfg, s)
+        cpu = {"value": n / dt, "unit": "ray-samples/s", "cores": O.threads(), "kind": "oracle",
+               "sample": s["desc"]}
+
+    if rank == 0:
+        value = world * samples_per_step * args.steps / (total_ms * 1e-3)
+        K = args.steps
+        line = {
+            "metric": METRIC, "value": value, "unit": "ray-samples/s", "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"config {cfg.cid}: {cfg.lattice} phantom, N={cfg.n_px}, {cfg.n_angles} angles, "
+                                   f"2x{cfg.n_det} det, J={cfg.n_subrays}, B={cfg.batch}; step = fwd + JVP + VJP + "
+                                   f"1 LM iteration ({cfg.n_cg} CG, alpha={cfg.alpha}, beta=0, trial)",
+                       "nominal_samples_per_pass": nominal, "sample_passes_per_step": sample_passes,
+                       "l2": "flushed between timed steps (256 MiB write, outside the events)"},
+            "per_op": {
+                "forward_samples_per_s": nominal * K / (phase["forward"] * 1e-3),
+                "jvp_samples_per_s": nominal * K / (phase["jvp"] * 1e-3),
+                "vjp_samples_per_s": nominal * K / (phase["vjp"] * 1e-3),
+                "lm_ms": phase["lm"] / K,
+                "forward_ms": phase["forward"] / K, "jvp_ms": phase["jvp"] / K, "vjp_ms": phase["vjp"] / K,
+                "projector_ms_per_launch": {k: (prof["ms"][k] / prof["launches"][k] if prof["launches"][k] else None)
+                                            for k in prof["ms"]},
+            },
+            "roofline": {"bound": "alu", "pipe": "shared-memory crossbar (128 B/clk/SM)", "kernel": f"proj_kernel<{dom}>",
+                         "achieved": achieved_gbs, "peak": peak_gbs, "unit": "GB/s", "frac": achieved_gbs / peak_gbs,
+                         "traffic": traffic,
+                         "peak_basis": f"128 B/clk/SM x 148 SMs x {sm_mhz:.0f} MHz (median SM clock under load)",
+                         "alg_bytes_per_sample": ALG_BYTES[dom], "units_per_launch": units,
+                         "launch_ms": per_launch_ms},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": prof["total_launches"],
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

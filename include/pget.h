@@ -1,0 +1,195 @@
+/*
+ * pget.h -- C ABI of the B200-native PGET hot path (arXiv 2604.26745).
+ *
+ * The library (paper_2604_26745_b200/libpget.so) evaluates, on one B200
+ * (sm_100a), the attenuated ray-tracing forward model of passive gamma emission
+ * tomography, its Jacobian-vector and vector-Jacobian products with respect to
+ * the emission lambda and the attenuation mu, and one regularised Gauss-Newton
+ * (Levenberg-Marquardt) step solved by conjugate gradients.
+ *
+ * Model (Sec. 2.1, eq:fwd_model):
+ *     F(lam,mu)(s,theta) = int_R lam(s theta_perp + t theta) exp(-B mu(s theta_perp + t theta, theta)) dt,
+ *     B mu(x,theta)      = int_0^inf mu(x + tau theta) dtau,
+ * discretised as BASELINE.json's ray-sampled quadrature:
+ *   - image grid Omega = [-1,1]^2, N x N cell-centred pixels, h = 2/N, row = y, col = x;
+ *   - angles theta_a = 2 pi a / n_angles; bank b looks along phi = theta_a + b pi with
+ *     omega = (cos phi, sin phi) pointing at the detector, omega_perp = (-sin phi, cos phi);
+ *   - detector offsets s_d = (2d - (n_det-1))/(n_det-1) (+ bank1_shift * pitch for bank 1),
+ *     J sub-rays at s_d + ((2j+1-J)/(2J)) pitch with normalised Gaussian weights
+ *     (sigma = subray_sigma * pitch)  [PAPER.md:33: two banks of 91 detectors];
+ *   - samples t_i = -T + (i + 1/2) Delta, Delta = step_px * h, T = Delta ceil((sqrt2 + h)/Delta),
+ *     bilinear interpolation of lam, mu at x_i = sigma omega_perp + t_i omega (zero outside);
+ *   - A_i = Delta (mu_i / 2 + sum_{k>i} mu_k)  (k > i: nearer the detector),
+ *     g_ray = Delta sum_i lam_i exp(-A_i),  y[a][b][d] = sum_j w_j g_ray(a,b,d,j).
+ * Derivatives (eq:frechet): D_lam F[dlam] = F(dlam, mu),
+ * D_mu F[dmu] = -F(lam B(dmu), mu), with the same quadrature for B; the VJP is the
+ * exact transpose of that discrete JVP (the adjoint F'^* used at PAPER.md:231, 277).
+ *
+ * Layouts (all float32, C-contiguous, CUDA device memory owned by the caller):
+ *   images    [batch][n_px][n_px]                     (lam, mu, dlam, dmu, g_lam, g_mu, s_lam, s_mu)
+ *   sinograms [batch][n_angles][n_banks][n_det]       (y, dy, w, y_meas), detector fastest
+ * Every device pointer must be 16-byte aligned (torch's allocator guarantees it).
+ *
+ * Ownership: the caller owns every buffer, including the workspace (size from
+ * pget_workspace_bytes; any device memory, e.g. a torch uint8 tensor).  The
+ * geometry handle owns only its small device tables, allocated in
+ * pget_geometry_create and freed in pget_geometry_destroy.  No other call
+ * allocates, frees or synchronises; everything is enqueued on `stream`.
+ *
+ * Errors: arguments are validated synchronously before anything is enqueued; on
+ * failure nothing is enqueued and a non-OK status is returned, with a message in
+ * pget_last_error_message() (thread-local).  Kernel launch failures return
+ * PGET_ERR_CUDA.  No C++ exception crosses this interface; nothing aborts.
+ *
+ * Threading: a handle is immutable after creation; concurrent calls on
+ * different streams are safe when their workspaces and outputs differ.
+ */
+#ifndef PGET_H
+#define PGET_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+struct CUstream_st;
+typedef struct CUstream_st* pget_stream_t;   /* == cudaStream_t; NULL = legacy default stream */
+
+typedef struct pget_geometry_s* pget_geometry; /* opaque */
+
+typedef enum {
+    PGET_OK = 0,
+    PGET_ERR_INVALID_ARGUMENT = 1,
+    PGET_ERR_SHAPE = 2,
+    PGET_ERR_ALIGNMENT = 3,
+    PGET_ERR_WORKSPACE = 4,
+    PGET_ERR_OUT_OF_MEMORY = 5,
+    PGET_ERR_CUDA = 6,
+    PGET_ERR_NOT_FINITE = 7
+} pget_status;
+
+/* Geometry descriptor (PAPER.md:33 detector banks; BASELINE.json configs). */
+typedef struct {
+    int32_t n_px;         /* N >= 2: image N x N on [-1,1]^2                              */
+    int32_t n_angles;     /* >= 1: theta_a = 2 pi a / n_angles                             */
+    int32_t n_banks;      /* 1 or 2 (opposing bank looks along theta + pi)                 */
+    int32_t n_det;        /* >= 2 detectors per bank spanning [-1, 1]                      */
+    int32_t n_subrays;    /* J in [1, 64] sub-rays per detector                            */
+    double subray_sigma;  /* > 0: Gaussian collimator sigma in detector pitches (0.4)      */
+    double step_px;       /* > 0: sample step Delta in pixels (0.5)                        */
+    double bank1_shift;   /* bank-1 offset shift in pitches (0 for the configs)            */
+    int32_t batch;        /* >= 1 independent image pairs per call                         */
+} pget_geometry_desc;
+
+typedef struct {
+    int64_t n_rays;             /* batch * n_angles * n_banks * n_det * n_subrays          */
+    int64_t n_samples_nominal;  /* batch * sum over rays of (i_hi - i_lo + 1): the unit of
+                                   the ray-samples/s metric                                 */
+    int64_t image_elems;        /* batch * n_px * n_px                                      */
+    int64_t sino_elems;         /* batch * n_angles * n_banks * n_det                       */
+    int32_t n_t;                /* unclipped samples per ray = 2 T / Delta                  */
+    int32_t n_px, n_angles, n_banks, n_det, n_subrays, batch;
+    double h, delta, T;
+} pget_geometry_info_t;
+
+/* Table ids for pget_geometry_export (bit-exact comparison with the oracle, pin P1). */
+enum {
+    PGET_TABLE_ANGLES = 0,  /* double [n_angles]                         theta_a              */
+    PGET_TABLE_DIRS = 1,    /* double [n_angles][n_banks][2]             (cos phi, sin phi)   */
+    PGET_TABLE_OFFSETS = 2, /* double [n_banks][n_det][n_subrays]        sigma_{b,d,j}        */
+    PGET_TABLE_WEIGHTS = 3, /* double [n_subrays]                        w_j                  */
+    PGET_TABLE_TLAT = 4,    /* double [3]                                (h, Delta, T)        */
+    PGET_TABLE_CLIP = 5     /* int32  [n_angles][n_banks][n_det][n_subrays][2]  (i_lo, i_hi); empty ray = (0,-1) */
+};
+
+/* Operation ids for pget_workspace_bytes. */
+enum { PGET_OP_FORWARD = 0, PGET_OP_JVP = 1, PGET_OP_VJP = 2, PGET_OP_GN_CG_STEP = 3, PGET_OP_GN_APPLY = 4 };
+
+/* Flags for pget_gn_cg_step. */
+#define PGET_GN_EVAL_TRIAL 1u   /* also evaluate f(u+s), rho, the accept decision and beta_next */
+#define PGET_MAX_CG 256
+
+/* Device-resident statistics of one LM iteration, per batch member (array of `batch`).
+ * (SURVEY.md §8(c.2) O7; PAPER.md:160-164 eq:m-function, :248 eq:rho_agreement.) */
+typedef struct {
+    double f;             /* f(u) = 1/2||F(u)-y||^2 + alpha/2(||L lam||^2 + ||L mu||^2)      */
+    double misfit;        /* 1/2 ||F(u) - y||^2                                               */
+    double reg;           /* R(u)                                                             */
+    double grad_norm;     /* ||b||, b = -grad f(u)                                            */
+    double pred;          /* m(0) - m(s) = <b,s> - 1/2(||Js||^2 + alpha ||Ls||^2)             */
+    double f_trial;       /* f(u+s)                      (PGET_GN_EVAL_TRIAL)                 */
+    double rho;           /* (f(u) - f(u+s)) / pred      (PGET_GN_EVAL_TRIAL)                 */
+    double beta_next;     /* x10 on reject (>= beta_min), x0.2 if rho > 0.75 (PGET_GN_EVAL_TRIAL) */
+    double beta_min;      /* 1e-3 <b,Hb>/<b,b>                                               */
+    double js2;           /* ||Js||^2                                                         */
+    double als2;          /* alpha ||Ls||^2                                                   */
+    double bs;            /* <b, s>                                                           */
+    int32_t accepted;     /* rho > eta = 0.1             (PGET_GN_EVAL_TRIAL)                 */
+    int32_t n_cg_done;    /* CG steps performed                                               */
+    int32_t breakdown;    /* 0 none, 1 zeta == 0, 2 <p,Hp> <= 0                              */
+    int32_t pad_;
+    double cg_res[PGET_MAX_CG + 1]; /* ||z_k||, k = 0..n_cg                                   */
+} pget_gn_stats;
+
+const char* pget_status_string(pget_status s);
+const char* pget_last_error_message(void);
+
+/* Build the geometry (host fp64 tables, O1 of SURVEY.md §8(c.2)) and upload its
+ * device tables on `device`.  *out receives the handle.  Synchronous.
+ * device < 0 creates a host-only handle (info and table export only; every compute
+ * call on it returns PGET_ERR_INVALID_ARGUMENT) -- usable without a GPU. */
+pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pget_geometry* out);
+pget_status pget_geometry_destroy(pget_geometry g);
+pget_status pget_geometry_info(pget_geometry g, pget_geometry_info_t* out);
+size_t pget_table_bytes(pget_geometry g, int table_id);                    /* 0 for a bad id */
+pget_status pget_geometry_export(pget_geometry g, int table_id, void* host_dst, size_t bytes);
+
+/* Workspace bytes needed by `op` (PGET_OP_*); 0 for a bad op. */
+size_t pget_workspace_bytes(pget_geometry g, int op);
+
+/* y = F(lam, mu)  (eq:fwd_model). */
+pget_status pget_forward(pget_geometry g, const float* lam, const float* mu, float* y,
+                         void* ws, size_t ws_bytes, pget_stream_t stream);
+
+/* dy = D_lam F[dlam] + D_mu F[dmu]  (eq:frechet); y = F(lam, mu) too when y != NULL. */
+pget_status pget_jvp(pget_geometry g, const float* lam, const float* mu, const float* dlam,
+                     const float* dmu, float* y_or_null, float* dy, void* ws, size_t ws_bytes,
+                     pget_stream_t stream);
+
+/* (g_lam, g_mu) = F'(lam, mu)^T w  (adjoint of eq:frechet). */
+pget_status pget_vjp(pget_geometry g, const float* lam, const float* mu, const float* w,
+                     float* g_lam, float* g_mu, void* ws, size_t ws_bytes, pget_stream_t stream);
+
+/* (q_lam, q_mu) = H p = J^T J p + alpha L^T L p + beta p at u = (lam, mu): the GN normal
+ * operator of eq:LMA-step with the Laplacian penalty (reading Q10). */
+pget_status pget_gn_apply(pget_geometry g, const float* lam, const float* mu, const float* p_lam,
+                          const float* p_mu, float alpha, float beta, float* q_lam, float* q_mu,
+                          void* ws, size_t ws_bytes, pget_stream_t stream);
+
+/* One LM iteration at u = (lam, mu) for measurements y_meas:
+ * r = F(u) - y; b = -(J^T r + alpha L^T L u); n_cg CG steps from s = 0 on
+ * (J^T J + alpha L^T L + beta I) s = b; pred; with PGET_GN_EVAL_TRIAL also f(u+s),
+ * rho, accept (rho > 0.1) and beta_next.  Writes s to (s_lam, s_mu) and `batch`
+ * pget_gn_stats structs to stats_dev (device memory).  0 <= n_cg <= PGET_MAX_CG. */
+pget_status pget_gn_cg_step(pget_geometry g, const float* lam, const float* mu, const float* y_meas,
+                            float alpha, float beta, int32_t n_cg, uint32_t flags, float* s_lam,
+                            float* s_mu, pget_gn_stats* stats_dev, void* ws, size_t ws_bytes,
+                            pget_stream_t stream);
+
+/* Tracing.  Between pget_profile_begin and pget_profile_end every kernel the library
+ * launches (on any stream, from any thread) is counted, and each projector launch is
+ * bracketed by two CUDA events recorded on the stream it is launched on (up to
+ * max_launches projector launches; later ones are counted but not timed).
+ * pget_profile_end waits for the recorded events and returns, per projector mode
+ * (0 forward, 1 JVP, 2 VJP, 3 GN normal product), the summed device time in ms and
+ * the launch count, plus the total number of library kernel launches.  Host-side. */
+pget_status pget_profile_begin(int32_t max_launches);
+pget_status pget_profile_end(double* ms_per_mode /* [4] */, int64_t* launches_per_mode /* [4] */,
+                             int64_t* total_launches);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PGET_H */

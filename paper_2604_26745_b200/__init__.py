@@ -1,0 +1,283 @@
+"""Python binding of libpget (include/pget.h): argument marshalling only.
+
+Every step of the hot path runs in the library's sm_100a kernels; this module
+only checks tensor shapes/dtypes, passes device pointers and the current torch
+stream through ctypes, and allocates outputs/workspaces with torch.  There is
+no CPU fallback: if libpget.so is missing or fails to load, importing the
+binding raises.
+
+Names follow the C ABI: Geometry (pget_geometry_create/destroy/info/export),
+forward, jvp, vjp, gn_apply, gn_cg_step.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from ._build import LIB, build as _build_lib, needs_build as _needs_build
+
+__all__ = ["Geometry", "forward", "jvp", "vjp", "gn_apply", "gn_cg_step", "GNStats", "lib",
+           "PGET_GN_EVAL_TRIAL", "TABLES", "OPS"]
+
+PGET_GN_EVAL_TRIAL = 1
+PGET_MAX_CG = 256
+TABLES = {"angles": 0, "dirs": 1, "offsets": 2, "weights": 3, "tlat": 4, "clip": 5}
+OPS = {"forward": 0, "jvp": 1, "vjp": 2, "gn_cg_step": 3, "gn_apply": 4}
+EXPORTED = ["pget_status_string", "pget_last_error_message", "pget_geometry_create", "pget_geometry_destroy",
+            "pget_geometry_info", "pget_table_bytes", "pget_geometry_export", "pget_workspace_bytes",
+            "pget_forward", "pget_jvp", "pget_vjp", "pget_gn_apply", "pget_gn_cg_step", "pget_profile_begin",
+            "pget_profile_end"]
+MODES = ("forward", "jvp", "vjp", "gn")
+
+
+class _Desc(C.Structure):
+    _fields_ = [("n_px", C.c_int32), ("n_angles", C.c_int32), ("n_banks", C.c_int32), ("n_det", C.c_int32),
+                ("n_subrays", C.c_int32), ("subray_sigma", C.c_double), ("step_px", C.c_double),
+                ("bank1_shift", C.c_double), ("batch", C.c_int32)]
+
+
+class _Info(C.Structure):
+    _fields_ = [("n_rays", C.c_int64), ("n_samples_nominal", C.c_int64), ("image_elems", C.c_int64),
+                ("sino_elems", C.c_int64), ("n_t", C.c_int32), ("n_px", C.c_int32), ("n_angles", C.c_int32),
+                ("n_banks", C.c_int32), ("n_det", C.c_int32), ("n_subrays", C.c_int32), ("batch", C.c_int32),
+                ("h", C.c_double), ("delta", C.c_double), ("T", C.c_double)]
+
+
+class GNStats(C.Structure):
+    _fields_ = [("f", C.c_double), ("misfit", C.c_double), ("reg", C.c_double), ("grad_norm", C.c_double),
+                ("pred", C.c_double), ("f_trial", C.c_double), ("rho", C.c_double), ("beta_next", C.c_double),
+                ("beta_min", C.c_double), ("js2", C.c_double), ("als2", C.c_double), ("bs", C.c_double),
+                ("accepted", C.c_int32), ("n_cg_done", C.c_int32), ("breakdown", C.c_int32), ("pad_", C.c_int32),
+                ("cg_res", C.c_double * (PGET_MAX_CG + 1))]
+
+    def to_dict(self, n_cg=None):
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("cg_res", "pad_")}
+        d["accepted"] = bool(d["accepted"])
+        n = self.n_cg_done if n_cg is None else n_cg
+        d["cg_res"] = np.array(self.cg_res[: n + 1])
+        return d
+
+
+_lib = None
+
+
+def lib():
+    """Load libpget.so (building it first if the sources are newer); raise if impossible."""
+    global _lib
+    if _lib is None:
+        if _needs_build():
+            _build_lib()
+        if not os.path.exists(LIB):
+            raise ImportError(f"libpget.so not found at {LIB}")
+        L = C.CDLL(LIB)
+        P, S = C.c_void_p, C.c_size_t
+        L.pget_status_string.restype = C.c_char_p
+        L.pget_status_string.argtypes = [C.c_int]
+        L.pget_last_error_message.restype = C.c_char_p
+        L.pget_geometry_create.argtypes = [C.POINTER(_Desc), C.c_int, C.POINTER(P)]
+        L.pget_geometry_destroy.argtypes = [P]
+        L.pget_geometry_info.argtypes = [P, C.POINTER(_Info)]
+        L.pget_table_bytes.argtypes = [P, C.c_int]
+        L.pget_table_bytes.restype = S
+        L.pget_geometry_export.argtypes = [P, C.c_int, P, S]
+        L.pget_workspace_bytes.argtypes = [P, C.c_int]
+        L.pget_workspace_bytes.restype = S
+        L.pget_forward.argtypes = [P, P, P, P, P, S, P]
+        L.pget_jvp.argtypes = [P, P, P, P, P, P, P, P, S, P]
+        L.pget_vjp.argtypes = [P, P, P, P, P, P, P, S, P]
+        L.pget_gn_apply.argtypes = [P, P, P, P, P, C.c_float, C.c_float, P, P, P, S, P]
+        L.pget_gn_cg_step.argtypes = [P, P, P, P, C.c_float, C.c_float, C.c_int32, C.c_uint32, P, P, P, P, S, P]
+        L.pget_profile_begin.argtypes = [C.c_int32]
+        L.pget_profile_end.argtypes = [P, P, P]
+        for n in ("pget_profile_begin", "pget_profile_end", "pget_geometry_create", "pget_geometry_destroy", "pget_geometry_info", "pget_geometry_export",
+                  "pget_forward", "pget_jvp", "pget_vjp", "pget_gn_apply", "pget_gn_cg_step"):
+            getattr(L, n).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _check(rc, what):
+    if rc != 0:
+        L = lib()
+        raise RuntimeError(f"{what}: {L.pget_status_string(rc).decode()}: {L.pget_last_error_message().decode()}")
+
+
+def _stream(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else None
+
+
+class Geometry:
+    """pget_geometry handle.  desc: dict with the pget_geometry_desc fields."""
+
+    def __init__(self, desc: dict, device: int | None = None):
+        self.desc = dict(desc)
+        if device is None:
+            import torch
+            device = torch.cuda.current_device()
+        self.device = int(device)           # device < 0: host-only handle (tables/info only)
+        d = _Desc(int(desc["n_px"]), int(desc["n_angles"]), int(desc.get("n_banks", 2)), int(desc.get("n_det", 91)),
+                  int(desc.get("n_subrays", 1)), float(desc.get("subray_sigma", 0.4)),
+                  float(desc.get("step_px", 0.5)), float(desc.get("bank1_shift", 0.0)), int(desc.get("batch", 1)))
+        h = C.c_void_p()
+        _check(lib().pget_geometry_create(C.byref(d), self.device, C.byref(h)), "pget_geometry_create")
+        self._h = h
+        info = _Info()
+        _check(lib().pget_geometry_info(h, C.byref(info)), "pget_geometry_info")
+        self.info = {k: getattr(info, k) for k, _ in _Info._fields_}
+        self._ws = {}
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().pget_geometry_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def img_shape(self):
+        i = self.info
+        return (i["batch"], i["n_px"], i["n_px"])
+
+    @property
+    def sino_shape(self):
+        i = self.info
+        return (i["batch"], i["n_angles"], i["n_banks"], i["n_det"])
+
+    def export(self, name: str):
+        tid = TABLES[name]
+        nbytes = lib().pget_table_bytes(self._h, tid)
+        dt = np.int32 if name == "clip" else np.float64
+        out = np.zeros(nbytes // np.dtype(dt).itemsize, dtype=dt)
+        _check(lib().pget_geometry_export(self._h, tid, out.ctypes.data_as(C.c_void_p), nbytes), "export")
+        return out
+
+    def workspace_bytes(self, op: str) -> int:
+        return int(lib().pget_workspace_bytes(self._h, OPS[op]))
+
+    def workspace(self, op: str):
+        """A cached torch uint8 workspace for `op` on this geometry's device."""
+        import torch
+        n = self.workspace_bytes(op)
+        ws = self._ws.get(op)
+        if ws is None or ws.numel() < n:
+            ws = torch.empty(max(n, 16), dtype=torch.uint8, device=f"cuda:{self.device}")
+            self._ws[op] = ws
+        return ws
+
+
+def _f32(t, shape, what):
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+        raise TypeError(f"{what}: expected a contiguous float32 CUDA tensor")
+    if tuple(t.shape) != tuple(shape) and t.numel() != int(np.prod(shape)):
+        raise ValueError(f"{what}: shape {tuple(t.shape)} != {tuple(shape)}")
+    return t
+
+
+def forward(g: Geometry, lam, mu, y=None, ws=None, stream=None):
+    import torch
+    _f32(lam, g.img_shape, "lam"); _f32(mu, g.img_shape, "mu")
+    if y is None:
+        y = torch.empty(g.sino_shape, dtype=torch.float32, device=lam.device)
+    ws = g.workspace("forward") if ws is None else ws
+    _check(lib().pget_forward(g.handle, _ptr(lam), _ptr(mu), _ptr(y), _ptr(ws), ws.numel(), _stream(stream)),
+           "pget_forward")
+    return y
+
+
+def jvp(g: Geometry, lam, mu, dlam, dmu, want_y=False, y=None, dy=None, ws=None, stream=None):
+    import torch
+    for t, n in ((lam, "lam"), (mu, "mu"), (dlam, "dlam"), (dmu, "dmu")):
+        _f32(t, g.img_shape, n)
+    if dy is None:
+        dy = torch.empty(g.sino_shape, dtype=torch.float32, device=lam.device)
+    if want_y and y is None:
+        y = torch.empty(g.sino_shape, dtype=torch.float32, device=lam.device)
+    ws = g.workspace("jvp") if ws is None else ws
+    _check(lib().pget_jvp(g.handle, _ptr(lam), _ptr(mu), _ptr(dlam), _ptr(dmu), _ptr(y) if want_y else None,
+                          _ptr(dy), _ptr(ws), ws.numel(), _stream(stream)), "pget_jvp")
+    return (y, dy) if want_y else dy
+
+
+def vjp(g: Geometry, lam, mu, w, g_lam=None, g_mu=None, ws=None, stream=None):
+    import torch
+    _f32(lam, g.img_shape, "lam"); _f32(mu, g.img_shape, "mu"); _f32(w, g.sino_shape, "w")
+    if g_lam is None:
+        g_lam = torch.empty(g.img_shape, dtype=torch.float32, device=lam.device)
+        g_mu = torch.empty(g.img_shape, dtype=torch.float32, device=lam.device)
+    ws = g.workspace("vjp") if ws is None else ws
+    _check(lib().pget_vjp(g.handle, _ptr(lam), _ptr(mu), _ptr(w), _ptr(g_lam), _ptr(g_mu), _ptr(ws), ws.numel(),
+                          _stream(stream)), "pget_vjp")
+    return g_lam, g_mu
+
+
+def gn_apply(g: Geometry, lam, mu, p_lam, p_mu, alpha, beta, ws=None, stream=None):
+    import torch
+    q_lam = torch.empty(g.img_shape, dtype=torch.float32, device=lam.device)
+    q_mu = torch.empty_like(q_lam)
+    ws = g.workspace("gn_apply") if ws is None else ws
+    _check(lib().pget_gn_apply(g.handle, _ptr(lam), _ptr(mu), _ptr(p_lam), _ptr(p_mu), float(alpha), float(beta),
+                               _ptr(q_lam), _ptr(q_mu), _ptr(ws), ws.numel(), _stream(stream)), "pget_gn_apply")
+    return q_lam, q_mu
+
+
+def stats_buffer(g: Geometry, device=None):
+    import torch
+    return torch.zeros(g.info["batch"] * C.sizeof(GNStats), dtype=torch.uint8,
+                       device=device or f"cuda:{g.device}")
+
+
+def read_stats(buf, batch: int, n_cg=None):
+    host = buf.cpu().numpy().tobytes()
+    out = []
+    for m in range(batch):
+        st = GNStats.from_buffer_copy(host[m * C.sizeof(GNStats):(m + 1) * C.sizeof(GNStats)])
+        out.append(st.to_dict(n_cg))
+    return out
+
+
+def gn_cg_step(g: Geometry, lam, mu, y_meas, alpha, beta, n_cg, flags=PGET_GN_EVAL_TRIAL, s_lam=None, s_mu=None,
+               stats=None, ws=None, stream=None):
+    """One LM iteration (pget_gn_cg_step).  Returns (s_lam, s_mu, stats_device_buffer)."""
+    import torch
+    _f32(lam, g.img_shape, "lam"); _f32(mu, g.img_shape, "mu"); _f32(y_meas, g.sino_shape, "y_meas")
+    if s_lam is None:
+        s_lam = torch.empty(g.img_shape, dtype=torch.float32, device=lam.device)
+        s_mu = torch.empty_like(s_lam)
+    if stats is None:
+        stats = stats_buffer(g, lam.device)
+    ws = g.workspace("gn_cg_step") if ws is None else ws
+    _check(lib().pget_gn_cg_step(g.handle, _ptr(lam), _ptr(mu), _ptr(y_meas), float(alpha), float(beta), int(n_cg),
+                                 int(flags), _ptr(s_lam), _ptr(s_mu), _ptr(stats), _ptr(ws), ws.numel(),
+                                 _stream(stream)), "pget_gn_cg_step")
+    return s_lam, s_mu, stats
+
+
+def profile_begin(max_launches: int = 4096):
+    """Start counting library kernel launches and timing projector launches (CUDA events)."""
+    _check(lib().pget_profile_begin(int(max_launches)), "pget_profile_begin")
+
+
+def profile_end():
+    """Stop tracing; returns {'ms': {mode: ms}, 'launches': {mode: n}, 'total_launches': n}."""
+    ms = (C.c_double * 4)()
+    n = (C.c_int64 * 4)()
+    tot = C.c_int64()
+    _check(lib().pget_profile_end(ms, n, C.byref(tot)), "pget_profile_end")
+    return {"ms": dict(zip(MODES, list(ms))), "launches": dict(zip(MODES, list(n))), "total_launches": tot.value}

@@ -1,0 +1,618 @@
+// api.cu -- the extern "C" boundary of libpget (include/pget.h): argument
+// validation, workspace carving, launch configuration and the LM-iteration
+// orchestration (SURVEY.md §3 call stacks 1-3).  Everything is enqueued on the
+// caller's stream; nothing here allocates, frees or synchronises except
+// pget_geometry_create / pget_geometry_destroy.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <atomic>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "kernels.cuh"
+
+using namespace pget;
+
+namespace {
+
+thread_local std::string g_err;
+
+// ---- tracing (pget_profile_begin / pget_profile_end)
+struct ProfRec {
+    int mode;
+    cudaEvent_t a, b;
+};
+struct Profiler {
+    std::mutex mu;
+    std::atomic<bool> on{false};
+    std::atomic<long long> total{0};
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    std::vector<ProfRec> recs;
+    long long mode_launches[4] = {0, 0, 0, 0};
+};
+Profiler g_prof;
+
+inline void note()
+{
+    if (g_prof.on.load(std::memory_order_relaxed)) g_prof.total.fetch_add(1, std::memory_order_relaxed);
+}
+
+pget_status fail(pget_status s, const std::string& msg)
+{
+    g_err = msg;
+    return s;
+}
+
+pget_status cuda_fail(cudaError_t e, const char* where)
+{
+    g_err = std::string(where) + ": " + cudaGetErrorString(e);
+    return PGET_ERR_CUDA;
+}
+
+#define CK(expr)                                          \
+    do {                                                  \
+        cudaError_t e_ = (expr);                          \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #expr); \
+    } while (0)
+
+constexpr int kNblk = 64;      // blocks per member of every reduction kernel (fixed order)
+constexpr int kVecThreads = 256;
+
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+struct ProjCfg {
+    int T, maxr, RbA, RbB;
+    size_t smem;
+    int rout_off, acc_off;
+};
+
+// Launch configuration of the projector for `mode`.
+ProjCfg proj_cfg(const Geometry& g, int mode)
+{
+    ProjCfg c;
+    int maxr = 1;
+    while ((g.R_pad + maxr - 1) / maxr > 1024) maxr *= 2;
+    c.maxr = maxr;
+    c.T = ((g.R_pad + maxr - 1) / maxr + 31) / 32 * 32;
+    const int ctas = std::max(1, std::min(4, 1536 / c.T));
+    const size_t limit = std::min<size_t>(g.smem_optin, 227 * 1024);
+    const size_t rout_bytes = 2 * sizeof(float) * g.R_pad;
+    long budget = static_cast<long>(limit / ctas) - 1024 - static_cast<long>(rout_bytes);
+    const int nfA = (mode == MODE_FWD || mode == MODE_VJP) ? 2 : 4;
+    auto rows = [&](int bytes_per_px) {
+        long r = budget / (static_cast<long>(g.Wp) * bytes_per_px) - 1;
+        return static_cast<int>(std::max<long>(1, std::min<long>(r, g.Hp - 1)));
+    };
+    c.RbA = rows(4 * nfA);
+    c.RbB = (mode == MODE_VJP || mode == MODE_GN) ? rows(16) : 1;
+    size_t regA = static_cast<size_t>(c.RbA + 1) * g.Wp * 4 * nfA;
+    size_t regB = (mode == MODE_VJP || mode == MODE_GN) ? static_cast<size_t>(c.RbB + 1) * g.Wp * 16 : 0;
+    size_t region = std::max(regA, regB);
+    region = (region + 15) & ~size_t(15);
+    c.rout_off = static_cast<int>(region / sizeof(float));
+    c.acc_off = static_cast<int>(static_cast<size_t>(c.RbB + 1) * g.Wp * 2);
+    c.smem = region + rout_bytes;
+    return c;
+}
+
+ProjArgs base_args(const Geometry& g, const ProjCfg& c)
+{
+    ProjArgs A;
+    std::memset(&A, 0, sizeof A);
+    A.rays = g.d_rays;
+    A.abdir = g.d_abdir;
+    A.w = g.d_w;
+    A.Hp = g.Hp;
+    A.Wp = g.Wp;
+    A.n_det = g.desc.n_det;
+    A.J = g.desc.n_subrays;
+    A.R = g.R;
+    A.R_pad = g.R_pad;
+    A.n_ab = g.n_ab;
+    A.RbA = c.RbA;
+    A.RbB = c.RbB;
+    A.rout_off = c.rout_off;
+    A.acc_off = c.acc_off;
+    A.delta = static_cast<float>(g.delta);
+    const double cf = -g.delta * 1.4426950408889634;   // -Delta log2(e)
+    A.cf = static_cast<float>(cf);
+    A.ch = static_cast<float>(0.5 * cf);
+    return A;
+}
+
+pget_status run_proj(const Geometry& g, int mode, ProjArgs A, cudaStream_t s)
+{
+    const ProjCfg c = proj_cfg(g, mode);
+    A.RbA = c.RbA;
+    A.RbB = c.RbB;
+    A.rout_off = c.rout_off;
+    A.acc_off = c.acc_off;
+    const int grid = g.desc.batch * g.n_ab;
+    cudaEvent_t ea = nullptr, eb = nullptr;
+    if (g_prof.on.load(std::memory_order_relaxed)) {
+        std::lock_guard<std::mutex> lk(g_prof.mu);
+        g_prof.total++;
+        g_prof.mode_launches[mode]++;
+        if (g_prof.used + 2 <= g_prof.pool.size()) {
+            ea = g_prof.pool[g_prof.used++];
+            eb = g_prof.pool[g_prof.used++];
+            g_prof.recs.push_back({mode, ea, eb});
+        }
+    }
+    if (ea) cudaEventRecord(ea, s);
+    cudaError_t e = launch_proj(mode, c.maxr, A, grid, c.T, c.smem, s);
+    if (eb) cudaEventRecord(eb, s);
+    if (e != cudaSuccess) return cuda_fail(e, "projector launch");
+    return PGET_OK;
+}
+
+// ---- workspace carving
+struct WS {
+    float2* img2 = nullptr;
+    float4* img4 = nullptr;
+    float2* acc = nullptr;
+    float *ysino = nullptr, *dysino = nullptr;
+    float *bl = nullptr, *bm = nullptr, *zl = nullptr, *zm = nullptr, *pl = nullptr, *pm = nullptr;
+    float *ql = nullptr, *qm = nullptr, *ul = nullptr, *um = nullptr;
+    double* part = nullptr;   // [8][B][kNblk]
+    CGState* cg = nullptr;
+    size_t bytes = 0;
+};
+
+WS carve(const Geometry& g, int op, char* base)
+{
+    WS w;
+    size_t off = 0;
+    const size_t B = g.desc.batch;
+    const size_t img = B * g.Hp * g.Wp;
+    const size_t n2 = B * g.desc.n_px * g.desc.n_px;
+    const size_t ns = B * g.n_ab * g.desc.n_det;
+    auto take = [&](size_t bytes) -> char* {
+        char* p = base ? base + off : nullptr;
+        off += align256(bytes);
+        return p;
+    };
+    const bool need2 = op == PGET_OP_FORWARD || op == PGET_OP_VJP || op == PGET_OP_GN_APPLY || op == PGET_OP_GN_CG_STEP;
+    const bool need4 = op == PGET_OP_JVP || op == PGET_OP_GN_APPLY || op == PGET_OP_GN_CG_STEP;
+    const bool needacc = op == PGET_OP_VJP || op == PGET_OP_GN_APPLY || op == PGET_OP_GN_CG_STEP;
+    if (need2) w.img2 = reinterpret_cast<float2*>(take(img * sizeof(float2)));
+    if (need4) w.img4 = reinterpret_cast<float4*>(take(img * sizeof(float4)));
+    if (needacc) w.acc = reinterpret_cast<float2*>(take(img * sizeof(float2)));
+    if (op == PGET_OP_GN_CG_STEP) {
+        w.ysino = reinterpret_cast<float*>(take(ns * sizeof(float)));
+        w.dysino = reinterpret_cast<float*>(take(ns * sizeof(float)));
+        float** vecs[] = {&w.bl, &w.bm, &w.zl, &w.zm, &w.pl, &w.pm, &w.ql, &w.qm, &w.ul, &w.um};
+        for (float** v : vecs) *v = reinterpret_cast<float*>(take(n2 * sizeof(float)));
+        w.part = reinterpret_cast<double*>(take(8 * B * kNblk * sizeof(double)));
+        w.cg = reinterpret_cast<CGState*>(take(B * sizeof(CGState)));
+    }
+    w.bytes = off;
+    return w;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+pget_status check_ptrs(std::initializer_list<const void*> ptrs, const char* what)
+{
+    for (const void* p : ptrs) {
+        if (!p) return fail(PGET_ERR_INVALID_ARGUMENT, std::string(what) + ": NULL device pointer");
+        if (!aligned16(p)) return fail(PGET_ERR_ALIGNMENT, std::string(what) + ": pointer not 16-byte aligned");
+    }
+    return PGET_OK;
+}
+
+pget_status check_common(pget_geometry h, int op, void* ws, size_t ws_bytes, WS* w)
+{
+    if (!h) return fail(PGET_ERR_INVALID_ARGUMENT, "NULL geometry handle");
+    if (h->g.device < 0) return fail(PGET_ERR_INVALID_ARGUMENT, "host-only geometry handle (device < 0)");
+    int dev = -1;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+    if (dev != h->g.device)
+        return fail(PGET_ERR_INVALID_ARGUMENT, "current CUDA device differs from the geometry's device");
+    const WS need = carve(h->g, op, nullptr);
+    if (ws_bytes < need.bytes) return fail(PGET_ERR_WORKSPACE, "workspace too small");
+    if (need.bytes && (!ws || !aligned16(ws))) return fail(PGET_ERR_WORKSPACE, "workspace NULL or misaligned");
+    *w = carve(h->g, op, static_cast<char*>(ws));
+    return PGET_OK;
+}
+
+int vec_grid(size_t n)
+{
+    return static_cast<int>(std::max<size_t>(1, std::min<size_t>(1184, (n + kVecThreads - 1) / kVecThreads)));
+}
+
+}  // namespace
+
+// =========================================================================================== C ABI
+extern "C" {
+
+const char* pget_status_string(pget_status s)
+{
+    switch (s) {
+    case PGET_OK: return "PGET_OK";
+    case PGET_ERR_INVALID_ARGUMENT: return "PGET_ERR_INVALID_ARGUMENT";
+    case PGET_ERR_SHAPE: return "PGET_ERR_SHAPE";
+    case PGET_ERR_ALIGNMENT: return "PGET_ERR_ALIGNMENT";
+    case PGET_ERR_WORKSPACE: return "PGET_ERR_WORKSPACE";
+    case PGET_ERR_OUT_OF_MEMORY: return "PGET_ERR_OUT_OF_MEMORY";
+    case PGET_ERR_CUDA: return "PGET_ERR_CUDA";
+    case PGET_ERR_NOT_FINITE: return "PGET_ERR_NOT_FINITE";
+    }
+    return "PGET_ERR_UNKNOWN";
+}
+
+const char* pget_last_error_message(void) { return g_err.c_str(); }
+
+pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pget_geometry* out)
+{
+    if (!out) return fail(PGET_ERR_INVALID_ARGUMENT, "out is NULL");
+    *out = nullptr;
+    pget_geometry h = new (std::nothrow) pget_geometry_s;
+    if (!h) return fail(PGET_ERR_OUT_OF_MEMORY, "host allocation failed");
+    std::string err;
+    pget_status st = build_geometry(desc, &h->g, &err);
+    if (st != PGET_OK) { delete h; return fail(st, err); }
+    Geometry& g = h->g;
+    if (g.desc.n_px > 2048) { delete h; return fail(PGET_ERR_INVALID_ARGUMENT, "n_px > 2048 not supported"); }
+    g.device = device;
+    if (device < 0) {   // host-only handle: tables and info, no device tables, no compute
+        *out = h;
+        return PGET_OK;
+    }
+    int prev = -1;
+    cudaError_t e = cudaGetDevice(&prev);
+    if (e == cudaSuccess) e = cudaSetDevice(device);
+    int optin = 0;
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g.sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    if (e == cudaSuccess) g.smem_optin = static_cast<size_t>(optin);
+    std::vector<RayP> rays;
+    std::vector<int8_t> abdir;
+    build_ray_params(g, &rays, &abdir);
+    if (e == cudaSuccess) e = cudaMalloc(&g.d_rays, rays.size() * sizeof(RayP));
+    if (e == cudaSuccess) e = cudaMalloc(&g.d_abdir, abdir.size());
+    if (e == cudaSuccess) e = cudaMalloc(&g.d_w, g.wf.size() * sizeof(float));
+    if (e == cudaSuccess) e = cudaMemcpy(g.d_rays, rays.data(), rays.size() * sizeof(RayP), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(g.d_abdir, abdir.data(), abdir.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(g.d_w, g.wf.data(), g.wf.size() * sizeof(float), cudaMemcpyHostToDevice);
+    size_t smax = 0;
+    for (int mode = 0; mode < 4; ++mode) smax = std::max(smax, proj_cfg(g, mode).smem);
+    if (e == cudaSuccess && smax > g.smem_optin) e = cudaErrorInvalidConfiguration;
+    if (e == cudaSuccess) e = set_proj_smem_limit(smax);
+    if (prev >= 0) cudaSetDevice(prev);
+    if (e != cudaSuccess) {
+        cudaFree(g.d_rays); cudaFree(g.d_abdir); cudaFree(g.d_w);
+        delete h;
+        return cuda_fail(e, "pget_geometry_create");
+    }
+    *out = h;
+    return PGET_OK;
+}
+
+pget_status pget_geometry_destroy(pget_geometry h)
+{
+    if (!h) return PGET_OK;
+    if (h->g.device < 0) { delete h; return PGET_OK; }
+    int prev = -1;
+    cudaGetDevice(&prev);
+    cudaSetDevice(h->g.device);
+    cudaFree(h->g.d_rays);
+    cudaFree(h->g.d_abdir);
+    cudaFree(h->g.d_w);
+    if (prev >= 0) cudaSetDevice(prev);
+    delete h;
+    return PGET_OK;
+}
+
+pget_status pget_geometry_info(pget_geometry h, pget_geometry_info_t* o)
+{
+    if (!h || !o) return fail(PGET_ERR_INVALID_ARGUMENT, "NULL argument");
+    const Geometry& g = h->g;
+    const pget_geometry_desc& d = g.desc;
+    o->n_rays = static_cast<int64_t>(d.batch) * g.n_ab * g.R;
+    o->n_samples_nominal = g.n_samples_nominal;
+    o->image_elems = static_cast<int64_t>(d.batch) * d.n_px * d.n_px;
+    o->sino_elems = static_cast<int64_t>(d.batch) * g.n_ab * d.n_det;
+    o->n_t = g.n_t;
+    o->n_px = d.n_px;
+    o->n_angles = d.n_angles;
+    o->n_banks = d.n_banks;
+    o->n_det = d.n_det;
+    o->n_subrays = d.n_subrays;
+    o->batch = d.batch;
+    o->h = g.h;
+    o->delta = g.delta;
+    o->T = g.T;
+    return PGET_OK;
+}
+
+size_t pget_table_bytes(pget_geometry h, int id)
+{
+    if (!h) return 0;
+    const Geometry& g = h->g;
+    switch (id) {
+    case PGET_TABLE_ANGLES: return g.angles.size() * sizeof(double);
+    case PGET_TABLE_DIRS: return g.dirs.size() * sizeof(double);
+    case PGET_TABLE_OFFSETS: return g.offsets.size() * sizeof(double);
+    case PGET_TABLE_WEIGHTS: return g.weights.size() * sizeof(double);
+    case PGET_TABLE_TLAT: return 3 * sizeof(double);
+    case PGET_TABLE_CLIP: return g.clip.size() * sizeof(int32_t);
+    }
+    return 0;
+}
+
+pget_status pget_geometry_export(pget_geometry h, int id, void* dst, size_t bytes)
+{
+    if (!h || !dst) return fail(PGET_ERR_INVALID_ARGUMENT, "NULL argument");
+    const size_t need = pget_table_bytes(h, id);
+    if (need == 0) return fail(PGET_ERR_INVALID_ARGUMENT, "bad table id");
+    if (bytes < need) return fail(PGET_ERR_SHAPE, "destination too small");
+    const Geometry& g = h->g;
+    const double tl[3] = {g.h, g.delta, g.T};
+    const void* src = nullptr;
+    switch (id) {
+    case PGET_TABLE_ANGLES: src = g.angles.data(); break;
+    case PGET_TABLE_DIRS: src = g.dirs.data(); break;
+    case PGET_TABLE_OFFSETS: src = g.offsets.data(); break;
+    case PGET_TABLE_WEIGHTS: src = g.weights.data(); break;
+    case PGET_TABLE_TLAT: src = tl; break;
+    case PGET_TABLE_CLIP: src = g.clip.data(); break;
+    }
+    std::memcpy(dst, src, need);
+    return PGET_OK;
+}
+
+size_t pget_workspace_bytes(pget_geometry h, int op)
+{
+    if (!h || op < 0 || op > PGET_OP_GN_APPLY) return 0;
+    return carve(h->g, op, nullptr).bytes + 256;
+}
+
+pget_status pget_forward(pget_geometry h, const float* lam, const float* mu, float* y, void* ws, size_t ws_bytes,
+                         pget_stream_t stream)
+{
+    WS w;
+    pget_status st = check_common(h, PGET_OP_FORWARD, ws, ws_bytes, &w);
+    if (st) return st;
+    if ((st = check_ptrs({lam, mu, y}, "pget_forward"))) return st;
+    const Geometry& g = h->g;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const size_t img = static_cast<size_t>(g.desc.batch) * g.Hp * g.Wp;
+    pack2_kernel<<<vec_grid(img), kVecThreads, 0, s>>>(lam, mu, nullptr, nullptr, w.img2, nullptr, nullptr,
+                                                      g.desc.n_px, g.Hp, g.Wp, g.desc.batch); note();
+    CK(cudaGetLastError());
+    ProjArgs A = base_args(g, proj_cfg(g, MODE_FWD));
+    A.img2 = w.img2;
+    A.y = y;
+    return run_proj(g, MODE_FWD, A, s);
+}
+
+pget_status pget_jvp(pget_geometry h, const float* lam, const float* mu, const float* dlam, const float* dmu,
+                     float* y, float* dy, void* ws, size_t ws_bytes, pget_stream_t stream)
+{
+    WS w;
+    pget_status st = check_common(h, PGET_OP_JVP, ws, ws_bytes, &w);
+    if (st) return st;
+    if ((st = check_ptrs({lam, mu, dlam, dmu, dy}, "pget_jvp"))) return st;
+    if (y && !aligned16(y)) return fail(PGET_ERR_ALIGNMENT, "pget_jvp: y not 16-byte aligned");
+    const Geometry& g = h->g;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const size_t img = static_cast<size_t>(g.desc.batch) * g.Hp * g.Wp;
+    pack4_kernel<<<vec_grid(img), kVecThreads, 0, s>>>(lam, mu, dlam, dmu, w.img4, g.desc.n_px, g.Hp, g.Wp,
+                                                      g.desc.batch); note();
+    CK(cudaGetLastError());
+    ProjArgs A = base_args(g, proj_cfg(g, MODE_JVP));
+    A.img4 = w.img4;
+    A.y = y;
+    A.dy = dy;
+    return run_proj(g, MODE_JVP, A, s);
+}
+
+static pget_status vjp_core(const Geometry& g, const WS& w, const float* w_in, cudaStream_t s)
+{
+    const size_t img = static_cast<size_t>(g.desc.batch) * g.Hp * g.Wp;
+    CK(cudaMemsetAsync(w.acc, 0, img * sizeof(float2), s));
+    ProjArgs A = base_args(g, proj_cfg(g, MODE_VJP));
+    A.img2 = w.img2;
+    A.acc = w.acc;
+    A.win = w_in;
+    return run_proj(g, MODE_VJP, A, s);
+}
+
+pget_status pget_vjp(pget_geometry h, const float* lam, const float* mu, const float* wv, float* g_lam, float* g_mu,
+                     void* ws, size_t ws_bytes, pget_stream_t stream)
+{
+    WS w;
+    pget_status st = check_common(h, PGET_OP_VJP, ws, ws_bytes, &w);
+    if (st) return st;
+    if ((st = check_ptrs({lam, mu, wv, g_lam, g_mu}, "pget_vjp"))) return st;
+    const Geometry& g = h->g;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int N = g.desc.n_px, B = g.desc.batch;
+    const size_t img = static_cast<size_t>(B) * g.Hp * g.Wp;
+    pack2_kernel<<<vec_grid(img), kVecThreads, 0, s>>>(lam, mu, nullptr, nullptr, w.img2, nullptr, nullptr, N,
+                                                      g.Hp, g.Wp, B); note();
+    CK(cudaGetLastError());
+    if ((st = vjp_core(g, w, wv, s))) return st;
+    finish_kernel<<<dim3(vec_grid(static_cast<size_t>(N) * N), B), kVecThreads, 0, s>>>(
+        w.acc, nullptr, nullptr, 0.f, 0.f, 1.f, g_lam, g_mu, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+        nullptr, nullptr, nullptr, N, g.Hp, g.Wp); note();
+    CK(cudaGetLastError());
+    return PGET_OK;
+}
+
+static pget_status gn_core(const Geometry& g, const WS& w, const float* lam, const float* mu, const float* pl,
+                           const float* pm, cudaStream_t s)
+{
+    const int N = g.desc.n_px, B = g.desc.batch;
+    const size_t img = static_cast<size_t>(B) * g.Hp * g.Wp;
+    pack4_kernel<<<vec_grid(img), kVecThreads, 0, s>>>(lam, mu, pl, pm, w.img4, N, g.Hp, g.Wp, B); note();
+    CK(cudaGetLastError());
+    CK(cudaMemsetAsync(w.acc, 0, img * sizeof(float2), s));
+    ProjArgs A = base_args(g, proj_cfg(g, MODE_GN));
+    A.img2 = w.img2;
+    A.img4 = w.img4;
+    A.acc = w.acc;
+    return run_proj(g, MODE_GN, A, s);
+}
+
+pget_status pget_gn_apply(pget_geometry h, const float* lam, const float* mu, const float* p_lam, const float* p_mu,
+                          float alpha, float beta, float* q_lam, float* q_mu, void* ws, size_t ws_bytes,
+                          pget_stream_t stream)
+{
+    WS w;
+    pget_status st = check_common(h, PGET_OP_GN_APPLY, ws, ws_bytes, &w);
+    if (st) return st;
+    if ((st = check_ptrs({lam, mu, p_lam, p_mu, q_lam, q_mu}, "pget_gn_apply"))) return st;
+    if (!std::isfinite(alpha) || !std::isfinite(beta) || alpha < 0.f || beta < 0.f)
+        return fail(PGET_ERR_INVALID_ARGUMENT, "alpha, beta must be finite and >= 0");
+    const Geometry& g = h->g;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int N = g.desc.n_px, B = g.desc.batch;
+    const size_t img = static_cast<size_t>(B) * g.Hp * g.Wp;
+    pack2_kernel<<<vec_grid(img), kVecThreads, 0, s>>>(lam, mu, nullptr, nullptr, w.img2, nullptr, nullptr, N,
+                                                      g.Hp, g.Wp, B); note();
+    CK(cudaGetLastError());
+    if ((st = gn_core(g, w, lam, mu, p_lam, p_mu, s))) return st;
+    finish_kernel<<<dim3(vec_grid(static_cast<size_t>(N) * N), B), kVecThreads, 0, s>>>(
+        w.acc, p_lam, p_mu, alpha, beta, 1.f, q_lam, q_mu, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+        nullptr, nullptr, nullptr, N, g.Hp, g.Wp); note();
+    CK(cudaGetLastError());
+    return PGET_OK;
+}
+
+pget_status pget_gn_cg_step(pget_geometry h, const float* lam, const float* mu, const float* y_meas, float alpha,
+                            float beta, int32_t n_cg, uint32_t flags, float* s_lam, float* s_mu,
+                            pget_gn_stats* stats, void* ws, size_t ws_bytes, pget_stream_t stream)
+{
+    WS w;
+    pget_status st = check_common(h, PGET_OP_GN_CG_STEP, ws, ws_bytes, &w);
+    if (st) return st;
+    if ((st = check_ptrs({lam, mu, y_meas, s_lam, s_mu, stats}, "pget_gn_cg_step"))) return st;
+    if (n_cg < 0 || n_cg > PGET_MAX_CG) return fail(PGET_ERR_INVALID_ARGUMENT, "n_cg out of [0, PGET_MAX_CG]");
+    if (!std::isfinite(alpha) || !std::isfinite(beta) || alpha < 0.f || beta < 0.f)
+        return fail(PGET_ERR_INVALID_ARGUMENT, "alpha, beta must be finite and >= 0");
+    const Geometry& g = h->g;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int N = g.desc.n_px, B = g.desc.batch;
+    const int n2 = N * N;
+    const int nsper = g.n_ab * g.desc.n_det;
+    const size_t img = static_cast<size_t>(B) * g.Hp * g.Wp;
+    const dim3 vg(kNblk, B);
+    double* P[8];
+    for (int k = 0; k < 8; ++k) P[k] = w.part + static_cast<size_t>(k) * B * kNblk;
+    const int sgrid = (B + 127) / 128;
+
+    // 1-2: r = F(u) - y, 1/2||r||^2, ||Lu||^2
+    pack2_kernel<<<vec_grid(img), kVecThreads, 0, s>>>(lam, mu, nullptr, nullptr, w.img2, nullptr, nullptr, N,
+                                                      g.Hp, g.Wp, B); note();
+    CK(cudaGetLastError());
+    {
+        ProjArgs A = base_args(g, proj_cfg(g, MODE_FWD));
+        A.img2 = w.img2;
+        A.y = w.ysino;
+        if ((st = run_proj(g, MODE_FWD, A, s))) return st;
+    }
+    residual_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, y_meas, P[0], nsper); note();
+    regsq_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, P[1], N); note();
+    CK(cudaGetLastError());
+    // 3: b = -(J^T r + alpha L^T L u); z = p = b; s = 0; ||b||^2
+    if ((st = vjp_core(g, w, w.ysino, s))) return st;
+    finish_kernel<<<vg, kVecThreads, 0, s>>>(w.acc, lam, mu, alpha, 0.f, -1.f, w.bl, w.bm, w.bl, w.bm, P[2], w.zl,
+                                            w.zm, w.pl, w.pm, s_lam, s_mu, N, g.Hp, g.Wp); note();
+    CK(cudaGetLastError());
+    scalar_kernel<<<sgrid, 128, 0, s>>>(SC_INIT, 0, P[0], P[1], P[2], kNblk, w.cg, stats, B, alpha, beta); note();
+    CK(cudaGetLastError());
+    // 5: CG
+    for (int k = 0; k < n_cg; ++k) {
+        if ((st = gn_core(g, w, lam, mu, w.pl, w.pm, s))) return st;
+        finish_kernel<<<vg, kVecThreads, 0, s>>>(w.acc, w.pl, w.pm, alpha, beta, 1.f, w.ql, w.qm, w.pl, w.pm, P[3],
+                                                nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, N, g.Hp, g.Wp); note();
+        scalar_kernel<<<sgrid, 128, 0, s>>>(SC_GAMMA, k, P[3], nullptr, nullptr, kNblk, w.cg, stats, B, alpha, beta); note();
+        cg_update1_kernel<<<vg, kVecThreads, 0, s>>>(s_lam, s_mu, w.zl, w.zm, w.pl, w.pm, w.ql, w.qm, w.cg, P[4], n2); note();
+        scalar_kernel<<<sgrid, 128, 0, s>>>(SC_ZETA, k, P[4], nullptr, nullptr, kNblk, w.cg, stats, B, alpha, beta); note();
+        cg_update2_kernel<<<vg, kVecThreads, 0, s>>>(w.zl, w.zm, w.pl, w.pm, w.cg, n2); note();
+        CK(cudaGetLastError());
+    }
+    // 6: pred = <b,s> - 1/2(||Js||^2 + alpha ||Ls||^2)
+    pack4_kernel<<<vec_grid(img), kVecThreads, 0, s>>>(lam, mu, s_lam, s_mu, w.img4, N, g.Hp, g.Wp, B); note();
+    CK(cudaGetLastError());
+    {
+        ProjArgs A = base_args(g, proj_cfg(g, MODE_JVP));
+        A.img4 = w.img4;
+        A.y = nullptr;
+        A.dy = w.dysino;
+        if ((st = run_proj(g, MODE_JVP, A, s))) return st;
+    }
+    sumsq_kernel<<<vg, kVecThreads, 0, s>>>(w.dysino, P[5], nsper); note();
+    regsq_kernel<<<vg, kVecThreads, 0, s>>>(s_lam, s_mu, P[6], N); note();
+    dot2_kernel<<<vg, kVecThreads, 0, s>>>(w.bl, w.bm, s_lam, s_mu, P[7], n2); note();
+    scalar_kernel<<<sgrid, 128, 0, s>>>(SC_PRED, 0, P[5], P[6], P[7], kNblk, w.cg, stats, B, alpha, beta); note();
+    CK(cudaGetLastError());
+    // 7-8: f(u+s), rho, accept, beta_next
+    if (flags & PGET_GN_EVAL_TRIAL) {
+        pack2_kernel<<<vec_grid(img), kVecThreads, 0, s>>>(lam, mu, s_lam, s_mu, w.img2, w.ul, w.um, N, g.Hp, g.Wp, B); note();
+        CK(cudaGetLastError());
+        ProjArgs A = base_args(g, proj_cfg(g, MODE_FWD));
+        A.img2 = w.img2;
+        A.y = w.ysino;
+        if ((st = run_proj(g, MODE_FWD, A, s))) return st;
+        residual_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, y_meas, P[0], nsper); note();
+        regsq_kernel<<<vg, kVecThreads, 0, s>>>(w.ul, w.um, P[1], N); note();
+        scalar_kernel<<<sgrid, 128, 0, s>>>(SC_TRIAL, 0, P[0], P[1], nullptr, kNblk, w.cg, stats, B, alpha, beta); note();
+        CK(cudaGetLastError());
+    }
+    return PGET_OK;
+}
+
+pget_status pget_profile_begin(int32_t max_launches)
+{
+    if (max_launches < 0) return fail(PGET_ERR_INVALID_ARGUMENT, "max_launches < 0");
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    for (cudaEvent_t e : g_prof.pool) cudaEventDestroy(e);
+    g_prof.pool.clear();
+    g_prof.recs.clear();
+    g_prof.used = 0;
+    for (int k = 0; k < 4; ++k) g_prof.mode_launches[k] = 0;
+    g_prof.total = 0;
+    for (int k = 0; k < 2 * max_launches; ++k) {
+        cudaEvent_t e;
+        cudaError_t err = cudaEventCreate(&e);
+        if (err != cudaSuccess) return cuda_fail(err, "cudaEventCreate");
+        g_prof.pool.push_back(e);
+    }
+    g_prof.on = true;
+    return PGET_OK;
+}
+
+pget_status pget_profile_end(double* ms, int64_t* launches, int64_t* total)
+{
+    std::lock_guard<std::mutex> lk(g_prof.mu);
+    g_prof.on = false;
+    double acc[4] = {0, 0, 0, 0};
+    for (const ProfRec& r : g_prof.recs) {
+        cudaError_t e = cudaEventSynchronize(r.b);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize");
+        float t = 0.f;
+        e = cudaEventElapsedTime(&t, r.a, r.b);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaEventElapsedTime");
+        acc[r.mode] += t;
+    }
+    for (int k = 0; k < 4; ++k) {
+        if (ms) ms[k] = acc[k];
+        if (launches) launches[k] = g_prof.mode_launches[k];
+    }
+    if (total) *total = g_prof.total.load();
+    return PGET_OK;
+}
+
+}  // extern "C"

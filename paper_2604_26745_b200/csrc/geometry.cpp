@@ -1,0 +1,171 @@
+// geometry.cpp -- host geometry builder of libpget (native C++, fp64).
+//
+// Builds the O1 tables of SURVEY.md §8(c.2) for the detector geometry of
+// PAPER.md:33 (two opposing banks of detectors, full rotation) and the
+// parallel-ray line parametrisation s*theta_perp + t*theta of PAPER.md:48-54
+// (eq:fwd_model).  The fp64 operation order follows the O1 text exactly and the
+// file is compiled with -ffp-contract=off, so the exported tables are bit-exact
+// with any other implementation of the same text (tests/test_abi.py compares them
+// with the oracle's; the two share no code).  It then derives the library's own
+// 32.32 fixed-point sample parametrisation (RayP) used by the kernels.
+#include <cmath>
+#include <cstdio>
+
+#include "internal.h"
+
+namespace pget {
+
+static const double kPi = 3.14159265358979323846;
+
+pget_status build_geometry(const pget_geometry_desc* d, Geometry* g, std::string* err)
+{
+    if (!d) { *err = "desc is NULL"; return PGET_ERR_INVALID_ARGUMENT; }
+    char buf[256];
+    if (d->n_px < 2 || d->n_px > 8192 || d->n_angles < 1 || d->n_angles > 1000000 || d->n_banks < 1 ||
+        d->n_banks > 2 || d->n_det < 2 || d->n_det > 100000 || d->n_subrays < 1 ||
+        d->n_subrays > kMaxSubrays || d->batch < 1 || !(d->subray_sigma > 0.0) || !(d->step_px > 0.0) ||
+        !std::isfinite(d->subray_sigma) || !std::isfinite(d->step_px) || !std::isfinite(d->bank1_shift) ||
+        d->step_px > 4.0) {
+        std::snprintf(buf, sizeof buf,
+                      "invalid geometry desc (n_px=%d n_angles=%d n_banks=%d n_det=%d J=%d batch=%d "
+                      "sigma=%g step=%g shift=%g)",
+                      d->n_px, d->n_angles, d->n_banks, d->n_det, d->n_subrays, d->batch, d->subray_sigma,
+                      d->step_px, d->bank1_shift);
+        *err = buf;
+        return PGET_ERR_INVALID_ARGUMENT;
+    }
+    g->desc = *d;
+    const int N = d->n_px, nA = d->n_angles, nB = d->n_banks, nd = d->n_det, J = d->n_subrays;
+
+    // t-lattice: h = 2/N, Delta = step_px h, T = Delta ceil((sqrt2 + h)/Delta), n_t = 2T/Delta
+    g->h = 2.0 / N;
+    g->delta = d->step_px * g->h;
+    const double m = std::ceil((std::sqrt(2.0) + g->h) / g->delta);
+    g->T = g->delta * m;
+    g->n_t = 2 * static_cast<int>(m);
+
+    // angles theta_a = 2 pi a / n_A; bank b: phi = theta_a + b pi
+    g->angles.resize(nA);
+    for (int a = 0; a < nA; ++a) g->angles[a] = 2.0 * kPi * static_cast<double>(a) / static_cast<double>(nA);
+    g->dirs.resize(static_cast<size_t>(nA) * nB * 2);
+    for (int a = 0; a < nA; ++a)
+        for (int b = 0; b < nB; ++b) {
+            const double phi = g->angles[a] + static_cast<double>(b) * kPi;
+            g->dirs[(static_cast<size_t>(a) * nB + b) * 2 + 0] = std::cos(phi);
+            g->dirs[(static_cast<size_t>(a) * nB + b) * 2 + 1] = std::sin(phi);
+        }
+
+    // offsets sigma_{b,d,j} = s_d (+ shift p on bank 1) + delta_j; p = 2/(n_det-1)
+    const double p = 2.0 / static_cast<double>(nd - 1);
+    g->offsets.resize(static_cast<size_t>(nB) * nd * J);
+    for (int b = 0; b < nB; ++b)
+        for (int dd = 0; dd < nd; ++dd) {
+            double s = static_cast<double>(2 * dd - (nd - 1)) / static_cast<double>(nd - 1);
+            if (b == 1) s = s + d->bank1_shift * p;
+            for (int j = 0; j < J; ++j) {
+                const double dj = static_cast<double>(2 * j + 1 - J) / static_cast<double>(2 * J) * p;
+                g->offsets[(static_cast<size_t>(b) * nd + dd) * J + j] = s + dj;
+            }
+        }
+
+    // weights w_j = exp(-delta_j^2 / (2 (sigma p)^2)) / sum
+    g->weights.resize(J);
+    {
+        const double sp = d->subray_sigma * p;
+        double sum = 0.0;
+        for (int j = 0; j < J; ++j) {
+            const double dj = static_cast<double>(2 * j + 1 - J) / static_cast<double>(2 * J) * p;
+            g->weights[j] = std::exp(-(dj * dj) / (2.0 * sp * sp));
+            sum += g->weights[j];
+        }
+        for (int j = 0; j < J; ++j) g->weights[j] = g->weights[j] / sum;
+    }
+    g->wf.resize(J);
+    for (int j = 0; j < J; ++j) g->wf[j] = static_cast<float>(g->weights[j]);
+
+    // clip: slab test of x(t) = sigma omega_perp + t omega against |x|,|y| <= 1 + h/2
+    const double bb = 1.0 + g->h / 2.0;
+    g->clip.resize(static_cast<size_t>(nA) * nB * nd * J * 2);
+    int64_t nominal = 0;
+    for (int a = 0; a < nA; ++a)
+        for (int b = 0; b < nB; ++b) {
+            const double c = g->dirs[(static_cast<size_t>(a) * nB + b) * 2 + 0];
+            const double s = g->dirs[(static_cast<size_t>(a) * nB + b) * 2 + 1];
+            const double om[2] = {c, s};
+            const double op[2] = {-s, c};
+            for (int dd = 0; dd < nd; ++dd)
+                for (int j = 0; j < J; ++j) {
+                    const double sigma = g->offsets[(static_cast<size_t>(b) * nd + dd) * J + j];
+                    double tin = -INFINITY, tout = INFINITY;
+                    for (int k = 0; k < 2; ++k) {
+                        const double base = sigma * op[k];
+                        if (om[k] == 0.0) {
+                            if (std::fabs(base) > bb) { tin = INFINITY; tout = -INFINITY; }
+                        } else {
+                            const double t1 = (-bb - base) / om[k];
+                            const double t2 = (bb - base) / om[k];
+                            const double lo = t1 < t2 ? t1 : t2, hi = t1 < t2 ? t2 : t1;
+                            if (lo > tin) tin = lo;
+                            if (hi < tout) tout = hi;
+                        }
+                    }
+                    int32_t ilo = 0, ihi = -1;
+                    if (tin <= tout) {
+                        double lo = std::ceil((tin + g->T) / g->delta - 0.5);
+                        double hi = std::floor((tout + g->T) / g->delta - 0.5);
+                        if (lo < 0.0) lo = 0.0;
+                        if (hi > static_cast<double>(g->n_t - 1)) hi = static_cast<double>(g->n_t - 1);
+                        if (lo <= hi) { ilo = static_cast<int32_t>(lo); ihi = static_cast<int32_t>(hi); }
+                    }
+                    const size_t r = ((static_cast<size_t>(a) * nB + b) * nd + dd) * J + j;
+                    g->clip[2 * r] = ilo;
+                    g->clip[2 * r + 1] = ihi;
+                    nominal += ihi - ilo + 1;
+                }
+        }
+    g->n_samples_nominal = nominal * d->batch;
+
+    g->R = nd * J;
+    g->R_pad = (g->R + 31) / 32 * 32;
+    g->n_ab = nA * nB;
+    g->Hp = N + 2 * kHalo;
+    g->Wp = (N + 2 * kHalo + 1) & ~1;   // even: 16-B aligned rows of float2 for the band copies
+    return PGET_OK;
+}
+
+// 32.32 fixed-point sample positions in padded pixel coordinates.
+void build_ray_params(const Geometry& g, std::vector<RayP>* rays, std::vector<int8_t>* abdir)
+{
+    const int nB = g.desc.n_banks, nd = g.desc.n_det, J = g.desc.n_subrays;
+    rays->resize(static_cast<size_t>(g.n_ab) * g.R);
+    abdir->resize(g.n_ab);
+    const double scale = 4294967296.0;   // 2^32
+    const int64_t bias = int64_t(1) << 8; // +2^-24 px: round the 23-bit fraction to nearest
+    const double t0 = -g.T + 0.5 * g.delta;
+    for (int ab = 0; ab < g.n_ab; ++ab) {
+        const int b = ab % nB;
+        const double c = g.dirs[static_cast<size_t>(ab) * 2 + 0];
+        const double s = g.dirs[static_cast<size_t>(ab) * 2 + 1];
+        const double du = g.delta * c / g.h, dv = g.delta * s / g.h;
+        const int64_t dU = std::llround(du * scale), dV = std::llround(dv * scale);
+        (*abdir)[ab] = dV > 0 ? 1 : (dV < 0 ? -1 : 0);
+        for (int dd = 0; dd < nd; ++dd)
+            for (int j = 0; j < J; ++j) {
+                const double sigma = g.offsets[(static_cast<size_t>(b) * nd + dd) * J + j];
+                const double x0 = sigma * (-s) + t0 * c;
+                const double y0 = sigma * c + t0 * s;
+                const double u0 = (x0 + 1.0) / g.h - 0.5 + kHalo;
+                const double v0 = (y0 + 1.0) / g.h - 0.5 + kHalo;
+                RayP& rp = (*rays)[static_cast<size_t>(ab) * g.R + dd * J + j];
+                rp.U0 = std::llround(u0 * scale) + bias;
+                rp.V0 = std::llround(v0 * scale) + bias;
+                rp.dU = dU;
+                rp.dV = dV;
+                const size_t r = static_cast<size_t>(ab) * nd * J + dd * J + j;
+                rp.ilo = g.clip[2 * r];
+                rp.ihi = g.clip[2 * r + 1];
+            }
+    }
+}
+
+}  // namespace pget

@@ -1,0 +1,62 @@
+// kernels.cuh -- kernel argument blocks and declarations (library-private).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace pget {
+
+enum { MODE_FWD = 0, MODE_JVP = 1, MODE_VJP = 2, MODE_GN = 3 };
+enum { SC_INIT = 0, SC_GAMMA = 1, SC_ZETA = 2, SC_PRED = 3, SC_TRIAL = 4 };
+
+struct ProjArgs {
+    const RayP* rays;      // [n_ab][R]
+    const int8_t* abdir;   // [n_ab]
+    const float* w;        // [J] sub-ray weights (float)
+    const float2* img2;    // [B][Hp][Wp] (lam, mu)
+    const float4* img4;    // [B][Hp][Wp] (lam, mu, dlam, dmu)
+    float2* acc;           // [B][Hp][Wp] adjoint accumulators (g_lam, g_mu)
+    const float* win;      // [B][n_ab][n_det] VJP weights
+    float* y;              // [B][n_ab][n_det]
+    float* dy;             // [B][n_ab][n_det]
+    int Hp, Wp, n_det, J, R, R_pad, n_ab;
+    int RbA, RbB;          // band heights (j0 rows) of sweep A / sweep B
+    int rout_off, acc_off; // float offsets into dynamic shared memory
+    float delta;           // Delta
+    float cf, ch;          // -Delta log2(e), -Delta log2(e) / 2
+};
+
+struct CGState {
+    double zeta, a, bcg;
+    int stop, pad_;
+};
+
+template <int MODE, int MAXR>
+__global__ void proj_kernel(ProjArgs A);
+
+__global__ void pack2_kernel(const float* lam, const float* mu, const float* slam, const float* smu, float2* out,
+                             float* ut_lam, float* ut_mu, int N, int Hp, int Wp, int B);
+__global__ void pack4_kernel(const float* lam, const float* mu, const float* dl, const float* dm, float4* out,
+                             int N, int Hp, int Wp, int B);
+__global__ void finish_kernel(const float2* acc, const float* xl, const float* xm, float alpha, float beta,
+                              float sign, float* outl, float* outm, const float* dotl, const float* dotm,
+                              double* partial, float* copy1l, float* copy1m, float* copy2l, float* copy2m,
+                              float* zerol, float* zerom, int N, int Hp, int Wp);
+__global__ void residual_kernel(float* y, const float* ymeas, double* partial, int nper);
+__global__ void sumsq_kernel(const float* x, double* partial, int nper);
+__global__ void regsq_kernel(const float* xl, const float* xm, double* partial, int N);
+__global__ void dot2_kernel(const float* al, const float* am, const float* bl, const float* bm, double* partial,
+                            int n2);
+__global__ void cg_update1_kernel(float* sl, float* sm, float* zl, float* zm, const float* pl, const float* pm,
+                                  const float* ql, const float* qm, const CGState* st, double* partial, int n2);
+__global__ void cg_update2_kernel(const float* zl, const float* zm, float* pl, float* pm, const CGState* st,
+                                  int n2);
+__global__ void scalar_kernel(int op, int k, const double* p0, const double* p1, const double* p2, int nblk,
+                              CGState* st, pget_gn_stats* stats, int B, double alpha, double beta);
+
+}  // namespace pget
+
+namespace pget {
+cudaError_t launch_proj(int mode, int maxr, const ProjArgs& A, int grid, int block, size_t smem, cudaStream_t s);
+cudaError_t set_proj_smem_limit(size_t smem);
+}  // namespace pget

@@ -1,0 +1,95 @@
+"""CPU tests of the C-ABI library: it loads, exports every symbol include/pget.h
+declares, validates arguments, and its host geometry tables are bit-exact with
+the oracle's (pin P1).  No compute call runs here (no GPU)."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2604_26745_b200 as pg
+import pget_data as P
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "pget.h")).read()
+    return sorted(set(re.findall(r"\b(pget_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = pg.lib()
+    names = declared_functions()
+    assert len(names) >= 13
+    out = subprocess.run(["nm", "-D", "--defined-only", pg.LIB], capture_output=True, text=True).stdout
+    exported = set(l.split()[-1] for l in out.splitlines() if l.strip())
+    for n in names:
+        assert n in exported, n
+        assert hasattr(lib, n)
+
+
+def test_library_links_no_oracle():
+    out = subprocess.run(["ldd", pg.LIB], capture_output=True, text=True).stdout
+    assert "oracle" not in out
+    out = subprocess.run(["nm", "-D", pg.LIB], capture_output=True, text=True).stdout
+    assert "orc_" not in out
+
+
+def _same_bits(a, b):
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    return a.shape == b.shape and a.tobytes() == b.tobytes()
+
+
+GEOMS = [P.geometry_desc(c) for c in (1, 2, 3, 4, 5)] + [
+    dict(n_px=33, n_angles=12, n_banks=2, n_det=7, n_subrays=2, subray_sigma=0.4, step_px=0.5, bank1_shift=0.0,
+         batch=1),
+    dict(n_px=16, n_angles=7, n_banks=1, n_det=5, n_subrays=9, subray_sigma=0.3, step_px=0.37, bank1_shift=0.0,
+         batch=3),
+    dict(n_px=24, n_angles=10, n_banks=2, n_det=11, n_subrays=3, subray_sigma=0.4, step_px=0.5, bank1_shift=6.5,
+         batch=1),
+]
+
+
+@pytest.mark.parametrize("gd", GEOMS)
+def test_tables_bit_exact_with_oracle(gd):
+    g = pg.Geometry(gd, device=-1)
+    t = O.tables(gd)
+    assert _same_bits(g.export("angles"), t["angles"].ravel())
+    assert _same_bits(g.export("dirs"), t["dirs"].ravel())
+    assert _same_bits(g.export("offsets"), t["offsets"].ravel())
+    assert _same_bits(g.export("weights"), t["weights"].ravel())
+    assert _same_bits(g.export("tlat"), t["tlat"].ravel())
+    assert _same_bits(g.export("clip"), t["clip"].ravel())
+    assert g.info["n_t"] == t["n_t"]
+    cl = t["clip"]
+    assert g.info["n_samples_nominal"] == int(np.clip(cl[..., 1] - cl[..., 0] + 1, 0, None).sum()) * gd["batch"]
+
+
+def test_shifted_bank_has_empty_rays():
+    gd = GEOMS[-1]
+    cl = pg.Geometry(gd, device=-1).export("clip").reshape(10, 2, 11, 3, 2)
+    assert np.any(cl[..., 0] > cl[..., 1])
+
+
+def test_invalid_desc_rejected():
+    for bad in (dict(n_px=1), dict(n_det=1), dict(n_subrays=0), dict(n_subrays=65), dict(n_banks=3),
+                dict(step_px=0.0), dict(subray_sigma=-1.0), dict(batch=0), dict(step_px=float("nan"))):
+        gd = dict(GEOMS[0], **bad)
+        with pytest.raises(RuntimeError, match="INVALID_ARGUMENT"):
+            pg.Geometry(gd, device=-1)
+
+
+def test_compute_on_host_only_handle_fails_cleanly():
+    import ctypes as C
+    g = pg.Geometry(GEOMS[5], device=-1)
+    rc = pg.lib().pget_forward(g.handle, None, None, None, None, 0, None)
+    assert rc == 1
+    assert b"host-only" in pg.lib().pget_last_error_message()
+    assert pg.lib().pget_workspace_bytes(g.handle, 99) == 0
+    assert pg.lib().pget_table_bytes(g.handle, 42) == 0
+    for op in pg.OPS:
+        assert g.workspace_bytes(op) > 0

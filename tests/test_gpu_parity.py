@@ -1,0 +1,258 @@
+"""GPU-vs-oracle parity (SURVEY.md §8(c) acceptance; north star tolerances):
+forward, JVP and VJP within 1e-5 relative L2 and 1e-4 max-relative (floor
+1e-3 ||o||_inf, reading Q17) per sinogram / gradient image and batch member, on
+the five BASELINE configs (full size, in the launch configuration bench.py
+times) and on small ragged/edge geometries.  Inputs are seeded (pget_data);
+expected values come from the fp64 oracle only.  Every call goes through the
+C ABI (paper_2604_26745_b200 -> libpget.so)."""
+import numpy as np
+import pytest
+
+import oracle as O
+import pget_data as P
+from tests.metrics import max_rel, rel_l2
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL_L2, TOL_MAX = 1e-5, 1e-4
+
+
+@pytest.fixture(scope="module")
+def pg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2604_26745_b200 as m
+    return m
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+
+
+def host(t):
+    return t.detach().cpu().numpy().astype(np.float64)
+
+
+def assert_parity(x, o, what, tl2=TOL_L2, tmax=TOL_MAX):
+    x = np.asarray(x)
+    o = np.asarray(o)
+    for m in range(o.shape[0]):
+        e2, em = rel_l2(x[m], o[m]), max_rel(x[m], o[m])
+        assert e2 <= tl2 and em <= tmax, f"{what}[member {m}]: rel_l2={e2:.3e} max_rel={em:.3e}"
+
+
+def inputs(cid, members=None):
+    lam, mu = P.make_phantom(cid)
+    dl, dm = P.rod_directions(cid)
+    lp, mp = P.make_phantom_prime(cid)
+    return lam, mu, dl, dm, lp, mp
+
+
+# ----------------------------------------------------------------------------------- full configs
+@pytest.mark.parametrize("cid", [1, 2, 3, 4])
+def test_config_fwd_jvp_vjp(pg, cid):
+    gd = P.geometry_desc(cid)
+    lam, mu, dl, dm, lp, mp = inputs(cid)
+    g = pg.Geometry(gd)
+    y = host(pg.forward(g, dev(lam), dev(mu)))
+    y_o, dy_o = O.jvp(gd, lam, mu, dl, dm, with_y=True)
+    assert_parity(y, y_o, f"cfg{cid} forward")
+    yj, dy = pg.jvp(g, dev(lam), dev(mu), dev(dl), dev(dm), want_y=True)
+    assert_parity(host(yj), y_o, f"cfg{cid} jvp.y")
+    assert_parity(host(dy), dy_o, f"cfg{cid} jvp")
+    w = O.forward(gd, lp, mp) - y_o                          # residual-like weights (Q17)
+    gl, gm = pg.vjp(g, dev(lam), dev(mu), dev(w))
+    gl_o, gm_o = O.vjp(gd, lam, mu, w.astype(np.float32))
+    assert_parity(host(gl), gl_o, f"cfg{cid} vjp.lam")
+    assert_parity(host(gm), gm_o, f"cfg{cid} vjp.mu")
+
+
+def test_config5_batched_sampled_members(pg):
+    """Config 5: one batched launch of 64 members; the oracle checks sampled members one by one."""
+    cid = 5
+    gd = P.geometry_desc(cid)
+    lam, mu, dl, dm, lp, mp = inputs(cid)
+    g = pg.Geometry(gd)
+    y = host(pg.forward(g, dev(lam), dev(mu)))
+    _, dy = pg.jvp(g, dev(lam), dev(mu), dev(dl), dev(dm), want_y=True)
+    dy = host(dy)
+    g1 = dict(gd, batch=1)
+    sample = [0, 21, 42, 63]
+    w = np.zeros(g.sino_shape, np.float32)
+    for m in sample:
+        y_o, dy_o = O.jvp(g1, lam[m:m + 1], mu[m:m + 1], dl[m:m + 1], dm[m:m + 1], with_y=True)
+        assert_parity(y[m:m + 1], y_o, f"cfg5 forward m={m}")
+        assert_parity(dy[m:m + 1], dy_o, f"cfg5 jvp m={m}")
+        w[m] = (O.forward(g1, lp[m:m + 1], mp[m:m + 1]) - y_o)[0]
+    gl, gm = pg.vjp(g, dev(lam), dev(mu), dev(w))
+    gl, gm = host(gl), host(gm)
+    for m in sample:
+        gl_o, gm_o = O.vjp(g1, lam[m:m + 1], mu[m:m + 1], w[m:m + 1])
+        assert_parity(gl[m:m + 1], gl_o, f"cfg5 vjp.lam m={m}")
+        assert_parity(gm[m:m + 1], gm_o, f"cfg5 vjp.mu m={m}")
+    # members whose weights are zero get exactly zero gradients
+    assert np.all(gl[1] == 0) and np.all(gm[1] == 0)
+
+
+# ----------------------------------------------------------------------------------- edge geometries
+EDGE = [
+    dict(n_px=8, n_angles=4, n_banks=2, n_det=5, n_subrays=2, subray_sigma=0.4, step_px=0.5, bank1_shift=0.0, batch=1),
+    dict(n_px=16, n_angles=7, n_banks=1, n_det=5, n_subrays=9, subray_sigma=0.3, step_px=0.37, bank1_shift=0.0,
+         batch=3),
+    dict(n_px=33, n_angles=12, n_banks=2, n_det=7, n_subrays=2, subray_sigma=0.4, step_px=0.5, bank1_shift=0.0,
+         batch=2),
+    dict(n_px=24, n_angles=10, n_banks=2, n_det=11, n_subrays=3, subray_sigma=0.4, step_px=0.5, bank1_shift=6.5,
+         batch=1),
+    dict(n_px=40, n_angles=16, n_banks=2, n_det=91, n_subrays=13, subray_sigma=0.4, step_px=0.5, bank1_shift=0.0,
+         batch=1),   # 1183 rays per angle-bank: 2 rays per thread
+    dict(n_px=300, n_angles=6, n_banks=2, n_det=37, n_subrays=1, subray_sigma=0.4, step_px=1.0, bank1_shift=0.0,
+         batch=1),   # many bands
+]
+
+
+def rand_inputs(gd, seed):
+    rng = np.random.default_rng(seed)
+    shp = (gd["batch"], gd["n_px"], gd["n_px"])
+    lam = rng.uniform(0, 1.5, shp).astype(np.float32)
+    mu = rng.uniform(0, 0.6, shp).astype(np.float32)
+    dl = rng.uniform(-0.5, 0.5, shp).astype(np.float32)
+    dm = rng.uniform(-0.05, 0.05, shp).astype(np.float32)
+    return lam, mu, dl, dm
+
+
+@pytest.mark.parametrize("k", range(len(EDGE)))
+def test_edge_geometries(pg, k):
+    gd = EDGE[k]
+    lam, mu, dl, dm = rand_inputs(gd, 100 + k)
+    g = pg.Geometry(gd)
+    y_o, dy_o = O.jvp(gd, lam, mu, dl, dm, with_y=True)
+    assert_parity(host(pg.forward(g, dev(lam), dev(mu))), y_o, "edge forward")
+    yj, dy = pg.jvp(g, dev(lam), dev(mu), dev(dl), dev(dm), want_y=True)
+    assert_parity(host(dy), dy_o, "edge jvp", tmax=3e-4)
+    lp = lam * np.float32(1.1)
+    w = (O.forward(gd, lp, mu) - y_o).astype(np.float32)
+    gl, gm = pg.vjp(g, dev(lam), dev(mu), dev(w))
+    gl_o, gm_o = O.vjp(gd, lam, mu, w)
+    assert_parity(host(gl), gl_o, "edge vjp.lam")
+    assert_parity(host(gm), gm_o, "edge vjp.mu")
+
+
+def test_degenerate_inputs(pg):
+    gd = EDGE[2]
+    g = pg.Geometry(gd)
+    lam, mu, dl, dm = rand_inputs(gd, 5)
+    z = np.zeros_like(lam)
+    assert np.all(host(pg.forward(g, dev(z), dev(mu))) == 0)                     # lam = 0 -> y = 0
+    y0 = host(pg.forward(g, dev(lam), dev(z)))                                    # mu = 0 -> Radon
+    assert_parity(y0, O.forward(gd, lam, z), "radon")
+    dy = host(pg.jvp(g, dev(lam), dev(mu), dev(dl), dev(z)))                      # dmu = 0 -> F(dlam, mu)
+    assert_parity(dy, O.forward(gd, dl, mu), "jvp dmu=0")
+    gl, gm = pg.vjp(g, dev(lam), dev(mu), dev(np.zeros(g.sino_shape, np.float32)))
+    assert np.all(host(gl) == 0) and np.all(host(gm) == 0)                       # w = 0 -> 0
+
+
+def test_adjoint_identity_gpu(pg):
+    gd = P.geometry_desc(2)
+    g = pg.Geometry(gd)
+    lam, mu = P.make_phantom(2)
+    wl, wm = P.white_directions(lam.shape, 11)
+    w = P.white_weights(g.sino_shape, 12)
+    jv = host(pg.jvp(g, dev(lam), dev(mu), dev(wl), dev(wm)))
+    gl, gm = pg.vjp(g, dev(lam), dev(mu), dev(w))
+    lhs = float(np.sum(jv * w))
+    rhs = float(np.sum(wl * host(gl)) + np.sum(wm * host(gm)))
+    assert abs(lhs - rhs) <= 1e-5 * np.linalg.norm(jv) * np.linalg.norm(w)
+
+
+def test_white_noise_rel_l2(pg):
+    """White-noise directions and N(0,1) weights: rel-L2 only (Q17)."""
+    gd = P.geometry_desc(2)
+    g = pg.Geometry(gd)
+    lam, mu = P.make_phantom(2)
+    wl, wm = P.white_directions(lam.shape, 21)
+    w = P.white_weights(g.sino_shape, 22)
+    dy = host(pg.jvp(g, dev(lam), dev(mu), dev(wl), dev(wm)))
+    assert rel_l2(dy, O.jvp(gd, lam, mu, wl, wm)) <= TOL_L2
+    gl, gm = pg.vjp(g, dev(lam), dev(mu), dev(w))
+    gl_o, gm_o = O.vjp(gd, lam, mu, w)
+    assert rel_l2(host(gl), gl_o) <= TOL_L2 and rel_l2(host(gm), gm_o) <= TOL_L2
+
+
+# ----------------------------------------------------------------------------------- GN operator / LM step
+@pytest.mark.parametrize("cid", [2, 3])
+def test_gn_apply_operator(pg, cid):
+    gd = P.geometry_desc(cid)
+    cfg = P.CONFIGS[cid]
+    g = pg.Geometry(gd)
+    lam, mu = P.initial_guess(gd["n_px"])
+    pl, pm = P.rod_directions(cid)
+    ql, qm = pg.gn_apply(g, dev(lam), dev(mu), dev(pl), dev(pm), cfg.alpha, 0.25)
+    ql_o, qm_o = O.apply_H(gd, lam, mu, cfg.alpha, 0.25, pl, pm)
+    x = np.concatenate([host(ql).ravel(), host(qm).ravel()])
+    o = np.concatenate([ql_o.ravel(), qm_o.ravel()])
+    assert rel_l2(x, o) <= TOL_L2
+
+
+def test_lm_iteration_cfg2(pg):
+    """One LM iteration (20 CG steps, alpha = 1e-3, beta = 0) on config 2 vs the oracle:
+    s rel-L2 <= 1e-3, f, pred and f(u+s) <= 1e-4 rel, same accept decision
+    (proposed LM-step parity)."""
+    cid = 2
+    cfg = P.CONFIGS[cid]
+    gd = P.geometry_desc(cid)
+    g = pg.Geometry(gd)
+    lt, mt = P.make_phantom(cid)
+    y = P.poisson_noise(O.forward(gd, lt, mt), cfg.noise_peak, cfg.seed)
+    l0, m0 = P.initial_guess(gd["n_px"])
+    sl, sm, st = pg.gn_cg_step(g, dev(l0), dev(m0), dev(y), cfg.alpha, 0.0, cfg.n_cg)
+    torch.cuda.synchronize()
+    S = pg.read_stats(st, 1, cfg.n_cg)[0]
+    sl_o, sm_o, So = O.gn_cg_step(gd, l0, m0, y, cfg.alpha, 0.0, cfg.n_cg)
+    s = np.concatenate([host(sl).ravel(), host(sm).ravel()])
+    so = np.concatenate([sl_o.ravel(), sm_o.ravel()])
+    assert rel_l2(s, so) <= 1e-3
+    for k in ("f", "misfit", "reg", "grad_norm"):
+        assert abs(S[k] - So[k]) <= 1e-5 * abs(So[k]), k
+    for k in ("pred", "f_trial"):
+        assert abs(S[k] - So[k]) <= 1e-4 * abs(So[k]), k
+    assert S["accepted"] == So["accepted"]
+    assert S["n_cg_done"] == So["n_cg_done"] == cfg.n_cg
+    assert abs(S["cg_res"][1] - So["cg_res"][1]) <= 1e-4 * So["cg_res"][1]
+
+
+def test_lm_iteration_small_batched(pg):
+    gd = dict(n_px=24, n_angles=16, n_banks=2, n_det=21, n_subrays=3, subray_sigma=0.4, step_px=0.5,
+              bank1_shift=0.0, batch=3)
+    g = pg.Geometry(gd)
+    lam, mu, _, _ = rand_inputs(gd, 7)
+    y = O.forward(gd, lam * 1.2, mu * 0.9).astype(np.float32)
+    sl, sm, st = pg.gn_cg_step(g, dev(lam), dev(mu), dev(y), 1e-3, 0.1, 8)
+    torch.cuda.synchronize()
+    S = pg.read_stats(st, 3, 8)
+    g1 = dict(gd, batch=1)
+    for m in range(3):
+        sl_o, sm_o, So = O.gn_cg_step(g1, lam[m:m + 1], mu[m:m + 1], y[m:m + 1], 1e-3, 0.1, 8)
+        s = np.concatenate([host(sl)[m].ravel(), host(sm)[m].ravel()])
+        assert rel_l2(s, np.concatenate([sl_o.ravel(), sm_o.ravel()])) <= 1e-3
+        assert abs(S[m]["pred"] - So["pred"]) <= 1e-4 * abs(So["pred"])
+        assert S[m]["accepted"] == So["accepted"]
+
+
+# ----------------------------------------------------------------------------------- errors
+def test_errors_fail_loudly(pg):
+    gd = EDGE[0]
+    g = pg.Geometry(gd)
+    lam, mu, _, _ = rand_inputs(gd, 1)
+    L, M = dev(lam), dev(mu)
+    y = torch.empty(g.sino_shape, device="cuda")
+    ws = g.workspace("forward")
+    import ctypes as C
+    rc = pg.lib().pget_forward(g.handle, C.c_void_p(L.data_ptr() + 4), C.c_void_p(M.data_ptr()),
+                               C.c_void_p(y.data_ptr()), C.c_void_p(ws.data_ptr()), ws.numel(), None)
+    assert rc == 3          # PGET_ERR_ALIGNMENT
+    rc = pg.lib().pget_forward(g.handle, C.c_void_p(L.data_ptr()), C.c_void_p(M.data_ptr()),
+                               C.c_void_p(y.data_ptr()), C.c_void_p(ws.data_ptr()), 16, None)
+    assert rc == 4          # PGET_ERR_WORKSPACE
+    with pytest.raises(RuntimeError, match="INVALID_ARGUMENT"):
+        pg.gn_cg_step(g, L, M, dev(np.zeros(g.sino_shape)), 1e-3, 0.0, 10 ** 6)
