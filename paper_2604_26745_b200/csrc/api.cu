@@ -69,58 +69,93 @@ constexpr int kVecThreads = 256;
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct ProjCfg {
-    int T, maxr, RbA, RbB;
+    int maxg, passesA, passesB, RbA, RbB, nbA, nbB, grid, KS;
     size_t smem;
-    int rout_off, acc_off;
+    int stage_bytes, off_wacc, off_rout, off_gsh;
 };
 
-// Launch configuration of the projector for `mode`.
+size_t align128(size_t x) { return (x + 127) & ~size_t(127); }
+
+// Launch configuration of the projector for `mode`: warps and CTAs per SM
+// are fixed per mode; the band height is the largest (<= 32 rows) whose double-buffered stage, the
+// warp rings (adjoint modes) and the per-ray arrays fit the per-CTA shared-memory budget.
 ProjCfg proj_cfg(const Geometry& g, int mode)
 {
     ProjCfg c;
-    int maxr = 1;
-    while ((g.R_pad + maxr - 1) / maxr > 1024) maxr *= 2;
-    c.maxr = maxr;
-    c.T = ((g.R_pad + maxr - 1) / maxr + 31) / 32 * 32;
-    const int ctas = std::max(1, std::min(4, 1536 / c.T));
-    const size_t limit = std::min<size_t>(g.smem_optin, 227 * 1024);
-    const size_t rout_bytes = 2 * sizeof(float) * g.R_pad;
-    long budget = static_cast<long>(limit / ctas) - 1024 - static_cast<long>(rout_bytes);
-    const int nfA = (mode == MODE_FWD || mode == MODE_VJP) ? 2 : 4;
-    auto rows = [&](int bytes_per_px) {
-        long r = budget / (static_cast<long>(g.Wp) * bytes_per_px) - 1;
-        return static_cast<int>(std::max<long>(1, std::min<long>(r, g.Hp - 1)));
-    };
-    c.RbA = rows(4 * nfA);
-    c.RbB = (mode == MODE_VJP || mode == MODE_GN) ? rows(16) : 1;
-    size_t regA = static_cast<size_t>(c.RbA + 1) * g.Wp * 4 * nfA;
-    size_t regB = (mode == MODE_VJP || mode == MODE_GN) ? static_cast<size_t>(c.RbB + 1) * g.Wp * 16 : 0;
-    size_t region = std::max(regA, regB);
-    region = (region + 15) & ~size_t(15);
-    c.rout_off = static_cast<int>(region / sizeof(float));
-    c.acc_off = static_cast<int>(static_cast<size_t>(c.RbB + 1) * g.Wp * 2);
-    c.smem = region + rout_bytes;
+    const int W = proj_warps(mode), cps = proj_ctas_per_sm(mode);
+    const bool hasB = mode == MODE_VJP || mode == MODE_GN;
+    const bool nf4 = mode == MODE_JVP || mode == MODE_GN;
+    const int ncgA = (g.R + 31) / 32;                 // sweep A: contiguous groups of 32 rays
+    const int gpw = std::max((ncgA + W - 1) / W, hasB ? (g.n_groups + W - 1) / W : 0);
+    c.maxg = gpw <= 1 ? 1 : (gpw <= 2 ? 2 : 4);
+    c.passesA = std::max(1, (ncgA + W * c.maxg - 1) / (W * c.maxg));
+    c.passesB = std::max(1, (g.n_groups + W * c.maxg - 1) / (W * c.maxg));
+    const size_t per_sm = 233472;   // 228 KB of shared memory per SM
+    const size_t budget = std::min<size_t>(g.smem_optin, per_sm / cps - 1024);
+    const size_t rout_b = align128(2 * sizeof(float) * g.R), gsh_b = align128(sizeof(float2) * g.R);
+    const size_t fixed = 128 + rout_b + gsh_b;
+    const size_t pixA = nf4 ? 16 : 8;
+    int Rb = std::min(32, g.P - 1);
+    size_t SB = 0, total = 0;
+    for (; Rb >= 1; --Rb) {
+        SB = align128(std::max<size_t>(static_cast<size_t>(Rb + 1) * g.P * pixA,
+                                       hasB ? static_cast<size_t>(Rb + 1) * g.P * 8 : 0));
+        total = fixed + 2 * SB + (hasB ? align128(static_cast<size_t>(W) * (Rb + 1) * g.P * 8) : 0);
+        if (total <= budget) break;
+    }
+    if (Rb < 1) Rb = 1;
+    c.RbA = c.RbB = Rb;
+    c.nbA = c.nbB = (g.P - 1 + Rb - 1) / Rb;
+    c.stage_bytes = static_cast<int>(SB);
+    c.off_wacc = static_cast<int>(128 + 2 * SB);
+    const size_t wacc_b = hasB ? align128(static_cast<size_t>(W) * (Rb + 1) * g.P * 8) : 0;
+    c.off_rout = static_cast<int>(c.off_wacc + wacc_b);
+    c.off_gsh = static_cast<int>(c.off_rout + rout_b);
+    c.smem = c.off_gsh + gsh_b;
+    c.grid = g.sm_count * cps;
+    // KS: the most partial-slot chunks (chunk_of) one CTA's task range spans
+    const int64_t T = static_cast<int64_t>(g.desc.batch) * g.n_ab;
+    c.KS = 1;
+    for (int k = 0; k < c.grid; ++k) {
+        const int64_t tb = static_cast<int64_t>(k) * T / c.grid, te = static_cast<int64_t>(k + 1) * T / c.grid;
+        if (te > tb)
+            c.KS = std::max<int>(c.KS, static_cast<int>(chunk_of(te - 1, g.n_ab, g.n_class0) -
+                                                        chunk_of(tb, g.n_ab, g.n_class0) + 1));
+    }
     return c;
 }
+
+int slot_pitch(const Geometry& g) { return (g.desc.n_px + 1) & ~1; }
 
 ProjArgs base_args(const Geometry& g, const ProjCfg& c)
 {
     ProjArgs A;
     std::memset(&A, 0, sizeof A);
     A.rays = g.d_rays;
-    A.abdir = g.d_abdir;
+    A.groups = g.d_groups;
+    A.task_ab = g.d_task_ab;
     A.w = g.d_w;
-    A.Hp = g.Hp;
-    A.Wp = g.Wp;
+    A.N = g.desc.n_px;
+    A.Ns = slot_pitch(g);
+    A.P = g.P;
     A.n_det = g.desc.n_det;
     A.J = g.desc.n_subrays;
     A.R = g.R;
-    A.R_pad = g.R_pad;
     A.n_ab = g.n_ab;
+    A.n_class0 = g.n_class0;
+    A.B = g.desc.batch;
+    A.n_groups = g.n_groups;
+    A.KS = c.KS;
     A.RbA = c.RbA;
     A.RbB = c.RbB;
-    A.rout_off = c.rout_off;
-    A.acc_off = c.acc_off;
+    A.nbA = c.nbA;
+    A.nbB = c.nbB;
+    A.passesA = c.passesA;
+    A.passesB = c.passesB;
+    A.stage_bytes = c.stage_bytes;
+    A.off_wacc = c.off_wacc;
+    A.off_rout = c.off_rout;
+    A.off_gsh = c.off_gsh;
     A.delta = static_cast<float>(g.delta);
     const double cf = -g.delta * 1.4426950408889634;   // -Delta log2(e)
     A.cf = static_cast<float>(cf);
@@ -128,14 +163,8 @@ ProjArgs base_args(const Geometry& g, const ProjCfg& c)
     return A;
 }
 
-pget_status run_proj(const Geometry& g, int mode, ProjArgs A, cudaStream_t s)
+pget_status run_proj(const Geometry& g, int mode, const ProjCfg& c, const ProjArgs& A, cudaStream_t s)
 {
-    const ProjCfg c = proj_cfg(g, mode);
-    A.RbA = c.RbA;
-    A.RbB = c.RbB;
-    A.rout_off = c.rout_off;
-    A.acc_off = c.acc_off;
-    const int grid = g.desc.batch * g.n_ab;
     cudaEvent_t ea = nullptr, eb = nullptr;
     if (g_prof.on.load(std::memory_order_relaxed)) {
         std::lock_guard<std::mutex> lk(g_prof.mu);
@@ -148,7 +177,7 @@ pget_status run_proj(const Geometry& g, int mode, ProjArgs A, cudaStream_t s)
         }
     }
     if (ea) cudaEventRecord(ea, s);
-    cudaError_t e = launch_proj(mode, c.maxr, A, grid, c.T, c.smem, s);
+    cudaError_t e = launch_proj(mode, c.maxg, A, c.grid, c.smem, s);
     if (eb) cudaEventRecord(eb, s);
     if (e != cudaSuccess) return cuda_fail(e, "projector launch");
     return PGET_OK;
@@ -156,9 +185,10 @@ pget_status run_proj(const Geometry& g, int mode, ProjArgs A, cudaStream_t s)
 
 // ---- workspace carving
 struct WS {
-    float2* img2 = nullptr;
-    float4* img4 = nullptr;
-    float2* acc = nullptr;
+    float2* img2[2] = {nullptr, nullptr};
+    float4* img4[2] = {nullptr, nullptr};
+    float2* slots = nullptr;
+    float2* gacc = nullptr;   // [B][N][N] reduced (g_lam, g_mu)
     float *ysino = nullptr, *dysino = nullptr;
     float *bl = nullptr, *bm = nullptr, *zl = nullptr, *zm = nullptr, *pl = nullptr, *pm = nullptr;
     float *ql = nullptr, *qm = nullptr, *ul = nullptr, *um = nullptr;
@@ -172,7 +202,7 @@ WS carve(const Geometry& g, int op, char* base)
     WS w;
     size_t off = 0;
     const size_t B = g.desc.batch;
-    const size_t img = B * g.Hp * g.Wp;
+    const size_t img = B * g.P * g.P;
     const size_t n2 = B * g.desc.n_px * g.desc.n_px;
     const size_t ns = B * g.n_ab * g.desc.n_det;
     auto take = [&](size_t bytes) -> char* {
@@ -183,9 +213,16 @@ WS carve(const Geometry& g, int op, char* base)
     const bool need2 = op == PGET_OP_FORWARD || op == PGET_OP_VJP || op == PGET_OP_GN_APPLY || op == PGET_OP_GN_CG_STEP;
     const bool need4 = op == PGET_OP_JVP || op == PGET_OP_GN_APPLY || op == PGET_OP_GN_CG_STEP;
     const bool needacc = op == PGET_OP_VJP || op == PGET_OP_GN_APPLY || op == PGET_OP_GN_CG_STEP;
-    if (need2) w.img2 = reinterpret_cast<float2*>(take(img * sizeof(float2)));
-    if (need4) w.img4 = reinterpret_cast<float4*>(take(img * sizeof(float4)));
-    if (needacc) w.acc = reinterpret_cast<float2*>(take(img * sizeof(float2)));
+    for (int k = 0; k < 2; ++k) {
+        if (need2) w.img2[k] = reinterpret_cast<float2*>(take(img * sizeof(float2)));
+        if (need4) w.img4[k] = reinterpret_cast<float4*>(take(img * sizeof(float4)));
+    }
+    if (needacc) {
+        const ProjCfg c = proj_cfg(g, MODE_VJP);   // VJP and GN share the grid and KS
+        const size_t plane = static_cast<size_t>(g.desc.n_px) * slot_pitch(g);
+        w.slots = reinterpret_cast<float2*>(take(static_cast<size_t>(c.grid) * c.KS * plane * sizeof(float2)));
+        w.gacc = reinterpret_cast<float2*>(take(n2 * sizeof(float2)));
+    }
     if (op == PGET_OP_GN_CG_STEP) {
         w.ysino = reinterpret_cast<float*>(take(ns * sizeof(float)));
         w.dysino = reinterpret_cast<float*>(take(ns * sizeof(float)));
@@ -276,21 +313,25 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     if (e == cudaSuccess) g.smem_optin = static_cast<size_t>(optin);
     std::vector<RayP> rays;
-    std::vector<int8_t> abdir;
-    build_ray_params(g, &rays, &abdir);
+    build_ray_params(g, &rays);
     if (e == cudaSuccess) e = cudaMalloc(&g.d_rays, rays.size() * sizeof(RayP));
-    if (e == cudaSuccess) e = cudaMalloc(&g.d_abdir, abdir.size());
+    if (e == cudaSuccess) e = cudaMalloc(&g.d_groups, g.groups.size() * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&g.d_task_ab, g.task_ab.size() * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMalloc(&g.d_w, g.wf.size() * sizeof(float));
     if (e == cudaSuccess) e = cudaMemcpy(g.d_rays, rays.data(), rays.size() * sizeof(RayP), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(g.d_abdir, abdir.data(), abdir.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(g.d_groups, g.groups.data(), g.groups.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(g.d_task_ab, g.task_ab.data(), g.task_ab.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(g.d_w, g.wf.data(), g.wf.size() * sizeof(float), cudaMemcpyHostToDevice);
-    size_t smax = 0;
-    for (int mode = 0; mode < 4; ++mode) smax = std::max(smax, proj_cfg(g, mode).smem);
-    if (e == cudaSuccess && smax > g.smem_optin) e = cudaErrorInvalidConfiguration;
-    if (e == cudaSuccess) e = set_proj_smem_limit(smax);
+    for (int mode = 0; mode < 4 && e == cudaSuccess; ++mode) {
+        const size_t sm = proj_cfg(g, mode).smem;
+        if (sm > g.smem_optin) e = cudaErrorInvalidConfiguration;
+        else e = set_proj_smem_limit(mode, sm);
+    }
     if (prev >= 0) cudaSetDevice(prev);
     if (e != cudaSuccess) {
-        cudaFree(g.d_rays); cudaFree(g.d_abdir); cudaFree(g.d_w);
+        cudaFree(g.d_rays); cudaFree(g.d_groups); cudaFree(g.d_task_ab); cudaFree(g.d_w);
         delete h;
         return cuda_fail(e, "pget_geometry_create");
     }
@@ -306,7 +347,8 @@ pget_status pget_geometry_destroy(pget_geometry h)
     cudaGetDevice(&prev);
     cudaSetDevice(h->g.device);
     cudaFree(h->g.d_rays);
-    cudaFree(h->g.d_abdir);
+    cudaFree(h->g.d_groups);
+    cudaFree(h->g.d_task_ab);
     cudaFree(h->g.d_w);
     if (prev >= 0) cudaSetDevice(prev);
     delete h;
@@ -377,6 +419,56 @@ size_t pget_workspace_bytes(pget_geometry h, int op)
     return carve(h->g, op, nullptr).bytes + 256;
 }
 
+// ---- building blocks (all enqueued on s)
+static pget_status pack2(const Geometry& g, const WS& w, const float* lam, const float* mu, const float* slam,
+                         const float* smu, float* ul, float* um, cudaStream_t s)
+{
+    const size_t img = static_cast<size_t>(g.desc.batch) * g.P * g.P;
+    pack2_kernel<<<vec_grid(img), kVecThreads, 0, s>>>(lam, mu, slam, smu, w.img2[0], w.img2[1], ul, um,
+                                                      g.desc.n_px, g.P, g.desc.batch); note();
+    CK(cudaGetLastError());
+    return PGET_OK;
+}
+
+static pget_status pack4(const Geometry& g, const WS& w, const float* lam, const float* mu, const float* dl,
+                         const float* dm, cudaStream_t s)
+{
+    const size_t img = static_cast<size_t>(g.desc.batch) * g.P * g.P;
+    pack4_kernel<<<vec_grid(img), kVecThreads, 0, s>>>(lam, mu, dl, dm, w.img4[0], w.img4[1], g.desc.n_px, g.P,
+                                                      g.desc.batch); note();
+    CK(cudaGetLastError());
+    return PGET_OK;
+}
+
+// y (and dy) from the packed images (MODE_FWD / MODE_JVP)
+static pget_status proj_out(const Geometry& g, const WS& w, int mode, float* y, float* dy, cudaStream_t s)
+{
+    const ProjCfg c = proj_cfg(g, mode);
+    ProjArgs A = base_args(g, c);
+    for (int k = 0; k < 2; ++k) { A.img2[k] = w.img2[k]; A.img4[k] = w.img4[k]; }
+    A.y = y;
+    A.dy = dy;
+    return run_proj(g, mode, c, A, s);
+}
+
+// adjoint projector into w.gacc (MODE_VJP with weights win, or MODE_GN), then the fixed-order reduction
+static pget_status proj_adjoint(const Geometry& g, const WS& w, int mode, const float* win, cudaStream_t s)
+{
+    const ProjCfg c = proj_cfg(g, mode);
+    ProjArgs A = base_args(g, c);
+    for (int k = 0; k < 2; ++k) { A.img2[k] = w.img2[k]; A.img4[k] = w.img4[k]; }
+    A.slots = w.slots;
+    A.win = win;
+    pget_status st = run_proj(g, mode, c, A, s);
+    if (st) return st;
+    const int N = g.desc.n_px;
+    const dim3 grid((N + 31) / 32, (N + 31) / 32, g.desc.batch);
+    reduce_slots_kernel<<<grid, dim3(32, 8), 0, s>>>(w.slots, w.gacc, N, slot_pitch(g), g.n_ab, g.n_class0,
+                                                    g.desc.batch, c.grid, c.KS, 0); note();
+    CK(cudaGetLastError());
+    return PGET_OK;
+}
+
 pget_status pget_forward(pget_geometry h, const float* lam, const float* mu, float* y, void* ws, size_t ws_bytes,
                          pget_stream_t stream)
 {
@@ -386,14 +478,8 @@ pget_status pget_forward(pget_geometry h, const float* lam, const float* mu, flo
     if ((st = check_ptrs({lam, mu, y}, "pget_forward"))) return st;
     const Geometry& g = h->g;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    const size_t img = static_cast<size_t>(g.desc.batch) * g.Hp * g.Wp;
-    pack2_kernel<<<vec_grid(img), kVecThreads, 0, s>>>(lam, mu, nullptr, nullptr, w.img2, nullptr, nullptr,
-                                                      g.desc.n_px, g.Hp, g.Wp, g.desc.batch); note();
-    CK(cudaGetLastError());
-    ProjArgs A = base_args(g, proj_cfg(g, MODE_FWD));
-    A.img2 = w.img2;
-    A.y = y;
-    return run_proj(g, MODE_FWD, A, s);
+    if ((st = pack2(g, w, lam, mu, nullptr, nullptr, nullptr, nullptr, s))) return st;
+    return proj_out(g, w, MODE_FWD, y, nullptr, s);
 }
 
 pget_status pget_jvp(pget_geometry h, const float* lam, const float* mu, const float* dlam, const float* dmu,
@@ -406,26 +492,8 @@ pget_status pget_jvp(pget_geometry h, const float* lam, const float* mu, const f
     if (y && !aligned16(y)) return fail(PGET_ERR_ALIGNMENT, "pget_jvp: y not 16-byte aligned");
     const Geometry& g = h->g;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    const size_t img = static_cast<size_t>(g.desc.batch) * g.Hp * g.Wp;
-    pack4_kernel<<<vec_grid(img), kVecThreads, 0, s>>>(lam, mu, dlam, dmu, w.img4, g.desc.n_px, g.Hp, g.Wp,
-                                                      g.desc.batch); note();
-    CK(cudaGetLastError());
-    ProjArgs A = base_args(g, proj_cfg(g, MODE_JVP));
-    A.img4 = w.img4;
-    A.y = y;
-    A.dy = dy;
-    return run_proj(g, MODE_JVP, A, s);
-}
-
-static pget_status vjp_core(const Geometry& g, const WS& w, const float* w_in, cudaStream_t s)
-{
-    const size_t img = static_cast<size_t>(g.desc.batch) * g.Hp * g.Wp;
-    CK(cudaMemsetAsync(w.acc, 0, img * sizeof(float2), s));
-    ProjArgs A = base_args(g, proj_cfg(g, MODE_VJP));
-    A.img2 = w.img2;
-    A.acc = w.acc;
-    A.win = w_in;
-    return run_proj(g, MODE_VJP, A, s);
+    if ((st = pack4(g, w, lam, mu, dlam, dmu, s))) return st;
+    return proj_out(g, w, MODE_JVP, y, dy, s);
 }
 
 pget_status pget_vjp(pget_geometry h, const float* lam, const float* mu, const float* wv, float* g_lam, float* g_mu,
@@ -438,31 +506,13 @@ pget_status pget_vjp(pget_geometry h, const float* lam, const float* mu, const f
     const Geometry& g = h->g;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int N = g.desc.n_px, B = g.desc.batch;
-    const size_t img = static_cast<size_t>(B) * g.Hp * g.Wp;
-    pack2_kernel<<<vec_grid(img), kVecThreads, 0, s>>>(lam, mu, nullptr, nullptr, w.img2, nullptr, nullptr, N,
-                                                      g.Hp, g.Wp, B); note();
-    CK(cudaGetLastError());
-    if ((st = vjp_core(g, w, wv, s))) return st;
+    if ((st = pack2(g, w, lam, mu, nullptr, nullptr, nullptr, nullptr, s))) return st;
+    if ((st = proj_adjoint(g, w, MODE_VJP, wv, s))) return st;
     finish_kernel<<<dim3(vec_grid(static_cast<size_t>(N) * N), B), kVecThreads, 0, s>>>(
-        w.acc, nullptr, nullptr, 0.f, 0.f, 1.f, g_lam, g_mu, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-        nullptr, nullptr, nullptr, N, g.Hp, g.Wp); note();
+        w.gacc, nullptr, nullptr, 0.f, 0.f, 1.f, g_lam, g_mu, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+        nullptr, nullptr, nullptr, N); note();
     CK(cudaGetLastError());
     return PGET_OK;
-}
-
-static pget_status gn_core(const Geometry& g, const WS& w, const float* lam, const float* mu, const float* pl,
-                           const float* pm, cudaStream_t s)
-{
-    const int N = g.desc.n_px, B = g.desc.batch;
-    const size_t img = static_cast<size_t>(B) * g.Hp * g.Wp;
-    pack4_kernel<<<vec_grid(img), kVecThreads, 0, s>>>(lam, mu, pl, pm, w.img4, N, g.Hp, g.Wp, B); note();
-    CK(cudaGetLastError());
-    CK(cudaMemsetAsync(w.acc, 0, img * sizeof(float2), s));
-    ProjArgs A = base_args(g, proj_cfg(g, MODE_GN));
-    A.img2 = w.img2;
-    A.img4 = w.img4;
-    A.acc = w.acc;
-    return run_proj(g, MODE_GN, A, s);
 }
 
 pget_status pget_gn_apply(pget_geometry h, const float* lam, const float* mu, const float* p_lam, const float* p_mu,
@@ -478,14 +528,12 @@ pget_status pget_gn_apply(pget_geometry h, const float* lam, const float* mu, co
     const Geometry& g = h->g;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int N = g.desc.n_px, B = g.desc.batch;
-    const size_t img = static_cast<size_t>(B) * g.Hp * g.Wp;
-    pack2_kernel<<<vec_grid(img), kVecThreads, 0, s>>>(lam, mu, nullptr, nullptr, w.img2, nullptr, nullptr, N,
-                                                      g.Hp, g.Wp, B); note();
-    CK(cudaGetLastError());
-    if ((st = gn_core(g, w, lam, mu, p_lam, p_mu, s))) return st;
+    if ((st = pack2(g, w, lam, mu, nullptr, nullptr, nullptr, nullptr, s))) return st;
+    if ((st = pack4(g, w, lam, mu, p_lam, p_mu, s))) return st;
+    if ((st = proj_adjoint(g, w, MODE_GN, nullptr, s))) return st;
     finish_kernel<<<dim3(vec_grid(static_cast<size_t>(N) * N), B), kVecThreads, 0, s>>>(
-        w.acc, p_lam, p_mu, alpha, beta, 1.f, q_lam, q_mu, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-        nullptr, nullptr, nullptr, N, g.Hp, g.Wp); note();
+        w.gacc, p_lam, p_mu, alpha, beta, 1.f, q_lam, q_mu, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+        nullptr, nullptr, nullptr, N); note();
     CK(cudaGetLastError());
     return PGET_OK;
 }
@@ -506,37 +554,30 @@ pget_status pget_gn_cg_step(pget_geometry h, const float* lam, const float* mu, 
     const int N = g.desc.n_px, B = g.desc.batch;
     const int n2 = N * N;
     const int nsper = g.n_ab * g.desc.n_det;
-    const size_t img = static_cast<size_t>(B) * g.Hp * g.Wp;
     const dim3 vg(kNblk, B);
     double* P[8];
     for (int k = 0; k < 8; ++k) P[k] = w.part + static_cast<size_t>(k) * B * kNblk;
     const int sgrid = (B + 127) / 128;
 
-    // 1-2: r = F(u) - y, 1/2||r||^2, ||Lu||^2
-    pack2_kernel<<<vec_grid(img), kVecThreads, 0, s>>>(lam, mu, nullptr, nullptr, w.img2, nullptr, nullptr, N,
-                                                      g.Hp, g.Wp, B); note();
-    CK(cudaGetLastError());
-    {
-        ProjArgs A = base_args(g, proj_cfg(g, MODE_FWD));
-        A.img2 = w.img2;
-        A.y = w.ysino;
-        if ((st = run_proj(g, MODE_FWD, A, s))) return st;
-    }
+    // 1-2: r = F(u) - y, 1/2||r||^2, ||Lu||^2   (u packed once for the whole iteration)
+    if ((st = pack2(g, w, lam, mu, nullptr, nullptr, nullptr, nullptr, s))) return st;
+    if ((st = proj_out(g, w, MODE_FWD, w.ysino, nullptr, s))) return st;
     residual_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, y_meas, P[0], nsper); note();
     regsq_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, P[1], N); note();
     CK(cudaGetLastError());
     // 3: b = -(J^T r + alpha L^T L u); z = p = b; s = 0; ||b||^2
-    if ((st = vjp_core(g, w, w.ysino, s))) return st;
-    finish_kernel<<<vg, kVecThreads, 0, s>>>(w.acc, lam, mu, alpha, 0.f, -1.f, w.bl, w.bm, w.bl, w.bm, P[2], w.zl,
-                                            w.zm, w.pl, w.pm, s_lam, s_mu, N, g.Hp, g.Wp); note();
+    if ((st = proj_adjoint(g, w, MODE_VJP, w.ysino, s))) return st;
+    finish_kernel<<<vg, kVecThreads, 0, s>>>(w.gacc, lam, mu, alpha, 0.f, -1.f, w.bl, w.bm, w.bl, w.bm, P[2], w.zl,
+                                            w.zm, w.pl, w.pm, s_lam, s_mu, N); note();
     CK(cudaGetLastError());
     scalar_kernel<<<sgrid, 128, 0, s>>>(SC_INIT, 0, P[0], P[1], P[2], kNblk, w.cg, stats, B, alpha, beta); note();
     CK(cudaGetLastError());
     // 5: CG
     for (int k = 0; k < n_cg; ++k) {
-        if ((st = gn_core(g, w, lam, mu, w.pl, w.pm, s))) return st;
-        finish_kernel<<<vg, kVecThreads, 0, s>>>(w.acc, w.pl, w.pm, alpha, beta, 1.f, w.ql, w.qm, w.pl, w.pm, P[3],
-                                                nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, N, g.Hp, g.Wp); note();
+        if ((st = pack4(g, w, lam, mu, w.pl, w.pm, s))) return st;
+        if ((st = proj_adjoint(g, w, MODE_GN, nullptr, s))) return st;
+        finish_kernel<<<vg, kVecThreads, 0, s>>>(w.gacc, w.pl, w.pm, alpha, beta, 1.f, w.ql, w.qm, w.pl, w.pm, P[3],
+                                                nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, N); note();
         scalar_kernel<<<sgrid, 128, 0, s>>>(SC_GAMMA, k, P[3], nullptr, nullptr, kNblk, w.cg, stats, B, alpha, beta); note();
         cg_update1_kernel<<<vg, kVecThreads, 0, s>>>(s_lam, s_mu, w.zl, w.zm, w.pl, w.pm, w.ql, w.qm, w.cg, P[4], n2); note();
         scalar_kernel<<<sgrid, 128, 0, s>>>(SC_ZETA, k, P[4], nullptr, nullptr, kNblk, w.cg, stats, B, alpha, beta); note();
@@ -544,15 +585,8 @@ pget_status pget_gn_cg_step(pget_geometry h, const float* lam, const float* mu, 
         CK(cudaGetLastError());
     }
     // 6: pred = <b,s> - 1/2(||Js||^2 + alpha ||Ls||^2)
-    pack4_kernel<<<vec_grid(img), kVecThreads, 0, s>>>(lam, mu, s_lam, s_mu, w.img4, N, g.Hp, g.Wp, B); note();
-    CK(cudaGetLastError());
-    {
-        ProjArgs A = base_args(g, proj_cfg(g, MODE_JVP));
-        A.img4 = w.img4;
-        A.y = nullptr;
-        A.dy = w.dysino;
-        if ((st = run_proj(g, MODE_JVP, A, s))) return st;
-    }
+    if ((st = pack4(g, w, lam, mu, s_lam, s_mu, s))) return st;
+    if ((st = proj_out(g, w, MODE_JVP, nullptr, w.dysino, s))) return st;
     sumsq_kernel<<<vg, kVecThreads, 0, s>>>(w.dysino, P[5], nsper); note();
     regsq_kernel<<<vg, kVecThreads, 0, s>>>(s_lam, s_mu, P[6], N); note();
     dot2_kernel<<<vg, kVecThreads, 0, s>>>(w.bl, w.bm, s_lam, s_mu, P[7], n2); note();
@@ -560,12 +594,8 @@ pget_status pget_gn_cg_step(pget_geometry h, const float* lam, const float* mu, 
     CK(cudaGetLastError());
     // 7-8: f(u+s), rho, accept, beta_next
     if (flags & PGET_GN_EVAL_TRIAL) {
-        pack2_kernel<<<vec_grid(img), kVecThreads, 0, s>>>(lam, mu, s_lam, s_mu, w.img2, w.ul, w.um, N, g.Hp, g.Wp, B); note();
-        CK(cudaGetLastError());
-        ProjArgs A = base_args(g, proj_cfg(g, MODE_FWD));
-        A.img2 = w.img2;
-        A.y = w.ysino;
-        if ((st = run_proj(g, MODE_FWD, A, s))) return st;
+        if ((st = pack2(g, w, lam, mu, s_lam, s_mu, w.ul, w.um, s))) return st;
+        if ((st = proj_out(g, w, MODE_FWD, w.ysino, nullptr, s))) return st;
         residual_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, y_meas, P[0], nsper); note();
         regsq_kernel<<<vg, kVecThreads, 0, s>>>(w.ul, w.um, P[1], N); note();
         scalar_kernel<<<sgrid, 128, 0, s>>>(SC_TRIAL, 0, P[0], P[1], nullptr, kNblk, w.cg, stats, B, alpha, beta); note();

@@ -126,19 +126,59 @@ pget_status build_geometry(const pget_geometry_desc* d, Geometry* g, std::string
     g->n_samples_nominal = nominal * d->batch;
 
     g->R = nd * J;
-    g->R_pad = (g->R + 31) / 32 * 32;
     g->n_ab = nA * nB;
-    g->Hp = N + 2 * kHalo;
-    g->Wp = (N + 2 * kHalo + 1) & ~1;   // even: 16-B aligned rows of float2 for the band copies
+    g->P = (N + 2 * kHalo + 1) & ~1;   // even: 16-B aligned rows of float2 for the bulk band copies
+
+    // orientation classes: class 1 when the ray runs closer to the x axis,
+    // so that in its oriented frame every ray crosses image rows at >= 1/sqrt2 rows per pixel.
+    g->orient.resize(g->n_ab);
+    g->task_ab.clear();
+    for (int ab = 0; ab < g->n_ab; ++ab) {
+        const double c = g->dirs[static_cast<size_t>(ab) * 2 + 0];
+        const double s = g->dirs[static_cast<size_t>(ab) * 2 + 1];
+        g->orient[ab] = std::fabs(c) > std::fabs(s) ? 1 : 0;
+    }
+    for (int cls = 0; cls < 2; ++cls)
+        for (int ab = 0; ab < g->n_ab; ++ab)
+            if (g->orient[ab] == cls) g->task_ab.push_back(ab);
+    g->n_class0 = 0;
+    for (int ab = 0; ab < g->n_ab; ++ab) g->n_class0 += g->orient[ab] == 0;
+
+    // comb groups: ray offsets are uniform with spacing a = (p/J)/h pixels; two rays S >= (2 sqrt2 + 1e-6)/a
+    // apart have sample points >= 2 px apart in max-norm, so their bilinear footprints never overlap.
+    {
+        const double a = (p / J) / g->h;
+        long S = static_cast<long>(std::ceil((2.0 * std::sqrt(2.0) + 1e-6) / a));
+        if (S < 1) S = 1;
+        if (S > g->R) S = g->R;
+        g->comb_S = static_cast<int>(S);
+        g->groups.clear();
+        std::vector<int32_t> cur;
+        auto flush = [&]() {
+            if (cur.empty()) return;
+            for (int k = 0; k < 32; ++k) g->groups.push_back(k < static_cast<int>(cur.size()) ? cur[k] : -1);
+            cur.clear();
+        };
+        for (int c0 = 0; c0 < S; ++c0)
+            for (int r = c0; r < g->R; r += static_cast<int>(S)) {
+                bool ok = cur.size() < 32;
+                for (int32_t q : cur)
+                    if (std::abs(q - r) < S) { ok = false; break; }
+                if (!ok) flush();
+                cur.push_back(r);
+            }
+        flush();
+        g->n_groups = static_cast<int>(g->groups.size() / 32);
+    }
     return PGET_OK;
 }
 
-// 32.32 fixed-point sample positions in padded pixel coordinates.
-void build_ray_params(const Geometry& g, std::vector<RayP>* rays, std::vector<int8_t>* abdir)
+// 32.32 fixed-point sample positions in padded pixel coordinates, in each angle-bank's oriented
+// frame (class 1: u and v swapped, the ray samples the transposed image).
+void build_ray_params(const Geometry& g, std::vector<RayP>* rays)
 {
     const int nB = g.desc.n_banks, nd = g.desc.n_det, J = g.desc.n_subrays;
     rays->resize(static_cast<size_t>(g.n_ab) * g.R);
-    abdir->resize(g.n_ab);
     const double scale = 4294967296.0;   // 2^32
     const int64_t bias = int64_t(1) << 8; // +2^-24 px: round the 23-bit fraction to nearest
     const double t0 = -g.T + 0.5 * g.delta;
@@ -148,7 +188,7 @@ void build_ray_params(const Geometry& g, std::vector<RayP>* rays, std::vector<in
         const double s = g.dirs[static_cast<size_t>(ab) * 2 + 1];
         const double du = g.delta * c / g.h, dv = g.delta * s / g.h;
         const int64_t dU = std::llround(du * scale), dV = std::llround(dv * scale);
-        (*abdir)[ab] = dV > 0 ? 1 : (dV < 0 ? -1 : 0);
+        const bool tr = g.orient[ab] != 0;
         for (int dd = 0; dd < nd; ++dd)
             for (int j = 0; j < J; ++j) {
                 const double sigma = g.offsets[(static_cast<size_t>(b) * nd + dd) * J + j];
@@ -157,10 +197,11 @@ void build_ray_params(const Geometry& g, std::vector<RayP>* rays, std::vector<in
                 const double u0 = (x0 + 1.0) / g.h - 0.5 + kHalo;
                 const double v0 = (y0 + 1.0) / g.h - 0.5 + kHalo;
                 RayP& rp = (*rays)[static_cast<size_t>(ab) * g.R + dd * J + j];
-                rp.U0 = std::llround(u0 * scale) + bias;
-                rp.V0 = std::llround(v0 * scale) + bias;
-                rp.dU = dU;
-                rp.dV = dV;
+                const int64_t U0 = std::llround(u0 * scale) + bias, V0 = std::llround(v0 * scale) + bias;
+                rp.U0 = tr ? V0 : U0;
+                rp.V0 = tr ? U0 : V0;
+                rp.dU = tr ? dV : dU;
+                rp.dV = tr ? dU : dV;
                 const size_t r = static_cast<size_t>(ab) * nd * J + dd * J + j;
                 rp.ilo = g.clip[2 * r];
                 rp.ihi = g.clip[2 * r + 1];

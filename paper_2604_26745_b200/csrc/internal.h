@@ -17,6 +17,8 @@ constexpr int kMaxSubrays = 64;
 
 // Per-ray sample parametrisation in padded pixel coordinates, 32.32 fixed point:
 //   u_i = U0 + i*dU, v_i = V0 + i*dV   (u = (x+1)/h - 1/2 + kHalo, v likewise)
+// in the angle-bank's oriented frame: for orientation class 1 (|dU| > |dV|) u and v are
+// swapped, i.e. the ray samples the transposed image.
 // U0/V0 carry a +2^-24 px rounding bias so that (low word >> 9) rounds the
 // fraction to nearest at 23 bits (see kernels.cu, frac23()).
 struct RayP {
@@ -39,14 +41,22 @@ struct Geometry {
     int64_t n_samples_nominal;
     // launch geometry
     int R;        // rays per angle-bank = n_det * J
-    int R_pad;    // rounded up to a multiple of 32
     int n_ab;     // n_angles * n_banks
-    int Hp, Wp;   // padded image rows / cols
+    int P;        // padded image side (rows = cols = P, even): N + 2 kHalo rounded up to even
+    // orientation classes: class 0 = |dV| >= |dU| (image used as is), class 1 = transposed image
+    std::vector<int8_t> orient;   // [n_ab]
+    std::vector<int32_t> task_ab; // [n_ab] angle-bank processing order: class 0 first, then class 1
+    int n_class0 = 0;
+    // comb ray groups: <= 32 rays whose offsets differ pairwise by >= comb_S rays (>= 2 sqrt2 px)
+    int comb_S = 1;
+    int n_groups = 0;
+    std::vector<int32_t> groups;  // [n_groups][32] ray index in the angle-bank, -1 = idle lane
     // device tables
-    RayP* d_rays = nullptr;      // [n_ab][R]
-    int8_t* d_abdir = nullptr;   // [n_ab] sign of dV
-    float* d_w = nullptr;        // [J] float weights
-    std::vector<float> wf;       // host copy of the float weights
+    RayP* d_rays = nullptr;       // [n_ab][R] oriented frame
+    int32_t* d_groups = nullptr;  // [n_groups][32]
+    int32_t* d_task_ab = nullptr; // [n_ab]
+    float* d_w = nullptr;         // [J] float weights
+    std::vector<float> wf;        // host copy of the float weights
     int sm_count = 148;
     size_t smem_optin = 227 * 1024;
 };
@@ -60,5 +70,5 @@ struct pget_geometry_s {
 namespace pget {
 // geometry.cpp
 pget_status build_geometry(const pget_geometry_desc* d, Geometry* g, std::string* err);
-void build_ray_params(const Geometry& g, std::vector<RayP>* rays, std::vector<int8_t>* abdir);
+void build_ray_params(const Geometry& g, std::vector<RayP>* rays);
 }  // namespace pget

@@ -1,22 +1,7 @@
-// kernels.cu -- sm_100a kernels of the PGET hot path.
-//
-// Ray-driven projector: one CTA per (batch member,
-// angle-bank); one lane per ray, 32 adjacent sub-rays per warp; the padded
-// lambda/mu image is staged into shared memory in bands of rows, visited in
-// detector-first order so that every ray's attenuation suffix sum
-//     A_i = Delta (mu_i / 2 + sum_{k>i} mu_k)          (B mu; reading Q8)
-// is a per-lane recurrence in registers carried across bands.  One ex2 per sample.
-//   MODE_FWD : y      = sum_j w_j Delta sum_i lam_i E_i                 (eq:fwd_model)
-//   MODE_JVP : + dy   = sum_j w_j Delta sum_i (dlam_i - lam_i dA_i) E_i  (eq:frechet)
-//   MODE_VJP : sweep A gives G = sum_i lam_i E_i per ray; sweep B scatters
-//              a_lam(i) = w_r Delta E_i and a_mu(i) = -w_r Delta^2 (G - Q_i - lam_i E_i / 2)
-//              (Q_i = sum_{k>i} lam_k E_k) with the transposed bilinear weights into a
-//              shared-memory band accumulator (no global atomics in the sample loop),
-//              flushed once per band.
-//   MODE_GN  : sweep A = fused JVP of p; per-detector w = sum_j w_j (Jp)_ray in shared
-//              memory; sweep B = VJP with those weights -> J^T J p   (eq:LMA-step)
-// Sample positions are 32.32 fixed point (exact integer stepping); the bilinear
-// fraction is taken from the low word (23 bits, rounded), see internal.h RayP.
+// kernels.cu -- the vector kernels of the PGET hot path on sm_100a: image packing for the
+// projector (proj.cu), the regulariser, residual and objective reductions and the CG updates of
+// the LM iteration.  Reductions use per-member fp64
+// block partials over a fixed grid, so every scalar is deterministic.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -25,307 +10,19 @@
 
 namespace pget {
 
-__device__ __forceinline__ float frac23(int64_t x)
-{
-    return __uint_as_float((static_cast<uint32_t>(x) >> 9) | 0x3f800000u) - 1.0f;
-}
-
-__device__ __forceinline__ int hi32(int64_t x) { return static_cast<int>(x >> 32); }
-
-__device__ __forceinline__ float ex2(float x)
-{
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
-// bilinear lerp of a (lam, mu) pair: a=(j0,i0) b=(j0,i0+1) c=(j0+1,i0) d=(j0+1,i0+1)
-__device__ __forceinline__ float2 bilerp2(float2 a, float2 b, float2 c, float2 d, float fu, float fv)
-{
-    const float2 m1 = make_float2(-1.f, -1.f);
-    const float2 u2 = make_float2(fu, fu), v2 = make_float2(fv, fv);
-    const float2 top = __ffma2_rn(u2, __ffma2_rn(a, m1, b), a);
-    const float2 bot = __ffma2_rn(u2, __ffma2_rn(c, m1, d), c);
-    return __ffma2_rn(v2, __ffma2_rn(top, m1, bot), top);
-}
-
-__device__ __forceinline__ float2 lo2(float4 x) { return make_float2(x.x, x.y); }
-__device__ __forceinline__ float2 hi2(float4 x) { return make_float2(x.z, x.w); }
-
-// Cooperative copy of `nfloat` floats (multiple of 4, 16-B aligned) global -> shared.
-__device__ __forceinline__ void stage(float* __restrict__ dst, const float* __restrict__ src, int nfloat)
-{
-    const float4* s4 = reinterpret_cast<const float4*>(src);
-    float4* d4 = reinterpret_cast<float4*>(dst);
-    const int n4 = nfloat >> 2;
-    for (int k = threadIdx.x; k < n4; k += blockDim.x) d4[k] = __ldg(s4 + k);
-}
-
-__device__ __forceinline__ void zero_smem(float* dst, int nfloat)
-{
-    float4* d4 = reinterpret_cast<float4*>(dst);
-    const int n4 = nfloat >> 2;
-    for (int k = threadIdx.x; k < n4; k += blockDim.x) d4[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-}
-
-// Band k of nb: j0 rows [r0, r1), staged rows [r0, r1] (the +1 row for the bilinear j0+1).
-__device__ __forceinline__ void band_rows(int k, int Rb, int Hp, int& r0, int& r1)
-{
-    r0 = k * Rb;
-    r1 = min(r0 + Rb, Hp - 1);
-}
-
 // ------------------------------------------------------------------------------------------
-// Sweep A: forward (+ fused JVP) recurrence over all bands.
-//   NF = 2: staged (lam, mu); NF = 4: staged (lam, mu, dlam, dmu).
-// State per ray k (registers): i[k] next sample, S[k] = -Delta log2e sum_{k>i} mu,
-// g[k] = sum lam E, and for NF = 4: dS[k] = Delta sum_{k>i} dmu, dg[k].
-template <int NF, int MAXR>
-__device__ __forceinline__ void sweep_a(const ProjArgs& A, const float* __restrict__ img, float* sbuf,
-                                        const RayP* __restrict__ rays, int dir, int nvalid,
-                                        float (&g)[MAXR], float (&dg)[MAXR])
-{
-    const int T = blockDim.x;
-    const int Wp = A.Wp, Hp = A.Hp, Rb = A.RbA;
-    const int nb = (Hp - 1 + Rb - 1) / Rb;
-    int icur[MAXR];
-    float S[MAXR], dS[MAXR];
-#pragma unroll
-    for (int k = 0; k < MAXR; ++k) {
-        const int r = threadIdx.x + k * T;
-        icur[k] = (r < nvalid) ? rays[r].ihi : -1;
-        S[k] = 0.f; g[k] = 0.f; dS[k] = 0.f; dg[k] = 0.f;
-    }
-    const float cf = A.cf, ch = A.ch, dl = A.delta, dlh = 0.5f * A.delta;
-    for (int kb = 0; kb < nb; ++kb) {
-        const int band = dir > 0 ? nb - 1 - kb : kb;
-        int r0, r1;
-        band_rows(band, Rb, Hp, r0, r1);
-        __syncthreads();   // previous band fully consumed
-        stage(sbuf, img + static_cast<size_t>(r0) * Wp * NF, (r1 - r0 + 1) * Wp * NF);
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < MAXR; ++k) {
-            const int r = threadIdx.x + k * T;
-            if (r >= nvalid) continue;
-            int i = icur[k];
-            const RayP rp = rays[r];
-            if (i < rp.ilo) continue;
-            int64_t u = rp.U0 + static_cast<int64_t>(i) * rp.dU;
-            int64_t v = rp.V0 + static_cast<int64_t>(i) * rp.dV;
-            float s = S[k], gg = g[k], ds = dS[k], dgg = dg[k];
-            while (i >= rp.ilo) {
-                const int iv = hi32(v);
-                if (iv < r0 || iv >= r1) break;
-                const int iu = hi32(u);
-                const float fu = frac23(u), fv = frac23(v);
-                const int o = (iv - r0) * Wp + iu;
-                float lam, mu, dlam = 0.f, dmu = 0.f;
-                if (NF == 2) {
-                    const float2* p = reinterpret_cast<const float2*>(sbuf) + o;
-                    const float2 x = bilerp2(p[0], p[1], p[Wp], p[Wp + 1], fu, fv);
-                    lam = x.x; mu = x.y;
-                } else {
-                    const float4* p = reinterpret_cast<const float4*>(sbuf) + o;
-                    const float4 a = p[0], b = p[1], c = p[Wp], d = p[Wp + 1];
-                    const float2 x = bilerp2(lo2(a), lo2(b), lo2(c), lo2(d), fu, fv);
-                    const float2 y = bilerp2(hi2(a), hi2(b), hi2(c), hi2(d), fu, fv);
-                    lam = x.x; mu = x.y; dlam = y.x; dmu = y.y;
-                }
-                const float E = ex2(fmaf(mu, ch, s));     // exp(-Delta (mu_i/2 + sum_{k>i} mu_k))
-                gg = fmaf(lam, E, gg);
-                s = fmaf(mu, cf, s);
-                if (NF == 4) {
-                    const float dA = fmaf(dmu, dlh, ds);    // Delta (dmu_i/2 + sum_{k>i} dmu_k)
-                    dgg = fmaf(fmaf(-lam, dA, dlam), E, dgg);
-                    ds = fmaf(dmu, dl, ds);
-                }
-                --i;
-                u -= rp.dU;
-                v -= rp.dV;
-            }
-            icur[k] = i; S[k] = s; g[k] = gg; dS[k] = ds; dg[k] = dgg;
-        }
-    }
-}
-
-__device__ __forceinline__ void sadd(float* p, float v) { atomicAdd(p, v); }
-
-// Sweep B: adjoint scatter.  kl[k] = w_r Delta, km[k] = -w_r Delta^2, G[k] = sum lam E (sweep A).
-template <int MAXR>
-__device__ __forceinline__ void sweep_b(const ProjArgs& A, const float* __restrict__ img, float* sbuf,
-                                        float* sacc, float2* __restrict__ gacc,
-                                        const RayP* __restrict__ rays, int dir, int nvalid,
-                                        const float (&kl)[MAXR], const float (&km)[MAXR],
-                                        const float (&G)[MAXR])
-{
-    const int T = blockDim.x;
-    const int Wp = A.Wp, Hp = A.Hp, Rb = A.RbB;
-    const int nb = (Hp - 1 + Rb - 1) / Rb;
-    int icur[MAXR];
-    float S[MAXR], Q[MAXR];
-#pragma unroll
-    for (int k = 0; k < MAXR; ++k) {
-        const int r = threadIdx.x + k * T;
-        icur[k] = (r < nvalid && kl[k] != 0.f) ? rays[r].ihi : -1;
-        S[k] = 0.f; Q[k] = 0.f;
-    }
-    const float cf = A.cf, ch = A.ch;
-    for (int kb = 0; kb < nb; ++kb) {
-        const int band = dir > 0 ? nb - 1 - kb : kb;
-        int r0, r1;
-        band_rows(band, Rb, Hp, r0, r1);
-        const int nrow = r1 - r0 + 1;
-        __syncthreads();
-        stage(sbuf, img + static_cast<size_t>(r0) * Wp * 2, nrow * Wp * 2);
-        zero_smem(sacc, nrow * Wp * 2);
-        __syncthreads();
-#pragma unroll
-        for (int k = 0; k < MAXR; ++k) {
-            const int r = threadIdx.x + k * T;
-            if (r >= nvalid) continue;
-            int i = icur[k];
-            const RayP rp = rays[r];
-            if (i < rp.ilo) continue;
-            int64_t u = rp.U0 + static_cast<int64_t>(i) * rp.dU;
-            int64_t v = rp.V0 + static_cast<int64_t>(i) * rp.dV;
-            float s = S[k], q = Q[k];
-            const float kll = kl[k], kmm = km[k], GG = G[k];
-            while (i >= rp.ilo) {
-                const int iv = hi32(v);
-                if (iv < r0 || iv >= r1) break;
-                const int iu = hi32(u);
-                const float fu = frac23(u), fv = frac23(v);
-                const int o = (iv - r0) * Wp + iu;
-                const float2* p = reinterpret_cast<const float2*>(sbuf) + o;
-                const float2 x = bilerp2(p[0], p[1], p[Wp], p[Wp + 1], fu, fv);
-                const float E = ex2(fmaf(x.y, ch, s));
-                const float le = x.x * E;
-                const float al = kll * E;
-                const float am = kmm * (GG - q - 0.5f * le);
-                q += le;
-                s = fmaf(x.y, cf, s);
-                // transposed bilinear weights
-                const float2 av = make_float2(al, am);
-                const float2 tv = __fmul2_rn(av, make_float2(fv, fv));       // row j0+1
-                const float2 bv = __ffma2_rn(tv, make_float2(-1.f, -1.f), av); // row j0
-                const float2 c11 = __fmul2_rn(tv, make_float2(fu, fu));
-                const float2 c10 = __ffma2_rn(c11, make_float2(-1.f, -1.f), tv);
-                const float2 c01 = __fmul2_rn(bv, make_float2(fu, fu));
-                const float2 c00 = __ffma2_rn(c01, make_float2(-1.f, -1.f), bv);
-                float* a0 = sacc + 2 * o;
-                sadd(a0 + 0, c00.x); sadd(a0 + 1, c00.y);
-                sadd(a0 + 2, c01.x); sadd(a0 + 3, c01.y);
-                float* a1 = a0 + 2 * Wp;
-                sadd(a1 + 0, c10.x); sadd(a1 + 1, c10.y);
-                sadd(a1 + 2, c11.x); sadd(a1 + 3, c11.y);
-                --i;
-                u -= rp.dU;
-                v -= rp.dV;
-            }
-            icur[k] = i; S[k] = s; Q[k] = q;
-        }
-        __syncthreads();
-        // flush the band accumulator (rows r0..r1) into the member's global accumulator
-        const float2* sa2 = reinterpret_cast<const float2*>(sacc);
-        float2* gdst = gacc + static_cast<size_t>(r0) * Wp;
-        for (int e = threadIdx.x; e < nrow * Wp; e += blockDim.x) {
-            const float2 val = sa2[e];
-            if (val.x != 0.f || val.y != 0.f) atomicAdd(gdst + e, val);
-        }
-    }
-}
-
-template <int MODE, int MAXR>
-__global__ void __launch_bounds__(1024, 1) proj_kernel(ProjArgs A)
-{
-    extern __shared__ __align__(16) float smem[];
-    const int ab = blockIdx.x % A.n_ab;
-    const int m = blockIdx.x / A.n_ab;
-    const int T = blockDim.x;
-    const int dir = A.abdir[ab];
-    const RayP* rays = A.rays + static_cast<size_t>(ab) * A.R;
-    const size_t imgsz = static_cast<size_t>(A.Hp) * A.Wp;
-    float* sbuf = smem;
-    float* rout = smem + A.rout_off;   // 2 * R_pad floats
-
-    float g[MAXR], dg[MAXR];
-    if (MODE == MODE_FWD || MODE == MODE_VJP)
-        sweep_a<2, MAXR>(A, reinterpret_cast<const float*>(A.img2 + m * imgsz), sbuf, rays, dir, A.R, g, dg);
-    else
-        sweep_a<4, MAXR>(A, reinterpret_cast<const float*>(A.img4 + m * imgsz), sbuf, rays, dir, A.R, g, dg);
-
-    const int J = A.J;
-    if (MODE == MODE_FWD || MODE == MODE_JVP) {
-#pragma unroll
-        for (int k = 0; k < MAXR; ++k) {
-            const int r = threadIdx.x + k * T;
-            if (r < A.R) {
-                rout[r] = A.delta * g[k];
-                if (MODE == MODE_JVP) rout[A.R_pad + r] = A.delta * dg[k];
-            }
-        }
-        __syncthreads();
-        const size_t obase = (static_cast<size_t>(m) * A.n_ab + ab) * A.n_det;
-        for (int d = threadIdx.x; d < A.n_det; d += T) {
-            float acc = 0.f, dacc = 0.f;
-            for (int j = 0; j < J; ++j) {
-                const float wj = A.w[j];
-                acc = fmaf(wj, rout[d * J + j], acc);
-                if (MODE == MODE_JVP) dacc = fmaf(wj, rout[A.R_pad + d * J + j], dacc);
-            }
-            if (A.y) A.y[obase + d] = acc;
-            if (MODE == MODE_JVP) A.dy[obase + d] = dacc;
-        }
-        return;
-    }
-
-    // adjoint weights per ray
-    float kl[MAXR], km[MAXR];
-    if (MODE == MODE_GN) {
-#pragma unroll
-        for (int k = 0; k < MAXR; ++k) {
-            const int r = threadIdx.x + k * T;
-            if (r < A.R) rout[r] = A.delta * dg[k];     // (J p)_ray
-        }
-        __syncthreads();
-    }
-    const size_t wbase = (static_cast<size_t>(m) * A.n_ab + ab) * A.n_det;
-#pragma unroll
-    for (int k = 0; k < MAXR; ++k) {
-        const int r = threadIdx.x + k * T;
-        kl[k] = 0.f; km[k] = 0.f;
-        if (r < A.R) {
-            const int d = r / J, j = r - d * J;
-            float wd;
-            if (MODE == MODE_GN) {
-                wd = 0.f;
-                for (int jj = 0; jj < J; ++jj) wd = fmaf(A.w[jj], rout[d * J + jj], wd);
-            } else {
-                wd = A.win[wbase + d];
-            }
-            const float wr = A.w[j] * wd;
-            kl[k] = wr * A.delta;
-            km[k] = -wr * A.delta * A.delta;
-        }
-    }
-    float* sacc = smem + A.acc_off;
-    sweep_b<MAXR>(A, reinterpret_cast<const float*>(A.img2 + m * imgsz), sbuf, sacc, A.acc + m * imgsz, rays,
-                  dir, A.R, kl, km, g);
-}
-
-// ------------------------------------------------------------------------------------------
-// image packing: padded interleaved images with a zero halo of kHalo pixels
+// image packing: padded P x P images with a zero halo of kHalo pixels, in the normal and in the
+// transposed orientation (orientation class 1 of the projector samples the transposed copy).
 __global__ void pack2_kernel(const float* __restrict__ lam, const float* __restrict__ mu,
                              const float* __restrict__ slam, const float* __restrict__ smu, float2* out,
-                             float* ut_lam, float* ut_mu, int N, int Hp, int Wp, int B)
+                             float2* outT, float* ut_lam, float* ut_mu, int N, int P, int B)
 {
-    const size_t total = static_cast<size_t>(B) * Hp * Wp;
+    const size_t total = static_cast<size_t>(B) * P * P;
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int ip = static_cast<int>(e % Wp);
-        const int jp = static_cast<int>((e / Wp) % Hp);
-        const size_t m = e / (static_cast<size_t>(Wp) * Hp);
+        const int ip = static_cast<int>(e % P);
+        const int jp = static_cast<int>((e / P) % P);
+        const size_t m = e / (static_cast<size_t>(P) * P);
         const int i = ip - kHalo, j = jp - kHalo;
         float2 val = make_float2(0.f, 0.f);
         if (i >= 0 && i < N && j >= 0 && j < N) {
@@ -339,19 +36,20 @@ __global__ void pack2_kernel(const float* __restrict__ lam, const float* __restr
             }
         }
         out[e] = val;
+        outT[(m * P + ip) * P + jp] = val;
     }
 }
 
 __global__ void pack4_kernel(const float* __restrict__ lam, const float* __restrict__ mu,
-                             const float* __restrict__ dl, const float* __restrict__ dm, float4* out, int N,
-                             int Hp, int Wp, int B)
+                             const float* __restrict__ dl, const float* __restrict__ dm, float4* out, float4* outT,
+                             int N, int P, int B)
 {
-    const size_t total = static_cast<size_t>(B) * Hp * Wp;
+    const size_t total = static_cast<size_t>(B) * P * P;
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int ip = static_cast<int>(e % Wp);
-        const int jp = static_cast<int>((e / Wp) % Hp);
-        const size_t m = e / (static_cast<size_t>(Wp) * Hp);
+        const int ip = static_cast<int>(e % P);
+        const int jp = static_cast<int>((e / P) % P);
+        const size_t m = e / (static_cast<size_t>(P) * P);
         const int i = ip - kHalo, j = jp - kHalo;
         float4 val = make_float4(0.f, 0.f, 0.f, 0.f);
         if (i >= 0 && i < N && j >= 0 && j < N) {
@@ -359,6 +57,7 @@ __global__ void pack4_kernel(const float* __restrict__ lam, const float* __restr
             val = make_float4(lam[src], mu[src], dl[src], dm[src]);
         }
         out[e] = val;
+        outT[(m * P + ip) * P + jp] = val;
     }
 }
 
@@ -405,7 +104,7 @@ __global__ void finish_kernel(const float2* __restrict__ acc, const float* __res
                               const float* __restrict__ xm, float alpha, float beta, float sign,
                               float* outl, float* outm, const float* __restrict__ dotl,
                               const float* __restrict__ dotm, double* partial, float* copy1l, float* copy1m,
-                              float* copy2l, float* copy2m, float* zerol, float* zerom, int N, int Hp, int Wp)
+                              float* copy2l, float* copy2m, float* zerol, float* zerom, int N)
 {
     __shared__ double sh[32];
     const int m = blockIdx.y;
@@ -415,7 +114,7 @@ __global__ void finish_kernel(const float2* __restrict__ acc, const float* __res
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n2;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const int i = static_cast<int>(e % N), j = static_cast<int>(e / N);
-        const float2 a = acc[(static_cast<size_t>(m) * Hp + j + kHalo) * Wp + i + kHalo];
+        const float2 a = acc[base + e];
         float ol = a.x, om = a.y;
         if (xl) {
             const float* pl = xl + base;
@@ -610,48 +309,3 @@ __global__ void scalar_kernel(int op, int k, const double* p0, const double* p1,
 
 }  // namespace pget
 
-namespace pget {
-
-// Host launcher of the projector (instantiates every (MODE, MAXR) pair).
-template <int MODE>
-static cudaError_t launch_mode(int maxr, const ProjArgs& A, int grid, int block, size_t smem, cudaStream_t s)
-{
-    switch (maxr) {
-    case 1: proj_kernel<MODE, 1><<<grid, block, smem, s>>>(A); break;
-    case 2: proj_kernel<MODE, 2><<<grid, block, smem, s>>>(A); break;
-    case 4: proj_kernel<MODE, 4><<<grid, block, smem, s>>>(A); break;
-    default: return cudaErrorInvalidValue;
-    }
-    return cudaGetLastError();
-}
-
-cudaError_t launch_proj(int mode, int maxr, const ProjArgs& A, int grid, int block, size_t smem, cudaStream_t s)
-{
-    switch (mode) {
-    case MODE_FWD: return launch_mode<MODE_FWD>(maxr, A, grid, block, smem, s);
-    case MODE_JVP: return launch_mode<MODE_JVP>(maxr, A, grid, block, smem, s);
-    case MODE_VJP: return launch_mode<MODE_VJP>(maxr, A, grid, block, smem, s);
-    case MODE_GN: return launch_mode<MODE_GN>(maxr, A, grid, block, smem, s);
-    }
-    return cudaErrorInvalidValue;
-}
-
-template <int MODE>
-static cudaError_t attr_mode(size_t smem)
-{
-    cudaError_t e;
-    if ((e = cudaFuncSetAttribute(proj_kernel<MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
-    if ((e = cudaFuncSetAttribute(proj_kernel<MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
-    return cudaFuncSetAttribute(proj_kernel<MODE, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-}
-
-cudaError_t set_proj_smem_limit(size_t smem)
-{
-    cudaError_t e;
-    if ((e = attr_mode<MODE_FWD>(smem))) return e;
-    if ((e = attr_mode<MODE_JVP>(smem))) return e;
-    if ((e = attr_mode<MODE_VJP>(smem))) return e;
-    return attr_mode<MODE_GN>(smem);
-}
-
-}  // namespace pget

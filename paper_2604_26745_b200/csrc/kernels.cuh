@@ -10,38 +10,53 @@ enum { MODE_FWD = 0, MODE_JVP = 1, MODE_VJP = 2, MODE_GN = 3 };
 enum { SC_INIT = 0, SC_GAMMA = 1, SC_ZETA = 2, SC_PRED = 3, SC_TRIAL = 4 };
 
 struct ProjArgs {
-    const RayP* rays;      // [n_ab][R]
-    const int8_t* abdir;   // [n_ab]
-    const float* w;        // [J] sub-ray weights (float)
-    const float2* img2;    // [B][Hp][Wp] (lam, mu)
-    const float4* img4;    // [B][Hp][Wp] (lam, mu, dlam, dmu)
-    float2* acc;           // [B][Hp][Wp] adjoint accumulators (g_lam, g_mu)
-    const float* win;      // [B][n_ab][n_det] VJP weights
-    float* y;              // [B][n_ab][n_det]
-    float* dy;             // [B][n_ab][n_det]
-    int Hp, Wp, n_det, J, R, R_pad, n_ab;
-    int RbA, RbB;          // band heights (j0 rows) of sweep A / sweep B
-    int rout_off, acc_off; // float offsets into dynamic shared memory
-    float delta;           // Delta
-    float cf, ch;          // -Delta log2(e), -Delta log2(e) / 2
+    const RayP* rays;       // [n_ab][R] oriented-frame fixed-point ray parameters
+    const int32_t* groups;  // [n_groups][32] comb ray groups (-1 = idle lane)
+    const int32_t* task_ab; // [n_ab] angle-bank order (class 0, then class 1)
+    const float* w;         // [J] sub-ray weights (float)
+    const float2* img2[2];  // [B][P][P] (lam, mu): normal / transposed, zero halo
+    const float4* img4[2];  // [B][P][P] (lam, mu, dlam, dmu)
+    float2* slots;          // [C][KS][N][Ns] per-CTA fp32 partial gradients (g_lam, g_mu)
+    const float* win;       // [B][n_ab][n_det] VJP weights
+    float* y;               // [B][n_ab][n_det]
+    float* dy;              // [B][n_ab][n_det]
+    int N, Ns, P, n_det, J, R, n_ab, n_class0, B, n_groups, KS;
+    int RbA, RbB, nbA, nbB, passesA, passesB;   // sweep A: 32 adjacent rays per warp; sweep B: comb groups
+    int stage_bytes, off_wacc, off_rout, off_gsh;   // dynamic shared memory layout (bytes)
+    float delta;            // Delta
+    float cf, ch;           // -Delta log2(e), -Delta log2(e) / 2
 };
+
+// Partial-gradient slots: the tasks (member, angle-bank) of one orientation class of one member are
+// cut into chunks of kChunk consecutive tasks; a CTA accumulates each chunk it touches into its own
+// fp32 slot (so a slot sums at most kChunk angle-banks) and reduce_slots_kernel adds the slots in fp64.
+constexpr int kChunk = 16;
+
+__host__ __device__ inline int64_t chunk_of(int64_t t, int n_ab, int n_class0)
+{
+    const int64_t m = t / n_ab;
+    const int k = static_cast<int>(t - m * n_ab);
+    const int nc0 = (n_class0 + kChunk - 1) / kChunk, nc1 = (n_ab - n_class0 + kChunk - 1) / kChunk;
+    const int local = k < n_class0 ? k / kChunk : nc0 + (k - n_class0) / kChunk;
+    return m * (nc0 + nc1) + local;
+}
 
 struct CGState {
     double zeta, a, bcg;
     int stop, pad_;
 };
 
-template <int MODE, int MAXR>
-__global__ void proj_kernel(ProjArgs A);
 
 __global__ void pack2_kernel(const float* lam, const float* mu, const float* slam, const float* smu, float2* out,
-                             float* ut_lam, float* ut_mu, int N, int Hp, int Wp, int B);
+                             float2* outT, float* ut_lam, float* ut_mu, int N, int P, int B);
 __global__ void pack4_kernel(const float* lam, const float* mu, const float* dl, const float* dm, float4* out,
-                             int N, int Hp, int Wp, int B);
+                             float4* outT, int N, int P, int B);
+__global__ void reduce_slots_kernel(const float2* slots, float2* out, int N, int Ns, int n_ab, int n_class0, int B,
+                                    int C, int KS, int unused);
 __global__ void finish_kernel(const float2* acc, const float* xl, const float* xm, float alpha, float beta,
                               float sign, float* outl, float* outm, const float* dotl, const float* dotm,
                               double* partial, float* copy1l, float* copy1m, float* copy2l, float* copy2m,
-                              float* zerol, float* zerom, int N, int Hp, int Wp);
+                              float* zerol, float* zerom, int N);
 __global__ void residual_kernel(float* y, const float* ymeas, double* partial, int nper);
 __global__ void sumsq_kernel(const float* x, double* partial, int nper);
 __global__ void regsq_kernel(const float* xl, const float* xm, double* partial, int N);
@@ -57,6 +72,8 @@ __global__ void scalar_kernel(int op, int k, const double* p0, const double* p1,
 }  // namespace pget
 
 namespace pget {
-cudaError_t launch_proj(int mode, int maxr, const ProjArgs& A, int grid, int block, size_t smem, cudaStream_t s);
-cudaError_t set_proj_smem_limit(size_t smem);
+cudaError_t launch_proj(int mode, int maxg, const ProjArgs& A, int grid, size_t smem, cudaStream_t s);
+cudaError_t set_proj_smem_limit(int mode, size_t smem);
+int proj_warps(int mode);
+int proj_ctas_per_sm(int mode);
 }  // namespace pget

@@ -1,0 +1,635 @@
+// proj.cu -- the ray-driven projector of the PGET hot path on sm_100a.
+//
+// Model (PAPER.md:48-54 eq:fwd_model, discretised per SURVEY.md §8(c.2) O1-O5):
+//   A_i  = Delta (mu_i / 2 + sum_{k>i} mu_k)                      (B mu, k > i: nearer the detector)
+//   y    = sum_j w_j Delta sum_i lam_i E_i,   E_i = exp(-A_i)
+//   dy   = sum_j w_j Delta sum_i (dlam_i - lam_i dA_i) E_i         (eq:frechet)
+//   VJP  : a_lam(i) = w_r Delta E_i,  a_mu(i) = -w_r Delta^2 (G - Q_i - lam_i E_i / 2),
+//          G = sum_i lam_i E_i, Q_i = sum_{k>i} lam_k E_k, scattered with the transposed bilinear
+//          weights (the exact transpose of the discrete JVP; adjoint F'^* of PAPER.md:231, 277)
+//   GN   : J^T (J p) fused per angle-bank: sweep A = JVP of p, per-detector (J p), sweep B = VJP.
+//
+// Execution model:
+//   * persistent CTAs, each owning a static contiguous range of tasks (member, angle-bank); angle-banks
+//     are ordered by orientation class; a CTA's range covers few (member, class, chunk) segments;
+//   * class 0 angle-banks sample the padded image as is, class 1 the transposed copy, so that in the
+//     oriented frame every ray advances >= 1/(2 sqrt2) rows per sample and crosses every row band;
+//   * the image is streamed through shared memory in row bands by 1-D bulk async copies (TMA engine,
+//     cp.async.bulk + mbarrier), double buffered across bands, passes and tasks;
+//   * a lane owns a ray; the 32 lanes of a warp own a "comb" of rays >= 2 sqrt2 px apart, so the
+//     bilinear footprints of a warp's samples never overlap: the VJP scatter is a plain shared-memory
+//     read-modify-write into a warp-private ring of band rows (no atomics in the sample loop);
+//   * per-ray sums that cancel (optical depth, JVP and adjoint sums) are Kahan-compensated
+//     (DESIGN.md "Precision"); one ex2 per sample;
+//   * the VJP band rows are flushed into a CTA-private fp32 partial image (one slot per segment);
+//     a fixed-order fp64 reduction of the slots (reduce_slots_kernel) makes the gradient deterministic.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.h"
+#include "kernels.cuh"
+
+namespace pget {
+
+// ------------------------------------------------------------------------------------------ helpers
+__device__ __forceinline__ float frac23(int64_t x)
+{
+    return __uint_as_float((static_cast<uint32_t>(x) >> 9) | 0x3f800000u) - 1.0f;
+}
+
+__device__ __forceinline__ int hi32(int64_t x) { return static_cast<int>(x >> 32); }
+
+__device__ __forceinline__ float ex2(float x)
+{
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// bilinear lerp of a channel pair: a=(j0,i0) b=(j0,i0+1) c=(j0+1,i0) d=(j0+1,i0+1)
+__device__ __forceinline__ float2 bilerp2(float2 a, float2 b, float2 c, float2 d, float fu, float fv)
+{
+    const float2 m1 = make_float2(-1.f, -1.f);
+    const float2 u2 = make_float2(fu, fu), v2 = make_float2(fv, fv);
+    const float2 top = __ffma2_rn(u2, __ffma2_rn(a, m1, b), a);
+    const float2 bot = __ffma2_rn(u2, __ffma2_rn(c, m1, d), c);
+    return __ffma2_rn(v2, __ffma2_rn(top, m1, bot), top);
+}
+
+__device__ __forceinline__ float2 lo2(float4 x) { return make_float2(x.x, x.y); }
+__device__ __forceinline__ float2 hi2(float4 x) { return make_float2(x.z, x.w); }
+
+// the four bilinear corners of a sample in the staged band: o = (iv - r0) * P + iu
+template <bool NF4>
+struct Px;
+template <>
+struct Px<true> {
+    float4 a, b, c, d;
+};
+template <>
+struct Px<false> {
+    float2 a, b, c, d;
+};
+__device__ __forceinline__ void load_px(Px<true>& x, const unsigned char* sb, int o, int P)
+{
+    const float4* p = reinterpret_cast<const float4*>(sb) + o;
+    x.a = p[0]; x.b = p[1]; x.c = p[P]; x.d = p[P + 1];
+}
+__device__ __forceinline__ void load_px(Px<false>& x, const unsigned char* sb, int o, int P)
+{
+    const float2* p = reinterpret_cast<const float2*>(sb) + o;
+    x.a = p[0]; x.b = p[1]; x.c = p[P]; x.d = p[P + 1];
+}
+
+// Kahan step: (s, c) += x  (the compensated sum is s - c)
+__device__ __forceinline__ void kahan(float& s, float& c, float x)
+{
+    const float y = x - c;
+    const float t = s + y;
+    c = (t - s) - y;
+    s = t;
+}
+
+// ---- mbarrier + 1-D bulk async copy (TMA engine)
+__device__ __forceinline__ uint32_t smem_u32(const void* p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// ------------------------------------------------------------------------------------------ tasks
+struct TaskInfo {
+    int m, ab, cls, dir;
+    int64_t seg;   // partial-slot chunk id (chunk_of)
+};
+
+__device__ __forceinline__ TaskInfo task_info(const ProjArgs& A, int64_t t)
+{
+    TaskInfo ti;
+    ti.m = static_cast<int>(t / A.n_ab);
+    const int k = static_cast<int>(t - static_cast<int64_t>(ti.m) * A.n_ab);
+    ti.ab = A.task_ab[k];
+    ti.cls = k >= A.n_class0 ? 1 : 0;
+    ti.seg = chunk_of(t, A.n_ab, A.n_class0);
+    ti.dir = A.rays[static_cast<size_t>(ti.ab) * A.R].dV > 0 ? 1 : -1;
+    return ti;
+}
+
+__device__ __forceinline__ void band_rows(int band, int Rb, int P, int& r0, int& r1)
+{
+    r0 = band * Rb;
+    r1 = min(r0 + Rb, P - 1);
+}
+
+// Issue the bulk copy of global stage `sidx` (a band of sweep A or B of some task) into `dst`.
+template <int MODE>
+__device__ void issue_stage(const ProjArgs& A, int64_t t0, int ns_task, int64_t sidx, void* dst, uint64_t* bar)
+{
+    const int64_t t = t0 + sidx / ns_task;
+    const int l = static_cast<int>(sidx % ns_task);
+    const TaskInfo ti = task_info(A, t);
+    const bool isA = l < A.passesA * A.nbA;
+    const int nb = isA ? A.nbA : A.nbB;
+    const int Rb = isA ? A.RbA : A.RbB;
+    const int kb = isA ? l % A.nbA : (l - A.passesA * A.nbA) % A.nbB;
+    const int band = ti.dir > 0 ? nb - 1 - kb : kb;
+    int r0, r1;
+    band_rows(band, Rb, A.P, r0, r1);
+    const size_t pix0 = static_cast<size_t>(ti.m) * A.P * A.P + static_cast<size_t>(r0) * A.P;
+    const size_t npix = static_cast<size_t>(r1 - r0 + 1) * A.P;
+    const char* src;
+    size_t bytes;
+    if (isA && (MODE == MODE_JVP || MODE == MODE_GN)) {
+        src = reinterpret_cast<const char*>(A.img4[ti.cls] + pix0);
+        bytes = npix * sizeof(float4);
+    } else {
+        src = reinterpret_cast<const char*>(A.img2[ti.cls] + pix0);
+        bytes = npix * sizeof(float2);
+    }
+    fence_proxy_async();
+    mbar_expect_tx(bar, static_cast<uint32_t>(bytes));
+    char* d = static_cast<char*>(dst);
+    for (size_t off = 0; off < bytes; off += 32768) {
+        const uint32_t n = static_cast<uint32_t>(bytes - off < 32768 ? bytes - off : 32768);
+        bulk_g2s(d + off, src + off, n, bar);
+    }
+}
+
+template <int MODE>
+struct ModeTraits {
+    static constexpr int W = (MODE == MODE_FWD || MODE == MODE_JVP) ? 16 : 8;   // warps per CTA
+    static constexpr int MINB = 1;                                               // CTAs per SM
+    static constexpr bool HAS_B = (MODE == MODE_VJP || MODE == MODE_GN);         // adjoint sweep
+    static constexpr bool NF4 = (MODE == MODE_JVP || MODE == MODE_GN);           // 4-channel sweep A
+    static constexpr bool COMP_S = (MODE != MODE_FWD);                           // compensated A_i
+    static constexpr bool COMP_G = HAS_B;                                        // compensated G
+};
+
+// ------------------------------------------------------------------------------------------ kernel
+template <int MODE, int MAXG>
+__global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MINB) proj_kernel(ProjArgs A)
+{
+    using TR = ModeTraits<MODE>;
+    constexpr int W = TR::W;
+    constexpr int NT = W * 32;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
+    unsigned char* const stage0 = smem + 128;   // stage buffer b at stage0 + b * stage_bytes
+    float2* wacc_all = reinterpret_cast<float2*>(smem + A.off_wacc);
+    float* rout = reinterpret_cast<float*>(smem + A.off_rout);      // [2R]
+    float2* gsh = reinterpret_cast<float2*>(smem + A.off_gsh);      // [R] (G, Gc)
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t Ttot = static_cast<int64_t>(A.B) * A.n_ab;
+    const int C = gridDim.x, c = blockIdx.x;
+    const int64_t t0 = static_cast<int64_t>(c) * Ttot / C, t1 = static_cast<int64_t>(c + 1) * Ttot / C;
+    const int ns_task = A.passesA * A.nbA + (TR::HAS_B ? A.passesB * A.nbB : 0);
+    const int64_t n_stages = (t1 - t0) * ns_task;
+    if (n_stages == 0) return;
+
+    const int P = A.P, R = A.R, J = A.J;
+    const int RB1 = A.RbB + 1;
+    float2* wacc = wacc_all + static_cast<size_t>(warp) * RB1 * P;
+    if (TR::HAS_B) {
+        float4* z = reinterpret_cast<float4*>(wacc_all);
+        const int n4 = W * RB1 * P / 2;
+        for (int k = tid; k < n4; k += NT) z[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (tid == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        issue_stage<MODE>(A, t0, ns_task, 0, stage0, &mbar[0]);
+        if (n_stages > 1) issue_stage<MODE>(A, t0, ns_task, 1, stage0 + A.stage_bytes, &mbar[1]);
+    }
+    int64_t s = 0;   // global stage counter
+
+    const float cf = A.cf, ch = A.ch, dl = A.delta, dlh = 0.5f * A.delta;
+    const int64_t seg0 = task_info(A, t0).seg;
+
+    for (int64_t t = t0; t < t1; ++t) {
+        const TaskInfo ti = task_info(A, t);
+        const RayP* rays = A.rays + static_cast<size_t>(ti.ab) * R;
+        const int64_t dU = rays[0].dU, dV = rays[0].dV;
+        const bool first_in_seg = (t == t0) || (task_info(A, t - 1).seg != ti.seg);
+
+        // ======================================================= sweep A: forward (+ JVP) recurrence
+        // lanes own 32 adjacent rays (neighbouring lanes read neighbouring pixels: shared-memory broadcast)
+        for (int pass = 0; pass < A.passesA; ++pass) {
+            int rr[MAXG], ii[MAXG], ilo[MAXG];
+            int64_t uu[MAXG], vv[MAXG];
+            float S[MAXG], Sc[MAXG], g[MAXG], gc[MAXG], dS[MAXG], dg[MAXG], dgc[MAXG];
+#pragma unroll
+            for (int k = 0; k < MAXG; ++k) {
+                const int r = ((pass * MAXG + k) * W + warp) * 32 + lane;
+                rr[k] = r < R ? r : -1;
+                ii[k] = -1; ilo[k] = 0; uu[k] = 0; vv[k] = 0;
+                if (rr[k] >= 0) {
+                    const RayP rp = rays[rr[k]];
+                    ii[k] = rp.ihi; ilo[k] = rp.ilo;
+                    uu[k] = rp.U0 + static_cast<int64_t>(rp.ihi) * dU;
+                    vv[k] = rp.V0 + static_cast<int64_t>(rp.ihi) * dV;
+                }
+                S[k] = Sc[k] = g[k] = gc[k] = dS[k] = dg[k] = dgc[k] = 0.f;
+            }
+            for (int kb = 0; kb < A.nbA; ++kb) {
+                const int band = ti.dir > 0 ? A.nbA - 1 - kb : kb;
+                int r0, r1;
+                band_rows(band, A.RbA, P, r0, r1);
+                const int b = static_cast<int>(s & 1);
+                mbar_wait(&mbar[b], static_cast<uint32_t>((s >> 1) & 1));
+                const unsigned char* sb = stage0 + b * A.stage_bytes;
+#pragma unroll
+                for (int k = 0; k < MAXG; ++k) {
+                    int i = ii[k];
+                    int64_t u = uu[k], v = vv[k];
+                    int iv = hi32(v);
+                    if (i < ilo[k] || iv < r0 || iv >= r1) continue;
+                    float s_ = S[k], sc = Sc[k], gg = g[k], ggc = gc[k], ds = dS[k], dgg = dg[k], dgc_ = dgc[k];
+                    // software pipeline: the corners of sample i-1 are loaded before sample i is evaluated
+                    Px<TR::NF4> cur;
+                    load_px(cur, sb, (iv - r0) * P + hi32(u), P);
+                    float fu = frac23(u), fv = frac23(v);
+                    while (true) {
+                        const int i2 = i - 1;
+                        const int64_t u2 = u - dU, v2 = v - dV;
+                        const int iv2 = hi32(v2);
+                        const bool nxt = i2 >= ilo[k] && iv2 >= r0 && iv2 < r1;
+                        Px<TR::NF4> nx;
+                        float fu2 = 0.f, fv2 = 0.f;
+                        if (nxt) {
+                            load_px(nx, sb, (iv2 - r0) * P + hi32(u2), P);
+                            fu2 = frac23(u2);
+                            fv2 = frac23(v2);
+                        }
+                        float lam, mu, dlam = 0.f, dmu = 0.f;
+                        if (TR::NF4) {
+                            const Px<true>& q = reinterpret_cast<const Px<true>&>(cur);
+                            const float2 x = bilerp2(lo2(q.a), lo2(q.b), lo2(q.c), lo2(q.d), fu, fv);
+                            const float2 y = bilerp2(hi2(q.a), hi2(q.b), hi2(q.c), hi2(q.d), fu, fv);
+                            lam = x.x; mu = x.y; dlam = y.x; dmu = y.y;
+                        } else {
+                            const Px<false>& q = reinterpret_cast<const Px<false>&>(cur);
+                            const float2 x = bilerp2(q.a, q.b, q.c, q.d, fu, fv);
+                            lam = x.x; mu = x.y;
+                        }
+                        float E;
+                        if (TR::COMP_S) {
+                            E = ex2(fmaf(mu, ch, s_) - sc);      // exp(-Delta(mu_i/2 + sum_{k>i} mu_k))
+                            kahan(s_, sc, mu * cf);
+                        } else {
+                            E = ex2(fmaf(mu, ch, s_));
+                            s_ = fmaf(mu, cf, s_);
+                        }
+                        if (TR::COMP_G) kahan(gg, ggc, lam * E);
+                        else gg = fmaf(lam, E, gg);
+                        if (TR::NF4) {
+                            const float dA = fmaf(dmu, dlh, ds);   // Delta (dmu_i/2 + sum_{k>i} dmu_k)
+                            kahan(dgg, dgc_, fmaf(-lam, dA, dlam) * E);
+                            ds = fmaf(dmu, dl, ds);
+                        }
+                        i = i2;
+                        u = u2;
+                        v = v2;
+                        if (!nxt) break;
+                        cur = nx;
+                        fu = fu2;
+                        fv = fv2;
+                    }
+                    ii[k] = i; uu[k] = u; vv[k] = v;
+                    S[k] = s_; Sc[k] = sc; g[k] = gg; gc[k] = ggc; dS[k] = ds; dg[k] = dgg; dgc[k] = dgc_;
+                }
+                __syncthreads();   // stage buffer b consumed
+                if (tid == 0 && s + 2 < n_stages) issue_stage<MODE>(A, t0, ns_task, s + 2, stage0 + b * A.stage_bytes, &mbar[b]);
+                ++s;
+            }
+            // per-ray results of this pass
+#pragma unroll
+            for (int k = 0; k < MAXG; ++k) {
+                const int r = rr[k];
+                if (r < 0) continue;
+                if (MODE == MODE_FWD) rout[r] = A.delta * g[k];
+                if (MODE == MODE_JVP) { rout[r] = A.delta * g[k]; rout[R + r] = A.delta * (dg[k] - dgc[k]); }
+                if (MODE == MODE_VJP) gsh[r] = make_float2(g[k], gc[k]);
+                if (MODE == MODE_GN) { gsh[r] = make_float2(g[k], gc[k]); rout[r] = A.delta * (dg[k] - dgc[k]); }
+            }
+        }
+        __syncthreads();
+
+        if (!TR::HAS_B) {
+            // sub-ray weighting and coalesced sinogram store
+            const size_t obase = (static_cast<size_t>(ti.m) * A.n_ab + ti.ab) * A.n_det;
+            for (int d = tid; d < A.n_det; d += NT) {
+                float acc = 0.f, dacc = 0.f;
+                for (int j = 0; j < J; ++j) {
+                    const float wj = A.w[j];
+                    acc = fmaf(wj, rout[d * J + j], acc);
+                    if (MODE == MODE_JVP) dacc = fmaf(wj, rout[R + d * J + j], dacc);
+                }
+                if (A.y) A.y[obase + d] = acc;
+                if (MODE == MODE_JVP) A.dy[obase + d] = dacc;
+            }
+            continue;   // rout is rewritten only after the next task's first band barrier
+        }
+
+        // ======================================================= sweep B: adjoint scatter (VJP / GN)
+        const size_t wbase = (static_cast<size_t>(ti.m) * A.n_ab + ti.ab) * A.n_det;
+        float2* slot = A.slots + (static_cast<size_t>(c) * A.KS + static_cast<size_t>(ti.seg - seg0)) *
+                                     static_cast<size_t>(A.N) * A.Ns;
+        const int npairs = P >> 1;
+        for (int pass = 0; pass < A.passesB; ++pass) {
+            int ii[MAXG], ilo[MAXG];
+            int64_t uu[MAXG], vv[MAXG];
+            float S[MAXG], Sc[MAXG], Q[MAXG], Qc[MAXG], kl[MAXG], km[MAXG], Gs[MAXG], Gcs[MAXG];
+#pragma unroll
+            for (int k = 0; k < MAXG; ++k) {
+                const int grp = (pass * MAXG + k) * W + warp;
+                const int r = grp < A.n_groups ? A.groups[grp * 32 + lane] : -1;
+                ii[k] = -1; ilo[k] = 0; uu[k] = 0; vv[k] = 0;
+                kl[k] = km[k] = Gs[k] = Gcs[k] = 0.f;
+                S[k] = Sc[k] = Q[k] = Qc[k] = 0.f;
+                if (r >= 0) {
+                    const int d = r / J, j = r - d * J;
+                    float wd;
+                    if (MODE == MODE_GN) {
+                        wd = 0.f;
+                        for (int jj = 0; jj < J; ++jj) wd = fmaf(A.w[jj], rout[d * J + jj], wd);
+                    } else {
+                        wd = A.win[wbase + d];
+                    }
+                    const float wr = A.w[j] * wd;
+                    kl[k] = wr * A.delta;
+                    km[k] = -wr * A.delta * A.delta;
+                    const float2 G = gsh[r];
+                    Gs[k] = G.x; Gcs[k] = G.y;
+                    if (wr != 0.f) {
+                        const RayP rp = rays[r];
+                        ii[k] = rp.ihi; ilo[k] = rp.ilo;
+                        uu[k] = rp.U0 + static_cast<int64_t>(rp.ihi) * dU;
+                        vv[k] = rp.V0 + static_cast<int64_t>(rp.ihi) * dV;
+                    }
+                }
+            }
+            for (int kb = 0; kb < A.nbB; ++kb) {
+                const int band = ti.dir > 0 ? A.nbB - 1 - kb : kb;
+                int r0, r1;
+                band_rows(band, A.RbB, P, r0, r1);
+                const int rbase = r0 % RB1;
+                const int b = static_cast<int>(s & 1);
+                mbar_wait(&mbar[b], static_cast<uint32_t>((s >> 1) & 1));
+                const float2* sb = reinterpret_cast<const float2*>(stage0 + b * A.stage_bytes);
+#pragma unroll
+                for (int k = 0; k < MAXG; ++k) {
+                    int i = ii[k];
+                    if (i < ilo[k]) continue;
+                    int64_t u = uu[k], v = vv[k];
+                    float s_ = S[k], sc = Sc[k], q = Q[k], qc = Qc[k];
+                    const float kll = kl[k], kmm = km[k], G = Gs[k], Gc = Gcs[k];
+                    int iv = hi32(v);
+                    if (iv < r0 || iv >= r1) continue;
+                    Px<false> cur;
+                    int iu = hi32(u);
+                    load_px(cur, reinterpret_cast<const unsigned char*>(sb), (iv - r0) * P + iu, P);
+                    float fu = frac23(u), fv = frac23(v);
+                    while (true) {
+                        const int i2 = i - 1;
+                        const int64_t u2 = u - dU, v2 = v - dV;
+                        const int iv2 = hi32(v2), iu2 = hi32(u2);
+                        const bool nxt = i2 >= ilo[k] && iv2 >= r0 && iv2 < r1;
+                        Px<false> nx;
+                        float fu2 = 0.f, fv2 = 0.f;
+                        if (nxt) {
+                            load_px(nx, reinterpret_cast<const unsigned char*>(sb), (iv2 - r0) * P + iu2, P);
+                            fu2 = frac23(u2);
+                            fv2 = frac23(v2);
+                        }
+                        const float2 x = bilerp2(cur.a, cur.b, cur.c, cur.d, fu, fv);
+                        const float E = ex2(fmaf(x.y, ch, s_) - sc);
+                        const float le = x.x * E;
+                        const float al = kll * E;
+                        const float am = kmm * (((G - q) - (Gc - qc)) - 0.5f * le);
+                        kahan(q, qc, le);
+                        kahan(s_, sc, x.y * cf);
+                        // transposed bilinear weights into the warp-private ring (comb lanes: no overlap)
+                        const float2 av = make_float2(al, am);
+                        const float2 tv = __fmul2_rn(av, make_float2(fv, fv));         // row j0+1
+                        const float2 bv = __ffma2_rn(tv, make_float2(-1.f, -1.f), av); // row j0
+                        const float2 c11 = __fmul2_rn(tv, make_float2(fu, fu));
+                        const float2 c10 = __ffma2_rn(c11, make_float2(-1.f, -1.f), tv);
+                        const float2 c01 = __fmul2_rn(bv, make_float2(fu, fu));
+                        const float2 c00 = __ffma2_rn(c01, make_float2(-1.f, -1.f), bv);
+                        int s0 = iv - r0 + rbase;
+                        if (s0 >= RB1) s0 -= RB1;
+                        const int s1 = (s0 + 1 == RB1) ? 0 : s0 + 1;
+                        float2* a0 = wacc + s0 * P + iu;
+                        float2* a1 = wacc + s1 * P + iu;
+                        float2 t00 = a0[0], t01 = a0[1], t10 = a1[0], t11 = a1[1];
+                        a0[0] = make_float2(t00.x + c00.x, t00.y + c00.y);
+                        a0[1] = make_float2(t01.x + c01.x, t01.y + c01.y);
+                        a1[0] = make_float2(t10.x + c10.x, t10.y + c10.y);
+                        a1[1] = make_float2(t11.x + c11.x, t11.y + c11.y);
+                        i = i2;
+                        u = u2;
+                        v = v2;
+                        if (!nxt) break;
+                        cur = nx;
+                        iv = iv2;
+                        iu = iu2;
+                        fu = fu2;
+                        fv = fv2;
+                    }
+                    ii[k] = i; uu[k] = u; vv[k] = v;
+                    S[k] = s_; Sc[k] = sc; Q[k] = q; Qc[k] = qc;
+                }
+                __syncthreads();   // stage buffer b and every warp ring consumed
+                if (tid == 0 && s + 2 < n_stages) issue_stage<MODE>(A, t0, ns_task, s + 2, stage0 + b * A.stage_bytes, &mbar[b]);
+                ++s;
+                // flush the finished rows of the band (all rows on the pass's last band; otherwise all but
+                // the row shared with the next band in processing order) into the CTA's partial slot.
+                // Element (row, pair) is always handled by thread (row * npairs + pair) % NT, so successive
+                // flushes of one slot element are issued by one thread in program order: deterministic.
+                const bool last = kb == A.nbB - 1;
+                const int carry = last ? -1 : (ti.dir > 0 ? r0 : r1);
+                const bool store = first_in_seg && pass == 0;
+                for (int r = r0; r <= r1; ++r) {
+                    if (r == carry) continue;
+                    const int sr = (r - r0 + rbase) % RB1;
+                    int q0 = tid - (r * npairs) % NT;
+                    if (q0 < 0) q0 += NT;
+                    for (int q = q0; q < npairs; q += NT) {
+                        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                        for (int w = 0; w < W; ++w) {
+                            float4* e = reinterpret_cast<float4*>(wacc_all + (static_cast<size_t>(w) * RB1 + sr) * P) + q;
+                            const float4 x = *e;
+                            acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+                            *e = make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
+                        const int ir = r - kHalo, ic = 2 * q - kHalo;
+                        if (ir >= 0 && ir < A.N && ic >= 0 && ic < A.Ns) {
+                            float4* dst = reinterpret_cast<float4*>(slot + static_cast<size_t>(ir) * A.Ns + ic);
+                            if (store) *dst = acc;
+                            else atomicAdd(dst, acc);
+                        }
+                    }
+                }
+                __syncthreads();   // rings zeroed before the next band's scatter
+            }
+        }
+        // gsh / rout reuse by the next task happens after at least one more barrier
+    }
+}
+
+// ------------------------------------------------------------------------------------------ reduction
+// g[m][j][i] = sum over the class-0 chunks of member m, over the CTAs touching the chunk, of slot[j][i]
+//            + the same over the class-1 chunks of slot[i][j]   (transposed frame)
+// in fp64, chunks and CTAs in increasing order (deterministic); written as float2 (g_lam, g_mu) [B][N][N].
+__device__ __forceinline__ int cta_of_task(int64_t x, int64_t Ttot, int C)
+{
+    int c = static_cast<int>((x * C) / Ttot);
+    if (c > C - 1) c = C - 1;
+    while (c > 0 && static_cast<int64_t>(c) * Ttot / C > x) --c;
+    while (c + 1 < C && static_cast<int64_t>(c + 1) * Ttot / C <= x) ++c;
+    return c;
+}
+
+__global__ void reduce_slots_kernel(const float2* __restrict__ slots, float2* __restrict__ out, int N, int Ns,
+                                    int n_ab, int n_class0, int B, int C, int KS, int unused)
+{
+    (void)unused;
+    __shared__ double2 tile[32][33];
+    const int m = blockIdx.z;
+    const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
+    const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+    const int64_t Ttot = static_cast<int64_t>(B) * n_ab;
+    const size_t plane = static_cast<size_t>(N) * Ns;
+    const int nc0 = (n_class0 + kChunk - 1) / kChunk, nc1 = (n_ab - n_class0 + kChunk - 1) / kChunk;
+    double2 acc[4], accT[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[k] = accT[k] = make_double2(0.0, 0.0);
+    for (int local = 0; local < nc0 + nc1; ++local) {
+        const int cls = local >= nc0 ? 1 : 0;
+        const int64_t cbeg = static_cast<int64_t>(m) * n_ab + (cls ? n_class0 : 0);
+        const int64_t cend = static_cast<int64_t>(m) * n_ab + (cls ? n_ab : n_class0);
+        const int64_t first = cbeg + static_cast<int64_t>(cls ? local - nc0 : local) * kChunk;
+        const int64_t last = min(first + kChunk, cend) - 1;
+        const int64_t ch = static_cast<int64_t>(m) * (nc0 + nc1) + local;
+        const int c_lo = cta_of_task(first, Ttot, C), c_hi = cta_of_task(last, Ttot, C);
+        for (int c = c_lo; c <= c_hi; ++c) {
+            const int64_t tb = static_cast<int64_t>(c) * Ttot / C;
+            if (static_cast<int64_t>(c + 1) * Ttot / C == tb) continue;   // CTA without tasks (Ttot < C)
+            const float2* sl = slots + (static_cast<size_t>(c) * KS + (ch - chunk_of(tb, n_ab, n_class0))) * plane;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                // class 0: element (row j, col i) = (j0 + ty + 8k, i0 + tx)
+                // class 1: element (row i, col j) of the transposed slot = (i0 + ty + 8k, j0 + tx)
+                const int rr = (cls ? i0 : j0) + ty + 8 * k, cc = (cls ? j0 : i0) + tx;
+                if (rr < N && cc < N) {
+                    const float2 v = sl[static_cast<size_t>(rr) * Ns + cc];
+                    double2& a = cls ? accT[k] : acc[k];
+                    a.x += v.x;
+                    a.y += v.y;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) tile[ty + 8 * k][tx] = accT[k];   // tile[i - i0][j - j0]
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int j = j0 + ty + 8 * k, i = i0 + tx;
+        if (j < N && i < N) {
+            const double2 t = tile[tx][ty + 8 * k];
+            out[(static_cast<size_t>(m) * N + j) * N + i] =
+                make_float2(static_cast<float>(acc[k].x + t.x), static_cast<float>(acc[k].y + t.y));
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------ launcher
+template <int MODE>
+static cudaError_t launch_mode(int maxg, const ProjArgs& A, int grid, size_t smem, cudaStream_t s)
+{
+    const int block = ModeTraits<MODE>::W * 32;
+    switch (maxg) {
+    case 1: proj_kernel<MODE, 1><<<grid, block, smem, s>>>(A); break;
+    case 2: proj_kernel<MODE, 2><<<grid, block, smem, s>>>(A); break;
+    case 4: proj_kernel<MODE, 4><<<grid, block, smem, s>>>(A); break;
+    default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_proj(int mode, int maxg, const ProjArgs& A, int grid, size_t smem, cudaStream_t s)
+{
+    switch (mode) {
+    case MODE_FWD: return launch_mode<MODE_FWD>(maxg, A, grid, smem, s);
+    case MODE_JVP: return launch_mode<MODE_JVP>(maxg, A, grid, smem, s);
+    case MODE_VJP: return launch_mode<MODE_VJP>(maxg, A, grid, smem, s);
+    case MODE_GN: return launch_mode<MODE_GN>(maxg, A, grid, smem, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+int proj_warps(int mode) { return (mode == MODE_FWD || mode == MODE_JVP) ? 16 : 8; }
+int proj_ctas_per_sm(int mode) { (void)mode; return 1; }
+
+template <int MODE>
+static cudaError_t attr_mode(size_t smem)
+{
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(proj_kernel<MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    if ((e = cudaFuncSetAttribute(proj_kernel<MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
+    return cudaFuncSetAttribute(proj_kernel<MODE, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+cudaError_t set_proj_smem_limit(int mode, size_t smem)
+{
+    switch (mode) {
+    case MODE_FWD: return attr_mode<MODE_FWD>(smem);
+    case MODE_JVP: return attr_mode<MODE_JVP>(smem);
+    case MODE_VJP: return attr_mode<MODE_VJP>(smem);
+    case MODE_GN: return attr_mode<MODE_GN>(smem);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace pget
