@@ -20,7 +20,7 @@
  *       -- PAPER.md:160-180 eq:m-function, eq:LMA-step; PAPER.md:248 eq:rho_agreement
  *       -- inner solver: plain CG (reading Q12) instead of the paper's SGP.
  *
- * Parity pins: see tests/test_oracle_*.py (P1-P12 of SURVEY.md §8(c.4)).
+ * Parity pins: tests/test_oracle.py (P1-P12 of SURVEY.md §8(c.4)); DESIGN.md "Oracle".
  * Compile: gcc -O2 -fopenmp -ffp-contract=off -fPIC -shared (no fast-math).
  */
 #include <math.h>

@@ -87,7 +87,7 @@ ProjCfg proj_cfg(const Geometry& g, int mode)
     const bool nf4 = mode == MODE_JVP || mode == MODE_GN;
     const int ncgA = (g.R + 31) / 32;                 // sweep A: contiguous groups of 32 rays
     const int gpw = std::max((ncgA + W - 1) / W, hasB ? (g.n_groups + W - 1) / W : 0);
-    c.maxg = gpw <= 1 ? 1 : (gpw <= 2 ? 2 : 4);
+    c.maxg = gpw >= 2 ? 2 : 1;   // groups per warp per pass (register-resident ray state)
     c.passesA = std::max(1, (ncgA + W * c.maxg - 1) / (W * c.maxg));
     c.passesB = std::max(1, (g.n_groups + W * c.maxg - 1) / (W * c.maxg));
     const size_t per_sm = 233472;   // 228 KB of shared memory per SM

@@ -191,13 +191,161 @@ __device__ void issue_stage(const ProjArgs& A, int64_t t0, int ns_task, int64_t 
 
 template <int MODE>
 struct ModeTraits {
-    static constexpr int W = (MODE == MODE_FWD || MODE == MODE_JVP) ? 16 : 8;   // warps per CTA
-    static constexpr int MINB = 1;                                               // CTAs per SM
+    static constexpr int W = 8;                                                  // warps per CTA
+    static constexpr int MINB = MODE == MODE_FWD ? 3 : (MODE == MODE_JVP ? 2 : 1); // CTAs per SM
     static constexpr bool HAS_B = (MODE == MODE_VJP || MODE == MODE_GN);         // adjoint sweep
     static constexpr bool NF4 = (MODE == MODE_JVP || MODE == MODE_GN);           // 4-channel sweep A
     static constexpr bool COMP_S = (MODE != MODE_FWD);                           // compensated A_i
     static constexpr bool COMP_G = HAS_B;                                        // compensated G
 };
+
+// ------------------------------------------------------------------------------------------ walkers
+// One lane walks one ray through one staged band, detector end first.  The four bilinear corners of
+// sample i-1 are loaded before sample i is evaluated (software pipeline: the shared-memory latency of
+// the next sample overlaps the arithmetic of the current one).  Measured alternative (DESIGN.md
+// "Projector"): caching the corners across samples of one cell cut shared-memory wavefronts 3x but the
+// per-lane move logic doubled the issued instructions and lost, so every sample loads its corners.
+template <bool NF4>
+struct CornerT;
+template <>
+struct CornerT<true> {
+    using T = float4;
+};
+template <>
+struct CornerT<false> {
+    using T = float2;
+};
+
+struct StateA {
+    float s, sc, g, gc, ds, dg, dgc;
+};
+
+// Sweep A: forward (+ JVP) recurrence.
+template <int MODE>
+__device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int P, int r0, int r1, int ilo,
+                                       int64_t dU, int64_t dV, float cf, float ch, float dl, float dlh, int& i,
+                                       int64_t& u, int64_t& v, StateA& st)
+{
+    using TR = ModeTraits<MODE>;
+    using Cn = typename CornerT<TR::NF4>::T;
+    const int iv = hi32(v);
+    if (i < ilo || iv < r0 || iv >= r1) return;
+    const Cn* img = reinterpret_cast<const Cn*>(sb);
+    int o = (iv - r0) * P + hi32(u);
+    Cn q00 = img[o], q01 = img[o + 1], q10 = img[o + P], q11 = img[o + P + 1];
+    float fu = frac23(u), fv = frac23(v);
+    float s_ = st.s, sc = st.sc, gg = st.g, ggc = st.gc, ds = st.ds, dgg = st.dg, dgc_ = st.dgc;
+    while (true) {
+        const int i2 = i - 1;
+        const int64_t u2 = u - dU, v2 = v - dV;
+        const int iv2 = hi32(v2);
+        const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;
+        Cn n00, n01, n10, n11;
+        if (nxt) {
+            o = (iv2 - r0) * P + hi32(u2);
+            n00 = img[o]; n01 = img[o + 1]; n10 = img[o + P]; n11 = img[o + P + 1];
+        }
+        float lam, mu, dlam = 0.f, dmu = 0.f;
+        if constexpr (TR::NF4) {
+            const float2 x = bilerp2(lo2(q00), lo2(q01), lo2(q10), lo2(q11), fu, fv);
+            const float2 y = bilerp2(hi2(q00), hi2(q01), hi2(q10), hi2(q11), fu, fv);
+            lam = x.x; mu = x.y; dlam = y.x; dmu = y.y;
+        } else {
+            const float2 x = bilerp2(q00, q01, q10, q11, fu, fv);
+            lam = x.x; mu = x.y;
+        }
+        float E;
+        if constexpr (TR::COMP_S) {
+            E = ex2(fmaf(mu, ch, s_) - sc);      // exp(-Delta(mu_i/2 + sum_{k>i} mu_k))
+            kahan(s_, sc, mu * cf);
+        } else {
+            E = ex2(fmaf(mu, ch, s_));
+            s_ = fmaf(mu, cf, s_);
+        }
+        if constexpr (TR::COMP_G) kahan(gg, ggc, lam * E);
+        else gg = fmaf(lam, E, gg);
+        if constexpr (TR::NF4) {
+            const float dA = fmaf(dmu, dlh, ds);   // Delta (dmu_i/2 + sum_{k>i} dmu_k)
+            kahan(dgg, dgc_, fmaf(-lam, dA, dlam) * E);
+            ds = fmaf(dmu, dl, ds);
+        }
+        i = i2;
+        u = u2;
+        v = v2;
+        if (!nxt) break;
+        q00 = n00; q01 = n01; q10 = n10; q11 = n11;
+        fu = frac23(u);
+        fv = frac23(v);
+    }
+    st.s = s_; st.sc = sc; st.g = gg; st.gc = ggc; st.ds = ds; st.dg = dgg; st.dgc = dgc_;
+}
+
+struct StateB {
+    float s, sc, q, qc;
+};
+
+// Sweep B: per-sample adjoint weights scattered with the transposed bilinear weights into the warp's
+// ring of band rows (plain shared-memory read-modify-write: comb lanes never share a pixel).
+// (Measured alternative: summing consecutive same-cell samples in registers before the
+// read-modify-write was 6 % slower on config 2.)
+__device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* __restrict__ ring, int P, int r0,
+                                       int r1, int rbase, int RB1, int ilo, int64_t dU, int64_t dV, float cf,
+                                       float ch, float kll, float kmm, float G, float Gc, int& i, int64_t& u,
+                                       int64_t& v, StateB& st)
+{
+    int iv = hi32(v), iu = hi32(u);
+    if (i < ilo || iv < r0 || iv >= r1) return;
+    int o = (iv - r0) * P + iu;
+    float2 q00 = img[o], q01 = img[o + 1], q10 = img[o + P], q11 = img[o + P + 1];
+    float fu = frac23(u), fv = frac23(v);
+    float s_ = st.s, sc = st.sc, q = st.q, qc = st.qc;
+    while (true) {
+        const int i2 = i - 1;
+        const int64_t u2 = u - dU, v2 = v - dV;
+        const int iv2 = hi32(v2), iu2 = hi32(u2);
+        const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;
+        float2 n00, n01, n10, n11;
+        if (nxt) {
+            o = (iv2 - r0) * P + iu2;
+            n00 = img[o]; n01 = img[o + 1]; n10 = img[o + P]; n11 = img[o + P + 1];
+        }
+        // a_lam = w_r Delta E_i, a_mu = -w_r Delta^2 (G - Q_i - lam_i E_i / 2)
+        const float2 x = bilerp2(q00, q01, q10, q11, fu, fv);
+        const float E = ex2(fmaf(x.y, ch, s_) - sc);
+        const float le = x.x * E;
+        const float al = kll * E;
+        const float am = kmm * (((G - q) - (Gc - qc)) - 0.5f * le);
+        kahan(q, qc, le);
+        kahan(s_, sc, x.y * cf);
+        const float2 av = make_float2(al, am);
+        const float2 tv = __fmul2_rn(av, make_float2(fv, fv));         // row j0+1
+        const float2 bv = __ffma2_rn(tv, make_float2(-1.f, -1.f), av); // row j0
+        const float2 c11 = __fmul2_rn(tv, make_float2(fu, fu));
+        const float2 c10 = __ffma2_rn(c11, make_float2(-1.f, -1.f), tv);
+        const float2 c01 = __fmul2_rn(bv, make_float2(fu, fu));
+        const float2 c00 = __ffma2_rn(c01, make_float2(-1.f, -1.f), bv);
+        int s0 = iv - r0 + rbase;
+        if (s0 >= RB1) s0 -= RB1;
+        const int s1 = (s0 + 1 == RB1) ? 0 : s0 + 1;
+        float2* a0 = ring + s0 * P + iu;
+        float2* a1 = ring + s1 * P + iu;
+        const float2 t00 = a0[0], t01 = a0[1], t10 = a1[0], t11 = a1[1];
+        a0[0] = make_float2(t00.x + c00.x, t00.y + c00.y);
+        a0[1] = make_float2(t01.x + c01.x, t01.y + c01.y);
+        a1[0] = make_float2(t10.x + c10.x, t10.y + c10.y);
+        a1[1] = make_float2(t11.x + c11.x, t11.y + c11.y);
+        i = i2;
+        u = u2;
+        v = v2;
+        if (!nxt) break;
+        q00 = n00; q01 = n01; q10 = n10; q11 = n11;
+        iv = iv2;
+        iu = iu2;
+        fu = frac23(u);
+        fv = frac23(v);
+    }
+    st.s = s_; st.sc = sc; st.q = q; st.qc = qc;
+}
 
 // ------------------------------------------------------------------------------------------ kernel
 template <int MODE, int MAXG>
@@ -255,7 +403,7 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
         for (int pass = 0; pass < A.passesA; ++pass) {
             int rr[MAXG], ii[MAXG], ilo[MAXG];
             int64_t uu[MAXG], vv[MAXG];
-            float S[MAXG], Sc[MAXG], g[MAXG], gc[MAXG], dS[MAXG], dg[MAXG], dgc[MAXG];
+            StateA st[MAXG];
 #pragma unroll
             for (int k = 0; k < MAXG; ++k) {
                 const int r = ((pass * MAXG + k) * W + warp) * 32 + lane;
@@ -267,7 +415,7 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                     uu[k] = rp.U0 + static_cast<int64_t>(rp.ihi) * dU;
                     vv[k] = rp.V0 + static_cast<int64_t>(rp.ihi) * dV;
                 }
-                S[k] = Sc[k] = g[k] = gc[k] = dS[k] = dg[k] = dgc[k] = 0.f;
+                st[k] = StateA{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             }
             for (int kb = 0; kb < A.nbA; ++kb) {
                 const int band = ti.dir > 0 ? A.nbA - 1 - kb : kb;
@@ -277,65 +425,8 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                 mbar_wait(&mbar[b], static_cast<uint32_t>((s >> 1) & 1));
                 const unsigned char* sb = stage0 + b * A.stage_bytes;
 #pragma unroll
-                for (int k = 0; k < MAXG; ++k) {
-                    int i = ii[k];
-                    int64_t u = uu[k], v = vv[k];
-                    int iv = hi32(v);
-                    if (i < ilo[k] || iv < r0 || iv >= r1) continue;
-                    float s_ = S[k], sc = Sc[k], gg = g[k], ggc = gc[k], ds = dS[k], dgg = dg[k], dgc_ = dgc[k];
-                    // software pipeline: the corners of sample i-1 are loaded before sample i is evaluated
-                    Px<TR::NF4> cur;
-                    load_px(cur, sb, (iv - r0) * P + hi32(u), P);
-                    float fu = frac23(u), fv = frac23(v);
-                    while (true) {
-                        const int i2 = i - 1;
-                        const int64_t u2 = u - dU, v2 = v - dV;
-                        const int iv2 = hi32(v2);
-                        const bool nxt = i2 >= ilo[k] && iv2 >= r0 && iv2 < r1;
-                        Px<TR::NF4> nx;
-                        float fu2 = 0.f, fv2 = 0.f;
-                        if (nxt) {
-                            load_px(nx, sb, (iv2 - r0) * P + hi32(u2), P);
-                            fu2 = frac23(u2);
-                            fv2 = frac23(v2);
-                        }
-                        float lam, mu, dlam = 0.f, dmu = 0.f;
-                        if (TR::NF4) {
-                            const Px<true>& q = reinterpret_cast<const Px<true>&>(cur);
-                            const float2 x = bilerp2(lo2(q.a), lo2(q.b), lo2(q.c), lo2(q.d), fu, fv);
-                            const float2 y = bilerp2(hi2(q.a), hi2(q.b), hi2(q.c), hi2(q.d), fu, fv);
-                            lam = x.x; mu = x.y; dlam = y.x; dmu = y.y;
-                        } else {
-                            const Px<false>& q = reinterpret_cast<const Px<false>&>(cur);
-                            const float2 x = bilerp2(q.a, q.b, q.c, q.d, fu, fv);
-                            lam = x.x; mu = x.y;
-                        }
-                        float E;
-                        if (TR::COMP_S) {
-                            E = ex2(fmaf(mu, ch, s_) - sc);      // exp(-Delta(mu_i/2 + sum_{k>i} mu_k))
-                            kahan(s_, sc, mu * cf);
-                        } else {
-                            E = ex2(fmaf(mu, ch, s_));
-                            s_ = fmaf(mu, cf, s_);
-                        }
-                        if (TR::COMP_G) kahan(gg, ggc, lam * E);
-                        else gg = fmaf(lam, E, gg);
-                        if (TR::NF4) {
-                            const float dA = fmaf(dmu, dlh, ds);   // Delta (dmu_i/2 + sum_{k>i} dmu_k)
-                            kahan(dgg, dgc_, fmaf(-lam, dA, dlam) * E);
-                            ds = fmaf(dmu, dl, ds);
-                        }
-                        i = i2;
-                        u = u2;
-                        v = v2;
-                        if (!nxt) break;
-                        cur = nx;
-                        fu = fu2;
-                        fv = fv2;
-                    }
-                    ii[k] = i; uu[k] = u; vv[k] = v;
-                    S[k] = s_; Sc[k] = sc; g[k] = gg; gc[k] = ggc; dS[k] = ds; dg[k] = dgg; dgc[k] = dgc_;
-                }
+                for (int k = 0; k < MAXG; ++k)
+                    walk_a<MODE>(sb, P, r0, r1, ilo[k], dU, dV, cf, ch, dl, dlh, ii[k], uu[k], vv[k], st[k]);
                 __syncthreads();   // stage buffer b consumed
                 if (tid == 0 && s + 2 < n_stages) issue_stage<MODE>(A, t0, ns_task, s + 2, stage0 + b * A.stage_bytes, &mbar[b]);
                 ++s;
@@ -345,10 +436,10 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
             for (int k = 0; k < MAXG; ++k) {
                 const int r = rr[k];
                 if (r < 0) continue;
-                if (MODE == MODE_FWD) rout[r] = A.delta * g[k];
-                if (MODE == MODE_JVP) { rout[r] = A.delta * g[k]; rout[R + r] = A.delta * (dg[k] - dgc[k]); }
-                if (MODE == MODE_VJP) gsh[r] = make_float2(g[k], gc[k]);
-                if (MODE == MODE_GN) { gsh[r] = make_float2(g[k], gc[k]); rout[r] = A.delta * (dg[k] - dgc[k]); }
+                if (MODE == MODE_FWD) rout[r] = A.delta * st[k].g;
+                if (MODE == MODE_JVP) { rout[r] = A.delta * st[k].g; rout[R + r] = A.delta * (st[k].dg - st[k].dgc); }
+                if (MODE == MODE_VJP) gsh[r] = make_float2(st[k].g, st[k].gc);
+                if (MODE == MODE_GN) { gsh[r] = make_float2(st[k].g, st[k].gc); rout[r] = A.delta * (st[k].dg - st[k].dgc); }
             }
         }
         __syncthreads();
@@ -377,14 +468,15 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
         for (int pass = 0; pass < A.passesB; ++pass) {
             int ii[MAXG], ilo[MAXG];
             int64_t uu[MAXG], vv[MAXG];
-            float S[MAXG], Sc[MAXG], Q[MAXG], Qc[MAXG], kl[MAXG], km[MAXG], Gs[MAXG], Gcs[MAXG];
+            float kl[MAXG], km[MAXG], Gs[MAXG], Gcs[MAXG];
+            StateB st[MAXG];
 #pragma unroll
             for (int k = 0; k < MAXG; ++k) {
                 const int grp = (pass * MAXG + k) * W + warp;
                 const int r = grp < A.n_groups ? A.groups[grp * 32 + lane] : -1;
                 ii[k] = -1; ilo[k] = 0; uu[k] = 0; vv[k] = 0;
                 kl[k] = km[k] = Gs[k] = Gcs[k] = 0.f;
-                S[k] = Sc[k] = Q[k] = Qc[k] = 0.f;
+                st[k] = StateB{0.f, 0.f, 0.f, 0.f};
                 if (r >= 0) {
                     const int d = r / J, j = r - d * J;
                     float wd;
@@ -416,68 +508,9 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                 mbar_wait(&mbar[b], static_cast<uint32_t>((s >> 1) & 1));
                 const float2* sb = reinterpret_cast<const float2*>(stage0 + b * A.stage_bytes);
 #pragma unroll
-                for (int k = 0; k < MAXG; ++k) {
-                    int i = ii[k];
-                    if (i < ilo[k]) continue;
-                    int64_t u = uu[k], v = vv[k];
-                    float s_ = S[k], sc = Sc[k], q = Q[k], qc = Qc[k];
-                    const float kll = kl[k], kmm = km[k], G = Gs[k], Gc = Gcs[k];
-                    int iv = hi32(v);
-                    if (iv < r0 || iv >= r1) continue;
-                    Px<false> cur;
-                    int iu = hi32(u);
-                    load_px(cur, reinterpret_cast<const unsigned char*>(sb), (iv - r0) * P + iu, P);
-                    float fu = frac23(u), fv = frac23(v);
-                    while (true) {
-                        const int i2 = i - 1;
-                        const int64_t u2 = u - dU, v2 = v - dV;
-                        const int iv2 = hi32(v2), iu2 = hi32(u2);
-                        const bool nxt = i2 >= ilo[k] && iv2 >= r0 && iv2 < r1;
-                        Px<false> nx;
-                        float fu2 = 0.f, fv2 = 0.f;
-                        if (nxt) {
-                            load_px(nx, reinterpret_cast<const unsigned char*>(sb), (iv2 - r0) * P + iu2, P);
-                            fu2 = frac23(u2);
-                            fv2 = frac23(v2);
-                        }
-                        const float2 x = bilerp2(cur.a, cur.b, cur.c, cur.d, fu, fv);
-                        const float E = ex2(fmaf(x.y, ch, s_) - sc);
-                        const float le = x.x * E;
-                        const float al = kll * E;
-                        const float am = kmm * (((G - q) - (Gc - qc)) - 0.5f * le);
-                        kahan(q, qc, le);
-                        kahan(s_, sc, x.y * cf);
-                        // transposed bilinear weights into the warp-private ring (comb lanes: no overlap)
-                        const float2 av = make_float2(al, am);
-                        const float2 tv = __fmul2_rn(av, make_float2(fv, fv));         // row j0+1
-                        const float2 bv = __ffma2_rn(tv, make_float2(-1.f, -1.f), av); // row j0
-                        const float2 c11 = __fmul2_rn(tv, make_float2(fu, fu));
-                        const float2 c10 = __ffma2_rn(c11, make_float2(-1.f, -1.f), tv);
-                        const float2 c01 = __fmul2_rn(bv, make_float2(fu, fu));
-                        const float2 c00 = __ffma2_rn(c01, make_float2(-1.f, -1.f), bv);
-                        int s0 = iv - r0 + rbase;
-                        if (s0 >= RB1) s0 -= RB1;
-                        const int s1 = (s0 + 1 == RB1) ? 0 : s0 + 1;
-                        float2* a0 = wacc + s0 * P + iu;
-                        float2* a1 = wacc + s1 * P + iu;
-                        float2 t00 = a0[0], t01 = a0[1], t10 = a1[0], t11 = a1[1];
-                        a0[0] = make_float2(t00.x + c00.x, t00.y + c00.y);
-                        a0[1] = make_float2(t01.x + c01.x, t01.y + c01.y);
-                        a1[0] = make_float2(t10.x + c10.x, t10.y + c10.y);
-                        a1[1] = make_float2(t11.x + c11.x, t11.y + c11.y);
-                        i = i2;
-                        u = u2;
-                        v = v2;
-                        if (!nxt) break;
-                        cur = nx;
-                        iv = iv2;
-                        iu = iu2;
-                        fu = fu2;
-                        fv = fv2;
-                    }
-                    ii[k] = i; uu[k] = u; vv[k] = v;
-                    S[k] = s_; Sc[k] = sc; Q[k] = q; Qc[k] = qc;
-                }
+                for (int k = 0; k < MAXG; ++k)
+                    walk_b(sb, wacc, P, r0, r1, rbase, RB1, ilo[k], dU, dV, cf, ch, kl[k], km[k], Gs[k],
+                           Gcs[k], ii[k], uu[k], vv[k], st[k]);
                 __syncthreads();   // stage buffer b and every warp ring consumed
                 if (tid == 0 && s + 2 < n_stages) issue_stage<MODE>(A, t0, ns_task, s + 2, stage0 + b * A.stage_bytes, &mbar[b]);
                 ++s;
@@ -592,7 +625,6 @@ static cudaError_t launch_mode(int maxg, const ProjArgs& A, int grid, size_t sme
     switch (maxg) {
     case 1: proj_kernel<MODE, 1><<<grid, block, smem, s>>>(A); break;
     case 2: proj_kernel<MODE, 2><<<grid, block, smem, s>>>(A); break;
-    case 4: proj_kernel<MODE, 4><<<grid, block, smem, s>>>(A); break;
     default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
@@ -609,16 +641,15 @@ cudaError_t launch_proj(int mode, int maxg, const ProjArgs& A, int grid, size_t 
     return cudaErrorInvalidValue;
 }
 
-int proj_warps(int mode) { return (mode == MODE_FWD || mode == MODE_JVP) ? 16 : 8; }
-int proj_ctas_per_sm(int mode) { (void)mode; return 1; }
+int proj_warps(int mode) { (void)mode; return 8; }
+int proj_ctas_per_sm(int mode) { return mode == MODE_FWD ? 3 : (mode == MODE_JVP ? 2 : 1); }
 
 template <int MODE>
 static cudaError_t attr_mode(size_t smem)
 {
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(proj_kernel<MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
-    if ((e = cudaFuncSetAttribute(proj_kernel<MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
-    return cudaFuncSetAttribute(proj_kernel<MODE, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return cudaFuncSetAttribute(proj_kernel<MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
 cudaError_t set_proj_smem_limit(int mode, size_t smem)
