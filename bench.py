@@ -300,7 +300,8 @@ def main():
     dom = max(prof["ms"], key=lambda k: prof["ms"][k])
     n_launch = max(prof["launches"][dom], 1)
     per_launch_ms = prof["ms"][dom] / n_launch
-    units = nominal                                     # nominal samples per launch (one pass over all rays)
+    traced = g.info["n_samples_traced"]
+    units = traced                                      # samples one launch actually evaluates
     achieved_gbs = ALG_BYTES[dom] * units / (per_launch_ms * 1e-3) / 1e9
     sm_mhz = (clk or {}).get("sm_mhz") or 1965.0
     peak_gbs = SMEM_B_PER_CLK_SM * N_SM * sm_mhz * 1e6 / 1e9
@@ -330,7 +331,9 @@ def main():
             "config": {"workload": f"config {cfg.cid}: {cfg.lattice} phantom, N={cfg.n_px}, {cfg.n_angles} angles, "
                                    f"2x{cfg.n_det} det, J={cfg.n_subrays}, B={cfg.batch}; step = fwd + JVP + VJP + "
                                    f"1 LM iteration ({cfg.n_cg} CG, alpha={cfg.alpha}, beta=0, trial)",
-                       "nominal_samples_per_pass": nominal, "sample_passes_per_step": sample_passes,
+                       "nominal_samples_per_pass": nominal, "traced_samples_per_pass": traced,
+                       "angle_banks_merged": bool(g.info["angle_banks_merged"]),
+                       "sample_passes_per_step": sample_passes,
                        "l2": "flushed between timed steps (256 MiB write, outside the events)"},
             "per_op": {
                 "forward_samples_per_s": nominal * K / (phase["forward"] * 1e-3),

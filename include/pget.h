@@ -92,6 +92,12 @@ typedef struct {
     int32_t n_t;                /* unclipped samples per ray = 2 T / Delta                  */
     int32_t n_px, n_angles, n_banks, n_det, n_subrays, batch;
     double h, delta, T;
+    int64_t n_samples_traced;   /* samples the projector actually evaluates per pass: equal to
+                                   n_samples_nominal, or about half of it when duplicate angle-banks
+                                   are merged (even n_angles, 2 banks, bank1_shift = 0: the rays of
+                                   (a + n_angles/2, 1 - b) are those of (a, b))                  */
+    int32_t angle_banks_merged; /* 1 when that merging is active                                  */
+    int32_t pad_;
 } pget_geometry_info_t;
 
 /* Table ids for pget_geometry_export (bit-exact comparison with the oracle, pin P1). */

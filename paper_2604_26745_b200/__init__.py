@@ -42,7 +42,8 @@ class _Info(C.Structure):
     _fields_ = [("n_rays", C.c_int64), ("n_samples_nominal", C.c_int64), ("image_elems", C.c_int64),
                 ("sino_elems", C.c_int64), ("n_t", C.c_int32), ("n_px", C.c_int32), ("n_angles", C.c_int32),
                 ("n_banks", C.c_int32), ("n_det", C.c_int32), ("n_subrays", C.c_int32), ("batch", C.c_int32),
-                ("h", C.c_double), ("delta", C.c_double), ("T", C.c_double)]
+                ("h", C.c_double), ("delta", C.c_double), ("T", C.c_double), ("n_samples_traced", C.c_int64),
+                ("angle_banks_merged", C.c_int32), ("pad_", C.c_int32)]
 
 
 class GNStats(C.Structure):

@@ -28,7 +28,8 @@ def needs_build() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or needs_build():
         tmp = LIB + f".tmp{os.getpid()}"
-        cmd = [nvcc()] + NVCC_FLAGS + ["-o", tmp] + SRC
+        extra = os.environ.get("PGET_NVCC_EXTRA", "").split()   # experiments only (e.g. -DPGET_ABLATE=1)
+        cmd = [nvcc()] + NVCC_FLAGS + extra + ["-o", tmp] + SRC
         if verbose:
             print(" ".join(cmd))
         subprocess.check_call(cmd)

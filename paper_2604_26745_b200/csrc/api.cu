@@ -70,6 +70,7 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct ProjCfg {
     int maxg, passesA, passesB, RbA, RbB, nbA, nbB, grid, KS;
+    int n_parts, part_det[Geometry::kMaxParts + 1];
     size_t smem;
     int stage_bytes, off_wacc, off_rout, off_gsh;
 };
@@ -85,11 +86,24 @@ ProjCfg proj_cfg(const Geometry& g, int mode)
     const int W = proj_warps(mode), cps = proj_ctas_per_sm(mode);
     const bool hasB = mode == MODE_VJP || mode == MODE_GN;
     const bool nf4 = mode == MODE_JVP || mode == MODE_GN;
-    const int ncgA = (g.R + 31) / 32;                 // sweep A: contiguous groups of 32 rays
-    const int gpw = std::max((ncgA + W - 1) / W, hasB ? (g.n_groups + W - 1) / W : 0);
+    // ray parts (tasks = member x traced angle-bank x part): the JVP (2 CTAs per SM) splits angle-banks
+    // into detector ranges until every CTA has >= 4 tasks or 8 parts, so its static task ranges balance;
+    // the other modes trace whole angle-banks (FWD: <= 1 task per CTA; VJP/GN: see build_parts).
+    c.n_parts = 1;
+    if (mode == MODE_JVP) {
+        const int64_t per = static_cast<int64_t>(g.desc.batch) * g.n_tab, ctas = int64_t(g.sm_count) * cps;
+        while (c.n_parts < Geometry::kMaxParts && c.n_parts < g.desc.n_det && per * c.n_parts < 4 * ctas) ++c.n_parts;
+    }
+    for (int q = 0; q <= Geometry::kMaxParts; ++q)
+        c.part_det[q] = q <= c.n_parts ? static_cast<int>((int64_t(g.desc.n_det) * q) / c.n_parts) : g.desc.n_det;
+    int ncgA = 1;
+    for (int q = 0; q < c.n_parts; ++q)
+        ncgA = std::max(ncgA, ((c.part_det[q + 1] - c.part_det[q]) * g.desc.n_subrays + 31) / 32);
+    const int ncgB = std::max(1, g.n_groups);   // comb groups (one part)
+    const int gpw = std::max((ncgA + W - 1) / W, hasB ? (ncgB + W - 1) / W : 0);
     c.maxg = gpw >= 2 ? 2 : 1;   // groups per warp per pass (register-resident ray state)
     c.passesA = std::max(1, (ncgA + W * c.maxg - 1) / (W * c.maxg));
-    c.passesB = std::max(1, (g.n_groups + W * c.maxg - 1) / (W * c.maxg));
+    c.passesB = std::max(1, (ncgB + W * c.maxg - 1) / (W * c.maxg));
     const size_t per_sm = 233472;   // 228 KB of shared memory per SM
     const size_t budget = std::min<size_t>(g.smem_optin, per_sm / cps - 1024);
     const size_t rout_b = align128(2 * sizeof(float) * g.R), gsh_b = align128(sizeof(float2) * g.R);
@@ -114,13 +128,13 @@ ProjCfg proj_cfg(const Geometry& g, int mode)
     c.smem = c.off_gsh + gsh_b;
     c.grid = g.sm_count * cps;
     // KS: the most partial-slot chunks (chunk_of) one CTA's task range spans
-    const int64_t T = static_cast<int64_t>(g.desc.batch) * g.n_ab;
+    const int ntp = g.n_tab * c.n_parts, nc0p = g.n_class0 * c.n_parts;   // tasks per member, class-0 tasks
+    const int64_t T = static_cast<int64_t>(g.desc.batch) * ntp;
     c.KS = 1;
     for (int k = 0; k < c.grid; ++k) {
         const int64_t tb = static_cast<int64_t>(k) * T / c.grid, te = static_cast<int64_t>(k + 1) * T / c.grid;
         if (te > tb)
-            c.KS = std::max<int>(c.KS, static_cast<int>(chunk_of(te - 1, g.n_ab, g.n_class0) -
-                                                        chunk_of(tb, g.n_ab, g.n_class0) + 1));
+            c.KS = std::max<int>(c.KS, static_cast<int>(chunk_of(te - 1, ntp, nc0p) - chunk_of(tb, ntp, nc0p) + 1));
     }
     return c;
 }
@@ -142,6 +156,13 @@ ProjArgs base_args(const Geometry& g, const ProjCfg& c)
     A.J = g.desc.n_subrays;
     A.R = g.R;
     A.n_ab = g.n_ab;
+    A.n_tab = g.n_tab;
+    A.n_parts = c.n_parts;
+    for (int q = 0; q <= Geometry::kMaxParts; ++q) {
+        A.part_det[q] = c.part_det[q];
+        A.part_grp[q] = c.n_parts == 1 ? (q == 0 ? 0 : g.n_groups) : 0;   // comb groups only for one part
+    }
+    A.dup_half = g.dup ? g.desc.n_angles / 2 : 0;
     A.n_class0 = g.n_class0;
     A.B = g.desc.batch;
     A.n_groups = g.n_groups;
@@ -362,6 +383,9 @@ pget_status pget_geometry_info(pget_geometry h, pget_geometry_info_t* o)
     const pget_geometry_desc& d = g.desc;
     o->n_rays = static_cast<int64_t>(d.batch) * g.n_ab * g.R;
     o->n_samples_nominal = g.n_samples_nominal;
+    o->n_samples_traced = g.n_samples_traced;
+    o->angle_banks_merged = g.dup ? 1 : 0;
+    o->pad_ = 0;
     o->image_elems = static_cast<int64_t>(d.batch) * d.n_px * d.n_px;
     o->sino_elems = static_cast<int64_t>(d.batch) * g.n_ab * d.n_det;
     o->n_t = g.n_t;
@@ -463,7 +487,8 @@ static pget_status proj_adjoint(const Geometry& g, const WS& w, int mode, const 
     if (st) return st;
     const int N = g.desc.n_px;
     const dim3 grid((N + 31) / 32, (N + 31) / 32, g.desc.batch);
-    reduce_slots_kernel<<<grid, dim3(32, 8), 0, s>>>(w.slots, w.gacc, N, slot_pitch(g), g.n_ab, g.n_class0,
+    reduce_slots_kernel<<<grid, dim3(32, 8), 0, s>>>(w.slots, w.gacc, N, slot_pitch(g), g.n_tab * c.n_parts,
+                                                    g.n_class0 * c.n_parts,
                                                     g.desc.batch, c.grid, c.KS, 0); note();
     CK(cudaGetLastError());
     return PGET_OK;

@@ -39,15 +39,28 @@ struct Geometry {
     std::vector<double> angles, dirs, offsets, weights;
     std::vector<int32_t> clip;
     int64_t n_samples_nominal;
+    int64_t n_samples_traced = 0;
     // launch geometry
     int R;        // rays per angle-bank = n_det * J
     int n_ab;     // n_angles * n_banks
+    // Duplicate angle-banks: with an even number of angles, two banks and no bank-1 shift, the rays of
+    // (a + n_A/2, bank 1 - b) are those of (a, b) (phi differs by 2 pi; offsets equal), so only the
+    // angle-banks with a < n_A/2 are traced and their results are written / their weights merged
+    // for both.  dup == false traces every angle-bank.
+    bool dup = false;
+    int n_tab;    // angle-banks traced per batch member (n_ab / 2 when dup, else n_ab)
     int P;        // padded image side (rows = cols = P, even): N + 2 kHalo rounded up to even
     // orientation classes: class 0 = |dV| >= |dU| (image used as is), class 1 = transposed image
     std::vector<int8_t> orient;   // [n_ab]
-    std::vector<int32_t> task_ab; // [n_ab] angle-bank processing order: class 0 first, then class 1
+    std::vector<int32_t> task_ab; // [n_tab] traced angle-banks in processing order: class 0, then class 1
     int n_class0 = 0;
-    // comb ray groups: <= 32 rays whose offsets differ pairwise by >= comb_S rays (>= 2 sqrt2 px)
+    // ray parts: a task is (member, traced angle-bank, part); part p owns detectors
+    // [part_det[p], part_det[p+1]) so that the static task ranges of the persistent CTAs balance
+    static constexpr int kMaxParts = 8;
+    int n_parts = 1;
+    int part_det[kMaxParts + 1] = {0};
+    int part_grp[kMaxParts + 1] = {0};   // comb groups of part p: [part_grp[p], part_grp[p+1])
+    // comb groups: <= 32 rays of one part whose offsets differ pairwise by >= comb_S rays (>= 2 sqrt2 px)
     int comb_S = 1;
     int n_groups = 0;
     std::vector<int32_t> groups;  // [n_groups][32] ray index in the angle-bank, -1 = idle lane
@@ -71,4 +84,5 @@ namespace pget {
 // geometry.cpp
 pget_status build_geometry(const pget_geometry_desc* d, Geometry* g, std::string* err);
 void build_ray_params(const Geometry& g, std::vector<RayP>* rays);
+void build_parts(Geometry* g, int np);
 }  // namespace pget

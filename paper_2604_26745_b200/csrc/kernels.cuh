@@ -21,6 +21,11 @@ struct ProjArgs {
     float* y;               // [B][n_ab][n_det]
     float* dy;              // [B][n_ab][n_det]
     int N, Ns, P, n_det, J, R, n_ab, n_class0, B, n_groups, KS;
+    int n_tab;              // traced angle-banks per member
+    int n_parts;            // ray parts per angle-bank: tasks per member = n_tab * n_parts
+    int part_det[Geometry::kMaxParts + 1];   // detectors of part p: [part_det[p], part_det[p+1])
+    int part_grp[Geometry::kMaxParts + 1];   // comb groups of part p
+    int dup_half;           // n_angles / 2 when duplicate angle-banks are merged (geometry dup), else 0
     int RbA, RbB, nbA, nbB, passesA, passesB;   // sweep A: 32 adjacent rays per warp; sweep B: comb groups
     int stage_bytes, off_wacc, off_rout, off_gsh;   // dynamic shared memory layout (bytes)
     float delta;            // Delta
@@ -32,11 +37,11 @@ struct ProjArgs {
 // fp32 slot (so a slot sums at most kChunk angle-banks) and reduce_slots_kernel adds the slots in fp64.
 constexpr int kChunk = 16;
 
-__host__ __device__ inline int64_t chunk_of(int64_t t, int n_ab, int n_class0)
+__host__ __device__ inline int64_t chunk_of(int64_t t, int n_tab, int n_class0)
 {
-    const int64_t m = t / n_ab;
-    const int k = static_cast<int>(t - m * n_ab);
-    const int nc0 = (n_class0 + kChunk - 1) / kChunk, nc1 = (n_ab - n_class0 + kChunk - 1) / kChunk;
+    const int64_t m = t / n_tab;
+    const int k = static_cast<int>(t - m * n_tab);
+    const int nc0 = (n_class0 + kChunk - 1) / kChunk, nc1 = (n_tab - n_class0 + kChunk - 1) / kChunk;
     const int local = k < n_class0 ? k / kChunk : nc0 + (k - n_class0) / kChunk;
     return m * (nc0 + nc1) + local;
 }
@@ -51,7 +56,7 @@ __global__ void pack2_kernel(const float* lam, const float* mu, const float* sla
                              float2* outT, float* ut_lam, float* ut_mu, int N, int P, int B);
 __global__ void pack4_kernel(const float* lam, const float* mu, const float* dl, const float* dm, float4* out,
                              float4* outT, int N, int P, int B);
-__global__ void reduce_slots_kernel(const float2* slots, float2* out, int N, int Ns, int n_ab, int n_class0, int B,
+__global__ void reduce_slots_kernel(const float2* slots, float2* out, int N, int Ns, int n_tab, int n_class0, int B,
                                     int C, int KS, int unused);
 __global__ void finish_kernel(const float2* acc, const float* xl, const float* xm, float alpha, float beta,
                               float sign, float* outl, float* outm, const float* dotl, const float* dotm,

@@ -29,6 +29,10 @@
 #include "internal.h"
 #include "kernels.cuh"
 
+#ifndef PGET_ABLATE
+#define PGET_ABLATE 0   // performance experiments only (scripts/ablate.sh); 0 in every real build
+#endif
+
 namespace pget {
 
 // ------------------------------------------------------------------------------------------ helpers
@@ -133,20 +137,31 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 
 // ------------------------------------------------------------------------------------------ tasks
 struct TaskInfo {
-    int m, ab, cls, dir;
+    int m, ab, cls, dir, part;
     int64_t seg;   // partial-slot chunk id (chunk_of)
 };
 
 __device__ __forceinline__ TaskInfo task_info(const ProjArgs& A, int64_t t)
 {
     TaskInfo ti;
-    ti.m = static_cast<int>(t / A.n_ab);
-    const int k = static_cast<int>(t - static_cast<int64_t>(ti.m) * A.n_ab);
+    const int ntp = A.n_tab * A.n_parts;
+    ti.m = static_cast<int>(t / ntp);
+    const int kp = static_cast<int>(t - static_cast<int64_t>(ti.m) * ntp);
+    const int k = kp / A.n_parts;
+    ti.part = kp - k * A.n_parts;
     ti.ab = A.task_ab[k];
     ti.cls = k >= A.n_class0 ? 1 : 0;
-    ti.seg = chunk_of(t, A.n_ab, A.n_class0);
+    ti.seg = chunk_of(t, ntp, A.n_class0 * A.n_parts);
     ti.dir = A.rays[static_cast<size_t>(ti.ab) * A.R].dV > 0 ? 1 : -1;
     return ti;
+}
+
+// the angle-bank whose rays duplicate those of ab (a + n_A/2, bank 1 - b); ab itself without dup
+__device__ __forceinline__ int dup_of(const ProjArgs& A, int ab)
+{
+    if (!A.dup_half) return ab;
+    const int a = ab >> 1, b = ab & 1;
+    return (a + A.dup_half) * 2 + (1 - b);
 }
 
 __device__ __forceinline__ void band_rows(int band, int Rb, int P, int& r0, int& r1)
@@ -191,7 +206,7 @@ __device__ void issue_stage(const ProjArgs& A, int64_t t0, int ns_task, int64_t 
 
 template <int MODE>
 struct ModeTraits {
-    static constexpr int W = 8;                                                  // warps per CTA
+    static constexpr int W = (MODE == MODE_VJP || MODE == MODE_GN) ? 12 : 8;    // warps per CTA
     static constexpr int MINB = MODE == MODE_FWD ? 3 : (MODE == MODE_JVP ? 2 : 1); // CTAs per SM
     static constexpr bool HAS_B = (MODE == MODE_VJP || MODE == MODE_GN);         // adjoint sweep
     static constexpr bool NF4 = (MODE == MODE_JVP || MODE == MODE_GN);           // 4-channel sweep A
@@ -285,13 +300,15 @@ struct StateB {
 };
 
 // Sweep B: per-sample adjoint weights scattered with the transposed bilinear weights into the warp's
-// ring of band rows (plain shared-memory read-modify-write: comb lanes never share a pixel).
+// band accumulator (rows r0..r1; plain shared-memory read-modify-write: comb lanes never share a
+// pixel).  The accumulator reads of sample i are issued first and the corner loads of sample i-1
+// next, so both latencies overlap the arithmetic of sample i.
 // (Measured alternative: summing consecutive same-cell samples in registers before the
 // read-modify-write was 6 % slower on config 2.)
-__device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* __restrict__ ring, int P, int r0,
-                                       int r1, int rbase, int RB1, int ilo, int64_t dU, int64_t dV, float cf,
-                                       float ch, float kll, float kmm, float G, float Gc, int& i, int64_t& u,
-                                       int64_t& v, StateB& st)
+__device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* __restrict__ acc, int P, int r0,
+                                       int r1, int abase, int sP, int ilo, int64_t dU, int64_t dV, float cf, float ch,
+                                       float kll, float kmm, float G, float Gc, int& i, int64_t& u, int64_t& v,
+                                       StateB& st)
 {
     int iv = hi32(v), iu = hi32(u);
     if (i < ilo || iv < r0 || iv >= r1) return;
@@ -300,14 +317,18 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
     float fu = frac23(u), fv = frac23(v);
     float s_ = st.s, sc = st.sc, q = st.q, qc = st.qc;
     while (true) {
+        // accumulator row of iv: abase + (iv - r0) * sP (sP = +-P, see the kernel), column iu
+        float2* a0 = acc + (abase + (iv - r0) * sP + iu);
+        const float2 t00 = a0[0], t01 = a0[1], t10 = a0[sP], t11 = a0[sP + 1];
         const int i2 = i - 1;
         const int64_t u2 = u - dU, v2 = v - dV;
-        const int iv2 = hi32(v2), iu2 = hi32(u2);
+        const int iv2 = hi32(v2);
         const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;
         float2 n00, n01, n10, n11;
+        int o2 = o;
         if (nxt) {
-            o = (iv2 - r0) * P + iu2;
-            n00 = img[o]; n01 = img[o + 1]; n10 = img[o + P]; n11 = img[o + P + 1];
+            o2 = (iv2 - r0) * P + hi32(u2);  // iv, iu of sample i-1 are recomputed after the step
+            n00 = img[o2]; n01 = img[o2 + 1]; n10 = img[o2 + P]; n11 = img[o2 + P + 1];
         }
         // a_lam = w_r Delta E_i, a_mu = -w_r Delta^2 (G - Q_i - lam_i E_i / 2)
         const float2 x = bilerp2(q00, q01, q10, q11, fu, fv);
@@ -324,23 +345,22 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
         const float2 c10 = __ffma2_rn(c11, make_float2(-1.f, -1.f), tv);
         const float2 c01 = __fmul2_rn(bv, make_float2(fu, fu));
         const float2 c00 = __ffma2_rn(c01, make_float2(-1.f, -1.f), bv);
-        int s0 = iv - r0 + rbase;
-        if (s0 >= RB1) s0 -= RB1;
-        const int s1 = (s0 + 1 == RB1) ? 0 : s0 + 1;
-        float2* a0 = ring + s0 * P + iu;
-        float2* a1 = ring + s1 * P + iu;
-        const float2 t00 = a0[0], t01 = a0[1], t10 = a1[0], t11 = a1[1];
+#if PGET_ABLATE == 1   // experiment: no scatter (keeps the arithmetic alive through one store)
+        if (c00.x == 12345.f) a0[0] = make_float2(t00.x + c00.x + c01.x + c10.x + c11.x, c00.y + c01.y + c10.y + c11.y);
+#else
         a0[0] = make_float2(t00.x + c00.x, t00.y + c00.y);
         a0[1] = make_float2(t01.x + c01.x, t01.y + c01.y);
-        a1[0] = make_float2(t10.x + c10.x, t10.y + c10.y);
-        a1[1] = make_float2(t11.x + c11.x, t11.y + c11.y);
+        a0[sP] = make_float2(t10.x + c10.x, t10.y + c10.y);
+        a0[sP + 1] = make_float2(t11.x + c11.x, t11.y + c11.y);
+#endif
         i = i2;
         u = u2;
         v = v2;
         if (!nxt) break;
         q00 = n00; q01 = n01; q10 = n10; q11 = n11;
+        o = o2;
         iv = iv2;
-        iu = iu2;
+        iu = hi32(u);
         fu = frac23(u);
         fv = frac23(v);
     }
@@ -362,7 +382,7 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
     float2* gsh = reinterpret_cast<float2*>(smem + A.off_gsh);      // [R] (G, Gc)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t Ttot = static_cast<int64_t>(A.B) * A.n_ab;
+    const int64_t Ttot = static_cast<int64_t>(A.B) * A.n_tab * A.n_parts;
     const int C = gridDim.x, c = blockIdx.x;
     const int64_t t0 = static_cast<int64_t>(c) * Ttot / C, t1 = static_cast<int64_t>(c + 1) * Ttot / C;
     const int ns_task = A.passesA * A.nbA + (TR::HAS_B ? A.passesB * A.nbB : 0);
@@ -397,6 +417,8 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
         const RayP* rays = A.rays + static_cast<size_t>(ti.ab) * R;
         const int64_t dU = rays[0].dU, dV = rays[0].dV;
         const bool first_in_seg = (t == t0) || (task_info(A, t - 1).seg != ti.seg);
+        const int dlo = A.part_det[ti.part], dhi = A.part_det[ti.part + 1];
+        const int prl = dlo * J, prh = dhi * J;   // rays of this part
 
         // ======================================================= sweep A: forward (+ JVP) recurrence
         // lanes own 32 adjacent rays (neighbouring lanes read neighbouring pixels: shared-memory broadcast)
@@ -406,8 +428,8 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
             StateA st[MAXG];
 #pragma unroll
             for (int k = 0; k < MAXG; ++k) {
-                const int r = ((pass * MAXG + k) * W + warp) * 32 + lane;
-                rr[k] = r < R ? r : -1;
+                const int r = prl + ((pass * MAXG + k) * W + warp) * 32 + lane;
+                rr[k] = r < prh ? r : -1;
                 ii[k] = -1; ilo[k] = 0; uu[k] = 0; vv[k] = 0;
                 if (rr[k] >= 0) {
                     const RayP rp = rays[rr[k]];
@@ -447,7 +469,8 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
         if (!TR::HAS_B) {
             // sub-ray weighting and coalesced sinogram store
             const size_t obase = (static_cast<size_t>(ti.m) * A.n_ab + ti.ab) * A.n_det;
-            for (int d = tid; d < A.n_det; d += NT) {
+            const size_t obase2 = (static_cast<size_t>(ti.m) * A.n_ab + dup_of(A, ti.ab)) * A.n_det;
+            for (int d = dlo + tid; d < dhi; d += NT) {
                 float acc = 0.f, dacc = 0.f;
                 for (int j = 0; j < J; ++j) {
                     const float wj = A.w[j];
@@ -456,12 +479,17 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                 }
                 if (A.y) A.y[obase + d] = acc;
                 if (MODE == MODE_JVP) A.dy[obase + d] = dacc;
+                if (A.dup_half) {   // the duplicate angle-bank measures the same rays
+                    if (A.y) A.y[obase2 + d] = acc;
+                    if (MODE == MODE_JVP) A.dy[obase2 + d] = dacc;
+                }
             }
             continue;   // rout is rewritten only after the next task's first band barrier
         }
 
         // ======================================================= sweep B: adjoint scatter (VJP / GN)
         const size_t wbase = (static_cast<size_t>(ti.m) * A.n_ab + ti.ab) * A.n_det;
+        const size_t wbase2 = (static_cast<size_t>(ti.m) * A.n_ab + dup_of(A, ti.ab)) * A.n_det;
         float2* slot = A.slots + (static_cast<size_t>(c) * A.KS + static_cast<size_t>(ti.seg - seg0)) *
                                      static_cast<size_t>(A.N) * A.Ns;
         const int npairs = P >> 1;
@@ -472,8 +500,8 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
             StateB st[MAXG];
 #pragma unroll
             for (int k = 0; k < MAXG; ++k) {
-                const int grp = (pass * MAXG + k) * W + warp;
-                const int r = grp < A.n_groups ? A.groups[grp * 32 + lane] : -1;
+                const int grp = A.part_grp[ti.part] + (pass * MAXG + k) * W + warp;
+                const int r = grp < A.part_grp[ti.part + 1] ? A.groups[grp * 32 + lane] : -1;
                 ii[k] = -1; ilo[k] = 0; uu[k] = 0; vv[k] = 0;
                 kl[k] = km[k] = Gs[k] = Gcs[k] = 0.f;
                 st[k] = StateB{0.f, 0.f, 0.f, 0.f};
@@ -483,8 +511,10 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                     if (MODE == MODE_GN) {
                         wd = 0.f;
                         for (int jj = 0; jj < J; ++jj) wd = fmaf(A.w[jj], rout[d * J + jj], wd);
+                        if (A.dup_half) wd *= 2.f;   // (J p) of the duplicate rays is the same
                     } else {
                         wd = A.win[wbase + d];
+                        if (A.dup_half) wd += A.win[wbase2 + d];
                     }
                     const float wr = A.w[j] * wd;
                     kl[k] = wr * A.delta;
@@ -503,14 +533,17 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                 const int band = ti.dir > 0 ? A.nbB - 1 - kb : kb;
                 int r0, r1;
                 band_rows(band, A.RbB, P, r0, r1);
-                const int rbase = r0 % RB1;
                 const int b = static_cast<int>(s & 1);
                 mbar_wait(&mbar[b], static_cast<uint32_t>((s >> 1) & 1));
                 const float2* sb = reinterpret_cast<const float2*>(stage0 + b * A.stage_bytes);
+                // accumulator rows flip direction every band (even kb: local row r - r0; odd kb:
+                // r0 + RbB - r), so the row shared with the next band keeps its local row: no wrap, no copy
+                const bool flip = kb & 1;
+                const int abase = flip ? A.RbB * P : 0, sP = flip ? -P : P;
 #pragma unroll
                 for (int k = 0; k < MAXG; ++k)
-                    walk_b(sb, wacc, P, r0, r1, rbase, RB1, ilo[k], dU, dV, cf, ch, kl[k], km[k], Gs[k],
-                           Gcs[k], ii[k], uu[k], vv[k], st[k]);
+                    walk_b(sb, wacc, P, r0, r1, abase, sP, ilo[k], dU, dV, cf, ch, kl[k], km[k], Gs[k], Gcs[k],
+                           ii[k], uu[k], vv[k], st[k]);
                 __syncthreads();   // stage buffer b and every warp ring consumed
                 if (tid == 0 && s + 2 < n_stages) issue_stage<MODE>(A, t0, ns_task, s + 2, stage0 + b * A.stage_bytes, &mbar[b]);
                 ++s;
@@ -523,23 +556,23 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                 const bool store = first_in_seg && pass == 0;
                 for (int r = r0; r <= r1; ++r) {
                     if (r == carry) continue;
-                    const int sr = (r - r0 + rbase) % RB1;
+                    const int lr = flip ? r0 + A.RbB - r : r - r0;
                     int q0 = tid - (r * npairs) % NT;
                     if (q0 < 0) q0 += NT;
                     for (int q = q0; q < npairs; q += NT) {
-                        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                        float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                         for (int w = 0; w < W; ++w) {
-                            float4* e = reinterpret_cast<float4*>(wacc_all + (static_cast<size_t>(w) * RB1 + sr) * P) + q;
+                            float4* e = reinterpret_cast<float4*>(wacc_all + (static_cast<size_t>(w) * RB1 + lr) * P) + q;
                             const float4 x = *e;
-                            acc.x += x.x; acc.y += x.y; acc.z += x.z; acc.w += x.w;
+                            sum.x += x.x; sum.y += x.y; sum.z += x.z; sum.w += x.w;
                             *e = make_float4(0.f, 0.f, 0.f, 0.f);
                         }
                         const int ir = r - kHalo, ic = 2 * q - kHalo;
                         if (ir >= 0 && ir < A.N && ic >= 0 && ic < A.Ns) {
                             float4* dst = reinterpret_cast<float4*>(slot + static_cast<size_t>(ir) * A.Ns + ic);
-                            if (store) *dst = acc;
-                            else atomicAdd(dst, acc);
+                            if (store) *dst = sum;
+                            else atomicAdd(dst, sum);
                         }
                     }
                 }
@@ -565,6 +598,7 @@ __device__ __forceinline__ int cta_of_task(int64_t x, int64_t Ttot, int C)
 
 __global__ void reduce_slots_kernel(const float2* __restrict__ slots, float2* __restrict__ out, int N, int Ns,
                                     int n_ab, int n_class0, int B, int C, int KS, int unused)
+// (n_ab here is the number of traced angle-banks per member, ProjArgs::n_tab)
 {
     (void)unused;
     __shared__ double2 tile[32][33];
@@ -641,7 +675,7 @@ cudaError_t launch_proj(int mode, int maxg, const ProjArgs& A, int grid, size_t 
     return cudaErrorInvalidValue;
 }
 
-int proj_warps(int mode) { (void)mode; return 8; }
+int proj_warps(int mode) { return (mode == MODE_VJP || mode == MODE_GN) ? 12 : 8; }
 int proj_ctas_per_sm(int mode) { return mode == MODE_FWD ? 3 : (mode == MODE_JVP ? 2 : 1); }
 
 template <int MODE>

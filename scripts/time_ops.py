@@ -1,0 +1,40 @@
+"""Median device time (CUDA events) of each public op on one config: forward, JVP, VJP, GN apply."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2604_26745_b200 as pg  # noqa: E402
+import pget_data as P  # noqa: E402
+
+cid = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+gd = P.geometry_desc(cid)
+g = pg.Geometry(gd)
+dev = lambda x: torch.from_numpy(np.ascontiguousarray(x, np.float32)).cuda()
+lam, mu = map(dev, P.make_phantom(cid))
+dl, dm = map(dev, P.rod_directions(cid))
+y = pg.forward(g, lam, mu)
+ops = {
+    "forward": lambda: pg.forward(g, lam, mu, y=y),
+    "jvp": lambda: pg.jvp(g, lam, mu, dl, dm),
+    "vjp": lambda: pg.vjp(g, lam, mu, y),
+    "gn": lambda: pg.gn_apply(g, lam, mu, dl, dm, 1e-3, 0.0),
+}
+nom = g.info["n_samples_nominal"]
+out = {}
+for name, f in ops.items():
+    for _ in range(3):
+        f()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        f()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    out[name] = float(np.median(ts))
+print(f"cfg{cid}", " ".join(f"{k}={v:.4f}ms({nom / v / 1e6:.3g}Gs/s)" for k, v in out.items()), flush=True)

@@ -108,6 +108,8 @@ EDGE = [
          batch=1),   # 1183 rays per angle-bank: 2 rays per thread
     dict(n_px=300, n_angles=6, n_banks=2, n_det=37, n_subrays=1, subray_sigma=0.4, step_px=1.0, bank1_shift=0.0,
          batch=1),   # many bands
+    dict(n_px=20, n_angles=9, n_banks=2, n_det=13, n_subrays=4, subray_sigma=0.4, step_px=0.5, bank1_shift=0.0,
+         batch=2),   # odd n_angles: no duplicate angle-banks to merge
 ]
 
 
