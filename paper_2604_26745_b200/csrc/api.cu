@@ -71,6 +71,7 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 struct ProjCfg {
     int maxg, passesA, passesB, RbA, RbB, nbA, nbB, grid, KS;
     int n_parts, part_det[Geometry::kMaxParts + 1];
+    int G;   // fp64 partial images of the slot reduction (adjoint modes)
     size_t smem;
     int stage_bytes, off_wacc, off_rout, off_gsh;
 };
@@ -135,6 +136,13 @@ ProjCfg proj_cfg(const Geometry& g, int mode)
         const int64_t tb = static_cast<int64_t>(k) * T / c.grid, te = static_cast<int64_t>(k + 1) * T / c.grid;
         if (te > tb)
             c.KS = std::max<int>(c.KS, static_cast<int>(chunk_of(te - 1, ntp, nc0p) - chunk_of(tb, ntp, nc0p) + 1));
+    }
+    // slot reduction: enough (tile, member, chunk-group) blocks to fill the GPU twice
+    {
+        const int tiles = ((g.desc.n_px + 31) / 32) * ((g.desc.n_px + 31) / 32);
+        const int nch = (nc0p + kChunk - 1) / kChunk + (ntp - nc0p + kChunk - 1) / kChunk;
+        const int64_t want = (2LL * g.sm_count + int64_t(tiles) * g.desc.batch - 1) / (int64_t(tiles) * g.desc.batch);
+        c.G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, nch)));
     }
     return c;
 }
@@ -209,7 +217,7 @@ struct WS {
     float2* img2[2] = {nullptr, nullptr};
     float4* img4[2] = {nullptr, nullptr};
     float2* slots = nullptr;
-    float2* gacc = nullptr;   // [B][N][N] reduced (g_lam, g_mu)
+    double2* gacc = nullptr;  // [G][B][N][N] fp64 partial gradients (g_lam, g_mu), G = ProjCfg::G
     float *ysino = nullptr, *dysino = nullptr;
     float *bl = nullptr, *bm = nullptr, *zl = nullptr, *zm = nullptr, *pl = nullptr, *pm = nullptr;
     float *ql = nullptr, *qm = nullptr, *ul = nullptr, *um = nullptr;
@@ -242,7 +250,7 @@ WS carve(const Geometry& g, int op, char* base)
         const ProjCfg c = proj_cfg(g, MODE_VJP);   // VJP and GN share the grid and KS
         const size_t plane = static_cast<size_t>(g.desc.n_px) * slot_pitch(g);
         w.slots = reinterpret_cast<float2*>(take(static_cast<size_t>(c.grid) * c.KS * plane * sizeof(float2)));
-        w.gacc = reinterpret_cast<float2*>(take(n2 * sizeof(float2)));
+        w.gacc = reinterpret_cast<double2*>(take(static_cast<size_t>(c.G) * n2 * sizeof(double2)));
     }
     if (op == PGET_OP_GN_CG_STEP) {
         w.ysino = reinterpret_cast<float*>(take(ns * sizeof(float)));
@@ -486,10 +494,9 @@ static pget_status proj_adjoint(const Geometry& g, const WS& w, int mode, const 
     pget_status st = run_proj(g, mode, c, A, s);
     if (st) return st;
     const int N = g.desc.n_px;
-    const dim3 grid((N + 31) / 32, (N + 31) / 32, g.desc.batch);
+    const dim3 grid((N + 31) / 32, (N + 31) / 32, g.desc.batch * c.G);
     reduce_slots_kernel<<<grid, dim3(32, 8), 0, s>>>(w.slots, w.gacc, N, slot_pitch(g), g.n_tab * c.n_parts,
-                                                    g.n_class0 * c.n_parts,
-                                                    g.desc.batch, c.grid, c.KS, 0); note();
+                                                    g.n_class0 * c.n_parts, g.desc.batch, c.grid, c.KS, c.G); note();
     CK(cudaGetLastError());
     return PGET_OK;
 }
@@ -534,7 +541,7 @@ pget_status pget_vjp(pget_geometry h, const float* lam, const float* mu, const f
     if ((st = pack2(g, w, lam, mu, nullptr, nullptr, nullptr, nullptr, s))) return st;
     if ((st = proj_adjoint(g, w, MODE_VJP, wv, s))) return st;
     finish_kernel<<<dim3(vec_grid(static_cast<size_t>(N) * N), B), kVecThreads, 0, s>>>(
-        w.gacc, nullptr, nullptr, 0.f, 0.f, 1.f, g_lam, g_mu, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+        w.gacc, proj_cfg(g, MODE_VJP).G, nullptr, nullptr, 0.f, 0.f, 1.f, g_lam, g_mu, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
         nullptr, nullptr, nullptr, N); note();
     CK(cudaGetLastError());
     return PGET_OK;
@@ -557,7 +564,7 @@ pget_status pget_gn_apply(pget_geometry h, const float* lam, const float* mu, co
     if ((st = pack4(g, w, lam, mu, p_lam, p_mu, s))) return st;
     if ((st = proj_adjoint(g, w, MODE_GN, nullptr, s))) return st;
     finish_kernel<<<dim3(vec_grid(static_cast<size_t>(N) * N), B), kVecThreads, 0, s>>>(
-        w.gacc, p_lam, p_mu, alpha, beta, 1.f, q_lam, q_mu, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+        w.gacc, proj_cfg(g, MODE_GN).G, p_lam, p_mu, alpha, beta, 1.f, q_lam, q_mu, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
         nullptr, nullptr, nullptr, N); note();
     CK(cudaGetLastError());
     return PGET_OK;
@@ -583,6 +590,7 @@ pget_status pget_gn_cg_step(pget_geometry h, const float* lam, const float* mu, 
     double* P[8];
     for (int k = 0; k < 8; ++k) P[k] = w.part + static_cast<size_t>(k) * B * kNblk;
     const int sgrid = (B + 127) / 128;
+    const int Gv = proj_cfg(g, MODE_VJP).G, Gg = proj_cfg(g, MODE_GN).G;
 
     // 1-2: r = F(u) - y, 1/2||r||^2, ||Lu||^2   (u packed once for the whole iteration)
     if ((st = pack2(g, w, lam, mu, nullptr, nullptr, nullptr, nullptr, s))) return st;
@@ -592,7 +600,7 @@ pget_status pget_gn_cg_step(pget_geometry h, const float* lam, const float* mu, 
     CK(cudaGetLastError());
     // 3: b = -(J^T r + alpha L^T L u); z = p = b; s = 0; ||b||^2
     if ((st = proj_adjoint(g, w, MODE_VJP, w.ysino, s))) return st;
-    finish_kernel<<<vg, kVecThreads, 0, s>>>(w.gacc, lam, mu, alpha, 0.f, -1.f, w.bl, w.bm, w.bl, w.bm, P[2], w.zl,
+    finish_kernel<<<vg, kVecThreads, 0, s>>>(w.gacc, Gv, lam, mu, alpha, 0.f, -1.f, w.bl, w.bm, w.bl, w.bm, P[2], w.zl,
                                             w.zm, w.pl, w.pm, s_lam, s_mu, N); note();
     CK(cudaGetLastError());
     scalar_kernel<<<sgrid, 128, 0, s>>>(SC_INIT, 0, P[0], P[1], P[2], kNblk, w.cg, stats, B, alpha, beta); note();
@@ -601,7 +609,7 @@ pget_status pget_gn_cg_step(pget_geometry h, const float* lam, const float* mu, 
     for (int k = 0; k < n_cg; ++k) {
         if ((st = pack4(g, w, lam, mu, w.pl, w.pm, s))) return st;
         if ((st = proj_adjoint(g, w, MODE_GN, nullptr, s))) return st;
-        finish_kernel<<<vg, kVecThreads, 0, s>>>(w.gacc, w.pl, w.pm, alpha, beta, 1.f, w.ql, w.qm, w.pl, w.pm, P[3],
+        finish_kernel<<<vg, kVecThreads, 0, s>>>(w.gacc, Gg, w.pl, w.pm, alpha, beta, 1.f, w.ql, w.qm, w.pl, w.pm, P[3],
                                                 nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, N); note();
         scalar_kernel<<<sgrid, 128, 0, s>>>(SC_GAMMA, k, P[3], nullptr, nullptr, kNblk, w.cg, stats, B, alpha, beta); note();
         cg_update1_kernel<<<vg, kVecThreads, 0, s>>>(s_lam, s_mu, w.zl, w.zm, w.pl, w.pm, w.ql, w.qm, w.cg, P[4], n2); note();

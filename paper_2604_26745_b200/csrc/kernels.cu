@@ -100,7 +100,7 @@ __device__ __forceinline__ float lap2_at(const float* __restrict__ x, int N, int
 //   grad mode (VJP out):  alpha = beta = 0, sign = 1, dotv = NULL
 //   b = -(J^T r + alpha L^T L u):  sign = -1, x = u, beta = 0, dotv = out (||b||^2), also copies
 //   q = J^T J p + alpha L^T L p + beta p:  sign = 1, x = p, dotv = p
-__global__ void finish_kernel(const float2* __restrict__ acc, const float* __restrict__ xl,
+__global__ void finish_kernel(const double2* __restrict__ part, int G, const float* __restrict__ xl,
                               const float* __restrict__ xm, float alpha, float beta, float sign,
                               float* outl, float* outm, const float* __restrict__ dotl,
                               const float* __restrict__ dotm, double* partial, float* copy1l, float* copy1m,
@@ -114,8 +114,13 @@ __global__ void finish_kernel(const float2* __restrict__ acc, const float* __res
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n2;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const int i = static_cast<int>(e % N), j = static_cast<int>(e / N);
-        const float2 a = acc[base + e];
-        float ol = a.x, om = a.y;
+        double2 a = part[base + e];   // the G fp64 partials of reduce_slots_kernel, in order
+        for (int g = 1; g < G; ++g) {
+            const double2 b = part[static_cast<size_t>(g) * gridDim.y * n2 + base + e];
+            a.x += b.x;
+            a.y += b.y;
+        }
+        float ol = static_cast<float>(a.x), om = static_cast<float>(a.y);
         if (xl) {
             const float* pl = xl + base;
             const float* pm = xm + base;

@@ -56,9 +56,9 @@ __global__ void pack2_kernel(const float* lam, const float* mu, const float* sla
                              float2* outT, float* ut_lam, float* ut_mu, int N, int P, int B);
 __global__ void pack4_kernel(const float* lam, const float* mu, const float* dl, const float* dm, float4* out,
                              float4* outT, int N, int P, int B);
-__global__ void reduce_slots_kernel(const float2* slots, float2* out, int N, int Ns, int n_tab, int n_class0, int B,
-                                    int C, int KS, int unused);
-__global__ void finish_kernel(const float2* acc, const float* xl, const float* xm, float alpha, float beta,
+__global__ void reduce_slots_kernel(const float2* slots, double2* part, int N, int Ns, int n_tp, int n_class0, int B,
+                                    int C, int KS, int G);
+__global__ void finish_kernel(const double2* part, int G, const float* xl, const float* xm, float alpha, float beta,
                               float sign, float* outl, float* outm, const float* dotl, const float* dotm,
                               double* partial, float* copy1l, float* copy1m, float* copy2l, float* copy2m,
                               float* zerol, float* zerom, int N);

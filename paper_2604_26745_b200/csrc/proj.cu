@@ -596,33 +596,35 @@ __device__ __forceinline__ int cta_of_task(int64_t x, int64_t Ttot, int C)
     return c;
 }
 
-__global__ void reduce_slots_kernel(const float2* __restrict__ slots, float2* __restrict__ out, int N, int Ns,
-                                    int n_ab, int n_class0, int B, int C, int KS, int unused)
-// (n_ab here is the number of traced angle-banks per member, ProjArgs::n_tab)
+__global__ void reduce_slots_kernel(const float2* __restrict__ slots, double2* __restrict__ part, int N, int Ns,
+                                    int n_tp, int n_class0, int B, int C, int KS, int G)
+// n_tp: tasks per member (traced angle-banks x parts), n_class0: class-0 tasks per member.
+// Block (tile, m * G + g) sums the chunks [g * nch / G, (g + 1) * nch / G) of member m into the fp64
+// partial part[g][m]; finish_kernel adds the G partials in order g = 0..G-1.
 {
-    (void)unused;
     __shared__ double2 tile[32][33];
-    const int m = blockIdx.z;
+    const int m = blockIdx.z / G, gq = blockIdx.z - m * G;
     const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
     const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
-    const int64_t Ttot = static_cast<int64_t>(B) * n_ab;
+    const int64_t Ttot = static_cast<int64_t>(B) * n_tp;
     const size_t plane = static_cast<size_t>(N) * Ns;
-    const int nc0 = (n_class0 + kChunk - 1) / kChunk, nc1 = (n_ab - n_class0 + kChunk - 1) / kChunk;
+    const int nc0 = (n_class0 + kChunk - 1) / kChunk, nc1 = (n_tp - n_class0 + kChunk - 1) / kChunk;
+    const int nch = nc0 + nc1;
     double2 acc[4], accT[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) acc[k] = accT[k] = make_double2(0.0, 0.0);
-    for (int local = 0; local < nc0 + nc1; ++local) {
+    for (int local = (gq * nch) / G; local < ((gq + 1) * nch) / G; ++local) {
         const int cls = local >= nc0 ? 1 : 0;
-        const int64_t cbeg = static_cast<int64_t>(m) * n_ab + (cls ? n_class0 : 0);
-        const int64_t cend = static_cast<int64_t>(m) * n_ab + (cls ? n_ab : n_class0);
+        const int64_t cbeg = static_cast<int64_t>(m) * n_tp + (cls ? n_class0 : 0);
+        const int64_t cend = static_cast<int64_t>(m) * n_tp + (cls ? n_tp : n_class0);
         const int64_t first = cbeg + static_cast<int64_t>(cls ? local - nc0 : local) * kChunk;
         const int64_t last = min(first + kChunk, cend) - 1;
-        const int64_t ch = static_cast<int64_t>(m) * (nc0 + nc1) + local;
+        const int64_t ch = static_cast<int64_t>(m) * nch + local;
         const int c_lo = cta_of_task(first, Ttot, C), c_hi = cta_of_task(last, Ttot, C);
         for (int c = c_lo; c <= c_hi; ++c) {
             const int64_t tb = static_cast<int64_t>(c) * Ttot / C;
             if (static_cast<int64_t>(c + 1) * Ttot / C == tb) continue;   // CTA without tasks (Ttot < C)
-            const float2* sl = slots + (static_cast<size_t>(c) * KS + (ch - chunk_of(tb, n_ab, n_class0))) * plane;
+            const float2* sl = slots + (static_cast<size_t>(c) * KS + (ch - chunk_of(tb, n_tp, n_class0))) * plane;
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 // class 0: element (row j, col i) = (j0 + ty + 8k, i0 + tx)
@@ -640,13 +642,13 @@ __global__ void reduce_slots_kernel(const float2* __restrict__ slots, float2* __
 #pragma unroll
     for (int k = 0; k < 4; ++k) tile[ty + 8 * k][tx] = accT[k];   // tile[i - i0][j - j0]
     __syncthreads();
+    double2* out = part + (static_cast<size_t>(gq) * B + m) * N * N;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int j = j0 + ty + 8 * k, i = i0 + tx;
         if (j < N && i < N) {
             const double2 t = tile[tx][ty + 8 * k];
-            out[(static_cast<size_t>(m) * N + j) * N + i] =
-                make_float2(static_cast<float>(acc[k].x + t.x), static_cast<float>(acc[k].y + t.y));
+            out[static_cast<size_t>(j) * N + i] = make_double2(acc[k].x + t.x, acc[k].y + t.y);
         }
     }
 }
