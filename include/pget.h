@@ -92,12 +92,16 @@ typedef struct {
     int32_t n_t;                /* unclipped samples per ray = 2 T / Delta                  */
     int32_t n_px, n_angles, n_banks, n_det, n_subrays, batch;
     double h, delta, T;
-    int64_t n_samples_traced;   /* samples the projector actually evaluates per pass: equal to
-                                   n_samples_nominal, or about half of it when duplicate angle-banks
-                                   are merged (even n_angles, 2 banks, bank1_shift = 0: the rays of
-                                   (a + n_angles/2, 1 - b) are those of (a, b))                  */
+    int64_t n_samples_traced;   /* line samples the forward / VJP / GN projector evaluates per pass:
+                                   n_samples_nominal, or about a quarter of it when angle_banks_merged:
+                                   with an even n_angles, 2 banks and bank1_shift = 0 the rays of
+                                   (a + n_angles/2, 1 - b) are those of (a, b), and bank 1 of angle a
+                                   traces the lines of bank 0 in the opposite direction, so one
+                                   traversal serves all four               */
     int32_t angle_banks_merged; /* 1 when that merging is active                                  */
     int32_t pad_;
+    int64_t n_samples_traced_jvp; /* the same for the JVP projector (both directions traced:
+                                     about half of nominal when merged)                          */
 } pget_geometry_info_t;
 
 /* Table ids for pget_geometry_export (bit-exact comparison with the oracle, pin P1). */

@@ -43,7 +43,7 @@ class _Info(C.Structure):
                 ("sino_elems", C.c_int64), ("n_t", C.c_int32), ("n_px", C.c_int32), ("n_angles", C.c_int32),
                 ("n_banks", C.c_int32), ("n_det", C.c_int32), ("n_subrays", C.c_int32), ("batch", C.c_int32),
                 ("h", C.c_double), ("delta", C.c_double), ("T", C.c_double), ("n_samples_traced", C.c_int64),
-                ("angle_banks_merged", C.c_int32), ("pad_", C.c_int32)]
+                ("angle_banks_merged", C.c_int32), ("pad_", C.c_int32), ("n_samples_traced_jvp", C.c_int64)]
 
 
 class GNStats(C.Structure):

@@ -72,6 +72,8 @@ struct ProjCfg {
     int maxg, passesA, passesB, RbA, RbB, nbA, nbB, grid, KS;
     int n_parts, part_det[Geometry::kMaxParts + 1];
     int G;   // fp64 partial images of the slot reduction (adjoint modes)
+    bool paired;          // line-paired projector (forward / VJP / GN of a dup geometry)
+    int ntab, nc0, toff;  // traced angle-banks per member, class-0 count, offset into d_task_ab
     size_t smem;
     int stage_bytes, off_wacc, off_rout, off_gsh;
 };
@@ -85,6 +87,10 @@ ProjCfg proj_cfg(const Geometry& g, int mode)
 {
     ProjCfg c;
     const int W = proj_warps(mode), cps = proj_ctas_per_sm(mode);
+    c.paired = g.dup && mode != MODE_JVP;
+    c.ntab = c.paired ? static_cast<int>(g.task_ab_p.size()) : g.n_tab;
+    c.nc0 = c.paired ? g.n_class0_p : g.n_class0;
+    c.toff = c.paired ? g.n_tab : 0;
     const bool hasB = mode == MODE_VJP || mode == MODE_GN;
     const bool nf4 = mode == MODE_JVP || mode == MODE_GN;
     // ray parts (tasks = member x traced angle-bank x part): the JVP (2 CTAs per SM) splits angle-banks
@@ -92,7 +98,7 @@ ProjCfg proj_cfg(const Geometry& g, int mode)
     // the other modes trace whole angle-banks (FWD: <= 1 task per CTA; VJP/GN: see build_parts).
     c.n_parts = 1;
     if (mode == MODE_JVP) {
-        const int64_t per = static_cast<int64_t>(g.desc.batch) * g.n_tab, ctas = int64_t(g.sm_count) * cps;
+        const int64_t per = static_cast<int64_t>(g.desc.batch) * c.ntab, ctas = int64_t(g.sm_count) * cps;
         while (c.n_parts < Geometry::kMaxParts && c.n_parts < g.desc.n_det && per * c.n_parts < 4 * ctas) ++c.n_parts;
     }
     for (int q = 0; q <= Geometry::kMaxParts; ++q)
@@ -107,7 +113,7 @@ ProjCfg proj_cfg(const Geometry& g, int mode)
     c.passesB = std::max(1, (ncgB + W * c.maxg - 1) / (W * c.maxg));
     const size_t per_sm = 233472;   // 228 KB of shared memory per SM
     const size_t budget = std::min<size_t>(g.smem_optin, per_sm / cps - 1024);
-    const size_t rout_b = align128(2 * sizeof(float) * g.R), gsh_b = align128(sizeof(float2) * g.R);
+    const size_t rout_b = align128(2 * sizeof(float) * g.R), gsh_b = align128(sizeof(float4) * g.R);
     const size_t fixed = 128 + rout_b + gsh_b;
     const size_t pixA = nf4 ? 16 : 8;
     int Rb = std::min(32, g.P - 1);
@@ -129,7 +135,7 @@ ProjCfg proj_cfg(const Geometry& g, int mode)
     c.smem = c.off_gsh + gsh_b;
     c.grid = g.sm_count * cps;
     // KS: the most partial-slot chunks (chunk_of) one CTA's task range spans
-    const int ntp = g.n_tab * c.n_parts, nc0p = g.n_class0 * c.n_parts;   // tasks per member, class-0 tasks
+    const int ntp = c.ntab * c.n_parts, nc0p = c.nc0 * c.n_parts;   // tasks per member, class-0 tasks
     const int64_t T = static_cast<int64_t>(g.desc.batch) * ntp;
     c.KS = 1;
     for (int k = 0; k < c.grid; ++k) {
@@ -155,7 +161,7 @@ ProjArgs base_args(const Geometry& g, const ProjCfg& c)
     std::memset(&A, 0, sizeof A);
     A.rays = g.d_rays;
     A.groups = g.d_groups;
-    A.task_ab = g.d_task_ab;
+    A.task_ab = g.d_task_ab + c.toff;
     A.w = g.d_w;
     A.N = g.desc.n_px;
     A.Ns = slot_pitch(g);
@@ -164,14 +170,14 @@ ProjArgs base_args(const Geometry& g, const ProjCfg& c)
     A.J = g.desc.n_subrays;
     A.R = g.R;
     A.n_ab = g.n_ab;
-    A.n_tab = g.n_tab;
+    A.n_tab = c.ntab;
     A.n_parts = c.n_parts;
     for (int q = 0; q <= Geometry::kMaxParts; ++q) {
         A.part_det[q] = c.part_det[q];
         A.part_grp[q] = c.n_parts == 1 ? (q == 0 ? 0 : g.n_groups) : 0;   // comb groups only for one part
     }
     A.dup_half = g.dup ? g.desc.n_angles / 2 : 0;
-    A.n_class0 = g.n_class0;
+    A.n_class0 = c.nc0;
     A.B = g.desc.batch;
     A.n_groups = g.n_groups;
     A.KS = c.KS;
@@ -206,7 +212,7 @@ pget_status run_proj(const Geometry& g, int mode, const ProjCfg& c, const ProjAr
         }
     }
     if (ea) cudaEventRecord(ea, s);
-    cudaError_t e = launch_proj(mode, c.maxg, A, c.grid, c.smem, s);
+    cudaError_t e = launch_proj(mode, c.maxg, c.paired, A, c.grid, c.smem, s);
     if (eb) cudaEventRecord(eb, s);
     if (e != cudaSuccess) return cuda_fail(e, "projector launch");
     return PGET_OK;
@@ -345,13 +351,15 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     build_ray_params(g, &rays);
     if (e == cudaSuccess) e = cudaMalloc(&g.d_rays, rays.size() * sizeof(RayP));
     if (e == cudaSuccess) e = cudaMalloc(&g.d_groups, g.groups.size() * sizeof(int32_t));
-    if (e == cudaSuccess) e = cudaMalloc(&g.d_task_ab, g.task_ab.size() * sizeof(int32_t));
+    std::vector<int32_t> tasks(g.task_ab);
+    tasks.insert(tasks.end(), g.task_ab_p.begin(), g.task_ab_p.end());
+    if (e == cudaSuccess) e = cudaMalloc(&g.d_task_ab, tasks.size() * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMalloc(&g.d_w, g.wf.size() * sizeof(float));
     if (e == cudaSuccess) e = cudaMemcpy(g.d_rays, rays.data(), rays.size() * sizeof(RayP), cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
         e = cudaMemcpy(g.d_groups, g.groups.data(), g.groups.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
-        e = cudaMemcpy(g.d_task_ab, g.task_ab.data(), g.task_ab.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+        e = cudaMemcpy(g.d_task_ab, tasks.data(), tasks.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(g.d_w, g.wf.data(), g.wf.size() * sizeof(float), cudaMemcpyHostToDevice);
     for (int mode = 0; mode < 4 && e == cudaSuccess; ++mode) {
         const size_t sm = proj_cfg(g, mode).smem;
@@ -391,7 +399,8 @@ pget_status pget_geometry_info(pget_geometry h, pget_geometry_info_t* o)
     const pget_geometry_desc& d = g.desc;
     o->n_rays = static_cast<int64_t>(d.batch) * g.n_ab * g.R;
     o->n_samples_nominal = g.n_samples_nominal;
-    o->n_samples_traced = g.n_samples_traced;
+    o->n_samples_traced = g.dup ? g.n_samples_traced_p : g.n_samples_traced;
+    o->n_samples_traced_jvp = g.n_samples_traced;
     o->angle_banks_merged = g.dup ? 1 : 0;
     o->pad_ = 0;
     o->image_elems = static_cast<int64_t>(d.batch) * d.n_px * d.n_px;
@@ -495,8 +504,8 @@ static pget_status proj_adjoint(const Geometry& g, const WS& w, int mode, const 
     if (st) return st;
     const int N = g.desc.n_px;
     const dim3 grid((N + 31) / 32, (N + 31) / 32, g.desc.batch * c.G);
-    reduce_slots_kernel<<<grid, dim3(32, 8), 0, s>>>(w.slots, w.gacc, N, slot_pitch(g), g.n_tab * c.n_parts,
-                                                    g.n_class0 * c.n_parts, g.desc.batch, c.grid, c.KS, c.G); note();
+    reduce_slots_kernel<<<grid, dim3(32, 8), 0, s>>>(w.slots, w.gacc, N, slot_pitch(g), c.ntab * c.n_parts,
+                                                    c.nc0 * c.n_parts, g.desc.batch, c.grid, c.KS, c.G); note();
     CK(cudaGetLastError());
     return PGET_OK;
 }

@@ -155,6 +155,22 @@ pget_status build_geometry(const pget_geometry_desc* d, Geometry* g, std::string
     g->n_samples_traced *= d->batch;
     g->n_class0 = 0;
     for (int ab = 0; ab < g->n_ab; ++ab) g->n_class0 += traced(ab) && g->orient[ab] == 0;
+    g->task_ab_p.clear();
+    g->n_class0_p = 0;
+    g->n_samples_traced_p = 0;
+    if (g->dup) {
+        for (int ab : g->task_ab)
+            if (ab % nB == 0) {
+                g->task_ab_p.push_back(ab);
+                g->n_class0_p += g->orient[ab] == 0;
+                for (int r = 0; r < g->R; ++r) {
+                    const size_t k = static_cast<size_t>(ab) * g->R + r;
+                    const int32_t lo = g->clip[2 * k], hi = g->clip[2 * k + 1];
+                    if (hi >= lo) g->n_samples_traced_p += hi - lo + 1;
+                }
+            }
+        g->n_samples_traced_p *= d->batch;
+    }
 
     {
         const double a = (p / J) / g->h;   // ray spacing in pixels

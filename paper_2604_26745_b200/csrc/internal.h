@@ -49,6 +49,12 @@ struct Geometry {
     // for both.  dup == false traces every angle-bank.
     bool dup = false;
     int n_tab;    // angle-banks traced per batch member (n_ab / 2 when dup, else n_ab)
+    // Line pairing (with dup): bank 1 of angle a traces the lines of bank 0 of angle a in the opposite
+    // direction (phi + pi, mirrored offsets), so the forward, VJP and GN projectors trace only the
+    // bank-0 angle-banks with a < n_A/2 and evaluate both directions per traversal.
+    std::vector<int32_t> task_ab_p;   // bank-0 traced angle-banks (class 0, then class 1); empty without dup
+    int n_class0_p = 0;
+    int64_t n_samples_traced_p = 0;
     int P;        // padded image side (rows = cols = P, even): N + 2 kHalo rounded up to even
     // orientation classes: class 0 = |dV| >= |dU| (image used as is), class 1 = transposed image
     std::vector<int8_t> orient;   // [n_ab]
@@ -67,7 +73,7 @@ struct Geometry {
     // device tables
     RayP* d_rays = nullptr;       // [n_ab][R] oriented frame
     int32_t* d_groups = nullptr;  // [n_groups][32]
-    int32_t* d_task_ab = nullptr; // [n_ab]
+    int32_t* d_task_ab = nullptr; // [n_tab + task_ab_p.size()]: task_ab then task_ab_p
     float* d_w = nullptr;         // [J] float weights
     std::vector<float> wf;        // host copy of the float weights
     int sm_count = 148;

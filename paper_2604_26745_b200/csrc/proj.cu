@@ -233,10 +233,15 @@ struct CornerT<false> {
 
 struct StateA {
     float s, sc, g, gc, ds, dg, dgc;
+    float p1, p1c, p2, p2c, p3, p3c;   // PAIRED: sums over e^{+A_i} for the reverse-direction ray
 };
 
-// Sweep A: forward (+ JVP) recurrence.
-template <int MODE>
+// Sweep A: forward (+ JVP) recurrence, detector end first.
+// PAIRED (line pairing): the same traversal also accumulates, for the ray of
+// the opposite bank on the same line (detector at the other end, optical depth A'_i = S - A_i),
+//   sum lam_i e^{A_i}                         (its forward:  e^{-S} * this),
+//   sum dlam_i e^{A_i}, sum lam_i dA_i e^{A_i}  (GN: its JVP = e^{-S}(p1 - dS p2 + p3), dA' = dS - dA).
+template <int MODE, bool PAIRED>
 __device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int P, int r0, int r1, int ilo,
                                        int64_t dU, int64_t dV, float cf, float ch, float dl, float dlh, int& i,
                                        int64_t& u, int64_t& v, StateA& st)
@@ -249,7 +254,7 @@ __device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int
     int o = (iv - r0) * P + hi32(u);
     Cn q00 = img[o], q01 = img[o + 1], q10 = img[o + P], q11 = img[o + P + 1];
     float fu = frac23(u), fv = frac23(v);
-    float s_ = st.s, sc = st.sc, gg = st.g, ggc = st.gc, ds = st.ds, dgg = st.dg, dgc_ = st.dgc;
+    StateA x_ = st;
     while (true) {
         const int i2 = i - 1;
         const int64_t u2 = u - dU, v2 = v - dV;
@@ -269,20 +274,32 @@ __device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int
             const float2 x = bilerp2(q00, q01, q10, q11, fu, fv);
             lam = x.x; mu = x.y;
         }
-        float E;
+        float arg;   // -log2(e) A_i
         if constexpr (TR::COMP_S) {
-            E = ex2(fmaf(mu, ch, s_) - sc);      // exp(-Delta(mu_i/2 + sum_{k>i} mu_k))
-            kahan(s_, sc, mu * cf);
+            arg = fmaf(mu, ch, x_.s) - x_.sc;
+            kahan(x_.s, x_.sc, mu * cf);
         } else {
-            E = ex2(fmaf(mu, ch, s_));
-            s_ = fmaf(mu, cf, s_);
+            arg = fmaf(mu, ch, x_.s);
+            x_.s = fmaf(mu, cf, x_.s);
         }
-        if constexpr (TR::COMP_G) kahan(gg, ggc, lam * E);
-        else gg = fmaf(lam, E, gg);
+        const float E = ex2(arg);      // exp(-Delta(mu_i/2 + sum_{k>i} mu_k))
+        if constexpr (TR::COMP_G) kahan(x_.g, x_.gc, lam * E);
+        else x_.g = fmaf(lam, E, x_.g);
+        float dA = 0.f;
         if constexpr (TR::NF4) {
-            const float dA = fmaf(dmu, dlh, ds);   // Delta (dmu_i/2 + sum_{k>i} dmu_k)
-            kahan(dgg, dgc_, fmaf(-lam, dA, dlam) * E);
-            ds = fmaf(dmu, dl, ds);
+            dA = fmaf(dmu, dlh, x_.ds);   // Delta (dmu_i/2 + sum_{k>i} dmu_k)
+            kahan(x_.dg, x_.dgc, fmaf(-lam, dA, dlam) * E);
+            x_.ds = fmaf(dmu, dl, x_.ds);
+        }
+        if constexpr (PAIRED && MODE == MODE_FWD) {
+            x_.p2 = fmaf(lam, ex2(-arg), x_.p2);
+        }
+        if constexpr (PAIRED && MODE == MODE_GN) {
+            const float eA = ex2(-arg);   // e^{A_i}
+            const float le = lam * eA;
+            kahan(x_.p1, x_.p1c, dlam * eA);
+            kahan(x_.p2, x_.p2c, le);
+            kahan(x_.p3, x_.p3c, le * dA);
         }
         i = i2;
         u = u2;
@@ -292,30 +309,39 @@ __device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int
         fu = frac23(u);
         fv = frac23(v);
     }
-    st.s = s_; st.sc = sc; st.g = gg; st.gc = ggc; st.ds = ds; st.dg = dgg; st.dgc = dgc_;
+    st = x_;
 }
 
 struct StateB {
-    float s, sc, q, qc;
+    float s, sc, q, qc, q1, q1c;
+};
+
+struct RayB {   // per-ray constants of sweep B
+    float kl, km, G, Gc;      // w_r Delta, -w_r Delta^2, G = sum lam E (compensated pair)
+    float kl1, km1, Sl, Slc;  // PAIRED: the same for the opposite-bank ray; -log2(e) S (pair)
 };
 
 // Sweep B: per-sample adjoint weights scattered with the transposed bilinear weights into the warp's
 // band accumulator (rows r0..r1; plain shared-memory read-modify-write: comb lanes never share a
 // pixel).  The accumulator reads of sample i are issued first and the corner loads of sample i-1
 // next, so both latencies overlap the arithmetic of sample i.
+//   a_lam(i) = w_r Delta E_i,  a_mu(i) = -w_r Delta^2 (G - Q_i - lam_i E_i / 2),  Q_i = sum_{k>i} lam_k E_k
+// PAIRED adds the opposite-bank ray of the same line (its detector at the low-i end):
+//   E'_i = e^{-(S - A_i)},  a_lam += w'_r Delta E'_i,  a_mu += -w'_r Delta^2 (Q'_i + lam_i E'_i / 2),
+//   Q'_i = sum_{k>i} lam_k E'_k  (samples farther from that detector, already visited).
 // (Measured alternative: summing consecutive same-cell samples in registers before the
 // read-modify-write was 6 % slower on config 2.)
+template <bool PAIRED>
 __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* __restrict__ acc, int P, int r0,
                                        int r1, int abase, int sP, int ilo, int64_t dU, int64_t dV, float cf, float ch,
-                                       float kll, float kmm, float G, float Gc, int& i, int64_t& u, int64_t& v,
-                                       StateB& st)
+                                       const RayB& rb, int& i, int64_t& u, int64_t& v, StateB& st)
 {
     int iv = hi32(v), iu = hi32(u);
     if (i < ilo || iv < r0 || iv >= r1) return;
     int o = (iv - r0) * P + iu;
     float2 q00 = img[o], q01 = img[o + 1], q10 = img[o + P], q11 = img[o + P + 1];
     float fu = frac23(u), fv = frac23(v);
-    float s_ = st.s, sc = st.sc, q = st.q, qc = st.qc;
+    StateB x_ = st;
     while (true) {
         // accumulator row of iv: abase + (iv - r0) * sP (sP = +-P, see the kernel), column iu
         float2* a0 = acc + (abase + (iv - r0) * sP + iu);
@@ -327,17 +353,24 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
         float2 n00, n01, n10, n11;
         int o2 = o;
         if (nxt) {
-            o2 = (iv2 - r0) * P + hi32(u2);  // iv, iu of sample i-1 are recomputed after the step
+            o2 = (iv2 - r0) * P + hi32(u2);
             n00 = img[o2]; n01 = img[o2 + 1]; n10 = img[o2 + P]; n11 = img[o2 + P + 1];
         }
-        // a_lam = w_r Delta E_i, a_mu = -w_r Delta^2 (G - Q_i - lam_i E_i / 2)
         const float2 x = bilerp2(q00, q01, q10, q11, fu, fv);
-        const float E = ex2(fmaf(x.y, ch, s_) - sc);
+        const float arg_hi = fmaf(x.y, ch, x_.s);
+        const float E = ex2(arg_hi - x_.sc);
         const float le = x.x * E;
-        const float al = kll * E;
-        const float am = kmm * (((G - q) - (Gc - qc)) - 0.5f * le);
-        kahan(q, qc, le);
-        kahan(s_, sc, x.y * cf);
+        float al = rb.kl * E;
+        float am = rb.km * (((rb.G - x_.q) - (rb.Gc - x_.qc)) - 0.5f * le);
+        if constexpr (PAIRED) {
+            const float E1 = ex2((rb.Sl - arg_hi) - (rb.Slc - x_.sc));   // e^{-(S - A_i)}
+            const float le1 = x.x * E1;
+            al = fmaf(rb.kl1, E1, al);
+            am = fmaf(rb.km1, (x_.q1 - x_.q1c) + 0.5f * le1, am);
+            kahan(x_.q1, x_.q1c, le1);
+        }
+        kahan(x_.q, x_.qc, le);
+        kahan(x_.s, x_.sc, x.y * cf);
         const float2 av = make_float2(al, am);
         const float2 tv = __fmul2_rn(av, make_float2(fv, fv));         // row j0+1
         const float2 bv = __ffma2_rn(tv, make_float2(-1.f, -1.f), av); // row j0
@@ -364,11 +397,11 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
         fu = frac23(u);
         fv = frac23(v);
     }
-    st.s = s_; st.sc = sc; st.q = q; st.qc = qc;
+    st = x_;
 }
 
 // ------------------------------------------------------------------------------------------ kernel
-template <int MODE, int MAXG>
+template <int MODE, int MAXG, bool PAIRED>
 __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MINB) proj_kernel(ProjArgs A)
 {
     using TR = ModeTraits<MODE>;
@@ -379,7 +412,7 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
     unsigned char* const stage0 = smem + 128;   // stage buffer b at stage0 + b * stage_bytes
     float2* wacc_all = reinterpret_cast<float2*>(smem + A.off_wacc);
     float* rout = reinterpret_cast<float*>(smem + A.off_rout);      // [2R]
-    float2* gsh = reinterpret_cast<float2*>(smem + A.off_gsh);      // [R] (G, Gc)
+    float4* gsh = reinterpret_cast<float4*>(smem + A.off_gsh);      // [R] (G, Gc, Sl, Slc)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t Ttot = static_cast<int64_t>(A.B) * A.n_tab * A.n_parts;
@@ -437,7 +470,7 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                     uu[k] = rp.U0 + static_cast<int64_t>(rp.ihi) * dU;
                     vv[k] = rp.V0 + static_cast<int64_t>(rp.ihi) * dV;
                 }
-                st[k] = StateA{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                st[k] = StateA{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             }
             for (int kb = 0; kb < A.nbA; ++kb) {
                 const int band = ti.dir > 0 ? A.nbA - 1 - kb : kb;
@@ -448,7 +481,7 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                 const unsigned char* sb = stage0 + b * A.stage_bytes;
 #pragma unroll
                 for (int k = 0; k < MAXG; ++k)
-                    walk_a<MODE>(sb, P, r0, r1, ilo[k], dU, dV, cf, ch, dl, dlh, ii[k], uu[k], vv[k], st[k]);
+                    walk_a<MODE, PAIRED>(sb, P, r0, r1, ilo[k], dU, dV, cf, ch, dl, dlh, ii[k], uu[k], vv[k], st[k]);
                 __syncthreads();   // stage buffer b consumed
                 if (tid == 0 && s + 2 < n_stages) issue_stage<MODE>(A, t0, ns_task, s + 2, stage0 + b * A.stage_bytes, &mbar[b]);
                 ++s;
@@ -458,10 +491,19 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
             for (int k = 0; k < MAXG; ++k) {
                 const int r = rr[k];
                 if (r < 0) continue;
-                if (MODE == MODE_FWD) rout[r] = A.delta * st[k].g;
-                if (MODE == MODE_JVP) { rout[r] = A.delta * st[k].g; rout[R + r] = A.delta * (st[k].dg - st[k].dgc); }
-                if (MODE == MODE_VJP) gsh[r] = make_float2(st[k].g, st[k].gc);
-                if (MODE == MODE_GN) { gsh[r] = make_float2(st[k].g, st[k].gc); rout[r] = A.delta * (st[k].dg - st[k].dgc); }
+                const StateA& q = st[k];
+                if (MODE == MODE_FWD) {
+                    rout[r] = A.delta * q.g;
+                    if (PAIRED) rout[R + r] = A.delta * ex2(q.s) * q.p2;   // e^{-S} sum lam e^{A}
+                }
+                if (MODE == MODE_JVP) { rout[r] = A.delta * q.g; rout[R + r] = A.delta * (q.dg - q.dgc); }
+                if (MODE == MODE_VJP || MODE == MODE_GN) gsh[r] = make_float4(q.g, q.gc, q.s, q.sc);
+                if (MODE == MODE_GN) {
+                    rout[r] = A.delta * (q.dg - q.dgc);
+                    if (PAIRED)   // opposite bank: e^{-S} (sum dlam e^A - dS sum lam e^A + sum lam dA e^A)
+                        rout[R + r] = A.delta * ex2(q.s - q.sc) *
+                                      (((q.p1 - q.p1c) + (q.p3 - q.p3c)) - q.ds * (q.p2 - q.p2c));
+                }
             }
         }
         __syncthreads();
@@ -470,18 +512,30 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
             // sub-ray weighting and coalesced sinogram store
             const size_t obase = (static_cast<size_t>(ti.m) * A.n_ab + ti.ab) * A.n_det;
             const size_t obase2 = (static_cast<size_t>(ti.m) * A.n_ab + dup_of(A, ti.ab)) * A.n_det;
+            const size_t pbase = (static_cast<size_t>(ti.m) * A.n_ab + ti.ab + 1) * A.n_det;       // bank 1
+            const size_t pbase2 = (static_cast<size_t>(ti.m) * A.n_ab + dup_of(A, ti.ab + 1)) * A.n_det;
             for (int d = dlo + tid; d < dhi; d += NT) {
                 float acc = 0.f, dacc = 0.f;
                 for (int j = 0; j < J; ++j) {
                     const float wj = A.w[j];
                     acc = fmaf(wj, rout[d * J + j], acc);
-                    if (MODE == MODE_JVP) dacc = fmaf(wj, rout[R + d * J + j], dacc);
+                    if (MODE == MODE_JVP || PAIRED) dacc = fmaf(wj, rout[R + d * J + j], dacc);
                 }
-                if (A.y) A.y[obase + d] = acc;
-                if (MODE == MODE_JVP) A.dy[obase + d] = dacc;
-                if (A.dup_half) {   // the duplicate angle-bank measures the same rays
-                    if (A.y) A.y[obase2 + d] = acc;
-                    if (MODE == MODE_JVP) A.dy[obase2 + d] = dacc;
+                if (MODE == MODE_JVP) {
+                    if (A.y) A.y[obase + d] = acc;
+                    A.dy[obase + d] = dacc;
+                    if (A.dup_half) {   // the duplicate angle-bank measures the same rays
+                        if (A.y) A.y[obase2 + d] = acc;
+                        A.dy[obase2 + d] = dacc;
+                    }
+                } else {
+                    A.y[obase + d] = acc;
+                    if (A.dup_half) A.y[obase2 + d] = acc;
+                    if (PAIRED) {   // bank 1, detector n-1-d: the same line traversed towards the other end
+                        const int dd = A.n_det - 1 - d;
+                        A.y[pbase + dd] = dacc;
+                        A.y[pbase2 + dd] = dacc;
+                    }
                 }
             }
             continue;   // rout is rewritten only after the next task's first band barrier
@@ -490,38 +544,42 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
         // ======================================================= sweep B: adjoint scatter (VJP / GN)
         const size_t wbase = (static_cast<size_t>(ti.m) * A.n_ab + ti.ab) * A.n_det;
         const size_t wbase2 = (static_cast<size_t>(ti.m) * A.n_ab + dup_of(A, ti.ab)) * A.n_det;
+        const size_t wpbase = (static_cast<size_t>(ti.m) * A.n_ab + ti.ab + 1) * A.n_det;   // PAIRED: bank 1
+        const size_t wpbase2 = (static_cast<size_t>(ti.m) * A.n_ab + dup_of(A, ti.ab + 1)) * A.n_det;
         float2* slot = A.slots + (static_cast<size_t>(c) * A.KS + static_cast<size_t>(ti.seg - seg0)) *
                                      static_cast<size_t>(A.N) * A.Ns;
         const int npairs = P >> 1;
         for (int pass = 0; pass < A.passesB; ++pass) {
             int ii[MAXG], ilo[MAXG];
             int64_t uu[MAXG], vv[MAXG];
-            float kl[MAXG], km[MAXG], Gs[MAXG], Gcs[MAXG];
+            RayB rb[MAXG];
             StateB st[MAXG];
 #pragma unroll
             for (int k = 0; k < MAXG; ++k) {
                 const int grp = A.part_grp[ti.part] + (pass * MAXG + k) * W + warp;
                 const int r = grp < A.part_grp[ti.part + 1] ? A.groups[grp * 32 + lane] : -1;
                 ii[k] = -1; ilo[k] = 0; uu[k] = 0; vv[k] = 0;
-                kl[k] = km[k] = Gs[k] = Gcs[k] = 0.f;
-                st[k] = StateB{0.f, 0.f, 0.f, 0.f};
+                rb[k] = RayB{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                st[k] = StateB{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
                 if (r >= 0) {
                     const int d = r / J, j = r - d * J;
-                    float wd;
+                    float wd = 0.f, wd1 = 0.f;
                     if (MODE == MODE_GN) {
-                        wd = 0.f;
-                        for (int jj = 0; jj < J; ++jj) wd = fmaf(A.w[jj], rout[d * J + jj], wd);
-                        if (A.dup_half) wd *= 2.f;   // (J p) of the duplicate rays is the same
+                        for (int jj = 0; jj < J; ++jj) {
+                            wd = fmaf(A.w[jj], rout[d * J + jj], wd);
+                            if (PAIRED) wd1 = fmaf(A.w[jj], rout[R + d * J + jj], wd1);
+                        }
+                        if (A.dup_half) { wd *= 2.f; wd1 *= 2.f; }   // (J p) of the duplicate rays is the same
                     } else {
                         wd = A.win[wbase + d];
                         if (A.dup_half) wd += A.win[wbase2 + d];
+                        if (PAIRED) wd1 = A.win[wpbase + A.n_det - 1 - d] + A.win[wpbase2 + A.n_det - 1 - d];
                     }
-                    const float wr = A.w[j] * wd;
-                    kl[k] = wr * A.delta;
-                    km[k] = -wr * A.delta * A.delta;
-                    const float2 G = gsh[r];
-                    Gs[k] = G.x; Gcs[k] = G.y;
-                    if (wr != 0.f) {
+                    const float wr = A.w[j] * wd, wr1 = A.w[j] * wd1;   // w_{J-1-j} = w_j
+                    const float4 G = gsh[r];
+                    rb[k] = RayB{wr * A.delta, -wr * A.delta * A.delta, G.x, G.y,
+                                 wr1 * A.delta, -wr1 * A.delta * A.delta, G.z, G.w};
+                    if (wr != 0.f || wr1 != 0.f) {
                         const RayP rp = rays[r];
                         ii[k] = rp.ihi; ilo[k] = rp.ilo;
                         uu[k] = rp.U0 + static_cast<int64_t>(rp.ihi) * dU;
@@ -542,8 +600,8 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                 const int abase = flip ? A.RbB * P : 0, sP = flip ? -P : P;
 #pragma unroll
                 for (int k = 0; k < MAXG; ++k)
-                    walk_b(sb, wacc, P, r0, r1, abase, sP, ilo[k], dU, dV, cf, ch, kl[k], km[k], Gs[k], Gcs[k],
-                           ii[k], uu[k], vv[k], st[k]);
+                    walk_b<PAIRED>(sb, wacc, P, r0, r1, abase, sP, ilo[k], dU, dV, cf, ch, rb[k], ii[k], uu[k], vv[k],
+                                   st[k]);
                 __syncthreads();   // stage buffer b and every warp ring consumed
                 if (tid == 0 && s + 2 < n_stages) issue_stage<MODE>(A, t0, ns_task, s + 2, stage0 + b * A.stage_bytes, &mbar[b]);
                 ++s;
@@ -655,24 +713,28 @@ __global__ void reduce_slots_kernel(const float2* __restrict__ slots, double2* _
 
 // ------------------------------------------------------------------------------------------ launcher
 template <int MODE>
-static cudaError_t launch_mode(int maxg, const ProjArgs& A, int grid, size_t smem, cudaStream_t s)
+static cudaError_t launch_mode(int maxg, bool paired, const ProjArgs& A, int grid, size_t smem, cudaStream_t s)
 {
     const int block = ModeTraits<MODE>::W * 32;
-    switch (maxg) {
-    case 1: proj_kernel<MODE, 1><<<grid, block, smem, s>>>(A); break;
-    case 2: proj_kernel<MODE, 2><<<grid, block, smem, s>>>(A); break;
-    default: return cudaErrorInvalidValue;
+    constexpr bool CP = MODE != MODE_JVP;   // the JVP is never line-paired
+    if (paired && CP) {
+        if (maxg == 1) proj_kernel<MODE, 1, CP><<<grid, block, smem, s>>>(A);
+        else proj_kernel<MODE, 2, CP><<<grid, block, smem, s>>>(A);
+    } else {
+        if (maxg == 1) proj_kernel<MODE, 1, false><<<grid, block, smem, s>>>(A);
+        else proj_kernel<MODE, 2, false><<<grid, block, smem, s>>>(A);
     }
     return cudaGetLastError();
 }
 
-cudaError_t launch_proj(int mode, int maxg, const ProjArgs& A, int grid, size_t smem, cudaStream_t s)
+cudaError_t launch_proj(int mode, int maxg, bool paired, const ProjArgs& A, int grid, size_t smem, cudaStream_t s)
 {
+    if (maxg != 1 && maxg != 2) return cudaErrorInvalidValue;
     switch (mode) {
-    case MODE_FWD: return launch_mode<MODE_FWD>(maxg, A, grid, smem, s);
-    case MODE_JVP: return launch_mode<MODE_JVP>(maxg, A, grid, smem, s);
-    case MODE_VJP: return launch_mode<MODE_VJP>(maxg, A, grid, smem, s);
-    case MODE_GN: return launch_mode<MODE_GN>(maxg, A, grid, smem, s);
+    case MODE_FWD: return launch_mode<MODE_FWD>(maxg, paired, A, grid, smem, s);
+    case MODE_JVP: return launch_mode<MODE_JVP>(maxg, paired, A, grid, smem, s);
+    case MODE_VJP: return launch_mode<MODE_VJP>(maxg, paired, A, grid, smem, s);
+    case MODE_GN: return launch_mode<MODE_GN>(maxg, paired, A, grid, smem, s);
     }
     return cudaErrorInvalidValue;
 }
@@ -683,9 +745,13 @@ int proj_ctas_per_sm(int mode) { return mode == MODE_FWD ? 3 : (mode == MODE_JVP
 template <int MODE>
 static cudaError_t attr_mode(size_t smem)
 {
+    constexpr bool CP = MODE != MODE_JVP;
+    const int v = static_cast<int>(smem);
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(proj_kernel<MODE, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))) return e;
-    return cudaFuncSetAttribute(proj_kernel<MODE, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if ((e = cudaFuncSetAttribute(proj_kernel<MODE, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, v))) return e;
+    if ((e = cudaFuncSetAttribute(proj_kernel<MODE, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, v))) return e;
+    if ((e = cudaFuncSetAttribute(proj_kernel<MODE, 1, CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, v))) return e;
+    return cudaFuncSetAttribute(proj_kernel<MODE, 2, CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
 }
 
 cudaError_t set_proj_smem_limit(int mode, size_t smem)
