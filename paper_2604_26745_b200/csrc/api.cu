@@ -13,6 +13,7 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "internal.h"
@@ -69,44 +70,32 @@ constexpr int kVecThreads = 256;
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct ProjCfg {
-    int maxg, passesA, passesB, RbA, RbB, nbA, nbB, grid, KS;
-    int n_parts, part_det[Geometry::kMaxParts + 1];
-    int G;   // fp64 partial images of the slot reduction (adjoint modes)
+    int kind;             // schedule: kSchedFwd / kSchedJvp / kSchedAdj
+    int maxg, passesA, passesB, RbA, RbB, nbA, nbB, grid;
+    int G;                // fp64 partial images of the slot reduction (adjoint modes)
     bool paired;          // line-paired projector (forward / VJP / GN of a dup geometry)
-    int ntab, nc0, toff;  // traced angle-banks per member, class-0 count, offset into d_task_ab
     size_t smem;
     int stage_bytes, off_wacc, off_rout, off_gsh;
 };
 
 size_t align128(size_t x) { return (x + 127) & ~size_t(127); }
 
+int sched_kind(int mode) { return mode == MODE_FWD ? kSchedFwd : (mode == MODE_JVP ? kSchedJvp : kSchedAdj); }
+
 // Launch configuration of the projector for `mode`: warps and CTAs per SM
-// are fixed per mode; the band height is the largest (<= 32 rows) whose double-buffered stage, the
-// warp rings (adjoint modes) and the per-ray arrays fit the per-CTA shared-memory budget.
+// are fixed per mode, the task schedule is the handle's (schedule.cpp); the band height is the
+// largest (<= 32 rows) whose double-buffered stage, the warp accumulators (adjoint modes) and the
+// per-ray arrays fit the per-CTA shared-memory budget.
 ProjCfg proj_cfg(const Geometry& g, int mode)
 {
     ProjCfg c;
     const int W = proj_warps(mode), cps = proj_ctas_per_sm(mode);
+    c.kind = sched_kind(mode);
+    const Schedule& S = g.sch[c.kind];
     c.paired = g.dup && mode != MODE_JVP;
-    c.ntab = c.paired ? static_cast<int>(g.task_ab_p.size()) : g.n_tab;
-    c.nc0 = c.paired ? g.n_class0_p : g.n_class0;
-    c.toff = c.paired ? g.n_tab : 0;
     const bool hasB = mode == MODE_VJP || mode == MODE_GN;
     const bool nf4 = mode == MODE_JVP || mode == MODE_GN;
-    // ray parts (tasks = member x traced angle-bank x part): the JVP (2 CTAs per SM) splits angle-banks
-    // into detector ranges until every CTA has >= 4 tasks or 8 parts, so its static task ranges balance;
-    // the other modes trace whole angle-banks (FWD: <= 1 task per CTA; VJP/GN: see build_parts).
-    c.n_parts = 1;
-    if (mode == MODE_JVP) {
-        const int64_t per = static_cast<int64_t>(g.desc.batch) * c.ntab, ctas = int64_t(g.sm_count) * cps;
-        while (c.n_parts < Geometry::kMaxParts && c.n_parts < g.desc.n_det && per * c.n_parts < 4 * ctas) ++c.n_parts;
-    }
-    for (int q = 0; q <= Geometry::kMaxParts; ++q)
-        c.part_det[q] = q <= c.n_parts ? static_cast<int>((int64_t(g.desc.n_det) * q) / c.n_parts) : g.desc.n_det;
-    int ncgA = 1;
-    for (int q = 0; q < c.n_parts; ++q)
-        ncgA = std::max(ncgA, ((c.part_det[q + 1] - c.part_det[q]) * g.desc.n_subrays + 31) / 32);
-    const int ncgB = std::max(1, g.n_groups);   // comb groups (one part)
+    const int ncgA = S.max_gA, ncgB = S.max_gB;
     const int gpw = std::max((ncgA + W - 1) / W, hasB ? (ncgB + W - 1) / W : 0);
     c.maxg = gpw >= 2 ? 2 : 1;   // groups per warp per pass (register-resident ray state)
     c.passesA = std::max(1, (ncgA + W * c.maxg - 1) / (W * c.maxg));
@@ -133,22 +122,12 @@ ProjCfg proj_cfg(const Geometry& g, int mode)
     c.off_rout = static_cast<int>(c.off_wacc + wacc_b);
     c.off_gsh = static_cast<int>(c.off_rout + rout_b);
     c.smem = c.off_gsh + gsh_b;
-    c.grid = g.sm_count * cps;
-    // KS: the most partial-slot chunks (chunk_of) one CTA's task range spans
-    const int ntp = c.ntab * c.n_parts, nc0p = c.nc0 * c.n_parts;   // tasks per member, class-0 tasks
-    const int64_t T = static_cast<int64_t>(g.desc.batch) * ntp;
-    c.KS = 1;
-    for (int k = 0; k < c.grid; ++k) {
-        const int64_t tb = static_cast<int64_t>(k) * T / c.grid, te = static_cast<int64_t>(k + 1) * T / c.grid;
-        if (te > tb)
-            c.KS = std::max<int>(c.KS, static_cast<int>(chunk_of(te - 1, ntp, nc0p) - chunk_of(tb, ntp, nc0p) + 1));
-    }
-    // slot reduction: enough (tile, member, chunk-group) blocks to fill the GPU twice
+    c.grid = S.C > 0 ? S.C : g.sm_count * cps;
+    // slot reduction: enough (tile, member, slot-range) blocks to fill the GPU twice
     {
         const int tiles = ((g.desc.n_px + 31) / 32) * ((g.desc.n_px + 31) / 32);
-        const int nch = (nc0p + kChunk - 1) / kChunk + (ntp - nc0p + kChunk - 1) / kChunk;
         const int64_t want = (2LL * g.sm_count + int64_t(tiles) * g.desc.batch - 1) / (int64_t(tiles) * g.desc.batch);
-        c.G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, nch)));
+        c.G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, std::max(1, S.max_slots_member))));
     }
     return c;
 }
@@ -159,9 +138,11 @@ ProjArgs base_args(const Geometry& g, const ProjCfg& c)
 {
     ProjArgs A;
     std::memset(&A, 0, sizeof A);
+    const Schedule& S = g.sch[c.kind];
     A.rays = g.d_rays;
-    A.groups = g.d_groups;
-    A.task_ab = g.d_task_ab + c.toff;
+    A.tasks = S.d_tasks;
+    A.cta_begin = S.d_cta_begin;
+    A.groups = S.d_groups;
     A.w = g.d_w;
     A.N = g.desc.n_px;
     A.Ns = slot_pitch(g);
@@ -170,17 +151,8 @@ ProjArgs base_args(const Geometry& g, const ProjCfg& c)
     A.J = g.desc.n_subrays;
     A.R = g.R;
     A.n_ab = g.n_ab;
-    A.n_tab = c.ntab;
-    A.n_parts = c.n_parts;
-    for (int q = 0; q <= Geometry::kMaxParts; ++q) {
-        A.part_det[q] = c.part_det[q];
-        A.part_grp[q] = c.n_parts == 1 ? (q == 0 ? 0 : g.n_groups) : 0;   // comb groups only for one part
-    }
     A.dup_half = g.dup ? g.desc.n_angles / 2 : 0;
-    A.n_class0 = c.nc0;
     A.B = g.desc.batch;
-    A.n_groups = g.n_groups;
-    A.KS = c.KS;
     A.RbA = c.RbA;
     A.RbB = c.RbB;
     A.nbA = c.nbA;
@@ -253,9 +225,10 @@ WS carve(const Geometry& g, int op, char* base)
         if (need4) w.img4[k] = reinterpret_cast<float4*>(take(img * sizeof(float4)));
     }
     if (needacc) {
-        const ProjCfg c = proj_cfg(g, MODE_VJP);   // VJP and GN share the grid and KS
+        const ProjCfg c = proj_cfg(g, MODE_VJP);   // VJP and GN share the adjoint schedule
         const size_t plane = static_cast<size_t>(g.desc.n_px) * slot_pitch(g);
-        w.slots = reinterpret_cast<float2*>(take(static_cast<size_t>(c.grid) * c.KS * plane * sizeof(float2)));
+        w.slots = reinterpret_cast<float2*>(take(static_cast<size_t>(std::max(1, g.sch[kSchedAdj].n_slots)) * plane *
+                                                 sizeof(float2)));
         w.gacc = reinterpret_cast<double2*>(take(static_cast<size_t>(c.G) * n2 * sizeof(double2)));
     }
     if (op == PGET_OP_GN_CG_STEP) {
@@ -304,6 +277,18 @@ int vec_grid(size_t n)
 
 }  // namespace
 
+void free_device_tables(Geometry* g)
+{
+    cudaFree(g->d_rays);
+    cudaFree(g->d_w);
+    g->d_rays = nullptr;
+    g->d_w = nullptr;
+    for (Schedule& S : g->sch) {
+        cudaFree(S.d_cta_begin); cudaFree(S.d_tasks); cudaFree(S.d_groups); cudaFree(S.d_red_off); cudaFree(S.d_red_slot);
+        S.d_cta_begin = nullptr; S.d_tasks = nullptr; S.d_groups = nullptr; S.d_red_off = nullptr; S.d_red_slot = nullptr;
+    }
+}
+
 // =========================================================================================== C ABI
 extern "C" {
 
@@ -350,16 +335,23 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     std::vector<RayP> rays;
     build_ray_params(g, &rays);
     if (e == cudaSuccess) e = cudaMalloc(&g.d_rays, rays.size() * sizeof(RayP));
-    if (e == cudaSuccess) e = cudaMalloc(&g.d_groups, g.groups.size() * sizeof(int32_t));
-    std::vector<int32_t> tasks(g.task_ab);
-    tasks.insert(tasks.end(), g.task_ab_p.begin(), g.task_ab_p.end());
-    if (e == cudaSuccess) e = cudaMalloc(&g.d_task_ab, tasks.size() * sizeof(int32_t));
+    for (int k = 0; k < 3 && e == cudaSuccess; ++k) {
+        const int mode = k == kSchedFwd ? MODE_FWD : (k == kSchedJvp ? MODE_JVP : MODE_VJP);
+        Schedule& S = g.sch[k];
+        build_schedule(g, k, g.sm_count * proj_ctas_per_sm(mode), &S);
+        auto up = [&](auto** dst, const auto& v) {
+            using T = typename std::remove_reference<decltype(v)>::type::value_type;
+            if (e == cudaSuccess) e = cudaMalloc(dst, std::max<size_t>(1, v.size()) * sizeof(T));
+            if (e == cudaSuccess && !v.empty()) e = cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+        };
+        up(&S.d_cta_begin, S.cta_begin);
+        up(&S.d_tasks, S.tasks);
+        up(&S.d_groups, S.groups);
+        up(&S.d_red_off, S.red_off);
+        up(&S.d_red_slot, S.red_slot);
+    }
     if (e == cudaSuccess) e = cudaMalloc(&g.d_w, g.wf.size() * sizeof(float));
     if (e == cudaSuccess) e = cudaMemcpy(g.d_rays, rays.data(), rays.size() * sizeof(RayP), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess)
-        e = cudaMemcpy(g.d_groups, g.groups.data(), g.groups.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess)
-        e = cudaMemcpy(g.d_task_ab, tasks.data(), tasks.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(g.d_w, g.wf.data(), g.wf.size() * sizeof(float), cudaMemcpyHostToDevice);
     for (int mode = 0; mode < 4 && e == cudaSuccess; ++mode) {
         const size_t sm = proj_cfg(g, mode).smem;
@@ -368,7 +360,7 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     }
     if (prev >= 0) cudaSetDevice(prev);
     if (e != cudaSuccess) {
-        cudaFree(g.d_rays); cudaFree(g.d_groups); cudaFree(g.d_task_ab); cudaFree(g.d_w);
+        free_device_tables(&g);
         delete h;
         return cuda_fail(e, "pget_geometry_create");
     }
@@ -383,10 +375,7 @@ pget_status pget_geometry_destroy(pget_geometry h)
     int prev = -1;
     cudaGetDevice(&prev);
     cudaSetDevice(h->g.device);
-    cudaFree(h->g.d_rays);
-    cudaFree(h->g.d_groups);
-    cudaFree(h->g.d_task_ab);
-    cudaFree(h->g.d_w);
+    free_device_tables(&h->g);
     if (prev >= 0) cudaSetDevice(prev);
     delete h;
     return PGET_OK;
@@ -504,8 +493,8 @@ static pget_status proj_adjoint(const Geometry& g, const WS& w, int mode, const 
     if (st) return st;
     const int N = g.desc.n_px;
     const dim3 grid((N + 31) / 32, (N + 31) / 32, g.desc.batch * c.G);
-    reduce_slots_kernel<<<grid, dim3(32, 8), 0, s>>>(w.slots, w.gacc, N, slot_pitch(g), c.ntab * c.n_parts,
-                                                    c.nc0 * c.n_parts, g.desc.batch, c.grid, c.KS, c.G); note();
+    reduce_slots_kernel<<<grid, dim3(32, 8), 0, s>>>(w.slots, w.gacc, N, slot_pitch(g), g.desc.batch, c.G,
+                                                    g.sch[kSchedAdj].d_red_off, g.sch[kSchedAdj].d_red_slot); note();
     CK(cudaGetLastError());
     return PGET_OK;
 }

@@ -179,44 +179,7 @@ pget_status build_geometry(const pget_geometry_desc* d, Geometry* g, std::string
         if (S > g->R) S = g->R;
         g->comb_S = static_cast<int>(S);
     }
-    build_parts(g, 1);
     return PGET_OK;
-}
-
-// Ray parts and comb groups for `np` parts (the adjoint modes use one part: their per-band ring
-// flush costs the same for every part, measured 1.4x slower with 4 parts on config 2).  Comb groups: ray offsets are uniform with spacing a = (p/J)/h pixels; two rays >= S = ceil((2 sqrt2 +
-// 1e-6)/a) apart have sample points >= 2 px apart in max-norm, so their bilinear footprints never
-// overlap.  Greedy: rays of the part in comb order (r mod S, then r), a new group whenever 32 lanes
-// are used or the next ray is closer than S to one already in the group.
-void build_parts(Geometry* g, int np)
-{
-    const int nd = g->desc.n_det, J = g->desc.n_subrays, S = g->comb_S;
-    np = std::max(1, std::min(np, std::min(nd, Geometry::kMaxParts)));
-    g->n_parts = np;
-    g->groups.clear();
-    for (int q = 0; q <= Geometry::kMaxParts; ++q)
-        g->part_det[q] = q <= np ? static_cast<int>((static_cast<int64_t>(nd) * q) / np) : nd;
-    for (int q = 0; q < np; ++q) {
-        g->part_grp[q] = static_cast<int>(g->groups.size() / 32);
-        const int r_lo = g->part_det[q] * J, r_hi = g->part_det[q + 1] * J;
-        std::vector<int32_t> cur;
-        auto flush = [&]() {
-            if (cur.empty()) return;
-            for (int k = 0; k < 32; ++k) g->groups.push_back(k < static_cast<int>(cur.size()) ? cur[k] : -1);
-            cur.clear();
-        };
-        for (int c0 = 0; c0 < S; ++c0)
-            for (int r = r_lo + c0; r < r_hi; r += S) {
-                bool ok = cur.size() < 32;
-                for (int32_t x : cur)
-                    if (std::abs(x - r) < S) { ok = false; break; }
-                if (!ok) flush();
-                cur.push_back(r);
-            }
-        flush();
-    }
-    g->n_groups = static_cast<int>(g->groups.size() / 32);
-    for (int q = np; q <= Geometry::kMaxParts; ++q) g->part_grp[q] = g->n_groups;
 }
 
 // 32.32 fixed-point sample positions in padded pixel coordinates, in each angle-bank's oriented

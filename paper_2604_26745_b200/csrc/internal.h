@@ -28,6 +28,36 @@ struct RayP {
 };
 static_assert(sizeof(RayP) == 40, "RayP layout");
 
+// One projector task (device table entry): member, traced angle-bank, detector range, the comb
+// groups (sweep B lane sets) of that range, and the partial slot of the adjoint kind.
+enum { kTaskClass1 = 1, kTaskFirst = 2 };
+struct TaskD {
+    int32_t m, ab;        // batch member, traced angle-bank
+    int32_t dlo, dhi;     // detectors [dlo, dhi)
+    int32_t gbeg, gend;   // comb groups [gbeg, gend) in Schedule::groups
+    int32_t slot;         // partial-gradient slot (adjoint kind), -1 otherwise
+    int32_t flags;        // kTaskClass1: orientation class 1; kTaskFirst: first task of its slot in its CTA
+};
+static_assert(sizeof(TaskD) == 32, "TaskD layout");
+
+enum { kSchedFwd = 0, kSchedJvp = 1, kSchedAdj = 2 };
+struct Schedule {
+    int C = 0;                        // persistent CTAs (grid size)
+    std::vector<int32_t> cta_begin;   // [C + 1]: CTA c runs tasks [cta_begin[c], cta_begin[c+1])
+    std::vector<TaskD> tasks;
+    std::vector<int32_t> groups;      // [n][32] comb groups, ray index in the angle-bank, -1 = idle lane
+    int n_slots = 0;                  // adjoint kind: partial slots
+    std::vector<int32_t> red_off;     // [2B + 1]: slots of (member m, class c) are red_slot[red_off[2m+c] ..)
+    std::vector<int32_t> red_slot;
+    int max_slots_member = 0;
+    int max_gA = 1, max_gB = 1;       // most sweep-A (32 adjacent rays) / sweep-B (comb) groups of a task
+    int32_t* d_cta_begin = nullptr;
+    TaskD* d_tasks = nullptr;
+    int32_t* d_groups = nullptr;
+    int32_t* d_red_off = nullptr;
+    int32_t* d_red_slot = nullptr;
+};
+
 // Host-side geometry (fp64 tables built per O1, bit-exact with the oracle's
 // formulas) plus the device copies the kernels read.
 struct Geometry {
@@ -60,24 +90,15 @@ struct Geometry {
     std::vector<int8_t> orient;   // [n_ab]
     std::vector<int32_t> task_ab; // [n_tab] traced angle-banks in processing order: class 0, then class 1
     int n_class0 = 0;
-    // ray parts: a task is (member, traced angle-bank, part); part p owns detectors
-    // [part_det[p], part_det[p+1]) so that the static task ranges of the persistent CTAs balance
-    static constexpr int kMaxParts = 8;
-    int n_parts = 1;
-    int part_det[kMaxParts + 1] = {0};
-    int part_grp[kMaxParts + 1] = {0};   // comb groups of part p: [part_grp[p], part_grp[p+1])
-    // comb groups: <= 32 rays of one part whose offsets differ pairwise by >= comb_S rays (>= 2 sqrt2 px)
+    // comb stride: rays >= comb_S apart (>= 2 sqrt2 px) have disjoint bilinear footprints
     int comb_S = 1;
-    int n_groups = 0;
-    std::vector<int32_t> groups;  // [n_groups][32] ray index in the angle-bank, -1 = idle lane
     // device tables
     RayP* d_rays = nullptr;       // [n_ab][R] oriented frame
-    int32_t* d_groups = nullptr;  // [n_groups][32]
-    int32_t* d_task_ab = nullptr; // [n_tab + task_ab_p.size()]: task_ab then task_ab_p
     float* d_w = nullptr;         // [J] float weights
     std::vector<float> wf;        // host copy of the float weights
     int sm_count = 148;
     size_t smem_optin = 227 * 1024;
+    Schedule sch[3];   // kSchedFwd, kSchedJvp, kSchedAdj (schedule.cpp), device copies owned here
 };
 
 }  // namespace pget
@@ -90,5 +111,5 @@ namespace pget {
 // geometry.cpp
 pget_status build_geometry(const pget_geometry_desc* d, Geometry* g, std::string* err);
 void build_ray_params(const Geometry& g, std::vector<RayP>* rays);
-void build_parts(Geometry* g, int np);
+void build_schedule(const Geometry& g, int kind, int C, Schedule* S);
 }  // namespace pget

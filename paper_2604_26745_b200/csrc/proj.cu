@@ -137,21 +137,22 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 
 // ------------------------------------------------------------------------------------------ tasks
 struct TaskInfo {
-    int m, ab, cls, dir, part;
-    int64_t seg;   // partial-slot chunk id (chunk_of)
+    int m, ab, cls, dir, dlo, dhi, gbeg, gend, slot, first;
 };
 
 __device__ __forceinline__ TaskInfo task_info(const ProjArgs& A, int64_t t)
 {
+    const TaskD td = A.tasks[t];
     TaskInfo ti;
-    const int ntp = A.n_tab * A.n_parts;
-    ti.m = static_cast<int>(t / ntp);
-    const int kp = static_cast<int>(t - static_cast<int64_t>(ti.m) * ntp);
-    const int k = kp / A.n_parts;
-    ti.part = kp - k * A.n_parts;
-    ti.ab = A.task_ab[k];
-    ti.cls = k >= A.n_class0 ? 1 : 0;
-    ti.seg = chunk_of(t, ntp, A.n_class0 * A.n_parts);
+    ti.m = td.m;
+    ti.ab = td.ab;
+    ti.cls = (td.flags & kTaskClass1) ? 1 : 0;
+    ti.first = (td.flags & kTaskFirst) ? 1 : 0;
+    ti.dlo = td.dlo;
+    ti.dhi = td.dhi;
+    ti.gbeg = td.gbeg;
+    ti.gend = td.gend;
+    ti.slot = td.slot;
     ti.dir = A.rays[static_cast<size_t>(ti.ab) * A.R].dV > 0 ? 1 : -1;
     return ti;
 }
@@ -415,9 +416,8 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
     float4* gsh = reinterpret_cast<float4*>(smem + A.off_gsh);      // [R] (G, Gc, Sl, Slc)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t Ttot = static_cast<int64_t>(A.B) * A.n_tab * A.n_parts;
-    const int C = gridDim.x, c = blockIdx.x;
-    const int64_t t0 = static_cast<int64_t>(c) * Ttot / C, t1 = static_cast<int64_t>(c + 1) * Ttot / C;
+    const int c = blockIdx.x;
+    const int64_t t0 = A.cta_begin[c], t1 = A.cta_begin[c + 1];
     const int ns_task = A.passesA * A.nbA + (TR::HAS_B ? A.passesB * A.nbB : 0);
     const int64_t n_stages = (t1 - t0) * ns_task;
     if (n_stages == 0) return;
@@ -443,15 +443,13 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
     int64_t s = 0;   // global stage counter
 
     const float cf = A.cf, ch = A.ch, dl = A.delta, dlh = 0.5f * A.delta;
-    const int64_t seg0 = task_info(A, t0).seg;
 
     for (int64_t t = t0; t < t1; ++t) {
         const TaskInfo ti = task_info(A, t);
         const RayP* rays = A.rays + static_cast<size_t>(ti.ab) * R;
         const int64_t dU = rays[0].dU, dV = rays[0].dV;
-        const bool first_in_seg = (t == t0) || (task_info(A, t - 1).seg != ti.seg);
-        const int dlo = A.part_det[ti.part], dhi = A.part_det[ti.part + 1];
-        const int prl = dlo * J, prh = dhi * J;   // rays of this part
+        const int dlo = ti.dlo, dhi = ti.dhi;
+        const int prl = dlo * J, prh = dhi * J;   // rays of this task
 
         // ======================================================= sweep A: forward (+ JVP) recurrence
         // lanes own 32 adjacent rays (neighbouring lanes read neighbouring pixels: shared-memory broadcast)
@@ -546,8 +544,7 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
         const size_t wbase2 = (static_cast<size_t>(ti.m) * A.n_ab + dup_of(A, ti.ab)) * A.n_det;
         const size_t wpbase = (static_cast<size_t>(ti.m) * A.n_ab + ti.ab + 1) * A.n_det;   // PAIRED: bank 1
         const size_t wpbase2 = (static_cast<size_t>(ti.m) * A.n_ab + dup_of(A, ti.ab + 1)) * A.n_det;
-        float2* slot = A.slots + (static_cast<size_t>(c) * A.KS + static_cast<size_t>(ti.seg - seg0)) *
-                                     static_cast<size_t>(A.N) * A.Ns;
+        float2* slot = A.slots + static_cast<size_t>(ti.slot) * A.N * A.Ns;
         const int npairs = P >> 1;
         for (int pass = 0; pass < A.passesB; ++pass) {
             int ii[MAXG], ilo[MAXG];
@@ -556,8 +553,8 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
             StateB st[MAXG];
 #pragma unroll
             for (int k = 0; k < MAXG; ++k) {
-                const int grp = A.part_grp[ti.part] + (pass * MAXG + k) * W + warp;
-                const int r = grp < A.part_grp[ti.part + 1] ? A.groups[grp * 32 + lane] : -1;
+                const int grp = ti.gbeg + (pass * MAXG + k) * W + warp;
+                const int r = grp < ti.gend ? A.groups[grp * 32 + lane] : -1;
                 ii[k] = -1; ilo[k] = 0; uu[k] = 0; vv[k] = 0;
                 rb[k] = RayB{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
                 st[k] = StateB{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -611,9 +608,9 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                 // flushes of one slot element are issued by one thread in program order: deterministic.
                 const bool last = kb == A.nbB - 1;
                 const int carry = last ? -1 : (ti.dir > 0 ? r0 : r1);
-                const bool store = first_in_seg && pass == 0;
+                const bool store = ti.first && pass == 0;
                 for (int r = r0; r <= r1; ++r) {
-                    if (r == carry) continue;
+                    if (r == carry || PGET_ABLATE == 2) continue;
                     const int lr = flip ? r0 + A.RbB - r : r - r0;
                     int q0 = tid - (r * npairs) % NT;
                     if (q0 < 0) q0 += NT;
@@ -642,58 +639,37 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
 }
 
 // ------------------------------------------------------------------------------------------ reduction
-// g[m][j][i] = sum over the class-0 chunks of member m, over the CTAs touching the chunk, of slot[j][i]
-//            + the same over the class-1 chunks of slot[i][j]   (transposed frame)
-// in fp64, chunks and CTAs in increasing order (deterministic); written as float2 (g_lam, g_mu) [B][N][N].
-__device__ __forceinline__ int cta_of_task(int64_t x, int64_t Ttot, int C)
-{
-    int c = static_cast<int>((x * C) / Ttot);
-    if (c > C - 1) c = C - 1;
-    while (c > 0 && static_cast<int64_t>(c) * Ttot / C > x) --c;
-    while (c + 1 < C && static_cast<int64_t>(c + 1) * Ttot / C <= x) ++c;
-    return c;
-}
-
+// g[m][j][i] = sum over the class-0 slots of member m of slot[j][i] + sum over its class-1 slots of
+// slot[i][j] (transposed frame), in fp64, slots in the schedule's fixed order.  Block (tile, m * G + g)
+// adds the g-th of G ranges of member m's slot list into part[g][m]; finish_kernel adds the G
+// partials in order g = 0..G-1 (deterministic).
 __global__ void reduce_slots_kernel(const float2* __restrict__ slots, double2* __restrict__ part, int N, int Ns,
-                                    int n_tp, int n_class0, int B, int C, int KS, int G)
-// n_tp: tasks per member (traced angle-banks x parts), n_class0: class-0 tasks per member.
-// Block (tile, m * G + g) sums the chunks [g * nch / G, (g + 1) * nch / G) of member m into the fp64
-// partial part[g][m]; finish_kernel adds the G partials in order g = 0..G-1.
+                                    int B, int G, const int32_t* __restrict__ red_off,
+                                    const int32_t* __restrict__ red_slot)
 {
     __shared__ double2 tile[32][33];
     const int m = blockIdx.z / G, gq = blockIdx.z - m * G;
     const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
     const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
-    const int64_t Ttot = static_cast<int64_t>(B) * n_tp;
     const size_t plane = static_cast<size_t>(N) * Ns;
-    const int nc0 = (n_class0 + kChunk - 1) / kChunk, nc1 = (n_tp - n_class0 + kChunk - 1) / kChunk;
-    const int nch = nc0 + nc1;
+    const int e0 = red_off[2 * m], e1 = red_off[2 * m + 1], e2 = red_off[2 * m + 2];
+    const int n = e2 - e0;
     double2 acc[4], accT[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) acc[k] = accT[k] = make_double2(0.0, 0.0);
-    for (int local = (gq * nch) / G; local < ((gq + 1) * nch) / G; ++local) {
-        const int cls = local >= nc0 ? 1 : 0;
-        const int64_t cbeg = static_cast<int64_t>(m) * n_tp + (cls ? n_class0 : 0);
-        const int64_t cend = static_cast<int64_t>(m) * n_tp + (cls ? n_tp : n_class0);
-        const int64_t first = cbeg + static_cast<int64_t>(cls ? local - nc0 : local) * kChunk;
-        const int64_t last = min(first + kChunk, cend) - 1;
-        const int64_t ch = static_cast<int64_t>(m) * nch + local;
-        const int c_lo = cta_of_task(first, Ttot, C), c_hi = cta_of_task(last, Ttot, C);
-        for (int c = c_lo; c <= c_hi; ++c) {
-            const int64_t tb = static_cast<int64_t>(c) * Ttot / C;
-            if (static_cast<int64_t>(c + 1) * Ttot / C == tb) continue;   // CTA without tasks (Ttot < C)
-            const float2* sl = slots + (static_cast<size_t>(c) * KS + (ch - chunk_of(tb, n_tp, n_class0))) * plane;
+    for (int e = e0 + (gq * n) / G; e < e0 + ((gq + 1) * n) / G; ++e) {
+        const int cls = e >= e1 ? 1 : 0;
+        const float2* sl = slots + static_cast<size_t>(red_slot[e]) * plane;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                // class 0: element (row j, col i) = (j0 + ty + 8k, i0 + tx)
-                // class 1: element (row i, col j) of the transposed slot = (i0 + ty + 8k, j0 + tx)
-                const int rr = (cls ? i0 : j0) + ty + 8 * k, cc = (cls ? j0 : i0) + tx;
-                if (rr < N && cc < N) {
-                    const float2 v = sl[static_cast<size_t>(rr) * Ns + cc];
-                    double2& a = cls ? accT[k] : acc[k];
-                    a.x += v.x;
-                    a.y += v.y;
-                }
+        for (int k = 0; k < 4; ++k) {
+            // class 0: element (row j, col i) = (j0 + ty + 8k, i0 + tx)
+            // class 1: element (row i, col j) of the transposed slot = (i0 + ty + 8k, j0 + tx)
+            const int rr = (cls ? i0 : j0) + ty + 8 * k, cc = (cls ? j0 : i0) + tx;
+            if (rr < N && cc < N) {
+                const float2 v = sl[static_cast<size_t>(rr) * Ns + cc];
+                double2& a = cls ? accT[k] : acc[k];
+                a.x += v.x;
+                a.y += v.y;
             }
         }
     }

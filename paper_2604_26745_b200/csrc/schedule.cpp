@@ -1,0 +1,184 @@
+// schedule.cpp -- static task schedules of the persistent projector (host, native C++).
+//
+// A projector task is (batch member, traced angle-bank, detector range).  For each projector kind
+// (forward, JVP, adjoint = VJP and GN) the host builds, once per geometry handle, the list of tasks
+// every CTA processes, from the exact per-task work (nominal samples of the task's rays, known from
+// the clip table):
+//   * many tasks per CTA (>= 8): contiguous member-major ranges, whole angle-banks;
+//   * otherwise the angle-banks are cut into p equal detector ranges (p = 1..4, the p with the
+//     smallest estimated makespan, a part costing work/p + a fixed per-part overhead) and the parts
+//     are assigned longest-first to the least-loaded CTA (LPT).
+// For the adjoint kind every task also gets a partial-gradient slot: consecutive tasks of one CTA
+// with the same (member, orientation class) share a slot (at most kSlotTasks of them, so an fp32
+// slot sums a bounded number of angle-banks); the slot lists per (member, class) drive the fixed-order
+// fp64 reduction (reduce_slots_kernel).  Comb groups (sweep B lane sets) are built per detector range.
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <map>
+#include <numeric>
+#include <queue>
+
+#include "internal.h"
+
+namespace pget {
+
+constexpr int kSlotTasks = 16;
+
+// comb groups of rays [r_lo, r_hi): <= 32 rays pairwise >= S apart (greedy, comb order)
+static void comb_groups(int r_lo, int r_hi, int S, std::vector<int32_t>* out)
+{
+    std::vector<int32_t> cur;
+    auto flush = [&]() {
+        if (cur.empty()) return;
+        for (int k = 0; k < 32; ++k) out->push_back(k < static_cast<int>(cur.size()) ? cur[k] : -1);
+        cur.clear();
+    };
+    for (int c0 = 0; c0 < S; ++c0)
+        for (int r = r_lo + c0; r < r_hi; r += S) {
+            bool ok = cur.size() < 32;
+            for (int32_t x : cur)
+                if (std::abs(x - r) < S) { ok = false; break; }
+            if (!ok) flush();
+            cur.push_back(r);
+        }
+    flush();
+}
+
+void build_schedule(const Geometry& g, int kind, int C, Schedule* S)
+{
+    const bool adjoint = kind == kSchedAdj;
+    const bool paired = g.dup && kind != kSchedJvp;
+    const std::vector<int32_t>& list = paired ? g.task_ab_p : g.task_ab;
+    const int B = g.desc.batch, nd = g.desc.n_det, J = g.desc.n_subrays;
+    const int ntab = static_cast<int>(list.size());
+    S->C = C;
+    S->tasks.clear();
+    S->groups.clear();
+    S->cta_begin.assign(C + 1, 0);
+
+    // work of each traced angle-bank (samples of its rays)
+    std::vector<double> cost(ntab, 0.0);
+    for (int k = 0; k < ntab; ++k)
+        for (int r = 0; r < g.R; ++r) {
+            const size_t e = static_cast<size_t>(list[k]) * g.R + r;
+            const int32_t lo = g.clip[2 * e], hi = g.clip[2 * e + 1];
+            if (hi >= lo) cost[k] += hi - lo + 1;
+        }
+    const int64_t T0 = static_cast<int64_t>(B) * ntab;
+
+    std::map<std::pair<int, int>, std::pair<int, int>> gcache;   // (p, q) -> comb group range
+    auto groups_of = [&](int p, int q) {
+        auto key = std::make_pair(p, q);
+        auto it = gcache.find(key);
+        if (it != gcache.end()) return it->second;
+        const int b = static_cast<int>(S->groups.size() / 32);
+        comb_groups((nd * q / p) * J, (nd * (q + 1) / p) * J, g.comb_S, &S->groups);
+        const auto rg = std::make_pair(b, static_cast<int>(S->groups.size() / 32));
+        gcache[key] = rg;
+        return rg;
+    };
+    auto make = [&](int m, int k, int p, int q) {
+        TaskD t;
+        t.m = m;
+        t.ab = list[k];
+        t.dlo = nd * q / p;
+        t.dhi = nd * (q + 1) / p;
+        const auto rg = groups_of(p, q);
+        t.gbeg = rg.first;
+        t.gend = rg.second;
+        t.slot = -1;
+        t.flags = g.orient[list[k]] ? kTaskClass1 : 0;
+        return t;
+    };
+
+    std::vector<std::vector<TaskD>> per(C);
+    if (T0 >= 8LL * C || ntab == 0) {
+        for (int c = 0; c < C; ++c) {
+            const int64_t tb = static_cast<int64_t>(c) * T0 / C, te = static_cast<int64_t>(c + 1) * T0 / C;
+            for (int64_t t = tb; t < te; ++t) per[c].push_back(make(static_cast<int>(t / ntab), static_cast<int>(t % ntab), 1, 0));
+        }
+    } else {
+        const double ovh = adjoint ? 0.15 : 0.08;   // per-part overhead, fraction of a whole angle-bank
+        double best = 1e300;
+        int best_p = 1;
+        std::vector<int> best_owner;
+        struct Item { double w; int m, k, q; };
+        for (int p = 1; p <= std::min(4, nd); ++p) {
+            std::vector<Item> items;
+            for (int m = 0; m < B; ++m)
+                for (int k = 0; k < ntab; ++k)
+                    for (int q = 0; q < p; ++q) {
+                        const double frac = static_cast<double>(nd * (q + 1) / p - nd * q / p) / nd;
+                        items.push_back({cost[k] * (frac + (p > 1 ? ovh : 0.0)), m, k, q});
+                    }
+            std::vector<int> order(items.size());
+            std::iota(order.begin(), order.end(), 0);
+            std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return items[a].w > items[b].w; });
+            using L = std::pair<double, int>;
+            std::priority_queue<L, std::vector<L>, std::greater<L>> heap;
+            for (int c = 0; c < C; ++c) heap.push({0.0, c});
+            std::vector<int> owner(items.size());
+            double mk = 0.0;
+            for (int idx : order) {
+                L top = heap.top();
+                heap.pop();
+                owner[idx] = top.second;
+                top.first += items[idx].w;
+                mk = std::max(mk, top.first);
+                heap.push(top);
+            }
+            if (mk < best * 0.98) { best = mk; best_p = p; best_owner = owner; }
+        }
+        // rebuild the chosen items in (m, class, k, q) order per CTA
+        std::vector<std::vector<std::array<int, 3>>> own(C);
+        int idx = 0;
+        for (int m = 0; m < B; ++m)
+            for (int k = 0; k < ntab; ++k)
+                for (int q = 0; q < best_p; ++q) own[best_owner[idx++]].push_back({m, k, q});
+        for (int c = 0; c < C; ++c)
+            for (const auto& it : own[c]) per[c].push_back(make(it[0], it[1], best_p, it[2]));
+    }
+    // flatten; slots for the adjoint kind
+    S->n_slots = 0;
+    std::vector<std::vector<int32_t>> lists(static_cast<size_t>(B) * 2);
+    for (int c = 0; c < C; ++c) {
+        S->cta_begin[c] = static_cast<int32_t>(S->tasks.size());
+        int run = 0, pm = -1, pc = -1;
+        for (TaskD t : per[c]) {
+            if (adjoint) {
+                const int cls = (t.flags & kTaskClass1) ? 1 : 0;
+                if (t.m != pm || cls != pc || run == kSlotTasks) {
+                    lists[static_cast<size_t>(t.m) * 2 + cls].push_back(S->n_slots);
+                    ++S->n_slots;
+                    run = 0;
+                    t.flags |= kTaskFirst;
+                }
+                t.slot = S->n_slots - 1;
+                ++run;
+                pm = t.m;
+                pc = cls;
+            }
+            S->tasks.push_back(t);
+        }
+    }
+    S->cta_begin[C] = static_cast<int32_t>(S->tasks.size());
+    S->red_off.assign(static_cast<size_t>(B) * 2 + 1, 0);
+    S->red_slot.clear();
+    for (size_t e = 0; e < lists.size(); ++e) {
+        S->red_off[e] = static_cast<int32_t>(S->red_slot.size());
+        S->red_slot.insert(S->red_slot.end(), lists[e].begin(), lists[e].end());
+    }
+    S->red_off[lists.size()] = static_cast<int32_t>(S->red_slot.size());
+    S->max_slots_member = 0;
+    for (int m = 0; m < B; ++m)
+        S->max_slots_member = std::max(S->max_slots_member, S->red_off[2 * m + 2] - S->red_off[2 * m]);
+    S->max_gA = 1;
+    S->max_gB = 1;
+    for (const TaskD& t : S->tasks) {
+        S->max_gA = std::max(S->max_gA, ((t.dhi - t.dlo) * J + 31) / 32);
+        S->max_gB = std::max(S->max_gB, t.gend - t.gbeg);
+    }
+}
+
+}  // namespace pget
