@@ -71,7 +71,7 @@ size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct ProjCfg {
     int kind;             // schedule: kSchedFwd / kSchedJvp / kSchedAdj
-    int maxg, passesA, passesB, RbA, RbB, nbA, nbB, grid;
+    int W, maxg, passesA, passesB, RbA, RbB, nbA, nbB, grid;   // W: warps per CTA of this geometry
     int G;                // fp64 partial images of the slot reduction (adjoint modes)
     bool paired;          // line-paired projector (forward / VJP / GN of a dup geometry)
     size_t smem;
@@ -89,17 +89,23 @@ int sched_kind(int mode) { return mode == MODE_FWD ? kSchedFwd : (mode == MODE_J
 ProjCfg proj_cfg(const Geometry& g, int mode)
 {
     ProjCfg c;
-    const int W = proj_warps(mode), cps = proj_ctas_per_sm(mode);
+    const int cps = proj_ctas_per_sm(mode);
     c.kind = sched_kind(mode);
     const Schedule& S = g.sch[c.kind];
     c.paired = g.dup && mode != MODE_JVP;
     const bool hasB = mode == MODE_VJP || mode == MODE_GN;
     const bool nf4 = mode == MODE_JVP || mode == MODE_GN;
-    const int ncgA = S.max_gA, ncgB = S.max_gB;
-    const int gpw = std::max((ncgA + W - 1) / W, hasB ? (ncgB + W - 1) / W : 0);
-    c.maxg = gpw >= 2 ? 2 : 1;   // groups per warp per pass (register-resident ray state)
-    c.passesA = std::max(1, (ncgA + W * c.maxg - 1) / (W * c.maxg));
-    c.passesB = std::max(1, (ncgB + W * c.maxg - 1) / (W * c.maxg));
+    // warps per CTA: the mode's most (measured: fewer warps with fuller lane slots lost on config 2);
+    // MAXG register-resident ray groups per warp and pass
+    const int ncgA = S.max_gA, ncgB = hasB ? S.max_gB : 0;
+    c.W = proj_warps(mode);
+    {
+        const int gpw = std::max((ncgA + c.W - 1) / c.W, (ncgB + c.W - 1) / c.W);
+        c.maxg = gpw >= 2 ? 2 : 1;
+        c.passesA = std::max(1, (ncgA + c.W * c.maxg - 1) / (c.W * c.maxg));
+        c.passesB = std::max(1, (ncgB + c.W * c.maxg - 1) / (c.W * c.maxg));
+    }
+    const int W = c.W;
     const size_t per_sm = 233472;   // 228 KB of shared memory per SM
     const size_t budget = std::min<size_t>(g.smem_optin, per_sm / cps - 1024);
     const size_t rout_b = align128(2 * sizeof(float) * g.R), gsh_b = align128(sizeof(float4) * g.R);
@@ -184,7 +190,7 @@ pget_status run_proj(const Geometry& g, int mode, const ProjCfg& c, const ProjAr
         }
     }
     if (ea) cudaEventRecord(ea, s);
-    cudaError_t e = launch_proj(mode, c.maxg, c.paired, A, c.grid, c.smem, s);
+    cudaError_t e = launch_proj(mode, c.maxg, c.paired, A, c.grid, c.W * 32, c.smem, s);
     if (eb) cudaEventRecord(eb, s);
     if (e != cudaSuccess) return cuda_fail(e, "projector launch");
     return PGET_OK;

@@ -60,7 +60,8 @@ __global__ void scalar_kernel(int op, int k, const double* p0, const double* p1,
 }  // namespace pget
 
 namespace pget {
-cudaError_t launch_proj(int mode, int maxg, bool paired, const ProjArgs& A, int grid, size_t smem, cudaStream_t s);
+cudaError_t launch_proj(int mode, int maxg, bool paired, const ProjArgs& A, int grid, int block, size_t smem,
+                        cudaStream_t s);
 cudaError_t set_proj_smem_limit(int mode, size_t smem);
 int proj_warps(int mode);
 int proj_ctas_per_sm(int mode);

@@ -207,7 +207,7 @@ __device__ void issue_stage(const ProjArgs& A, int64_t t0, int ns_task, int64_t 
 
 template <int MODE>
 struct ModeTraits {
-    static constexpr int W = (MODE == MODE_VJP || MODE == MODE_GN) ? 12 : 8;    // warps per CTA
+    static constexpr int W = (MODE == MODE_VJP || MODE == MODE_GN) ? 12 : 8;    // most warps per CTA
     static constexpr int MINB = MODE == MODE_FWD ? 3 : (MODE == MODE_JVP ? 2 : 1); // CTAs per SM
     static constexpr bool HAS_B = (MODE == MODE_VJP || MODE == MODE_GN);         // adjoint sweep
     static constexpr bool NF4 = (MODE == MODE_JVP || MODE == MODE_GN);           // 4-channel sweep A
@@ -406,8 +406,8 @@ template <int MODE, int MAXG, bool PAIRED>
 __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MINB) proj_kernel(ProjArgs A)
 {
     using TR = ModeTraits<MODE>;
-    constexpr int W = TR::W;
-    constexpr int NT = W * 32;
+    const int W = blockDim.x >> 5;   // warps of this launch (<= TR::W, chosen per geometry: proj_cfg)
+    const int NT = blockDim.x;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
     unsigned char* const stage0 = smem + 128;   // stage buffer b at stage0 + b * stage_bytes
@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                     if (q0 < 0) q0 += NT;
                     for (int q = q0; q < npairs; q += NT) {
                         float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
+#pragma unroll 4
                         for (int w = 0; w < W; ++w) {
                             float4* e = reinterpret_cast<float4*>(wacc_all + (static_cast<size_t>(w) * RB1 + lr) * P) + q;
                             const float4 x = *e;
@@ -689,9 +689,9 @@ __global__ void reduce_slots_kernel(const float2* __restrict__ slots, double2* _
 
 // ------------------------------------------------------------------------------------------ launcher
 template <int MODE>
-static cudaError_t launch_mode(int maxg, bool paired, const ProjArgs& A, int grid, size_t smem, cudaStream_t s)
+static cudaError_t launch_mode(int maxg, bool paired, const ProjArgs& A, int grid, int block, size_t smem,
+                               cudaStream_t s)
 {
-    const int block = ModeTraits<MODE>::W * 32;
     constexpr bool CP = MODE != MODE_JVP;   // the JVP is never line-paired
     if (paired && CP) {
         if (maxg == 1) proj_kernel<MODE, 1, CP><<<grid, block, smem, s>>>(A);
@@ -703,19 +703,20 @@ static cudaError_t launch_mode(int maxg, bool paired, const ProjArgs& A, int gri
     return cudaGetLastError();
 }
 
-cudaError_t launch_proj(int mode, int maxg, bool paired, const ProjArgs& A, int grid, size_t smem, cudaStream_t s)
+cudaError_t launch_proj(int mode, int maxg, bool paired, const ProjArgs& A, int grid, int block, size_t smem,
+                        cudaStream_t s)
 {
     if (maxg != 1 && maxg != 2) return cudaErrorInvalidValue;
     switch (mode) {
-    case MODE_FWD: return launch_mode<MODE_FWD>(maxg, paired, A, grid, smem, s);
-    case MODE_JVP: return launch_mode<MODE_JVP>(maxg, paired, A, grid, smem, s);
-    case MODE_VJP: return launch_mode<MODE_VJP>(maxg, paired, A, grid, smem, s);
-    case MODE_GN: return launch_mode<MODE_GN>(maxg, paired, A, grid, smem, s);
+    case MODE_FWD: return launch_mode<MODE_FWD>(maxg, paired, A, grid, block, smem, s);
+    case MODE_JVP: return launch_mode<MODE_JVP>(maxg, paired, A, grid, block, smem, s);
+    case MODE_VJP: return launch_mode<MODE_VJP>(maxg, paired, A, grid, block, smem, s);
+    case MODE_GN: return launch_mode<MODE_GN>(maxg, paired, A, grid, block, smem, s);
     }
     return cudaErrorInvalidValue;
 }
 
-int proj_warps(int mode) { return (mode == MODE_VJP || mode == MODE_GN) ? 12 : 8; }
+int proj_warps(int mode) { return (mode == MODE_VJP || mode == MODE_GN) ? 12 : 8; }   // the most
 int proj_ctas_per_sm(int mode) { return mode == MODE_FWD ? 3 : (mode == MODE_JVP ? 2 : 1); }
 
 template <int MODE>
