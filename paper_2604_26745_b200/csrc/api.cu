@@ -95,16 +95,23 @@ ProjCfg proj_cfg(const Geometry& g, int mode)
     c.paired = g.dup && mode != MODE_JVP;
     const bool hasB = mode == MODE_VJP || mode == MODE_GN;
     const bool nf4 = mode == MODE_JVP || mode == MODE_GN;
-    // warps per CTA: the mode's most (measured: fewer warps with fuller lane slots lost on config 2);
-    // MAXG register-resident ray groups per warp and pass
+    // Warps per CTA and ray groups per warp.  Every warp of a band should carry the same number of
+    // groups (the band ends at a CTA barrier).  Adjoint modes: one register-resident group per warp
+    // (<= 128 registers for up to 16 warps) and W = the group count divided evenly over the fewest
+    // passes (config 2: 15 groups -> 15 warps, 1 pass; configs 3/4: 26 -> 13 warps, 2 passes).
+    // Forward / JVP: 8 warps, up to 2 groups per warp.
     const int ncgA = S.max_gA, ncgB = hasB ? S.max_gB : 0;
-    c.W = proj_warps(mode);
-    {
-        const int gpw = std::max((ncgA + c.W - 1) / c.W, (ncgB + c.W - 1) / c.W);
-        c.maxg = gpw >= 2 ? 2 : 1;
-        c.passesA = std::max(1, (ncgA + c.W * c.maxg - 1) / (c.W * c.maxg));
-        c.passesB = std::max(1, (ncgB + c.W * c.maxg - 1) / (c.W * c.maxg));
+    if (hasB) {
+        const int gmax = std::max(ncgA, ncgB);
+        const int passes = (gmax + proj_warps(mode) - 1) / proj_warps(mode);
+        c.W = std::max(4, (gmax + passes - 1) / passes);
+        c.maxg = 1;
+    } else {
+        c.W = proj_warps(mode);
+        c.maxg = (ncgA + c.W - 1) / c.W >= 2 ? 2 : 1;
     }
+    c.passesA = std::max(1, (ncgA + c.W * c.maxg - 1) / (c.W * c.maxg));
+    c.passesB = std::max(1, (ncgB + c.W * c.maxg - 1) / (c.W * c.maxg));
     const int W = c.W;
     const size_t per_sm = 233472;   // 228 KB of shared memory per SM
     const size_t budget = std::min<size_t>(g.smem_optin, per_sm / cps - 1024);

@@ -207,7 +207,7 @@ __device__ void issue_stage(const ProjArgs& A, int64_t t0, int ns_task, int64_t 
 
 template <int MODE>
 struct ModeTraits {
-    static constexpr int W = (MODE == MODE_VJP || MODE == MODE_GN) ? 12 : 8;    // most warps per CTA
+    static constexpr int W = (MODE == MODE_VJP || MODE == MODE_GN) ? 16 : 8;    // most warps per CTA
     static constexpr int MINB = MODE == MODE_FWD ? 3 : (MODE == MODE_JVP ? 2 : 1); // CTAs per SM
     static constexpr bool HAS_B = (MODE == MODE_VJP || MODE == MODE_GN);         // adjoint sweep
     static constexpr bool NF4 = (MODE == MODE_JVP || MODE == MODE_GN);           // 4-channel sweep A
@@ -716,7 +716,7 @@ cudaError_t launch_proj(int mode, int maxg, bool paired, const ProjArgs& A, int 
     return cudaErrorInvalidValue;
 }
 
-int proj_warps(int mode) { return (mode == MODE_VJP || mode == MODE_GN) ? 12 : 8; }   // the most
+int proj_warps(int mode) { return (mode == MODE_VJP || mode == MODE_GN) ? 16 : 8; }   // the most
 int proj_ctas_per_sm(int mode) { return mode == MODE_FWD ? 3 : (mode == MODE_JVP ? 2 : 1); }
 
 template <int MODE>
