@@ -546,6 +546,15 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
         const size_t wpbase2 = (static_cast<size_t>(ti.m) * A.n_ab + dup_of(A, ti.ab + 1)) * A.n_det;
         float2* slot = A.slots + static_cast<size_t>(ti.slot) * A.N * A.Ns;
         const int npairs = P >> 1;
+        // columns the task's rays can touch in a band of rows [v0, v1] (oriented frame): between the
+        // lines of its first and last ray; the band flush reads and clears only those (a detector
+        // range of an angle-bank flushes its share of the image, not all of it)
+        const RayP rfirst = rays[prl], rlast = rays[prh - 1];
+        const double kuv = static_cast<double>(dU) / static_cast<double>(dV);
+        auto ucol = [&](const RayP& rp, double vrow) {
+            return (static_cast<double>(rp.U0) + (vrow * 4294967296.0 - static_cast<double>(rp.V0)) * kuv) *
+                   (1.0 / 4294967296.0);
+        };
         for (int pass = 0; pass < A.passesB; ++pass) {
             int ii[MAXG], ilo[MAXG];
             int64_t uu[MAXG], vv[MAXG];
@@ -608,13 +617,21 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                 // flushes of one slot element are issued by one thread in program order: deterministic.
                 const bool last = kb == A.nbB - 1;
                 const int carry = last ? -1 : (ti.dir > 0 ? r0 : r1);
-                const bool store = ti.first && pass == 0;
+                const bool store = ti.first && pass == 0;   // the slot's first writer covers every column
+                int qlo = 0, qhi = npairs - 1;
+                if (!store) {
+                    const double a0 = ucol(rfirst, r0 - 1.0), a1 = ucol(rfirst, r1 + 1.0);
+                    const double b0 = ucol(rlast, r0 - 1.0), b1 = ucol(rlast, r1 + 1.0);
+                    const double umin = fmin(fmin(a0, a1), fmin(b0, b1)), umax = fmax(fmax(a0, a1), fmax(b0, b1));
+                    qlo = max(0, static_cast<int>(floor(umin)) - 2) >> 1;
+                    qhi = min(P - 1, static_cast<int>(floor(umax)) + 3) >> 1;
+                }
                 for (int r = r0; r <= r1; ++r) {
                     if (r == carry || PGET_ABLATE == 2) continue;
                     const int lr = flip ? r0 + A.RbB - r : r - r0;
-                    int q0 = tid - (r * npairs) % NT;
+                    int q0 = tid - (r * npairs + qlo) % NT;
                     if (q0 < 0) q0 += NT;
-                    for (int q = q0; q < npairs; q += NT) {
+                    for (int q = qlo + q0; q <= qhi; q += NT) {
                         float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 4
                         for (int w = 0; w < W; ++w) {

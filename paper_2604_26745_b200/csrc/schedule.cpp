@@ -99,7 +99,9 @@ void build_schedule(const Geometry& g, int kind, int C, Schedule* S)
             for (int64_t t = tb; t < te; ++t) per[c].push_back(make(static_cast<int>(t / ntab), static_cast<int>(t % ntab), 1, 0));
         }
     } else {
-        const double ovh = adjoint ? 0.15 : 0.08;   // per-part overhead, fraction of a whole angle-bank
+        // per-part overhead (band streaming, barriers, flush) as a fraction of a whole angle-bank; it
+        // scales with the band count over the work, ~1/N (measured: 0.06 right at N = 256, too low at 128)
+        const double ovh = (adjoint ? 0.06 : 0.04) * 256.0 / g.desc.n_px;
         double best = 1e300;
         int best_p = 1;
         std::vector<int> best_owner;
