@@ -345,6 +345,11 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&g.sm_count, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     if (e == cudaSuccess) g.smem_optin = static_cast<size_t>(optin);
+    int coop = 0, per_sm = 0;
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
+    if (e == cudaSuccess && !coop) e = cudaErrorNotSupported;
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, cg_fused_kernel, kVecThreads, 0);
+    if (e == cudaSuccess) g.cg_coop_blocks = std::max(1, per_sm) * g.sm_count;
     std::vector<RayP> rays;
     build_ray_params(g, &rays);
     if (e == cudaSuccess) e = cudaMalloc(&g.d_rays, rays.size() * sizeof(RayP));
@@ -620,12 +625,18 @@ pget_status pget_gn_cg_step(pget_geometry h, const float* lam, const float* mu, 
     for (int k = 0; k < n_cg; ++k) {
         if ((st = pack4(g, w, lam, mu, w.pl, w.pm, s))) return st;
         if ((st = proj_adjoint(g, w, MODE_GN, nullptr, s))) return st;
-        finish_kernel<<<vg, kVecThreads, 0, s>>>(w.gacc, Gg, w.pl, w.pm, alpha, beta, 1.f, w.ql, w.qm, w.pl, w.pm, P[3],
-                                                nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, N); note();
-        scalar_kernel<<<sgrid, 128, 0, s>>>(SC_GAMMA, k, P[3], nullptr, nullptr, kNblk, w.cg, stats, B, alpha, beta); note();
-        cg_update1_kernel<<<vg, kVecThreads, 0, s>>>(s_lam, s_mu, w.zl, w.zm, w.pl, w.pm, w.ql, w.qm, w.cg, P[4], n2); note();
-        scalar_kernel<<<sgrid, 128, 0, s>>>(SC_ZETA, k, P[4], nullptr, nullptr, kNblk, w.cg, stats, B, alpha, beta); note();
-        cg_update2_kernel<<<vg, kVecThreads, 0, s>>>(w.zl, w.zm, w.pl, w.pm, w.cg, n2); note();
+        {   // finish + gamma + update1 + zeta + update2: one cooperative launch (grid-wide syncs)
+            int kk = k, NN = N, BB = B, nb = kNblk, GG = Gg;
+            float al = alpha, be = beta;
+            double *pg = P[3], *pz = P[4];
+            CGState* cgs = w.cg;
+            void* args[] = {&w.gacc, &GG, &al, &be, &s_lam, &s_mu, &w.zl, &w.zm, &w.pl, &w.pm, &w.ql, &w.qm,
+                            &pg, &pz, &cgs, &stats, &kk, &NN, &BB, &nb};
+            const int grid = std::min(B * kNblk, g.cg_coop_blocks);
+            CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cg_fused_kernel), dim3(grid), dim3(kVecThreads),
+                                           args, 0, s));
+            note();
+        }
         CK(cudaGetLastError());
     }
     // 6: pred = <b,s> - 1/2(||Js||^2 + alpha ||Ls||^2)

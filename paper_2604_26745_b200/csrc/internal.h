@@ -97,6 +97,7 @@ struct Geometry {
     float* d_w = nullptr;         // [J] float weights
     std::vector<float> wf;        // host copy of the float weights
     int sm_count = 148;
+    int cg_coop_blocks = 148;   // co-resident blocks of cg_fused_kernel (cooperative launch bound)
     size_t smem_optin = 227 * 1024;
     Schedule sch[3];   // kSchedFwd, kSchedJvp, kSchedAdj (schedule.cpp), device copies owned here
 };

@@ -2,6 +2,7 @@
 // projector (proj.cu), the regulariser, residual and objective reductions and the CG updates of
 // the LM iteration.  Reductions use per-member fp64
 // block partials over a fixed grid, so every scalar is deterministic.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -312,5 +313,114 @@ __global__ void scalar_kernel(int op, int k, const double* p0, const double* p1,
     }
 }
 
-}  // namespace pget
 
+// One CG step after the GN projector, fused into a single cooperative launch (grid-wide syncs):
+//   q = H p  (the G fp64 slot partials + alpha L^T L p + beta p),   gamma = <p, q>,
+//   a = zeta / gamma,  s += a p,  z -= a q,  zeta' = <z, z>,  p = z + (zeta' / zeta) p,
+// with the same fixed-order fp64 block partials (nblk per member) and the same stop rules and
+// statistics as finish / scalar(SC_GAMMA) / cg_update1 / scalar(SC_ZETA) / cg_update2.
+// Work unit (member m, block-in-member j) -> elements e = j * blockDim + tid (+ nblk * blockDim).
+__global__ void cg_fused_kernel(const double2* __restrict__ part, int G, float alpha, float beta, float* sl,
+                                float* sm, float* zl, float* zm, float* pl, float* pm, float* ql, float* qm,
+                                double* pg, double* pz, CGState* st, pget_gn_stats* stats, int k, int N, int B,
+                                int nblk)
+{
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double sh[32];
+    const size_t n2 = static_cast<size_t>(N) * N;
+    const int units = B * nblk;
+    const size_t stride = static_cast<size_t>(nblk) * blockDim.x;
+    // phase 1: q = H p, <p, q> partials
+    for (int mj = blockIdx.x; mj < units; mj += gridDim.x) {
+        const int m = mj / nblk, j = mj - m * nblk;
+        const size_t base = static_cast<size_t>(m) * n2;
+        double dsum = 0.0;
+        if (!st[m].stop) {
+            for (size_t e = static_cast<size_t>(j) * blockDim.x + threadIdx.x; e < n2; e += stride) {
+                const int i = static_cast<int>(e % N), jj = static_cast<int>(e / N);
+                double2 a = part[base + e];
+                for (int g = 1; g < G; ++g) {
+                    const double2 b = part[static_cast<size_t>(g) * B * n2 + base + e];
+                    a.x += b.x;
+                    a.y += b.y;
+                }
+                const float* xl = pl + base;
+                const float* xm = pm + base;
+                const float ol = static_cast<float>(a.x) + alpha * lap2_at(xl, N, jj, i) + beta * xl[e];
+                const float om = static_cast<float>(a.y) + alpha * lap2_at(xm, N, jj, i) + beta * xm[e];
+                ql[base + e] = ol;
+                qm[base + e] = om;
+                dsum += static_cast<double>(ol) * xl[e] + static_cast<double>(om) * xm[e];
+            }
+        }
+        const double t = block_sum(dsum, sh);
+        if (threadIdx.x == 0) pg[mj] = t;
+    }
+    grid.sync();
+    // phase 2: a = zeta / <p, q>; s += a p; z -= a q; ||z||^2 partials
+    for (int mj = blockIdx.x; mj < units; mj += gridDim.x) {
+        const int m = mj / nblk, j = mj - m * nblk;
+        const size_t base = static_cast<size_t>(m) * n2;
+        const CGState c = st[m];
+        double gam = 0.0;
+        for (int q = 0; q < nblk; ++q) gam += pg[m * nblk + q];
+        double zs = 0.0;
+        if (!c.stop && gam > 0.0) {
+            const float a = static_cast<float>(c.zeta / gam);
+            for (size_t e = static_cast<size_t>(j) * blockDim.x + threadIdx.x; e < n2; e += stride) {
+                const size_t q = base + e;
+                sl[q] = fmaf(a, pl[q], sl[q]);
+                sm[q] = fmaf(a, pm[q], sm[q]);
+                const float z1 = fmaf(-a, ql[q], zl[q]);
+                const float z2 = fmaf(-a, qm[q], zm[q]);
+                zl[q] = z1;
+                zm[q] = z2;
+                zs += static_cast<double>(z1) * z1 + static_cast<double>(z2) * z2;
+            }
+        }
+        const double t = block_sum(zs, sh);
+        if (threadIdx.x == 0) pz[mj] = t;
+    }
+    grid.sync();
+    // phase 3: p = z + (zeta' / zeta) p; state and statistics (unit (m, 0), thread 0)
+    for (int mj = blockIdx.x; mj < units; mj += gridDim.x) {
+        const int m = mj / nblk, j = mj - m * nblk;
+        const size_t base = static_cast<size_t>(m) * n2;
+        const CGState c = st[m];
+        double gam = 0.0, z2 = 0.0;
+        for (int q = 0; q < nblk; ++q) {
+            gam += pg[m * nblk + q];
+            z2 += pz[m * nblk + q];
+        }
+        const bool run = !c.stop && gam > 0.0;
+        const double bcg = run ? z2 / c.zeta : 0.0;
+        if (run && z2 != 0.0) {
+            const float bc = static_cast<float>(bcg);
+            for (size_t e = static_cast<size_t>(j) * blockDim.x + threadIdx.x; e < n2; e += stride) {
+                const size_t q = base + e;
+                pl[q] = fmaf(bc, pl[q], zl[q]);
+                pm[q] = fmaf(bc, pm[q], zm[q]);
+            }
+        }
+        __syncthreads();   // every thread of the block read st[m] before it changes
+        if (j == 0 && threadIdx.x == 0 && !c.stop) {
+            CGState& w = st[m];
+            pget_gn_stats& S = stats[m];
+            if (k == 0) S.beta_min = 1e-3 * gam / c.zeta;
+            if (!(gam > 0.0)) {
+                w.stop = 1;
+                S.breakdown = 2;
+            } else {
+                w.a = c.zeta / gam;
+                w.bcg = bcg;
+                w.zeta = z2;
+                S.cg_res[k + 1] = sqrt(z2);
+                S.n_cg_done = k + 1;
+                if (z2 == 0.0) { w.stop = 1; S.breakdown = 1; }
+            }
+        }
+    }
+}
+
+}  // namespace pget

@@ -54,6 +54,9 @@ __global__ void cg_update1_kernel(float* sl, float* sm, float* zl, float* zm, co
                                   const float* ql, const float* qm, const CGState* st, double* partial, int n2);
 __global__ void cg_update2_kernel(const float* zl, const float* zm, float* pl, float* pm, const CGState* st,
                                   int n2);
+__global__ void cg_fused_kernel(const double2* part, int G, float alpha, float beta, float* sl, float* sm, float* zl,
+                                float* zm, float* pl, float* pm, float* ql, float* qm, double* pg, double* pz,
+                                CGState* st, pget_gn_stats* stats, int k, int N, int B, int nblk);
 __global__ void scalar_kernel(int op, int k, const double* p0, const double* p1, const double* p2, int nblk,
                               CGState* st, pget_gn_stats* stats, int B, double alpha, double beta);
 
