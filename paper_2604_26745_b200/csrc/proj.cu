@@ -626,10 +626,15 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                     qlo = max(0, static_cast<int>(floor(umin)) - 2) >> 1;
                     qhi = min(P - 1, static_cast<int>(floor(umax)) + 3) >> 1;
                 }
+                int off = (r0 * npairs + qlo) % NT;   // (r * npairs + qlo) % NT, advanced per row (no division)
                 for (int r = r0; r <= r1; ++r) {
+                    if (r > r0) {
+                        off += npairs;
+                        while (off >= NT) off -= NT;
+                    }
                     if (r == carry || PGET_ABLATE == 2) continue;
                     const int lr = flip ? r0 + A.RbB - r : r - r0;
-                    int q0 = tid - (r * npairs + qlo) % NT;
+                    int q0 = tid - off;
                     if (q0 < 0) q0 += NT;
                     for (int q = qlo + q0; q <= qhi; q += NT) {
                         float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
