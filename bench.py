@@ -94,6 +94,29 @@ def dist_env():
     return rank, world, local
 
 
+def workload(cfg):
+    """The workload string both arms report in `config` (BASELINE.json configs[cfg - 1])."""
+    return (f"config {cfg.cid}: {cfg.lattice} phantom, N={cfg.n_px}, {cfg.n_angles} angles, 2x{cfg.n_det} det, "
+            f"J={cfg.n_subrays}, B={cfg.batch}; step = fwd + JVP + VJP + 1 LM iteration ({cfg.n_cg} CG, "
+            f"alpha={cfg.alpha}, beta=0, trial)")
+
+
+def max_over_ranks(ms, world, device):
+    """Device time of the slowest rank (all_reduce MAX over the process group): the job's clock."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_rate(units_per_step, steps, world, max_ms):
+    """Whole-job throughput: every rank runs its own replica of the step (independent assemblies,
+    no data-path collective, "scaling": "weak"), timed by the slowest rank."""
+    return world * units_per_step * steps / (max_ms * 1e-3)
+
+
 def reference_arm(args, rank, world):
     """--impl reference: the fp64 oracle (the paper has no code; the oracle is the reference
     arm for this tier) on a bounded sample of the same workload, on the host cores."""
@@ -114,7 +137,7 @@ def reference_arm(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "ray-samples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(times),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"config {cfg.cid} (bounded sample: {sample['desc']})"},
+        "config": {"workload": workload(cfg), "sample": sample["desc"]},
         "cpu_baseline": {"value": value, "unit": "ray-samples/s", "cores": O.threads(), "kind": "oracle",
                          "sample": sample["desc"]},
         "e2e": {"value": value, "unit": "ray-samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -249,11 +272,7 @@ def main():
         phase["jvp"] += e[1].elapsed_time(e[2])
         phase["vjp"] += e[2].elapsed_time(e[3])
         phase["lm"] += e[3].elapsed_time(e[4])
-    total_ms = sum(phase.values())
-    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms = max_over_ranks(sum(phase.values()), world, "cuda")
 
     # ---- end to end through the public API with host buffers (pinned), copies timed
     e2e = None
@@ -290,10 +309,8 @@ def main():
             b.record()
             b.synchronize()
             tot += a.elapsed_time(b)
-        te = torch.tensor([tot], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": world * samples_per_step * args.steps / (float(te.item()) * 1e-3), "unit": "ray-samples/s",
+        e2e = {"value": job_rate(samples_per_step, args.steps, world, max_over_ranks(tot, world, "cuda")),
+               "unit": "ray-samples/s",
                "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo}
 
     # ---- roofline of the dominant kernel (GN normal product projector) from live CUDA events
@@ -322,15 +339,13 @@ def main():
                "sample": s["desc"]}
 
     if rank == 0:
-        value = world * samples_per_step * args.steps / (total_ms * 1e-3)
+        value = job_rate(samples_per_step, args.steps, world, total_ms)
         K = args.steps
         line = {
             "metric": METRIC, "value": value, "unit": "ray-samples/s", "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"config {cfg.cid}: {cfg.lattice} phantom, N={cfg.n_px}, {cfg.n_angles} angles, "
-                                   f"2x{cfg.n_det} det, J={cfg.n_subrays}, B={cfg.batch}; step = fwd + JVP + VJP + "
-                                   f"1 LM iteration ({cfg.n_cg} CG, alpha={cfg.alpha}, beta=0, trial)",
+            "config": {"workload": workload(cfg),
                        "nominal_samples_per_pass": nominal, "traced_samples_per_pass": traced,
                        "angle_banks_merged": bool(g.info["angle_banks_merged"]),
                        "sample_passes_per_step": sample_passes,
