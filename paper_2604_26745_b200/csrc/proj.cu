@@ -29,6 +29,19 @@
 #include "internal.h"
 #include "kernels.cuh"
 
+// PGET_DEBUG builds (-DPGET_DEBUG, scripts/debug_check.sh) trap on any out-of-range shared-memory
+// index of the sample loops (compute-sanitizer is closed on the GPU pool).
+#ifdef PGET_DEBUG
+#define PGET_CHECK(c) \
+    do {              \
+        if (!(c)) __trap(); \
+    } while (0)
+#else
+#define PGET_CHECK(c) \
+    do {              \
+    } while (0)
+#endif
+
 #ifndef PGET_ABLATE
 #define PGET_ABLATE 0   // performance experiments only (scripts/ablate.sh); 0 in every real build
 #endif
@@ -257,6 +270,7 @@ __device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int
     if (i < ilo || iv < r0 || iv >= r1) return;
     const Cn* img = reinterpret_cast<const Cn*>(sb);
     int o = (iv - r0) * P + hi32(u);
+    PGET_CHECK(o >= 0 && o + P + 1 < (r1 - r0 + 1) * P);
     Cn q00 = img[o], q01 = img[o + 1], q10 = img[o + P], q11 = img[o + P + 1];
     float fu = frac23(u), fv = frac23(v);
     StateA x_ = st;
@@ -268,6 +282,7 @@ __device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int
         Cn n00, n01, n10, n11;
         if (nxt) {
             o = (iv2 - r0) * P + hi32(u2);
+            PGET_CHECK(o >= 0 && o + P + 1 < (r1 - r0 + 1) * P);
             n00 = img[o]; n01 = img[o + 1]; n10 = img[o + P]; n11 = img[o + P + 1];
         }
         float lam, mu, dlam = 0.f, dmu = 0.f;
@@ -350,6 +365,7 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
     StateB x_ = st;
     while (true) {
         // accumulator row of iv: abase + (iv - r0) * sP (sP = +-P, see the kernel), column iu
+        PGET_CHECK(iu >= 0 && iu + 1 < P && iv >= r0 && iv < r1);
         float2* a0 = acc + (abase + (iv - r0) * sP + iu);
         const float2 t00 = a0[0], t01 = a0[1], t10 = a0[sP], t11 = a0[sP + 1];
         const int i2 = i - 1;
@@ -360,6 +376,7 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
         int o2 = o;
         if (nxt) {
             o2 = (iv2 - r0) * P + hi32(u2);
+            PGET_CHECK(o2 >= 0 && o2 + P + 1 < (r1 - r0 + 1) * P);
             n00 = img[o2]; n01 = img[o2 + 1]; n10 = img[o2 + P]; n11 = img[o2 + P + 1];
         }
         const float2 x = bilerp2(q00, q01, q10, q11, fu, fv);
@@ -639,6 +656,7 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                     }
                     if (r == carry || PGET_ABLATE == 2) continue;
                     const int lr = flip ? r0 + A.RbB - r : r - r0;
+                    PGET_CHECK(lr >= 0 && lr < RB1);
                     int q0 = tid - off;
                     if (q0 < 0) q0 += NT;
                     for (int q = qlo + q0; q <= qhi; q += NT) {

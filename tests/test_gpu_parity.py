@@ -263,3 +263,21 @@ def test_errors_fail_loudly(pg):
     assert rc == 4          # PGET_ERR_WORKSPACE
     with pytest.raises(RuntimeError, match="INVALID_ARGUMENT"):
         pg.gn_cg_step(g, L, M, dev(np.zeros(g.sino_shape)), 1e-3, 0.0, 10 ** 6)
+
+
+# ----------------------------------------------------------------------------------- determinism (Q18)
+@pytest.mark.parametrize("cid", [2, 3])
+def test_adjoint_bitwise_deterministic(pg, cid):
+    """VJP and GN product: no atomics in the sample loop, fixed-thread slot flushes, fixed-order fp64
+    slot reduction -> bitwise identical results run to run (DESIGN.md R-determinism)."""
+    gd = P.geometry_desc(cid)
+    g = pg.Geometry(gd)
+    lam, mu, dl, dm, lp, mp = inputs(cid)
+    w = dev(O.forward(gd, lp, mp) - O.forward(gd, lam, mu))
+    L, M, DL, DM = dev(lam), dev(mu), dev(dl), dev(dm)
+    a = [host(x) for x in pg.vjp(g, L, M, w)]
+    b = [host(x) for x in pg.vjp(g, L, M, w)]
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))
+    c = [host(x) for x in pg.gn_apply(g, L, M, DL, DM, 1e-3, 0.0)]
+    d = [host(x) for x in pg.gn_apply(g, L, M, DL, DM, 1e-3, 0.0)]
+    assert all(np.array_equal(x, y) for x, y in zip(c, d))
