@@ -259,6 +259,12 @@ struct StateA {
 // the opposite bank on the same line (detector at the other end, optical depth A'_i = S - A_i),
 //   sum lam_i e^{A_i}                         (its forward:  e^{-S} * this),
 //   sum dlam_i e^{A_i}, sum lam_i dA_i e^{A_i}  (GN: its JVP = e^{-S}(p1 - dS p2 + p3), dA' = dS - dA).
+template <bool NF4>
+struct SmpA {   // one sample of a ray in sweep A: its corners (prefetched) and fractions
+    typename CornerT<NF4>::T c00, c01, c10, c11;
+    float fu, fv;
+};
+
 template <int MODE, bool PAIRED>
 __device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int P, int r0, int r1, int ilo,
                                        int64_t dU, int64_t dV, float cf, float ch, float dl, float dlh, int& i,
@@ -266,32 +272,31 @@ __device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int
 {
     using TR = ModeTraits<MODE>;
     using Cn = typename CornerT<TR::NF4>::T;
-    const int iv = hi32(v);
-    if (i < ilo || iv < r0 || iv >= r1) return;
+    const int iv0 = hi32(v);
+    if (i < ilo || iv0 < r0 || iv0 >= r1) return;
     const Cn* img = reinterpret_cast<const Cn*>(sb);
-    int o = (iv - r0) * P + hi32(u);
-    PGET_CHECK(o >= 0 && o + P + 1 < (r1 - r0 + 1) * P);
-    Cn q00 = img[o], q01 = img[o + 1], q10 = img[o + P], q11 = img[o + P + 1];
-    float fu = frac23(u), fv = frac23(v);
+    auto load = [&](SmpA<TR::NF4>& x, int64_t uu, int64_t vv, int ivv) {
+        const int o = (ivv - r0) * P + hi32(uu);
+        PGET_CHECK(o >= 0 && o + P + 1 < (r1 - r0 + 1) * P);
+        x.c00 = img[o]; x.c01 = img[o + 1]; x.c10 = img[o + P]; x.c11 = img[o + P + 1];
+        x.fu = frac23(uu);
+        x.fv = frac23(vv);
+    };
     StateA x_ = st;
-    while (true) {
+    // sample i with corners cur; prefetch sample i-1 into nx; alternating roles (no register copies)
+    auto step = [&](const SmpA<TR::NF4>& cur, SmpA<TR::NF4>& nx) -> bool {
         const int i2 = i - 1;
         const int64_t u2 = u - dU, v2 = v - dV;
         const int iv2 = hi32(v2);
         const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;
-        Cn n00, n01, n10, n11;
-        if (nxt) {
-            o = (iv2 - r0) * P + hi32(u2);
-            PGET_CHECK(o >= 0 && o + P + 1 < (r1 - r0 + 1) * P);
-            n00 = img[o]; n01 = img[o + 1]; n10 = img[o + P]; n11 = img[o + P + 1];
-        }
+        if (nxt) load(nx, u2, v2, iv2);
         float lam, mu, dlam = 0.f, dmu = 0.f;
         if constexpr (TR::NF4) {
-            const float2 x = bilerp2(lo2(q00), lo2(q01), lo2(q10), lo2(q11), fu, fv);
-            const float2 y = bilerp2(hi2(q00), hi2(q01), hi2(q10), hi2(q11), fu, fv);
+            const float2 x = bilerp2(lo2(cur.c00), lo2(cur.c01), lo2(cur.c10), lo2(cur.c11), cur.fu, cur.fv);
+            const float2 y = bilerp2(hi2(cur.c00), hi2(cur.c01), hi2(cur.c10), hi2(cur.c11), cur.fu, cur.fv);
             lam = x.x; mu = x.y; dlam = y.x; dmu = y.y;
         } else {
-            const float2 x = bilerp2(q00, q01, q10, q11, fu, fv);
+            const float2 x = bilerp2(cur.c00, cur.c01, cur.c10, cur.c11, cur.fu, cur.fv);
             lam = x.x; mu = x.y;
         }
         float arg;   // -log2(e) A_i
@@ -325,10 +330,11 @@ __device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int
         i = i2;
         u = u2;
         v = v2;
-        if (!nxt) break;
-        q00 = n00; q01 = n01; q10 = n10; q11 = n11;
-        fu = frac23(u);
-        fv = frac23(v);
+        return nxt;
+    };
+    SmpA<TR::NF4> sa, sb2;
+    load(sa, u, v, iv0);
+    while (step(sa, sb2) && step(sb2, sa)) {
     }
     st = x_;
 }
