@@ -115,7 +115,8 @@ enum {
 };
 
 /* Operation ids for pget_workspace_bytes. */
-enum { PGET_OP_FORWARD = 0, PGET_OP_JVP = 1, PGET_OP_VJP = 2, PGET_OP_GN_CG_STEP = 3, PGET_OP_GN_APPLY = 4 };
+enum { PGET_OP_FORWARD = 0, PGET_OP_JVP = 1, PGET_OP_VJP = 2, PGET_OP_GN_CG_STEP = 3, PGET_OP_GN_APPLY = 4,
+       PGET_OP_SAFEGUARD = 5 };
 
 /* Flags for pget_gn_cg_step. */
 #define PGET_GN_EVAL_TRIAL 1u   /* also evaluate f(u+s), rho, the accept decision and beta_next */
@@ -142,6 +143,24 @@ typedef struct {
     int32_t pad_;
     double cg_res[PGET_MAX_CG + 1]; /* ||z_k||, k = 0..n_cg                                   */
 } pget_gn_stats;
+
+/* Device-resident result of the Prop. 1 safeguard check, per batch member (array of `batch`).
+ * (Prop. 1 eq:rho_agreement, eq:uk+1_condition;
+ * Algorithm 2; m_k of eq:m-function.)
+ * m_k(s) = f(u) + <r, J s> + alpha (<L lam, L s_lam> + <L mu, L s_mu>) + 1/2 ||J s||^2
+ *          + alpha/2 ||L s||^2   (the stacked F~ = (F, sqrt(alpha) L) of reading Q10). */
+typedef struct {
+    double f;             /* f(u_k) = m_k(0)                                                  */
+    double f_cand;        /* f(u~)                                                            */
+    double m_cand;        /* m_k(s~), s~ = u~ - u_k                                           */
+    double m_lm;          /* m_k(s_k)                                                         */
+    double pred_cand;     /* m_k(0) - m_k(s~)                                                 */
+    double pred_lm;       /* m_k(0) - m_k(s_k)                                                */
+    double rho_cand;      /* (f(u_k) - f(u~)) / pred_cand; 0 when pred_cand == 0               */
+    double kappa;         /* the threshold used                                               */
+    int32_t accepted;     /* m_cand <= m_lm and pred_cand > 0 and rho_cand > kappa             */
+    int32_t pad_;
+} pget_safeguard_stats;
 
 const char* pget_status_string(pget_status s);
 const char* pget_last_error_message(void);
@@ -187,6 +206,21 @@ pget_status pget_gn_cg_step(pget_geometry g, const float* lam, const float* mu, 
                             float alpha, float beta, int32_t n_cg, uint32_t flags, float* s_lam,
                             float* s_mu, pget_gn_stats* stats_dev, void* ws, size_t ws_bytes,
                             pget_stream_t stream);
+
+/* Safeguarded acceptance of an externally supplied candidate u~ = (cand_lam, cand_mu) against the
+ * LM step s_k = (s_lam, s_mu) at u_k = (lam, mu) (Proposition 1; the check of
+ * Algorithm 2):  u_next = u~ if m_k(s~) <= m_k(s_k) and rho_k(s~) > kappa
+ * (and m_k(0) - m_k(s~) > 0, reading R-safeguard), else u_k + s_k (fp32 sum), per batch member.
+ * Costs two JVP launches (J s~ together with F(u_k), then J s_k) and one forward launch (F(u~)).
+ * alpha must be the penalty weight the step s_k was computed with; kappa > 0 (the paper's
+ * kappa = eta = 0.1, reading Q11).  All arrays are device memory of the image / sinogram shapes
+ * of the other calls; u_next_lam / u_next_mu may alias cand_* but not lam, mu, s_*.  `stats_dev`
+ * receives `batch` pget_safeguard_stats.  Errors as for pget_gn_cg_step. */
+pget_status pget_safeguard(pget_geometry g, const float* lam, const float* mu, const float* y_meas,
+                           const float* s_lam, const float* s_mu, const float* cand_lam,
+                           const float* cand_mu, float alpha, float kappa, float* u_next_lam,
+                           float* u_next_mu, pget_safeguard_stats* stats_dev, void* ws,
+                           size_t ws_bytes, pget_stream_t stream);
 
 /* Tracing.  Between pget_profile_begin and pget_profile_end every kernel the library
  * launches (on any stream, from any thread) is counted, and each projector launch is

@@ -50,6 +50,7 @@ def _load():
             ("orc_jvp", [P] * 7), ("orc_vjp", [P] * 6), ("orc_n_t", [P]),
             ("orc_gn_cg_step", [P, P, P, P, C.c_double, C.c_double, C.c_int, P, P, P]),
             ("orc_apply_H", [P, P, P, C.c_double, C.c_double, P, P]),
+            ("orc_safeguard", [P, P, P, P, P, P, P, P, C.c_double, C.c_double, P, P]),
         ]:
             f = getattr(_lib, name)
             f.argtypes = args
@@ -194,3 +195,28 @@ def ray_adjoint(lam_s, mu_s, delta):
     dm = np.zeros_like(l)
     lib.orc_ray_adjoint(len(l), _p(l), _p(m), float(delta), _p(dl), _p(dm))
     return dl, dm
+
+
+def safeguard(g, lam, mu, y, s_lam, s_mu, c_lam, c_mu, alpha, kappa=0.1):
+    """Prop. 1 safeguard (O8), per batch member.  Returns ((u_next_lam, u_next_mu), [dict per member])."""
+    lib = _load()
+    B = int(g.get("batch", 1))
+    shp = img_shape(g)
+    arrs = [_f64(a).reshape(shp) for a in (lam, mu, s_lam, s_mu, c_lam, c_mu)]
+    ys = _f64(y).reshape(B, -1)
+    g1 = dict(g, batch=1)
+    d = _desc(g1)
+    nl, nm, res = np.zeros(shp), np.zeros(shp), []
+    for m in range(B):
+        l, u, sl, sm, cl, cm = (np.ascontiguousarray(a[m]) for a in arrs)
+        ym = np.ascontiguousarray(ys[m])
+        un = np.zeros(2 * l.size)
+        out = np.zeros(7)
+        rc = lib.orc_safeguard(C.byref(d), _p(l), _p(u), _p(ym), _p(sl), _p(sm), _p(cl), _p(cm), float(alpha),
+                               float(kappa), _p(un), _p(out))
+        assert rc == 0, rc
+        nl[m] = un[:l.size].reshape(l.shape)
+        nm[m] = un[l.size:].reshape(l.shape)
+        res.append(dict(f=out[0], f_cand=out[1], m0=out[2], m_cand=out[3], m_lm=out[4], rho_cand=out[5],
+                        accepted=bool(out[6]), pred_cand=out[2] - out[3], pred_lm=out[2] - out[4]))
+    return (nl, nm), res

@@ -19,6 +19,8 @@
  *   LM step (J^T J + alpha L^T L + beta I) s = -grad f, m_k, rho_k
  *       -- PAPER.md:160-180 eq:m-function, eq:LMA-step; PAPER.md:248 eq:rho_agreement
  *       -- inner solver: plain CG (reading Q12) instead of the paper's SGP.
+ *   safeguard u_{k+1} = u~ iff m_k(s~) <= m_k(s_k) and rho_k(s~) > kappa
+ *       -- PAPER.md:241-258 Prop. 1 eq:uk+1_condition; Algorithm 2 PAPER.md:290-313 (O8, N2)
  *
  * Parity pins: tests/test_oracle.py (P1-P12 of SURVEY.md §8(c.4)); DESIGN.md "Oracle".
  * Compile: gcc -O2 -fopenmp -ffp-contract=off -fPIC -shared (no fast-math).
@@ -559,6 +561,71 @@ int orc_gn_cg_step(const orc_desc* g, const double* lam, const double* mu, const
     memcpy(s_lam, s, sizeof(double) * npx);
     memcpy(s_mu, s + npx, sizeof(double) * npx);
     free(r); free(ys); free(bvec); free(s); free(z); free(p); free(q); free(tl); free(tm); free(ut);
+    return 0;
+}
+
+/* ------------------------------------------------------------------ O8 Prop. 1 safeguard */
+/* m_k(s) of eq:m-function, written out for the stacked operator
+ * F~(u) = (F(lam,mu), sqrt(alpha) L lam, sqrt(alpha) L mu), y~ = (y, 0, 0) (reading Q10):
+ *   r~ = F~(u) - y~,  F~'_k s = (J s, sqrt(alpha) L s_lam, sqrt(alpha) L s_mu),
+ *   m_k(s) = 1/2 ||r~||^2 + <F~'_k s, r~> + 1/2 ||F~'_k s||^2.                                */
+static double model_m(const orc_desc* g, const double* lam, const double* mu, const double* r,
+                      const double* sl, const double* sm, double alpha, double* js, double* tl,
+                      double* tm)
+{
+    size_t ns = (size_t)g->batch * g->n_angles * g->n_banks * g->n_det;
+    size_t npx = (size_t)g->batch * g->n_px * g->n_px;
+    double half_rr = 0.5 * dot(r, r, ns), cross = 0.0, half_ss = 0.0;
+    orc_jvp(g, lam, mu, sl, sm, NULL, js);                      /* J s (eq:frechet) */
+    cross += dot(js, r, ns);
+    half_ss += 0.5 * dot(js, js, ns);
+    for (int f = 0; f < 2; ++f) {
+        orc_laplacian(g->n_px, g->batch, f ? mu : lam, tl);      /* sqrt(alpha) L u-part / sqrt(alpha) */
+        orc_laplacian(g->n_px, g->batch, f ? sm : sl, tm);       /* sqrt(alpha) L s-part / sqrt(alpha) */
+        half_rr += 0.5 * alpha * dot(tl, tl, npx);
+        cross += alpha * dot(tm, tl, npx);
+        half_ss += 0.5 * alpha * dot(tm, tm, npx);
+    }
+    return half_rr + cross + half_ss;
+}
+
+/* Proposition 1 / the check of Algorithm 2 for one
+ * candidate u~ = (c_lam, c_mu) and the LM step s_k = (s_lam, s_mu) at u_k = (lam, mu):
+ *   s~ = u~ - u_k;  rho_k(s~) = (f(u_k) - f(u~)) / (m_k(0) - m_k(s~))   (eq:rho_agreement)
+ *   u_{k+1} = u~ if m_k(s~) <= m_k(s_k) and rho_k(s~) > kappa, else u_k + s_k (eq:uk+1_condition)
+ * plus m_k(0) - m_k(s~) > 0 (reading R-safeguard: rho undefined / the model does not decrease).
+ * out: [0] f(u_k)  [1] f(u~)  [2] m_k(0)  [3] m_k(s~)  [4] m_k(s_k)  [5] rho_k(s~)  [6] accepted.
+ * u_next (2 npx, [lam | mu]) receives u_{k+1}.  The whole descriptor (all batch members) is one
+ * problem here; the Python wrapper calls it per member.                                           */
+int orc_safeguard(const orc_desc* g, const double* lam, const double* mu, const double* y,
+                  const double* s_lam, const double* s_mu, const double* c_lam, const double* c_mu,
+                  double alpha, double kappa, double* u_next, double* out)
+{
+    size_t npx = (size_t)g->batch * g->n_px * g->n_px;
+    size_t ns = (size_t)g->batch * g->n_angles * g->n_banks * g->n_det;
+    double* r = (double*)malloc(sizeof(double) * ns);
+    double* js = (double*)malloc(sizeof(double) * ns);
+    double* tl = (double*)malloc(sizeof(double) * npx);
+    double* tm = (double*)malloc(sizeof(double) * npx);
+    double* st = (double*)malloc(sizeof(double) * 2 * npx);
+    double* z = (double*)calloc(2 * npx, sizeof(double));
+    if (!r || !js || !tl || !tm || !st || !z) return -2;
+    double mis, reg;
+    double f0 = objective(g, lam, mu, y, alpha, &mis, &reg, r, tl);    /* r = F(u_k) - y */
+    for (size_t i = 0; i < npx; ++i) { st[i] = c_lam[i] - lam[i]; st[npx + i] = c_mu[i] - mu[i]; }
+    double m0 = model_m(g, lam, mu, r, z, z + npx, alpha, js, tl, tm);
+    double mc = model_m(g, lam, mu, r, st, st + npx, alpha, js, tl, tm);
+    double ml = model_m(g, lam, mu, r, s_lam, s_mu, alpha, js, tl, tm);
+    double fc = objective(g, c_lam, c_mu, y, alpha, &mis, &reg, js, tl);
+    double pred = m0 - mc;
+    double rho = pred != 0.0 ? (f0 - fc) / pred : 0.0;
+    int acc = mc <= ml && pred > 0.0 && rho > kappa;
+    for (size_t i = 0; i < npx; ++i) {
+        u_next[i] = acc ? c_lam[i] : lam[i] + s_lam[i];
+        u_next[npx + i] = acc ? c_mu[i] : mu[i] + s_mu[i];
+    }
+    out[0] = f0; out[1] = fc; out[2] = m0; out[3] = mc; out[4] = ml; out[5] = rho; out[6] = acc;
+    free(r); free(js); free(tl); free(tm); free(st); free(z);
     return 0;
 }
 

@@ -18,16 +18,16 @@ import numpy as np
 
 from ._build import LIB, build as _build_lib, needs_build as _needs_build
 
-__all__ = ["Geometry", "forward", "jvp", "vjp", "gn_apply", "gn_cg_step", "GNStats", "lib",
+__all__ = ["Geometry", "forward", "jvp", "vjp", "gn_apply", "gn_cg_step", "safeguard", "GNStats", "SafeguardStats", "lib",
            "PGET_GN_EVAL_TRIAL", "TABLES", "OPS"]
 
 PGET_GN_EVAL_TRIAL = 1
 PGET_MAX_CG = 256
 TABLES = {"angles": 0, "dirs": 1, "offsets": 2, "weights": 3, "tlat": 4, "clip": 5}
-OPS = {"forward": 0, "jvp": 1, "vjp": 2, "gn_cg_step": 3, "gn_apply": 4}
+OPS = {"forward": 0, "jvp": 1, "vjp": 2, "gn_cg_step": 3, "gn_apply": 4, "safeguard": 5}
 EXPORTED = ["pget_status_string", "pget_last_error_message", "pget_geometry_create", "pget_geometry_destroy",
             "pget_geometry_info", "pget_table_bytes", "pget_geometry_export", "pget_workspace_bytes",
-            "pget_forward", "pget_jvp", "pget_vjp", "pget_gn_apply", "pget_gn_cg_step", "pget_profile_begin",
+            "pget_forward", "pget_jvp", "pget_vjp", "pget_gn_apply", "pget_gn_cg_step", "pget_safeguard", "pget_profile_begin",
             "pget_profile_end"]
 MODES = ("forward", "jvp", "vjp", "gn")
 
@@ -61,6 +61,17 @@ class GNStats(C.Structure):
         return d
 
 
+class SafeguardStats(C.Structure):
+    _fields_ = [("f", C.c_double), ("f_cand", C.c_double), ("m_cand", C.c_double), ("m_lm", C.c_double),
+                ("pred_cand", C.c_double), ("pred_lm", C.c_double), ("rho_cand", C.c_double), ("kappa", C.c_double),
+                ("accepted", C.c_int32), ("pad_", C.c_int32)]
+
+    def to_dict(self):
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "pad_"}
+        d["accepted"] = bool(d["accepted"])
+        return d
+
+
 _lib = None
 
 
@@ -90,10 +101,11 @@ def lib():
         L.pget_vjp.argtypes = [P, P, P, P, P, P, P, S, P]
         L.pget_gn_apply.argtypes = [P, P, P, P, P, C.c_float, C.c_float, P, P, P, S, P]
         L.pget_gn_cg_step.argtypes = [P, P, P, P, C.c_float, C.c_float, C.c_int32, C.c_uint32, P, P, P, P, S, P]
+        L.pget_safeguard.argtypes = [P, P, P, P, P, P, P, P, C.c_float, C.c_float, P, P, P, P, S, P]
         L.pget_profile_begin.argtypes = [C.c_int32]
         L.pget_profile_end.argtypes = [P, P, P]
         for n in ("pget_profile_begin", "pget_profile_end", "pget_geometry_create", "pget_geometry_destroy", "pget_geometry_info", "pget_geometry_export",
-                  "pget_forward", "pget_jvp", "pget_vjp", "pget_gn_apply", "pget_gn_cg_step"):
+                  "pget_forward", "pget_jvp", "pget_vjp", "pget_gn_apply", "pget_gn_cg_step", "pget_safeguard"):
             getattr(L, n).restype = C.c_int
         _lib = L
     return _lib
@@ -282,3 +294,25 @@ def profile_end():
     tot = C.c_int64()
     _check(lib().pget_profile_end(ms, n, C.byref(tot)), "pget_profile_end")
     return {"ms": dict(zip(MODES, list(ms))), "launches": dict(zip(MODES, list(n))), "total_launches": tot.value}
+
+
+def safeguard(g: Geometry, lam, mu, y_meas, s_lam, s_mu, cand_lam, cand_mu, alpha, kappa=0.1, u_next=None,
+              ws=None, stream=None):
+    """Prop. 1 safeguard (pget_safeguard).  Returns ((u_next_lam, u_next_mu), [stats dict per member])."""
+    import torch
+    for t, n in ((lam, "lam"), (mu, "mu"), (s_lam, "s_lam"), (s_mu, "s_mu"), (cand_lam, "cand_lam"),
+                 (cand_mu, "cand_mu")):
+        _f32(t, g.img_shape, n)
+    _f32(y_meas, g.sino_shape, "y_meas")
+    if u_next is None:
+        u_next = (torch.empty(g.img_shape, dtype=torch.float32, device=lam.device),
+                  torch.empty(g.img_shape, dtype=torch.float32, device=lam.device))
+    B = g.info["batch"]
+    buf = torch.zeros(B * C.sizeof(SafeguardStats), dtype=torch.uint8, device=lam.device)
+    ws = g.workspace("safeguard") if ws is None else ws
+    _check(lib().pget_safeguard(g.handle, _ptr(lam), _ptr(mu), _ptr(y_meas), _ptr(s_lam), _ptr(s_mu), _ptr(cand_lam),
+                                _ptr(cand_mu), float(alpha), float(kappa), _ptr(u_next[0]), _ptr(u_next[1]),
+                                _ptr(buf), _ptr(ws), ws.numel(), _stream(stream)), "pget_safeguard")
+    host = buf.cpu().numpy().tobytes()
+    n = C.sizeof(SafeguardStats)
+    return u_next, [SafeguardStats.from_buffer_copy(host[m * n:(m + 1) * n]).to_dict() for m in range(B)]

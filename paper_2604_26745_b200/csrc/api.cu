@@ -230,8 +230,10 @@ WS carve(const Geometry& g, int op, char* base)
         off += align256(bytes);
         return p;
     };
-    const bool need2 = op == PGET_OP_FORWARD || op == PGET_OP_VJP || op == PGET_OP_GN_APPLY || op == PGET_OP_GN_CG_STEP;
-    const bool need4 = op == PGET_OP_JVP || op == PGET_OP_GN_APPLY || op == PGET_OP_GN_CG_STEP;
+    const bool guard = op == PGET_OP_SAFEGUARD;
+    const bool need2 = op == PGET_OP_FORWARD || op == PGET_OP_VJP || op == PGET_OP_GN_APPLY || op == PGET_OP_GN_CG_STEP ||
+                       guard;
+    const bool need4 = op == PGET_OP_JVP || op == PGET_OP_GN_APPLY || op == PGET_OP_GN_CG_STEP || guard;
     const bool needacc = op == PGET_OP_VJP || op == PGET_OP_GN_APPLY || op == PGET_OP_GN_CG_STEP;
     for (int k = 0; k < 2; ++k) {
         if (need2) w.img2[k] = reinterpret_cast<float2*>(take(img * sizeof(float2)));
@@ -251,6 +253,13 @@ WS carve(const Geometry& g, int op, char* base)
         for (float** v : vecs) *v = reinterpret_cast<float*>(take(n2 * sizeof(float)));
         w.part = reinterpret_cast<double*>(take(8 * B * kNblk * sizeof(double)));
         w.cg = reinterpret_cast<CGState*>(take(B * sizeof(CGState)));
+    }
+    if (guard) {
+        w.ysino = reinterpret_cast<float*>(take(ns * sizeof(float)));
+        w.dysino = reinterpret_cast<float*>(take(ns * sizeof(float)));
+        w.zl = reinterpret_cast<float*>(take(n2 * sizeof(float)));
+        w.zm = reinterpret_cast<float*>(take(n2 * sizeof(float)));
+        w.part = reinterpret_cast<double*>(take(12 * B * kNblk * sizeof(double)));
     }
     w.bytes = off;
     return w;
@@ -463,7 +472,7 @@ pget_status pget_geometry_export(pget_geometry h, int id, void* dst, size_t byte
 
 size_t pget_workspace_bytes(pget_geometry h, int op)
 {
-    if (!h || op < 0 || op > PGET_OP_GN_APPLY) return 0;
+    if (!h || op < 0 || op > PGET_OP_SAFEGUARD) return 0;
     return carve(h->g, op, nullptr).bytes + 256;
 }
 
@@ -656,6 +665,60 @@ pget_status pget_gn_cg_step(pget_geometry h, const float* lam, const float* mu, 
         scalar_kernel<<<sgrid, 128, 0, s>>>(SC_TRIAL, 0, P[0], P[1], nullptr, kNblk, w.cg, stats, B, alpha, beta); note();
         CK(cudaGetLastError());
     }
+    return PGET_OK;
+}
+
+// Prop. 1 safeguard (Algorithm 2): m_k(s~), m_k(s_k), f(u~), rho, accept.
+pget_status pget_safeguard(pget_geometry h, const float* lam, const float* mu, const float* y_meas, const float* s_lam,
+                           const float* s_mu, const float* cand_lam, const float* cand_mu, float alpha, float kappa,
+                           float* u_next_lam, float* u_next_mu, pget_safeguard_stats* stats, void* ws,
+                           size_t ws_bytes, pget_stream_t stream)
+{
+    WS w;
+    pget_status st = check_common(h, PGET_OP_SAFEGUARD, ws, ws_bytes, &w);
+    if (st) return st;
+    if ((st = check_ptrs({lam, mu, y_meas, s_lam, s_mu, cand_lam, cand_mu, u_next_lam, u_next_mu, stats},
+                         "pget_safeguard")))
+        return st;
+    if (!std::isfinite(alpha) || alpha < 0.f) return fail(PGET_ERR_INVALID_ARGUMENT, "alpha must be finite and >= 0");
+    if (!std::isfinite(kappa) || !(kappa > 0.f)) return fail(PGET_ERR_INVALID_ARGUMENT, "kappa must be finite and > 0");
+    for (const float* p : {lam, mu, s_lam, s_mu})
+        if (p == u_next_lam || p == u_next_mu)
+            return fail(PGET_ERR_INVALID_ARGUMENT, "pget_safeguard: u_next aliases lam, mu or s");
+    const Geometry& g = h->g;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int N = g.desc.n_px, B = g.desc.batch;
+    const int n2 = N * N;
+    const int nsper = g.n_ab * g.desc.n_det;
+    const dim3 vg(kNblk, B);
+    double* P[12];
+    for (int k = 0; k < 12; ++k) P[k] = w.part + static_cast<size_t>(k) * B * kNblk;
+    const size_t nimg = static_cast<size_t>(B) * n2;
+    // s~ = u~ - u;  F(u) and J s~ in one JVP launch
+    diff2_kernel<<<vec_grid(nimg), kVecThreads, 0, s>>>(cand_lam, cand_mu, lam, mu, w.zl, w.zm, nimg); note();
+    CK(cudaGetLastError());
+    if ((st = pack4(g, w, lam, mu, w.zl, w.zm, s))) return st;
+    if ((st = proj_out(g, w, MODE_JVP, w.ysino, w.dysino, s))) return st;
+    residual_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, y_meas, P[0], nsper); note();
+    regsq_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, P[1], N); note();
+    dotsq_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, w.dysino, P[2], P[3], nsper); note();
+    lapdot_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, w.zl, w.zm, P[4], P[5], N); note();
+    CK(cudaGetLastError());
+    // J s_k
+    if ((st = pack4(g, w, lam, mu, s_lam, s_mu, s))) return st;
+    if ((st = proj_out(g, w, MODE_JVP, nullptr, w.dysino, s))) return st;
+    dotsq_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, w.dysino, P[6], P[7], nsper); note();
+    lapdot_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, s_lam, s_mu, P[8], P[9], N); note();
+    CK(cudaGetLastError());
+    // f(u~)
+    if ((st = pack2(g, w, cand_lam, cand_mu, nullptr, nullptr, nullptr, nullptr, s))) return st;
+    if ((st = proj_out(g, w, MODE_FWD, w.ysino, nullptr, s))) return st;
+    residual_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, y_meas, P[10], nsper); note();
+    regsq_kernel<<<vg, kVecThreads, 0, s>>>(cand_lam, cand_mu, P[11], N); note();
+    guard_scalar_kernel<<<(B + 127) / 128, 128, 0, s>>>(w.part, kNblk, B, alpha, kappa, stats); note();
+    guard_select_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, s_lam, s_mu, cand_lam, cand_mu, stats, u_next_lam,
+                                                  u_next_mu, n2); note();
+    CK(cudaGetLastError());
     return PGET_OK;
 }
 

@@ -255,6 +255,98 @@ __device__ __forceinline__ double psum(const double* partial, int m, int nblk)
     return t;
 }
 
+// ---- Prop. 1 safeguard: model values m_k(s) from per-member partial sums
+// partial <a, b> and ||b||^2 of per-member vectors (sinograms)
+__global__ void dotsq_kernel(const float* __restrict__ a, const float* __restrict__ b, double* pdot, double* psq,
+                             int nper)
+{
+    __shared__ double sh[32];
+    const int m = blockIdx.y;
+    double d = 0.0, q = 0.0;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nper; e += gridDim.x * blockDim.x) {
+        const size_t k = static_cast<size_t>(m) * nper + e;
+        const double bv = b[k];
+        d += static_cast<double>(a[k]) * bv;
+        q += bv * bv;
+    }
+    const double td = block_sum(d, sh);
+    if (threadIdx.x == 0) pdot[m * gridDim.x + blockIdx.x] = td;
+    const double tq = block_sum(q, sh);
+    if (threadIdx.x == 0) psq[m * gridDim.x + blockIdx.x] = tq;
+}
+
+// partial <L u, L s> and ||L s||^2 over both parts (lam, mu)
+__global__ void lapdot_kernel(const float* __restrict__ ul, const float* __restrict__ um, const float* __restrict__ sl,
+                              const float* __restrict__ sm, double* pdot, double* psq, int N)
+{
+    __shared__ double sh[32];
+    const int m = blockIdx.y;
+    const size_t n2 = static_cast<size_t>(N) * N;
+    double d = 0.0, q = 0.0;
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n2;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(e % N), j = static_cast<int>(e / N);
+        const double a1 = lap_at(ul + m * n2, N, j, i), b1 = lap_at(sl + m * n2, N, j, i);
+        const double a2 = lap_at(um + m * n2, N, j, i), b2 = lap_at(sm + m * n2, N, j, i);
+        d += a1 * b1 + a2 * b2;
+        q += b1 * b1 + b2 * b2;
+    }
+    const double td = block_sum(d, sh);
+    if (threadIdx.x == 0) pdot[m * gridDim.x + blockIdx.x] = td;
+    const double tq = block_sum(q, sh);
+    if (threadIdx.x == 0) psq[m * gridDim.x + blockIdx.x] = tq;
+}
+
+// out = a - b over both parts (s~ = u~ - u)
+__global__ void diff2_kernel(const float* __restrict__ al, const float* __restrict__ am, const float* __restrict__ bl,
+                             const float* __restrict__ bm, float* ol, float* om, size_t n)
+{
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        ol[e] = al[e] - bl[e];
+        om[e] = am[e] - bm[e];
+    }
+}
+
+// one thread per member.  P: [0] 1/2||r||^2  [1] ||Lu||^2  [2] <r,Js~>  [3] ||Js~||^2  [4] <Lu,Ls~>
+// [5] ||Ls~||^2  [6..9] the same four for s_k  [10] 1/2||F(u~)-y||^2  [11] ||Lu~||^2
+__global__ void guard_scalar_kernel(const double* P, int nblk, int B, double alpha, double kappa,
+                                    pget_safeguard_stats* out)
+{
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= B) return;
+    auto v = [&](int k) { return psum(P + static_cast<size_t>(k) * B * nblk, m, nblk); };
+    pget_safeguard_stats S;
+    S.f = v(0) + 0.5 * alpha * v(1);
+    S.m_cand = S.f + v(2) + alpha * v(4) + 0.5 * (v(3) + alpha * v(5));
+    S.m_lm = S.f + v(6) + alpha * v(8) + 0.5 * (v(7) + alpha * v(9));
+    S.pred_cand = S.f - S.m_cand;
+    S.pred_lm = S.f - S.m_lm;
+    S.f_cand = v(10) + 0.5 * alpha * v(11);
+    S.rho_cand = S.pred_cand != 0.0 ? (S.f - S.f_cand) / S.pred_cand : 0.0;
+    S.kappa = kappa;
+    S.accepted = (S.m_cand <= S.m_lm && S.pred_cand > 0.0 && S.rho_cand > kappa) ? 1 : 0;
+    S.pad_ = 0;
+    out[m] = S;
+}
+
+// u_next = accepted ? u~ : u + s  (per member)
+__global__ void guard_select_kernel(const float* __restrict__ ul, const float* __restrict__ um,
+                                    const float* __restrict__ sl, const float* __restrict__ sm, const float* cl,
+                                    const float* cm, const pget_safeguard_stats* st, float* ol, float* om, int n2)
+{
+    const int m = blockIdx.y;
+    const bool acc = st[m].accepted != 0;
+    const size_t base = static_cast<size_t>(m) * n2;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n2; e += gridDim.x * blockDim.x) {
+        const size_t k = base + e;
+        const float a = acc ? cl[k] : ul[k] + sl[k];
+        const float b = acc ? cm[k] : um[k] + sm[k];
+        ol[k] = a;
+        om[k] = b;
+    }
+}
+
 // Scalar steps of the LM iteration (one thread per member).
 __global__ void scalar_kernel(int op, int k, const double* p0, const double* p1, const double* p2, int nblk,
                               CGState* st, pget_gn_stats* stats, int B, double alpha, double beta)

@@ -57,6 +57,16 @@ __global__ void cg_update2_kernel(const float* zl, const float* zm, float* pl, f
 __global__ void cg_fused_kernel(const double2* part, int G, float alpha, float beta, float* sl, float* sm, float* zl,
                                 float* zm, float* pl, float* pm, float* ql, float* qm, double* pg, double* pz,
                                 CGState* st, pget_gn_stats* stats, int k, int N, int B, int nblk);
+__global__ void dotsq_kernel(const float* a, const float* b, double* pdot, double* psq, int nper);
+__global__ void lapdot_kernel(const float* ul, const float* um, const float* sl, const float* sm, double* pdot,
+                              double* psq, int N);
+__global__ void diff2_kernel(const float* al, const float* am, const float* bl, const float* bm, float* ol,
+                             float* om, size_t n);
+__global__ void guard_scalar_kernel(const double* P, int nblk, int B, double alpha, double kappa,
+                                    pget_safeguard_stats* out);
+__global__ void guard_select_kernel(const float* ul, const float* um, const float* sl, const float* sm,
+                                    const float* cl, const float* cm, const pget_safeguard_stats* st, float* ol,
+                                    float* om, int n2);
 __global__ void scalar_kernel(int op, int k, const double* p0, const double* p1, const double* p2, int nblk,
                               CGState* st, pget_gn_stats* stats, int B, double alpha, double beta);
 

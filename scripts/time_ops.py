@@ -1,4 +1,5 @@
-"""Median device time (CUDA events) of each public op on one config: forward, JVP, VJP, GN apply."""
+"""Median device time (CUDA events) of each public op on one config: forward, JVP, VJP, GN apply,
+safeguard (its time includes the stats device-to-host read of the binding)."""
 import os
 import sys
 
@@ -22,6 +23,7 @@ ops = {
     "jvp": lambda: pg.jvp(g, lam, mu, dl, dm),
     "vjp": lambda: pg.vjp(g, lam, mu, y),
     "gn": lambda: pg.gn_apply(g, lam, mu, dl, dm, 1e-3, 0.0),
+    "safeguard": lambda: pg.safeguard(g, lam, mu, y, dl, dm, lam + dl, mu + dm, 1e-3),
 }
 nom = g.info["n_samples_nominal"]
 out = {}

@@ -1,0 +1,145 @@
+"""GPU-vs-oracle parity of the Prop. 1 safeguard (PAPER.md:241-258,
+Algorithm 2) through the C ABI (pget_safeguard).
+
+The candidates stand in for the learned operator G_theta (no trained weights, SURVEY.md §8 OUT):
+identity (u~ = u_k), the LM step itself (u_k + s_k), an overshoot (u_k + 1.5 s_k), the ground
+truth u†, a blend towards u†, and a wild random candidate.  s_k comes from the GPU's own
+gn_cg_step, rounded to fp32 and handed to both sides as an input (no CG chaos enters: reading
+R-LM concerns s_k itself, not the check).
+
+Tolerances (reading R-safeguard in DESIGN.md): f and m_k are sums of squares and cross terms of
+sinograms that the kernels produce within rel-L2 1e-5 (north star), so an absolute error of
+order 1e-5 * ||F|| * (||r|| + ||J s||) is the floor; the tests allow 4e-5 * (||y|| + ||r||) *
+(||r|| + ||J s~|| + ||J s_k||) plus 1e-6 relative.  The accept decision is compared exactly
+whenever both of its margins (m_k(s~) - m_k(s_k), rho - kappa) exceed that tolerance; u_next is
+compared bit-exactly against the selection the kernel's own decision implies."""
+import numpy as np
+import pytest
+
+import oracle as O
+import pget_data as P
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2604_26745_b200 as m
+    return m
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).cuda()
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def _candidates(l0, m0, sl, sm, lt, mt, seed, more=None):
+    rng = np.random.default_rng(seed)
+    out = {
+        "identity": (l0, m0),
+        "lm": (l0 + sl, m0 + sm),
+        "overshoot": (l0 + 1.5 * sl, m0 + 1.5 * sm),
+        "truth": (lt, mt),
+        "blend": (l0 + sl + 0.3 * (lt - l0 - sl), m0 + sm + 0.3 * (mt - m0 - sm)),
+        "wild": (l0 + 3.0 * rng.standard_normal(l0.shape), m0 + 0.3 * rng.standard_normal(m0.shape)),
+    }
+    if more is not None:       # u_k + a longer CG solve of the same model: m_k lower (Krylov monotonicity)
+        out["more_cg"] = (l0 + more[0], m0 + more[1])
+    return out
+
+
+def _check(pg, gd, g, lam, mu, y, sl, sm, lt, mt, alpha, seed=11, kappa=0.1, more=None):
+    f32 = lambda a: np.asarray(a, dtype=np.float32)
+    lam, mu, y, sl, sm = f32(lam), f32(mu), f32(y), f32(sl), f32(sm)
+    B = gd["batch"]
+    nx = lambda a, m: float(np.linalg.norm(np.asarray(a, np.float64).reshape(B, -1)[m]))
+    decided = []
+    for name, (cl, cm) in _candidates(lam, mu, sl, sm, lt, mt, seed, more).items():
+        cl, cm = f32(cl), f32(cm)
+        (ul, um), S = pg.safeguard(g, dev(lam), dev(mu), dev(y), dev(sl), dev(sm), dev(cl), dev(cm), alpha, kappa)
+        torch.cuda.synchronize()
+        (ol, om), So = O.safeguard(gd, lam, mu, y, sl, sm, cl, cm, alpha, kappa)
+        r = O.forward(gd, lam, mu) - y
+        js_c = O.jvp(gd, lam, mu, cl - lam, cm - mu)
+        js_l = O.jvp(gd, lam, mu, sl, sm)
+        for m in range(B):
+            a, o = S[m], So[m]
+            scale = 4e-5 * (nx(y, m) + nx(r, m)) * (nx(r, m) + nx(js_c, m) + nx(js_l, m))
+            tol = lambda v: scale + 1e-6 * abs(v)
+            for k in ("f", "f_cand", "m_cand", "m_lm"):
+                assert abs(a[k] - o[k]) <= tol(o[k]), f"{name}[{m}] {k}: {a[k]!r} vs {o[k]!r} (tol {tol(o[k]):.3e})"
+            if name == "identity":       # s~ = 0 exactly on both sides
+                assert a["pred_cand"] == 0.0 and a["rho_cand"] == 0.0 and not a["accepted"]
+            if o["pred_cand"] > 10 * scale:
+                rt = (2 * scale + 1e-6 * abs(o["f"])) / o["pred_cand"] * (1 + abs(o["rho_cand"]))
+                assert abs(a["rho_cand"] - o["rho_cand"]) <= rt + 1e-9, f"{name}[{m}] rho"
+                clear = abs(o["m_cand"] - o["m_lm"]) > 2 * tol(o["m_lm"]) and abs(o["rho_cand"] - kappa) > 2 * rt
+            else:
+                clear = o["m_cand"] - o["m_lm"] > 2 * tol(o["m_lm"]) or o["pred_cand"] < -2 * scale
+            if clear:
+                assert a["accepted"] == o["accepted"], f"{name}[{m}] decision"
+                decided.append((name, m, bool(o["accepted"])))
+            want_l = cl[m] if a["accepted"] else lam[m] + sl[m]     # fp32 sum, as the kernel
+            want_m = cm[m] if a["accepted"] else mu[m] + sm[m]
+            np.testing.assert_array_equal(host(ul)[m], want_l)
+            np.testing.assert_array_equal(host(um)[m], want_m)
+            if a["accepted"] == o["accepted"]:
+                np.testing.assert_allclose(host(ul)[m], ol[m], rtol=1e-6, atol=1e-6 * np.abs(ol[m]).max())
+    return decided
+
+
+def test_safeguard_cfg2(pg):
+    cid = 2
+    cfg = P.CONFIGS[cid]
+    gd = P.geometry_desc(cid)
+    g = pg.Geometry(gd)
+    lt, mt = P.make_phantom(cid)
+    y = P.poisson_noise(O.forward(gd, lt, mt), cfg.noise_peak, cfg.seed)
+    l0, m0 = P.initial_guess(gd["n_px"])
+    sl, sm, _ = pg.gn_cg_step(g, dev(l0), dev(m0), dev(y), cfg.alpha, 0.0, cfg.n_cg)
+    torch.cuda.synchronize()
+    decided = _check(pg, gd, g, l0, m0, y, host(sl), host(sm), lt, mt, cfg.alpha)
+    # the blend's and the LM step's own margins are below the cancellation-bound tolerance
+    # (m_k ~ 7 is f ~ 3958 minus pred ~ 3951 here); the other four are decided and rejected
+    # (the ground truth too: m_k(u† - u_k) = 19.5 > m_k(s_k) = 6.7)
+    assert {"identity", "overshoot", "truth", "wild"} <= {d[0] for d in decided}, decided
+
+
+def test_safeguard_small_batched(pg):
+    gd = dict(n_px=24, n_angles=16, n_banks=2, n_det=21, n_subrays=3, subray_sigma=0.4, step_px=0.5,
+              bank1_shift=0.0, batch=3)
+    g = pg.Geometry(gd)
+    rng = np.random.default_rng(4)
+    lt = rng.uniform(0.5, 1.5, size=(3, 24, 24))
+    mt = rng.uniform(0.05, 0.3, size=(3, 24, 24))
+    y = O.forward(gd, lt, mt).astype(np.float32)
+    l0 = np.full_like(lt, 0.8)
+    m0 = np.full_like(mt, 0.12)
+    # a short LM solve (2 CG steps) against a longer one (24) as the candidate: the candidate's model
+    # value is far below the step's, so acceptance is decided well outside the tolerance
+    sl, sm, _ = pg.gn_cg_step(g, dev(l0), dev(m0), dev(y), 1e-3, 0.0, 2)
+    ml, mm, _ = pg.gn_cg_step(g, dev(l0), dev(m0), dev(y), 1e-3, 0.0, 24)
+    torch.cuda.synchronize()
+    decided = _check(pg, gd, g, l0, m0, y, host(sl), host(sm), lt, mt, 1e-3, seed=5, more=(host(ml), host(mm)))
+    assert len(decided) >= 12, decided
+    assert any(d[2] for d in decided), decided       # at least one clear acceptance
+
+
+def test_safeguard_errors(pg):
+    gd = dict(n_px=16, n_angles=8, n_banks=2, n_det=9, n_subrays=1, subray_sigma=0.4, step_px=0.5,
+              bank1_shift=0.0, batch=1)
+    g = pg.Geometry(gd)
+    z = torch.zeros(g.img_shape, device="cuda")
+    y = torch.zeros(g.sino_shape, device="cuda")
+    with pytest.raises(RuntimeError, match="kappa"):
+        pg.safeguard(g, z, z, y, z, z, z, z, 1e-3, kappa=0.0)
+    with pytest.raises(RuntimeError, match="alpha"):
+        pg.safeguard(g, z, z, y, z, z, z, z, -1.0)
+    with pytest.raises(RuntimeError, match="aliases"):
+        pg.safeguard(g, z, z.clone(), y, z.clone(), z.clone(), z.clone(), z.clone(), 1e-3, u_next=(z, z.clone()))

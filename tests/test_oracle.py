@@ -411,3 +411,103 @@ def test_p1_sample_counts_golden(cid):
     assert int(np.clip(cl[..., 1] - cl[..., 0] + 1, 0, None).sum()) * g["batch"] == gold["samples"]
     assert cl[..., 0].size * g["batch"] == gold["rays"]
     assert t["n_t"] == gold["n_t"]
+
+
+# ----------------------------------------------------------------------------- P13 safeguard (O8, N2)
+def _lm_case(n_px=24, n_angles=16, n_cg=6):
+    cfg = P.CONFIGS[2]
+    g = P.geometry_desc(2, n_px=n_px, n_angles=n_angles)
+    lt, mt = P.make_phantom(2, n_px=n_px)
+    y = P.poisson_noise(O.forward(g, lt, mt), 1e4, 2)
+    l0, m0 = P.initial_guess(n_px)
+    sl, sm, st = O.gn_cg_step(g, l0, m0, y, cfg.alpha, 0.0, n_cg)
+    return cfg, g, (lt, mt), y, (l0, m0), (sl, sm), st
+
+
+def test_p13_candidate_equal_to_lm_step_matches_vjp_route():
+    """u~ = u_k + s_k: m_k(s~) = m_k(s_k), and pred / rho equal the LM wrap's values, which that
+    route computes as <b,s> - 1/2(...) with b from the VJP (adjoint of the JVP used here)."""
+    cfg, g, _, y, (l0, m0), (sl, sm), st = _lm_case()
+    (nl, nm), [r] = O.safeguard(g, l0, m0, y, sl, sm, l0 + sl, m0 + sm, cfg.alpha, 0.1)
+    assert abs(r["m0"] - st["f"]) <= 1e-12 * st["f"]            # m_k(0) = f(u_k)
+    assert abs(r["m_cand"] - r["m_lm"]) <= 1e-12 * st["f"]
+    assert abs(r["pred_lm"] - st["pred"]) <= 1e-8 * st["pred"]
+    assert abs(r["f_cand"] - st["f_trial"]) <= 1e-12 * st["f"]
+    assert abs(r["rho_cand"] - st["rho"]) <= 1e-7 * abs(st["rho"])
+    assert r["accepted"] == st["accepted"]
+    np.testing.assert_array_equal(nl, l0 + sl)
+
+
+def test_p13_model_exact_for_lambda_only_steps():
+    """F is linear in lam (eq:frechet: D_lam F[dlam] = F(dlam, mu)) and the penalty is quadratic,
+    so for s = (s_lam, 0) the model is exact: m_k(s) = f(u_k + s) for any s_lam."""
+    cfg, g, _, y, (l0, m0), _, _ = _lm_case(n_px=16, n_angles=8)
+    rng = np.random.default_rng(5)
+    z = np.zeros_like(l0)
+    for scale in (1e-2, 1.0, 30.0):
+        dl = scale * rng.standard_normal(l0.shape)
+        _, [r] = O.safeguard(g, l0, m0, y, z, z, l0 + dl, m0, cfg.alpha, 0.1)
+        assert abs(r["m_cand"] - r["f_cand"]) <= 1e-10 * max(r["f_cand"], r["f"])
+
+
+def test_p13_model_slope_and_curvature():
+    """d/dt m_k(t s)|0 = d/dt f(u_k + t s)|0 (central differences of f); m_k(t s) is a quadratic in t
+    (third differences vanish); and for a CG step from 0 with beta = 0, t = 1 minimises m_k(t s_k)
+    (Galerkin condition <s, H s> = <b, s>)."""
+    cfg, g, _, y, (l0, m0), (sl, sm), _ = _lm_case()
+    rng = np.random.default_rng(9)
+    dl, dm = 0.05 * rng.standard_normal(l0.shape), 0.01 * rng.standard_normal(m0.shape)
+    z = np.zeros_like(l0)
+
+    def m_of(t, al=dl, am=dm):
+        _, [r] = O.safeguard(g, l0, m0, y, z, z, l0 + t * al, m0 + t * am, cfg.alpha, 0.1)
+        return r["m_cand"], r["f_cand"], r["f"]
+
+    h = 1e-4
+    mp, fp, f0 = m_of(h)
+    mn, fn, _ = m_of(-h)
+    assert abs((mp - mn) - (fp - fn)) <= 1e-5 * abs(fp - fn)
+    vals = [m_of(t)[0] for t in (0.0, 1.0, 2.0, 3.0)]
+    third = vals[3] - 3 * vals[2] + 3 * vals[1] - vals[0]
+    assert abs(third) <= 1e-9 * max(abs(v) for v in vals)
+    ms = [m_of(t, sl, sm)[0] for t in (0.9, 1.0, 1.1)]
+    assert ms[1] < ms[0] and ms[1] < ms[2]
+
+
+def test_p13_decision_rule_cases():
+    """Each condition of eq:uk+1_condition rejects on its own: u~ = u_k (no model decrease),
+    u~ = u_k + 1.5 s_k (m_k(s~) > m_k(s_k) by the Galerkin property), a wild candidate (model rises);
+    u~ = u_k + s_k is accepted exactly when the LM step is."""
+    cfg, g, _, y, (l0, m0), (sl, sm), st = _lm_case()
+    rng = np.random.default_rng(3)
+    cases = {
+        "identity": (l0, m0),
+        "overshoot": (l0 + 1.5 * sl, m0 + 1.5 * sm),
+        "wild": (l0 + 5.0 * rng.standard_normal(l0.shape), m0 + rng.standard_normal(m0.shape)),
+        "lm": (l0 + sl, m0 + sm),
+    }
+    out = {k: O.safeguard(g, l0, m0, y, sl, sm, cl, cm, cfg.alpha, 0.1) for k, (cl, cm) in cases.items()}
+    r = out["identity"][1][0]
+    assert r["pred_cand"] == 0.0 and r["rho_cand"] == 0.0 and not r["accepted"]
+    np.testing.assert_array_equal(out["identity"][0][0], l0 + sl)
+    r = out["overshoot"][1][0]
+    assert r["m_cand"] > r["m_lm"] and not r["accepted"]
+    r = out["wild"][1][0]
+    # f rises and the model rises more: rho > kappa although the candidate is worse; the model tests
+    # (m_k(s~) <= m_k(s_k), pred > 0) reject it
+    assert r["f_cand"] > r["f"] and r["pred_cand"] < 0 and r["m_cand"] > r["m_lm"] and not r["accepted"]
+    assert out["lm"][1][0]["accepted"] == st["accepted"]
+
+
+def test_p13_ground_truth_candidate_noise_free():
+    """Noise-free data y = F(u†) and u~ = u†: f(u~) is the penalty alone, (alpha/2)||L u†||^2."""
+    cfg = P.CONFIGS[2]
+    n = 16
+    g = P.geometry_desc(2, n_px=n, n_angles=8)
+    lt, mt = P.make_phantom(2, n_px=n)
+    y = O.forward(g, lt, mt)
+    l0, m0 = P.initial_guess(n)
+    sl, sm, _ = O.gn_cg_step(g, l0, m0, y, cfg.alpha, 0.0, 4)
+    _, [r] = O.safeguard(g, l0, m0, y, sl, sm, lt, mt, cfg.alpha, 0.1)
+    reg = 0.5 * cfg.alpha * (np.sum(O.laplacian(lt) ** 2) + np.sum(O.laplacian(mt) ** 2))
+    assert abs(r["f_cand"] - reg) <= 1e-12 * max(reg, 1e-300) + 1e-14 * r["f"]
