@@ -574,6 +574,7 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
         const size_t wpbase2 = (static_cast<size_t>(ti.m) * A.n_ab + dup_of(A, ti.ab + 1)) * A.n_det;
         float2* slot = A.slots + static_cast<size_t>(ti.slot) * A.N * A.Ns;
         const int npairs = P >> 1;
+        const float inv_np = 1.0f / static_cast<float>(npairs);
         // columns the task's rays can touch in a band of rows [v0, v1] (oriented frame): between the
         // lines of its first and last ray; the band flush reads and clears only those (a detector
         // range of an angle-bank flushes its share of the image, not all of it)
@@ -654,32 +655,28 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                     qlo = max(0, static_cast<int>(floor(umin)) - 2) >> 1;
                     qhi = min(P - 1, static_cast<int>(floor(umax)) + 3) >> 1;
                 }
-                int off = (r0 * npairs + qlo) % NT;   // (r * npairs + qlo) % NT, advanced per row (no division)
-                for (int r = r0; r <= r1; ++r) {
-                    if (r > r0) {
-                        off += npairs;
-                        while (off >= NT) off -= NT;
-                    }
-                    if (r == carry || PGET_ABLATE == 2) continue;
+                // flat element index e = r * npairs + q over the band's rows; thread tid takes e = tid (mod NT)
+                const int e_beg = r0 * npairs, e_end = (r1 + 1) * npairs;
+                for (int e = e_beg + (tid - e_beg % NT + NT) % NT; e < e_end; e += NT) {
+                    int r = __float2int_rd(static_cast<float>(e) * inv_np);
+                    int q = e - r * npairs;
+                    if (q < 0) { --r; q += npairs; } else if (q >= npairs) { ++r; q -= npairs; }
+                    if (r == carry || q < qlo || q > qhi || PGET_ABLATE == 2) continue;
                     const int lr = flip ? r0 + A.RbB - r : r - r0;
                     PGET_CHECK(lr >= 0 && lr < RB1);
-                    int q0 = tid - off;
-                    if (q0 < 0) q0 += NT;
-                    for (int q = qlo + q0; q <= qhi; q += NT) {
-                        float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+                    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 4
-                        for (int w = 0; w < W; ++w) {
-                            float4* e = reinterpret_cast<float4*>(wacc_all + (static_cast<size_t>(w) * RB1 + lr) * P) + q;
-                            const float4 x = *e;
-                            sum.x += x.x; sum.y += x.y; sum.z += x.z; sum.w += x.w;
-                            *e = make_float4(0.f, 0.f, 0.f, 0.f);
-                        }
-                        const int ir = r - kHalo, ic = 2 * q - kHalo;
-                        if (ir >= 0 && ir < A.N && ic >= 0 && ic < A.Ns) {
-                            float4* dst = reinterpret_cast<float4*>(slot + static_cast<size_t>(ir) * A.Ns + ic);
-                            if (store) *dst = sum;
-                            else atomicAdd(dst, sum);
-                        }
+                    for (int w = 0; w < W; ++w) {
+                        float4* el = reinterpret_cast<float4*>(wacc_all + (static_cast<size_t>(w) * RB1 + lr) * P) + q;
+                        const float4 x = *el;
+                        sum.x += x.x; sum.y += x.y; sum.z += x.z; sum.w += x.w;
+                        *el = make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                    const int ir = r - kHalo, ic = 2 * q - kHalo;
+                    if (ir >= 0 && ir < A.N && ic >= 0 && ic < A.Ns) {
+                        float4* dst = reinterpret_cast<float4*>(slot + static_cast<size_t>(ir) * A.Ns + ic);
+                        if (store) *dst = sum;
+                        else atomicAdd(dst, sum);
                     }
                 }
                 __syncthreads();   // rings zeroed before the next band's scatter
