@@ -5,7 +5,7 @@
 // every CTA processes, from the exact per-task work (nominal samples of the task's rays, known from
 // the clip table):
 //   * many tasks per CTA (>= 8): contiguous member-major ranges, whole angle-banks;
-//   * otherwise the angle-banks are cut into p equal detector ranges (p = 1..4, the p with the
+//   * otherwise the angle-banks are cut into p equal detector ranges (p = 1..2, the p with the
 //     smallest estimated makespan, a part costing work/p + a fixed per-part overhead) and the parts
 //     are assigned longest-first to the least-loaded CTA (LPT).
 // For the adjoint kind every task also gets a partial-gradient slot: consecutive tasks of one CTA
@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdlib>
 #include <map>
 #include <numeric>
 #include <queue>
@@ -106,7 +107,12 @@ void build_schedule(const Geometry& g, int kind, int C, Schedule* S)
         int best_p = 1;
         std::vector<int> best_owner;
         struct Item { double w; int m, k, q; };
-        for (int p = 1; p <= std::min(4, nd); ++p) {
+        // p <= 2: measured on configs 2-4 (scripts/pmax_exp.sh), p = 3 or 4 is never faster than p = 2
+        // (narrower parts mean fewer ray groups, so fewer warps per CTA and emptier comb lanes), and
+        // p = 2 beats whole angle-banks on configs 2-4 (JVP config 2: p=3 0.198 ms, p=2 0.170 ms)
+        int pmax = std::min(2, nd);
+        if (const char* e = std::getenv("PGET_SCHED_PMAX")) pmax = std::max(1, std::min(pmax, std::atoi(e)));   // experiments
+        for (int p = 1; p <= pmax; ++p) {
             std::vector<Item> items;
             for (int m = 0; m < B; ++m)
                 for (int k = 0; k < ntab; ++k)
