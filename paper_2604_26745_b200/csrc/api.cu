@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <atomic>
 #include <mutex>
@@ -147,6 +148,72 @@ ProjCfg proj_cfg(const Geometry& g, int mode)
 
 int slot_pitch(const Geometry& g) { return (g.desc.n_px + 1) & ~1; }
 
+// Launch configuration of the segmented adjoint.  Phase A: 8 warps,
+// 2 CTAs per SM, up to 2 groups of 32 adjacent rays per warp, shared memory = two float4 stage
+// buffers.  Phase B: one CTA per SM, one comb group per warp (W = the group count over the fewest
+// passes of <= 16 warps), shared memory = two float2 stages + the warps' band accumulators + the
+// per-ray constants.  Band heights: the largest (<= 32 rows) that fits.
+struct SegCfg {
+    int WA, maxgA, passesA, RbA, gridA, stageA;
+    size_t smemA;
+    int WB, passesB, RbB, gridB, stageB, off_wacc, off_rout, off_gsh, off_rsc, off_q1;
+    size_t smemB;
+};
+
+SegCfg seg_cfg(const Geometry& g)
+{
+    const Schedule& S = g.sch[kSchedAdj];
+    SegCfg c;
+    const int ngA = (g.R + 31) / 32;
+    c.WA = 8;
+    c.maxgA = ngA > c.WA ? 2 : 1;
+    c.passesA = std::max(1, (ngA + c.WA * c.maxgA - 1) / (c.WA * c.maxgA));
+    const size_t per_sm = 233472;
+    {
+        const size_t budget = std::min<size_t>(g.smem_optin, per_sm / 2 - 1024);
+        int Rb = std::min(32, g.P - 1);
+        size_t SB = 0;
+        for (; Rb > 1; --Rb) {
+            SB = align128(static_cast<size_t>(Rb + 1) * g.P * sizeof(float4));
+            if (128 + 2 * SB <= budget) break;
+        }
+        SB = align128(static_cast<size_t>(Rb + 1) * g.P * sizeof(float4));
+        c.RbA = Rb;
+        c.stageA = static_cast<int>(SB);
+        c.smemA = 128 + 2 * SB;
+        c.gridA = S.CA > 0 ? S.CA : 2 * g.sm_count;
+    }
+    {
+        const int ngB = std::max(1, S.max_gB);
+        const int passes = (ngB + 15) / 16;
+        c.WB = std::max(4, (ngB + passes - 1) / passes);
+        c.passesB = (ngB + c.WB - 1) / c.WB;
+        const size_t budget = std::min<size_t>(g.smem_optin, per_sm - 1024);
+        const size_t rout_b = align128(2 * sizeof(float) * g.R), gsh_b = align128(sizeof(float4) * g.R);
+        const size_t rsc_b = align128(sizeof(float) * g.R), q1_b = align128(sizeof(float2) * g.R);
+        const size_t fixed = 128 + rout_b + gsh_b + rsc_b + q1_b;
+        int Rb = std::min(32, g.P - 1);
+        size_t SB = 0, wacc = 0;
+        for (; Rb > 1; --Rb) {
+            SB = align128(static_cast<size_t>(Rb + 1) * g.P * sizeof(float2));
+            wacc = align128(static_cast<size_t>(c.WB) * (Rb + 1) * g.P * sizeof(float2));
+            if (fixed + 2 * SB + wacc <= budget) break;
+        }
+        SB = align128(static_cast<size_t>(Rb + 1) * g.P * sizeof(float2));
+        wacc = align128(static_cast<size_t>(c.WB) * (Rb + 1) * g.P * sizeof(float2));
+        c.RbB = Rb;
+        c.stageB = static_cast<int>(SB);
+        c.off_wacc = static_cast<int>(128 + 2 * SB);
+        c.off_rout = static_cast<int>(c.off_wacc + wacc);
+        c.off_gsh = static_cast<int>(c.off_rout + rout_b);
+        c.off_rsc = static_cast<int>(c.off_gsh + gsh_b);
+        c.off_q1 = static_cast<int>(c.off_rsc + rsc_b);
+        c.smemB = c.off_q1 + q1_b;
+        c.gridB = S.C > 0 ? S.C : g.sm_count;
+    }
+    return c;
+}
+
 ProjArgs base_args(const Geometry& g, const ProjCfg& c)
 {
     ProjArgs A;
@@ -203,12 +270,64 @@ pget_status run_proj(const Geometry& g, int mode, const ProjCfg& c, const ProjAr
     return PGET_OK;
 }
 
+// the segmented adjoint: phase A then phase B on s, bracketed together by the profiler's events
+pget_status run_seg(const Geometry& g, int mode, ProjArgs A, float* segp, cudaStream_t s)
+{
+    const Schedule& S = g.sch[kSchedAdj];
+    const SegCfg c = seg_cfg(g);
+    cudaEvent_t ea = nullptr, eb = nullptr;
+    if (g_prof.on.load(std::memory_order_relaxed)) {
+        std::lock_guard<std::mutex> lk(g_prof.mu);
+        g_prof.total += 2;
+        g_prof.mode_launches[mode]++;
+        if (g_prof.used + 2 <= g_prof.pool.size()) {
+            ea = g_prof.pool[g_prof.used++];
+            eb = g_prof.pool[g_prof.used++];
+            g_prof.recs.push_back({mode, ea, eb});
+        }
+    }
+    A.segp = segp;
+    A.K = S.K;
+    A.seg_rows = S.d_seg_rows;
+    A.n_groups = S.max_gB;
+    A.groups = S.d_groups;
+    if (ea) cudaEventRecord(ea, s);
+    // phase A
+    A.units = S.d_unitsA;
+    A.u_begin = S.d_ua_begin;
+    A.stages = S.d_stA;
+    A.s_begin = S.d_sa_begin;
+    A.RbA = c.RbA;
+    A.passesA = c.passesA;
+    A.stage_bytes = c.stageA;
+    cudaError_t e = launch_seg(0, mode, c.maxgA, g.dup, A, c.gridA, c.WA * 32, c.smemA, s);
+    if (e == cudaSuccess) {
+        A.units = S.d_unitsB;
+        A.u_begin = S.d_ub_begin;
+        A.stages = S.d_stB;
+        A.s_begin = S.d_sb_begin;
+        A.RbB = c.RbB;
+        A.passesB = c.passesB;
+        A.stage_bytes = c.stageB;
+        A.off_wacc = c.off_wacc;
+        A.off_rout = c.off_rout;
+        A.off_gsh = c.off_gsh;
+        A.off_rsc = c.off_rsc;
+        A.off_q1 = c.off_q1;
+        e = launch_seg(1, mode, 1, g.dup, A, c.gridB, c.WB * 32, c.smemB, s);
+    }
+    if (eb) cudaEventRecord(eb, s);
+    if (e != cudaSuccess) return cuda_fail(e, "segmented projector launch");
+    return PGET_OK;
+}
+
 // ---- workspace carving
 struct WS {
     float2* img2[2] = {nullptr, nullptr};
     float4* img4[2] = {nullptr, nullptr};
     float2* slots = nullptr;
     double2* gacc = nullptr;  // [G][B][N][N] fp64 partial gradients (g_lam, g_mu), G = ProjCfg::G
+    float* segp = nullptr;    // segmented adjoint: [n_canon][kSegFields][R] phase-A partial sums
     float *ysino = nullptr, *dysino = nullptr;
     float *bl = nullptr, *bm = nullptr, *zl = nullptr, *zm = nullptr, *pl = nullptr, *pm = nullptr;
     float *ql = nullptr, *qm = nullptr, *ul = nullptr, *um = nullptr;
@@ -245,6 +364,9 @@ WS carve(const Geometry& g, int op, char* base)
         w.slots = reinterpret_cast<float2*>(take(static_cast<size_t>(std::max(1, g.sch[kSchedAdj].n_slots)) * plane *
                                                  sizeof(float2)));
         w.gacc = reinterpret_cast<double2*>(take(static_cast<size_t>(c.G) * n2 * sizeof(double2)));
+        if (g.adj_seg)
+            w.segp = reinterpret_cast<float*>(take(static_cast<size_t>(g.sch[kSchedAdj].n_canon) * kSegFields *
+                                                   g.R * sizeof(float)));
     }
     if (op == PGET_OP_GN_CG_STEP) {
         w.ysino = reinterpret_cast<float*>(take(ns * sizeof(float)));
@@ -308,6 +430,11 @@ void free_device_tables(Geometry* g)
     for (Schedule& S : g->sch) {
         cudaFree(S.d_cta_begin); cudaFree(S.d_tasks); cudaFree(S.d_groups); cudaFree(S.d_red_off); cudaFree(S.d_red_slot);
         S.d_cta_begin = nullptr; S.d_tasks = nullptr; S.d_groups = nullptr; S.d_red_off = nullptr; S.d_red_slot = nullptr;
+        cudaFree(S.d_unitsA); cudaFree(S.d_unitsB); cudaFree(S.d_ua_begin); cudaFree(S.d_ub_begin);
+        cudaFree(S.d_sa_begin); cudaFree(S.d_sb_begin); cudaFree(S.d_stA); cudaFree(S.d_stB); cudaFree(S.d_seg_rows);
+        S.d_unitsA = S.d_unitsB = nullptr;
+        S.d_ua_begin = S.d_ub_begin = S.d_sa_begin = S.d_sb_begin = S.d_seg_rows = nullptr;
+        S.d_stA = S.d_stB = nullptr;
     }
 }
 
@@ -362,10 +489,17 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     std::vector<RayP> rays;
     build_ray_params(g, &rays);
     if (e == cudaSuccess) e = cudaMalloc(&g.d_rays, rays.size() * sizeof(RayP));
+    if (const char* ev = std::getenv("PGET_ADJ_FUSED")) g.adj_seg = std::atoi(ev) == 0;   // A/B experiments
     for (int k = 0; k < 3 && e == cudaSuccess; ++k) {
         const int mode = k == kSchedFwd ? MODE_FWD : (k == kSchedJvp ? MODE_JVP : MODE_VJP);
         Schedule& S = g.sch[k];
-        build_schedule(g, k, g.sm_count * proj_ctas_per_sm(mode), &S);
+        if (k == kSchedAdj && g.adj_seg) {
+            build_adj_schedule(g, rays, 2 * g.sm_count, g.sm_count, &S);
+            const SegCfg sc = seg_cfg(g);
+            build_adj_stages(sc.RbA, sc.passesA, sc.RbB, sc.passesB, &S);
+        } else {
+            build_schedule(g, k, g.sm_count * proj_ctas_per_sm(mode), &S);
+        }
         auto up = [&](auto** dst, const auto& v) {
             using T = typename std::remove_reference<decltype(v)>::type::value_type;
             if (e == cudaSuccess) e = cudaMalloc(dst, std::max<size_t>(1, v.size()) * sizeof(T));
@@ -376,6 +510,17 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
         up(&S.d_groups, S.groups);
         up(&S.d_red_off, S.red_off);
         up(&S.d_red_slot, S.red_slot);
+        if (k == kSchedAdj && g.adj_seg) {
+            up(&S.d_unitsA, S.unitsA);
+            up(&S.d_unitsB, S.unitsB);
+            up(&S.d_ua_begin, S.ua_begin);
+            up(&S.d_ub_begin, S.ub_begin);
+            up(&S.d_stA, S.stA);
+            up(&S.d_stB, S.stB);
+            up(&S.d_sa_begin, S.sa_begin);
+            up(&S.d_sb_begin, S.sb_begin);
+            up(&S.d_seg_rows, S.seg_rows);
+        }
     }
     if (e == cudaSuccess) e = cudaMalloc(&g.d_w, g.wf.size() * sizeof(float));
     if (e == cudaSuccess) e = cudaMemcpy(g.d_rays, rays.data(), rays.size() * sizeof(RayP), cudaMemcpyHostToDevice);
@@ -384,6 +529,14 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
         const size_t sm = proj_cfg(g, mode).smem;
         if (sm > g.smem_optin) e = cudaErrorInvalidConfiguration;
         else e = set_proj_smem_limit(mode, sm);
+    }
+    if (g.adj_seg && e == cudaSuccess) {
+        const SegCfg sc = seg_cfg(g);
+        if (sc.smemA > g.smem_optin || sc.smemB > g.smem_optin) e = cudaErrorInvalidConfiguration;
+        for (int mode : {MODE_VJP, MODE_GN}) {
+            if (e == cudaSuccess) e = set_seg_smem_limit(0, mode, sc.smemA);
+            if (e == cudaSuccess) e = set_seg_smem_limit(1, mode, sc.smemB);
+        }
     }
     if (prev >= 0) cudaSetDevice(prev);
     if (e != cudaSuccess) {
@@ -516,7 +669,7 @@ static pget_status proj_adjoint(const Geometry& g, const WS& w, int mode, const 
     for (int k = 0; k < 2; ++k) { A.img2[k] = w.img2[k]; A.img4[k] = w.img4[k]; }
     A.slots = w.slots;
     A.win = win;
-    pget_status st = run_proj(g, mode, c, A, s);
+    pget_status st = g.adj_seg ? run_seg(g, mode, A, w.segp, s) : run_proj(g, mode, c, A, s);
     if (st) return st;
     const int N = g.desc.n_px;
     const dim3 grid((N + 31) / 32, (N + 31) / 32, g.desc.batch * c.G);

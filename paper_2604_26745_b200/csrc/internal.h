@@ -40,6 +40,51 @@ struct TaskD {
 };
 static_assert(sizeof(TaskD) == 32, "TaskD layout");
 
+// Segmented adjoint (VJP / GN): a unit is (member, traced angle-bank, row segment k of K) over all
+// detectors.  Phase A traces every ray of the unit through the segment's rows and stores per-ray
+// partial sums; phase B combines the K partials of each ray (optical depth before the segment, the
+// tail of G, ...) and scatters the segment's adjoint.  Rows are those of the oriented frame
+// (padded); segment k covers sample rows [seg_rows[k], seg_rows[k+1]).
+struct UnitD {
+    int32_t m, ab;        // batch member, traced angle-bank
+    int32_t seg;          // row segment
+    int32_t canon;        // (m * n_tab + tab) * K + seg: index of the unit's partials
+    int32_t slot;         // phase B: partial-gradient slot
+    int32_t flags;        // kTaskClass1; kTaskFirst: first unit of its slot (the slot is zeroed first)
+    int32_t pad0, pad1;
+};
+static_assert(sizeof(UnitD) == 32, "UnitD layout");
+
+// One staged band of a phase: unit (index into the phase's unit list) and band j of the unit in
+// processing order.
+struct StageD {
+    int32_t unit, j;
+};
+
+// Sample-row entry of a segment: the largest sample index i <= ihi whose row lies inside the
+// segment when the ray is walked from its detector end (dV > 0: rows decrease with i, so the bound
+// is the exclusive top row `rtop`; dV < 0: the inclusive bottom row `rbot`).  May be < ilo (empty).
+#ifdef __CUDACC__
+#define PGET_HD __host__ __device__
+#else
+#define PGET_HD
+#endif
+PGET_HD inline int64_t pget_floordiv(int64_t a, int64_t b)   // b > 0
+{
+    const int64_t q = a / b;
+    return (a % b != 0 && a < 0) ? q - 1 : q;
+}
+PGET_HD inline int seg_entry(const RayP& rp, int rtop_or_rbot)
+{
+    const int64_t bound = static_cast<int64_t>(rtop_or_rbot) << 32;
+    int64_t i;
+    if (rp.dV > 0) i = pget_floordiv(bound - 1 - rp.V0, rp.dV);   // V0 + i dV <= bound - 1
+    else i = pget_floordiv(rp.V0 - bound, -rp.dV);               // V0 + i dV >= bound
+    if (i > rp.ihi) i = rp.ihi;
+    if (i < static_cast<int64_t>(rp.ilo) - 1) i = static_cast<int64_t>(rp.ilo) - 1;
+    return static_cast<int>(i);
+}
+
 enum { kSchedFwd = 0, kSchedJvp = 1, kSchedAdj = 2 };
 struct Schedule {
     int C = 0;                        // persistent CTAs (grid size)
@@ -51,6 +96,20 @@ struct Schedule {
     std::vector<int32_t> red_slot;
     int max_slots_member = 0;
     int max_gA = 1, max_gB = 1;       // most sweep-A (32 adjacent rays) / sweep-B (comb) groups of a task
+    // segmented adjoint (kind kSchedAdj): K row segments, units and stage lists of phases A and B
+    int K = 0;
+    std::vector<int32_t> seg_rows;    // [K + 1]
+    int CA = 0;                       // phase-A CTAs (phase B uses C)
+    std::vector<UnitD> unitsA, unitsB;
+    std::vector<int32_t> ua_begin, ub_begin;   // [CA + 1], [C + 1]
+    std::vector<StageD> stA, stB;
+    std::vector<int32_t> sa_begin, sb_begin;   // [CA + 1], [C + 1]
+    int64_t n_canon = 0;
+    UnitD* d_unitsA = nullptr;
+    UnitD* d_unitsB = nullptr;
+    int32_t *d_ua_begin = nullptr, *d_ub_begin = nullptr, *d_sa_begin = nullptr, *d_sb_begin = nullptr;
+    StageD *d_stA = nullptr, *d_stB = nullptr;
+    int32_t* d_seg_rows = nullptr;
     int32_t* d_cta_begin = nullptr;
     TaskD* d_tasks = nullptr;
     int32_t* d_groups = nullptr;
@@ -100,6 +159,7 @@ struct Geometry {
     int cg_coop_blocks = 148;   // co-resident blocks of cg_fused_kernel (cooperative launch bound)
     size_t smem_optin = 227 * 1024;
     Schedule sch[3];   // kSchedFwd, kSchedJvp, kSchedAdj (schedule.cpp), device copies owned here
+    bool adj_seg = true;   // adjoint (VJP / GN) as the segmented two-phase projector (else the fused one)
 };
 
 }  // namespace pget
@@ -113,4 +173,8 @@ namespace pget {
 pget_status build_geometry(const pget_geometry_desc* d, Geometry* g, std::string* err);
 void build_ray_params(const Geometry& g, std::vector<RayP>* rays);
 void build_schedule(const Geometry& g, int kind, int C, Schedule* S);
+// segmented adjoint schedule: units over CA phase-A CTAs and C phase-B CTAs, slots, comb groups;
+// then (once the band heights are known) the stage lists of both phases
+void build_adj_schedule(const Geometry& g, const std::vector<RayP>& rays, int CA, int C, Schedule* S);
+void build_adj_stages(int RbA, int passesA, int RbB, int passesB, Schedule* S);
 }  // namespace pget

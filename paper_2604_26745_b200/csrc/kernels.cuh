@@ -27,7 +27,18 @@ struct ProjArgs {
     int stage_bytes, off_wacc, off_rout, off_gsh;   // dynamic shared memory layout (bytes)
     float delta;            // Delta
     float cf, ch;           // -Delta log2(e), -Delta log2(e) / 2
+    // segmented adjoint (seg_a_kernel / seg_b_kernel): the phase's units and stage lists per CTA,
+    // the K row segments, the per-(unit, ray) partial sums of phase A
+    const UnitD* units;
+    const int32_t* u_begin;
+    const StageD* stages;
+    const int32_t* s_begin;
+    const int32_t* seg_rows;
+    int K, n_groups, off_rsc, off_q1;
+    float* segp;            // [n_canon][kSegFields][R]
 };
+
+constexpr int kSegFields = 9;   // s, sc, g, gc, ds, dg, p1, p2, p3 (see seg_a_kernel)
 
 struct CGState {
     double zeta, a, bcg;
@@ -76,6 +87,9 @@ namespace pget {
 cudaError_t launch_proj(int mode, int maxg, bool paired, const ProjArgs& A, int grid, int block, size_t smem,
                         cudaStream_t s);
 cudaError_t set_proj_smem_limit(int mode, size_t smem);
+cudaError_t launch_seg(int phase, int mode, int maxg, bool paired, const ProjArgs& A, int grid, int block,
+                       size_t smem, cudaStream_t s);
+cudaError_t set_seg_smem_limit(int phase, int mode, size_t smem);
 int proj_warps(int mode);
 int proj_ctas_per_sm(int mode);
 }  // namespace pget

@@ -317,7 +317,7 @@ __device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int
             else x_.dg = fmaf(fmaf(-lam, dA, dlam), E, x_.dg);
             x_.ds = fmaf(dmu, dl, x_.ds);
         }
-        if constexpr (PAIRED && MODE == MODE_FWD) {
+        if constexpr (PAIRED && (MODE == MODE_FWD || MODE == MODE_VJP)) {   // VJP: segmented phase A only
             x_.p2 = fmaf(lam, ex2(-arg), x_.p2);
         }
         if constexpr (PAIRED && MODE == MODE_GN) {
@@ -686,6 +686,369 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
     }
 }
 
+// ------------------------------------------------------------------------------------------ segmented adjoint
+// The adjoint (VJP, GN) as two launches over units (member, traced angle-bank, row segment k of K)
+// with all detectors.  Along a ray walked from its bank-0 detector
+// the segments come in the order q = 0..K-1 (q = seg for dV < 0, K-1-seg for dV > 0).  Phase A
+// evaluates, per ray and segment, the local sums that the whole-ray recurrences split into
+// (log2-domain optical depth L_q of the segment, G_q = sum lam e^{-A_loc}, and for GN the JVP sums);
+// phase B rebuilds from the K partials of its ray
+//   scale  = e^{-(depth before the segment)},  T = tail of G from the segment on, in the segment's
+//   frame,  the reverse-direction offsets,  and (GN) the whole-ray (J p) of both directions,
+// then scatters the segment's adjoint exactly as sweep B of proj_kernel with those constants.
+struct UnitInfo {
+    int m, ab, seg, canon, slot, cls, first, dir, ylo, yhi, nb;
+};
+
+__device__ __forceinline__ UnitInfo unit_info(const ProjArgs& A, int u, int Rb)
+{
+    const UnitD ud = A.units[u];
+    UnitInfo x;
+    x.m = ud.m;
+    x.ab = ud.ab;
+    x.seg = ud.seg;
+    x.canon = ud.canon;
+    x.slot = ud.slot;
+    x.cls = (ud.flags & kTaskClass1) ? 1 : 0;
+    x.first = (ud.flags & kTaskFirst) ? 1 : 0;
+    x.dir = A.rays[static_cast<size_t>(ud.ab) * A.R].dV > 0 ? 1 : -1;
+    x.ylo = A.seg_rows[ud.seg];
+    x.yhi = A.seg_rows[ud.seg + 1];
+    x.nb = (x.yhi - x.ylo + Rb - 1) / Rb;
+    return x;
+}
+
+// rows of band j (processing order) of a unit: sample rows [r0, r1), staged rows r0..r1
+__device__ __forceinline__ void seg_band(const UnitInfo& ui, int j, int Rb, int& r0, int& r1)
+{
+    const int b = ui.dir > 0 ? ui.nb - 1 - j : j;
+    r0 = ui.ylo + b * Rb;
+    r1 = min(r0 + Rb, ui.yhi);
+}
+
+template <bool F4>
+__device__ void issue_seg_stage(const ProjArgs& A, int Rb, int64_t sidx, void* dst, uint64_t* bar)
+{
+    const StageD sd = A.stages[sidx];
+    const UnitInfo ui = unit_info(A, sd.unit, Rb);
+    int r0, r1;
+    seg_band(ui, sd.j, Rb, r0, r1);
+    const size_t pix0 = static_cast<size_t>(ui.m) * A.P * A.P + static_cast<size_t>(r0) * A.P;
+    const size_t npix = static_cast<size_t>(r1 - r0 + 1) * A.P;
+    const char* src = F4 ? reinterpret_cast<const char*>(A.img4[ui.cls] + pix0)
+                         : reinterpret_cast<const char*>(A.img2[ui.cls] + pix0);
+    const size_t bytes = npix * (F4 ? sizeof(float4) : sizeof(float2));
+    fence_proxy_async();
+    mbar_expect_tx(bar, static_cast<uint32_t>(bytes));
+    char* d = static_cast<char*>(dst);
+    for (size_t off = 0; off < bytes; off += 32768) {
+        const uint32_t n = static_cast<uint32_t>(bytes - off < 32768 ? bytes - off : 32768);
+        bulk_g2s(d + off, src + off, n, bar);
+    }
+}
+
+// Phase A: sweep A of every ray of the CTA's units through the unit's rows; per-ray partials to A.segp.
+template <int MODE, int MAXG, bool PAIRED>
+__global__ void __launch_bounds__(256, 2) seg_a_kernel(ProjArgs A)
+{
+    using TR = ModeTraits<MODE>;
+    const int W = blockDim.x >> 5;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
+    unsigned char* const stage0 = smem + 128;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c = blockIdx.x;
+    const int64_t sb0 = A.s_begin[c];
+    const int64_t n_stages = A.s_begin[c + 1] - sb0;
+    if (n_stages == 0) return;
+    const int P = A.P, R = A.R, Rb = A.RbA;
+    if (tid == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        issue_seg_stage<TR::NF4>(A, Rb, sb0, stage0, &mbar[0]);
+        if (n_stages > 1) issue_seg_stage<TR::NF4>(A, Rb, sb0 + 1, stage0 + A.stage_bytes, &mbar[1]);
+    }
+    int64_t s = 0;
+    const float cf = A.cf, ch = A.ch, dl = A.delta, dlh = 0.5f * A.delta;
+    for (int u = A.u_begin[c]; u < A.u_begin[c + 1]; ++u) {
+        const UnitInfo ui = unit_info(A, u, Rb);
+        const RayP* rays = A.rays + static_cast<size_t>(ui.ab) * R;
+        const int64_t dU = rays[0].dU, dV = rays[0].dV;
+        const int bound = ui.dir > 0 ? ui.yhi : ui.ylo;
+        float* part = A.segp + static_cast<size_t>(ui.canon) * kSegFields * R;
+        for (int pass = 0; pass < A.passesA; ++pass) {
+            int rr[MAXG], ii[MAXG], ilo[MAXG];
+            int64_t uu[MAXG], vv[MAXG];
+            StateA st[MAXG];
+#pragma unroll
+            for (int k = 0; k < MAXG; ++k) {
+                const int r = ((pass * MAXG + k) * W + warp) * 32 + lane;
+                rr[k] = r < R ? r : -1;
+                ii[k] = -1; ilo[k] = 0; uu[k] = 0; vv[k] = 0;
+                if (rr[k] >= 0) {
+                    const RayP rp = rays[r];
+                    ii[k] = seg_entry(rp, bound);
+                    ilo[k] = rp.ilo;
+                    uu[k] = rp.U0 + static_cast<int64_t>(ii[k]) * dU;
+                    vv[k] = rp.V0 + static_cast<int64_t>(ii[k]) * dV;
+                }
+                st[k] = StateA{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            }
+            for (int j = 0; j < ui.nb; ++j) {
+                int r0, r1;
+                seg_band(ui, j, Rb, r0, r1);
+                const int b = static_cast<int>(s & 1);
+                mbar_wait(&mbar[b], static_cast<uint32_t>((s >> 1) & 1));
+                const unsigned char* sbuf = stage0 + b * A.stage_bytes;
+#pragma unroll
+                for (int k = 0; k < MAXG; ++k)
+                    walk_a<MODE, PAIRED>(sbuf, P, r0, r1, ilo[k], dU, dV, cf, ch, dl, dlh, ii[k], uu[k], vv[k], st[k]);
+                __syncthreads();   // stage buffer b consumed
+                if (tid == 0 && s + 2 < n_stages)
+                    issue_seg_stage<TR::NF4>(A, Rb, sb0 + s + 2, stage0 + b * A.stage_bytes, &mbar[b]);
+                ++s;
+            }
+#pragma unroll
+            for (int k = 0; k < MAXG; ++k) {
+                const int r = rr[k];
+                if (r < 0) continue;
+                const StateA& q = st[k];
+                part[0 * R + r] = q.s;
+                part[1 * R + r] = q.sc;
+                part[2 * R + r] = q.g;
+                part[3 * R + r] = q.gc;
+                if (MODE == MODE_GN) {
+                    part[4 * R + r] = q.ds;
+                    part[5 * R + r] = q.dg - q.dgc;
+                    part[6 * R + r] = q.p1;
+                    part[8 * R + r] = q.p3;
+                }
+                if (PAIRED) part[7 * R + r] = q.p2;
+            }
+        }
+    }
+}
+
+// Phase B: per-ray constants from the K partials, then sweep B of the unit (comb groups) into the
+// unit's partial slot (zeroed by the slot's first unit; every flush adds).
+template <int MODE, bool PAIRED>
+__global__ void __launch_bounds__(512, 1) seg_b_kernel(ProjArgs A)
+{
+    const int W = blockDim.x >> 5;
+    const int NT = blockDim.x;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
+    unsigned char* const stage0 = smem + 128;
+    float2* wacc_all = reinterpret_cast<float2*>(smem + A.off_wacc);
+    float* rout = reinterpret_cast<float*>(smem + A.off_rout);      // [2R] (GN: J p of both directions)
+    float4* gsh = reinterpret_cast<float4*>(smem + A.off_gsh);      // [R] (T, Tc, Sl, Slc)
+    float* rsc = reinterpret_cast<float*>(smem + A.off_rsc);        // [R] e^{-depth before the segment}
+    float2* q1i = reinterpret_cast<float2*>(smem + A.off_q1);       // [R] reverse-direction Q offset (pair)
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c = blockIdx.x;
+    const int64_t sb0 = A.s_begin[c];
+    const int64_t n_stages = A.s_begin[c + 1] - sb0;
+    if (n_stages == 0) return;
+    const int P = A.P, R = A.R, J = A.J, K = A.K, Rb = A.RbB;
+    const int RB1 = Rb + 1;
+    float2* wacc = wacc_all + static_cast<size_t>(warp) * RB1 * P;
+    {
+        float4* z = reinterpret_cast<float4*>(wacc_all);
+        const int n4 = W * RB1 * P / 2;
+        for (int k = tid; k < n4; k += NT) z[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    if (tid == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        issue_seg_stage<false>(A, Rb, sb0, stage0, &mbar[0]);
+        if (n_stages > 1) issue_seg_stage<false>(A, Rb, sb0 + 1, stage0 + A.stage_bytes, &mbar[1]);
+    }
+    int64_t s = 0;
+    const float cf = A.cf, ch = A.ch;
+    const int npairs = P >> 1;
+    const float inv_np = 1.0f / static_cast<float>(npairs);
+    const size_t plane = static_cast<size_t>(A.N) * A.Ns;
+
+    for (int u = A.u_begin[c]; u < A.u_begin[c + 1]; ++u) {
+        const UnitInfo ui = unit_info(A, u, Rb);
+        const RayP* rays = A.rays + static_cast<size_t>(ui.ab) * R;
+        const int64_t dU = rays[0].dU, dV = rays[0].dV;
+        const int bound = ui.dir > 0 ? ui.yhi : ui.ylo;
+        const int qme = ui.dir > 0 ? K - 1 - ui.seg : ui.seg;
+        const float* part0 = A.segp + static_cast<size_t>(ui.canon - ui.seg) * kSegFields * R;
+        // ---- per-ray constants (fp64 combination of the K segment partials, in ray order)
+        for (int r = tid; r < R; r += NT) {
+            // fixed-size, fully unrolled (K <= 4): register-resident
+            double Lb[5], dLb[5], gq[4], p1q[4], p2q[4], p3q[4], dgq[4];
+            Lb[0] = 0.0;
+            dLb[0] = 0.0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                gq[q] = p1q[q] = p2q[q] = p3q[q] = dgq[q] = 0.0;
+                double sq = 0.0, dsq = 0.0;
+                if (q < K) {
+                    const float* pq = part0 + static_cast<size_t>(ui.dir > 0 ? K - 1 - q : q) * kSegFields * R;
+                    sq = static_cast<double>(pq[0 * R + r]) - pq[1 * R + r];
+                    gq[q] = static_cast<double>(pq[2 * R + r]) - pq[3 * R + r];
+                    if (PAIRED) p2q[q] = pq[7 * R + r];
+                    if (MODE == MODE_GN) {
+                        dsq = pq[4 * R + r];
+                        dgq[q] = pq[5 * R + r];
+                        p1q[q] = pq[6 * R + r];
+                        p3q[q] = pq[8 * R + r];
+                    }
+                }
+                Lb[q + 1] = Lb[q] + sq;
+                dLb[q + 1] = dLb[q] + dsq;
+            }
+            double Lme = 0.0, LK = 0.0, dLK = 0.0;
+#pragma unroll
+            for (int q = 0; q < 5; ++q) {
+                if (q == qme) Lme = Lb[q];
+                if (q == K) { LK = Lb[q]; dLK = dLb[q]; }
+            }
+            double T = 0.0, Qoff = 0.0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                if (q >= qme && q < K) T += exp2(Lb[q] - Lme) * gq[q];
+                if (PAIRED && q < qme) Qoff += exp2(LK - Lb[q]) * p2q[q];
+            }
+            const double Sl = LK - Lme;
+            const float Th = static_cast<float>(T), Sh = static_cast<float>(Sl), Qh = static_cast<float>(Qoff);
+            gsh[r] = make_float4(Th, static_cast<float>(static_cast<double>(Th) - T), Sh,
+                                 static_cast<float>(static_cast<double>(Sh) - Sl));
+            rsc[r] = static_cast<float>(exp2(Lme));
+            q1i[r] = make_float2(Qh, static_cast<float>(static_cast<double>(Qh) - Qoff));
+            if (MODE == MODE_GN) {
+                double dG = 0.0, P1 = 0.0, P2 = 0.0, P3 = 0.0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (q < K) {
+                        dG += exp2(Lb[q]) * (dgq[q] - dLb[q] * gq[q]);
+                        if (PAIRED) {
+                            const double e = exp2(-Lb[q]);
+                            P1 += e * p1q[q];
+                            P2 += e * p2q[q];
+                            P3 += e * (p3q[q] + dLb[q] * p2q[q]);
+                        }
+                    }
+                }
+                rout[r] = static_cast<float>(A.delta * dG);
+                if (PAIRED) rout[R + r] = static_cast<float>(A.delta * exp2(LK) * (P1 + P3 - dLK * P2));
+            }
+        }
+        float2* slot = A.slots + static_cast<size_t>(ui.slot) * plane;
+        if (ui.first) {   // the slot's first unit zeroes it (later flushes of the slot only add)
+            float4* z = reinterpret_cast<float4*>(slot);
+            for (size_t k = tid; k < plane / 2; k += NT) z[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        __syncthreads();
+        const size_t wbase = (static_cast<size_t>(ui.m) * A.n_ab + ui.ab) * A.n_det;
+        const size_t wbase2 = (static_cast<size_t>(ui.m) * A.n_ab + dup_of(A, ui.ab)) * A.n_det;
+        const size_t wpbase = (static_cast<size_t>(ui.m) * A.n_ab + ui.ab + 1) * A.n_det;
+        const size_t wpbase2 = (static_cast<size_t>(ui.m) * A.n_ab + dup_of(A, ui.ab + 1)) * A.n_det;
+        const RayP rfirst = rays[0], rlast = rays[R - 1];
+        const double kuv = static_cast<double>(dU) / static_cast<double>(dV);
+        auto ucol = [&](const RayP& rp, double vrow) {
+            return (static_cast<double>(rp.U0) + (vrow * 4294967296.0 - static_cast<double>(rp.V0)) * kuv) *
+                   (1.0 / 4294967296.0);
+        };
+        for (int pass = 0; pass < A.passesB; ++pass) {
+            const int grp = pass * W + warp;
+            const int r = grp < A.n_groups ? A.groups[grp * 32 + lane] : -1;
+            int ii = -1, ilo = 0;
+            int64_t uu = 0, vv = 0;
+            RayB rb{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            StateB st{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            if (r >= 0) {
+                const int d = r / J, j = r - d * J;
+                float wd = 0.f, wd1 = 0.f;
+                if (MODE == MODE_GN) {
+                    for (int jj = 0; jj < J; ++jj) {
+                        wd = fmaf(A.w[jj], rout[d * J + jj], wd);
+                        if (PAIRED) wd1 = fmaf(A.w[jj], rout[R + d * J + jj], wd1);
+                    }
+                    if (A.dup_half) { wd *= 2.f; wd1 *= 2.f; }
+                } else {
+                    wd = A.win[wbase + d];
+                    if (A.dup_half) wd += A.win[wbase2 + d];
+                    if (PAIRED) wd1 = A.win[wpbase + A.n_det - 1 - d] + A.win[wpbase2 + A.n_det - 1 - d];
+                }
+                const float wr = A.w[j] * wd, wr1 = A.w[j] * wd1;
+                const float sc = rsc[r];
+                const float4 G = gsh[r];
+                const float2 q1 = q1i[r];
+                rb = RayB{wr * A.delta * sc, -wr * A.delta * A.delta * sc, G.x, G.y,
+                          wr1 * A.delta, -wr1 * A.delta * A.delta, G.z, G.w};
+                st.q1 = q1.x;
+                st.q1c = q1.y;
+                if (wr != 0.f || wr1 != 0.f) {
+                    const RayP rp = rays[r];
+                    ii = seg_entry(rp, bound);
+                    ilo = rp.ilo;
+                    uu = rp.U0 + static_cast<int64_t>(ii) * dU;
+                    vv = rp.V0 + static_cast<int64_t>(ii) * dV;
+                }
+            }
+            for (int j = 0; j < ui.nb; ++j) {
+                int r0, r1;
+                seg_band(ui, j, Rb, r0, r1);
+                const int b = static_cast<int>(s & 1);
+                mbar_wait(&mbar[b], static_cast<uint32_t>((s >> 1) & 1));
+                const float2* sbuf = reinterpret_cast<const float2*>(stage0 + b * A.stage_bytes);
+                const bool flip = j & 1;
+                const int abase = flip ? Rb * P : 0, sP = flip ? -P : P;
+                walk_b<PAIRED>(sbuf, wacc, P, r0, r1, abase, sP, ilo, dU, dV, cf, ch, rb, ii, uu, vv, st);
+                __syncthreads();   // stage buffer b and every warp ring consumed
+                if (tid == 0 && s + 2 < n_stages)
+                    issue_seg_stage<false>(A, Rb, sb0 + s + 2, stage0 + b * A.stage_bytes, &mbar[b]);
+                ++s;
+                // flush (as proj_kernel): finished rows into the slot, column-limited, fixed thread per element
+                const bool last = j == ui.nb - 1;
+                const int carry = last ? -1 : (ui.dir > 0 ? r0 : r1);
+                int qlo, qhi;
+                {
+                    const double a0 = ucol(rfirst, r0 - 1.0), a1 = ucol(rfirst, r1 + 1.0);
+                    const double b0 = ucol(rlast, r0 - 1.0), b1 = ucol(rlast, r1 + 1.0);
+                    const double umin = fmin(fmin(a0, a1), fmin(b0, b1)), umax = fmax(fmax(a0, a1), fmax(b0, b1));
+                    qlo = max(0, static_cast<int>(floor(umin)) - 2) >> 1;
+                    qhi = min(P - 1, static_cast<int>(floor(umax)) + 3) >> 1;
+                }
+                const int e_beg = r0 * npairs, e_end = (r1 + 1) * npairs;
+                for (int e = e_beg + (tid - e_beg % NT + NT) % NT; e < e_end; e += NT) {
+                    int rw = __float2int_rd(static_cast<float>(e) * inv_np);
+                    int q = e - rw * npairs;
+                    if (q < 0) { --rw; q += npairs; } else if (q >= npairs) { ++rw; q -= npairs; }
+                    if (rw == carry || q < qlo || q > qhi) continue;
+                    const int lr = flip ? r0 + Rb - rw : rw - r0;
+                    PGET_CHECK(lr >= 0 && lr < RB1);
+                    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+                    for (int w = 0; w < W; ++w) {
+                        float4* el = reinterpret_cast<float4*>(wacc_all + (static_cast<size_t>(w) * RB1 + lr) * P) + q;
+                        const float4 x = *el;
+                        sum.x += x.x; sum.y += x.y; sum.z += x.z; sum.w += x.w;
+                        *el = make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                    const int ir = rw - kHalo, ic = 2 * q - kHalo;
+                    if (ir >= 0 && ir < A.N && ic >= 0 && ic < A.Ns)
+                        atomicAdd(reinterpret_cast<float4*>(slot + static_cast<size_t>(ir) * A.Ns + ic), sum);
+                }
+                __syncthreads();   // rings zeroed before the next band's scatter
+            }
+        }
+    }
+}
+
 // ------------------------------------------------------------------------------------------ reduction
 // g[m][j][i] = sum over the class-0 slots of member m of slot[j][i] + sum over its class-1 slots of
 // slot[i][j] (transposed frame), in fp64, slots in the schedule's fixed order.  Block (tile, m * G + g)
@@ -761,6 +1124,57 @@ cudaError_t launch_proj(int mode, int maxg, bool paired, const ProjArgs& A, int 
     case MODE_VJP: return launch_mode<MODE_VJP>(maxg, paired, A, grid, block, smem, s);
     case MODE_GN: return launch_mode<MODE_GN>(maxg, paired, A, grid, block, smem, s);
     }
+    return cudaErrorInvalidValue;
+}
+
+template <int MODE>
+static cudaError_t launch_seg_mode(int phase, int maxg, bool paired, const ProjArgs& A, int grid, int block,
+                                   size_t smem, cudaStream_t s)
+{
+    if (phase == 0) {
+        if (paired) {
+            if (maxg == 1) seg_a_kernel<MODE, 1, true><<<grid, block, smem, s>>>(A);
+            else seg_a_kernel<MODE, 2, true><<<grid, block, smem, s>>>(A);
+        } else {
+            if (maxg == 1) seg_a_kernel<MODE, 1, false><<<grid, block, smem, s>>>(A);
+            else seg_a_kernel<MODE, 2, false><<<grid, block, smem, s>>>(A);
+        }
+    } else {
+        if (paired) seg_b_kernel<MODE, true><<<grid, block, smem, s>>>(A);
+        else seg_b_kernel<MODE, false><<<grid, block, smem, s>>>(A);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_seg(int phase, int mode, int maxg, bool paired, const ProjArgs& A, int grid, int block,
+                       size_t smem, cudaStream_t s)
+{
+    if (maxg != 1 && maxg != 2) return cudaErrorInvalidValue;
+    if (mode == MODE_VJP) return launch_seg_mode<MODE_VJP>(phase, maxg, paired, A, grid, block, smem, s);
+    if (mode == MODE_GN) return launch_seg_mode<MODE_GN>(phase, maxg, paired, A, grid, block, smem, s);
+    return cudaErrorInvalidValue;
+}
+
+template <int MODE>
+static cudaError_t seg_attr_mode(int phase, size_t smem)
+{
+    const int v = static_cast<int>(smem);
+    const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    cudaError_t e;
+    if (phase == 0) {
+        if ((e = cudaFuncSetAttribute(seg_a_kernel<MODE, 1, true>, a, v))) return e;
+        if ((e = cudaFuncSetAttribute(seg_a_kernel<MODE, 2, true>, a, v))) return e;
+        if ((e = cudaFuncSetAttribute(seg_a_kernel<MODE, 1, false>, a, v))) return e;
+        return cudaFuncSetAttribute(seg_a_kernel<MODE, 2, false>, a, v);
+    }
+    if ((e = cudaFuncSetAttribute(seg_b_kernel<MODE, true>, a, v))) return e;
+    return cudaFuncSetAttribute(seg_b_kernel<MODE, false>, a, v);
+}
+
+cudaError_t set_seg_smem_limit(int phase, int mode, size_t smem)
+{
+    if (mode == MODE_VJP) return seg_attr_mode<MODE_VJP>(phase, smem);
+    if (mode == MODE_GN) return seg_attr_mode<MODE_GN>(phase, smem);
     return cudaErrorInvalidValue;
 }
 

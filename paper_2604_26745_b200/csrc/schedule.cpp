@@ -189,4 +189,193 @@ void build_schedule(const Geometry& g, int kind, int C, Schedule* S)
     }
 }
 
+// ------------------------------------------------------------------ segmented adjoint (VJP / GN)
+// Units (member, traced angle-bank, row segment) over all detectors: full 32-lane comb groups and the
+// most warps per CTA, while K segments per angle-bank give enough units to balance the CTAs.  The
+// unit cost is the exact number of its samples (seg_entry of the segment bounds, per ray) plus a
+// fixed per-unit overhead; units are assigned longest-first to the least-loaded CTA, separately for
+// phase A (CA CTAs) and phase B (C CTAs), and listed per CTA in (member, class, angle-bank, segment)
+// order so that consecutive units of one (member, class) share a partial slot (<= kSlotTasks).
+void build_adj_schedule(const Geometry& g, const std::vector<RayP>& rays, int CA, int C, Schedule* S)
+{
+    const bool paired = g.dup;
+    const std::vector<int32_t>& list = paired ? g.task_ab_p : g.task_ab;
+    const int B = g.desc.batch, R = g.R;
+    const int ntab = static_cast<int>(list.size());
+    const int rows = g.P - 1;   // sample rows [0, P - 1)
+    S->CA = CA;
+    S->C = C;
+    // per-segment sample counts of every traced angle-bank, for K = 1..4
+    auto seg_rows_of = [&](int K) {
+        std::vector<int32_t> y(K + 1);
+        for (int k = 0; k <= K; ++k) y[k] = static_cast<int32_t>((static_cast<int64_t>(rows) * k) / K);
+        return y;
+    };
+    auto costs_of = [&](const std::vector<int32_t>& y) {
+        const int K = static_cast<int>(y.size()) - 1;
+        std::vector<double> c(static_cast<size_t>(ntab) * K, 0.0);
+        for (int t = 0; t < ntab; ++t)
+            for (int r = 0; r < R; ++r) {
+                const RayP& rp = rays[static_cast<size_t>(list[t]) * R + r];
+                for (int k = 0; k < K; ++k) {
+                    const int n = rp.dV > 0 ? seg_entry(rp, y[k + 1]) - seg_entry(rp, y[k])
+                                            : seg_entry(rp, y[k]) - seg_entry(rp, y[k + 1]);
+                    c[static_cast<size_t>(t) * K + k] += std::max(0, n);
+                }
+            }
+        return c;
+    };
+    auto lpt = [&](const std::vector<double>& w, int ncta, std::vector<int>* owner) {
+        std::vector<int> order(w.size());
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return w[a] > w[b]; });
+        using L = std::pair<double, int>;
+        std::priority_queue<L, std::vector<L>, std::greater<L>> heap;
+        for (int c = 0; c < ncta; ++c) heap.push({0.0, c});
+        owner->assign(w.size(), 0);
+        double mk = 0.0;
+        for (int idx : order) {
+            L top = heap.top();
+            heap.pop();
+            (*owner)[idx] = top.second;
+            top.first += w[idx];
+            mk = std::max(mk, top.first);
+            heap.push(top);
+        }
+        return mk;
+    };
+    // choose K (phase B makespan, per-unit overhead kUnitOvh of a mean angle-bank)
+    constexpr double kUnitOvh = 0.04;
+    int Kmax = std::max(1, std::min(4, rows / 8));   // segments of >= 8 rows
+    int Kforce = 0;
+    if (const char* e = std::getenv("PGET_SEG_K")) Kforce = std::atoi(e);   // experiments
+    double best = 1e300;
+    int bestK = 1;
+    for (int K = 1; K <= Kmax; ++K) {
+        if (Kforce > 0 && K != std::min(Kforce, Kmax)) continue;
+        const std::vector<double> c = costs_of(seg_rows_of(K));
+        double mean = 0.0;
+        for (double v : c) mean += v;
+        mean = ntab ? mean / ntab : 1.0;   // samples of a mean angle-bank
+        std::vector<double> w;
+        for (int m = 0; m < B; ++m)
+            for (double v : c) w.push_back(v / std::max(mean, 1.0) + kUnitOvh);
+        std::vector<int> own;
+        const double mk = lpt(w, C, &own);
+        if (mk < best * 0.98) { best = mk; bestK = K; }
+    }
+    const int K = bestK;
+    S->K = K;
+    S->seg_rows = seg_rows_of(K);
+    const std::vector<double> c = costs_of(S->seg_rows);
+    double mean = 0.0;
+    for (double v : c) mean += v;
+    mean = ntab ? mean / ntab : 1.0;
+    // canonical units
+    std::vector<UnitD> all;
+    std::vector<double> w;
+    for (int m = 0; m < B; ++m)
+        for (int t = 0; t < ntab; ++t)
+            for (int k = 0; k < K; ++k) {
+                UnitD u{};
+                u.m = m;
+                u.ab = list[t];
+                u.seg = k;
+                u.canon = (m * ntab + t) * K + k;
+                u.slot = -1;
+                u.flags = g.orient[list[t]] ? kTaskClass1 : 0;
+                all.push_back(u);
+                w.push_back(c[static_cast<size_t>(t) * K + k] / std::max(mean, 1.0) + kUnitOvh);
+            }
+    S->n_canon = static_cast<int64_t>(all.size());
+    auto assign = [&](int ncta, std::vector<UnitD>* units, std::vector<int32_t>* begin) {
+        std::vector<int> own;
+        lpt(w, ncta, &own);
+        std::vector<std::vector<int>> per(ncta);
+        for (size_t i = 0; i < all.size(); ++i) per[own[i]].push_back(static_cast<int>(i));
+        units->clear();
+        begin->assign(ncta + 1, 0);
+        for (int cta = 0; cta < ncta; ++cta) {
+            (*begin)[cta] = static_cast<int32_t>(units->size());
+            std::sort(per[cta].begin(), per[cta].end(), [&](int a, int b) {
+                const UnitD &x = all[a], &y = all[b];
+                const int cx = x.flags & kTaskClass1, cy = y.flags & kTaskClass1;
+                if (x.m != y.m) return x.m < y.m;
+                if (cx != cy) return cx < cy;
+                return x.canon < y.canon;
+            });
+            for (int i : per[cta]) units->push_back(all[i]);
+        }
+        (*begin)[ncta] = static_cast<int32_t>(units->size());
+    };
+    assign(CA, &S->unitsA, &S->ua_begin);
+    assign(C, &S->unitsB, &S->ub_begin);
+    const int ngA = (R + 31) / 32;
+    std::vector<int32_t> grp;
+    comb_groups(0, R, g.comb_S, &grp);
+    const int ngB = static_cast<int>(grp.size() / 32);
+    S->groups = grp;
+    S->max_gA = ngA;
+    S->max_gB = ngB;
+    S->tasks.clear();
+    S->cta_begin.assign(C + 1, 0);
+    // slots of phase B (as build_schedule's adjoint kind, per unit)
+    S->n_slots = 0;
+    std::vector<std::vector<int32_t>> lists(static_cast<size_t>(B) * 2);
+    for (int cta = 0; cta < C; ++cta) {
+        int run = 0, pm = -1, pc = -1;
+        for (int u = S->ub_begin[cta]; u < S->ub_begin[cta + 1]; ++u) {
+            UnitD& t = S->unitsB[u];
+            const int cls = (t.flags & kTaskClass1) ? 1 : 0;
+            if (t.m != pm || cls != pc || run == kSlotTasks) {
+                lists[static_cast<size_t>(t.m) * 2 + cls].push_back(S->n_slots);
+                ++S->n_slots;
+                run = 0;
+                t.flags |= kTaskFirst;
+            }
+            t.slot = S->n_slots - 1;
+            ++run;
+            pm = t.m;
+            pc = cls;
+        }
+    }
+    S->red_off.assign(static_cast<size_t>(B) * 2 + 1, 0);
+    S->red_slot.clear();
+    for (size_t e = 0; e < lists.size(); ++e) {
+        S->red_off[e] = static_cast<int32_t>(S->red_slot.size());
+        S->red_slot.insert(S->red_slot.end(), lists[e].begin(), lists[e].end());
+    }
+    S->red_off[lists.size()] = static_cast<int32_t>(S->red_slot.size());
+    S->max_slots_member = 0;
+    for (int m = 0; m < B; ++m)
+        S->max_slots_member = std::max(S->max_slots_member, S->red_off[2 * m + 2] - S->red_off[2 * m]);
+    S->stA.clear();
+    S->stB.clear();
+    S->sa_begin.clear();
+    S->sb_begin.clear();
+}
+
+// stage lists of both phases (band j of a unit in processing order; passes repeat the unit's bands)
+void build_adj_stages(int RbA, int passesA, int RbB, int passesB, Schedule* S)
+{
+    auto stages = [&](const std::vector<UnitD>& units, const std::vector<int32_t>& ub, int Rb, int passes,
+                      std::vector<StageD>* st, std::vector<int32_t>* sb) {
+        const int ncta = static_cast<int>(ub.size()) - 1;
+        st->clear();
+        sb->assign(ncta + 1, 0);
+        for (int cta = 0; cta < ncta; ++cta) {
+            (*sb)[cta] = static_cast<int32_t>(st->size());
+            for (int u = ub[cta]; u < ub[cta + 1]; ++u) {
+                const int nrow = S->seg_rows[units[u].seg + 1] - S->seg_rows[units[u].seg];
+                const int nb = (nrow + Rb - 1) / Rb;
+                for (int p = 0; p < passes; ++p)
+                    for (int j = 0; j < nb; ++j) st->push_back(StageD{u, j});
+            }
+        }
+        (*sb)[ncta] = static_cast<int32_t>(st->size());
+    };
+    stages(S->unitsA, S->ua_begin, RbA, passesA, &S->stA, &S->sa_begin);
+    stages(S->unitsB, S->ub_begin, RbB, passesB, &S->stB, &S->sb_begin);
+}
+
 }  // namespace pget

@@ -11,7 +11,7 @@ import paper_2604_26745_b200 as pg  # noqa: E402
 import pget_data as P  # noqa: E402
 
 cid = int(sys.argv[1]) if len(sys.argv) > 1 else 2
-reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+reps = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 20
 gd = P.geometry_desc(cid)
 g = pg.Geometry(gd)
 dev = lambda x: torch.from_numpy(np.ascontiguousarray(x, np.float32)).cuda()
@@ -25,6 +25,9 @@ ops = {
     "gn": lambda: pg.gn_apply(g, lam, mu, dl, dm, 1e-3, 0.0),
     "safeguard": lambda: pg.safeguard(g, lam, mu, y, dl, dm, lam + dl, mu + dm, 1e-3),
 }
+if "--lm" in sys.argv:   # one LM iteration (20 CG steps) at u0 for the measurements y = F(u)
+    l0, m0 = map(dev, P.initial_guess(gd["n_px"], gd["batch"]))
+    ops["lm"] = lambda: pg.gn_cg_step(g, l0, m0, y, 1e-3, 0.0, 20)
 nom = g.info["n_samples_nominal"]
 out = {}
 for name, f in ops.items():

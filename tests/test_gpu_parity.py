@@ -281,3 +281,39 @@ def test_adjoint_bitwise_deterministic(pg, cid):
     c = [host(x) for x in pg.gn_apply(g, L, M, DL, DM, 1e-3, 0.0)]
     d = [host(x) for x in pg.gn_apply(g, L, M, DL, DM, 1e-3, 0.0)]
     assert all(np.array_equal(x, y) for x, y in zip(c, d))
+
+
+def test_lm_iteration_config5_batched(pg):
+    """one batched LM iteration over 64 assemblies of the config-5 recipe (one
+    gn_cg_step call, every launch covering all members).  Four distinct noisy problems are tiled over
+    the batch (the oracle forward of 64 members would dominate the test); members at different batch
+    positions are checked against the per-member oracle with the R-LM tolerances of
+    test_lm_iteration_cfg2."""
+    cid = 5
+    cfg = P.CONFIGS[cid]
+    gd = P.geometry_desc(cid)
+    B = gd["batch"]
+    g = pg.Geometry(gd)
+    g1 = dict(gd, batch=1)
+    lt, mt = P.make_phantom(cid)
+    ys = [P.poisson_noise(O.forward(g1, lt[k:k + 1], mt[k:k + 1]), 1e4, 50 + k) for k in range(4)]
+    y = np.concatenate([ys[m % 4] for m in range(B)])
+    l0, m0 = P.initial_guess(gd["n_px"], B)
+    sl, sm, st = pg.gn_cg_step(g, dev(l0), dev(m0), dev(y), cfg.alpha, 0.0, cfg.n_cg)
+    torch.cuda.synchronize()
+    S = pg.read_stats(st, B, cfg.n_cg)
+    for m in (1, 38):
+        k = m % 4
+        sl_o, sm_o, So = O.gn_cg_step(g1, l0[m:m + 1], m0[m:m + 1], ys[k], cfg.alpha, 0.0, cfg.n_cg)
+        for key in ("f", "misfit", "reg", "grad_norm"):
+            assert abs(S[m][key] - So[key]) <= 1e-5 * abs(So[key]), (m, key)
+        assert abs(S[m]["cg_res"][1] - So["cg_res"][1]) <= 1e-4 * So["cg_res"][1]
+        assert abs(S[m]["pred"] - So["pred"]) <= 1e-3 * abs(So["pred"])
+        assert abs(S[m]["rho"] - So["rho"]) <= 1e-3
+        assert S[m]["accepted"] == So["accepted"]
+        s = np.concatenate([host(sl)[m].ravel(), host(sm)[m].ravel()])
+        assert rel_l2(s, np.concatenate([sl_o.ravel(), sm_o.ravel()])) <= 0.1
+    # the same problem at other batch positions gives the same statistics (to fp32 reduction order)
+    for m in range(4, B, 4):
+        assert abs(S[m]["f"] - S[0]["f"]) <= 1e-6 * S[0]["f"]
+        assert abs(S[m]["pred"] - S[0]["pred"]) <= 1e-3 * abs(S[0]["pred"])
