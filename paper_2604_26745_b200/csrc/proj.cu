@@ -356,8 +356,13 @@ struct RayB {   // per-ray constants of sweep B
 // PAIRED adds the opposite-bank ray of the same line (its detector at the low-i end):
 //   E'_i = e^{-(S - A_i)},  a_lam += w'_r Delta E'_i,  a_mu += -w'_r Delta^2 (Q'_i + lam_i E'_i / 2),
 //   Q'_i = sum_{k>i} lam_k E'_k  (samples farther from that detector, already visited).
-// (Measured alternative: summing consecutive same-cell samples in registers before the
-// read-modify-write was 6 % slower on config 2.)
+#ifndef PGET_SCATTER
+#define PGET_SCATTER 1
+#endif
+// PGET_SCATTER 1: the coefficients of consecutive samples in the same 2x2 cell are summed in
+// registers and read-modify-written once when the ray leaves the cell (a cell spans ~1.5-2 samples):
+// fewer shared-memory accesses, and those only by the lanes that change cell (bank-conflict bound
+// since the segmented adjoint).  0: one read-modify-write per sample (prefetched accumulator reads).
 template <bool PAIRED>
 __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* __restrict__ acc, int P, int r0,
                                        int r1, int abase, int sP, int ilo, int64_t dU, int64_t dV, float cf, float ch,
@@ -369,11 +374,18 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
     float2 q00 = img[o], q01 = img[o + 1], q10 = img[o + P], q11 = img[o + P + 1];
     float fu = frac23(u), fv = frac23(v);
     StateB x_ = st;
+#if PGET_SCATTER == 1
+    int poff = -1;
+    float2 p00 = make_float2(0.f, 0.f), p01 = p00, p10 = p00, p11 = p00;
+#endif
     while (true) {
         // accumulator row of iv: abase + (iv - r0) * sP (sP = +-P, see the kernel), column iu
         PGET_CHECK(iu >= 0 && iu + 1 < P && iv >= r0 && iv < r1);
-        float2* a0 = acc + (abase + (iv - r0) * sP + iu);
+        const int aoff = abase + (iv - r0) * sP + iu;
+#if PGET_SCATTER == 0
+        float2* a0 = acc + aoff;
         const float2 t00 = a0[0], t01 = a0[1], t10 = a0[sP], t11 = a0[sP + 1];
+#endif
         const int i2 = i - 1;
         const int64_t u2 = u - dU, v2 = v - dV;
         const int iv2 = hi32(v2);
@@ -407,13 +419,29 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
         const float2 c10 = __ffma2_rn(c11, make_float2(-1.f, -1.f), tv);
         const float2 c01 = __fmul2_rn(bv, make_float2(fu, fu));
         const float2 c00 = __ffma2_rn(c01, make_float2(-1.f, -1.f), bv);
-#if PGET_ABLATE == 1   // experiment: no scatter (keeps the arithmetic alive through one store)
-        if (c00.x == 12345.f) a0[0] = make_float2(t00.x + c00.x + c01.x + c10.x + c11.x, c00.y + c01.y + c10.y + c11.y);
-#else
+#if PGET_SCATTER == 0
         a0[0] = make_float2(t00.x + c00.x, t00.y + c00.y);
         a0[1] = make_float2(t01.x + c01.x, t01.y + c01.y);
         a0[sP] = make_float2(t10.x + c10.x, t10.y + c10.y);
         a0[sP + 1] = make_float2(t11.x + c11.x, t11.y + c11.y);
+#else
+        if (aoff != poff) {
+            if (poff >= 0) {
+                float2* pa = acc + poff;
+                const float2 t00 = pa[0], t01 = pa[1], t10 = pa[sP], t11 = pa[sP + 1];
+                pa[0] = make_float2(t00.x + p00.x, t00.y + p00.y);
+                pa[1] = make_float2(t01.x + p01.x, t01.y + p01.y);
+                pa[sP] = make_float2(t10.x + p10.x, t10.y + p10.y);
+                pa[sP + 1] = make_float2(t11.x + p11.x, t11.y + p11.y);
+            }
+            poff = aoff;
+            p00 = c00; p01 = c01; p10 = c10; p11 = c11;
+        } else {
+            p00.x += c00.x; p00.y += c00.y;
+            p01.x += c01.x; p01.y += c01.y;
+            p10.x += c10.x; p10.y += c10.y;
+            p11.x += c11.x; p11.y += c11.y;
+        }
 #endif
         i = i2;
         u = u2;
@@ -426,6 +454,16 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
         fu = frac23(u);
         fv = frac23(v);
     }
+#if PGET_SCATTER == 1
+    {   // the last cell
+        float2* pa = acc + poff;
+        const float2 t00 = pa[0], t01 = pa[1], t10 = pa[sP], t11 = pa[sP + 1];
+        pa[0] = make_float2(t00.x + p00.x, t00.y + p00.y);
+        pa[1] = make_float2(t01.x + p01.x, t01.y + p01.y);
+        pa[sP] = make_float2(t10.x + p10.x, t10.y + p10.y);
+        pa[sP + 1] = make_float2(t11.x + p11.x, t11.y + p11.y);
+    }
+#endif
     st = x_;
 }
 
