@@ -1106,19 +1106,36 @@ __global__ void reduce_slots_kernel(const float2* __restrict__ slots, double2* _
     double2 acc[4], accT[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) acc[k] = accT[k] = make_double2(0.0, 0.0);
-    for (int e = e0 + (gq * n) / G; e < e0 + ((gq + 1) * n) / G; ++e) {
-        const int cls = e >= e1 ? 1 : 0;
-        const float2* sl = slots + static_cast<size_t>(red_slot[e]) * plane;
+    // slots in list order; four slots' loads are issued before their (in-order) additions, so each
+    // thread keeps 16 loads in flight (the kernel is latency-bound otherwise)
+    const int eb = e0 + (gq * n) / G, ee = e0 + ((gq + 1) * n) / G;
+    for (int e = eb; e < ee; e += 4) {
+        float2 v[4][4];
+        int cl[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            // class 0: element (row j, col i) = (j0 + ty + 8k, i0 + tx)
-            // class 1: element (row i, col j) of the transposed slot = (i0 + ty + 8k, j0 + tx)
-            const int rr = (cls ? i0 : j0) + ty + 8 * k, cc = (cls ? j0 : i0) + tx;
-            if (rr < N && cc < N) {
-                const float2 v = sl[static_cast<size_t>(rr) * Ns + cc];
-                double2& a = cls ? accT[k] : acc[k];
-                a.x += v.x;
-                a.y += v.y;
+        for (int t = 0; t < 4; ++t) {
+            cl[t] = -1;
+            if (e + t < ee) {
+                const int cls = e + t >= e1 ? 1 : 0;
+                cl[t] = cls;
+                const float2* sl = slots + static_cast<size_t>(red_slot[e + t]) * plane;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    // class 0: element (row j, col i) = (j0 + ty + 8k, i0 + tx)
+                    // class 1: element (row i, col j) of the transposed slot = (i0 + ty + 8k, j0 + tx)
+                    const int rr = (cls ? i0 : j0) + ty + 8 * k, cc = (cls ? j0 : i0) + tx;
+                    v[t][k] = (rr < N && cc < N) ? sl[static_cast<size_t>(rr) * Ns + cc] : make_float2(0.f, 0.f);
+                }
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            if (cl[t] < 0) continue;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                double2& a = cl[t] ? accT[k] : acc[k];
+                a.x += v[t][k].x;
+                a.y += v[t][k].y;
             }
         }
     }
