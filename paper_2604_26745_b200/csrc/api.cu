@@ -148,9 +148,9 @@ ProjCfg proj_cfg(const Geometry& g, int mode)
 
 int slot_pitch(const Geometry& g) { return (g.desc.n_px + 1) & ~1; }
 
-// Launch configuration of the segmented adjoint.  Phase A: 8 warps,
-// 2 CTAs per SM, up to 2 groups of 32 adjacent rays per warp, shared memory = two float4 stage
-// buffers.  Phase B: one CTA per SM, one comb group per warp (W = the group count over the fewest
+// Launch configuration of the segmented adjoint.  Phase A: 16 warps,
+// 1 CTA per SM (measured best of 4x4, 8x2, 8x1, 12x1, 16x1: scripts/sega_exp.sh), up to 2 groups of
+// 32 adjacent rays per warp, shared memory = two float4 stage buffers.  Phase B: one CTA per SM, one comb group per warp (W = the group count over the fewest
 // passes of <= 16 warps), shared memory = two float2 stages + the warps' band accumulators + the
 // per-ray constants.  Band heights: the largest (<= 32 rows) that fits.
 struct SegCfg {
@@ -165,12 +165,12 @@ SegCfg seg_cfg(const Geometry& g)
     const Schedule& S = g.sch[kSchedAdj];
     SegCfg c;
     const int ngA = (g.R + 31) / 32;
-    c.WA = 8;
+    c.WA = g.segA_W;
     c.maxgA = ngA > c.WA ? 2 : 1;
     c.passesA = std::max(1, (ngA + c.WA * c.maxgA - 1) / (c.WA * c.maxgA));
     const size_t per_sm = 233472;
     {
-        const size_t budget = std::min<size_t>(g.smem_optin, per_sm / 2 - 1024);
+        const size_t budget = std::min<size_t>(g.smem_optin, per_sm / g.segA_cps - 1024);
         int Rb = std::min(32, g.P - 1);
         size_t SB = 0;
         for (; Rb > 1; --Rb) {
@@ -181,7 +181,7 @@ SegCfg seg_cfg(const Geometry& g)
         c.RbA = Rb;
         c.stageA = static_cast<int>(SB);
         c.smemA = 128 + 2 * SB;
-        c.gridA = S.CA > 0 ? S.CA : 2 * g.sm_count;
+        c.gridA = S.CA > 0 ? S.CA : g.segA_cps * g.sm_count;
     }
     {
         const int ngB = std::max(1, S.max_gB);
@@ -490,11 +490,14 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     build_ray_params(g, &rays);
     if (e == cudaSuccess) e = cudaMalloc(&g.d_rays, rays.size() * sizeof(RayP));
     if (const char* ev = std::getenv("PGET_ADJ_FUSED")) g.adj_seg = std::atoi(ev) == 0;   // A/B experiments
+    if (const char* ev = std::getenv("PGET_SEGA_W")) g.segA_W = std::max(1, std::min(16, std::atoi(ev)));
+    if (const char* ev = std::getenv("PGET_SEGA_CPS")) g.segA_cps = std::max(1, std::min(4, std::atoi(ev)));
+    if (g.segA_W * 32 * g.segA_cps > 2048) g.segA_cps = 2048 / (g.segA_W * 32);
     for (int k = 0; k < 3 && e == cudaSuccess; ++k) {
         const int mode = k == kSchedFwd ? MODE_FWD : (k == kSchedJvp ? MODE_JVP : MODE_VJP);
         Schedule& S = g.sch[k];
         if (k == kSchedAdj && g.adj_seg) {
-            build_adj_schedule(g, rays, 2 * g.sm_count, g.sm_count, &S);
+            build_adj_schedule(g, rays, g.segA_cps * g.sm_count, g.sm_count, &S);
             const SegCfg sc = seg_cfg(g);
             build_adj_stages(sc.RbA, sc.passesA, sc.RbB, sc.passesB, &S);
         } else {

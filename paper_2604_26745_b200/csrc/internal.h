@@ -160,6 +160,7 @@ struct Geometry {
     size_t smem_optin = 227 * 1024;
     Schedule sch[3];   // kSchedFwd, kSchedJvp, kSchedAdj (schedule.cpp), device copies owned here
     bool adj_seg = true;   // adjoint (VJP / GN) as the segmented two-phase projector (else the fused one)
+    int segA_W = 16, segA_cps = 1;   // segmented phase A: warps per CTA, CTAs per SM (scripts/sega_exp.sh)
 };
 
 }  // namespace pget

@@ -787,7 +787,7 @@ __device__ void issue_seg_stage(const ProjArgs& A, int Rb, int64_t sidx, void* d
 
 // Phase A: sweep A of every ray of the CTA's units through the unit's rows; per-ray partials to A.segp.
 template <int MODE, int MAXG, bool PAIRED>
-__global__ void __launch_bounds__(256, 2) seg_a_kernel(ProjArgs A)
+__global__ void __launch_bounds__(512, 1) seg_a_kernel(ProjArgs A)   // 16 warps x 1 CTA/SM by default
 {
     using TR = ModeTraits<MODE>;
     const int W = blockDim.x >> 5;
