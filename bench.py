@@ -372,7 +372,7 @@ def main():
                 "projector_ms_per_launch": {k: (prof["ms"][k] / prof["launches"][k] if prof["launches"][k] else None)
                                             for k in prof["ms"]},
             },
-            "roofline": {"bound": "alu", "pipe": "shared-memory crossbar (128 B/clk/SM)", "kernel": f"proj_kernel<{dom}>",
+            "roofline": {"bound": "alu", "pipe": "shared-memory crossbar (128 B/clk/SM)", "kernel": (f"{dom}: seg_a_kernel + seg_b_kernel (segmented adjoint, one launch pair)" if dom in ("gn", "vjp") else f"proj_kernel<{dom}>"),
                          "achieved": achieved_gbs, "peak": peak_gbs, "unit": "GB/s", "frac": achieved_gbs / peak_gbs,
                          "traffic": traffic,
                          "peak_basis": f"128 B/clk/SM x 148 SMs x {sm_mhz:.0f} MHz (median SM clock under load)",

@@ -58,7 +58,12 @@ def full(rep):
     res = []
     for d in data:
         name = d[hdr.index("Kernel Name")]
-        mode = MODES.get(name.split("<")[1].split(",")[0].strip(), "?") if "proj_kernel<" in name else name
+        if "proj_kernel<" in name:
+            mode = MODES.get(name.split("<")[1].split(",")[0].strip(), "?")
+        elif "seg_a_kernel<" in name or "seg_b_kernel<" in name:   # segmented adjoint: phase A / B
+            mode = MODES.get(name.split("<")[1].split(",")[0].strip(), "?") + (" A" if "seg_a" in name else " B")
+        else:
+            mode = name
         vals = {}
         for k, lab in KEYS:
             if k in hdr:
@@ -76,8 +81,9 @@ def main():
              "serialised launches: compare shares, not absolute times).", ""]
     tab, n, T = launches(lst)
     lines += [f"{n} launches, {T / 1e3:.2f} ms total.", ""] + tab + [""]
-    lines += ["Full capture: `ncu --set full --clock-control none --import-source on -k regex:proj_kernel -c 4 "
-              "python scripts/prof_ops.py 2 1` (one launch of each projector mode, config 2).", ""]
+    lines += ["Full capture: `ncu --set full --clock-control none --import-source on -k regex:\"proj_kernel|seg_\" -c 6 "
+              "python scripts/prof_ops.py 2 1` (one launch of each projector kernel, config 2: forward and JVP "
+              "fused, VJP and GN as segmented phases A and B).", ""]
     res = full(rep)
     labs = [lab for _, lab in KEYS]
     lines.append("| metric | " + " | ".join(m for m, _, _ in res) + " |")
@@ -95,7 +101,9 @@ def main():
         rb, wb = v.get("dram read"), v.get("dram write")
         if rb and wb:
             mult = {"byte": 1, "B": 1, "Kbyte": 1e3, "KB": 1e3, "Mbyte": 1e6, "MB": 1e6, "Gbyte": 1e9, "GB": 1e9}
-            traffic[mode] = float(rb[0].replace(",", "")) * mult[rb[1]] + float(wb[0].replace(",", "")) * mult[wb[1]]
+            key = mode.split(" ")[0]   # the two phases of a segmented mode add up to one launch of that mode
+            traffic[key] = traffic.get(key, 0.0) + float(rb[0].replace(",", "")) * mult[rb[1]] + \
+                float(wb[0].replace(",", "")) * mult[wb[1]]
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     old = json.load(open(tp)) if os.path.exists(tp) else {}
     old["cfg2"] = traffic
