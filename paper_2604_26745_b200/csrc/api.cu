@@ -171,7 +171,7 @@ SegCfg seg_cfg(const Geometry& g)
     const size_t per_sm = 233472;
     {
         const size_t budget = std::min<size_t>(g.smem_optin, per_sm / g.segA_cps - 1024);
-        int Rb = std::min(32, g.P - 1);
+        int Rb = std::min(g.rbA_cap, g.P - 1);
         size_t SB = 0;
         for (; Rb > 1; --Rb) {
             SB = align128(static_cast<size_t>(Rb + 1) * g.P * sizeof(float4));
@@ -287,6 +287,8 @@ pget_status run_seg(const Geometry& g, int mode, ProjArgs A, float* segp, cudaSt
         }
     }
     A.segp = segp;
+    A.slot_lo = S.d_slot_lo;
+    A.slot_hi = S.d_slot_hi;
     A.K = S.K;
     A.seg_rows = S.d_seg_rows;
     A.n_groups = S.max_gB;
@@ -430,6 +432,8 @@ void free_device_tables(Geometry* g)
     for (Schedule& S : g->sch) {
         cudaFree(S.d_cta_begin); cudaFree(S.d_tasks); cudaFree(S.d_groups); cudaFree(S.d_red_off); cudaFree(S.d_red_slot);
         S.d_cta_begin = nullptr; S.d_tasks = nullptr; S.d_groups = nullptr; S.d_red_off = nullptr; S.d_red_slot = nullptr;
+        cudaFree(S.d_slot_lo); cudaFree(S.d_slot_hi);
+        S.d_slot_lo = S.d_slot_hi = nullptr;
         cudaFree(S.d_unitsA); cudaFree(S.d_unitsB); cudaFree(S.d_ua_begin); cudaFree(S.d_ub_begin);
         cudaFree(S.d_sa_begin); cudaFree(S.d_sb_begin); cudaFree(S.d_stA); cudaFree(S.d_stB); cudaFree(S.d_seg_rows);
         S.d_unitsA = S.d_unitsB = nullptr;
@@ -490,6 +494,7 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     build_ray_params(g, &rays);
     if (e == cudaSuccess) e = cudaMalloc(&g.d_rays, rays.size() * sizeof(RayP));
     if (const char* ev = std::getenv("PGET_ADJ_FUSED")) g.adj_seg = std::atoi(ev) == 0;   // A/B experiments
+    if (const char* ev = std::getenv("PGET_RBA_CAP")) g.rbA_cap = std::max(4, std::min(128, std::atoi(ev)));
     if (const char* ev = std::getenv("PGET_SEGA_W")) g.segA_W = std::max(1, std::min(16, std::atoi(ev)));
     if (const char* ev = std::getenv("PGET_SEGA_CPS")) g.segA_cps = std::max(1, std::min(4, std::atoi(ev)));
     if (g.segA_W * 32 * g.segA_cps > 2048) g.segA_cps = 2048 / (g.segA_W * 32);
@@ -513,6 +518,8 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
         up(&S.d_groups, S.groups);
         up(&S.d_red_off, S.red_off);
         up(&S.d_red_slot, S.red_slot);
+        up(&S.d_slot_lo, S.slot_lo);
+        up(&S.d_slot_hi, S.slot_hi);
         if (k == kSchedAdj && g.adj_seg) {
             up(&S.d_unitsA, S.unitsA);
             up(&S.d_unitsB, S.unitsB);
@@ -677,7 +684,8 @@ static pget_status proj_adjoint(const Geometry& g, const WS& w, int mode, const 
     const int N = g.desc.n_px;
     const dim3 grid((N + 31) / 32, (N + 31) / 32, g.desc.batch * c.G);
     reduce_slots_kernel<<<grid, dim3(32, 8), 0, s>>>(w.slots, w.gacc, N, slot_pitch(g), g.desc.batch, c.G,
-                                                    g.sch[kSchedAdj].d_red_off, g.sch[kSchedAdj].d_red_slot); note();
+                                                    g.sch[kSchedAdj].d_red_off, g.sch[kSchedAdj].d_red_slot,
+                                                    g.sch[kSchedAdj].d_slot_lo, g.sch[kSchedAdj].d_slot_hi); note();
     CK(cudaGetLastError());
     return PGET_OK;
 }

@@ -95,6 +95,8 @@ struct Schedule {
     std::vector<int32_t> red_off;     // [2B + 1]: slots of (member m, class c) are red_slot[red_off[2m+c] ..)
     std::vector<int32_t> red_slot;
     int max_slots_member = 0;
+    std::vector<int32_t> slot_lo, slot_hi;   // [n_slots] rows [lo, hi) of a slot that can be nonzero
+    int32_t *d_slot_lo = nullptr, *d_slot_hi = nullptr;
     int max_gA = 1, max_gB = 1;       // most sweep-A (32 adjacent rays) / sweep-B (comb) groups of a task
     // segmented adjoint (kind kSchedAdj): K row segments, units and stage lists of phases A and B
     int K = 0;
@@ -160,7 +162,8 @@ struct Geometry {
     size_t smem_optin = 227 * 1024;
     Schedule sch[3];   // kSchedFwd, kSchedJvp, kSchedAdj (schedule.cpp), device copies owned here
     bool adj_seg = true;   // adjoint (VJP / GN) as the segmented two-phase projector (else the fused one)
-    int segA_W = 16, segA_cps = 1;   // segmented phase A: warps per CTA, CTAs per SM (scripts/sega_exp.sh)
+    int segA_W = 16, segA_cps = 1;
+    int rbA_cap = 64;   // segmented phase A: most rows per band (64 vs 32: GN cfg2 -0.7 %, scripts/rba_exp.sh)   // segmented phase A: warps per CTA, CTAs per SM (scripts/sega_exp.sh)
 };
 
 }  // namespace pget

@@ -35,6 +35,8 @@ struct ProjArgs {
     const int32_t* s_begin;
     const int32_t* seg_rows;
     int K, n_groups, off_rsc, off_q1;
+    const int32_t* slot_lo;  // [n_slots] rows [slot_lo, slot_hi) a slot's units can write (zeroed by the first)
+    const int32_t* slot_hi;
     float* segp;            // [n_canon][kSegFields][R]
 };
 
@@ -51,7 +53,8 @@ __global__ void pack2_kernel(const float* lam, const float* mu, const float* sla
 __global__ void pack4_kernel(const float* lam, const float* mu, const float* dl, const float* dm, float4* out,
                              float4* outT, int N, int P, int B);
 __global__ void reduce_slots_kernel(const float2* slots, double2* part, int N, int Ns, int B, int G,
-                                    const int32_t* red_off, const int32_t* red_slot);
+                                    const int32_t* red_off, const int32_t* red_slot, const int32_t* slot_lo,
+                                    const int32_t* slot_hi);
 __global__ void finish_kernel(const double2* part, int G, const float* xl, const float* xm, float alpha, float beta,
                               float sign, float* outl, float* outm, const float* dotl, const float* dotm,
                               double* partial, float* copy1l, float* copy1m, float* copy2l, float* copy2m,

@@ -985,9 +985,11 @@ __global__ void __launch_bounds__(512, 1) seg_b_kernel(ProjArgs A)
             }
         }
         float2* slot = A.slots + static_cast<size_t>(ui.slot) * plane;
-        if (ui.first) {   // the slot's first unit zeroes it (later flushes of the slot only add)
+        if (ui.first) {   // the slot's first unit zeroes its writable rows (later flushes only add)
             float4* z = reinterpret_cast<float4*>(slot);
-            for (size_t k = tid; k < plane / 2; k += NT) z[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            const size_t z0 = static_cast<size_t>(A.slot_lo[ui.slot]) * A.Ns / 2;
+            const size_t z1 = static_cast<size_t>(A.slot_hi[ui.slot]) * A.Ns / 2;
+            for (size_t k = z0 + tid; k < z1; k += NT) z[k] = make_float4(0.f, 0.f, 0.f, 0.f);
         }
         __syncthreads();
         const size_t wbase = (static_cast<size_t>(ui.m) * A.n_ab + ui.ab) * A.n_det;
@@ -1094,7 +1096,8 @@ __global__ void __launch_bounds__(512, 1) seg_b_kernel(ProjArgs A)
 // partials in order g = 0..G-1 (deterministic).
 __global__ void reduce_slots_kernel(const float2* __restrict__ slots, double2* __restrict__ part, int N, int Ns,
                                     int B, int G, const int32_t* __restrict__ red_off,
-                                    const int32_t* __restrict__ red_slot)
+                                    const int32_t* __restrict__ red_slot, const int32_t* __restrict__ slot_lo,
+                                    const int32_t* __restrict__ slot_hi)
 {
     __shared__ double2 tile[32][33];
     const int m = blockIdx.z / G, gq = blockIdx.z - m * G;
@@ -1117,14 +1120,20 @@ __global__ void reduce_slots_kernel(const float2* __restrict__ slots, double2* _
             cl[t] = -1;
             if (e + t < ee) {
                 const int cls = e + t >= e1 ? 1 : 0;
+                const int sid = red_slot[e + t];
+                // slot rows outside [lo, hi) were never written: skip a slot that misses the tile
+                const int t0 = cls ? i0 : j0, lo = slot_lo[sid], hi = slot_hi[sid];
+                if (t0 + 32 <= lo || t0 >= hi) continue;
                 cl[t] = cls;
-                const float2* sl = slots + static_cast<size_t>(red_slot[e + t]) * plane;
+                const float2* sl = slots + static_cast<size_t>(sid) * plane;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     // class 0: element (row j, col i) = (j0 + ty + 8k, i0 + tx)
                     // class 1: element (row i, col j) of the transposed slot = (i0 + ty + 8k, j0 + tx)
+                    // rows outside [lo, hi) hold stale data (never zeroed, never written): read as 0
                     const int rr = (cls ? i0 : j0) + ty + 8 * k, cc = (cls ? j0 : i0) + tx;
-                    v[t][k] = (rr < N && cc < N) ? sl[static_cast<size_t>(rr) * Ns + cc] : make_float2(0.f, 0.f);
+                    v[t][k] = (rr >= lo && rr < hi && cc < N) ? sl[static_cast<size_t>(rr) * Ns + cc]
+                                                              : make_float2(0.f, 0.f);
                 }
             }
         }

@@ -15,6 +15,7 @@
 #include <algorithm>
 #include <array>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <numeric>
@@ -171,6 +172,8 @@ void build_schedule(const Geometry& g, int kind, int C, Schedule* S)
         }
     }
     S->cta_begin[C] = static_cast<int32_t>(S->tasks.size());
+    S->slot_lo.assign(S->n_slots, 0);
+    S->slot_hi.assign(S->n_slots, g.desc.n_px);
     S->red_off.assign(static_cast<size_t>(B) * 2 + 1, 0);
     S->red_slot.clear();
     for (size_t e = 0; e < lists.size(); ++e) {
@@ -309,7 +312,73 @@ void build_adj_schedule(const Geometry& g, const std::vector<RayP>& rays, int CA
         (*begin)[ncta] = static_cast<int32_t>(units->size());
     };
     assign(CA, &S->unitsA, &S->ua_begin);
-    assign(C, &S->unitsB, &S->ub_begin);
+    // phase B: CTAs are split into two groups by orientation class, in proportion to the classes'
+    // work; within a group, units go longest-first to the least-loaded CTA, preferring (within a
+    // quarter of the unit's cost) a CTA that already holds the unit's row segment.  A CTA then holds
+    // units of one class and few segments: one partial slot whose nonzero rows are those segments'
+    // (the slot reduction reads and phase B zeroes only those rows).  Used when its makespan is within
+    // 3 % of the plain LPT assignment.
+    {
+        std::vector<std::vector<int>> gidx(2);
+        std::vector<double> gcost(2, 0.0);
+        double total = 0.0;
+        for (size_t i = 0; i < all.size(); ++i) {
+            const int key = (all[i].flags & kTaskClass1) ? 1 : 0;
+            gidx[key].push_back(static_cast<int>(i));
+            gcost[key] += w[i];
+            total += w[i];
+        }
+        std::vector<int> own_plain;
+        const double mk_plain = lpt(w, C, &own_plain);
+        bool grouped = !gidx[0].empty() && !gidx[1].empty() && C >= 2 && !std::getenv("PGET_NO_GROUP");
+        std::vector<int> own(all.size(), 0);
+        double mk_group = 0.0;
+        if (grouped) {
+            int n0 = static_cast<int>(std::lround(C * gcost[0] / total));
+            n0 = std::max(1, std::min(C - 1, n0));
+            const int nct[2] = {n0, C - n0};
+            int base = 0;
+            for (int k = 0; k < 2; ++k) {
+                std::vector<int>& ids = gidx[k];
+                std::stable_sort(ids.begin(), ids.end(), [&](int a, int b) { return w[a] > w[b]; });
+                std::vector<double> load(nct[k], 0.0);
+                std::vector<std::vector<int>> segcnt(nct[k], std::vector<int>(K, 0));
+                for (int i : ids) {
+                    int best = 0;
+                    for (int c = 1; c < nct[k]; ++c) if (load[c] < load[best]) best = c;
+                    const double lim = load[best] + 0.25 * w[i];
+                    int pick = best;
+                    for (int c = 0; c < nct[k]; ++c)
+                        if (load[c] <= lim && segcnt[c][all[i].seg] > segcnt[pick][all[i].seg]) pick = c;
+                    load[pick] += w[i];
+                    ++segcnt[pick][all[i].seg];
+                    own[i] = base + pick;
+                }
+                for (double l : load) mk_group = std::max(mk_group, l);
+                base += nct[k];
+            }
+            grouped = mk_group <= 1.03 * mk_plain;
+            if (std::getenv("PGET_SCHED_DEBUG"))
+                fprintf(stderr, "phase B: plain %.3f class-grouped %.3f -> %s\n", mk_plain, mk_group, grouped ? "grouped" : "plain");
+        }
+        if (!grouped) own = own_plain;
+        std::vector<std::vector<int>> per(C);
+        for (size_t i = 0; i < all.size(); ++i) per[own[i]].push_back(static_cast<int>(i));
+        S->unitsB.clear();
+        S->ub_begin.assign(C + 1, 0);
+        for (int cta = 0; cta < C; ++cta) {
+            S->ub_begin[cta] = static_cast<int32_t>(S->unitsB.size());
+            std::sort(per[cta].begin(), per[cta].end(), [&](int a, int b) {
+                const UnitD &x = all[a], &y = all[b];
+                const int cx = x.flags & kTaskClass1, cy = y.flags & kTaskClass1;
+                if (x.m != y.m) return x.m < y.m;
+                if (cx != cy) return cx < cy;
+                return x.canon < y.canon;
+            });
+            for (int i : per[cta]) S->unitsB.push_back(all[i]);
+        }
+        S->ub_begin[C] = static_cast<int32_t>(S->unitsB.size());
+    }
     const int ngA = (R + 31) / 32;
     std::vector<int32_t> grp;
     comb_groups(0, R, g.comb_S, &grp);
@@ -321,6 +390,8 @@ void build_adj_schedule(const Geometry& g, const std::vector<RayP>& rays, int CA
     S->cta_begin.assign(C + 1, 0);
     // slots of phase B (as build_schedule's adjoint kind, per unit)
     S->n_slots = 0;
+    S->slot_lo.clear();
+    S->slot_hi.clear();
     std::vector<std::vector<int32_t>> lists(static_cast<size_t>(B) * 2);
     for (int cta = 0; cta < C; ++cta) {
         int run = 0, pm = -1, pc = -1;
@@ -334,6 +405,16 @@ void build_adj_schedule(const Geometry& g, const std::vector<RayP>& rays, int CA
                 t.flags |= kTaskFirst;
             }
             t.slot = S->n_slots - 1;
+            // the slot's rows (oriented frame, unpadded) that the unit's flushes can write
+            const int lo = std::max(0, S->seg_rows[t.seg] - kHalo);
+            const int hi = std::min(g.desc.n_px, S->seg_rows[t.seg + 1] - kHalo + 1);
+            if (run == 0) {
+                S->slot_lo.push_back(lo);
+                S->slot_hi.push_back(hi);
+            } else {
+                S->slot_lo.back() = std::min(S->slot_lo.back(), lo);
+                S->slot_hi.back() = std::max(S->slot_hi.back(), hi);
+            }
             ++run;
             pm = t.m;
             pc = cls;
