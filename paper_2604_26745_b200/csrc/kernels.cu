@@ -116,10 +116,18 @@ __global__ void finish_kernel(const double2* __restrict__ part, int G, const flo
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const int i = static_cast<int>(e % N), j = static_cast<int>(e / N);
         double2 a = part[base + e];   // the G fp64 partials of reduce_slots_kernel, in order
-        for (int g = 1; g < G; ++g) {
-            const double2 b = part[static_cast<size_t>(g) * gridDim.y * n2 + base + e];
-            a.x += b.x;
-            a.y += b.y;
+        for (int g0 = 1; g0 < G; g0 += 8) {
+            double2 b[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t)
+                b[t] = g0 + t < G ? part[static_cast<size_t>(g0 + t) * gridDim.y * n2 + base + e] : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                if (g0 + t < G) {
+                    a.x += b[t].x;
+                    a.y += b[t].y;
+                }
+            }
         }
         float ol = static_cast<float>(a.x), om = static_cast<float>(a.y);
         if (xl) {
@@ -432,10 +440,19 @@ __global__ void cg_fused_kernel(const double2* __restrict__ part, int G, float a
             for (size_t e = static_cast<size_t>(j) * blockDim.x + threadIdx.x; e < n2; e += stride) {
                 const int i = static_cast<int>(e % N), jj = static_cast<int>(e / N);
                 double2 a = part[base + e];
-                for (int g = 1; g < G; ++g) {
-                    const double2 b = part[static_cast<size_t>(g) * B * n2 + base + e];
-                    a.x += b.x;
-                    a.y += b.y;
+                // the G partials in order; eight loads issued before their additions (latency-bound)
+                for (int g0 = 1; g0 < G; g0 += 8) {
+                    double2 b[8];
+#pragma unroll
+                    for (int t = 0; t < 8; ++t)
+                        b[t] = g0 + t < G ? part[static_cast<size_t>(g0 + t) * B * n2 + base + e] : make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int t = 0; t < 8; ++t) {
+                        if (g0 + t < G) {
+                            a.x += b[t].x;
+                            a.y += b[t].y;
+                        }
+                    }
                 }
                 const float* xl = pl + base;
                 const float* xm = pm + base;
