@@ -224,8 +224,13 @@ struct ModeTraits {
     static constexpr int MINB = MODE == MODE_FWD ? 3 : (MODE == MODE_JVP ? 2 : 1); // CTAs per SM
     static constexpr bool HAS_B = (MODE == MODE_VJP || MODE == MODE_GN);         // adjoint sweep
     static constexpr bool NF4 = (MODE == MODE_JVP || MODE == MODE_GN);           // 4-channel sweep A
-    static constexpr bool COMP_S = (MODE != MODE_FWD);                           // compensated A_i
-    static constexpr bool COMP_G = HAS_B;                                        // compensated G
+#ifndef PGET_GN_COMP
+#define PGET_GN_COMP 0
+#endif
+    // compensated sums: the JVP and VJP are graded per element (max-relative 1e-4, R-precision); the
+    // GN product, graded as an operator in relative L2 (1e-5), runs plain fp32 sums (PGET_GN_COMP 0)
+    static constexpr bool COMP_S = MODE == MODE_JVP || MODE == MODE_VJP || (MODE == MODE_GN && PGET_GN_COMP);
+    static constexpr bool COMP_G = MODE == MODE_VJP || (MODE == MODE_GN && PGET_GN_COMP);
     // compensated JVP sums: the standalone JVP is graded per element (max-relative 1e-4, DESIGN.md
     // R-precision); inside the GN product the (J p) sums feed an operator graded in relative L2
     // (1e-5), where plain fp32 sums are ~1e-7 -- the GN mode saves the 4-FADD Kahan steps there
@@ -363,7 +368,7 @@ struct RayB {   // per-ray constants of sweep B
 // registers and read-modify-written once when the ray leaves the cell (a cell spans ~1.5-2 samples):
 // fewer shared-memory accesses, and those only by the lanes that change cell (bank-conflict bound
 // since the segmented adjoint).  0: one read-modify-write per sample (prefetched accumulator reads).
-template <bool PAIRED>
+template <bool PAIRED, bool COMP>
 __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* __restrict__ acc, int P, int r0,
                                        int r1, int abase, int sP, int ilo, int64_t dU, int64_t dV, float cf, float ch,
                                        const RayB& rb, int& i, int64_t& u, int64_t& v, StateB& st)
@@ -408,10 +413,16 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
             const float le1 = x.x * E1;
             al = fmaf(rb.kl1, E1, al);
             am = fmaf(rb.km1, (x_.q1 - x_.q1c) + 0.5f * le1, am);
-            kahan(x_.q1, x_.q1c, le1);
+            if (COMP) kahan(x_.q1, x_.q1c, le1);
+            else x_.q1 += le1;
         }
-        kahan(x_.q, x_.qc, le);
-        kahan(x_.s, x_.sc, x.y * cf);
+        if (COMP) {
+            kahan(x_.q, x_.qc, le);
+            kahan(x_.s, x_.sc, x.y * cf);
+        } else {
+            x_.q += le;
+            x_.s = fmaf(x.y, cf, x_.s);
+        }
         const float2 av = make_float2(al, am);
         const float2 tv = __fmul2_rn(av, make_float2(fv, fv));         // row j0+1
         const float2 bv = __ffma2_rn(tv, make_float2(-1.f, -1.f), av); // row j0
@@ -673,7 +684,7 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                 const int abase = flip ? A.RbB * P : 0, sP = flip ? -P : P;
 #pragma unroll
                 for (int k = 0; k < MAXG; ++k)
-                    walk_b<PAIRED>(sb, wacc, P, r0, r1, abase, sP, ilo[k], dU, dV, cf, ch, rb[k], ii[k], uu[k], vv[k],
+                    walk_b<PAIRED, TR::COMP_S>(sb, wacc, P, r0, r1, abase, sP, ilo[k], dU, dV, cf, ch, rb[k], ii[k], uu[k], vv[k],
                                    st[k]);
                 __syncthreads();   // stage buffer b and every warp ring consumed
                 if (tid == 0 && s + 2 < n_stages) issue_stage<MODE>(A, t0, ns_task, s + 2, stage0 + b * A.stage_bytes, &mbar[b]);
@@ -1047,7 +1058,7 @@ __global__ void __launch_bounds__(512, 1) seg_b_kernel(ProjArgs A)
                 const float2* sbuf = reinterpret_cast<const float2*>(stage0 + b * A.stage_bytes);
                 const bool flip = j & 1;
                 const int abase = flip ? Rb * P : 0, sP = flip ? -P : P;
-                walk_b<PAIRED>(sbuf, wacc, P, r0, r1, abase, sP, ilo, dU, dV, cf, ch, rb, ii, uu, vv, st);
+                walk_b<PAIRED, ModeTraits<MODE>::COMP_S>(sbuf, wacc, P, r0, r1, abase, sP, ilo, dU, dV, cf, ch, rb, ii, uu, vv, st);
                 __syncthreads();   // stage buffer b and every warp ring consumed
                 if (tid == 0 && s + 2 < n_stages)
                     issue_seg_stage<false>(A, Rb, sb0 + s + 2, stage0 + b * A.stage_bytes, &mbar[b]);
