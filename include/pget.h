@@ -116,7 +116,7 @@ enum {
 
 /* Operation ids for pget_workspace_bytes. */
 enum { PGET_OP_FORWARD = 0, PGET_OP_JVP = 1, PGET_OP_VJP = 2, PGET_OP_GN_CG_STEP = 3, PGET_OP_GN_APPLY = 4,
-       PGET_OP_SAFEGUARD = 5 };
+       PGET_OP_SAFEGUARD = 5, PGET_OP_LM_SOLVE = 6 };
 
 /* Flags for pget_gn_cg_step. */
 #define PGET_GN_EVAL_TRIAL 1u   /* also evaluate f(u+s), rho, the accept decision and beta_next */
@@ -143,6 +143,20 @@ typedef struct {
     int32_t pad_;
     double cg_res[PGET_MAX_CG + 1]; /* ||z_k||, k = 0..n_cg                                   */
 } pget_gn_stats;
+
+/* Parameters of pget_lm_solve (host struct).  (PAPER.md:144-182, 288.) */
+#define PGET_LM_BOX 1u   /* project every iterate onto [lam_lo, lam_hi] x [mu_lo, mu_hi] */
+typedef struct {
+    int32_t n_iter;       /* LM iterations                                                    */
+    int32_t n_cg;         /* CG steps per iteration, 0 <= n_cg <= PGET_MAX_CG                  */
+    float alpha0;         /* penalty weight of iteration 0                                     */
+    float alpha_decay;    /* alpha_k = alpha0 / alpha_decay^min(k, k_freeze) (paper: 5, :288)   */
+    int32_t k_freeze;     /* iteration from which alpha stays fixed                            */
+    float beta0;          /* initial LM parameter of every member                              */
+    float lam_lo, lam_hi, mu_lo, mu_hi;   /* the box (PGET_LM_BOX)                              */
+    uint32_t flags;       /* PGET_LM_BOX                                                       */
+    int32_t pad_;
+} pget_lm_params;
 
 /* Device-resident result of the Prop. 1 safeguard check, per batch member (array of `batch`).
  * (Prop. 1 eq:rho_agreement, eq:uk+1_condition;
@@ -206,6 +220,20 @@ pget_status pget_gn_cg_step(pget_geometry g, const float* lam, const float* mu, 
                             float alpha, float beta, int32_t n_cg, uint32_t flags, float* s_lam,
                             float* s_mu, pget_gn_stats* stats_dev, void* ws, size_t ws_bytes,
                             pget_stream_t stream);
+
+/* Full LM solve (the paper's deterministic LMA iterated; the alpha continuation
+ * alpha_k = alpha0 / 5^k frozen later), per batch member, on the device: for
+ * k = 0..n_iter-1 one pget_gn_cg_step at (u_k, alpha_k, beta_k) with PGET_GN_EVAL_TRIAL, where with
+ * PGET_LM_BOX the CG step is first replaced by s' = clamp(u_k + s) - u_k (pred and rho then refer to
+ * s'; reading R-N1: a projected step instead of the paper's scaled gradient projection); then
+ * u_{k+1} = u_k + s' if rho > 0.1 (accepted) else u_k, and beta_{k+1} = beta_next (x10 on reject, at
+ * least beta_min; x0.2 if rho > 0.75).  With PGET_LM_BOX the initial guess is clamped first.
+ * lam, mu: device images, updated in place.  stats_dev: n_iter * batch pget_gn_stats records, iteration-major,
+ * receiving every iteration's statistics.  Workspace: pget_workspace_bytes(g, PGET_OP_LM_SOLVE).
+ * No host synchronisation; errors as for pget_gn_cg_step. */
+pget_status pget_lm_solve(pget_geometry g, float* lam, float* mu, const float* y_meas,
+                          const pget_lm_params* params, pget_gn_stats* stats_dev, void* ws,
+                          size_t ws_bytes, pget_stream_t stream);
 
 /* Safeguarded acceptance of an externally supplied candidate u~ = (cand_lam, cand_mu) against the
  * LM step s_k = (s_lam, s_mu) at u_k = (lam, mu) (Proposition 1; the check of

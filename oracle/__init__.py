@@ -51,6 +51,7 @@ def _load():
             ("orc_gn_cg_step", [P, P, P, P, C.c_double, C.c_double, C.c_int, P, P, P]),
             ("orc_apply_H", [P, P, P, C.c_double, C.c_double, P, P]),
             ("orc_safeguard", [P, P, P, P, P, P, P, P, C.c_double, C.c_double, P, P]),
+            ("orc_lm_solve", [P, P, P, P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_double, P, P]),
         ]:
             f = getattr(_lib, name)
             f.argtypes = args
@@ -220,3 +221,28 @@ def safeguard(g, lam, mu, y, s_lam, s_mu, c_lam, c_mu, alpha, kappa=0.1):
         res.append(dict(f=out[0], f_cand=out[1], m0=out[2], m_cand=out[3], m_lm=out[4], rho_cand=out[5],
                         accepted=bool(out[6]), pred_cand=out[2] - out[3], pred_lm=out[2] - out[4]))
     return (nl, nm), res
+
+
+def lm_solve(g, lam, mu, y, n_iter, n_cg, alpha0, alpha_decay=5.0, k_freeze=0, beta0=0.0, box=None):
+    """O9: n_iter LM iterations per batch member.  Returns ((lam, mu), [[stats dict per iteration]
+    per member])."""
+    lib = _load()
+    B = int(g.get("batch", 1))
+    shp = img_shape(g)
+    lam_o, mu_o = _f64(lam).reshape(shp).copy(), _f64(mu).reshape(shp).copy()
+    ys = _f64(y).reshape(B, -1)
+    d = _desc(dict(g, batch=1))
+    bx = None if box is None else np.ascontiguousarray(box, dtype=np.float64)
+    out = []
+    for m in range(B):
+        l = np.ascontiguousarray(lam_o[m])
+        u = np.ascontiguousarray(mu_o[m])
+        st = np.zeros(n_iter * (ST_CG + n_cg + 1))
+        rc = lib.orc_lm_solve(C.byref(d), _p(l), _p(u), _p(np.ascontiguousarray(ys[m])), int(n_iter), int(n_cg),
+                              float(alpha0), float(alpha_decay), int(k_freeze), float(beta0),
+                              None if bx is None else _p(bx), _p(st))
+        assert rc == 0, rc
+        lam_o[m], mu_o[m] = l, u
+        row = ST_CG + n_cg + 1
+        out.append([stats_dict(st[k * row:(k + 1) * row], n_cg) for k in range(n_iter)])
+    return (lam_o, mu_o), out

@@ -19,6 +19,7 @@
  *   LM step (J^T J + alpha L^T L + beta I) s = -grad f, m_k, rho_k
  *       -- PAPER.md:160-180 eq:m-function, eq:LMA-step; PAPER.md:248 eq:rho_agreement
  *       -- inner solver: plain CG (reading Q12) instead of the paper's SGP.
+ *   LM solve: alpha continuation, beta schedule, box projection -- PAPER.md:144-182, 288 (O9, N1)
  *   safeguard u_{k+1} = u~ iff m_k(s~) <= m_k(s_k) and rho_k(s~) > kappa
  *       -- PAPER.md:241-258 Prop. 1 eq:uk+1_condition; Algorithm 2 PAPER.md:290-313 (O8, N2)
  *
@@ -476,8 +477,21 @@ static double objective(const orc_desc* g, const double* lam, const double* mu, 
     return *misfit + *reg;
 }
 
+/* One LM iteration; box (NULL or {lam_lo, lam_hi, mu_lo, mu_hi}) replaces the CG step by the step
+ * actually taken inside the box, s' = clamp(u + s) - u, before pred and the trial (reading R-N1). */
+static int lm_step(const orc_desc* g, const double* lam, const double* mu, const double* y, double alpha,
+                   double beta, int n_cg, const double* box, double* s_lam, double* s_mu, double* stats);
+
 int orc_gn_cg_step(const orc_desc* g, const double* lam, const double* mu, const double* y,
                    double alpha, double beta, int n_cg, double* s_lam, double* s_mu, double* stats)
+{
+    return lm_step(g, lam, mu, y, alpha, beta, n_cg, NULL, s_lam, s_mu, stats);
+}
+
+static double clampd(double x, double lo, double hi) { return x < lo ? lo : (x > hi ? hi : x); }
+
+static int lm_step(const orc_desc* g, const double* lam, const double* mu, const double* y, double alpha,
+                   double beta, int n_cg, const double* box, double* s_lam, double* s_mu, double* stats)
 {
     size_t npx = (size_t)g->batch * g->n_px * g->n_px;
     size_t ns = (size_t)g->batch * g->n_angles * g->n_banks * g->n_det;
@@ -533,6 +547,12 @@ int orc_gn_cg_step(const orc_desc* g, const double* lam, const double* mu, const
     stats[9] = k;
     stats[11] = beta_min;
 
+    /* (N1) the step actually taken inside the box */
+    if (box)
+        for (size_t i = 0; i < npx; ++i) {
+            s[i] = clampd(lam[i] + s[i], box[0], box[1]) - lam[i];
+            s[npx + i] = clampd(mu[i] + s[npx + i], box[2], box[3]) - mu[i];
+        }
     /* 6: pred = <b,s> - 1/2(||Js||^2 + alpha||Ls||^2) */
     orc_jvp(g, lam, mu, s, s + npx, NULL, ys);
     double js2 = dot(ys, ys, ns);
@@ -547,6 +567,11 @@ int orc_gn_cg_step(const orc_desc* g, const double* lam, const double* mu, const
 
     /* 7: f(u+s), rho */
     for (size_t i = 0; i < npx; ++i) { ut[i] = lam[i] + s[i]; ut[npx + i] = mu[i] + s[npx + i]; }
+    if (box)
+        for (size_t i = 0; i < npx; ++i) {
+            ut[i] = clampd(ut[i], box[0], box[1]);
+            ut[npx + i] = clampd(ut[npx + i], box[2], box[3]);
+        }
     double mis2, reg2;
     double f1 = objective(g, ut, ut + npx, y, alpha, &mis2, &reg2, r, tl);
     double rho = (f0 - f1) / pred;
@@ -626,6 +651,40 @@ int orc_safeguard(const orc_desc* g, const double* lam, const double* mu, const 
     }
     out[0] = f0; out[1] = fc; out[2] = m0; out[3] = mc; out[4] = ml; out[5] = rho; out[6] = acc;
     free(r); free(js); free(tl); free(tm); free(st); free(z);
+    return 0;
+}
+
+/* ------------------------------------------------------------------ O9 LM solve (N1) */
+/* n_iter LM iterations: alpha_k = alpha0 / decay^min(k, k_freeze),
+ * beta_0 = beta0 then beta_{k+1} = beta_next of iteration k, u_{k+1} = trial point if rho > 0.1 else
+ * u_k; with a box the initial guess is clamped and every step projected (lm_step).  lam, mu updated
+ * in place; stats: n_iter rows of (ST_CG + n_cg + 1) doubles as orc_gn_cg_step's. */
+int orc_lm_solve(const orc_desc* g, double* lam, double* mu, const double* y, int n_iter, int n_cg,
+                 double alpha0, double decay, int k_freeze, double beta0, const double* box, double* stats)
+{
+    size_t npx = (size_t)g->batch * g->n_px * g->n_px;
+    double* sl = (double*)malloc(sizeof(double) * npx);
+    double* sm = (double*)malloc(sizeof(double) * npx);
+    if (!sl || !sm) return -2;
+    if (box)
+        for (size_t i = 0; i < npx; ++i) { lam[i] = clampd(lam[i], box[0], box[1]); mu[i] = clampd(mu[i], box[2], box[3]); }
+    double alpha = alpha0, beta = beta0;
+    const int row = ST_CG + n_cg + 1;
+    for (int k = 0; k < n_iter; ++k) {
+        if (k > 0 && k <= k_freeze) alpha /= decay;
+        double* st = stats + (size_t)k * row;
+        int rc = lm_step(g, lam, mu, y, alpha, beta, n_cg, box, sl, sm, st);
+        if (rc) { free(sl); free(sm); return rc; }
+        if (st[7] != 0.0)
+            for (size_t i = 0; i < npx; ++i) {
+                double a = lam[i] + sl[i], b = mu[i] + sm[i];
+                if (box) { a = clampd(a, box[0], box[1]); b = clampd(b, box[2], box[3]); }
+                lam[i] = a;
+                mu[i] = b;
+            }
+        beta = st[8];
+    }
+    free(sl); free(sm);
     return 0;
 }
 

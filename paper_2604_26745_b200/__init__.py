@@ -18,16 +18,16 @@ import numpy as np
 
 from ._build import LIB, build as _build_lib, needs_build as _needs_build
 
-__all__ = ["Geometry", "forward", "jvp", "vjp", "gn_apply", "gn_cg_step", "safeguard", "GNStats", "SafeguardStats", "lib",
+__all__ = ["Geometry", "forward", "jvp", "vjp", "gn_apply", "gn_cg_step", "safeguard", "lm_solve", "GNStats", "SafeguardStats", "LMParams", "lib",
            "PGET_GN_EVAL_TRIAL", "TABLES", "OPS"]
 
 PGET_GN_EVAL_TRIAL = 1
 PGET_MAX_CG = 256
 TABLES = {"angles": 0, "dirs": 1, "offsets": 2, "weights": 3, "tlat": 4, "clip": 5}
-OPS = {"forward": 0, "jvp": 1, "vjp": 2, "gn_cg_step": 3, "gn_apply": 4, "safeguard": 5}
+OPS = {"forward": 0, "jvp": 1, "vjp": 2, "gn_cg_step": 3, "gn_apply": 4, "safeguard": 5, "lm_solve": 6}
 EXPORTED = ["pget_status_string", "pget_last_error_message", "pget_geometry_create", "pget_geometry_destroy",
             "pget_geometry_info", "pget_table_bytes", "pget_geometry_export", "pget_workspace_bytes",
-            "pget_forward", "pget_jvp", "pget_vjp", "pget_gn_apply", "pget_gn_cg_step", "pget_safeguard", "pget_profile_begin",
+            "pget_forward", "pget_jvp", "pget_vjp", "pget_gn_apply", "pget_gn_cg_step", "pget_safeguard", "pget_lm_solve", "pget_profile_begin",
             "pget_profile_end"]
 MODES = ("forward", "jvp", "vjp", "gn")
 
@@ -59,6 +59,15 @@ class GNStats(C.Structure):
         n = self.n_cg_done if n_cg is None else n_cg
         d["cg_res"] = np.array(self.cg_res[: n + 1])
         return d
+
+
+PGET_LM_BOX = 1
+
+
+class LMParams(C.Structure):
+    _fields_ = [("n_iter", C.c_int32), ("n_cg", C.c_int32), ("alpha0", C.c_float), ("alpha_decay", C.c_float),
+                ("k_freeze", C.c_int32), ("beta0", C.c_float), ("lam_lo", C.c_float), ("lam_hi", C.c_float),
+                ("mu_lo", C.c_float), ("mu_hi", C.c_float), ("flags", C.c_uint32), ("pad_", C.c_int32)]
 
 
 class SafeguardStats(C.Structure):
@@ -102,10 +111,11 @@ def lib():
         L.pget_gn_apply.argtypes = [P, P, P, P, P, C.c_float, C.c_float, P, P, P, S, P]
         L.pget_gn_cg_step.argtypes = [P, P, P, P, C.c_float, C.c_float, C.c_int32, C.c_uint32, P, P, P, P, S, P]
         L.pget_safeguard.argtypes = [P, P, P, P, P, P, P, P, C.c_float, C.c_float, P, P, P, P, S, P]
+        L.pget_lm_solve.argtypes = [P, P, P, P, C.POINTER(LMParams), P, P, S, P]
         L.pget_profile_begin.argtypes = [C.c_int32]
         L.pget_profile_end.argtypes = [P, P, P]
         for n in ("pget_profile_begin", "pget_profile_end", "pget_geometry_create", "pget_geometry_destroy", "pget_geometry_info", "pget_geometry_export",
-                  "pget_forward", "pget_jvp", "pget_vjp", "pget_gn_apply", "pget_gn_cg_step", "pget_safeguard"):
+                  "pget_forward", "pget_jvp", "pget_vjp", "pget_gn_apply", "pget_gn_cg_step", "pget_safeguard", "pget_lm_solve"):
             getattr(L, n).restype = C.c_int
         _lib = L
     return _lib
@@ -316,3 +326,23 @@ def safeguard(g: Geometry, lam, mu, y_meas, s_lam, s_mu, cand_lam, cand_mu, alph
     host = buf.cpu().numpy().tobytes()
     n = C.sizeof(SafeguardStats)
     return u_next, [SafeguardStats.from_buffer_copy(host[m * n:(m + 1) * n]).to_dict() for m in range(B)]
+
+
+def lm_solve(g: Geometry, lam, mu, y_meas, n_iter, n_cg=20, alpha0=1e-3, alpha_decay=5.0, k_freeze=0, beta0=0.0,
+             box=None, ws=None, stream=None):
+    """Full LM solve (pget_lm_solve): lam, mu are updated in place.  box = (lam_lo, lam_hi, mu_lo, mu_hi)
+    or None.  Returns [[stats dict per member] per iteration]."""
+    import torch
+    _f32(lam, g.img_shape, "lam"); _f32(mu, g.img_shape, "mu"); _f32(y_meas, g.sino_shape, "y_meas")
+    p = LMParams(int(n_iter), int(n_cg), float(alpha0), float(alpha_decay), int(k_freeze), float(beta0),
+                 *(float(x) for x in (box if box is not None else (0.0, 0.0, 0.0, 0.0))),
+                 PGET_LM_BOX if box is not None else 0, 0)
+    B = g.info["batch"]
+    buf = torch.zeros(max(1, n_iter) * B * C.sizeof(GNStats), dtype=torch.uint8, device=lam.device)
+    ws = g.workspace("lm_solve") if ws is None else ws
+    _check(lib().pget_lm_solve(g.handle, _ptr(lam), _ptr(mu), _ptr(y_meas), C.byref(p), _ptr(buf), _ptr(ws),
+                               ws.numel(), _stream(stream)), "pget_lm_solve")
+    host = buf.cpu().numpy().tobytes()
+    n = C.sizeof(GNStats)
+    return [[GNStats.from_buffer_copy(host[(k * B + m) * n:(k * B + m + 1) * n]).to_dict(n_cg) for m in range(B)]
+            for k in range(n_iter)]

@@ -333,6 +333,7 @@ struct WS {
     float *ysino = nullptr, *dysino = nullptr;
     float *bl = nullptr, *bm = nullptr, *zl = nullptr, *zm = nullptr, *pl = nullptr, *pm = nullptr;
     float *ql = nullptr, *qm = nullptr, *ul = nullptr, *um = nullptr;
+    float *sl = nullptr, *sm = nullptr, *beta = nullptr;   // pget_lm_solve
     double* part = nullptr;   // [8][B][kNblk]
     CGState* cg = nullptr;
     size_t bytes = 0;
@@ -352,10 +353,10 @@ WS carve(const Geometry& g, int op, char* base)
         return p;
     };
     const bool guard = op == PGET_OP_SAFEGUARD;
-    const bool need2 = op == PGET_OP_FORWARD || op == PGET_OP_VJP || op == PGET_OP_GN_APPLY || op == PGET_OP_GN_CG_STEP ||
-                       guard;
-    const bool need4 = op == PGET_OP_JVP || op == PGET_OP_GN_APPLY || op == PGET_OP_GN_CG_STEP || guard;
-    const bool needacc = op == PGET_OP_VJP || op == PGET_OP_GN_APPLY || op == PGET_OP_GN_CG_STEP;
+    const bool lm = op == PGET_OP_GN_CG_STEP || op == PGET_OP_LM_SOLVE;
+    const bool need2 = op == PGET_OP_FORWARD || op == PGET_OP_VJP || op == PGET_OP_GN_APPLY || lm || guard;
+    const bool need4 = op == PGET_OP_JVP || op == PGET_OP_GN_APPLY || lm || guard;
+    const bool needacc = op == PGET_OP_VJP || op == PGET_OP_GN_APPLY || lm;
     for (int k = 0; k < 2; ++k) {
         if (need2) w.img2[k] = reinterpret_cast<float2*>(take(img * sizeof(float2)));
         if (need4) w.img4[k] = reinterpret_cast<float4*>(take(img * sizeof(float4)));
@@ -370,13 +371,18 @@ WS carve(const Geometry& g, int op, char* base)
             w.segp = reinterpret_cast<float*>(take(static_cast<size_t>(g.sch[kSchedAdj].n_canon) * kSegFields *
                                                    g.R * sizeof(float)));
     }
-    if (op == PGET_OP_GN_CG_STEP) {
+    if (op == PGET_OP_GN_CG_STEP || op == PGET_OP_LM_SOLVE) {
         w.ysino = reinterpret_cast<float*>(take(ns * sizeof(float)));
         w.dysino = reinterpret_cast<float*>(take(ns * sizeof(float)));
         float** vecs[] = {&w.bl, &w.bm, &w.zl, &w.zm, &w.pl, &w.pm, &w.ql, &w.qm, &w.ul, &w.um};
         for (float** v : vecs) *v = reinterpret_cast<float*>(take(n2 * sizeof(float)));
         w.part = reinterpret_cast<double*>(take(8 * B * kNblk * sizeof(double)));
         w.cg = reinterpret_cast<CGState*>(take(B * sizeof(CGState)));
+        if (op == PGET_OP_LM_SOLVE) {   // the step, per-member beta
+            w.sl = reinterpret_cast<float*>(take(n2 * sizeof(float)));
+            w.sm = reinterpret_cast<float*>(take(n2 * sizeof(float)));
+            w.beta = reinterpret_cast<float*>(take(B * sizeof(float)));
+        }
     }
     if (guard) {
         w.ysino = reinterpret_cast<float*>(take(ns * sizeof(float)));
@@ -635,17 +641,18 @@ pget_status pget_geometry_export(pget_geometry h, int id, void* dst, size_t byte
 
 size_t pget_workspace_bytes(pget_geometry h, int op)
 {
-    if (!h || op < 0 || op > PGET_OP_SAFEGUARD) return 0;
+    if (!h || op < 0 || op > PGET_OP_LM_SOLVE) return 0;
     return carve(h->g, op, nullptr).bytes + 256;
 }
 
 // ---- building blocks (all enqueued on s)
 static pget_status pack2(const Geometry& g, const WS& w, const float* lam, const float* mu, const float* slam,
-                         const float* smu, float* ul, float* um, cudaStream_t s)
+                         const float* smu, float* ul, float* um, cudaStream_t s, const float4* box = nullptr)
 {
     const size_t img = static_cast<size_t>(g.desc.batch) * g.P * g.P;
     pack2_kernel<<<vec_grid(img), kVecThreads, 0, s>>>(lam, mu, slam, smu, w.img2[0], w.img2[1], ul, um,
-                                                      g.desc.n_px, g.P, g.desc.batch); note();
+                                                      g.desc.n_px, g.P, g.desc.batch, box ? 1 : 0,
+                                                      box ? *box : make_float4(0.f, 0.f, 0.f, 0.f)); note();
     CK(cudaGetLastError());
     return PGET_OK;
 }
@@ -759,19 +766,15 @@ pget_status pget_gn_apply(pget_geometry h, const float* lam, const float* mu, co
     return PGET_OK;
 }
 
-pget_status pget_gn_cg_step(pget_geometry h, const float* lam, const float* mu, const float* y_meas, float alpha,
-                            float beta, int32_t n_cg, uint32_t flags, float* s_lam, float* s_mu,
-                            pget_gn_stats* stats, void* ws, size_t ws_bytes, pget_stream_t stream)
+// One LM iteration (see pget_gn_cg_step) on a carved workspace.  betav (device, per member, nullable)
+// overrides beta; box (nullable) projects the step onto [lam_lo, lam_hi] x [mu_lo, mu_hi] before
+// pred and the trial (reading R-N1).
+static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const float* mu,
+                              const float* y_meas, float alpha, float beta, const float* betav, int32_t n_cg,
+                              uint32_t flags, float* s_lam, float* s_mu, pget_gn_stats* stats, const float4* box,
+                              cudaStream_t s)
 {
-    WS w;
-    pget_status st = check_common(h, PGET_OP_GN_CG_STEP, ws, ws_bytes, &w);
-    if (st) return st;
-    if ((st = check_ptrs({lam, mu, y_meas, s_lam, s_mu, stats}, "pget_gn_cg_step"))) return st;
-    if (n_cg < 0 || n_cg > PGET_MAX_CG) return fail(PGET_ERR_INVALID_ARGUMENT, "n_cg out of [0, PGET_MAX_CG]");
-    if (!std::isfinite(alpha) || !std::isfinite(beta) || alpha < 0.f || beta < 0.f)
-        return fail(PGET_ERR_INVALID_ARGUMENT, "alpha, beta must be finite and >= 0");
-    const Geometry& g = h->g;
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    pget_status st;
     const int N = g.desc.n_px, B = g.desc.batch;
     const int n2 = N * N;
     const int nsper = g.n_ab * g.desc.n_det;
@@ -792,7 +795,7 @@ pget_status pget_gn_cg_step(pget_geometry h, const float* lam, const float* mu, 
     finish_kernel<<<vg, kVecThreads, 0, s>>>(w.gacc, Gv, lam, mu, alpha, 0.f, -1.f, w.bl, w.bm, w.bl, w.bm, P[2], w.zl,
                                             w.zm, w.pl, w.pm, s_lam, s_mu, N); note();
     CK(cudaGetLastError());
-    scalar_kernel<<<sgrid, 128, 0, s>>>(SC_INIT, 0, P[0], P[1], P[2], kNblk, w.cg, stats, B, alpha, beta); note();
+    scalar_kernel<<<sgrid, 128, 0, s>>>(SC_INIT, 0, P[0], P[1], P[2], kNblk, w.cg, stats, B, alpha, beta, betav); note();
     CK(cudaGetLastError());
     // 5: CG
     for (int k = 0; k < n_cg; ++k) {
@@ -803,7 +806,8 @@ pget_status pget_gn_cg_step(pget_geometry h, const float* lam, const float* mu, 
             float al = alpha, be = beta;
             double *pg = P[3], *pz = P[4];
             CGState* cgs = w.cg;
-            void* args[] = {&w.gacc, &GG, &al, &be, &s_lam, &s_mu, &w.zl, &w.zm, &w.pl, &w.pm, &w.ql, &w.qm,
+            const float* bv = betav;
+            void* args[] = {&w.gacc, &GG, &al, &be, &bv, &s_lam, &s_mu, &w.zl, &w.zm, &w.pl, &w.pm, &w.ql, &w.qm,
                             &pg, &pz, &cgs, &stats, &kk, &NN, &BB, &nb};
             const int grid = std::min(B * kNblk, g.cg_coop_blocks);
             CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cg_fused_kernel), dim3(grid), dim3(kVecThreads),
@@ -812,21 +816,86 @@ pget_status pget_gn_cg_step(pget_geometry h, const float* lam, const float* mu, 
         }
         CK(cudaGetLastError());
     }
+    // (N1) the step actually taken inside the box: s <- clamp(u + s) - u
+    if (box) {
+        const size_t n = static_cast<size_t>(B) * n2;
+        project_step_kernel<<<vec_grid(n), kVecThreads, 0, s>>>(lam, mu, s_lam, s_mu, n, box->x, box->y, box->z,
+                                                                box->w); note();
+        CK(cudaGetLastError());
+    }
     // 6: pred = <b,s> - 1/2(||Js||^2 + alpha ||Ls||^2)
     if ((st = pack4(g, w, lam, mu, s_lam, s_mu, s))) return st;
     if ((st = proj_out(g, w, MODE_JVP, nullptr, w.dysino, s))) return st;
     sumsq_kernel<<<vg, kVecThreads, 0, s>>>(w.dysino, P[5], nsper); note();
     regsq_kernel<<<vg, kVecThreads, 0, s>>>(s_lam, s_mu, P[6], N); note();
     dot2_kernel<<<vg, kVecThreads, 0, s>>>(w.bl, w.bm, s_lam, s_mu, P[7], n2); note();
-    scalar_kernel<<<sgrid, 128, 0, s>>>(SC_PRED, 0, P[5], P[6], P[7], kNblk, w.cg, stats, B, alpha, beta); note();
+    scalar_kernel<<<sgrid, 128, 0, s>>>(SC_PRED, 0, P[5], P[6], P[7], kNblk, w.cg, stats, B, alpha, beta, betav); note();
     CK(cudaGetLastError());
     // 7-8: f(u+s), rho, accept, beta_next
     if (flags & PGET_GN_EVAL_TRIAL) {
-        if ((st = pack2(g, w, lam, mu, s_lam, s_mu, w.ul, w.um, s))) return st;
+        if ((st = pack2(g, w, lam, mu, s_lam, s_mu, w.ul, w.um, s, box))) return st;
         if ((st = proj_out(g, w, MODE_FWD, w.ysino, nullptr, s))) return st;
         residual_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, y_meas, P[0], nsper); note();
         regsq_kernel<<<vg, kVecThreads, 0, s>>>(w.ul, w.um, P[1], N); note();
-        scalar_kernel<<<sgrid, 128, 0, s>>>(SC_TRIAL, 0, P[0], P[1], nullptr, kNblk, w.cg, stats, B, alpha, beta); note();
+        scalar_kernel<<<sgrid, 128, 0, s>>>(SC_TRIAL, 0, P[0], P[1], nullptr, kNblk, w.cg, stats, B, alpha, beta, betav); note();
+        CK(cudaGetLastError());
+    }
+    return PGET_OK;
+}
+
+pget_status pget_gn_cg_step(pget_geometry h, const float* lam, const float* mu, const float* y_meas, float alpha,
+                            float beta, int32_t n_cg, uint32_t flags, float* s_lam, float* s_mu,
+                            pget_gn_stats* stats, void* ws, size_t ws_bytes, pget_stream_t stream)
+{
+    WS w;
+    pget_status st = check_common(h, PGET_OP_GN_CG_STEP, ws, ws_bytes, &w);
+    if (st) return st;
+    if ((st = check_ptrs({lam, mu, y_meas, s_lam, s_mu, stats}, "pget_gn_cg_step"))) return st;
+    if (n_cg < 0 || n_cg > PGET_MAX_CG) return fail(PGET_ERR_INVALID_ARGUMENT, "n_cg out of [0, PGET_MAX_CG]");
+    if (!std::isfinite(alpha) || !std::isfinite(beta) || alpha < 0.f || beta < 0.f)
+        return fail(PGET_ERR_INVALID_ARGUMENT, "alpha, beta must be finite and >= 0");
+    return gn_cg_impl(h->g, w, lam, mu, y_meas, alpha, beta, nullptr, n_cg, flags, s_lam, s_mu, stats, nullptr,
+                      reinterpret_cast<cudaStream_t>(stream));
+}
+
+// Full LM solve: n_iter LM iterations with the alpha
+// continuation, per-member beta schedule, box projection and accept/reject, all on the device.
+pget_status pget_lm_solve(pget_geometry h, float* lam, float* mu, const float* y_meas, const pget_lm_params* prm,
+                          pget_gn_stats* stats, void* ws, size_t ws_bytes, pget_stream_t stream)
+{
+    WS w;
+    pget_status st = check_common(h, PGET_OP_LM_SOLVE, ws, ws_bytes, &w);
+    if (st) return st;
+    if ((st = check_ptrs({lam, mu, y_meas, stats}, "pget_lm_solve"))) return st;
+    if (!prm) return fail(PGET_ERR_INVALID_ARGUMENT, "pget_lm_solve: NULL params");
+    const pget_lm_params p = *prm;
+    if (p.n_iter < 0 || p.n_cg < 0 || p.n_cg > PGET_MAX_CG || p.k_freeze < 0)
+        return fail(PGET_ERR_INVALID_ARGUMENT, "pget_lm_solve: n_iter, n_cg or k_freeze out of range");
+    if (!std::isfinite(p.alpha0) || p.alpha0 < 0.f || !std::isfinite(p.alpha_decay) || p.alpha_decay < 1.f ||
+        !std::isfinite(p.beta0) || p.beta0 < 0.f)
+        return fail(PGET_ERR_INVALID_ARGUMENT, "pget_lm_solve: alpha0 >= 0, alpha_decay >= 1, beta0 >= 0 required");
+    const bool use_box = (p.flags & PGET_LM_BOX) != 0;
+    if (use_box && !(p.lam_lo <= p.lam_hi && p.mu_lo <= p.mu_hi))
+        return fail(PGET_ERR_INVALID_ARGUMENT, "pget_lm_solve: empty box");
+    const Geometry& g = h->g;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int N = g.desc.n_px, B = g.desc.batch, n2 = N * N;
+    const float4 box = make_float4(p.lam_lo, p.lam_hi, p.mu_lo, p.mu_hi);
+    fill_kernel<<<(B + 127) / 128, 128, 0, s>>>(w.beta, p.beta0, B); note();
+    CK(cudaGetLastError());
+    if (use_box) {   // the initial guess itself is projected onto the box
+        const size_t n = static_cast<size_t>(B) * n2;
+        clamp_kernel<<<vec_grid(n), kVecThreads, 0, s>>>(lam, mu, n, box.x, box.y, box.z, box.w); note();
+        CK(cudaGetLastError());
+    }
+    double alpha = p.alpha0;
+    for (int k = 0; k < p.n_iter; ++k) {
+        if (k > 0 && k <= p.k_freeze) alpha /= p.alpha_decay;   // alpha_k = alpha0 / decay^min(k, k_freeze)
+        pget_gn_stats* sk = stats + static_cast<size_t>(k) * B;
+        if ((st = gn_cg_impl(g, w, lam, mu, y_meas, static_cast<float>(alpha), 0.f, w.beta, p.n_cg,
+                             PGET_GN_EVAL_TRIAL, w.sl, w.sm, sk, use_box ? &box : nullptr, s)))
+            return st;
+        lm_update_kernel<<<dim3(vec_grid(n2), B), kVecThreads, 0, s>>>(lam, mu, w.ul, w.um, sk, w.beta, n2); note();
         CK(cudaGetLastError());
     }
     return PGET_OK;

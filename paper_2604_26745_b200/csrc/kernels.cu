@@ -16,8 +16,10 @@ namespace pget {
 // transposed orientation (orientation class 1 of the projector samples the transposed copy).
 __global__ void pack2_kernel(const float* __restrict__ lam, const float* __restrict__ mu,
                              const float* __restrict__ slam, const float* __restrict__ smu, float2* out,
-                             float2* outT, float* ut_lam, float* ut_mu, int N, int P, int B)
+                             float2* outT, float* ut_lam, float* ut_mu, int N, int P, int B, int has_box,
+                             float4 box)
 {
+    // has_box: box = (lam_lo, lam_hi, mu_lo, mu_hi) clamps the trial point u + s
     const size_t total = static_cast<size_t>(B) * P * P;
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -32,6 +34,10 @@ __global__ void pack2_kernel(const float* __restrict__ lam, const float* __restr
             if (slam) {
                 val.x += slam[src];
                 val.y += smu[src];
+                if (has_box) {
+                    val.x = fminf(fmaxf(val.x, box.x), box.y);
+                    val.y = fminf(fmaxf(val.y, box.z), box.w);
+                }
                 ut_lam[src] = val.x;
                 ut_mu[src] = val.y;
             }
@@ -355,12 +361,57 @@ __global__ void guard_select_kernel(const float* __restrict__ ul, const float* _
     }
 }
 
+// ---- full LM solve
+// box projection of the LM step: s <- clamp(u + s) - u (the step actually taken, reading R-N1)
+__global__ void project_step_kernel(const float* __restrict__ ul, const float* __restrict__ um, float* sl, float* sm,
+                                    size_t n, float llo, float lhi, float mlo, float mhi)
+{
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        sl[e] = fminf(fmaxf(ul[e] + sl[e], llo), lhi) - ul[e];
+        sm[e] = fminf(fmaxf(um[e] + sm[e], mlo), mhi) - um[e];
+    }
+}
+
+// accepted members take the trial point (evaluated by the LM wrap, clamped to the box when one is
+// set); every member takes its next LM parameter
+__global__ void lm_update_kernel(float* ul, float* um, const float* __restrict__ tl, const float* __restrict__ tm,
+                                 const pget_gn_stats* stats, float* betav, int n2)
+{
+    const int m = blockIdx.y;
+    const bool acc = stats[m].accepted != 0;
+    const size_t base = static_cast<size_t>(m) * n2;
+    if (acc)
+        for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n2; e += gridDim.x * blockDim.x) {
+            ul[base + e] = tl[base + e];
+            um[base + e] = tm[base + e];
+        }
+    if (blockIdx.x == 0 && threadIdx.x == 0) betav[m] = static_cast<float>(stats[m].beta_next);
+}
+
+__global__ void clamp_kernel(float* ul, float* um, size_t n, float llo, float lhi, float mlo, float mhi)
+{
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        ul[e] = fminf(fmaxf(ul[e], llo), lhi);
+        um[e] = fminf(fmaxf(um[e], mlo), mhi);
+    }
+}
+
+__global__ void fill_kernel(float* x, float v, int n)
+{
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n) x[e] = v;
+}
+
 // Scalar steps of the LM iteration (one thread per member).
 __global__ void scalar_kernel(int op, int k, const double* p0, const double* p1, const double* p2, int nblk,
-                              CGState* st, pget_gn_stats* stats, int B, double alpha, double beta)
+                              CGState* st, pget_gn_stats* stats, int B, double alpha, double beta_h,
+                              const float* betav)
 {
     const int m = blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= B) return;
+    const double beta = betav ? static_cast<double>(betav[m]) : beta_h;   // per-member LM parameter
     CGState& c = st[m];
     pget_gn_stats& S = stats[m];
     if (op == SC_INIT) {             // p0: 1/2||r||^2, p1: ||Lu||^2, p2: ||b||^2
@@ -420,10 +471,10 @@ __global__ void scalar_kernel(int op, int k, const double* p0, const double* p1,
 // with the same fixed-order fp64 block partials (nblk per member) and the same stop rules and
 // statistics as finish / scalar(SC_GAMMA) / cg_update1 / scalar(SC_ZETA) / cg_update2.
 // Work unit (member m, block-in-member j) -> elements e = j * blockDim + tid (+ nblk * blockDim).
-__global__ void cg_fused_kernel(const double2* __restrict__ part, int G, float alpha, float beta, float* sl,
-                                float* sm, float* zl, float* zm, float* pl, float* pm, float* ql, float* qm,
-                                double* pg, double* pz, CGState* st, pget_gn_stats* stats, int k, int N, int B,
-                                int nblk)
+__global__ void cg_fused_kernel(const double2* __restrict__ part, int G, float alpha, float beta_h,
+                                const float* betav, float* sl, float* sm, float* zl, float* zm, float* pl,
+                                float* pm, float* ql, float* qm, double* pg, double* pz, CGState* st,
+                                pget_gn_stats* stats, int k, int N, int B, int nblk)
 {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
@@ -436,6 +487,7 @@ __global__ void cg_fused_kernel(const double2* __restrict__ part, int G, float a
         const int m = mj / nblk, j = mj - m * nblk;
         const size_t base = static_cast<size_t>(m) * n2;
         double dsum = 0.0;
+        const float beta = betav ? betav[m] : beta_h;
         if (!st[m].stop) {
             for (size_t e = static_cast<size_t>(j) * blockDim.x + threadIdx.x; e < n2; e += stride) {
                 const int i = static_cast<int>(e % N), jj = static_cast<int>(e / N);

@@ -49,7 +49,14 @@ struct CGState {
 
 
 __global__ void pack2_kernel(const float* lam, const float* mu, const float* slam, const float* smu, float2* out,
-                             float2* outT, float* ut_lam, float* ut_mu, int N, int P, int B);
+                             float2* outT, float* ut_lam, float* ut_mu, int N, int P, int B, int has_box,
+                             float4 box);
+__global__ void project_step_kernel(const float* ul, const float* um, float* sl, float* sm, size_t n, float llo,
+                                    float lhi, float mlo, float mhi);
+__global__ void lm_update_kernel(float* ul, float* um, const float* tl, const float* tm, const pget_gn_stats* stats,
+                                 float* betav, int n2);
+__global__ void fill_kernel(float* x, float v, int n);
+__global__ void clamp_kernel(float* ul, float* um, size_t n, float llo, float lhi, float mlo, float mhi);
 __global__ void pack4_kernel(const float* lam, const float* mu, const float* dl, const float* dm, float4* out,
                              float4* outT, int N, int P, int B);
 __global__ void reduce_slots_kernel(const float2* slots, double2* part, int N, int Ns, int B, int G,
@@ -68,9 +75,10 @@ __global__ void cg_update1_kernel(float* sl, float* sm, float* zl, float* zm, co
                                   const float* ql, const float* qm, const CGState* st, double* partial, int n2);
 __global__ void cg_update2_kernel(const float* zl, const float* zm, float* pl, float* pm, const CGState* st,
                                   int n2);
-__global__ void cg_fused_kernel(const double2* part, int G, float alpha, float beta, float* sl, float* sm, float* zl,
-                                float* zm, float* pl, float* pm, float* ql, float* qm, double* pg, double* pz,
-                                CGState* st, pget_gn_stats* stats, int k, int N, int B, int nblk);
+__global__ void cg_fused_kernel(const double2* part, int G, float alpha, float beta_h, const float* betav, float* sl,
+                                float* sm, float* zl, float* zm, float* pl, float* pm, float* ql, float* qm,
+                                double* pg, double* pz, CGState* st, pget_gn_stats* stats, int k, int N, int B,
+                                int nblk);
 __global__ void dotsq_kernel(const float* a, const float* b, double* pdot, double* psq, int nper);
 __global__ void lapdot_kernel(const float* ul, const float* um, const float* sl, const float* sm, double* pdot,
                               double* psq, int N);
@@ -82,7 +90,8 @@ __global__ void guard_select_kernel(const float* ul, const float* um, const floa
                                     const float* cl, const float* cm, const pget_safeguard_stats* st, float* ol,
                                     float* om, int n2);
 __global__ void scalar_kernel(int op, int k, const double* p0, const double* p1, const double* p2, int nblk,
-                              CGState* st, pget_gn_stats* stats, int B, double alpha, double beta);
+                              CGState* st, pget_gn_stats* stats, int B, double alpha, double beta_h,
+                              const float* betav);
 
 }  // namespace pget
 

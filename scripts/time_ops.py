@@ -28,6 +28,14 @@ ops = {
 if "--lm" in sys.argv:   # one LM iteration (20 CG steps) at u0 for the measurements y = F(u)
     l0, m0 = map(dev, P.initial_guess(gd["n_px"], gd["batch"]))
     ops["lm"] = lambda: pg.gn_cg_step(g, l0, m0, y, 1e-3, 0.0, 20)
+if "--solve" in sys.argv:   # a 10-iteration LM solve (N1) from u0 with a box, restarted each repetition
+    l0h, m0h = P.initial_guess(gd["n_px"], gd["batch"])
+    ls, ms = dev(l0h), dev(m0h)
+    def solve():
+        ls.copy_(torch.from_numpy(l0h)); ms.copy_(torch.from_numpy(m0h))
+        return pg.lm_solve(g, ls, ms, y, 10, 20, alpha0=1e-2, alpha_decay=5.0, k_freeze=3, beta0=0.0,
+                           box=(0.0, 2.0, 0.0, 1.0))
+    ops["solve10"] = solve
 nom = g.info["n_samples_nominal"]
 out = {}
 for name, f in ops.items():

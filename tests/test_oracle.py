@@ -511,3 +511,85 @@ def test_p13_ground_truth_candidate_noise_free():
     _, [r] = O.safeguard(g, l0, m0, y, sl, sm, lt, mt, cfg.alpha, 0.1)
     reg = 0.5 * cfg.alpha * (np.sum(O.laplacian(lt) ** 2) + np.sum(O.laplacian(mt) ** 2))
     assert abs(r["f_cand"] - reg) <= 1e-12 * max(reg, 1e-300) + 1e-14 * r["f"]
+
+
+# ----------------------------------------------------------------------------- P14 LM solve (O9, N1)
+def _tiny_lm(n_px=16, n_angles=8, noise=True):
+    g = P.geometry_desc(2, n_px=n_px, n_angles=n_angles)
+    lt, mt = P.make_phantom(2, n_px=n_px)
+    yc = O.forward(g, lt, mt)
+    y = P.poisson_noise(yc, 1e4, 3) if noise else yc
+    l0, m0 = P.initial_guess(n_px)
+    return g, (lt, mt), y, (l0, m0)
+
+
+def test_p14_one_iteration_is_the_lm_wrap():
+    g, _, y, (l0, m0) = _tiny_lm()
+    (l1, m1), [sts] = O.lm_solve(g, l0, m0, y, 1, 6, 1e-3, beta0=0.05)
+    sl, sm, st = O.gn_cg_step(g, l0, m0, y, 1e-3, 0.05, 6)
+    for k in ("f", "pred", "f_trial", "rho", "beta_next"):
+        assert sts[0][k] == st[k], k
+    if st["accepted"]:
+        np.testing.assert_allclose(l1, l0 + sl, rtol=0, atol=0)
+    else:
+        np.testing.assert_array_equal(l1, l0)
+
+
+def test_p14_objective_chain_and_beta_rules():
+    """Constant alpha: f_{k+1} = f(u_k + s_k) when iteration k is accepted, else f_k; the LM parameter
+    follows the x10 (reject, >= beta_min) / x0.2 (rho > 0.75) rules from beta0."""
+    g, _, y, (l0, m0) = _tiny_lm()
+    _, [sts] = O.lm_solve(g, l0, m0, y, 6, 6, 1e-3, k_freeze=0, beta0=1.0)
+    beta = 1.0
+    for k in range(6):
+        s = sts[k]
+        if k + 1 < 6:
+            want = s["f_trial"] if s["accepted"] else s["f"]
+            assert abs(sts[k + 1]["f"] - want) <= 1e-12 * want
+        if s["accepted"]:
+            assert s["beta_next"] in (beta, 0.2 * beta)
+            assert (s["beta_next"] == 0.2 * beta) == (s["rho"] > 0.75)
+        else:
+            assert s["beta_next"] == max(10.0 * beta, s["beta_min"])
+        beta = s["beta_next"]
+    assert sts[-1]["f_trial"] < sts[0]["f"]
+
+
+def test_p14_alpha_continuation():
+    """alpha_k = alpha0 / 5^min(k, k_freeze): R(u_k) / (||L lam_k||^2 + ||L mu_k||^2) = alpha_k / 2."""
+    g, _, y, (l0, m0) = _tiny_lm()
+    n, kf = 5, 2
+    _, [sts] = O.lm_solve(g, l0, m0, y, n, 4, 1e-2, alpha_decay=5.0, k_freeze=kf, beta0=0.1)
+    for k in range(n):
+        (lk, mk), _ = O.lm_solve(g, l0, m0, y, k, 4, 1e-2, alpha_decay=5.0, k_freeze=kf, beta0=0.1)   # u_k
+        q = np.sum(O.laplacian(lk) ** 2) + np.sum(O.laplacian(mk) ** 2)
+        ak = 1e-2 / 5.0 ** min(k, kf)
+        assert abs(sts[k]["reg"] - 0.5 * ak * q) <= 1e-12 * sts[k]["reg"]
+
+
+def test_p14_box_projection():
+    """Every iterate lies in the box; a box that never binds reproduces the unconstrained solve; a
+    binding box changes the trajectory."""
+    g, _, y, (l0, m0) = _tiny_lm()
+    big = (-1e9, 1e9, -1e9, 1e9)
+    (la, ma), sa = O.lm_solve(g, l0, m0, y, 3, 6, 1e-3, beta0=0.1)
+    (lb, mb), sb = O.lm_solve(g, l0, m0, y, 3, 6, 1e-3, beta0=0.1, box=big)
+    np.testing.assert_array_equal(la, lb)
+    np.testing.assert_array_equal(ma, mb)
+    box = (0.0, 1.2, 0.0, 0.4)
+    (lc, mc), sc = O.lm_solve(g, l0, m0, y, 4, 6, 1e-3, beta0=0.1, box=box)
+    assert lc.min() >= 0.0 and lc.max() <= 1.2 and mc.min() >= 0.0 and mc.max() <= 0.4
+    (ld, md), _ = O.lm_solve(g, l0, m0, y, 4, 6, 1e-3, beta0=0.1)
+    assert ld.min() < 0.0 or ld.max() > 1.2 or md.min() < 0.0 or md.max() > 0.4   # the box binds
+    assert not np.array_equal(lc, ld)
+
+
+def test_p14_converges_on_noise_free_data():
+    """Noise-free data, alpha continuation 1e-2 / 5^k frozen at k = 4: the data misfit falls by more
+    than two orders of magnitude in 8 iterations and the iterate approaches the phantom."""
+    g, (lt, mt), y, (l0, m0) = _tiny_lm(noise=False)
+    (l8, m8), [sts] = O.lm_solve(g, l0, m0, y, 8, 12, 1e-2, alpha_decay=5.0, k_freeze=4, beta0=0.0)
+    assert sts[-1]["misfit"] < 1e-2 * sts[0]["misfit"]
+    e0 = np.linalg.norm(np.concatenate([(l0 - lt).ravel(), (m0 - mt).ravel()]))
+    e8 = np.linalg.norm(np.concatenate([(l8 - lt).ravel(), (m8 - mt).ravel()]))
+    assert e8 < 0.5 * e0
