@@ -176,6 +176,29 @@ def run_oracle_step(O, P, cfg, s):
     return time.perf_counter() - t0, s["samples_per_step"]
 
 
+def roofline_ncu(cid, dom):
+    """The north star's ncu view of the dominant kernel(s): speed-of-light fractions (issue slots,
+    FP32 and SFU pipes, L1/shared) from the committed ncu capture (profiles/ncu_sol.json, written by
+    scripts/ncu_summary.py); for the segmented modes one entry per phase kernel, weighted by time."""
+    p = os.path.join(ROOT, "profiles", "ncu_sol.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        d = json.load(open(p))
+        sol = d.get(f"cfg{cid}", {})
+        parts = {k: v for k, v in sol.items() if k == dom or k.startswith(dom + " ")}
+        if not parts:
+            return None
+        out = {"source": d.get("source"), "kernels": parts}
+        T = sum(v["duration_us"] or 0.0 for v in parts.values())
+        for key in ("sm_sol_pct", "issue_active_pct", "l1_smem_pct", "fma_pipe_pct", "xu_pipe_pct"):
+            out[key + "_time_weighted"] = (sum((v[key] or 0.0) * (v["duration_us"] or 0.0) for v in parts.values()) / T
+                                           if T else None)
+        return out
+    except Exception:
+        return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -378,6 +401,7 @@ def main():
                          "peak_basis": f"128 B/clk/SM x 148 SMs x {sm_mhz:.0f} MHz (median SM clock under load)",
                          "alg_bytes_per_sample": ALG_BYTES[dom], "units_per_launch": units,
                          "launch_ms": per_launch_ms},
+            "roofline_ncu": roofline_ncu(cfg.cid, dom),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

@@ -31,6 +31,7 @@ KEYS = [
     ("smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio", "stall barrier"),
     ("smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio", "stall math throttle"),
     ("sm__cycles_elapsed.avg.per_second", "SM clock"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM SOL %"),
 ]
 
 
@@ -104,6 +105,19 @@ def main():
             key = mode.split(" ")[0]   # the two phases of a segmented mode add up to one launch of that mode
             traffic[key] = traffic.get(key, 0.0) + float(rb[0].replace(",", "")) * mult[rb[1]] + \
                 float(wb[0].replace(",", "")) * mult[wb[1]]
+    # ncu speed-of-light fractions per kernel (the north star's "FP32/SFU issue" roofline as ncu
+    # measures it), for bench.py's roofline_ncu
+    sol = {}
+    for mode, name, v in res:
+        def num(lab):
+            x = v.get(lab)
+            return float(x[0].replace(",", "")) if x else None
+        sol[mode] = {"kernel": name.split("(")[0].replace("void ", ""), "duration_us": num("duration"),
+                     "sm_sol_pct": num("SM SOL %"), "issue_active_pct": num("issue active %"),
+                     "l1_smem_pct": num("L1/smem throughput %"), "fma_pipe_pct": num("FMA pipe %"),
+                     "xu_pipe_pct": num("XU (MUFU) %")}
+    json.dump({"cfg2": sol, "source": f"profiles/ncu_summary_{tag}.md"},
+              open(os.path.join(ROOT, "profiles", "ncu_sol.json"), "w"), indent=1)
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     old = json.load(open(tp)) if os.path.exists(tp) else {}
     old["cfg2"] = traffic
