@@ -165,7 +165,7 @@ SegCfg seg_cfg(const Geometry& g)
     const Schedule& S = g.sch[kSchedAdj];
     SegCfg c;
     const int ngA = (g.R + 31) / 32;
-    c.WA = g.segA_W;
+    c.WA = g.segA_W;   // consumer warps (the kernel adds one producer warp)
     c.maxgA = ngA > c.WA ? 2 : 1;
     c.passesA = std::max(1, (ngA + c.WA * c.maxgA - 1) / (c.WA * c.maxgA));
     const size_t per_sm = 233472;
@@ -173,14 +173,15 @@ SegCfg seg_cfg(const Geometry& g)
         const size_t budget = std::min<size_t>(g.smem_optin, per_sm / g.segA_cps - 1024);
         int Rb = std::min(g.rbA_cap, g.P - 1);
         size_t SB = 0;
+        constexpr int kStagesA = 3;   // seg_a_kernel's kSegAStages
         for (; Rb > 1; --Rb) {
             SB = align128(static_cast<size_t>(Rb + 1) * g.P * sizeof(float4));
-            if (128 + 2 * SB <= budget) break;
+            if (128 + kStagesA * SB <= budget) break;
         }
         SB = align128(static_cast<size_t>(Rb + 1) * g.P * sizeof(float4));
         c.RbA = Rb;
         c.stageA = static_cast<int>(SB);
-        c.smemA = 128 + 2 * SB;
+        c.smemA = 128 + kStagesA * SB;
         c.gridA = S.CA > 0 ? S.CA : g.segA_cps * g.sm_count;
     }
     {
@@ -302,7 +303,7 @@ pget_status run_seg(const Geometry& g, int mode, ProjArgs A, float* segp, cudaSt
     A.RbA = c.RbA;
     A.passesA = c.passesA;
     A.stage_bytes = c.stageA;
-    cudaError_t e = launch_seg(0, mode, c.maxgA, g.dup, A, c.gridA, c.WA * 32, c.smemA, s);
+    cudaError_t e = launch_seg(0, mode, c.maxgA, g.dup, A, c.gridA, (c.WA + 1) * 32, c.smemA, s);
     if (e == cudaSuccess) {
         A.units = S.d_unitsB;
         A.u_begin = S.d_ub_begin;
@@ -501,9 +502,9 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     if (e == cudaSuccess) e = cudaMalloc(&g.d_rays, rays.size() * sizeof(RayP));
     if (const char* ev = std::getenv("PGET_ADJ_FUSED")) g.adj_seg = std::atoi(ev) == 0;   // A/B experiments
     if (const char* ev = std::getenv("PGET_RBA_CAP")) g.rbA_cap = std::max(4, std::min(128, std::atoi(ev)));
-    if (const char* ev = std::getenv("PGET_SEGA_W")) g.segA_W = std::max(1, std::min(16, std::atoi(ev)));
+    if (const char* ev = std::getenv("PGET_SEGA_W")) g.segA_W = std::max(1, std::min(15, std::atoi(ev)));
     if (const char* ev = std::getenv("PGET_SEGA_CPS")) g.segA_cps = std::max(1, std::min(4, std::atoi(ev)));
-    if (g.segA_W * 32 * g.segA_cps > 2048) g.segA_cps = 2048 / (g.segA_W * 32);
+    if ((g.segA_W + 1) * 32 * g.segA_cps > 2048) g.segA_cps = 2048 / ((g.segA_W + 1) * 32);
     for (int k = 0; k < 3 && e == cudaSuccess; ++k) {
         const int mode = k == kSchedFwd ? MODE_FWD : (k == kSchedJvp ? MODE_JVP : MODE_VJP);
         Schedule& S = g.sch[k];

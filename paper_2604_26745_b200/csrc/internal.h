@@ -162,7 +162,7 @@ struct Geometry {
     size_t smem_optin = 227 * 1024;
     Schedule sch[3];   // kSchedFwd, kSchedJvp, kSchedAdj (schedule.cpp), device copies owned here
     bool adj_seg = true;   // adjoint (VJP / GN) as the segmented two-phase projector (else the fused one)
-    int segA_W = 16, segA_cps = 1;
+    int segA_W = 15, segA_cps = 1;
     int rbA_cap = 64;   // segmented phase A: most rows per band (64 vs 32: GN cfg2 -0.7 %, scripts/rba_exp.sh)   // segmented phase A: warps per CTA, CTAs per SM (scripts/sega_exp.sh)
 };
 

@@ -124,6 +124,11 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes)
                  : "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar)
+{
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
 {
     asm volatile(
@@ -797,13 +802,19 @@ __device__ void issue_seg_stage(const ProjArgs& A, int Rb, int64_t sidx, void* d
 }
 
 // Phase A: sweep A of every ray of the CTA's units through the unit's rows; per-ray partials to A.segp.
+// Warp-specialised pipeline: the last warp only issues the stage copies (kSegAStages buffers, a
+// "full" mbarrier per buffer completed by the copy's bytes, an "empty" mbarrier per buffer on which
+// every consumer warp arrives when done with it), so consumer warps never wait for one another.
+constexpr int kSegAStages = 3;
+
 template <int MODE, int MAXG, bool PAIRED>
-__global__ void __launch_bounds__(512, 1) seg_a_kernel(ProjArgs A)   // 16 warps x 1 CTA/SM by default
+__global__ void __launch_bounds__(512, 1) seg_a_kernel(ProjArgs A)   // W consumer warps + 1 producer warp
 {
     using TR = ModeTraits<MODE>;
-    const int W = blockDim.x >> 5;
+    const int W = (blockDim.x >> 5) - 1;   // consumer warps
     extern __shared__ __align__(128) unsigned char smem[];
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+    uint64_t* empty = full + kSegAStages;
     unsigned char* const stage0 = smem + 128;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int c = blockIdx.x;
@@ -812,14 +823,21 @@ __global__ void __launch_bounds__(512, 1) seg_a_kernel(ProjArgs A)   // 16 warps
     if (n_stages == 0) return;
     const int P = A.P, R = A.R, Rb = A.RbA;
     if (tid == 0) {
-        mbar_init(&mbar[0], 1);
-        mbar_init(&mbar[1], 1);
+        for (int b = 0; b < kSegAStages; ++b) {
+            mbar_init(&full[b], 1);
+            mbar_init(&empty[b], W);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (tid == 0) {
-        issue_seg_stage<TR::NF4>(A, Rb, sb0, stage0, &mbar[0]);
-        if (n_stages > 1) issue_seg_stage<TR::NF4>(A, Rb, sb0 + 1, stage0 + A.stage_bytes, &mbar[1]);
+    if (warp == W) {   // producer
+        if (lane == 0)
+            for (int64_t s = 0; s < n_stages; ++s) {
+                const int b = static_cast<int>(s % kSegAStages);
+                if (s >= kSegAStages) mbar_wait(&empty[b], static_cast<uint32_t>((s / kSegAStages - 1) & 1));
+                issue_seg_stage<TR::NF4>(A, Rb, sb0 + s, stage0 + b * A.stage_bytes, &full[b]);
+            }
+        return;
     }
     int64_t s = 0;
     const float cf = A.cf, ch = A.ch, dl = A.delta, dlh = 0.5f * A.delta;
@@ -850,15 +868,14 @@ __global__ void __launch_bounds__(512, 1) seg_a_kernel(ProjArgs A)   // 16 warps
             for (int j = 0; j < ui.nb; ++j) {
                 int r0, r1;
                 seg_band(ui, j, Rb, r0, r1);
-                const int b = static_cast<int>(s & 1);
-                mbar_wait(&mbar[b], static_cast<uint32_t>((s >> 1) & 1));
+                const int b = static_cast<int>(s % kSegAStages);
+                mbar_wait(&full[b], static_cast<uint32_t>((s / kSegAStages) & 1));
                 const unsigned char* sbuf = stage0 + b * A.stage_bytes;
 #pragma unroll
                 for (int k = 0; k < MAXG; ++k)
                     walk_a<MODE, PAIRED>(sbuf, P, r0, r1, ilo[k], dU, dV, cf, ch, dl, dlh, ii[k], uu[k], vv[k], st[k]);
-                __syncthreads();   // stage buffer b consumed
-                if (tid == 0 && s + 2 < n_stages)
-                    issue_seg_stage<TR::NF4>(A, Rb, sb0 + s + 2, stage0 + b * A.stage_bytes, &mbar[b]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[b]);   // this warp is done with buffer b
                 ++s;
             }
 #pragma unroll
