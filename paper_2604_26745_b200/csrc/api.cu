@@ -331,6 +331,8 @@ struct WS {
     float2* slots = nullptr;
     double2* gacc = nullptr;  // [G][B][N][N] fp64 partial gradients (g_lam, g_mu), G = ProjCfg::G
     float* segp = nullptr;    // segmented adjoint: [n_canon][kSegFields][R] phase-A partial sums
+    float4* cache = nullptr;  // GN with cached Jacobian entries: [B][rows][32]
+    float* jp = nullptr;      // [n_canon][2][R] per-segment (J p) partials
     float *ysino = nullptr, *dysino = nullptr;
     float *bl = nullptr, *bm = nullptr, *zl = nullptr, *zm = nullptr, *pl = nullptr, *pm = nullptr;
     float *ql = nullptr, *qm = nullptr, *ul = nullptr, *um = nullptr;
@@ -371,6 +373,11 @@ WS carve(const Geometry& g, int op, char* base)
         if (g.adj_seg)
             w.segp = reinterpret_cast<float*>(take(static_cast<size_t>(g.sch[kSchedAdj].n_canon) * kSegFields *
                                                    g.R * sizeof(float)));
+        if (g.adj_seg && g.gn_cached && op != PGET_OP_VJP) {
+            const Schedule& S = g.sch[kSchedAdj];
+            w.cache = reinterpret_cast<float4*>(take(static_cast<size_t>(B) * S.cache_rows_member * 32 * sizeof(float4)));
+            w.jp = reinterpret_cast<float*>(take(static_cast<size_t>(S.n_canon) * 2 * g.R * sizeof(float)));
+        }
     }
     if (op == PGET_OP_GN_CG_STEP || op == PGET_OP_LM_SOLVE) {
         w.ysino = reinterpret_cast<float*>(take(ns * sizeof(float)));
@@ -443,6 +450,8 @@ void free_device_tables(Geometry* g)
         S.d_slot_lo = S.d_slot_hi = nullptr;
         cudaFree(S.d_unitsA); cudaFree(S.d_unitsB); cudaFree(S.d_ua_begin); cudaFree(S.d_ub_begin);
         cudaFree(S.d_sa_begin); cudaFree(S.d_sb_begin); cudaFree(S.d_stA); cudaFree(S.d_stB); cudaFree(S.d_seg_rows);
+        cudaFree(S.d_cache_off);
+        S.d_cache_off = nullptr;
         S.d_unitsA = S.d_unitsB = nullptr;
         S.d_ua_begin = S.d_ub_begin = S.d_sa_begin = S.d_sb_begin = S.d_seg_rows = nullptr;
         S.d_stA = S.d_stB = nullptr;
@@ -501,6 +510,12 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     build_ray_params(g, &rays);
     if (e == cudaSuccess) e = cudaMalloc(&g.d_rays, rays.size() * sizeof(RayP));
     if (const char* ev = std::getenv("PGET_ADJ_FUSED")) g.adj_seg = std::atoi(ev) == 0;   // A/B experiments
+    if (const char* ev = std::getenv("PGET_GN_CACHE_MAX_GB")) g.cache_max_gb = std::atof(ev);
+    if (const char* ev = std::getenv("PGET_GN_CACHE")) {   // 0: recompute, 1: hybrid, 2: fully cached
+        const int v = std::atoi(ev);
+        g.gn_cached = v != 0;
+        g.gn_hybrid = v == 1;
+    }
     if (const char* ev = std::getenv("PGET_RBA_CAP")) g.rbA_cap = std::max(4, std::min(128, std::atoi(ev)));
     if (const char* ev = std::getenv("PGET_SEGA_W")) g.segA_W = std::max(1, std::min(15, std::atoi(ev)));
     if (const char* ev = std::getenv("PGET_SEGA_CPS")) g.segA_cps = std::max(1, std::min(4, std::atoi(ev)));
@@ -512,6 +527,10 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
             build_adj_schedule(g, rays, g.segA_cps * g.sm_count, g.sm_count, &S);
             const SegCfg sc = seg_cfg(g);
             build_adj_stages(sc.RbA, sc.passesA, sc.RbB, sc.passesB, &S);
+            // the coefficient cache only while it stays small next to HBM (config 2: 0.4 GB, config 4:
+            // 2.7 GB; config 5's 64 assemblies would need 25 GB: recompute there)
+            const double cache_gb = static_cast<double>(g.desc.batch) * S.cache_rows_member * 32 * sizeof(float4) / 1e9;
+            if (cache_gb > g.cache_max_gb) g.gn_cached = false;
         } else {
             build_schedule(g, k, g.sm_count * proj_ctas_per_sm(mode), &S);
         }
@@ -537,6 +556,7 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
             up(&S.d_sa_begin, S.sa_begin);
             up(&S.d_sb_begin, S.sb_begin);
             up(&S.d_seg_rows, S.seg_rows);
+            up(&S.d_cache_off, S.cache_off);
         }
     }
     if (e == cudaSuccess) e = cudaMalloc(&g.d_w, g.wf.size() * sizeof(float));
@@ -554,6 +574,7 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
             if (e == cudaSuccess) e = set_seg_smem_limit(0, mode, sc.smemA);
             if (e == cudaSuccess) e = set_seg_smem_limit(1, mode, sc.smemB);
         }
+        if (e == cudaSuccess) e = set_gnc_smem_limit(sc.smemB);
     }
     if (prev >= 0) cudaSetDevice(prev);
     if (e != cudaSuccess) {
@@ -698,6 +719,104 @@ static pget_status proj_adjoint(const Geometry& g, const WS& w, int mode, const 
     return PGET_OK;
 }
 
+// GN with cached Jacobian entries: args shared by the three kernels (phase-B units,
+// groups, stage list and launch shape of the segmented adjoint)
+static ProjArgs gnc_args(const Geometry& g, const WS& w)
+{
+    const Schedule& S = g.sch[kSchedAdj];
+    const SegCfg c = seg_cfg(g);
+    ProjArgs A = base_args(g, proj_cfg(g, MODE_GN));
+    for (int k = 0; k < 2; ++k) { A.img2[k] = w.img2[k]; A.img4[k] = w.img4[k]; }
+    A.slots = w.slots;
+    A.segp = w.segp;
+    A.slot_lo = S.d_slot_lo;
+    A.slot_hi = S.d_slot_hi;
+    A.K = S.K;
+    A.seg_rows = S.d_seg_rows;
+    A.n_groups = S.max_gB;
+    A.groups = S.d_groups;
+    A.units = S.d_unitsB;
+    A.u_begin = S.d_ub_begin;
+    A.stages = S.d_stB;
+    A.s_begin = S.d_sb_begin;
+    A.RbB = c.RbB;
+    A.passesB = c.passesB;
+    A.stage_bytes = c.stageB;
+    A.off_wacc = c.off_wacc;
+    A.off_rout = c.off_rout;
+    A.off_gsh = c.off_gsh;
+    A.off_rsc = c.off_rsc;
+    A.off_q1 = c.off_q1;
+    A.cache = w.cache;
+    A.cache_off = S.d_cache_off;
+    A.cache_rows_member = S.cache_rows_member;
+    A.ntab = S.ntab;
+    A.jp = w.jp;
+    return A;
+}
+
+// the cache from the VJP-mode phase-A partials in w.segp (of u, whose (lam, mu) bands are in w.img2)
+static pget_status gnc_build(const Geometry& g, const WS& w, cudaStream_t s)
+{
+    const SegCfg c = seg_cfg(g);
+    cudaError_t e = launch_gnc(0, g.dup, gnc_args(g, w), c.gridB, c.WB * 32, c.smemB, s);
+    note();
+    if (e != cudaSuccess) return cuda_fail(e, "lin_kernel launch");
+    return PGET_OK;
+}
+
+// q-partials of H p from the cache: p packed into w.img2, (J p) partials, scatter, slot reduction
+// hybrid (g.gn_hybrid): the (J p) of p recomputed by the GN-mode phase A from (u, p) (pack4 into
+// w.img4), the scatter from the cache; else the (J p) from the cache too (jvpc_kernel)
+static pget_status gnc_product(const Geometry& g, const WS& w, const float* lam, const float* mu, const float* pl,
+                               const float* pm, cudaStream_t s)
+{
+    pget_status st = g.gn_hybrid ? pack4(g, w, lam, mu, pl, pm, s)
+                                 : pack2(g, w, pl, pm, nullptr, nullptr, nullptr, nullptr, s, nullptr);
+    if (st) return st;
+    const SegCfg c = seg_cfg(g);
+    ProjArgs A = gnc_args(g, w);
+    if (g.gn_hybrid) A.jp = nullptr;
+    cudaEvent_t ea = nullptr, eb = nullptr;
+    if (g_prof.on.load(std::memory_order_relaxed)) {
+        std::lock_guard<std::mutex> lk(g_prof.mu);
+        g_prof.total += 2;
+        g_prof.mode_launches[MODE_GN]++;
+        if (g_prof.used + 2 <= g_prof.pool.size()) {
+            ea = g_prof.pool[g_prof.used++];
+            eb = g_prof.pool[g_prof.used++];
+            g_prof.recs.push_back({MODE_GN, ea, eb});
+        }
+    }
+    if (ea) cudaEventRecord(ea, s);
+    cudaError_t e;
+    if (g.gn_hybrid) {
+        const Schedule& S = g.sch[kSchedAdj];
+        ProjArgs Aa = A;
+        Aa.units = S.d_unitsA;
+        Aa.u_begin = S.d_ua_begin;
+        Aa.stages = S.d_stA;
+        Aa.s_begin = S.d_sa_begin;
+        Aa.RbA = c.RbA;
+        Aa.passesA = c.passesA;
+        Aa.stage_bytes = c.stageA;
+        e = launch_seg(0, MODE_GN, c.maxgA, g.dup, Aa, c.gridA, (c.WA + 1) * 32, c.smemA, s);
+    } else {
+        e = launch_gnc(1, g.dup, A, c.gridB, c.WB * 32, c.smemB, s);
+    }
+    if (e == cudaSuccess) e = launch_gnc(2, g.dup, A, c.gridB, c.WB * 32, c.smemB, s);
+    if (eb) cudaEventRecord(eb, s);
+    if (e != cudaSuccess) return cuda_fail(e, "cached GN launch");
+    const ProjCfg pc = proj_cfg(g, MODE_GN);
+    const int N = g.desc.n_px;
+    const dim3 grid((N + 31) / 32, (N + 31) / 32, g.desc.batch * pc.G);
+    reduce_slots_kernel<<<grid, dim3(32, 8), 0, s>>>(w.slots, w.gacc, N, slot_pitch(g), g.desc.batch, pc.G,
+                                                    g.sch[kSchedAdj].d_red_off, g.sch[kSchedAdj].d_red_slot,
+                                                    g.sch[kSchedAdj].d_slot_lo, g.sch[kSchedAdj].d_slot_hi); note();
+    CK(cudaGetLastError());
+    return PGET_OK;
+}
+
 pget_status pget_forward(pget_geometry h, const float* lam, const float* mu, float* y, void* ws, size_t ws_bytes,
                          pget_stream_t stream)
 {
@@ -758,8 +877,25 @@ pget_status pget_gn_apply(pget_geometry h, const float* lam, const float* mu, co
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int N = g.desc.n_px, B = g.desc.batch;
     if ((st = pack2(g, w, lam, mu, nullptr, nullptr, nullptr, nullptr, s))) return st;
-    if ((st = pack4(g, w, lam, mu, p_lam, p_mu, s))) return st;
-    if ((st = proj_adjoint(g, w, MODE_GN, nullptr, s))) return st;
+    if (g.adj_seg && g.gn_cached) {   // phase A (VJP mode) of u -> cache -> cached product
+        const SegCfg c = seg_cfg(g);
+        const Schedule& S = g.sch[kSchedAdj];
+        ProjArgs A = gnc_args(g, w);
+        A.units = S.d_unitsA;
+        A.u_begin = S.d_ua_begin;
+        A.stages = S.d_stA;
+        A.s_begin = S.d_sa_begin;
+        A.RbA = c.RbA;
+        A.passesA = c.passesA;
+        A.stage_bytes = c.stageA;
+        CK(launch_seg(0, MODE_VJP, c.maxgA, g.dup, A, c.gridA, (c.WA + 1) * 32, c.smemA, s));
+        note();
+        if ((st = gnc_build(g, w, s))) return st;
+        if ((st = gnc_product(g, w, lam, mu, p_lam, p_mu, s))) return st;
+    } else {
+        if ((st = pack4(g, w, lam, mu, p_lam, p_mu, s))) return st;
+        if ((st = proj_adjoint(g, w, MODE_GN, nullptr, s))) return st;
+    }
     finish_kernel<<<dim3(vec_grid(static_cast<size_t>(N) * N), B), kVecThreads, 0, s>>>(
         w.gacc, proj_cfg(g, MODE_GN).G, p_lam, p_mu, alpha, beta, 1.f, q_lam, q_mu, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
         nullptr, nullptr, nullptr, N); note();
@@ -798,10 +934,16 @@ static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const f
     CK(cudaGetLastError());
     scalar_kernel<<<sgrid, 128, 0, s>>>(SC_INIT, 0, P[0], P[1], P[2], kNblk, w.cg, stats, B, alpha, beta, betav); note();
     CK(cudaGetLastError());
+    const bool cached = g.adj_seg && g.gn_cached;
+    if (cached && n_cg > 0 && (st = gnc_build(g, w, s))) return st;   // the VJP above left u's partials
     // 5: CG
     for (int k = 0; k < n_cg; ++k) {
-        if ((st = pack4(g, w, lam, mu, w.pl, w.pm, s))) return st;
-        if ((st = proj_adjoint(g, w, MODE_GN, nullptr, s))) return st;
+        if (cached) {
+            if ((st = gnc_product(g, w, lam, mu, w.pl, w.pm, s))) return st;
+        } else {
+            if ((st = pack4(g, w, lam, mu, w.pl, w.pm, s))) return st;
+            if ((st = proj_adjoint(g, w, MODE_GN, nullptr, s))) return st;
+        }
         {   // finish + gamma + update1 + zeta + update2: one cooperative launch (grid-wide syncs)
             int kk = k, NN = N, BB = B, nb = kNblk, GG = Gg;
             float al = alpha, be = beta;

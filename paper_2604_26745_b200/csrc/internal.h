@@ -112,6 +112,12 @@ struct Schedule {
     int32_t *d_ua_begin = nullptr, *d_ub_begin = nullptr, *d_sa_begin = nullptr, *d_sb_begin = nullptr;
     StageD *d_stA = nullptr, *d_stB = nullptr;
     int32_t* d_seg_rows = nullptr;
+    // GN coefficient cache layout: rows of 32 lanes x float4 at cache_off[(t * K + k) * ngB + g]
+    // (+ m * cache_rows_member), t = traced angle-bank index, k = segment, g = comb group
+    int ntab = 0;
+    std::vector<int64_t> cache_off;
+    int64_t cache_rows_member = 0;
+    int64_t* d_cache_off = nullptr;
     int32_t* d_cta_begin = nullptr;
     TaskD* d_tasks = nullptr;
     int32_t* d_groups = nullptr;
@@ -162,6 +168,9 @@ struct Geometry {
     size_t smem_optin = 227 * 1024;
     Schedule sch[3];   // kSchedFwd, kSchedJvp, kSchedAdj (schedule.cpp), device copies owned here
     bool adj_seg = true;   // adjoint (VJP / GN) as the segmented two-phase projector (else the fused one)
+    double cache_max_gb = 8.0;   // larger caches fall back to the recomputing GN product
+    bool gn_hybrid = true;   // cached scatter with the recomputed (J p) (PGET_GN_CACHE=1)
+    bool gn_cached = true;   // GN product from the per-LM-iteration Jacobian-entry cache (PGET_GN_CACHE=0: recompute)
     int segA_W = 15, segA_cps = 1;
     int rbA_cap = 64;   // segmented phase A: most rows per band (64 vs 32: GN cfg2 -0.7 %, scripts/rba_exp.sh)   // segmented phase A: warps per CTA, CTAs per SM (scripts/sega_exp.sh)
 };

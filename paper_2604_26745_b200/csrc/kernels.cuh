@@ -37,6 +37,12 @@ struct ProjArgs {
     int K, n_groups, off_rsc, off_q1;
     const int32_t* slot_lo;  // [n_slots] rows [slot_lo, slot_hi) a slot's units can write (zeroed by the first)
     const int32_t* slot_hi;
+    // GN with cached Jacobian coefficients (lin_kernel / jvpc_kernel / gnb_kernel)
+    float4* cache;           // rows of 32 lanes: (alpha, beta, alpha', beta') per sample
+    const int64_t* cache_off;
+    int64_t cache_rows_member;
+    int ntab;
+    float* jp;               // [n_canon][2][R] per-ray JVP partials of a segment (both directions)
     float* segp;            // [n_canon][kSegFields][R]
 };
 
@@ -102,6 +108,9 @@ cudaError_t set_proj_smem_limit(int mode, size_t smem);
 cudaError_t launch_seg(int phase, int mode, int maxg, bool paired, const ProjArgs& A, int grid, int block,
                        size_t smem, cudaStream_t s);
 cudaError_t set_seg_smem_limit(int phase, int mode, size_t smem);
+// GN with cached coefficients: phase 0 lin_kernel, 1 jvpc_kernel, 2 gnb_kernel
+cudaError_t launch_gnc(int phase, bool paired, const ProjArgs& A, int grid, int block, size_t smem, cudaStream_t s);
+cudaError_t set_gnc_smem_limit(size_t smem);
 int proj_warps(int mode);
 int proj_ctas_per_sm(int mode);
 }  // namespace pget

@@ -442,7 +442,7 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
         a0[sP + 1] = make_float2(t11.x + c11.x, t11.y + c11.y);
 #else
         if (aoff != poff) {
-            if (poff >= 0) {
+            if (poff >= 0 && (PGET_ABLATE != 1 || p00.x == 12345.f)) {   // ABLATE 1: no scatter
                 float2* pa = acc + poff;
                 const float2 t00 = pa[0], t01 = pa[1], t10 = pa[sP], t11 = pa[sP + 1];
                 pa[0] = make_float2(t00.x + p00.x, t00.y + p00.y);
@@ -1075,12 +1075,554 @@ __global__ void __launch_bounds__(512, 1) seg_b_kernel(ProjArgs A)
                 const float2* sbuf = reinterpret_cast<const float2*>(stage0 + b * A.stage_bytes);
                 const bool flip = j & 1;
                 const int abase = flip ? Rb * P : 0, sP = flip ? -P : P;
-                walk_b<PAIRED, ModeTraits<MODE>::COMP_S>(sbuf, wacc, P, r0, r1, abase, sP, ilo, dU, dV, cf, ch, rb, ii, uu, vv, st);
+                if (PGET_ABLATE != 3)   // 3: no sweep B walk at all
+                    walk_b<PAIRED, ModeTraits<MODE>::COMP_S>(sbuf, wacc, P, r0, r1, abase, sP, ilo, dU, dV, cf, ch, rb, ii,
+                                                             uu, vv, st);
                 __syncthreads();   // stage buffer b and every warp ring consumed
                 if (tid == 0 && s + 2 < n_stages)
                     issue_seg_stage<false>(A, Rb, sb0 + s + 2, stage0 + b * A.stage_bytes, &mbar[b]);
                 ++s;
                 // flush (as proj_kernel): finished rows into the slot, column-limited, fixed thread per element
+                const bool last = j == ui.nb - 1;
+                const int carry = last ? -1 : (ui.dir > 0 ? r0 : r1);
+                int qlo, qhi;
+                {
+                    const double a0 = ucol(rfirst, r0 - 1.0), a1 = ucol(rfirst, r1 + 1.0);
+                    const double b0 = ucol(rlast, r0 - 1.0), b1 = ucol(rlast, r1 + 1.0);
+                    const double umin = fmin(fmin(a0, a1), fmin(b0, b1)), umax = fmax(fmax(a0, a1), fmax(b0, b1));
+                    qlo = max(0, static_cast<int>(floor(umin)) - 2) >> 1;
+                    qhi = min(P - 1, static_cast<int>(floor(umax)) + 3) >> 1;
+                }
+                const int e_beg = r0 * npairs, e_end = (r1 + 1) * npairs;
+                for (int e = e_beg + (tid - e_beg % NT + NT) % NT; e < e_end; e += NT) {
+                    int rw = __float2int_rd(static_cast<float>(e) * inv_np);
+                    int q = e - rw * npairs;
+                    if (q < 0) { --rw; q += npairs; } else if (q >= npairs) { ++rw; q -= npairs; }
+                    if (rw == carry || q < qlo || q > qhi || PGET_ABLATE == 2) continue;   // 2: no flush
+                    const int lr = flip ? r0 + Rb - rw : rw - r0;
+                    PGET_CHECK(lr >= 0 && lr < RB1);
+                    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+                    for (int w = 0; w < W; ++w) {
+                        float4* el = reinterpret_cast<float4*>(wacc_all + (static_cast<size_t>(w) * RB1 + lr) * P) + q;
+                        const float4 x = *el;
+                        sum.x += x.x; sum.y += x.y; sum.z += x.z; sum.w += x.w;
+                        *el = make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                    const int ir = rw - kHalo, ic = 2 * q - kHalo;
+                    if (ir >= 0 && ir < A.N && ic >= 0 && ic < A.Ns)
+                        atomicAdd(reinterpret_cast<float4*>(slot + static_cast<size_t>(ir) * A.Ns + ic), sum);
+                }
+                __syncthreads();   // rings zeroed before the next band's scatter
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------ GN, cached coefficients
+// The Jacobian of one LM iteration is fixed while CG runs, and every GN product J^T (J p) needs, per
+// line sample i of ray r, only the Jacobian entries of the sample (the adjoint weights at w_r = 1):
+//   alpha_i = dy_r / dlam_i = Delta E_i,     beta_i = dy_r / dmu_i = -Delta^2 (G - Q_i - lam_i E_i / 2)
+// and (line pairing) alpha'_i, beta'_i of the opposite-bank ray, so that
+//   (J p)_r = sum_i (dlam_i alpha_i + dmu_i beta_i),     J^T w scatters w_r (alpha_i, beta_i) bilinearly.
+// lin_kernel writes them once per LM iteration (the segmented phase-B walk with w = 1, compensated
+// sums), jvpc_kernel forms the per-ray (J p) partials of each segment from staged p and the cache,
+// gnb_kernel scatters w_r (alpha_i, beta_i) + w'_r (alpha'_i, beta'_i) -- no image, no exp -- into the
+// warp band accumulators and slots of seg_b_kernel.  Cache layout: per (member, traced angle-bank,
+// segment, comb group) kmax rows of 32 lanes (schedule.cpp); a lane's k-th sample of the unit is
+// row k of its block.
+__device__ __forceinline__ float4* cache_lane(const ProjArgs& A, const UnitInfo& ui, int grp, int lane, int* kend)
+{
+    const int t = (ui.canon / A.K) % A.ntab;
+    const int64_t idx = (static_cast<int64_t>(t) * A.K + ui.seg) * A.n_groups + grp;
+    const int64_t off = A.cache_off[idx];
+    *kend = static_cast<int>(A.cache_off[idx + 1] - off);   // rows of the block
+    const int64_t row = static_cast<int64_t>(ui.m) * A.cache_rows_member + off;
+    return A.cache + row * 32 + lane;
+}
+
+// per-ray constants of a segment for the adjoint at w = 1 (seg_b_kernel's combination, VJP part)
+template <bool PAIRED>
+__device__ __forceinline__ void seg_constants(const ProjArgs& A, const UnitInfo& ui, int r, float4* gsh, float* rsc,
+                                              float2* q1i)
+{
+    const int R = A.R, K = A.K;
+    const int qme = ui.dir > 0 ? K - 1 - ui.seg : ui.seg;
+    const float* part0 = A.segp + static_cast<size_t>(ui.canon - ui.seg) * kSegFields * R;
+    double Lb[5], gq[4], p2q[4];
+    Lb[0] = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        gq[q] = p2q[q] = 0.0;
+        double sq = 0.0;
+        if (q < K) {
+            const float* pq = part0 + static_cast<size_t>(ui.dir > 0 ? K - 1 - q : q) * kSegFields * R;
+            sq = static_cast<double>(pq[0 * R + r]) - pq[1 * R + r];
+            gq[q] = static_cast<double>(pq[2 * R + r]) - pq[3 * R + r];
+            if (PAIRED) p2q[q] = pq[7 * R + r];
+        }
+        Lb[q + 1] = Lb[q] + sq;
+    }
+    double Lme = 0.0, LK = 0.0;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+        if (q == qme) Lme = Lb[q];
+        if (q == K) LK = Lb[q];
+    }
+    double T = 0.0, Qoff = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (q >= qme && q < K) T += exp2(Lb[q] - Lme) * gq[q];
+        if (PAIRED && q < qme) Qoff += exp2(LK - Lb[q]) * p2q[q];
+    }
+    const double Sl = LK - Lme;
+    const float Th = static_cast<float>(T), Sh = static_cast<float>(Sl), Qh = static_cast<float>(Qoff);
+    gsh[r] = make_float4(Th, static_cast<float>(static_cast<double>(Th) - T), Sh,
+                         static_cast<float>(static_cast<double>(Sh) - Sl));
+    rsc[r] = static_cast<float>(exp2(Lme));
+    q1i[r] = make_float2(Qh, static_cast<float>(static_cast<double>(Qh) - Qoff));
+}
+
+// whole-ray (J p) of both directions from the GN-mode phase-A segment partials (seg_b_kernel's GN
+// combination, in ray order)
+template <bool PAIRED>
+__device__ __forceinline__ void gn_rout_from_seg(const ProjArgs& A, const UnitInfo& ui, int r, float* rout)
+{
+    const int R = A.R, K = A.K;
+    const float* part0 = A.segp + static_cast<size_t>(ui.canon - ui.seg) * kSegFields * R;
+    double Lb[5], dLb[5], gq[4], p1q[4], p2q[4], p3q[4], dgq[4];
+    Lb[0] = 0.0;
+    dLb[0] = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        gq[q] = p1q[q] = p2q[q] = p3q[q] = dgq[q] = 0.0;
+        double sq = 0.0, dsq = 0.0;
+        if (q < K) {
+            const float* pq = part0 + static_cast<size_t>(ui.dir > 0 ? K - 1 - q : q) * kSegFields * R;
+            sq = static_cast<double>(pq[0 * R + r]) - pq[1 * R + r];
+            gq[q] = static_cast<double>(pq[2 * R + r]) - pq[3 * R + r];
+            if (PAIRED) p2q[q] = pq[7 * R + r];
+            dsq = pq[4 * R + r];
+            dgq[q] = pq[5 * R + r];
+            p1q[q] = pq[6 * R + r];
+            p3q[q] = pq[8 * R + r];
+        }
+        Lb[q + 1] = Lb[q] + sq;
+        dLb[q + 1] = dLb[q] + dsq;
+    }
+    double LK = 0.0, dLK = 0.0;
+#pragma unroll
+    for (int q = 0; q < 5; ++q)
+        if (q == K) { LK = Lb[q]; dLK = dLb[q]; }
+    double dG = 0.0, P1 = 0.0, P2 = 0.0, P3 = 0.0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (q < K) {
+            dG += exp2(Lb[q]) * (dgq[q] - dLb[q] * gq[q]);
+            if (PAIRED) {
+                const double e = exp2(-Lb[q]);
+                P1 += e * p1q[q];
+                P2 += e * p2q[q];
+                P3 += e * (p3q[q] + dLb[q] * p2q[q]);
+            }
+        }
+    }
+    rout[r] = static_cast<float>(A.delta * dG);
+    rout[R + r] = PAIRED ? static_cast<float>(A.delta * exp2(LK) * (P1 + P3 - dLK * P2)) : 0.f;
+}
+
+// lin walk: the Jacobian entries of every sample of the band into the lane's cache block
+template <bool PAIRED>
+__device__ __forceinline__ void walk_lin(const float2* __restrict__ img, int P, int r0, int r1, int ilo, int64_t dU,
+                                         int64_t dV, float cf, float ch, const RayB& rb, int& i, int64_t& u,
+                                         int64_t& v, StateB& st, float4* cl, int& k)
+{
+    int iv = hi32(v), iu = hi32(u);
+    if (i < ilo || iv < r0 || iv >= r1) return;
+    int o = (iv - r0) * P + iu;
+    float2 q00 = img[o], q01 = img[o + 1], q10 = img[o + P], q11 = img[o + P + 1];
+    float fu = frac23(u), fv = frac23(v);
+    StateB x_ = st;
+    while (true) {
+        const int i2 = i - 1;
+        const int64_t u2 = u - dU, v2 = v - dV;
+        const int iv2 = hi32(v2);
+        const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;
+        float2 n00, n01, n10, n11;
+        int o2 = o;
+        if (nxt) {
+            o2 = (iv2 - r0) * P + hi32(u2);
+            n00 = img[o2]; n01 = img[o2 + 1]; n10 = img[o2 + P]; n11 = img[o2 + P + 1];
+        }
+        const float2 x = bilerp2(q00, q01, q10, q11, fu, fv);
+        const float arg_hi = fmaf(x.y, ch, x_.s);
+        const float E = ex2(arg_hi - x_.sc);
+        const float le = x.x * E;
+        float4 cv;
+        cv.x = rb.kl * E;
+        cv.y = rb.km * (((rb.G - x_.q) - (rb.Gc - x_.qc)) - 0.5f * le);
+        cv.z = 0.f;
+        cv.w = 0.f;
+        if constexpr (PAIRED) {
+            const float E1 = ex2((rb.Sl - arg_hi) - (rb.Slc - x_.sc));
+            const float le1 = x.x * E1;
+            cv.z = rb.kl1 * E1;
+            cv.w = rb.km1 * ((x_.q1 - x_.q1c) + 0.5f * le1);
+            kahan(x_.q1, x_.q1c, le1);
+        }
+        kahan(x_.q, x_.qc, le);
+        kahan(x_.s, x_.sc, x.y * cf);
+        __stcs(cl + static_cast<int64_t>(k) * 32, cv);   // streaming store: written once, read 2 x n_cg times
+        ++k;
+        i = i2;
+        u = u2;
+        v = v2;
+        if (!nxt) break;
+        q00 = n00; q01 = n01; q10 = n10; q11 = n11;
+        o = o2;
+        fu = frac23(u);
+        fv = frac23(v);
+    }
+    st = x_;
+}
+
+// Cached entries are streamed from HBM: a 4-slot register ring (the entry of sample k+4 is loaded
+// into the slot just consumed) plus an L2 prefetch 16 samples ahead keep several loads in flight per
+// lane; kend bounds the reads to the lane's cache block.
+__device__ __forceinline__ float4 ld_entry(const float4* __restrict__ cl, int k, int kend)
+{
+    return k < kend ? __ldg(cl + static_cast<int64_t>(k) * 32) : make_float4(0.f, 0.f, 0.f, 0.f);
+}
+__device__ __forceinline__ void pf_entry(const float4* cl, int k, int kend)
+{
+    if (k < kend) asm volatile("prefetch.global.L2 [%0];" ::"l"(cl + static_cast<int64_t>(k) * 32));
+}
+
+// jvpc walk: (J p) partial sums of the band from staged p = (dlam, dmu) and the cached entries
+__device__ __forceinline__ void walk_jvpc(const float2* __restrict__ img, int P, int r0, int r1, int ilo, int64_t dU,
+                                          int64_t dV, int& i, int64_t& u, int64_t& v, const float4* __restrict__ cl,
+                                          int& k, int kend, float& acc, float& acc1)
+{
+    const int iv0 = hi32(v);
+    if (i < ilo || iv0 < r0 || iv0 >= r1) return;
+    float4 c0 = ld_entry(cl, k, kend), c1 = ld_entry(cl, k + 1, kend), c2 = ld_entry(cl, k + 2, kend),
+           c3 = ld_entry(cl, k + 3, kend);
+    int o = (iv0 - r0) * P + hi32(u);
+    float2 q00 = img[o], q01 = img[o + 1], q10 = img[o + P], q11 = img[o + P + 1];
+    float fu = frac23(u), fv = frac23(v);
+    auto step = [&](float4& c) -> bool {
+        const int i2 = i - 1;
+        const int64_t u2 = u - dU, v2 = v - dV;
+        const int iv2 = hi32(v2);
+        const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;
+        float2 n00 = q00, n01 = q01, n10 = q10, n11 = q11;
+        int o2 = o;
+        if (nxt) {
+            o2 = (iv2 - r0) * P + hi32(u2);
+            n00 = img[o2]; n01 = img[o2 + 1]; n10 = img[o2 + P]; n11 = img[o2 + P + 1];
+        }
+        const float2 d = bilerp2(q00, q01, q10, q11, fu, fv);
+        acc = fmaf(d.x, c.x, fmaf(d.y, c.y, acc));
+        acc1 = fmaf(d.x, c.z, fmaf(d.y, c.w, acc1));
+        pf_entry(cl, k + 16, kend);
+        c = ld_entry(cl, k + 4, kend);
+        ++k;
+        i = i2;
+        u = u2;
+        v = v2;
+        q00 = n00; q01 = n01; q10 = n10; q11 = n11;
+        o = o2;
+        fu = frac23(u);
+        fv = frac23(v);
+        return nxt;
+    };
+    while (step(c0) && step(c1) && step(c2) && step(c3)) {
+    }
+}
+
+// gnb walk: scatter w_r (alpha, beta) + w'_r (alpha', beta') of the band's samples (same-cell registers)
+__device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0, int r1, int abase, int sP, int ilo,
+                                         int64_t dU, int64_t dV, float wr, float wr1, int& i, int64_t& u, int64_t& v,
+                                         const float4* __restrict__ cl, int& k, int kend)
+{
+    const int iv0 = hi32(v);
+    if (i < ilo || iv0 < r0 || iv0 >= r1) return;
+    int poff = -1;
+    float2 p00 = make_float2(0.f, 0.f), p01 = p00, p10 = p00, p11 = p00;
+    auto rmw = [&](int off, float2 a, float2 b, float2 c, float2 d) {
+        float2* pa = acc + off;
+        const float2 t00 = pa[0], t01 = pa[1], t10 = pa[sP], t11 = pa[sP + 1];
+        pa[0] = make_float2(t00.x + a.x, t00.y + a.y);
+        pa[1] = make_float2(t01.x + b.x, t01.y + b.y);
+        pa[sP] = make_float2(t10.x + c.x, t10.y + c.y);
+        pa[sP + 1] = make_float2(t11.x + d.x, t11.y + d.y);
+    };
+    float4 c0 = ld_entry(cl, k, kend), c1 = ld_entry(cl, k + 1, kend), c2 = ld_entry(cl, k + 2, kend),
+           c3 = ld_entry(cl, k + 3, kend);
+    int iv = iv0;
+    auto step = [&](float4& c) -> bool {
+        const int aoff = abase + (iv - r0) * sP + hi32(u);
+        const float fu = frac23(u), fv = frac23(v);
+        const int i2 = i - 1;
+        const int64_t u2 = u - dU, v2 = v - dV;
+        const int iv2 = hi32(v2);
+        const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;
+        const float2 av = make_float2(fmaf(wr, c.x, wr1 * c.z), fmaf(wr, c.y, wr1 * c.w));
+        pf_entry(cl, k + 16, kend);
+        c = ld_entry(cl, k + 4, kend);
+        const float2 tv = __fmul2_rn(av, make_float2(fv, fv));         // row j0+1
+        const float2 bv = __ffma2_rn(tv, make_float2(-1.f, -1.f), av); // row j0
+        const float2 c11 = __fmul2_rn(tv, make_float2(fu, fu));
+        const float2 c10 = __ffma2_rn(c11, make_float2(-1.f, -1.f), tv);
+        const float2 c01 = __fmul2_rn(bv, make_float2(fu, fu));
+        const float2 c00 = __ffma2_rn(c01, make_float2(-1.f, -1.f), bv);
+        if (aoff != poff) {
+            if (poff >= 0) rmw(poff, p00, p01, p10, p11);
+            poff = aoff;
+            p00 = c00; p01 = c01; p10 = c10; p11 = c11;
+        } else {
+            p00.x += c00.x; p00.y += c00.y;
+            p01.x += c01.x; p01.y += c01.y;
+            p10.x += c10.x; p10.y += c10.y;
+            p11.x += c11.x; p11.y += c11.y;
+        }
+        ++k;
+        i = i2;
+        u = u2;
+        v = v2;
+        iv = iv2;
+        return nxt;
+    };
+    while (step(c0) && step(c1) && step(c2) && step(c3)) {
+    }
+    rmw(poff, p00, p01, p10, p11);
+}
+
+// per-unit lane setup shared by the three kernels: the lane's ray of comb group grp, its entry
+// sample into the unit's segment and position; false if the lane has no ray
+__device__ __forceinline__ bool lane_ray(const ProjArgs& A, const UnitInfo& ui, const RayP* rays, int grp, int lane,
+                                         int64_t dU, int64_t dV, int& r, int& ii, int& ilo, int64_t& uu, int64_t& vv)
+{
+    r = grp < A.n_groups ? A.groups[grp * 32 + lane] : -1;
+    ii = -1; ilo = 0; uu = 0; vv = 0;
+    if (r < 0) return false;
+    const RayP rp = rays[r];
+    ii = seg_entry(rp, ui.dir > 0 ? ui.yhi : ui.ylo);
+    ilo = rp.ilo;
+    uu = rp.U0 + static_cast<int64_t>(ii) * dU;
+    vv = rp.V0 + static_cast<int64_t>(ii) * dV;
+    return true;
+}
+
+// lin_kernel: once per LM iteration.  Stages (lam, mu) bands like seg_b_kernel (same units, groups,
+// stage list); needs the segment partials of the VJP-mode phase A.
+template <bool PAIRED>
+__global__ void __launch_bounds__(512, 1) lin_kernel(ProjArgs A)
+{
+    const int W = blockDim.x >> 5;
+    const int NT = blockDim.x;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
+    unsigned char* const stage0 = smem + 128;
+    float4* gsh = reinterpret_cast<float4*>(smem + A.off_gsh);
+    float* rsc = reinterpret_cast<float*>(smem + A.off_rsc);
+    float2* q1i = reinterpret_cast<float2*>(smem + A.off_q1);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c = blockIdx.x;
+    const int64_t sb0 = A.s_begin[c];
+    const int64_t n_stages = A.s_begin[c + 1] - sb0;
+    if (n_stages == 0) return;
+    const int P = A.P, R = A.R, Rb = A.RbB;
+    if (tid == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        issue_seg_stage<false>(A, Rb, sb0, stage0, &mbar[0]);
+        if (n_stages > 1) issue_seg_stage<false>(A, Rb, sb0 + 1, stage0 + A.stage_bytes, &mbar[1]);
+    }
+    int64_t s = 0;
+    const float cf = A.cf, ch = A.ch;
+    for (int u = A.u_begin[c]; u < A.u_begin[c + 1]; ++u) {
+        const UnitInfo ui = unit_info(A, u, Rb);
+        const RayP* rays = A.rays + static_cast<size_t>(ui.ab) * R;
+        const int64_t dU = rays[0].dU, dV = rays[0].dV;
+        for (int r = tid; r < R; r += NT) seg_constants<PAIRED>(A, ui, r, gsh, rsc, q1i);
+        __syncthreads();
+        for (int pass = 0; pass < A.passesB; ++pass) {
+            const int grp = pass * W + warp;
+            int r, ii, ilo, k = 0;
+            int64_t uu, vv;
+            RayB rb{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            StateB st{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            float4* cl = nullptr;
+            if (lane_ray(A, ui, rays, grp, lane, dU, dV, r, ii, ilo, uu, vv)) {
+                const float sc = rsc[r];
+                const float4 G = gsh[r];
+                const float2 q1 = q1i[r];
+                rb = RayB{A.delta * sc, -A.delta * A.delta * sc, G.x, G.y, A.delta, -A.delta * A.delta, G.z, G.w};
+                st.q1 = q1.x;
+                st.q1c = q1.y;
+                int kend_unused;
+                cl = cache_lane(A, ui, grp, lane, &kend_unused);
+            }
+            for (int j = 0; j < ui.nb; ++j) {
+                int r0, r1;
+                seg_band(ui, j, Rb, r0, r1);
+                const int b = static_cast<int>(s & 1);
+                mbar_wait(&mbar[b], static_cast<uint32_t>((s >> 1) & 1));
+                const float2* sbuf = reinterpret_cast<const float2*>(stage0 + b * A.stage_bytes);
+                walk_lin<PAIRED>(sbuf, P, r0, r1, ilo, dU, dV, cf, ch, rb, ii, uu, vv, st, cl, k);
+                __syncthreads();   // stage buffer b consumed
+                if (tid == 0 && s + 2 < n_stages)
+                    issue_seg_stage<false>(A, Rb, sb0 + s + 2, stage0 + b * A.stage_bytes, &mbar[b]);
+                ++s;
+            }
+        }
+        __syncthreads();   // gsh / rsc / q1i are rewritten by the next unit
+    }
+}
+
+// jvpc_kernel: per CG step, the per-ray (J p) partials of every unit from staged p (float2 bands of
+// (dlam, dmu), the same stage list) and the cache.
+__global__ void __launch_bounds__(512, 1) jvpc_kernel(ProjArgs A)
+{
+    const int W = blockDim.x >> 5;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
+    unsigned char* const stage0 = smem + 128;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c = blockIdx.x;
+    const int64_t sb0 = A.s_begin[c];
+    const int64_t n_stages = A.s_begin[c + 1] - sb0;
+    if (n_stages == 0) return;
+    const int P = A.P, R = A.R, Rb = A.RbB;
+    if (tid == 0) {
+        mbar_init(&mbar[0], 1);
+        mbar_init(&mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        issue_seg_stage<false>(A, Rb, sb0, stage0, &mbar[0]);
+        if (n_stages > 1) issue_seg_stage<false>(A, Rb, sb0 + 1, stage0 + A.stage_bytes, &mbar[1]);
+    }
+    int64_t s = 0;
+    for (int u = A.u_begin[c]; u < A.u_begin[c + 1]; ++u) {
+        const UnitInfo ui = unit_info(A, u, Rb);
+        const RayP* rays = A.rays + static_cast<size_t>(ui.ab) * R;
+        const int64_t dU = rays[0].dU, dV = rays[0].dV;
+        float* jp = A.jp + static_cast<size_t>(ui.canon) * 2 * R;
+        for (int pass = 0; pass < A.passesB; ++pass) {
+            const int grp = pass * W + warp;
+            int r, ii, ilo, k = 0, kend = 0;
+            int64_t uu, vv;
+            float acc = 0.f, acc1 = 0.f;
+            const float4* cl = nullptr;
+            if (lane_ray(A, ui, rays, grp, lane, dU, dV, r, ii, ilo, uu, vv)) cl = cache_lane(A, ui, grp, lane, &kend);
+            for (int j = 0; j < ui.nb; ++j) {
+                int r0, r1;
+                seg_band(ui, j, Rb, r0, r1);
+                const int b = static_cast<int>(s & 1);
+                mbar_wait(&mbar[b], static_cast<uint32_t>((s >> 1) & 1));
+                const float2* sbuf = reinterpret_cast<const float2*>(stage0 + b * A.stage_bytes);
+                walk_jvpc(sbuf, P, r0, r1, ilo, dU, dV, ii, uu, vv, cl, k, kend, acc, acc1);
+                __syncthreads();   // stage buffer b consumed
+                if (tid == 0 && s + 2 < n_stages)
+                    issue_seg_stage<false>(A, Rb, sb0 + s + 2, stage0 + b * A.stage_bytes, &mbar[b]);
+                ++s;
+            }
+            if (r >= 0) {
+                jp[r] = acc;
+                jp[R + r] = acc1;
+            }
+        }
+    }
+}
+
+// gnb_kernel: per CG step, w_r from the (J p) partials, then the cached scatter into slots (as
+// seg_b_kernel; no image staging).
+template <bool PAIRED>
+__global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
+{
+    const int W = blockDim.x >> 5;
+    const int NT = blockDim.x;
+    extern __shared__ __align__(128) unsigned char smem[];
+    float2* wacc_all = reinterpret_cast<float2*>(smem + A.off_wacc);
+    float* rout = reinterpret_cast<float*>(smem + A.off_rout);   // [2R] whole-ray (J p), both directions
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int c = blockIdx.x;
+    if (A.u_begin[c] == A.u_begin[c + 1]) return;
+    const int P = A.P, R = A.R, J = A.J, K = A.K, Rb = A.RbB;
+    const int RB1 = Rb + 1;
+    float2* wacc = wacc_all + static_cast<size_t>(warp) * RB1 * P;
+    {
+        float4* z = reinterpret_cast<float4*>(wacc_all);
+        const int n4 = W * RB1 * P / 2;
+        for (int k = tid; k < n4; k += NT) z[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const int npairs = P >> 1;
+    const float inv_np = 1.0f / static_cast<float>(npairs);
+    const size_t plane = static_cast<size_t>(A.N) * A.Ns;
+    for (int u = A.u_begin[c]; u < A.u_begin[c + 1]; ++u) {
+        const UnitInfo ui = unit_info(A, u, Rb);
+        const RayP* rays = A.rays + static_cast<size_t>(ui.ab) * R;
+        const int64_t dU = rays[0].dU, dV = rays[0].dV;
+        const float* jp0 = A.jp ? A.jp + static_cast<size_t>(ui.canon - ui.seg) * 2 * R : nullptr;
+        for (int r = tid; r < R; r += NT) {   // whole-ray (J p)
+            if (A.jp) {   // the K cached-entry partials of jvpc_kernel, in fixed order
+                float a = 0.f, a1 = 0.f;
+                for (int q = 0; q < K; ++q) {
+                    a += jp0[static_cast<size_t>(q) * 2 * R + r];
+                    a1 += jp0[static_cast<size_t>(q) * 2 * R + R + r];
+                }
+                rout[r] = a;
+                rout[R + r] = a1;
+            } else {      // the GN-mode phase-A partials (recomputed JVP of p)
+                gn_rout_from_seg<PAIRED>(A, ui, r, rout);
+            }
+        }
+        float2* slot = A.slots + static_cast<size_t>(ui.slot) * plane;
+        if (ui.first) {
+            float4* z = reinterpret_cast<float4*>(slot);
+            const size_t z0 = static_cast<size_t>(A.slot_lo[ui.slot]) * A.Ns / 2;
+            const size_t z1 = static_cast<size_t>(A.slot_hi[ui.slot]) * A.Ns / 2;
+            for (size_t k = z0 + tid; k < z1; k += NT) z[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        __syncthreads();
+        const RayP rfirst = rays[0], rlast = rays[R - 1];
+        const double kuv = static_cast<double>(dU) / static_cast<double>(dV);
+        auto ucol = [&](const RayP& rp, double vrow) {
+            return (static_cast<double>(rp.U0) + (vrow * 4294967296.0 - static_cast<double>(rp.V0)) * kuv) *
+                   (1.0 / 4294967296.0);
+        };
+        for (int pass = 0; pass < A.passesB; ++pass) {
+            const int grp = pass * W + warp;
+            int r, ii, ilo, k = 0, kend = 0;
+            int64_t uu, vv;
+            float wr = 0.f, wr1 = 0.f;
+            const float4* cl = nullptr;
+            if (lane_ray(A, ui, rays, grp, lane, dU, dV, r, ii, ilo, uu, vv)) {
+                const int d = r / J, j = r - d * J;
+                float wd = 0.f, wd1 = 0.f;
+                for (int jj = 0; jj < J; ++jj) {
+                    wd = fmaf(A.w[jj], rout[d * J + jj], wd);
+                    wd1 = fmaf(A.w[jj], rout[R + d * J + jj], wd1);
+                }
+                if (A.dup_half) { wd *= 2.f; wd1 *= 2.f; }
+                wr = A.w[j] * wd;
+                wr1 = A.w[j] * wd1;
+                cl = cache_lane(A, ui, grp, lane, &kend);
+            }
+            for (int j = 0; j < ui.nb; ++j) {
+                int r0, r1;
+                seg_band(ui, j, Rb, r0, r1);
+                const bool flip = j & 1;
+                const int abase = flip ? Rb * P : 0, sP = flip ? -P : P;
+                walk_gnb(wacc, P, r0, r1, abase, sP, ilo, dU, dV, wr, wr1, ii, uu, vv, cl, k, kend);
+                __syncthreads();   // every warp ring complete
                 const bool last = j == ui.nb - 1;
                 const int carry = last ? -1 : (ui.dir > 0 ? r0 : r1);
                 int qlo, qhi;
@@ -1115,6 +1657,32 @@ __global__ void __launch_bounds__(512, 1) seg_b_kernel(ProjArgs A)
             }
         }
     }
+}
+
+cudaError_t launch_gnc(int phase, bool paired, const ProjArgs& A, int grid, int block, size_t smem, cudaStream_t s)
+{
+    if (phase == 0) {
+        if (paired) lin_kernel<true><<<grid, block, smem, s>>>(A);
+        else lin_kernel<false><<<grid, block, smem, s>>>(A);
+    } else if (phase == 1) {
+        jvpc_kernel<<<grid, block, smem, s>>>(A);
+    } else {
+        if (paired) gnb_kernel<true><<<grid, block, smem, s>>>(A);
+        else gnb_kernel<false><<<grid, block, smem, s>>>(A);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t set_gnc_smem_limit(size_t smem)
+{
+    const int v = static_cast<int>(smem);
+    const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(lin_kernel<true>, a, v))) return e;
+    if ((e = cudaFuncSetAttribute(lin_kernel<false>, a, v))) return e;
+    if ((e = cudaFuncSetAttribute(jvpc_kernel, a, v))) return e;
+    if ((e = cudaFuncSetAttribute(gnb_kernel<true>, a, v))) return e;
+    return cudaFuncSetAttribute(gnb_kernel<false>, a, v);
 }
 
 // ------------------------------------------------------------------------------------------ reduction

@@ -386,6 +386,31 @@ void build_adj_schedule(const Geometry& g, const std::vector<RayP>& rays, int CA
     S->groups = grp;
     S->max_gA = ngA;
     S->max_gB = ngB;
+    // Jacobian-coefficient cache of the GN product: per
+    // (traced angle-bank t, segment k, comb group gi) a block of kmax rows of 32 lanes, kmax = the
+    // most samples any lane of the group has in the segment; per member the same layout.
+    S->cache_off.assign(static_cast<size_t>(ntab) * K * ngB + 1, 0);
+    {
+        int64_t off = 0;
+        for (int t = 0; t < ntab; ++t)
+            for (int k = 0; k < K; ++k)
+                for (int gi = 0; gi < ngB; ++gi) {
+                    S->cache_off[(static_cast<size_t>(t) * K + k) * ngB + gi] = off;
+                    int kmax = 0;
+                    for (int l = 0; l < 32; ++l) {
+                        const int r = grp[static_cast<size_t>(gi) * 32 + l];
+                        if (r < 0) continue;
+                        const RayP& rp = rays[static_cast<size_t>(list[t]) * R + r];
+                        const int n = rp.dV > 0 ? seg_entry(rp, S->seg_rows[k + 1]) - seg_entry(rp, S->seg_rows[k])
+                                                : seg_entry(rp, S->seg_rows[k]) - seg_entry(rp, S->seg_rows[k + 1]);
+                        kmax = std::max(kmax, n);
+                    }
+                    off += kmax;
+                }
+        S->cache_off[static_cast<size_t>(ntab) * K * ngB] = off;
+        S->cache_rows_member = off;
+    }
+    S->ntab = ntab;
     S->tasks.clear();
     S->cta_begin.assign(C + 1, 0);
     // slots of phase B (as build_schedule's adjoint kind, per unit)
