@@ -186,7 +186,7 @@ def roofline_ncu(cid, dom):
     try:
         d = json.load(open(p))
         sol = d.get(f"cfg{cid}", {})
-        parts = {k: v for k, v in sol.items() if k == dom or k.startswith(dom + " ")}
+        parts = {k: v for k, v in sol.items() if (k == dom or k.startswith(dom + " ")) and "#" not in k}
         if not parts:
             return None
         out = {"source": d.get("source"), "kernels": parts}
@@ -395,7 +395,8 @@ def main():
                 "projector_ms_per_launch": {k: (prof["ms"][k] / prof["launches"][k] if prof["launches"][k] else None)
                                             for k in prof["ms"]},
             },
-            "roofline": {"bound": "alu", "pipe": "shared-memory crossbar (128 B/clk/SM)", "kernel": (f"{dom}: seg_a_kernel + seg_b_kernel (segmented adjoint, one launch pair)" if dom in ("gn", "vjp") else f"proj_kernel<{dom}>"),
+            "roofline": {"bound": "alu", "pipe": "shared-memory crossbar (128 B/clk/SM)", "kernel": ({"gn": "gn: seg_a_kernel<GN> + gnb_kernel (recomputed J p, cached scatter; one launch pair per CG step)",
+                                    "vjp": "vjp: seg_a_kernel + seg_b_kernel (segmented adjoint, one launch pair)"}.get(dom, f"proj_kernel<{dom}>")),
                          "achieved": achieved_gbs, "peak": peak_gbs, "unit": "GB/s", "frac": achieved_gbs / peak_gbs,
                          "traffic": traffic,
                          "peak_basis": f"128 B/clk/SM x 148 SMs x {sm_mhz:.0f} MHz (median SM clock under load)",

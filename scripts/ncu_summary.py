@@ -63,8 +63,15 @@ def full(rep):
             mode = MODES.get(name.split("<")[1].split(",")[0].strip(), "?")
         elif "seg_a_kernel<" in name or "seg_b_kernel<" in name:   # segmented adjoint: phase A / B
             mode = MODES.get(name.split("<")[1].split(",")[0].strip(), "?") + (" A" if "seg_a" in name else " B")
+        elif "gnb_kernel" in name:       # GN scatter from the coefficient cache (phase B of the GN product)
+            mode = "gn B"
+        elif "lin_kernel" in name:       # the cache build, once per LM iteration
+            mode = "lin"
         else:
             mode = name
+        seen = [m for m, _, _ in res]
+        if mode in seen:                 # e.g. the VJP-mode phase A that precedes the cache build
+            mode = mode + " #%d" % (seen.count(mode) + 1 + sum(1 for x in seen if x.startswith(mode + " #")))
         vals = {}
         for k, lab in KEYS:
             if k in hdr:
@@ -82,9 +89,9 @@ def main():
              "serialised launches: compare shares, not absolute times).", ""]
     tab, n, T = launches(lst)
     lines += [f"{n} launches, {T / 1e3:.2f} ms total.", ""] + tab + [""]
-    lines += ["Full capture: `ncu --set full --clock-control none --import-source on -k regex:\"proj_kernel|seg_\" -c 6 "
+    lines += ["Full capture: `ncu --set full --clock-control none --import-source on -k regex:\"proj_kernel|seg_|lin_kernel|gnb_kernel\" -c 8 "
               "python scripts/prof_ops.py 2 1` (one launch of each projector kernel, config 2: forward and JVP "
-              "fused, VJP and GN as segmented phases A and B).", ""]
+              "fused, VJP as segmented phases A and B, GN as the VJP-mode phase A + cache build (lin) + GN-mode phase A + cached scatter (gnb)).", ""]
     res = full(rep)
     labs = [lab for _, lab in KEYS]
     lines.append("| metric | " + " | ".join(m for m, _, _ in res) + " |")
@@ -102,6 +109,8 @@ def main():
         rb, wb = v.get("dram read"), v.get("dram write")
         if rb and wb:
             mult = {"byte": 1, "B": 1, "Kbyte": 1e3, "KB": 1e3, "Mbyte": 1e6, "MB": 1e6, "Gbyte": 1e9, "GB": 1e9}
+            if "#" in mode or mode == "lin":   # not part of one launch of a mode
+                continue
             key = mode.split(" ")[0]   # the two phases of a segmented mode add up to one launch of that mode
             traffic[key] = traffic.get(key, 0.0) + float(rb[0].replace(",", "")) * mult[rb[1]] + \
                 float(wb[0].replace(",", "")) * mult[wb[1]]

@@ -9,6 +9,6 @@ timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --l
     python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/ncu_launches_$tag.log 2>&1
 echo "ncu launches rc=$?"
 timeout 300 python scripts/prof_ops.py 2 1 > gpurun_out/prof_plain.log 2>&1 && \
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"proj_kernel|seg_" -c 6 \
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"proj_kernel|seg_|lin_kernel|gnb_kernel" -c 8 \
     -o gpurun_out/full_$tag python scripts/prof_ops.py 2 1 > gpurun_out/ncu_full_$tag.log 2>&1
 echo "ncu full rc=$?"
