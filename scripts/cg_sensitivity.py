@@ -8,10 +8,22 @@ run: profiles/cg_sensitivity_r01.txt.
 """
 import sys, time; sys.path.insert(0,'.')
 import numpy as np, oracle as O, pget_data as P
-cid=2; cfg=P.CONFIGS[cid]; gd=P.geometry_desc(cid)
-lt,mt=P.make_phantom(cid)
-y=P.poisson_noise(O.forward(gd,lt,mt),cfg.noise_peak,cfg.seed)
-l0,m0=P.initial_guess(gd['n_px'])
+# usage: cg_sensitivity.py [cfg2 | cfg5:<member>] [eps ...]; cfg5:<m> is the problem of
+# tests/test_gpu_parity.py::test_lm_iteration_config5_batched for batch member m
+case = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
+EPS = [float(x) for x in sys.argv[2:]] or [1e-7]
+if case == "cfg2":
+    cid=2; cfg=P.CONFIGS[cid]; gd=P.geometry_desc(cid)
+    lt,mt=P.make_phantom(cid)
+    y=P.poisson_noise(O.forward(gd,lt,mt),cfg.noise_peak,cfg.seed)
+    l0,m0=P.initial_guess(gd['n_px'])
+else:
+    cid=5; cfg=P.CONFIGS[cid]; m=int(case.split(":")[1]); k=m%4
+    gd=dict(P.geometry_desc(cid), batch=1)
+    LT,MT=P.make_phantom(cid)
+    lt,mt=LT[k:k+1],MT[k:k+1]
+    y=P.poisson_noise(O.forward(gd,lt,mt),1e4,50+k)
+    l0,m0=P.initial_guess(gd['n_px'])
 t=time.time()
 sl,sm,S=O.gn_cg_step(gd,l0,m0,y,cfg.alpha,0.0,cfg.n_cg)
 print('oracle step',time.time()-t,'s; cg_res',S['cg_res'][[0,1,5,10,15,20]], 'pred',S['pred'],'rho',S['rho'])
@@ -34,8 +46,6 @@ def cg(eps,seed):
         g=p@q; a=zeta/g; s+=a*p; z-=a*q; z2=z@z; p=z+(z2/zeta)*p; zeta=z2
     return s
 s0=cg(0,0); print('numpy CG vs oracle', np.linalg.norm(s0-s_ref)/np.linalg.norm(s_ref))
-for eps in [1e-7,1e-6]:
-    s1=cg(eps,1); print('eps',eps,'rel diff', np.linalg.norm(s1-s_ref)/np.linalg.norm(s_ref))
 def pred_of(s):
     sl_,sm_=s[:n].reshape(l0.shape),s[n:].reshape(l0.shape)
     dy=O.jvp(gd,l0,m0,sl_,sm_)
@@ -47,6 +57,7 @@ def f_of(s):
     return 0.5*np.sum(r**2)+0.5*cfg.alpha*(np.sum(O.laplacian(ul)**2)+np.sum(O.laplacian(um)**2))
 pr=pred_of(s_ref); fr=f_of(s_ref)
 print('ref pred',pr,'f1',fr,'oracle',S['pred'],S['f_trial'])
-for seed in [1,2]:
-    s1=cg(1e-7,seed)
-    print('seed',seed,'s diff',np.linalg.norm(s1-s_ref)/np.linalg.norm(s_ref),'pred rel',abs(pred_of(s1)-pr)/abs(pr),'f1 rel',abs(f_of(s1)-fr)/abs(fr))
+for eps in EPS:
+    for seed in [1,2,3]:
+        s1=cg(eps,seed)
+        print(case,'eps',eps,'seed',seed,'s diff',np.linalg.norm(s1-s_ref)/np.linalg.norm(s_ref),'pred rel',abs(pred_of(s1)-pr)/abs(pr),'f1 rel',abs(f_of(s1)-fr)/abs(fr), flush=True)
