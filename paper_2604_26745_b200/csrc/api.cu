@@ -385,7 +385,7 @@ WS carve(const Geometry& g, int op, char* base)
         float** vecs[] = {&w.bl, &w.bm, &w.zl, &w.zm, &w.pl, &w.pm, &w.ql, &w.qm, &w.ul, &w.um};
         for (float** v : vecs) *v = reinterpret_cast<float*>(take(n2 * sizeof(float)));
         w.part = reinterpret_cast<double*>(take(8 * B * kNblk * sizeof(double)));
-        w.cg = reinterpret_cast<CGState*>(take(B * sizeof(CGState)));
+        w.cg = reinterpret_cast<CGState*>(take(2 * B * sizeof(CGState)));   // double-buffered (cg_fused_kernel)
         if (op == PGET_OP_LM_SOLVE) {   // the step, per-member beta
             w.sl = reinterpret_cast<float*>(take(n2 * sizeof(float)));
             w.sm = reinterpret_cast<float*>(take(n2 * sizeof(float)));

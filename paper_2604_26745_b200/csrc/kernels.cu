@@ -482,6 +482,11 @@ __global__ void cg_fused_kernel(const double2* __restrict__ part, int G, float a
     const size_t n2 = static_cast<size_t>(N) * N;
     const int units = B * nblk;
     const size_t stride = static_cast<size_t>(nblk) * blockDim.x;
+    // CG state double-buffered by step parity: this launch reads st_in and writes st_out only, so no
+    // block can see a member's state change while another block of that member still reads it
+    CGState* st_in = st + static_cast<size_t>(k & 1) * B;
+    CGState* st_out = st + static_cast<size_t>((k + 1) & 1) * B;
+    st = st_in;
     // phase 1: q = H p, <p, q> partials
     for (int mj = blockIdx.x; mj < units; mj += gridDim.x) {
         const int m = mj / nblk, j = mj - m * nblk;
@@ -564,9 +569,9 @@ __global__ void cg_fused_kernel(const double2* __restrict__ part, int G, float a
                 pm[q] = fmaf(bc, pm[q], zm[q]);
             }
         }
-        __syncthreads();   // every thread of the block read st[m] before it changes
+        if (j == 0 && threadIdx.x == 0) st_out[m] = c;   // carried over (stopped members keep theirs)
         if (j == 0 && threadIdx.x == 0 && !c.stop) {
-            CGState& w = st[m];
+            CGState& w = st_out[m];
             pget_gn_stats& S = stats[m];
             if (k == 0) S.beta_min = 1e-3 * gam / c.zeta;
             if (!(gam > 0.0)) {
