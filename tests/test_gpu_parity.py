@@ -320,7 +320,10 @@ def test_lm_iteration_config5_batched(pg):
         assert S[m]["accepted"] == So["accepted"]
         s = np.concatenate([host(sl)[m].ravel(), host(sm)[m].ravel()])
         assert rel_l2(s, np.concatenate([sl_o.ravel(), sm_o.ravel()])) <= 0.1
-    # the same problem at other batch positions gives the same statistics (to fp32 reduction order)
-    for m in range(4, B, 4):
-        assert abs(S[m]["f"] - S[0]["f"]) <= 1e-6 * S[0]["f"]
-        assert abs(S[m]["pred"] - S[0]["pred"]) <= 1e-3 * abs(S[0]["pred"])
+    # the same problem at other batch positions gives the same statistics up to the slot partition of
+    # the fp32 gradient sums (measured spread of pred 1e-5; a race in the batched CG state once made
+    # it 9 %)
+    for k in range(4):
+        for m in range(k + 4, B, 4):
+            assert abs(S[m]["f"] - S[k]["f"]) <= 1e-6 * S[k]["f"]
+            assert abs(S[m]["pred"] - S[k]["pred"]) <= 1e-4 * abs(S[k]["pred"]), (k, m)
