@@ -272,7 +272,7 @@ pget_status run_proj(const Geometry& g, int mode, const ProjCfg& c, const ProjAr
 }
 
 // the segmented adjoint: phase A then phase B on s, bracketed together by the profiler's events
-pget_status run_seg(const Geometry& g, int mode, ProjArgs A, float* segp, cudaStream_t s)
+pget_status run_seg(const Geometry& g, int mode, ProjArgs A, float* segp, cudaStream_t s, float4* cache = nullptr)
 {
     const Schedule& S = g.sch[kSchedAdj];
     const SegCfg c = seg_cfg(g);
@@ -288,6 +288,10 @@ pget_status run_seg(const Geometry& g, int mode, ProjArgs A, float* segp, cudaSt
         }
     }
     A.segp = segp;
+    A.cache = cache;   // VJP: also write the GN Jacobian-entry cache (fused lin_kernel)
+    A.cache_off = S.d_cache_off;
+    A.cache_rows_member = S.cache_rows_member;
+    A.ntab = S.ntab;
     A.slot_lo = S.d_slot_lo;
     A.slot_hi = S.d_slot_hi;
     A.K = S.K;
@@ -701,14 +705,16 @@ static pget_status proj_out(const Geometry& g, const WS& w, int mode, float* y, 
 }
 
 // adjoint projector into w.gacc (MODE_VJP with weights win, or MODE_GN), then the fixed-order reduction
-static pget_status proj_adjoint(const Geometry& g, const WS& w, int mode, const float* win, cudaStream_t s)
+static pget_status proj_adjoint(const Geometry& g, const WS& w, int mode, const float* win, cudaStream_t s,
+                                bool build_cache = false)
 {
     const ProjCfg c = proj_cfg(g, mode);
     ProjArgs A = base_args(g, c);
     for (int k = 0; k < 2; ++k) { A.img2[k] = w.img2[k]; A.img4[k] = w.img4[k]; }
     A.slots = w.slots;
     A.win = win;
-    pget_status st = g.adj_seg ? run_seg(g, mode, A, w.segp, s) : run_proj(g, mode, c, A, s);
+    pget_status st = g.adj_seg ? run_seg(g, mode, A, w.segp, s, build_cache ? w.cache : nullptr)
+                               : run_proj(g, mode, c, A, s);
     if (st) return st;
     const int N = g.desc.n_px;
     const dim3 grid((N + 31) / 32, (N + 31) / 32, g.desc.batch * c.G);
@@ -928,14 +934,15 @@ static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const f
     regsq_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, P[1], N); note();
     CK(cudaGetLastError());
     // 3: b = -(J^T r + alpha L^T L u); z = p = b; s = 0; ||b||^2
-    if ((st = proj_adjoint(g, w, MODE_VJP, w.ysino, s))) return st;
+    const bool cached = g.adj_seg && g.gn_cached;
+    // the gradient VJP also writes the GN Jacobian-entry cache (fused cache build)
+    if ((st = proj_adjoint(g, w, MODE_VJP, w.ysino, s, cached && n_cg > 0))) return st;
     finish_kernel<<<vg, kVecThreads, 0, s>>>(w.gacc, Gv, lam, mu, alpha, 0.f, -1.f, w.bl, w.bm, w.bl, w.bm, P[2], w.zl,
                                             w.zm, w.pl, w.pm, s_lam, s_mu, N); note();
     CK(cudaGetLastError());
     scalar_kernel<<<sgrid, 128, 0, s>>>(SC_INIT, 0, P[0], P[1], P[2], kNblk, w.cg, stats, B, alpha, beta, betav); note();
     CK(cudaGetLastError());
-    const bool cached = g.adj_seg && g.gn_cached;
-    if (cached && n_cg > 0 && (st = gnc_build(g, w, s))) return st;   // the VJP above left u's partials
+
     // 5: CG
     for (int k = 0; k < n_cg; ++k) {
         if (cached) {

@@ -373,10 +373,14 @@ struct RayB {   // per-ray constants of sweep B
 // registers and read-modify-written once when the ray leaves the cell (a cell spans ~1.5-2 samples):
 // fewer shared-memory accesses, and those only by the lanes that change cell (bank-conflict bound
 // since the segmented adjoint).  0: one read-modify-write per sample (prefetched accumulator reads).
-template <bool PAIRED, bool COMP>
+// CACHE (the LM wrap's gradient VJP): rb holds the unit-weight constants; every sample's Jacobian
+// entries (alpha, beta, alpha', beta') go to the lane's cache block (row k) and the scatter weights
+// are w_r (alpha, beta) + w'_r (alpha', beta') -- the cache build of lin_kernel fused into the VJP.
+template <bool PAIRED, bool COMP, bool CACHE = false>
 __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* __restrict__ acc, int P, int r0,
                                        int r1, int abase, int sP, int ilo, int64_t dU, int64_t dV, float cf, float ch,
-                                       const RayB& rb, int& i, int64_t& u, int64_t& v, StateB& st)
+                                       const RayB& rb, int& i, int64_t& u, int64_t& v, StateB& st,
+                                       float wr = 0.f, float wr1 = 0.f, float4* cl = nullptr, int* kp = nullptr)
 {
     int iv = hi32(v), iu = hi32(u);
     if (i < ilo || iv < r0 || iv >= r1) return;
@@ -413,7 +417,21 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
         const float le = x.x * E;
         float al = rb.kl * E;
         float am = rb.km * (((rb.G - x_.q) - (rb.Gc - x_.qc)) - 0.5f * le);
-        if constexpr (PAIRED) {
+        if constexpr (CACHE) {   // unit-weight entries: store, then weight
+            float4 cv = make_float4(al, am, 0.f, 0.f);
+            if constexpr (PAIRED) {
+                const float E1 = ex2((rb.Sl - arg_hi) - (rb.Slc - x_.sc));
+                const float le1 = x.x * E1;
+                cv.z = rb.kl1 * E1;
+                cv.w = rb.km1 * ((x_.q1 - x_.q1c) + 0.5f * le1);
+                if (COMP) kahan(x_.q1, x_.q1c, le1);
+                else x_.q1 += le1;
+            }
+            __stcs(cl + static_cast<int64_t>(*kp) * 32, cv);
+            ++*kp;
+            al = fmaf(wr, cv.x, wr1 * cv.z);
+            am = fmaf(wr, cv.y, wr1 * cv.w);
+        } else if constexpr (PAIRED) {
             const float E1 = ex2((rb.Sl - arg_hi) - (rb.Slc - x_.sc));   // e^{-(S - A_i)}
             const float le1 = x.x * E1;
             al = fmaf(rb.kl1, E1, al);
@@ -901,7 +919,9 @@ __global__ void __launch_bounds__(512, 1) seg_a_kernel(ProjArgs A)   // W consum
 
 // Phase B: per-ray constants from the K partials, then sweep B of the unit (comb groups) into the
 // unit's partial slot (zeroed by the slot's first unit; every flush adds).
-template <int MODE, bool PAIRED>
+__device__ __forceinline__ float4* cache_lane(const ProjArgs& A, const UnitInfo& ui, int grp, int lane, int* kend);
+
+template <int MODE, bool PAIRED, bool CACHE>
 __global__ void __launch_bounds__(512, 1) seg_b_kernel(ProjArgs A)
 {
     const int W = blockDim.x >> 5;
@@ -1033,10 +1053,12 @@ __global__ void __launch_bounds__(512, 1) seg_b_kernel(ProjArgs A)
         for (int pass = 0; pass < A.passesB; ++pass) {
             const int grp = pass * W + warp;
             const int r = grp < A.n_groups ? A.groups[grp * 32 + lane] : -1;
-            int ii = -1, ilo = 0;
+            int ii = -1, ilo = 0, kc = 0;
             int64_t uu = 0, vv = 0;
             RayB rb{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             StateB st{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            float cw = 0.f, cw1 = 0.f;
+            float4* cl = nullptr;
             if (r >= 0) {
                 const int d = r / J, j = r - d * J;
                 float wd = 0.f, wd1 = 0.f;
@@ -1055,11 +1077,19 @@ __global__ void __launch_bounds__(512, 1) seg_b_kernel(ProjArgs A)
                 const float sc = rsc[r];
                 const float4 G = gsh[r];
                 const float2 q1 = q1i[r];
-                rb = RayB{wr * A.delta * sc, -wr * A.delta * A.delta * sc, G.x, G.y,
-                          wr1 * A.delta, -wr1 * A.delta * A.delta, G.z, G.w};
+                if (CACHE) {   // unit-weight constants; the lane's weights apply after the cache store
+                    rb = RayB{A.delta * sc, -A.delta * A.delta * sc, G.x, G.y, A.delta, -A.delta * A.delta, G.z, G.w};
+                    cw = wr;
+                    cw1 = wr1;
+                    int kend_unused;
+                    cl = cache_lane(A, ui, grp, lane, &kend_unused);
+                } else {
+                    rb = RayB{wr * A.delta * sc, -wr * A.delta * A.delta * sc, G.x, G.y,
+                              wr1 * A.delta, -wr1 * A.delta * A.delta, G.z, G.w};
+                }
                 st.q1 = q1.x;
                 st.q1c = q1.y;
-                if (wr != 0.f || wr1 != 0.f) {
+                if (CACHE || wr != 0.f || wr1 != 0.f) {
                     const RayP rp = rays[r];
                     ii = seg_entry(rp, bound);
                     ilo = rp.ilo;
@@ -1076,8 +1106,8 @@ __global__ void __launch_bounds__(512, 1) seg_b_kernel(ProjArgs A)
                 const bool flip = j & 1;
                 const int abase = flip ? Rb * P : 0, sP = flip ? -P : P;
                 if (PGET_ABLATE != 3)   // 3: no sweep B walk at all
-                    walk_b<PAIRED, ModeTraits<MODE>::COMP_S>(sbuf, wacc, P, r0, r1, abase, sP, ilo, dU, dV, cf, ch, rb, ii,
-                                                             uu, vv, st);
+                    walk_b<PAIRED, ModeTraits<MODE>::COMP_S, CACHE>(sbuf, wacc, P, r0, r1, abase, sP, ilo, dU, dV, cf, ch,
+                                                                    rb, ii, uu, vv, st, cw, cw1, cl, &kc);
                 __syncthreads();   // stage buffer b and every warp ring consumed
                 if (tid == 0 && s + 2 < n_stages)
                     issue_seg_stage<false>(A, Rb, sb0 + s + 2, stage0 + b * A.stage_bytes, &mbar[b]);
@@ -1800,8 +1830,14 @@ static cudaError_t launch_seg_mode(int phase, int maxg, bool paired, const ProjA
             else seg_a_kernel<MODE, 2, false><<<grid, block, smem, s>>>(A);
         }
     } else {
-        if (paired) seg_b_kernel<MODE, true><<<grid, block, smem, s>>>(A);
-        else seg_b_kernel<MODE, false><<<grid, block, smem, s>>>(A);
+        const bool cache = MODE == MODE_VJP && A.cache != nullptr;   // fused cache build (LM wrap)
+        if (cache) {
+            if (paired) seg_b_kernel<MODE, true, MODE == MODE_VJP><<<grid, block, smem, s>>>(A);
+            else seg_b_kernel<MODE, false, MODE == MODE_VJP><<<grid, block, smem, s>>>(A);
+        } else {
+            if (paired) seg_b_kernel<MODE, true, false><<<grid, block, smem, s>>>(A);
+            else seg_b_kernel<MODE, false, false><<<grid, block, smem, s>>>(A);
+        }
     }
     return cudaGetLastError();
 }
@@ -1827,8 +1863,10 @@ static cudaError_t seg_attr_mode(int phase, size_t smem)
         if ((e = cudaFuncSetAttribute(seg_a_kernel<MODE, 1, false>, a, v))) return e;
         return cudaFuncSetAttribute(seg_a_kernel<MODE, 2, false>, a, v);
     }
-    if ((e = cudaFuncSetAttribute(seg_b_kernel<MODE, true>, a, v))) return e;
-    return cudaFuncSetAttribute(seg_b_kernel<MODE, false>, a, v);
+    if ((e = cudaFuncSetAttribute(seg_b_kernel<MODE, true, false>, a, v))) return e;
+    if ((e = cudaFuncSetAttribute(seg_b_kernel<MODE, false, false>, a, v))) return e;
+    if ((e = cudaFuncSetAttribute(seg_b_kernel<MODE, true, MODE == MODE_VJP>, a, v))) return e;
+    return cudaFuncSetAttribute(seg_b_kernel<MODE, false, MODE == MODE_VJP>, a, v);
 }
 
 cudaError_t set_seg_smem_limit(int phase, int mode, size_t smem)
