@@ -209,6 +209,7 @@ def main():
     ap.add_argument("--ref-angles", type=int, default=36)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the step directly instead of a CUDA graph")
     args = ap.parse_args()
     rank, world, local = dist_env()
     if args.impl == "reference":
@@ -274,6 +275,26 @@ def main():
     sample_passes = 3 + sum(v * (2 if k == "gn" else 1) for k, v in lmp.items())
     samples_per_step = nominal * sample_passes
 
+    # ---- the whole step captured once in a CUDA graph (every library launch is capturable, the
+    #      cooperative CG kernel included; replays give bit-identical results) and replayed; the
+    #      library launches of one step are counted during the capture
+    if args.no_graph:
+        run_step = step
+        per_step_launches = None
+    else:
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        gstep = torch.cuda.CUDAGraph()
+        pg.profile_begin(0)
+        with torch.cuda.graph(gstep, stream=cs):
+            step()
+        per_step_launches = pg.profile_end()["total_launches"]
+        torch.cuda.synchronize()
+        run_step = gstep.replay
+        for _ in range(2):
+            run_step()
+        torch.cuda.synchronize()
+
     # ---- the timed region (value): K whole steps, events at the step boundaries only, library
     #      launches counted (pget_profile_begin(0): counting, no per-launch events)
     se = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
@@ -286,10 +307,12 @@ def main():
     for k in range(args.steps):
         flush.zero_()                       # L2 flush between timed steps (outside the events)
         se[k][0].record()
-        step()
+        run_step()
         se[k][1].record()
     torch.cuda.synchronize()
     launches = pg.profile_end()["total_launches"]
+    if per_step_launches is not None:        # graph replays bypass the host-side counter
+        launches = per_step_launches * args.steps
     if world > 1:
         dist.barrier()
     total_ms = max_over_ranks(sum(a.elapsed_time(b) for a, b in se), world, "cuda")
@@ -336,12 +359,23 @@ def main():
         for _ in range(2):
             e2e_step()
         torch.cuda.synchronize()
+        run_e2e = e2e_step
+        if not args.no_graph:   # the copies and the step captured together, as the user would
+            ce = torch.cuda.Stream()
+            ce.wait_stream(torch.cuda.current_stream())
+            ge = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(ge, stream=ce):
+                e2e_step()
+            torch.cuda.synchronize()
+            run_e2e = ge.replay
+            run_e2e()
+            torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         tot = 0.0
         for _ in range(args.steps):
             flush.zero_()
             a.record()
-            e2e_step()
+            run_e2e()
             b.record()
             b.synchronize()
             tot += a.elapsed_time(b)
@@ -385,7 +419,8 @@ def main():
                        "nominal_samples_per_pass": nominal, "traced_samples_per_pass": traced,
                        "angle_banks_merged": bool(g.info["angle_banks_merged"]),
                        "sample_passes_per_step": sample_passes,
-                       "l2": "flushed between timed steps (256 MiB write, outside the events)"},
+                       "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                       "launch": "direct" if args.no_graph else "the whole step captured once as a CUDA graph, replayed"},
             "per_op": {
                 "forward_samples_per_s": nominal * K / (phase["forward"] * 1e-3),
                 "jvp_samples_per_s": nominal * K / (phase["jvp"] * 1e-3),
@@ -403,6 +438,15 @@ def main():
                          "alg_bytes_per_sample": ALG_BYTES[dom], "units_per_launch": units,
                          "launch_ms": per_launch_ms},
             "roofline_ncu": roofline_ncu(cfg.cid, dom),
+            # SURVEY.md 8(d)'s bound model of the LM iteration on NOMINAL samples: 43 pass-equivalents
+            # (2 forward x 32 B + 21 VJP-class x 96 B + 20 JVP-class x 64 B per nominal sample) through
+            # the shared-memory crossbar; frac > 1 means the line pairing / duplicate merging saved
+            # more than the kernels lose to the crossbar
+            "lm_bound_model": {
+                "bound_ms": nominal * (2 * 32 + 21 * 96 + 20 * 64) / (peak_gbs * 1e9) * 1e3,
+                "measured_ms": phase["lm"] / K,
+                "frac": (nominal * (2 * 32 + 21 * 96 + 20 * 64) / (peak_gbs * 1e9) * 1e3) / (phase["lm"] / K),
+                "basis": "SURVEY.md 8(d): nominal samples x 3360 B at 128 B/clk/SM x 148 SMs x SM clock"},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
