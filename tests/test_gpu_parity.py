@@ -327,3 +327,32 @@ def test_lm_iteration_config5_batched(pg):
         for m in range(k + 4, B, 4):
             assert abs(S[m]["f"] - S[k]["f"]) <= 1e-6 * S[k]["f"]
             assert abs(S[m]["pred"] - S[k]["pred"]) <= 1e-4 * abs(S[k]["pred"]), (k, m)
+
+
+def test_lm_iteration_cuda_graph_capture(pg):
+    """Every launch of an LM iteration (the cooperative CG kernel included) is capturable: one
+    gn_cg_step captured in a CUDA graph and replayed gives the same bits as a direct call (what
+    bench.py times)."""
+    gd = dict(n_px=24, n_angles=16, n_banks=2, n_det=21, n_subrays=3, subray_sigma=0.4, step_px=0.5,
+              bank1_shift=0.0, batch=2)
+    g = pg.Geometry(gd)
+    lam, mu, _, _ = rand_inputs(gd, 3)
+    y = O.forward(gd, lam * 1.1, mu * 0.9).astype(np.float32)
+    L, M, Y = dev(lam), dev(mu), dev(y)
+    sl, sm = torch.empty(g.img_shape, device="cuda"), torch.empty(g.img_shape, device="cuda")
+    st = pg.stats_buffer(g)
+    ws = g.workspace("gn_cg_step")
+    step = lambda: pg.gn_cg_step(g, L, M, Y, 1e-3, 0.0, 6, s_lam=sl, s_mu=sm, stats=st, ws=ws)
+    step()
+    torch.cuda.synchronize()
+    ref_s, ref_st = sl.clone(), st.clone()
+    cs = torch.cuda.Stream()
+    cs.wait_stream(torch.cuda.current_stream())
+    gr = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gr, stream=cs):
+        step()
+    sl.zero_()
+    st.zero_()
+    gr.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(sl, ref_s) and torch.equal(st, ref_st)
