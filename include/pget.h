@@ -250,6 +250,15 @@ pget_status pget_safeguard(pget_geometry g, const float* lam, const float* mu, c
                            float* u_next_mu, pget_safeguard_stats* stats_dev, void* ws,
                            size_t ws_bytes, pget_stream_t stream);
 
+/* Diagnostic: checks on the host that the handle's static schedules are consistent (every
+ * (member, angle-bank, detector) of the forward/JVP schedules covered once; the adjoint's row
+ * segments partition every ray's samples; every unit scheduled once per phase; partial slots hold
+ * <= 16 units of one CTA and their row ranges cover the units' rows; every slot reduced once; the
+ * coefficient-cache blocks cover every lane; comb lanes >= comb stride apart).  Works on host-only
+ * handles (device < 0).  PGET_OK or PGET_ERR_INVALID_ARGUMENT with the violated rule in
+ * pget_last_error_message(). */
+pget_status pget_schedule_check(pget_geometry g);
+
 /* Tracing.  Between pget_profile_begin and pget_profile_end every kernel the library
  * launches (on any stream, from any thread) is counted, and each projector launch is
  * bracketed by two CUDA events recorded on the stream it is launched on (up to

@@ -112,10 +112,11 @@ def lib():
         L.pget_gn_cg_step.argtypes = [P, P, P, P, C.c_float, C.c_float, C.c_int32, C.c_uint32, P, P, P, P, S, P]
         L.pget_safeguard.argtypes = [P, P, P, P, P, P, P, P, C.c_float, C.c_float, P, P, P, P, S, P]
         L.pget_lm_solve.argtypes = [P, P, P, P, C.POINTER(LMParams), P, P, S, P]
+        L.pget_schedule_check.argtypes = [P]
         L.pget_profile_begin.argtypes = [C.c_int32]
         L.pget_profile_end.argtypes = [P, P, P]
         for n in ("pget_profile_begin", "pget_profile_end", "pget_geometry_create", "pget_geometry_destroy", "pget_geometry_info", "pget_geometry_export",
-                  "pget_forward", "pget_jvp", "pget_vjp", "pget_gn_apply", "pget_gn_cg_step", "pget_safeguard", "pget_lm_solve"):
+                  "pget_forward", "pget_jvp", "pget_vjp", "pget_gn_apply", "pget_gn_cg_step", "pget_safeguard", "pget_lm_solve", "pget_schedule_check"):
             getattr(L, n).restype = C.c_int
         _lib = L
     return _lib
@@ -189,6 +190,10 @@ class Geometry:
         out = np.zeros(nbytes // np.dtype(dt).itemsize, dtype=dt)
         _check(lib().pget_geometry_export(self._h, tid, out.ctypes.data_as(C.c_void_p), nbytes), "export")
         return out
+
+    def schedule_check(self):
+        """Host-side consistency check of the handle's static schedules (raises on a violation)."""
+        _check(lib().pget_schedule_check(self._h), "pget_schedule_check")
 
     def workspace_bytes(self, op: str) -> int:
         return int(lib().pget_workspace_bytes(self._h, OPS[op]))

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <atomic>
+#include <map>
 #include <mutex>
 #include <new>
 #include <string>
@@ -328,6 +329,24 @@ pget_status run_seg(const Geometry& g, int mode, ProjArgs A, float* segp, cudaSt
     return PGET_OK;
 }
 
+// the three schedules of a handle on the host (sm_count CTAs per SM-count, the kernels' CTAs per SM)
+void build_host_schedules(Geometry& g, const std::vector<RayP>& rays)
+{
+    for (int k = 0; k < 3; ++k) {
+        const int mode = k == kSchedFwd ? MODE_FWD : (k == kSchedJvp ? MODE_JVP : MODE_VJP);
+        Schedule& S = g.sch[k];
+        if (k == kSchedAdj && g.adj_seg) {
+            build_adj_schedule(g, rays, g.segA_cps * g.sm_count, g.sm_count, &S);
+            const SegCfg sc = seg_cfg(g);
+            build_adj_stages(sc.RbA, sc.passesA, sc.RbB, sc.passesB, &S);
+            const double cache_gb = static_cast<double>(g.desc.batch) * S.cache_rows_member * 32 * sizeof(float4) / 1e9;
+            if (cache_gb > g.cache_max_gb) g.gn_cached = false;
+        } else {
+            build_schedule(g, k, g.sm_count * proj_ctas_per_sm(mode), &S);
+        }
+    }
+}
+
 // ---- workspace carving
 struct WS {
     float2* img2[2] = {nullptr, nullptr};
@@ -494,7 +513,10 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     Geometry& g = h->g;
     if (g.desc.n_px > 2048) { delete h; return fail(PGET_ERR_INVALID_ARGUMENT, "n_px > 2048 not supported"); }
     g.device = device;
-    if (device < 0) {   // host-only handle: tables and info, no device tables, no compute
+    if (device < 0) {   // host-only handle: tables, info and the host schedules; no device tables, no compute
+        std::vector<RayP> rays;
+        build_ray_params(g, &rays);
+        build_host_schedules(g, rays);
         *out = h;
         return PGET_OK;
     }
@@ -524,20 +546,11 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     if (const char* ev = std::getenv("PGET_SEGA_W")) g.segA_W = std::max(1, std::min(15, std::atoi(ev)));
     if (const char* ev = std::getenv("PGET_SEGA_CPS")) g.segA_cps = std::max(1, std::min(4, std::atoi(ev)));
     if ((g.segA_W + 1) * 32 * g.segA_cps > 2048) g.segA_cps = 2048 / ((g.segA_W + 1) * 32);
+    // the coefficient cache only while it stays small next to HBM (config 2: 0.4 GB, config 4:
+    // 2.7 GB; config 5's 64 assemblies would need 25 GB: recompute there)
+    build_host_schedules(g, rays);
     for (int k = 0; k < 3 && e == cudaSuccess; ++k) {
-        const int mode = k == kSchedFwd ? MODE_FWD : (k == kSchedJvp ? MODE_JVP : MODE_VJP);
         Schedule& S = g.sch[k];
-        if (k == kSchedAdj && g.adj_seg) {
-            build_adj_schedule(g, rays, g.segA_cps * g.sm_count, g.sm_count, &S);
-            const SegCfg sc = seg_cfg(g);
-            build_adj_stages(sc.RbA, sc.passesA, sc.RbB, sc.passesB, &S);
-            // the coefficient cache only while it stays small next to HBM (config 2: 0.4 GB, config 4:
-            // 2.7 GB; config 5's 64 assemblies would need 25 GB: recompute there)
-            const double cache_gb = static_cast<double>(g.desc.batch) * S.cache_rows_member * 32 * sizeof(float4) / 1e9;
-            if (cache_gb > g.cache_max_gb) g.gn_cached = false;
-        } else {
-            build_schedule(g, k, g.sm_count * proj_ctas_per_sm(mode), &S);
-        }
         auto up = [&](auto** dst, const auto& v) {
             using T = typename std::remove_reference<decltype(v)>::type::value_type;
             if (e == cudaSuccess) e = cudaMalloc(dst, std::max<size_t>(1, v.size()) * sizeof(T));
@@ -1102,6 +1115,121 @@ pget_status pget_safeguard(pget_geometry h, const float* lam, const float* mu, c
     guard_select_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, s_lam, s_mu, cand_lam, cand_mu, stats, u_next_lam,
                                                   u_next_mu, n2); note();
     CK(cudaGetLastError());
+    return PGET_OK;
+}
+
+// Host-side consistency of a handle's static schedules (diagnostic; tests/test_abi.py).
+pget_status pget_schedule_check(pget_geometry h)
+{
+    if (!h) return fail(PGET_ERR_INVALID_ARGUMENT, "NULL geometry handle");
+    const Geometry& g = h->g;
+    const int B = g.desc.batch, R = g.R, nd = g.desc.n_det, J = g.desc.n_subrays;
+    std::vector<RayP> rays;
+    build_ray_params(g, &rays);
+    auto bad = [&](const std::string& m) { return fail(PGET_ERR_INVALID_ARGUMENT, "schedule check: " + m); };
+    // fused kinds: every (member, traced angle-bank, detector) covered exactly once
+    for (int k = 0; k < 2; ++k) {
+        const Schedule& S = g.sch[k];
+        const bool paired = g.dup && k != kSchedJvp;
+        const std::vector<int32_t>& list = paired ? g.task_ab_p : g.task_ab;
+        std::map<std::pair<int, int>, std::vector<int>> cover;
+        for (const TaskD& t : S.tasks) {
+            auto& v = cover[{t.m, t.ab}];
+            if (v.empty()) v.assign(nd, 0);
+            for (int d = t.dlo; d < t.dhi; ++d) ++v[d];
+        }
+        if (cover.size() != static_cast<size_t>(B) * list.size()) return bad("fused tasks miss an angle-bank");
+        for (auto& kv : cover)
+            for (int c : kv.second)
+                if (c != 1) return bad("a detector is covered " + std::to_string(c) + " times");
+        if (S.cta_begin.size() != static_cast<size_t>(S.C) + 1 || S.cta_begin.back() != static_cast<int>(S.tasks.size()))
+            return bad("fused CTA ranges");
+    }
+    if (!g.adj_seg) return PGET_OK;
+    const Schedule& S = g.sch[kSchedAdj];
+    const int K = S.K, ntab = S.ntab, ngB = S.max_gB;
+    const std::vector<int32_t>& list = g.dup ? g.task_ab_p : g.task_ab;
+    if (K < 1 || S.seg_rows.size() != static_cast<size_t>(K) + 1 || S.seg_rows.front() != 0 ||
+        S.seg_rows.back() != g.P - 1)
+        return bad("segment rows");
+    // segments partition every ray's samples
+    for (int t = 0; t < ntab; ++t)
+        for (int r = 0; r < R; ++r) {
+            const RayP& rp = rays[static_cast<size_t>(list[t]) * R + r];
+            int64_t n = 0;
+            for (int k = 0; k < K; ++k)
+                n += rp.dV > 0 ? seg_entry(rp, S.seg_rows[k + 1]) - seg_entry(rp, S.seg_rows[k])
+                               : seg_entry(rp, S.seg_rows[k]) - seg_entry(rp, S.seg_rows[k + 1]);
+            const int64_t want = rp.ihi >= rp.ilo ? rp.ihi - rp.ilo + 1 : 0;
+            if (n != want) return bad("segments do not partition a ray's samples");
+        }
+    // units: each canonical unit once per phase, in CTA ranges
+    for (int ph = 0; ph < 2; ++ph) {
+        const std::vector<UnitD>& U = ph ? S.unitsB : S.unitsA;
+        const std::vector<int32_t>& ub = ph ? S.ub_begin : S.ua_begin;
+        std::vector<int> seen(static_cast<size_t>(S.n_canon), 0);
+        for (const UnitD& u : U) {
+            if (u.canon < 0 || u.canon >= S.n_canon) return bad("unit index");
+            if (u.canon != (u.m * ntab + static_cast<int>(std::find(list.begin(), list.end(), u.ab) - list.begin())) * K + u.seg)
+                return bad("canonical unit index");
+            ++seen[u.canon];
+        }
+        for (int c : seen)
+            if (c != 1) return bad("a unit is scheduled " + std::to_string(c) + " times");
+        if (ub.back() != static_cast<int>(U.size())) return bad("unit CTA ranges");
+    }
+    // slots: <= 16 units, one CTA, one (member, class), rows inside the slot range; reduce lists
+    std::vector<int> used(static_cast<size_t>(S.n_slots), 0);
+    for (int c = 0; c < S.C; ++c) {
+        int prev = -1;
+        for (int u = S.ub_begin[c]; u < S.ub_begin[c + 1]; ++u) {
+            const UnitD& t = S.unitsB[u];
+            if (t.slot < 0 || t.slot >= S.n_slots) return bad("slot index");
+            if (t.slot != prev && used[t.slot]) return bad("a slot spans CTAs or runs");
+            if ((t.flags & kTaskFirst) != 0 && t.slot == prev) return bad("first flag");
+            ++used[t.slot];
+            const int lo = std::max(0, S.seg_rows[t.seg] - kHalo);
+            const int hi = std::min(g.desc.n_px, S.seg_rows[t.seg + 1] - kHalo + 1);
+            if (lo < S.slot_lo[t.slot] || hi > S.slot_hi[t.slot]) return bad("slot rows");
+            prev = t.slot;
+        }
+    }
+    for (int c : used)
+        if (c < 1 || c > 16) return bad("slot with " + std::to_string(c) + " units");
+    std::vector<int> inl(static_cast<size_t>(S.n_slots), 0);
+    for (int e = 0; e < S.red_off.back(); ++e) ++inl[S.red_slot[e]];
+    for (int c : inl)
+        if (c != 1) return bad("reduce lists");
+    // cache blocks cover the longest lane of every comb group
+    for (int t = 0; t < ntab; ++t)
+        for (int k = 0; k < K; ++k)
+            for (int gi = 0; gi < ngB; ++gi) {
+                const size_t idx = (static_cast<size_t>(t) * K + k) * ngB + gi;
+                const int64_t rows = S.cache_off[idx + 1] - S.cache_off[idx];
+                for (int l = 0; l < 32; ++l) {
+                    const int r = S.groups[static_cast<size_t>(gi) * 32 + l];
+                    if (r < 0) continue;
+                    const RayP& rp = rays[static_cast<size_t>(list[t]) * R + r];
+                    const int n = rp.dV > 0 ? seg_entry(rp, S.seg_rows[k + 1]) - seg_entry(rp, S.seg_rows[k])
+                                            : seg_entry(rp, S.seg_rows[k]) - seg_entry(rp, S.seg_rows[k + 1]);
+                    if (n > rows) return bad("cache block shorter than a lane");
+                }
+            }
+    // comb groups: every ray once, lanes of a group >= comb_S rays apart
+    std::vector<int> rseen(R, 0);
+    for (int gi = 0; gi < ngB; ++gi)
+        for (int l = 0; l < 32; ++l) {
+            const int r = S.groups[static_cast<size_t>(gi) * 32 + l];
+            if (r < 0) continue;
+            ++rseen[r];
+            for (int l2 = 0; l2 < l; ++l2) {
+                const int r2 = S.groups[static_cast<size_t>(gi) * 32 + l2];
+                if (r2 >= 0 && std::abs(r2 - r) < g.comb_S) return bad("comb lanes too close");
+            }
+        }
+    for (int c : rseen)
+        if (c != 1) return bad("comb groups do not cover every ray once");
+    (void)J;
     return PGET_OK;
 }
 

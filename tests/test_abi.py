@@ -93,3 +93,20 @@ def test_compute_on_host_only_handle_fails_cleanly():
     assert pg.lib().pget_table_bytes(g.handle, 42) == 0
     for op in pg.OPS:
         assert g.workspace_bytes(op) > 0
+
+
+@pytest.mark.parametrize("gd", [P.geometry_desc(c) for c in (1, 2, 3, 4)] + [
+    dict(n_px=33, n_angles=12, n_banks=2, n_det=7, n_subrays=2, subray_sigma=0.4, step_px=0.5, bank1_shift=0.0,
+         batch=3),
+    dict(n_px=16, n_angles=7, n_banks=1, n_det=5, n_subrays=9, subray_sigma=0.3, step_px=0.37, bank1_shift=0.0,
+         batch=1),
+    dict(n_px=24, n_angles=10, n_banks=2, n_det=11, n_subrays=3, subray_sigma=0.4, step_px=0.5, bank1_shift=6.5,
+         batch=2),
+    dict(n_px=64, n_angles=90, n_banks=2, n_det=91, n_subrays=1, subray_sigma=0.4, step_px=0.5, bank1_shift=0.0,
+         batch=7),
+], ids=["cfg1", "cfg2", "cfg3", "cfg4", "odd33", "onebank", "shift", "batch7"])
+def test_static_schedules_consistent(gd):
+    """Host logic: the static schedules (fused forward/JVP task lists, the segmented adjoint's units,
+    stages, slots, reduce lists, coefficient-cache layout, comb groups) pass pget_schedule_check."""
+    g = pg.Geometry(gd, device=-1)
+    g.schedule_check()
