@@ -1282,6 +1282,7 @@ __device__ __forceinline__ void walk_lin(const float2* __restrict__ img, int P, 
         int o2 = o;
         if (nxt) {
             o2 = (iv2 - r0) * P + hi32(u2);
+            PGET_CHECK(o2 >= 0 && o2 + P + 1 < (r1 - r0 + 1) * P);
             n00 = img[o2]; n01 = img[o2 + 1]; n10 = img[o2 + P]; n11 = img[o2 + P + 1];
         }
         const float2 x = bilerp2(q00, q01, q10, q11, fu, fv);
@@ -1392,6 +1393,7 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
     int iv = iv0;
     auto step = [&](float4& c) -> bool {
         const int aoff = abase + (iv - r0) * sP + hi32(u);
+        PGET_CHECK(hi32(u) >= 0 && hi32(u) + 1 < P && iv >= r0 && iv < r1 && k < kend);
         const float fu = frac23(u), fv = frac23(v);
         const int i2 = i - 1;
         const int64_t u2 = u - dU, v2 = v - dV;
