@@ -986,10 +986,33 @@ static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const f
                                                                 box->w); note();
         CK(cudaGetLastError());
     }
-    // 6: pred = <b,s> - 1/2(||Js||^2 + alpha ||Ls||^2)
+    // 6: pred = <b,s> - 1/2(||Js||^2 + alpha ||Ls||^2); ||Js||^2 from the paired GN-mode phase A of
+    //    (u, s) when the segmented adjoint is on (the norm only needs GN-level accuracy), else from
+    //    the standalone JVP
     if ((st = pack4(g, w, lam, mu, s_lam, s_mu, s))) return st;
-    if ((st = proj_out(g, w, MODE_JVP, nullptr, w.dysino, s))) return st;
-    sumsq_kernel<<<vg, kVecThreads, 0, s>>>(w.dysino, P[5], nsper); note();
+    if (g.adj_seg) {
+        const SegCfg c = seg_cfg(g);
+        const Schedule& S = g.sch[kSchedAdj];
+        ProjArgs A = gnc_args(g, w);
+        ProjArgs Aa = A;
+        Aa.units = S.d_unitsA;
+        Aa.u_begin = S.d_ua_begin;
+        Aa.stages = S.d_stA;
+        Aa.s_begin = S.d_sa_begin;
+        Aa.RbA = c.RbA;
+        Aa.passesA = c.passesA;
+        Aa.stage_bytes = c.stageA;
+        CK(launch_seg(0, MODE_GN, c.maxgA, g.dup, Aa, c.gridA, (c.WA + 1) * 32, c.smemA, s));
+        note();
+        double* sq = reinterpret_cast<double*>(w.ysino);   // per (member, angle-bank); ysino is free here
+        CK(launch_jsq(g.dup, A, sq, c.gridB, c.WB * 32, c.smemB, s));
+        note();
+        CK(launch_jsq_member(sq, S.ntab, B, kNblk, P[5], s));
+        note();
+    } else {
+        if ((st = proj_out(g, w, MODE_JVP, nullptr, w.dysino, s))) return st;
+        sumsq_kernel<<<vg, kVecThreads, 0, s>>>(w.dysino, P[5], nsper); note();
+    }
     regsq_kernel<<<vg, kVecThreads, 0, s>>>(s_lam, s_mu, P[6], N); note();
     dot2_kernel<<<vg, kVecThreads, 0, s>>>(w.bl, w.bm, s_lam, s_mu, P[7], n2); note();
     scalar_kernel<<<sgrid, 128, 0, s>>>(SC_PRED, 0, P[5], P[6], P[7], kNblk, w.cg, stats, B, alpha, beta, betav); note();

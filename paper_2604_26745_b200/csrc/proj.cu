@@ -1691,6 +1691,71 @@ __global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
     }
 }
 
+// ||J s||^2 of the LM wrap's pred from the GN-mode phase-A partials of (u, s) (paired: the two banks
+// of a line per traversal; duplicate angle-banks counted twice): each block takes the segment-0
+// units of its unit list, i.e. every (member, traced angle-bank) once, and writes that angle-bank's
+// sum of squared detector values to sq[canon / K]
+template <bool PAIRED>
+__global__ void __launch_bounds__(512, 1) jsq_kernel(ProjArgs A, double* sq)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
+    float* rout = reinterpret_cast<float*>(smem + A.off_rout);
+    __shared__ double red[32];
+    const int tid = threadIdx.x, NT = blockDim.x;
+    const int c = blockIdx.x;
+    const int R = A.R, J = A.J;
+    for (int u = A.u_begin[c]; u < A.u_begin[c + 1]; ++u) {
+        if (A.units[u].seg != 0) continue;
+        const UnitInfo ui = unit_info(A, u, A.RbB);
+        for (int r = tid; r < R; r += NT) gn_rout_from_seg<PAIRED>(A, ui, r, rout);
+        __syncthreads();
+        double acc = 0.0;
+        for (int d = tid; d < A.n_det; d += NT) {
+            float yf = 0.f, yr = 0.f;
+            for (int j = 0; j < J; ++j) {
+                yf = fmaf(A.w[j], rout[d * J + j], yf);
+                yr = fmaf(A.w[j], rout[R + d * J + j], yr);
+            }
+            acc += static_cast<double>(yf) * yf + static_cast<double>(yr) * yr;
+        }
+        if (A.dup_half) acc *= 2.0;   // the duplicate angle-bank measures the same rays
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+        if ((tid & 31) == 0) red[tid >> 5] = acc;
+        __syncthreads();
+        if (tid == 0) {
+            double t = 0.0;
+            for (int w = 0; w < (NT >> 5); ++w) t += red[w];
+            sq[ui.canon / A.K] = t;
+        }
+        __syncthreads();   // rout and red are rewritten by the next unit
+    }
+}
+
+// per member: the angle-banks' sums in order into partial[m * nblk] (the other nblk - 1 partials 0)
+__global__ void jsq_member_kernel(const double* __restrict__ sq, int ntab, int B, int nblk, double* partial)
+{
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= B) return;
+    double t = 0.0;
+    for (int i = 0; i < ntab; ++i) t += sq[static_cast<size_t>(m) * ntab + i];
+    partial[static_cast<size_t>(m) * nblk] = t;
+    for (int k = 1; k < nblk; ++k) partial[static_cast<size_t>(m) * nblk + k] = 0.0;
+}
+
+cudaError_t launch_jsq(bool paired, const ProjArgs& A, double* sq, int grid, int block, size_t smem, cudaStream_t s)
+{
+    if (paired) jsq_kernel<true><<<grid, block, smem, s>>>(A, sq);
+    else jsq_kernel<false><<<grid, block, smem, s>>>(A, sq);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_jsq_member(const double* sq, int ntab, int B, int nblk, double* partial, cudaStream_t s)
+{
+    jsq_member_kernel<<<(B + 127) / 128, 128, 0, s>>>(sq, ntab, B, nblk, partial);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_gnc(int phase, bool paired, const ProjArgs& A, int grid, int block, size_t smem, cudaStream_t s)
 {
     if (phase == 0) {
@@ -1714,6 +1779,8 @@ cudaError_t set_gnc_smem_limit(size_t smem)
     if ((e = cudaFuncSetAttribute(lin_kernel<false>, a, v))) return e;
     if ((e = cudaFuncSetAttribute(jvpc_kernel, a, v))) return e;
     if ((e = cudaFuncSetAttribute(gnb_kernel<true>, a, v))) return e;
+    if ((e = cudaFuncSetAttribute(jsq_kernel<true>, a, v))) return e;
+    if ((e = cudaFuncSetAttribute(jsq_kernel<false>, a, v))) return e;
     return cudaFuncSetAttribute(gnb_kernel<false>, a, v);
 }
 
