@@ -345,6 +345,11 @@ void build_host_schedules(Geometry& g, const std::vector<RayP>& rays)
             build_schedule(g, k, g.sm_count * proj_ctas_per_sm(mode), &S);
         }
     }
+    if (g.adj_seg && g.jvp_seg) {   // segmented standalone JVP (phase A only)
+        build_adj_schedule(g, rays, g.segA_cps * g.sm_count, g.sm_count, &g.schJ, true);
+        const SegCfg sc = seg_cfg(g);
+        build_adj_stages(sc.RbA, sc.passesA, sc.RbB, sc.passesB, &g.schJ);
+    }
 }
 
 // ---- workspace carving
@@ -354,6 +359,7 @@ struct WS {
     float2* slots = nullptr;
     double2* gacc = nullptr;  // [G][B][N][N] fp64 partial gradients (g_lam, g_mu), G = ProjCfg::G
     float* segp = nullptr;    // segmented adjoint: [n_canon][kSegFields][R] phase-A partial sums
+    float* segpJ = nullptr;   // segmented standalone JVP: [n_canonJ][kSegFields][R]
     float4* cache = nullptr;  // GN with cached Jacobian entries: [B][rows][32]
     float* jp = nullptr;      // [n_canon][2][R] per-segment (J p) partials
     float *ysino = nullptr, *dysino = nullptr;
@@ -402,6 +408,8 @@ WS carve(const Geometry& g, int op, char* base)
             w.jp = reinterpret_cast<float*>(take(static_cast<size_t>(S.n_canon) * 2 * g.R * sizeof(float)));
         }
     }
+    if ((op == PGET_OP_JVP || guard) && g.adj_seg && g.jvp_seg)
+        w.segpJ = reinterpret_cast<float*>(take(static_cast<size_t>(g.schJ.n_canon) * kSegFields * g.R * sizeof(float)));
     if (op == PGET_OP_GN_CG_STEP || op == PGET_OP_LM_SOLVE) {
         w.ysino = reinterpret_cast<float*>(take(ns * sizeof(float)));
         w.dysino = reinterpret_cast<float*>(take(ns * sizeof(float)));
@@ -475,6 +483,13 @@ void free_device_tables(Geometry* g)
         cudaFree(S.d_sa_begin); cudaFree(S.d_sb_begin); cudaFree(S.d_stA); cudaFree(S.d_stB); cudaFree(S.d_seg_rows);
         cudaFree(S.d_cache_off);
         S.d_cache_off = nullptr;
+    }
+    {
+        Schedule& S = g->schJ;
+        cudaFree(S.d_unitsA); cudaFree(S.d_ua_begin); cudaFree(S.d_stA); cudaFree(S.d_sa_begin); cudaFree(S.d_seg_rows);
+        S.d_unitsA = nullptr; S.d_ua_begin = S.d_sa_begin = S.d_seg_rows = nullptr; S.d_stA = nullptr;
+        cudaFree(g->d_tabsJ);
+        g->d_tabsJ = nullptr;
         S.d_unitsA = S.d_unitsB = nullptr;
         S.d_ua_begin = S.d_ub_begin = S.d_sa_begin = S.d_sb_begin = S.d_seg_rows = nullptr;
         S.d_stA = S.d_stB = nullptr;
@@ -536,6 +551,7 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     build_ray_params(g, &rays);
     if (e == cudaSuccess) e = cudaMalloc(&g.d_rays, rays.size() * sizeof(RayP));
     if (const char* ev = std::getenv("PGET_ADJ_FUSED")) g.adj_seg = std::atoi(ev) == 0;   // A/B experiments
+    if (const char* ev = std::getenv("PGET_JVP_FUSED")) g.jvp_seg = std::atoi(ev) == 0;
     if (const char* ev = std::getenv("PGET_GN_CACHE_MAX_GB")) g.cache_max_gb = std::atof(ev);
     if (const char* ev = std::getenv("PGET_GN_CACHE")) {   // 0: recompute, 1: hybrid, 2: fully cached
         const int v = std::atoi(ev);
@@ -576,6 +592,20 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
             up(&S.d_cache_off, S.cache_off);
         }
     }
+    if (g.adj_seg && g.jvp_seg) {
+        Schedule& S = g.schJ;
+        auto up = [&](auto** dst, const auto& v) {
+            using T = typename std::remove_reference<decltype(v)>::type::value_type;
+            if (e == cudaSuccess) e = cudaMalloc(dst, std::max<size_t>(1, v.size()) * sizeof(T));
+            if (e == cudaSuccess && !v.empty()) e = cudaMemcpy(*dst, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+        };
+        up(&S.d_unitsA, S.unitsA);
+        up(&S.d_ua_begin, S.ua_begin);
+        up(&S.d_stA, S.stA);
+        up(&S.d_sa_begin, S.sa_begin);
+        up(&S.d_seg_rows, S.seg_rows);
+        up(&g.d_tabsJ, g.task_ab);
+    }
     if (e == cudaSuccess) e = cudaMalloc(&g.d_w, g.wf.size() * sizeof(float));
     if (e == cudaSuccess) e = cudaMemcpy(g.d_rays, rays.data(), rays.size() * sizeof(RayP), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(g.d_w, g.wf.data(), g.wf.size() * sizeof(float), cudaMemcpyHostToDevice);
@@ -592,6 +622,7 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
             if (e == cudaSuccess) e = set_seg_smem_limit(1, mode, sc.smemB);
         }
         if (e == cudaSuccess) e = set_gnc_smem_limit(sc.smemB);
+        if (e == cudaSuccess && g.jvp_seg) e = set_seg_smem_limit(0, MODE_JVP, sc.smemA);
     }
     if (prev >= 0) cudaSetDevice(prev);
     if (e != cudaSuccess) {
@@ -836,6 +867,46 @@ static pget_status gnc_product(const Geometry& g, const WS& w, const float* lam,
     return PGET_OK;
 }
 
+// the standalone JVP of the packed (u, d) in w.img4: segmented (phase A over every traced angle-bank
+// + fp64 combine) when enabled, else the fused projector
+static pget_status jvp_out(const Geometry& g, const WS& w, float* y, float* dy, cudaStream_t s)
+{
+    if (!(g.adj_seg && g.jvp_seg)) return proj_out(g, w, MODE_JVP, y, dy, s);
+    const Schedule& S = g.schJ;
+    const SegCfg c = seg_cfg(g);
+    ProjArgs A = base_args(g, proj_cfg(g, MODE_JVP));
+    for (int k = 0; k < 2; ++k) { A.img2[k] = w.img2[k]; A.img4[k] = w.img4[k]; }
+    A.y = y;
+    A.dy = dy;
+    A.segp = w.segpJ;
+    A.K = S.K;
+    A.seg_rows = S.d_seg_rows;
+    A.units = S.d_unitsA;
+    A.u_begin = S.d_ua_begin;
+    A.stages = S.d_stA;
+    A.s_begin = S.d_sa_begin;
+    A.RbA = c.RbA;
+    A.passesA = c.passesA;
+    A.stage_bytes = c.stageA;
+    cudaEvent_t ea = nullptr, eb = nullptr;
+    if (g_prof.on.load(std::memory_order_relaxed)) {
+        std::lock_guard<std::mutex> lk(g_prof.mu);
+        g_prof.total += 2;
+        g_prof.mode_launches[MODE_JVP]++;
+        if (g_prof.used + 2 <= g_prof.pool.size()) {
+            ea = g_prof.pool[g_prof.used++];
+            eb = g_prof.pool[g_prof.used++];
+            g_prof.recs.push_back({MODE_JVP, ea, eb});
+        }
+    }
+    if (ea) cudaEventRecord(ea, s);
+    cudaError_t e = launch_seg(0, MODE_JVP, c.maxgA, false, A, c.gridA, (c.WA + 1) * 32, c.smemA, s);
+    if (e == cudaSuccess) e = launch_jvp_combine(A, g.d_tabsJ, static_cast<int>(g.task_ab.size()), g.desc.batch, s);
+    if (eb) cudaEventRecord(eb, s);
+    if (e != cudaSuccess) return cuda_fail(e, "segmented JVP launch");
+    return PGET_OK;
+}
+
 pget_status pget_forward(pget_geometry h, const float* lam, const float* mu, float* y, void* ws, size_t ws_bytes,
                          pget_stream_t stream)
 {
@@ -860,7 +931,7 @@ pget_status pget_jvp(pget_geometry h, const float* lam, const float* mu, const f
     const Geometry& g = h->g;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if ((st = pack4(g, w, lam, mu, dlam, dmu, s))) return st;
-    return proj_out(g, w, MODE_JVP, y, dy, s);
+    return jvp_out(g, w, y, dy, s);
 }
 
 pget_status pget_vjp(pget_geometry h, const float* lam, const float* mu, const float* wv, float* g_lam, float* g_mu,
@@ -1117,7 +1188,7 @@ pget_status pget_safeguard(pget_geometry h, const float* lam, const float* mu, c
     diff2_kernel<<<vec_grid(nimg), kVecThreads, 0, s>>>(cand_lam, cand_mu, lam, mu, w.zl, w.zm, nimg); note();
     CK(cudaGetLastError());
     if ((st = pack4(g, w, lam, mu, w.zl, w.zm, s))) return st;
-    if ((st = proj_out(g, w, MODE_JVP, w.ysino, w.dysino, s))) return st;
+    if ((st = jvp_out(g, w, w.ysino, w.dysino, s))) return st;
     residual_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, y_meas, P[0], nsper); note();
     regsq_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, P[1], N); note();
     dotsq_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, w.dysino, P[2], P[3], nsper); note();
@@ -1125,7 +1196,7 @@ pget_status pget_safeguard(pget_geometry h, const float* lam, const float* mu, c
     CK(cudaGetLastError());
     // J s_k
     if ((st = pack4(g, w, lam, mu, s_lam, s_mu, s))) return st;
-    if ((st = proj_out(g, w, MODE_JVP, nullptr, w.dysino, s))) return st;
+    if ((st = jvp_out(g, w, nullptr, w.dysino, s))) return st;
     dotsq_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, w.dysino, P[6], P[7], nsper); note();
     lapdot_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, s_lam, s_mu, P[8], P[9], N); note();
     CK(cudaGetLastError());

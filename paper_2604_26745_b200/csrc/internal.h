@@ -167,6 +167,10 @@ struct Geometry {
     int cg_coop_blocks = 148;   // co-resident blocks of cg_fused_kernel (cooperative launch bound)
     size_t smem_optin = 227 * 1024;
     Schedule sch[3];   // kSchedFwd, kSchedJvp, kSchedAdj (schedule.cpp), device copies owned here
+    // segmented standalone JVP: phase-A units over every traced angle-bank (unpaired) + a combine
+    Schedule schJ;
+    bool jvp_seg = true;
+    int32_t* d_tabsJ = nullptr;   // [ntab] traced angle-banks of schJ (task_ab)
     bool adj_seg = true;   // adjoint (VJP / GN) as the segmented two-phase projector (else the fused one)
     double cache_max_gb = 8.0;   // larger caches fall back to the recomputing GN product
     bool gn_hybrid = true;   // cached scatter with the recomputed (J p) (PGET_GN_CACHE=1)
@@ -188,6 +192,7 @@ void build_ray_params(const Geometry& g, std::vector<RayP>* rays);
 void build_schedule(const Geometry& g, int kind, int C, Schedule* S);
 // segmented adjoint schedule: units over CA phase-A CTAs and C phase-B CTAs, slots, comb groups;
 // then (once the band heights are known) the stage lists of both phases
-void build_adj_schedule(const Geometry& g, const std::vector<RayP>& rays, int CA, int C, Schedule* S);
+void build_adj_schedule(const Geometry& g, const std::vector<RayP>& rays, int CA, int C, Schedule* S,
+                        bool unpaired = false);
 void build_adj_stages(int RbA, int passesA, int RbB, int passesB, Schedule* S);
 }  // namespace pget

@@ -911,10 +911,67 @@ __global__ void __launch_bounds__(512, 1) seg_a_kernel(ProjArgs A)   // W consum
                     part[6 * R + r] = q.p1;
                     part[8 * R + r] = q.p3;
                 }
+                if (MODE == MODE_JVP) {   // the compensated JVP sum kept as its pair
+                    part[4 * R + r] = q.ds;
+                    part[5 * R + r] = q.dg;
+                    part[6 * R + r] = q.dgc;
+                }
                 if (PAIRED) part[7 * R + r] = q.p2;
             }
         }
     }
+}
+
+// Segmented standalone JVP: y and dy of every ray from its K phase-A segment partials (fp64, in ray
+// order), then the sub-ray weighting and the sinogram stores (duplicate angle-banks too).  Block
+// (t, m): traced angle-bank t of member m.
+__global__ void __launch_bounds__(256) jvp_combine_kernel(ProjArgs A, const int32_t* __restrict__ tabs, int ntab)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    float* ry = reinterpret_cast<float*>(smem);          // [R]
+    float* rdy = ry + A.R;                                // [R]
+    const int t = blockIdx.x, m = blockIdx.y;
+    const int R = A.R, J = A.J, K = A.K;
+    const int ab = tabs[t];
+    const int dir = A.rays[static_cast<size_t>(ab) * R].dV > 0 ? 1 : -1;
+    const float* part0 = A.segp + static_cast<size_t>((m * ntab + t) * K) * kSegFields * R;
+    for (int r = threadIdx.x; r < R; r += blockDim.x) {
+        double L = 0.0, dL = 0.0, y = 0.0, dy = 0.0;
+        for (int q = 0; q < K; ++q) {
+            const float* pq = part0 + static_cast<size_t>(dir > 0 ? K - 1 - q : q) * kSegFields * R;
+            const double e = exp2(L);
+            const double gq = static_cast<double>(pq[2 * R + r]) - pq[3 * R + r];
+            const double dgq = static_cast<double>(pq[5 * R + r]) - pq[6 * R + r];
+            y += e * gq;
+            dy += e * (dgq - dL * gq);
+            L += static_cast<double>(pq[0 * R + r]) - pq[1 * R + r];
+            dL += pq[4 * R + r];
+        }
+        ry[r] = static_cast<float>(A.delta * y);
+        rdy[r] = static_cast<float>(A.delta * dy);
+    }
+    __syncthreads();
+    const size_t obase = (static_cast<size_t>(m) * A.n_ab + ab) * A.n_det;
+    const size_t obase2 = (static_cast<size_t>(m) * A.n_ab + dup_of(A, ab)) * A.n_det;
+    for (int d = threadIdx.x; d < A.n_det; d += blockDim.x) {
+        float acc = 0.f, dacc = 0.f;
+        for (int j = 0; j < J; ++j) {
+            acc = fmaf(A.w[j], ry[d * J + j], acc);
+            dacc = fmaf(A.w[j], rdy[d * J + j], dacc);
+        }
+        if (A.y) A.y[obase + d] = acc;
+        A.dy[obase + d] = dacc;
+        if (A.dup_half) {
+            if (A.y) A.y[obase2 + d] = acc;
+            A.dy[obase2 + d] = dacc;
+        }
+    }
+}
+
+cudaError_t launch_jvp_combine(const ProjArgs& A, const int32_t* tabs, int ntab, int B, cudaStream_t s)
+{
+    jvp_combine_kernel<<<dim3(ntab, B), 256, 2 * A.R * sizeof(float), s>>>(A, tabs, ntab);
+    return cudaGetLastError();
 }
 
 // Phase B: per-ray constants from the K partials, then sweep B of the unit (comb groups) into the
@@ -1915,6 +1972,11 @@ cudaError_t launch_seg(int phase, int mode, int maxg, bool paired, const ProjArg
                        size_t smem, cudaStream_t s)
 {
     if (maxg != 1 && maxg != 2) return cudaErrorInvalidValue;
+    if (mode == MODE_JVP && phase == 0) {   // the standalone JVP: phase A only, unpaired
+        if (maxg == 1) seg_a_kernel<MODE_JVP, 1, false><<<grid, block, smem, s>>>(A);
+        else seg_a_kernel<MODE_JVP, 2, false><<<grid, block, smem, s>>>(A);
+        return cudaGetLastError();
+    }
     if (mode == MODE_VJP) return launch_seg_mode<MODE_VJP>(phase, maxg, paired, A, grid, block, smem, s);
     if (mode == MODE_GN) return launch_seg_mode<MODE_GN>(phase, maxg, paired, A, grid, block, smem, s);
     return cudaErrorInvalidValue;
@@ -1940,6 +2002,12 @@ static cudaError_t seg_attr_mode(int phase, size_t smem)
 
 cudaError_t set_seg_smem_limit(int phase, int mode, size_t smem)
 {
+    if (mode == MODE_JVP) {
+        const int v = static_cast<int>(smem);
+        cudaError_t e = cudaFuncSetAttribute(seg_a_kernel<MODE_JVP, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
+        if (e) return e;
+        return cudaFuncSetAttribute(seg_a_kernel<MODE_JVP, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
+    }
     if (mode == MODE_VJP) return seg_attr_mode<MODE_VJP>(phase, smem);
     if (mode == MODE_GN) return seg_attr_mode<MODE_GN>(phase, smem);
     return cudaErrorInvalidValue;

@@ -199,9 +199,9 @@ void build_schedule(const Geometry& g, int kind, int C, Schedule* S)
 // fixed per-unit overhead; units are assigned longest-first to the least-loaded CTA, separately for
 // phase A (CA CTAs) and phase B (C CTAs), and listed per CTA in (member, class, angle-bank, segment)
 // order so that consecutive units of one (member, class) share a partial slot (<= kSlotTasks).
-void build_adj_schedule(const Geometry& g, const std::vector<RayP>& rays, int CA, int C, Schedule* S)
+void build_adj_schedule(const Geometry& g, const std::vector<RayP>& rays, int CA, int C, Schedule* S, bool unpaired)
 {
-    const bool paired = g.dup;
+    const bool paired = g.dup && !unpaired;   // unpaired: the standalone JVP (every traced angle-bank)
     const std::vector<int32_t>& list = paired ? g.task_ab_p : g.task_ab;
     const int B = g.desc.batch, R = g.R;
     const int ntab = static_cast<int>(list.size());
