@@ -273,7 +273,8 @@ pget_status run_proj(const Geometry& g, int mode, const ProjCfg& c, const ProjAr
 }
 
 // the segmented adjoint: phase A then phase B on s, bracketed together by the profiler's events
-pget_status run_seg(const Geometry& g, int mode, ProjArgs A, float* segp, cudaStream_t s, float4* cache = nullptr)
+pget_status run_seg(const Geometry& g, int mode, ProjArgs A, float* segp, cudaStream_t s, float4* cache = nullptr,
+                    bool have_a = false)
 {
     const Schedule& S = g.sch[kSchedAdj];
     const SegCfg c = seg_cfg(g);
@@ -308,7 +309,9 @@ pget_status run_seg(const Geometry& g, int mode, ProjArgs A, float* segp, cudaSt
     A.RbA = c.RbA;
     A.passesA = c.passesA;
     A.stage_bytes = c.stageA;
-    cudaError_t e = launch_seg(0, mode, c.maxgA, g.dup, A, c.gridA, (c.WA + 1) * 32, c.smemA, s);
+    // have_a: segp already holds this u's VJP-mode phase-A partials (the segmented forward of the same
+    // u wrote them), so only phase B runs
+    cudaError_t e = have_a ? cudaSuccess : launch_seg(0, mode, c.maxgA, g.dup, A, c.gridA, (c.WA + 1) * 32, c.smemA, s);
     if (e == cudaSuccess) {
         A.units = S.d_unitsB;
         A.u_begin = S.d_ub_begin;
@@ -490,6 +493,8 @@ void free_device_tables(Geometry* g)
         S.d_unitsA = nullptr; S.d_ua_begin = S.d_sa_begin = S.d_seg_rows = nullptr; S.d_stA = nullptr;
         cudaFree(g->d_tabsJ);
         g->d_tabsJ = nullptr;
+        cudaFree(g->d_tabsA);
+        g->d_tabsA = nullptr;
         S.d_unitsA = S.d_unitsB = nullptr;
         S.d_ua_begin = S.d_ub_begin = S.d_sa_begin = S.d_sb_begin = S.d_seg_rows = nullptr;
         S.d_stA = S.d_stB = nullptr;
@@ -552,6 +557,7 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     if (e == cudaSuccess) e = cudaMalloc(&g.d_rays, rays.size() * sizeof(RayP));
     if (const char* ev = std::getenv("PGET_ADJ_FUSED")) g.adj_seg = std::atoi(ev) == 0;   // A/B experiments
     if (const char* ev = std::getenv("PGET_JVP_FUSED")) g.jvp_seg = std::atoi(ev) == 0;
+    if (const char* ev = std::getenv("PGET_FWD_FUSED")) g.fwd_seg = std::atoi(ev) == 0;
     if (const char* ev = std::getenv("PGET_GN_CACHE_MAX_GB")) g.cache_max_gb = std::atof(ev);
     if (const char* ev = std::getenv("PGET_GN_CACHE")) {   // 0: recompute, 1: hybrid, 2: fully cached
         const int v = std::atoi(ev);
@@ -605,6 +611,12 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
         up(&S.d_sa_begin, S.sa_begin);
         up(&S.d_seg_rows, S.seg_rows);
         up(&g.d_tabsJ, g.task_ab);
+    }
+    if (g.adj_seg && e == cudaSuccess) {   // traced angle-banks of the adjoint schedule (segmented forward)
+        const std::vector<int32_t>& lst = g.dup ? g.task_ab_p : g.task_ab;
+        e = cudaMalloc(&g.d_tabsA, std::max<size_t>(1, lst.size()) * sizeof(int32_t));
+        if (e == cudaSuccess && !lst.empty())
+            e = cudaMemcpy(g.d_tabsA, lst.data(), lst.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
     }
     if (e == cudaSuccess) e = cudaMalloc(&g.d_w, g.wf.size() * sizeof(float));
     if (e == cudaSuccess) e = cudaMemcpy(g.d_rays, rays.data(), rays.size() * sizeof(RayP), cudaMemcpyHostToDevice);
@@ -750,14 +762,14 @@ static pget_status proj_out(const Geometry& g, const WS& w, int mode, float* y, 
 
 // adjoint projector into w.gacc (MODE_VJP with weights win, or MODE_GN), then the fixed-order reduction
 static pget_status proj_adjoint(const Geometry& g, const WS& w, int mode, const float* win, cudaStream_t s,
-                                bool build_cache = false)
+                                bool build_cache = false, bool have_a = false)
 {
     const ProjCfg c = proj_cfg(g, mode);
     ProjArgs A = base_args(g, c);
     for (int k = 0; k < 2; ++k) { A.img2[k] = w.img2[k]; A.img4[k] = w.img4[k]; }
     A.slots = w.slots;
     A.win = win;
-    pget_status st = g.adj_seg ? run_seg(g, mode, A, w.segp, s, build_cache ? w.cache : nullptr)
+    pget_status st = g.adj_seg ? run_seg(g, mode, A, w.segp, s, build_cache ? w.cache : nullptr, have_a)
                                : run_proj(g, mode, c, A, s);
     if (st) return st;
     const int N = g.desc.n_px;
@@ -867,6 +879,48 @@ static pget_status gnc_product(const Geometry& g, const WS& w, const float* lam,
     return PGET_OK;
 }
 
+// the forward of the packed u in w.img2: segmented (the VJP-mode phase A of the adjoint schedule +
+// fp64 combine) when enabled, else the fused projector.  Used for the LM wrap's F(u), whose phase-A
+// partials the gradient VJP then reuses, and its trial forward; the standalone forward stays fused
+// (measured faster alone on configs 2, 3 and 5)
+static pget_status fwd_out(const Geometry& g, const WS& w, float* y, cudaStream_t s)
+{
+    if (!(g.adj_seg && g.fwd_seg)) return proj_out(g, w, MODE_FWD, y, nullptr, s);
+    const Schedule& S = g.sch[kSchedAdj];
+    const SegCfg c = seg_cfg(g);
+    ProjArgs A = base_args(g, proj_cfg(g, MODE_VJP));
+    for (int k = 0; k < 2; ++k) { A.img2[k] = w.img2[k]; A.img4[k] = w.img4[k]; }
+    A.y = y;
+    A.segp = w.segp;
+    A.K = S.K;
+    A.seg_rows = S.d_seg_rows;
+    A.units = S.d_unitsA;
+    A.u_begin = S.d_ua_begin;
+    A.stages = S.d_stA;
+    A.s_begin = S.d_sa_begin;
+    A.RbA = c.RbA;
+    A.passesA = c.passesA;
+    A.stage_bytes = c.stageA;
+    cudaEvent_t ea = nullptr, eb = nullptr;
+    if (g_prof.on.load(std::memory_order_relaxed)) {
+        std::lock_guard<std::mutex> lk(g_prof.mu);
+        g_prof.total += 2;
+        g_prof.mode_launches[MODE_FWD]++;
+        if (g_prof.used + 2 <= g_prof.pool.size()) {
+            ea = g_prof.pool[g_prof.used++];
+            eb = g_prof.pool[g_prof.used++];
+            g_prof.recs.push_back({MODE_FWD, ea, eb});
+        }
+    }
+    if (ea) cudaEventRecord(ea, s);
+    cudaError_t e = launch_seg(0, MODE_VJP, c.maxgA, g.dup, A, c.gridA, (c.WA + 1) * 32, c.smemA, s);
+    const int ntab = static_cast<int>((g.dup ? g.task_ab_p : g.task_ab).size());
+    if (e == cudaSuccess) e = launch_fwd_combine(g.dup, A, g.d_tabsA, ntab, g.desc.batch, s);
+    if (eb) cudaEventRecord(eb, s);
+    if (e != cudaSuccess) return cuda_fail(e, "segmented forward launch");
+    return PGET_OK;
+}
+
 // the standalone JVP of the packed (u, d) in w.img4: segmented (phase A over every traced angle-bank
 // + fp64 combine) when enabled, else the fused projector
 static pget_status jvp_out(const Geometry& g, const WS& w, float* y, float* dy, cudaStream_t s)
@@ -917,7 +971,7 @@ pget_status pget_forward(pget_geometry h, const float* lam, const float* mu, flo
     const Geometry& g = h->g;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if ((st = pack2(g, w, lam, mu, nullptr, nullptr, nullptr, nullptr, s))) return st;
-    return proj_out(g, w, MODE_FWD, y, nullptr, s);
+    return proj_out(g, w, MODE_FWD, y, nullptr, s);   // fused: faster standalone on configs 2, 3, 5
 }
 
 pget_status pget_jvp(pget_geometry h, const float* lam, const float* mu, const float* dlam, const float* dmu,
@@ -1013,14 +1067,15 @@ static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const f
 
     // 1-2: r = F(u) - y, 1/2||r||^2, ||Lu||^2   (u packed once for the whole iteration)
     if ((st = pack2(g, w, lam, mu, nullptr, nullptr, nullptr, nullptr, s))) return st;
-    if ((st = proj_out(g, w, MODE_FWD, w.ysino, nullptr, s))) return st;
+    if ((st = fwd_out(g, w, w.ysino, s))) return st;
     residual_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, y_meas, P[0], nsper); note();
     regsq_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, P[1], N); note();
     CK(cudaGetLastError());
     // 3: b = -(J^T r + alpha L^T L u); z = p = b; s = 0; ||b||^2
     const bool cached = g.adj_seg && g.gn_cached;
     // the gradient VJP also writes the GN Jacobian-entry cache (fused cache build)
-    if ((st = proj_adjoint(g, w, MODE_VJP, w.ysino, s, cached && n_cg > 0))) return st;
+    // F(u) above was the segmented forward: its phase-A partials of u are the VJP's phase A
+    if ((st = proj_adjoint(g, w, MODE_VJP, w.ysino, s, cached && n_cg > 0, g.adj_seg && g.fwd_seg))) return st;
     finish_kernel<<<vg, kVecThreads, 0, s>>>(w.gacc, Gv, lam, mu, alpha, 0.f, -1.f, w.bl, w.bm, w.bl, w.bm, P[2], w.zl,
                                             w.zm, w.pl, w.pm, s_lam, s_mu, N); note();
     CK(cudaGetLastError());
@@ -1091,7 +1146,7 @@ static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const f
     // 7-8: f(u+s), rho, accept, beta_next
     if (flags & PGET_GN_EVAL_TRIAL) {
         if ((st = pack2(g, w, lam, mu, s_lam, s_mu, w.ul, w.um, s, box))) return st;
-        if ((st = proj_out(g, w, MODE_FWD, w.ysino, nullptr, s))) return st;
+        if ((st = fwd_out(g, w, w.ysino, s))) return st;
         residual_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, y_meas, P[0], nsper); note();
         regsq_kernel<<<vg, kVecThreads, 0, s>>>(w.ul, w.um, P[1], N); note();
         scalar_kernel<<<sgrid, 128, 0, s>>>(SC_TRIAL, 0, P[0], P[1], nullptr, kNblk, w.cg, stats, B, alpha, beta, betav); note();

@@ -171,6 +171,8 @@ struct Geometry {
     Schedule schJ;
     bool jvp_seg = true;
     int32_t* d_tabsJ = nullptr;   // [ntab] traced angle-banks of schJ (task_ab)
+    bool fwd_seg = true;          // forward as the segmented VJP-mode phase A + combine
+    int32_t* d_tabsA = nullptr;   // traced angle-banks of the adjoint schedule (task_ab_p or task_ab)
     bool adj_seg = true;   // adjoint (VJP / GN) as the segmented two-phase projector (else the fused one)
     double cache_max_gb = 8.0;   // larger caches fall back to the recomputing GN product
     bool gn_hybrid = true;   // cached scatter with the recomputed (J p) (PGET_GN_CACHE=1)

@@ -112,6 +112,7 @@ cudaError_t set_seg_smem_limit(int phase, int mode, size_t smem);
 cudaError_t launch_gnc(int phase, bool paired, const ProjArgs& A, int grid, int block, size_t smem, cudaStream_t s);
 cudaError_t set_gnc_smem_limit(size_t smem);
 cudaError_t launch_jvp_combine(const ProjArgs& A, const int32_t* tabs, int ntab, int B, cudaStream_t s);
+cudaError_t launch_fwd_combine(bool paired, const ProjArgs& A, const int32_t* tabs, int ntab, int B, cudaStream_t s);
 cudaError_t launch_jsq(bool paired, const ProjArgs& A, double* sq, int grid, int block, size_t smem, cudaStream_t s);
 cudaError_t launch_jsq_member(const double* sq, int ntab, int B, int nblk, double* partial, cudaStream_t s);
 int proj_warps(int mode);

@@ -968,6 +968,58 @@ __global__ void __launch_bounds__(256) jvp_combine_kernel(ProjArgs A, const int3
     }
 }
 
+// Segmented forward: y of both banks of every line from the VJP-mode phase-A partials of the
+// (paired when possible) adjoint schedule: bank 0 G = sum_q 2^{L_q} G_q; bank 1 (the same line
+// walked from the other end) e^{-S} sum_q 2^{-L_q} p2_q; duplicate angle-banks too.
+template <bool PAIRED>
+__global__ void __launch_bounds__(256) fwd_combine_kernel(ProjArgs A, const int32_t* __restrict__ tabs, int ntab)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    float* ry = reinterpret_cast<float*>(smem);   // [2R]
+    const int t = blockIdx.x, m = blockIdx.y;
+    const int R = A.R, J = A.J, K = A.K;
+    const int ab = tabs[t];
+    const int dir = A.rays[static_cast<size_t>(ab) * R].dV > 0 ? 1 : -1;
+    const float* part0 = A.segp + static_cast<size_t>((m * ntab + t) * K) * kSegFields * R;
+    for (int r = threadIdx.x; r < R; r += blockDim.x) {
+        double L = 0.0, y = 0.0, p2 = 0.0;
+        for (int q = 0; q < K; ++q) {
+            const float* pq = part0 + static_cast<size_t>(dir > 0 ? K - 1 - q : q) * kSegFields * R;
+            y += exp2(L) * (static_cast<double>(pq[2 * R + r]) - pq[3 * R + r]);
+            if (PAIRED) p2 += exp2(-L) * pq[7 * R + r];
+            L += static_cast<double>(pq[0 * R + r]) - pq[1 * R + r];
+        }
+        ry[r] = static_cast<float>(A.delta * y);
+        if (PAIRED) ry[R + r] = static_cast<float>(A.delta * exp2(L) * p2);
+    }
+    __syncthreads();
+    const size_t obase = (static_cast<size_t>(m) * A.n_ab + ab) * A.n_det;
+    const size_t obase2 = (static_cast<size_t>(m) * A.n_ab + dup_of(A, ab)) * A.n_det;
+    const size_t pbase = (static_cast<size_t>(m) * A.n_ab + ab + 1) * A.n_det;
+    const size_t pbase2 = (static_cast<size_t>(m) * A.n_ab + dup_of(A, ab + 1)) * A.n_det;
+    for (int d = threadIdx.x; d < A.n_det; d += blockDim.x) {
+        float acc = 0.f, acc1 = 0.f;
+        for (int j = 0; j < J; ++j) {
+            acc = fmaf(A.w[j], ry[d * J + j], acc);
+            if (PAIRED) acc1 = fmaf(A.w[j], ry[R + d * J + j], acc1);
+        }
+        A.y[obase + d] = acc;
+        if (A.dup_half) A.y[obase2 + d] = acc;
+        if (PAIRED) {   // bank 1, detector n-1-d
+            const int dd = A.n_det - 1 - d;
+            A.y[pbase + dd] = acc1;
+            A.y[pbase2 + dd] = acc1;
+        }
+    }
+}
+
+cudaError_t launch_fwd_combine(bool paired, const ProjArgs& A, const int32_t* tabs, int ntab, int B, cudaStream_t s)
+{
+    if (paired) fwd_combine_kernel<true><<<dim3(ntab, B), 256, 2 * A.R * sizeof(float), s>>>(A, tabs, ntab);
+    else fwd_combine_kernel<false><<<dim3(ntab, B), 256, 2 * A.R * sizeof(float), s>>>(A, tabs, ntab);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_jvp_combine(const ProjArgs& A, const int32_t* tabs, int ntab, int B, cudaStream_t s)
 {
     jvp_combine_kernel<<<dim3(ntab, B), 256, 2 * A.R * sizeof(float), s>>>(A, tabs, ntab);
