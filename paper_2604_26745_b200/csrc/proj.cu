@@ -366,6 +366,9 @@ struct RayB {   // per-ray constants of sweep B
 // PAIRED adds the opposite-bank ray of the same line (its detector at the low-i end):
 //   E'_i = e^{-(S - A_i)},  a_lam += w'_r Delta E'_i,  a_mu += -w'_r Delta^2 (Q'_i + lam_i E'_i / 2),
 //   Q'_i = sum_{k>i} lam_k E'_k  (samples farther from that detector, already visited).
+#ifndef PGET_PF_DIST
+#define PGET_PF_DIST 8   // samples between a cache entry's L2 prefetch and its use (4: +4 %, 16: +0.6 %, 32: +3 %, none: +3 % LM; scripts/pf_exp.sh)
+#endif
 #ifndef PGET_SCATTER
 #define PGET_SCATTER 1
 #endif
@@ -1464,7 +1467,7 @@ __device__ __forceinline__ void walk_jvpc(const float2* __restrict__ img, int P,
         const float2 d = bilerp2(q00, q01, q10, q11, fu, fv);
         acc = fmaf(d.x, c.x, fmaf(d.y, c.y, acc));
         acc1 = fmaf(d.x, c.z, fmaf(d.y, c.w, acc1));
-        pf_entry(cl, k + 16, kend);
+        pf_entry(cl, k + PGET_PF_DIST, kend);
         c = ld_entry(cl, k + 4, kend);
         ++k;
         i = i2;
@@ -1509,7 +1512,7 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
         const int iv2 = hi32(v2);
         const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;
         const float2 av = make_float2(fmaf(wr, c.x, wr1 * c.z), fmaf(wr, c.y, wr1 * c.w));
-        pf_entry(cl, k + 16, kend);
+        pf_entry(cl, k + PGET_PF_DIST, kend);
         c = ld_entry(cl, k + 4, kend);
         const float2 tv = __fmul2_rn(av, make_float2(fv, fv));         // row j0+1
         const float2 bv = __ffma2_rn(tv, make_float2(-1.f, -1.f), av); // row j0
