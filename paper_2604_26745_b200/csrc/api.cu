@@ -174,7 +174,7 @@ SegCfg seg_cfg(const Geometry& g)
         const size_t budget = std::min<size_t>(g.smem_optin, per_sm / g.segA_cps - 1024);
         int Rb = std::min(g.rbA_cap, g.P - 1);
         size_t SB = 0;
-        constexpr int kStagesA = 3;   // seg_a_kernel's kSegAStages
+        constexpr int kStagesA = kSegAStages;
         for (; Rb > 1; --Rb) {
             SB = align128(static_cast<size_t>(Rb + 1) * g.P * sizeof(float4));
             if (128 + kStagesA * SB <= budget) break;

@@ -46,7 +46,11 @@ struct ProjArgs {
     float* segp;            // [n_canon][kSegFields][R]
 };
 
-constexpr int kSegFields = 9;   // s, sc, g, gc, ds, dg, p1, p2, p3 (see seg_a_kernel)
+constexpr int kSegFields = 9;
+#ifndef PGET_SEGA_STAGES
+#define PGET_SEGA_STAGES 3
+#endif
+constexpr int kSegAStages = PGET_SEGA_STAGES;   // stage buffers of the warp-specialised phase A   // s, sc, g, gc, ds, dg, p1, p2, p3 (see seg_a_kernel)
 
 struct CGState {
     double zeta, a, bcg;

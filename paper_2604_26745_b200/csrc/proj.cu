@@ -826,7 +826,7 @@ __device__ void issue_seg_stage(const ProjArgs& A, int Rb, int64_t sidx, void* d
 // Warp-specialised pipeline: the last warp only issues the stage copies (kSegAStages buffers, a
 // "full" mbarrier per buffer completed by the copy's bytes, an "empty" mbarrier per buffer on which
 // every consumer warp arrives when done with it), so consumer warps never wait for one another.
-constexpr int kSegAStages = 3;
+
 
 template <int MODE, int MAXG, bool PAIRED>
 __global__ void __launch_bounds__(512, 1) seg_a_kernel(ProjArgs A)   // W consumer warps + 1 producer warp
