@@ -158,6 +158,8 @@ struct SegCfg {
     int WA, maxgA, passesA, RbA, gridA, stageA;
     size_t smemA;
     int WB, passesB, RbB, gridB, stageB, off_wacc, off_rout, off_gsh, off_rsc, off_q1;
+    int RbG, off_waccG, off_routG;   // gnb_kernel: no stage buffers, so taller bands
+    size_t smemG;
     size_t smemB;
 };
 
@@ -212,6 +214,19 @@ SegCfg seg_cfg(const Geometry& g)
         c.off_q1 = static_cast<int>(c.off_rsc + rsc_b);
         c.smemB = c.off_q1 + q1_b;
         c.gridB = S.C > 0 ? S.C : g.sm_count;
+        {
+            int Rbg = std::min(32, g.P - 1);
+            size_t wg = 0;
+            for (; Rbg > 1; --Rbg) {
+                wg = align128(static_cast<size_t>(c.WB) * (Rbg + 1) * g.P * sizeof(float2));
+                if (128 + wg + rout_b <= budget) break;
+            }
+            wg = align128(static_cast<size_t>(c.WB) * (Rbg + 1) * g.P * sizeof(float2));
+            c.RbG = g.gnb_tall ? Rbg : c.RbB;
+            c.off_waccG = g.gnb_tall ? 128 : c.off_wacc;
+            c.off_routG = g.gnb_tall ? static_cast<int>(128 + wg) : c.off_rout;
+            c.smemG = g.gnb_tall ? 128 + wg + rout_b : c.smemB;
+        }
     }
     return c;
 }
@@ -558,6 +573,8 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     if (const char* ev = std::getenv("PGET_ADJ_FUSED")) g.adj_seg = std::atoi(ev) == 0;   // A/B experiments
     if (const char* ev = std::getenv("PGET_JVP_FUSED")) g.jvp_seg = std::atoi(ev) == 0;
     if (const char* ev = std::getenv("PGET_FWD_FUSED")) g.fwd_seg = std::atoi(ev) == 0;
+    g.gnb_tall = g.P >= 200;   // measured: config 4 -3.6 % LM, config 2 +0.8 %
+    if (const char* ev = std::getenv("PGET_GNB_TALL")) g.gnb_tall = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_GN_CACHE_MAX_GB")) g.cache_max_gb = std::atof(ev);
     if (const char* ev = std::getenv("PGET_GN_CACHE")) {   // 0: recompute, 1: hybrid, 2: fully cached
         const int v = std::atoi(ev);
@@ -633,7 +650,7 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
             if (e == cudaSuccess) e = set_seg_smem_limit(0, mode, sc.smemA);
             if (e == cudaSuccess) e = set_seg_smem_limit(1, mode, sc.smemB);
         }
-        if (e == cudaSuccess) e = set_gnc_smem_limit(sc.smemB);
+        if (e == cudaSuccess) e = set_gnc_smem_limit(std::max(sc.smemB, sc.smemG));
         if (e == cudaSuccess && g.jvp_seg) e = set_seg_smem_limit(0, MODE_JVP, sc.smemA);
     }
     if (prev >= 0) cudaSetDevice(prev);
@@ -866,7 +883,13 @@ static pget_status gnc_product(const Geometry& g, const WS& w, const float* lam,
     } else {
         e = launch_gnc(1, g.dup, A, c.gridB, c.WB * 32, c.smemB, s);
     }
-    if (e == cudaSuccess) e = launch_gnc(2, g.dup, A, c.gridB, c.WB * 32, c.smemB, s);
+    if (e == cudaSuccess) {
+        ProjArgs Ag = A;
+        Ag.RbB = c.RbG;
+        Ag.off_wacc = c.off_waccG;
+        Ag.off_rout = c.off_routG;
+        e = launch_gnc(2, g.dup, Ag, c.gridB, c.WB * 32, c.smemG, s);
+    }
     if (eb) cudaEventRecord(eb, s);
     if (e != cudaSuccess) return cuda_fail(e, "cached GN launch");
     const ProjCfg pc = proj_cfg(g, MODE_GN);

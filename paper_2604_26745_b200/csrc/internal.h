@@ -174,6 +174,7 @@ struct Geometry {
     bool fwd_seg = true;          // forward as the segmented VJP-mode phase A + combine
     int32_t* d_tabsA = nullptr;   // traced angle-banks of the adjoint schedule (task_ab_p or task_ab)
     bool adj_seg = true;   // adjoint (VJP / GN) as the segmented two-phase projector (else the fused one)
+    bool gnb_tall = true;   // gnb_kernel with its own (taller) bands: no stage buffers to fit
     double cache_max_gb = 8.0;   // larger caches fall back to the recomputing GN product
     bool gn_hybrid = true;   // cached scatter with the recomputed (J p) (PGET_GN_CACHE=1)
     bool gn_cached = true;   // GN product from the per-LM-iteration Jacobian-entry cache (PGET_GN_CACHE=0: recompute)
