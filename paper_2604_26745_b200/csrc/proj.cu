@@ -930,7 +930,7 @@ __global__ void __launch_bounds__(512, 1) seg_a_kernel(ProjArgs A)   // W consum
 // (t, m): traced angle-bank t of member m.
 __global__ void __launch_bounds__(256) jvp_combine_kernel(ProjArgs A, const int32_t* __restrict__ tabs, int ntab)
 {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     float* ry = reinterpret_cast<float*>(smem);          // [R]
     float* rdy = ry + A.R;                                // [R]
     const int t = blockIdx.x, m = blockIdx.y;
@@ -977,7 +977,7 @@ __global__ void __launch_bounds__(256) jvp_combine_kernel(ProjArgs A, const int3
 template <bool PAIRED>
 __global__ void __launch_bounds__(256) fwd_combine_kernel(ProjArgs A, const int32_t* __restrict__ tabs, int ntab)
 {
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];
     float* ry = reinterpret_cast<float*>(smem);   // [2R]
     const int t = blockIdx.x, m = blockIdx.y;
     const int R = A.R, J = A.J, K = A.K;
