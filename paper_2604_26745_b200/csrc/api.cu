@@ -422,7 +422,8 @@ WS carve(const Geometry& g, int op, char* base)
                                                    g.R * sizeof(float)));
         if (g.adj_seg && g.gn_cached && op != PGET_OP_VJP) {
             const Schedule& S = g.sch[kSchedAdj];
-            w.cache = reinterpret_cast<float4*>(take(static_cast<size_t>(B) * S.cache_rows_member * 32 * sizeof(float4)));
+            w.cache = reinterpret_cast<float4*>(
+                take((static_cast<size_t>(B) * S.cache_rows_member + kCachePadRows) * 32 * sizeof(float4)));
             w.jp = reinterpret_cast<float*>(take(static_cast<size_t>(S.n_canon) * 2 * g.R * sizeof(float)));
         }
     }

@@ -47,6 +47,9 @@ struct ProjArgs {
 };
 
 constexpr int kSegFields = 9;
+// rows of 32 entries allocated past the end of the GN coefficient cache: gnb_kernel's entry ring and
+// L2 prefetch read ahead of a lane's last sample without bounds checks (the values are never used)
+constexpr int kCachePadRows = 16;
 #ifndef PGET_SEGA_STAGES
 #define PGET_SEGA_STAGES 3
 #endif

@@ -1483,10 +1483,13 @@ __device__ __forceinline__ void walk_jvpc(const float2* __restrict__ img, int P,
     }
 }
 
-// gnb walk: scatter w_r (alpha, beta) + w'_r (alpha', beta') of the band's samples (same-cell registers)
+// gnb walk: scatter w_r (alpha, beta) + w'_r (alpha', beta') of the band's samples (same-cell registers).
+// ck points at the lane's next entry; the ring reads up to 4 rows and the prefetch PGET_PF_DIST rows
+// past it unchecked (kCachePadRows rows are allocated past the cache).
+static_assert(PGET_PF_DIST + 4 <= kCachePadRows, "cache read-ahead exceeds the padding");
 __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0, int r1, int abase, int sP, int ilo,
                                          int64_t dU, int64_t dV, float wr, float wr1, int& i, int64_t& u, int64_t& v,
-                                         const float4* __restrict__ cl, int& k, int kend)
+                                         const float4*& ck, const float4* cend)
 {
     const int iv0 = hi32(v);
     if (i < ilo || iv0 < r0 || iv0 >= r1) return;
@@ -1500,20 +1503,21 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
         pa[sP] = make_float2(t10.x + c.x, t10.y + c.y);
         pa[sP + 1] = make_float2(t11.x + d.x, t11.y + d.y);
     };
-    float4 c0 = ld_entry(cl, k, kend), c1 = ld_entry(cl, k + 1, kend), c2 = ld_entry(cl, k + 2, kend),
-           c3 = ld_entry(cl, k + 3, kend);
+    const float4* p = ck;
+    float4 c0 = __ldg(p), c1 = __ldg(p + 32), c2 = __ldg(p + 64), c3 = __ldg(p + 96);
     int iv = iv0;
     auto step = [&](float4& c) -> bool {
         const int aoff = abase + (iv - r0) * sP + hi32(u);
-        PGET_CHECK(hi32(u) >= 0 && hi32(u) + 1 < P && iv >= r0 && iv < r1 && k < kend);
+        PGET_CHECK(hi32(u) >= 0 && hi32(u) + 1 < P && iv >= r0 && iv < r1 && p < cend);
         const float fu = frac23(u), fv = frac23(v);
         const int i2 = i - 1;
         const int64_t u2 = u - dU, v2 = v - dV;
         const int iv2 = hi32(v2);
         const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;
         const float2 av = make_float2(fmaf(wr, c.x, wr1 * c.z), fmaf(wr, c.y, wr1 * c.w));
-        pf_entry(cl, k + PGET_PF_DIST, kend);
-        c = ld_entry(cl, k + 4, kend);
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(p + PGET_PF_DIST * 32));
+        c = __ldg(p + 4 * 32);
+        p += 32;
         const float2 tv = __fmul2_rn(av, make_float2(fv, fv));         // row j0+1
         const float2 bv = __ffma2_rn(tv, make_float2(-1.f, -1.f), av); // row j0
         const float2 c11 = __fmul2_rn(tv, make_float2(fu, fu));
@@ -1521,7 +1525,7 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
         const float2 c01 = __fmul2_rn(bv, make_float2(fu, fu));
         const float2 c00 = __ffma2_rn(c01, make_float2(-1.f, -1.f), bv);
         if (aoff != poff) {
-            if (poff >= 0) rmw(poff, p00, p01, p10, p11);
+            if (poff >= 0 && (PGET_ABLATE != 1 || p00.x == 12345.f)) rmw(poff, p00, p01, p10, p11);   // ABLATE 1: no scatter
             poff = aoff;
             p00 = c00; p01 = c01; p10 = c10; p11 = c11;
         } else {
@@ -1530,7 +1534,6 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
             p10.x += c10.x; p10.y += c10.y;
             p11.x += c11.x; p11.y += c11.y;
         }
-        ++k;
         i = i2;
         u = u2;
         v = v2;
@@ -1540,6 +1543,7 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
     while (step(c0) && step(c1) && step(c2) && step(c3)) {
     }
     rmw(poff, p00, p01, p10, p11);
+    ck = p;
 }
 
 // per-unit lane setup shared by the three kernels: the lane's ray of comb group grp, its entry
@@ -1744,7 +1748,7 @@ __global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
         };
         for (int pass = 0; pass < A.passesB; ++pass) {
             const int grp = pass * W + warp;
-            int r, ii, ilo, k = 0, kend = 0;
+            int r, ii, ilo, kend = 0;
             int64_t uu, vv;
             float wr = 0.f, wr1 = 0.f;
             const float4* cl = nullptr;
@@ -1760,12 +1764,14 @@ __global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
                 wr1 = A.w[j] * wd1;
                 cl = cache_lane(A, ui, grp, lane, &kend);
             }
+            const float4* const cend = cl + static_cast<int64_t>(kend) * 32;
             for (int j = 0; j < ui.nb; ++j) {
                 int r0, r1;
                 seg_band(ui, j, Rb, r0, r1);
                 const bool flip = j & 1;
                 const int abase = flip ? Rb * P : 0, sP = flip ? -P : P;
-                walk_gnb(wacc, P, r0, r1, abase, sP, ilo, dU, dV, wr, wr1, ii, uu, vv, cl, k, kend);
+                if (PGET_ABLATE != 3)   // 3: no walk
+                    walk_gnb(wacc, P, r0, r1, abase, sP, ilo, dU, dV, wr, wr1, ii, uu, vv, cl, cend);
                 __syncthreads();   // every warp ring complete
                 const bool last = j == ui.nb - 1;
                 const int carry = last ? -1 : (ui.dir > 0 ? r0 : r1);
@@ -1782,7 +1788,7 @@ __global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
                     int rw = __float2int_rd(static_cast<float>(e) * inv_np);
                     int q = e - rw * npairs;
                     if (q < 0) { --rw; q += npairs; } else if (q >= npairs) { ++rw; q -= npairs; }
-                    if (rw == carry || q < qlo || q > qhi) continue;
+                    if (rw == carry || q < qlo || q > qhi || PGET_ABLATE == 2) continue;   // 2: no flush
                     const int lr = flip ? r0 + Rb - rw : rw - r0;
                     PGET_CHECK(lr >= 0 && lr < RB1);
                     float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
