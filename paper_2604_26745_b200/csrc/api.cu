@@ -856,11 +856,14 @@ static pget_status gnc_product(const Geometry& g, const WS& w, const float* lam,
     if (st) return st;
     const SegCfg c = seg_cfg(g);
     ProjArgs A = gnc_args(g, w);
-    if (g.gn_hybrid) A.jp = nullptr;
+    if (g.gn_hybrid) {   // the per-ray scatter weights into w.jp's space (unused by the hybrid product)
+        A.jp = nullptr;
+        A.gw = w.jp;
+    }
     cudaEvent_t ea = nullptr, eb = nullptr;
     if (g_prof.on.load(std::memory_order_relaxed)) {
         std::lock_guard<std::mutex> lk(g_prof.mu);
-        g_prof.total += 2;
+        g_prof.total += g.gn_hybrid ? 3 : 2;   // phase A (+ gnw) + scatter
         g_prof.mode_launches[MODE_GN]++;
         if (g_prof.used + 2 <= g_prof.pool.size()) {
             ea = g_prof.pool[g_prof.used++];
@@ -881,6 +884,7 @@ static pget_status gnc_product(const Geometry& g, const WS& w, const float* lam,
         Aa.passesA = c.passesA;
         Aa.stage_bytes = c.stageA;
         e = launch_seg(0, MODE_GN, c.maxgA, g.dup, Aa, c.gridA, (c.WA + 1) * 32, c.smemA, s);
+        if (e == cudaSuccess) e = launch_gnw(g.dup, A, g.d_tabsA, S.ntab, g.desc.batch, s);
     } else {
         e = launch_gnc(1, g.dup, A, c.gridB, c.WB * 32, c.smemB, s);
     }

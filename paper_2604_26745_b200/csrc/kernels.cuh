@@ -44,6 +44,7 @@ struct ProjArgs {
     int ntab;
     float* jp;               // [n_canon][2][R] per-ray JVP partials of a segment (both directions)
     float* segp;            // [n_canon][kSegFields][R]
+    float* gw;              // [B * ntab][2][R] GN scatter weights (w_r, w'_r) of gnw_kernel, or null
 };
 
 constexpr int kSegFields = 9;
@@ -120,6 +121,7 @@ cudaError_t launch_gnc(int phase, bool paired, const ProjArgs& A, int grid, int 
 cudaError_t set_gnc_smem_limit(size_t smem);
 cudaError_t launch_jvp_combine(const ProjArgs& A, const int32_t* tabs, int ntab, int B, cudaStream_t s);
 cudaError_t launch_fwd_combine(bool paired, const ProjArgs& A, const int32_t* tabs, int ntab, int B, cudaStream_t s);
+cudaError_t launch_gnw(bool paired, const ProjArgs& A, const int32_t* tabs, int ntab, int B, cudaStream_t s);
 cudaError_t launch_jsq(bool paired, const ProjArgs& A, double* sq, int grid, int block, size_t smem, cudaStream_t s);
 cudaError_t launch_jsq_member(const double* sq, int ntab, int B, int nblk, double* partial, cudaStream_t s);
 int proj_warps(int mode);

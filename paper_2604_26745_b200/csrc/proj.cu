@@ -1328,10 +1328,10 @@ __device__ __forceinline__ void seg_constants(const ProjArgs& A, const UnitInfo&
 // whole-ray (J p) of both directions from the GN-mode phase-A segment partials (seg_b_kernel's GN
 // combination, in ray order)
 template <bool PAIRED>
-__device__ __forceinline__ void gn_rout_from_seg(const ProjArgs& A, const UnitInfo& ui, int r, float* rout)
+__device__ __forceinline__ void gn_rout_from_seg(const ProjArgs& A, int canon0, int dir, int r, float* rout)
 {
     const int R = A.R, K = A.K;
-    const float* part0 = A.segp + static_cast<size_t>(ui.canon - ui.seg) * kSegFields * R;
+    const float* part0 = A.segp + static_cast<size_t>(canon0) * kSegFields * R;
     double Lb[5], dLb[5], gq[4], p1q[4], p2q[4], p3q[4], dgq[4];
     Lb[0] = 0.0;
     dLb[0] = 0.0;
@@ -1340,7 +1340,7 @@ __device__ __forceinline__ void gn_rout_from_seg(const ProjArgs& A, const UnitIn
         gq[q] = p1q[q] = p2q[q] = p3q[q] = dgq[q] = 0.0;
         double sq = 0.0, dsq = 0.0;
         if (q < K) {
-            const float* pq = part0 + static_cast<size_t>(ui.dir > 0 ? K - 1 - q : q) * kSegFields * R;
+            const float* pq = part0 + static_cast<size_t>(dir > 0 ? K - 1 - q : q) * kSegFields * R;
             sq = static_cast<double>(pq[0 * R + r]) - pq[1 * R + r];
             gq[q] = static_cast<double>(pq[2 * R + r]) - pq[3 * R + r];
             if (PAIRED) p2q[q] = pq[7 * R + r];
@@ -1690,6 +1690,52 @@ __global__ void __launch_bounds__(512, 1) jvpc_kernel(ProjArgs A)
     }
 }
 
+// the scatter weights of ray r from the whole-ray (J p) of its angle-bank: w_r = w_j sum_j' w_j' (J p)_{d,j'}
+// (both directions; doubled for a duplicate-merged angle-bank)
+__device__ __forceinline__ void gn_weights(const ProjArgs& A, const float* rout, int r, float& wr, float& wr1)
+{
+    const int J = A.J, R = A.R;
+    const int d = r / J, j = r - d * J;
+    float wd = 0.f, wd1 = 0.f;
+    for (int jj = 0; jj < J; ++jj) {
+        wd = fmaf(A.w[jj], rout[d * J + jj], wd);
+        wd1 = fmaf(A.w[jj], rout[R + d * J + jj], wd1);
+    }
+    if (A.dup_half) { wd *= 2.f; wd1 *= 2.f; }
+    wr = A.w[j] * wd;
+    wr1 = A.w[j] * wd1;
+}
+
+// gnw_kernel: per CG step and (member, traced angle-bank), the whole-ray (J p) of the GN-mode phase-A
+// partials (once, instead of once per segment unit inside gnb_kernel) and the scatter weights, to A.gw
+template <bool PAIRED>
+__global__ void __launch_bounds__(256) gnw_kernel(ProjArgs A, const int32_t* __restrict__ tabs, int ntab)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
+    float* rout = reinterpret_cast<float*>(smem);   // [2R]
+    const int t = blockIdx.x, m = blockIdx.y;
+    const int R = A.R;
+    const int ab = tabs[t];
+    const int dir = A.rays[static_cast<size_t>(ab) * R].dV > 0 ? 1 : -1;
+    const int ct = m * ntab + t;
+    for (int r = threadIdx.x; r < R; r += blockDim.x) gn_rout_from_seg<PAIRED>(A, ct * A.K, dir, r, rout);
+    __syncthreads();
+    float* gw = A.gw + static_cast<size_t>(ct) * 2 * R;
+    for (int r = threadIdx.x; r < R; r += blockDim.x) {
+        float wr, wr1;
+        gn_weights(A, rout, r, wr, wr1);
+        gw[r] = wr;
+        gw[R + r] = wr1;
+    }
+}
+
+cudaError_t launch_gnw(bool paired, const ProjArgs& A, const int32_t* tabs, int ntab, int B, cudaStream_t s)
+{
+    if (paired) gnw_kernel<true><<<dim3(ntab, B), 256, 2 * A.R * sizeof(float), s>>>(A, tabs, ntab);
+    else gnw_kernel<false><<<dim3(ntab, B), 256, 2 * A.R * sizeof(float), s>>>(A, tabs, ntab);
+    return cudaGetLastError();
+}
+
 // gnb_kernel: per CG step, w_r from the (J p) partials, then the cached scatter into slots (as
 // seg_b_kernel; no image staging).
 template <bool PAIRED>
@@ -1703,7 +1749,7 @@ __global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int c = blockIdx.x;
     if (A.u_begin[c] == A.u_begin[c + 1]) return;
-    const int P = A.P, R = A.R, J = A.J, K = A.K, Rb = A.RbB;
+    const int P = A.P, R = A.R, K = A.K, Rb = A.RbB;
     const int RB1 = Rb + 1;
     float2* wacc = wacc_all + static_cast<size_t>(warp) * RB1 * P;
     {
@@ -1719,7 +1765,7 @@ __global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
         const RayP* rays = A.rays + static_cast<size_t>(ui.ab) * R;
         const int64_t dU = rays[0].dU, dV = rays[0].dV;
         const float* jp0 = A.jp ? A.jp + static_cast<size_t>(ui.canon - ui.seg) * 2 * R : nullptr;
-        for (int r = tid; r < R; r += NT) {   // whole-ray (J p)
+        for (int r = tid; r < R && !A.gw; r += NT) {   // whole-ray (J p) (gw: done by gnw_kernel)
             if (A.jp) {   // the K cached-entry partials of jvpc_kernel, in fixed order
                 float a = 0.f, a1 = 0.f;
                 for (int q = 0; q < K; ++q) {
@@ -1729,7 +1775,7 @@ __global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
                 rout[r] = a;
                 rout[R + r] = a1;
             } else {      // the GN-mode phase-A partials (recomputed JVP of p)
-                gn_rout_from_seg<PAIRED>(A, ui, r, rout);
+                gn_rout_from_seg<PAIRED>(A, ui.canon - ui.seg, ui.dir, r, rout);
             }
         }
         float2* slot = A.slots + static_cast<size_t>(ui.slot) * plane;
@@ -1753,15 +1799,13 @@ __global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
             float wr = 0.f, wr1 = 0.f;
             const float4* cl = nullptr;
             if (lane_ray(A, ui, rays, grp, lane, dU, dV, r, ii, ilo, uu, vv)) {
-                const int d = r / J, j = r - d * J;
-                float wd = 0.f, wd1 = 0.f;
-                for (int jj = 0; jj < J; ++jj) {
-                    wd = fmaf(A.w[jj], rout[d * J + jj], wd);
-                    wd1 = fmaf(A.w[jj], rout[R + d * J + jj], wd1);
+                if (A.gw) {
+                    const float* gw = A.gw + static_cast<size_t>((ui.canon - ui.seg) / K) * 2 * R;
+                    wr = gw[r];
+                    wr1 = gw[R + r];
+                } else {
+                    gn_weights(A, rout, r, wr, wr1);
                 }
-                if (A.dup_half) { wd *= 2.f; wd1 *= 2.f; }
-                wr = A.w[j] * wd;
-                wr1 = A.w[j] * wd1;
                 cl = cache_lane(A, ui, grp, lane, &kend);
             }
             const float4* const cend = cl + static_cast<int64_t>(kend) * 32;
@@ -1825,7 +1869,7 @@ __global__ void __launch_bounds__(512, 1) jsq_kernel(ProjArgs A, double* sq)
     for (int u = A.u_begin[c]; u < A.u_begin[c + 1]; ++u) {
         if (A.units[u].seg != 0) continue;
         const UnitInfo ui = unit_info(A, u, A.RbB);
-        for (int r = tid; r < R; r += NT) gn_rout_from_seg<PAIRED>(A, ui, r, rout);
+        for (int r = tid; r < R; r += NT) gn_rout_from_seg<PAIRED>(A, ui.canon - ui.seg, ui.dir, r, rout);
         __syncthreads();
         double acc = 0.0;
         for (int d = tid; d < A.n_det; d += NT) {
