@@ -226,6 +226,19 @@ SegCfg seg_cfg(const Geometry& g)
             c.off_waccG = g.gnb_tall ? 128 : c.off_wacc;
             c.off_routG = g.gnb_tall ? static_cast<int>(128 + wg) : c.off_rout;
             c.smemG = g.gnb_tall ? 128 + wg + rout_b : c.smemB;
+            if (g.gnb_int && g.gn_hybrid) {   // one shared accumulator: bands up to the whole padded image
+                int Rbi = g.P - 1;
+                size_t wi = 0;
+                for (; Rbi > 1; --Rbi) {
+                    wi = align128(static_cast<size_t>(Rbi + 1) * g.P * sizeof(int2));
+                    if (128 + wi + rout_b <= budget) break;
+                }
+                wi = align128(static_cast<size_t>(Rbi + 1) * g.P * sizeof(int2));
+                c.RbG = Rbi;
+                c.off_waccG = 128;
+                c.off_routG = static_cast<int>(128 + wi);
+                c.smemG = 128 + wi + rout_b;
+            }
         }
     }
     return c;
@@ -289,7 +302,7 @@ pget_status run_proj(const Geometry& g, int mode, const ProjCfg& c, const ProjAr
 
 // the segmented adjoint: phase A then phase B on s, bracketed together by the profiler's events
 pget_status run_seg(const Geometry& g, int mode, ProjArgs A, float* segp, cudaStream_t s, float4* cache = nullptr,
-                    bool have_a = false)
+                    bool have_a = false, float* gscale = nullptr)
 {
     const Schedule& S = g.sch[kSchedAdj];
     const SegCfg c = seg_cfg(g);
@@ -306,6 +319,8 @@ pget_status run_seg(const Geometry& g, int mode, ProjArgs A, float* segp, cudaSt
     }
     A.segp = segp;
     A.cache = cache;   // VJP: also write the GN Jacobian-entry cache (fused lin_kernel)
+    A.gscale = cache ? gscale : nullptr;
+    A.cellmax = g.cellmax;
     A.cache_off = S.d_cache_off;
     A.cache_rows_member = S.cache_rows_member;
     A.ntab = S.ntab;
@@ -380,6 +395,7 @@ struct WS {
     float* segpJ = nullptr;   // segmented standalone JVP: [n_canonJ][kSegFields][R]
     float4* cache = nullptr;  // GN with cached Jacobian entries: [B][rows][32]
     float* jp = nullptr;      // [n_canon][2][R] per-segment (J p) partials
+    float* gscale = nullptr;  // [B * ntab][8] fixed-point scale bounds (gnb_kernel INTACC)
     float *ysino = nullptr, *dysino = nullptr;
     float *bl = nullptr, *bm = nullptr, *zl = nullptr, *zm = nullptr, *pl = nullptr, *pm = nullptr;
     float *ql = nullptr, *qm = nullptr, *ul = nullptr, *um = nullptr;
@@ -425,6 +441,8 @@ WS carve(const Geometry& g, int op, char* base)
             w.cache = reinterpret_cast<float4*>(
                 take((static_cast<size_t>(B) * S.cache_rows_member + kCachePadRows) * 32 * sizeof(float4)));
             w.jp = reinterpret_cast<float*>(take(static_cast<size_t>(S.n_canon) * 2 * g.R * sizeof(float)));
+            if (g.gnb_int && g.gn_hybrid)
+                w.gscale = reinterpret_cast<float*>(take(static_cast<size_t>(B) * S.ntab * 8 * sizeof(float)));
         }
     }
     if ((op == PGET_OP_JVP || guard) && g.adj_seg && g.jvp_seg)
@@ -576,6 +594,7 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     if (const char* ev = std::getenv("PGET_FWD_FUSED")) g.fwd_seg = std::atoi(ev) == 0;
     g.gnb_tall = g.P >= 200;   // measured: config 4 -3.6 % LM, config 2 +0.8 %
     if (const char* ev = std::getenv("PGET_GNB_TALL")) g.gnb_tall = std::atoi(ev) != 0;
+    if (const char* ev = std::getenv("PGET_GNB_INT")) g.gnb_int = g.gnb_int && std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_GN_CACHE_MAX_GB")) g.cache_max_gb = std::atof(ev);
     if (const char* ev = std::getenv("PGET_GN_CACHE")) {   // 0: recompute, 1: hybrid, 2: fully cached
         const int v = std::atoi(ev);
@@ -787,7 +806,9 @@ static pget_status proj_adjoint(const Geometry& g, const WS& w, int mode, const 
     for (int k = 0; k < 2; ++k) { A.img2[k] = w.img2[k]; A.img4[k] = w.img4[k]; }
     A.slots = w.slots;
     A.win = win;
-    pget_status st = g.adj_seg ? run_seg(g, mode, A, w.segp, s, build_cache ? w.cache : nullptr, have_a)
+    if (build_cache && w.gscale)   // the builder's entry bounds start from 0 (atomicMax)
+        CK(cudaMemsetAsync(w.gscale, 0, static_cast<size_t>(g.desc.batch) * g.sch[kSchedAdj].ntab * 8 * sizeof(float), s));
+    pget_status st = g.adj_seg ? run_seg(g, mode, A, w.segp, s, build_cache ? w.cache : nullptr, have_a, w.gscale)
                                : run_proj(g, mode, c, A, s);
     if (st) return st;
     const int N = g.desc.n_px;
@@ -832,6 +853,8 @@ static ProjArgs gnc_args(const Geometry& g, const WS& w)
     A.cache_rows_member = S.cache_rows_member;
     A.ntab = S.ntab;
     A.jp = w.jp;
+    A.gscale = w.gscale;
+    A.cellmax = g.cellmax;
     return A;
 }
 
@@ -839,6 +862,7 @@ static ProjArgs gnc_args(const Geometry& g, const WS& w)
 static pget_status gnc_build(const Geometry& g, const WS& w, cudaStream_t s)
 {
     const SegCfg c = seg_cfg(g);
+    if (w.gscale) CK(cudaMemsetAsync(w.gscale, 0, static_cast<size_t>(g.desc.batch) * g.sch[kSchedAdj].ntab * 8 * sizeof(float), s));
     cudaError_t e = launch_gnc(0, g.dup, gnc_args(g, w), c.gridB, c.WB * 32, c.smemB, s);
     note();
     if (e != cudaSuccess) return cuda_fail(e, "lin_kernel launch");

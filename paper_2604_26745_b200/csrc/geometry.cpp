@@ -178,6 +178,12 @@ pget_status build_geometry(const pget_geometry_desc* d, Geometry* g, std::string
         if (S < 1) S = 1;
         if (S > g->R) S = g->R;
         g->comb_S = static_cast<int>(S);
+        // samples whose 2x2 bilinear support contains a given pixel: rays within the support's
+        // width (2 sqrt2 px) x samples of one ray inside it; consecutive samples in one cell
+        const double st = d->step_px;
+        const double n_near = (std::floor(2.0 * std::sqrt(2.0) / a) + 2.0) * (std::floor(2.0 * std::sqrt(2.0) / st) + 2.0);
+        g->cellmax = static_cast<int>(std::floor(std::sqrt(2.0) / st)) + 1;
+        g->gnb_int = n_near < 512.0 * g->cellmax;
     }
     return PGET_OK;
 }

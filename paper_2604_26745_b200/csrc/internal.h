@@ -175,6 +175,11 @@ struct Geometry {
     int32_t* d_tabsA = nullptr;   // traced angle-banks of the adjoint schedule (task_ab_p or task_ab)
     bool adj_seg = true;   // adjoint (VJP / GN) as the segmented two-phase projector (else the fused one)
     bool gnb_tall = true;   // gnb_kernel with its own (taller) bands: no stage buffers to fit
+    // gnb_kernel with one shared 32-bit fixed-point accumulator (native shared integer atomics):
+    // requires every pixel's per-unit sum below 2^31 at the scale that keeps a pending cell below
+    // 2^22, i.e. (samples near a pixel) / cellmax < 512 (geometry.cpp)
+    bool gnb_int = true;
+    int cellmax = 1;        // max consecutive samples of one ray inside one pixel cell
     double cache_max_gb = 8.0;   // larger caches fall back to the recomputing GN product
     bool gn_hybrid = true;   // cached scatter with the recomputed (J p) (PGET_GN_CACHE=1)
     bool gn_cached = true;   // GN product from the per-LM-iteration Jacobian-entry cache (PGET_GN_CACHE=0: recompute)

@@ -45,6 +45,8 @@ struct ProjArgs {
     float* jp;               // [n_canon][2][R] per-ray JVP partials of a segment (both directions)
     float* segp;            // [n_canon][kSegFields][R]
     float* gw;              // [B * ntab][2][R] GN scatter weights (w_r, w'_r) of gnw_kernel, or null
+    float* gscale;          // [B * ntab][8] fixed-point scale bounds of the cached scatter (null: float path)
+    int cellmax;            // max consecutive samples of a ray in one pixel cell
 };
 
 constexpr int kSegFields = 9;

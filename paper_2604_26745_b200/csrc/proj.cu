@@ -383,7 +383,8 @@ template <bool PAIRED, bool COMP, bool CACHE = false>
 __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* __restrict__ acc, int P, int r0,
                                        int r1, int abase, int sP, int ilo, int64_t dU, int64_t dV, float cf, float ch,
                                        const RayB& rb, int& i, int64_t& u, int64_t& v, StateB& st,
-                                       float wr = 0.f, float wr1 = 0.f, float4* cl = nullptr, int* kp = nullptr)
+                                       float wr = 0.f, float wr1 = 0.f, float4* cl = nullptr, int* kp = nullptr,
+                                       float2* emax = nullptr)
 {
     int iv = hi32(v), iu = hi32(u);
     if (i < ilo || iv < r0 || iv >= r1) return;
@@ -432,6 +433,8 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
             }
             __stcs(cl + static_cast<int64_t>(*kp) * 32, cv);
             ++*kp;
+            emax->x = fmaxf(emax->x, fmaxf(fabsf(cv.x), fabsf(cv.z)));   // magnitude bounds of the entries
+            emax->y = fmaxf(emax->y, fmaxf(fabsf(cv.y), fabsf(cv.w)));   // (gnb_kernel's fixed-point scale)
             al = fmaf(wr, cv.x, wr1 * cv.z);
             am = fmaf(wr, cv.y, wr1 * cv.w);
         } else if constexpr (PAIRED) {
@@ -1033,6 +1036,24 @@ cudaError_t launch_jvp_combine(const ProjArgs& A, const int32_t* tabs, int ntab,
 // unit's partial slot (zeroed by the slot's first unit; every flush adds).
 __device__ __forceinline__ float4* cache_lane(const ProjArgs& A, const UnitInfo& ui, int grp, int lane, int* kend);
 
+// the cache builders' magnitude bounds of the entries, per (member, traced angle-bank):
+// gscale[ct * 8 + 0] = max |alpha|, |alpha'|; [1] = max |beta|, |beta'| (float bits, atomicMax of
+// non-negative floats; zeroed before the build).  Warp-uniform call.
+__device__ __forceinline__ void entry_bounds(const ProjArgs& A, const UnitInfo& ui, float2 am)
+{
+    if (!A.gscale) return;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        am.x = fmaxf(am.x, __shfl_xor_sync(0xffffffffu, am.x, o));
+        am.y = fmaxf(am.y, __shfl_xor_sync(0xffffffffu, am.y, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+        int* gs = reinterpret_cast<int*>(A.gscale + static_cast<size_t>((ui.canon - ui.seg) / A.K) * 8);
+        atomicMax(gs, __float_as_int(am.x));
+        atomicMax(gs + 1, __float_as_int(am.y));
+    }
+}
+
 template <int MODE, bool PAIRED, bool CACHE>
 __global__ void __launch_bounds__(512, 1) seg_b_kernel(ProjArgs A)
 {
@@ -1171,6 +1192,7 @@ __global__ void __launch_bounds__(512, 1) seg_b_kernel(ProjArgs A)
             StateB st{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             float cw = 0.f, cw1 = 0.f;
             float4* cl = nullptr;
+            float2 am = make_float2(0.f, 0.f);
             if (r >= 0) {
                 const int d = r / J, j = r - d * J;
                 float wd = 0.f, wd1 = 0.f;
@@ -1219,7 +1241,7 @@ __global__ void __launch_bounds__(512, 1) seg_b_kernel(ProjArgs A)
                 const int abase = flip ? Rb * P : 0, sP = flip ? -P : P;
                 if (PGET_ABLATE != 3)   // 3: no sweep B walk at all
                     walk_b<PAIRED, ModeTraits<MODE>::COMP_S, CACHE>(sbuf, wacc, P, r0, r1, abase, sP, ilo, dU, dV, cf, ch,
-                                                                    rb, ii, uu, vv, st, cw, cw1, cl, &kc);
+                                                                    rb, ii, uu, vv, st, cw, cw1, cl, &kc, &am);
                 __syncthreads();   // stage buffer b and every warp ring consumed
                 if (tid == 0 && s + 2 < n_stages)
                     issue_seg_stage<false>(A, Rb, sb0 + s + 2, stage0 + b * A.stage_bytes, &mbar[b]);
@@ -1257,6 +1279,7 @@ __global__ void __launch_bounds__(512, 1) seg_b_kernel(ProjArgs A)
                 }
                 __syncthreads();   // rings zeroed before the next band's scatter
             }
+            if (CACHE) entry_bounds(A, ui, am);
         }
     }
 }
@@ -1377,7 +1400,7 @@ __device__ __forceinline__ void gn_rout_from_seg(const ProjArgs& A, int canon0, 
 template <bool PAIRED>
 __device__ __forceinline__ void walk_lin(const float2* __restrict__ img, int P, int r0, int r1, int ilo, int64_t dU,
                                          int64_t dV, float cf, float ch, const RayB& rb, int& i, int64_t& u,
-                                         int64_t& v, StateB& st, float4* cl, int& k)
+                                         int64_t& v, StateB& st, float4* cl, int& k, float2& am)
 {
     int iv = hi32(v), iu = hi32(u);
     if (i < ilo || iv < r0 || iv >= r1) return;
@@ -1416,6 +1439,8 @@ __device__ __forceinline__ void walk_lin(const float2* __restrict__ img, int P, 
         kahan(x_.q, x_.qc, le);
         kahan(x_.s, x_.sc, x.y * cf);
         __stcs(cl + static_cast<int64_t>(k) * 32, cv);   // streaming store: written once, read 2 x n_cg times
+        am.x = fmaxf(am.x, fmaxf(fabsf(cv.x), fabsf(cv.z)));
+        am.y = fmaxf(am.y, fmaxf(fabsf(cv.y), fabsf(cv.w)));
         ++k;
         i = i2;
         u = u2;
@@ -1486,22 +1511,48 @@ __device__ __forceinline__ void walk_jvpc(const float2* __restrict__ img, int P,
 // gnb walk: scatter w_r (alpha, beta) + w'_r (alpha', beta') of the band's samples (same-cell registers).
 // ck points at the lane's next entry; the ring reads up to 4 rows and the prefetch PGET_PF_DIST rows
 // past it unchecked (kCachePadRows rows are allocated past the cache).
+// INTACC: one block-shared accumulator of 32-bit fixed-point pairs, added to with native shared
+// integer atomics (red.shared.add.u32): a pending cell's four float2 sums are scaled by S (a power of
+// two, |value * S| < 2^22 by construction, see gnb_kernel), rounded to integers with the
+// 1.5 * 2^23 magic-number FFMA and added.  Integer addition is associative, so the result does not
+// depend on the order in which warps and lanes add.
 static_assert(PGET_PF_DIST + 4 <= kCachePadRows, "cache read-ahead exceeds the padding");
+__device__ __forceinline__ void red_s32(uint32_t addr, int v)
+{
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+template <bool INTACC>
 __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0, int r1, int abase, int sP, int ilo,
                                          int64_t dU, int64_t dV, float wr, float wr1, int& i, int64_t& u, int64_t& v,
-                                         const float4*& ck, const float4* cend)
+                                         const float4*& ck, const float4* cend, float2 S)
 {
     const int iv0 = hi32(v);
     if (i < ilo || iv0 < r0 || iv0 >= r1) return;
     int poff = -1;
     float2 p00 = make_float2(0.f, 0.f), p01 = p00, p10 = p00, p11 = p00;
+    const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(acc));
     auto rmw = [&](int off, float2 a, float2 b, float2 c, float2 d) {
-        float2* pa = acc + off;
-        const float2 t00 = pa[0], t01 = pa[1], t10 = pa[sP], t11 = pa[sP + 1];
-        pa[0] = make_float2(t00.x + a.x, t00.y + a.y);
-        pa[1] = make_float2(t01.x + b.x, t01.y + b.y);
-        pa[sP] = make_float2(t10.x + c.x, t10.y + c.y);
-        pa[sP + 1] = make_float2(t11.x + d.x, t11.y + d.y);
+        if constexpr (INTACC) {
+            const float2 mg = make_float2(12582912.f, 12582912.f);   // 1.5 * 2^23
+            const float2 ta = __ffma2_rn(a, S, mg), tb = __ffma2_rn(b, S, mg);
+            const float2 tc = __ffma2_rn(c, S, mg), td = __ffma2_rn(d, S, mg);
+            const uint32_t a0 = sbase + static_cast<uint32_t>(off * 8), a1 = sbase + static_cast<uint32_t>((off + sP) * 8);
+            red_s32(a0, __float_as_int(ta.x) - 0x4B400000);
+            red_s32(a0 + 4, __float_as_int(ta.y) - 0x4B400000);
+            red_s32(a0 + 8, __float_as_int(tb.x) - 0x4B400000);
+            red_s32(a0 + 12, __float_as_int(tb.y) - 0x4B400000);
+            red_s32(a1, __float_as_int(tc.x) - 0x4B400000);
+            red_s32(a1 + 4, __float_as_int(tc.y) - 0x4B400000);
+            red_s32(a1 + 8, __float_as_int(td.x) - 0x4B400000);
+            red_s32(a1 + 12, __float_as_int(td.y) - 0x4B400000);
+        } else {
+            float2* pa = acc + off;
+            const float2 t00 = pa[0], t01 = pa[1], t10 = pa[sP], t11 = pa[sP + 1];
+            pa[0] = make_float2(t00.x + a.x, t00.y + a.y);
+            pa[1] = make_float2(t01.x + b.x, t01.y + b.y);
+            pa[sP] = make_float2(t10.x + c.x, t10.y + c.y);
+            pa[sP + 1] = make_float2(t11.x + d.x, t11.y + d.y);
+        }
     };
     const float4* p = ck;
     float4 c0 = __ldg(p), c1 = __ldg(p + 32), c2 = __ldg(p + 64), c3 = __ldg(p + 96);
@@ -1606,6 +1657,7 @@ __global__ void __launch_bounds__(512, 1) lin_kernel(ProjArgs A)
             RayB rb{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             StateB st{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             float4* cl = nullptr;
+            float2 am = make_float2(0.f, 0.f);
             if (lane_ray(A, ui, rays, grp, lane, dU, dV, r, ii, ilo, uu, vv)) {
                 const float sc = rsc[r];
                 const float4 G = gsh[r];
@@ -1622,12 +1674,13 @@ __global__ void __launch_bounds__(512, 1) lin_kernel(ProjArgs A)
                 const int b = static_cast<int>(s & 1);
                 mbar_wait(&mbar[b], static_cast<uint32_t>((s >> 1) & 1));
                 const float2* sbuf = reinterpret_cast<const float2*>(stage0 + b * A.stage_bytes);
-                walk_lin<PAIRED>(sbuf, P, r0, r1, ilo, dU, dV, cf, ch, rb, ii, uu, vv, st, cl, k);
+                walk_lin<PAIRED>(sbuf, P, r0, r1, ilo, dU, dV, cf, ch, rb, ii, uu, vv, st, cl, k, am);
                 __syncthreads();   // stage buffer b consumed
                 if (tid == 0 && s + 2 < n_stages)
                     issue_seg_stage<false>(A, Rb, sb0 + s + 2, stage0 + b * A.stage_bytes, &mbar[b]);
                 ++s;
             }
+            entry_bounds(A, ui, am);
         }
         __syncthreads();   // gsh / rsc / q1i are rewritten by the next unit
     }
@@ -1721,11 +1774,32 @@ __global__ void __launch_bounds__(256) gnw_kernel(ProjArgs A, const int32_t* __r
     for (int r = threadIdx.x; r < R; r += blockDim.x) gn_rout_from_seg<PAIRED>(A, ct * A.K, dir, r, rout);
     __syncthreads();
     float* gw = A.gw + static_cast<size_t>(ct) * 2 * R;
+    float wm = 0.f, wm1 = 0.f;
     for (int r = threadIdx.x; r < R; r += blockDim.x) {
         float wr, wr1;
         gn_weights(A, rout, r, wr, wr1);
         gw[r] = wr;
         gw[R + r] = wr1;
+        wm = fmaxf(wm, fabsf(wr));
+        wm1 = fmaxf(wm1, fabsf(wr1));
+    }
+    if (A.gscale) {   // max |w_r|, |w'_r| of the angle-bank: gscale[ct * 8 + 2, 3]
+        __shared__ float red[2][8];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+            wm1 = fmaxf(wm1, __shfl_xor_sync(0xffffffffu, wm1, o));
+        }
+        if ((threadIdx.x & 31) == 0) { red[0][threadIdx.x >> 5] = wm; red[1][threadIdx.x >> 5] = wm1; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int k = 1; k < static_cast<int>(blockDim.x >> 5); ++k) {
+                wm = fmaxf(wm, red[0][k]);
+                wm1 = fmaxf(wm1, red[1][k]);
+            }
+            A.gscale[static_cast<size_t>(ct) * 8 + 2] = wm;
+            A.gscale[static_cast<size_t>(ct) * 8 + 3] = wm1;
+        }
     }
 }
 
@@ -1738,7 +1812,7 @@ cudaError_t launch_gnw(bool paired, const ProjArgs& A, const int32_t* tabs, int 
 
 // gnb_kernel: per CG step, w_r from the (J p) partials, then the cached scatter into slots (as
 // seg_b_kernel; no image staging).
-template <bool PAIRED>
+template <bool PAIRED, bool INTACC>
 __global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
 {
     const int W = blockDim.x >> 5;
@@ -1751,10 +1825,11 @@ __global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
     if (A.u_begin[c] == A.u_begin[c + 1]) return;
     const int P = A.P, R = A.R, K = A.K, Rb = A.RbB;
     const int RB1 = Rb + 1;
-    float2* wacc = wacc_all + static_cast<size_t>(warp) * RB1 * P;
+    const int NACC = INTACC ? 1 : W;   // INTACC: one shared fixed-point accumulator, else one per warp
+    float2* wacc = wacc_all + (INTACC ? 0 : static_cast<size_t>(warp) * RB1 * P);
     {
         float4* z = reinterpret_cast<float4*>(wacc_all);
-        const int n4 = W * RB1 * P / 2;
+        const int n4 = NACC * RB1 * P / 2;
         for (int k = tid; k < n4; k += NT) z[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
     const int npairs = P >> 1;
@@ -1792,6 +1867,20 @@ __global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
             return (static_cast<double>(rp.U0) + (vrow * 4294967296.0 - static_cast<double>(rp.V0)) * kuv) *
                    (1.0 / 4294967296.0);
         };
+        // INTACC fixed-point scales of the unit's angle-bank: a pixel's pending-cell value is at most
+        // cellmax samples x (max|w_r| + max|w'_r|) x the entry bound (bilinear weights <= 1); S, a power
+        // of two (exact scaling both ways), puts that bound, raised by 2^-10 against rounding in the
+        // pending sums, below 2^22, where the magic-number rounding is exact
+        float2 S = make_float2(1.f, 1.f), iS = make_float2(1.f, 1.f);
+        if constexpr (INTACC) {
+            const float* gs = A.gscale + static_cast<size_t>((ui.canon - ui.seg) / K) * 8;
+            const float wsum = (gs[2] + gs[3]) * (static_cast<float>(A.cellmax) * (1.f + 0x1p-10f));
+            int ex, ey;
+            frexpf(wsum * gs[0], &ex);
+            frexpf(wsum * gs[1], &ey);
+            S = make_float2(ldexpf(1.f, 22 - ex), ldexpf(1.f, 22 - ey));
+            iS = make_float2(ldexpf(1.f, ex - 22), ldexpf(1.f, ey - 22));
+        }
         for (int pass = 0; pass < A.passesB; ++pass) {
             const int grp = pass * W + warp;
             int r, ii, ilo, kend = 0;
@@ -1815,7 +1904,7 @@ __global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
                 const bool flip = j & 1;
                 const int abase = flip ? Rb * P : 0, sP = flip ? -P : P;
                 if (PGET_ABLATE != 3)   // 3: no walk
-                    walk_gnb(wacc, P, r0, r1, abase, sP, ilo, dU, dV, wr, wr1, ii, uu, vv, cl, cend);
+                    walk_gnb<INTACC>(wacc, P, r0, r1, abase, sP, ilo, dU, dV, wr, wr1, ii, uu, vv, cl, cend, S);
                 __syncthreads();   // every warp ring complete
                 const bool last = j == ui.nb - 1;
                 const int carry = last ? -1 : (ui.dir > 0 ? r0 : r1);
@@ -1836,12 +1925,20 @@ __global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
                     const int lr = flip ? r0 + Rb - rw : rw - r0;
                     PGET_CHECK(lr >= 0 && lr < RB1);
                     float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if constexpr (INTACC) {
+                        int4* el = reinterpret_cast<int4*>(wacc_all + static_cast<size_t>(lr) * P) + q;
+                        const int4 x = *el;
+                        *el = make_int4(0, 0, 0, 0);
+                        sum = make_float4(static_cast<float>(x.x) * iS.x, static_cast<float>(x.y) * iS.y,
+                                          static_cast<float>(x.z) * iS.x, static_cast<float>(x.w) * iS.y);
+                    } else {
 #pragma unroll 4
-                    for (int w = 0; w < W; ++w) {
-                        float4* el = reinterpret_cast<float4*>(wacc_all + (static_cast<size_t>(w) * RB1 + lr) * P) + q;
-                        const float4 x = *el;
-                        sum.x += x.x; sum.y += x.y; sum.z += x.z; sum.w += x.w;
-                        *el = make_float4(0.f, 0.f, 0.f, 0.f);
+                        for (int w = 0; w < W; ++w) {
+                            float4* el = reinterpret_cast<float4*>(wacc_all + (static_cast<size_t>(w) * RB1 + lr) * P) + q;
+                            const float4 x = *el;
+                            sum.x += x.x; sum.y += x.y; sum.z += x.z; sum.w += x.w;
+                            *el = make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
                     }
                     const int ir = rw - kHalo, ic = 2 * q - kHalo;
                     if (ir >= 0 && ir < A.N && ic >= 0 && ic < A.Ns)
@@ -1926,8 +2023,13 @@ cudaError_t launch_gnc(int phase, bool paired, const ProjArgs& A, int grid, int 
     } else if (phase == 1) {
         jvpc_kernel<<<grid, block, smem, s>>>(A);
     } else {
-        if (paired) gnb_kernel<true><<<grid, block, smem, s>>>(A);
-        else gnb_kernel<false><<<grid, block, smem, s>>>(A);
+        if (A.gscale) {
+            if (paired) gnb_kernel<true, true><<<grid, block, smem, s>>>(A);
+            else gnb_kernel<false, true><<<grid, block, smem, s>>>(A);
+        } else {
+            if (paired) gnb_kernel<true, false><<<grid, block, smem, s>>>(A);
+            else gnb_kernel<false, false><<<grid, block, smem, s>>>(A);
+        }
     }
     return cudaGetLastError();
 }
@@ -1940,10 +2042,12 @@ cudaError_t set_gnc_smem_limit(size_t smem)
     if ((e = cudaFuncSetAttribute(lin_kernel<true>, a, v))) return e;
     if ((e = cudaFuncSetAttribute(lin_kernel<false>, a, v))) return e;
     if ((e = cudaFuncSetAttribute(jvpc_kernel, a, v))) return e;
-    if ((e = cudaFuncSetAttribute(gnb_kernel<true>, a, v))) return e;
+    if ((e = cudaFuncSetAttribute(gnb_kernel<true, false>, a, v))) return e;
+    if ((e = cudaFuncSetAttribute(gnb_kernel<true, true>, a, v))) return e;
+    if ((e = cudaFuncSetAttribute(gnb_kernel<false, true>, a, v))) return e;
     if ((e = cudaFuncSetAttribute(jsq_kernel<true>, a, v))) return e;
     if ((e = cudaFuncSetAttribute(jsq_kernel<false>, a, v))) return e;
-    return cudaFuncSetAttribute(gnb_kernel<false>, a, v);
+    return cudaFuncSetAttribute(gnb_kernel<false, false>, a, v);
 }
 
 // ------------------------------------------------------------------------------------------ reduction
