@@ -1511,7 +1511,8 @@ __device__ __forceinline__ void walk_jvpc(const float2* __restrict__ img, int P,
 // gnb walk: scatter w_r (alpha, beta) + w'_r (alpha', beta') of the band's samples (same-cell registers).
 // ck points at the lane's next entry; the ring reads up to 4 rows and the prefetch PGET_PF_DIST rows
 // past it unchecked (kCachePadRows rows are allocated past the cache).
-// INTACC: one block-shared accumulator of 32-bit fixed-point pairs, added to with native shared
+// INTACC: one block-shared accumulator of 32-bit fixed-point values in two planes (lambda, mu; planar
+// so that a warp's adds spread over all 32 banks), added to with native shared
 // integer atomics (red.shared.add.u32): a pending cell's four float2 sums are scaled by S (a power of
 // two, |value * S| < 2^22 by construction, see gnb_kernel), rounded to integers with the
 // 1.5 * 2^23 magic-number FFMA and added.  Integer addition is associative, so the result does not
@@ -1524,7 +1525,7 @@ __device__ __forceinline__ void red_s32(uint32_t addr, int v)
 template <bool INTACC>
 __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0, int r1, int abase, int sP, int ilo,
                                          int64_t dU, int64_t dV, float wr, float wr1, int& i, int64_t& u, int64_t& v,
-                                         const float4*& ck, const float4* cend, float2 S)
+                                         const float4*& ck, const float4* cend, float2 S, uint32_t planeB)
 {
     const int iv0 = hi32(v);
     if (i < ilo || iv0 < r0 || iv0 >= r1) return;
@@ -1536,15 +1537,15 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
             const float2 mg = make_float2(12582912.f, 12582912.f);   // 1.5 * 2^23
             const float2 ta = __ffma2_rn(a, S, mg), tb = __ffma2_rn(b, S, mg);
             const float2 tc = __ffma2_rn(c, S, mg), td = __ffma2_rn(d, S, mg);
-            const uint32_t a0 = sbase + static_cast<uint32_t>(off * 8), a1 = sbase + static_cast<uint32_t>((off + sP) * 8);
+            const uint32_t a0 = sbase + static_cast<uint32_t>(off * 4), a1 = sbase + static_cast<uint32_t>((off + sP) * 4);
             red_s32(a0, __float_as_int(ta.x) - 0x4B400000);
-            red_s32(a0 + 4, __float_as_int(ta.y) - 0x4B400000);
-            red_s32(a0 + 8, __float_as_int(tb.x) - 0x4B400000);
-            red_s32(a0 + 12, __float_as_int(tb.y) - 0x4B400000);
+            red_s32(a0 + planeB, __float_as_int(ta.y) - 0x4B400000);
+            red_s32(a0 + 4, __float_as_int(tb.x) - 0x4B400000);
+            red_s32(a0 + 4 + planeB, __float_as_int(tb.y) - 0x4B400000);
             red_s32(a1, __float_as_int(tc.x) - 0x4B400000);
-            red_s32(a1 + 4, __float_as_int(tc.y) - 0x4B400000);
-            red_s32(a1 + 8, __float_as_int(td.x) - 0x4B400000);
-            red_s32(a1 + 12, __float_as_int(td.y) - 0x4B400000);
+            red_s32(a1 + planeB, __float_as_int(tc.y) - 0x4B400000);
+            red_s32(a1 + 4, __float_as_int(td.x) - 0x4B400000);
+            red_s32(a1 + 4 + planeB, __float_as_int(td.y) - 0x4B400000);
         } else {
             float2* pa = acc + off;
             const float2 t00 = pa[0], t01 = pa[1], t10 = pa[sP], t11 = pa[sP + 1];
@@ -1904,7 +1905,8 @@ __global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
                 const bool flip = j & 1;
                 const int abase = flip ? Rb * P : 0, sP = flip ? -P : P;
                 if (PGET_ABLATE != 3)   // 3: no walk
-                    walk_gnb<INTACC>(wacc, P, r0, r1, abase, sP, ilo, dU, dV, wr, wr1, ii, uu, vv, cl, cend, S);
+                    walk_gnb<INTACC>(wacc, P, r0, r1, abase, sP, ilo, dU, dV, wr, wr1, ii, uu, vv, cl, cend, S,
+                                     static_cast<uint32_t>(RB1 * P * 4));
                 __syncthreads();   // every warp ring complete
                 const bool last = j == ui.nb - 1;
                 const int carry = last ? -1 : (ui.dir > 0 ? r0 : r1);
@@ -1926,11 +1928,13 @@ __global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
                     PGET_CHECK(lr >= 0 && lr < RB1);
                     float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
                     if constexpr (INTACC) {
-                        int4* el = reinterpret_cast<int4*>(wacc_all + static_cast<size_t>(lr) * P) + q;
-                        const int4 x = *el;
-                        *el = make_int4(0, 0, 0, 0);
-                        sum = make_float4(static_cast<float>(x.x) * iS.x, static_cast<float>(x.y) * iS.y,
-                                          static_cast<float>(x.z) * iS.x, static_cast<float>(x.w) * iS.y);
+                        int2* el = reinterpret_cast<int2*>(wacc_all) + static_cast<size_t>(lr) * (P / 2) + q;
+                        int2* em = el + static_cast<size_t>(RB1) * (P / 2);   // mu plane
+                        const int2 xl = *el, xm = *em;
+                        *el = make_int2(0, 0);
+                        *em = make_int2(0, 0);
+                        sum = make_float4(static_cast<float>(xl.x) * iS.x, static_cast<float>(xm.x) * iS.y,
+                                          static_cast<float>(xl.y) * iS.x, static_cast<float>(xm.y) * iS.y);
                     } else {
 #pragma unroll 4
                         for (int w = 0; w < W; ++w) {
