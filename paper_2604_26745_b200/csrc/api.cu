@@ -436,7 +436,9 @@ WS carve(const Geometry& g, int op, char* base)
         if (g.adj_seg)
             w.segp = reinterpret_cast<float*>(take(static_cast<size_t>(g.sch[kSchedAdj].n_canon) * kSegFields *
                                                    g.R * sizeof(float)));
-        if (g.adj_seg && g.gn_cached && op != PGET_OP_VJP) {
+        const bool uses_cache = op == PGET_OP_GN_CG_STEP || op == PGET_OP_LM_SOLVE ||
+                                (op == PGET_OP_GN_APPLY && g.gn_apply_cached);
+        if (g.adj_seg && g.gn_cached && uses_cache) {
             const Schedule& S = g.sch[kSchedAdj];
             w.cache = reinterpret_cast<float4*>(
                 take((static_cast<size_t>(B) * S.cache_rows_member + kCachePadRows) * 32 * sizeof(float4)));
@@ -595,6 +597,7 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     g.gnb_tall = g.P >= 200;   // measured: config 4 -3.6 % LM, config 2 +0.8 %
     if (const char* ev = std::getenv("PGET_GNB_TALL")) g.gnb_tall = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_GNB_INT")) g.gnb_int = g.gnb_int && std::atoi(ev) != 0;
+    if (const char* ev = std::getenv("PGET_GN_APPLY_CACHED")) g.gn_apply_cached = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_GN_CACHE_MAX_GB")) g.cache_max_gb = std::atof(ev);
     if (const char* ev = std::getenv("PGET_GN_CACHE")) {   // 0: recompute, 1: hybrid, 2: fully cached
         const int v = std::atoi(ev);
@@ -605,8 +608,8 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     if (const char* ev = std::getenv("PGET_SEGA_W")) g.segA_W = std::max(1, std::min(15, std::atoi(ev)));
     if (const char* ev = std::getenv("PGET_SEGA_CPS")) g.segA_cps = std::max(1, std::min(4, std::atoi(ev)));
     if ((g.segA_W + 1) * 32 * g.segA_cps > 2048) g.segA_cps = 2048 / ((g.segA_W + 1) * 32);
-    // the coefficient cache only while it stays small next to HBM (config 2: 0.4 GB, config 4:
-    // 2.7 GB; config 5's 64 assemblies would need 25 GB: recompute there)
+    // the coefficient cache while it stays well inside HBM (config 2: 0.4 GB, config 4: 2.7 GB,
+    // config 5's 64 assemblies: 25 GB of 180; measured: config 5 LM iteration 307 -> 210 ms)
     build_host_schedules(g, rays);
     for (int k = 0; k < 3 && e == cudaSuccess; ++k) {
         Schedule& S = g.sch[k];
@@ -1073,7 +1076,7 @@ pget_status pget_gn_apply(pget_geometry h, const float* lam, const float* mu, co
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int N = g.desc.n_px, B = g.desc.batch;
     if ((st = pack2(g, w, lam, mu, nullptr, nullptr, nullptr, nullptr, s))) return st;
-    if (g.adj_seg && g.gn_cached) {   // phase A (VJP mode) of u -> cache -> cached product
+    if (g.adj_seg && g.gn_cached && g.gn_apply_cached) {   // phase A (VJP mode) of u -> cache -> cached product
         const SegCfg c = seg_cfg(g);
         const Schedule& S = g.sch[kSchedAdj];
         ProjArgs A = gnc_args(g, w);

@@ -179,8 +179,11 @@ struct Geometry {
     // requires every pixel's per-unit sum below 2^31 at the scale that keeps a pending cell below
     // 2^22, i.e. (samples near a pixel) / cellmax < 512 (geometry.cpp)
     bool gnb_int = true;
+    // pget_gn_apply through the cache too (one product per call: building the cache costs more than
+    // it saves; tests set PGET_GN_APPLY_CACHED=1 to pin the cached product at the operator tolerance)
+    bool gn_apply_cached = false;
     int cellmax = 1;        // max consecutive samples of one ray inside one pixel cell
-    double cache_max_gb = 8.0;   // larger caches fall back to the recomputing GN product
+    double cache_max_gb = 48.0;   // larger caches fall back to the recomputing GN product (config 5: 25 GB)
     bool gn_hybrid = true;   // cached scatter with the recomputed (J p) (PGET_GN_CACHE=1)
     bool gn_cached = true;   // GN product from the per-LM-iteration Jacobian-entry cache (PGET_GN_CACHE=0: recompute)
     int segA_W = 15, segA_cps = 1;

@@ -182,8 +182,14 @@ def test_white_noise_rel_l2(pg):
 
 
 # ----------------------------------------------------------------------------------- GN operator / LM step
+# the GN product as pget_gn_apply runs it (recomputed), and through the LM iteration's cached scatter
+# (PGET_GN_APPLY_CACHED=1; fixed-point shared accumulator, or per-warp float accumulators with
+# PGET_GNB_INT=0), all at the operator tolerance
+@pytest.mark.parametrize("path", ["recompute", "cached", "cached_float"])
 @pytest.mark.parametrize("cid", [2, 3])
-def test_gn_apply_operator(pg, cid):
+def test_gn_apply_operator(pg, cid, path, monkeypatch):
+    monkeypatch.setenv("PGET_GN_APPLY_CACHED", "0" if path == "recompute" else "1")
+    monkeypatch.setenv("PGET_GNB_INT", "0" if path == "cached_float" else "1")
     gd = P.geometry_desc(cid)
     cfg = P.CONFIGS[cid]
     g = pg.Geometry(gd)
@@ -273,10 +279,14 @@ def test_errors_fail_loudly(pg):
 
 
 # ----------------------------------------------------------------------------------- determinism (Q18)
+@pytest.mark.parametrize("cached", [False, True])
 @pytest.mark.parametrize("cid", [2, 3])
-def test_adjoint_bitwise_deterministic(pg, cid):
-    """VJP and GN product: no atomics in the sample loop, fixed-thread slot flushes, fixed-order fp64
-    slot reduction -> bitwise identical results run to run (DESIGN.md R-determinism)."""
+def test_adjoint_bitwise_deterministic(pg, cid, cached, monkeypatch):
+    """VJP and GN product: no floating-point atomics in the sample loop (per-warp float accumulators,
+    or the cached scatter's shared fixed-point accumulator whose integer sums do not depend on the
+    order), fixed-thread slot flushes, fixed-order fp64 slot reduction -> bitwise identical results
+    run to run (DESIGN.md R-determinism)."""
+    monkeypatch.setenv("PGET_GN_APPLY_CACHED", "1" if cached else "0")
     gd = P.geometry_desc(cid)
     g = pg.Geometry(gd)
     lam, mu, dl, dm, lp, mp = inputs(cid)
