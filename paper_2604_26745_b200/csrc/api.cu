@@ -226,8 +226,12 @@ SegCfg seg_cfg(const Geometry& g)
             c.off_waccG = g.gnb_tall ? 128 : c.off_wacc;
             c.off_routG = g.gnb_tall ? static_cast<int>(128 + wg) : c.off_rout;
             c.smemG = g.gnb_tall ? 128 + wg + rout_b : c.smemB;
-            if (g.gnb_int && g.gn_hybrid) {   // one shared accumulator: bands up to the whole padded image
-                int Rbi = g.P - 1;
+            if (g.gnb_int && g.gn_hybrid) {   // one shared accumulator: bands up to a whole segment
+                int maxseg = 1;
+                for (size_t k = 0; k + 1 < S.seg_rows.size(); ++k)
+                    maxseg = std::max(maxseg, S.seg_rows[k + 1] - S.seg_rows[k]);
+                // no more shared memory than a segment needs: the rest stays L1 for the entry stream
+                int Rbi = std::min(g.P - 1, maxseg);
                 size_t wi = 0;
                 for (; Rbi > 1; --Rbi) {
                     wi = align128(static_cast<size_t>(Rbi + 1) * g.P * sizeof(int2));
@@ -876,9 +880,10 @@ static pget_status gnc_build(const Geometry& g, const WS& w, cudaStream_t s)
 // hybrid (g.gn_hybrid): the (J p) of p recomputed by the GN-mode phase A from (u, p) (pack4 into
 // w.img4), the scatter from the cache; else the (J p) from the cache too (jvpc_kernel)
 static pget_status gnc_product(const Geometry& g, const WS& w, const float* lam, const float* mu, const float* pl,
-                               const float* pm, cudaStream_t s)
+                               const float* pm, cudaStream_t s, bool packed = false)
 {
-    pget_status st = g.gn_hybrid ? pack4(g, w, lam, mu, pl, pm, s)
+    // packed: w.img4 already holds (lam, mu, pl, pm) (the fused CG kernel mirrors its p update there)
+    pget_status st = g.gn_hybrid ? (packed ? PGET_OK : pack4(g, w, lam, mu, pl, pm, s))
                                  : pack2(g, w, pl, pm, nullptr, nullptr, nullptr, nullptr, s, nullptr);
     if (st) return st;
     const SegCfg c = seg_cfg(g);
@@ -1139,20 +1144,26 @@ static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const f
 
     // 5: CG
     for (int k = 0; k < n_cg; ++k) {
+        // p of step k > 0 was packed by step k-1's fused CG kernel
+        const bool packed = k > 0 && (!cached || g.gn_hybrid);
         if (cached) {
-            if ((st = gnc_product(g, w, lam, mu, w.pl, w.pm, s))) return st;
+            if ((st = gnc_product(g, w, lam, mu, w.pl, w.pm, s, packed))) return st;
         } else {
-            if ((st = pack4(g, w, lam, mu, w.pl, w.pm, s))) return st;
+            if (!packed && (st = pack4(g, w, lam, mu, w.pl, w.pm, s))) return st;
             if ((st = proj_adjoint(g, w, MODE_GN, nullptr, s))) return st;
         }
         {   // finish + gamma + update1 + zeta + update2: one cooperative launch (grid-wide syncs)
-            int kk = k, NN = N, BB = B, nb = kNblk, GG = Gg;
+            int kk = k, NN = N, BB = B, nb = kNblk, GG = Gg, PP = g.P;
             float al = alpha, be = beta;
             double *pg = P[3], *pz = P[4];
             CGState* cgs = w.cg;
             const float* bv = betav;
+            // mirror p into the packed float4 images for the next product (not after the last step)
+            const bool mirror = k + 1 < n_cg && (!cached || g.gn_hybrid);
+            float4* i4n = mirror ? w.img4[0] : nullptr;
+            float4* i4t = mirror ? w.img4[1] : nullptr;
             void* args[] = {&w.gacc, &GG, &al, &be, &bv, &s_lam, &s_mu, &w.zl, &w.zm, &w.pl, &w.pm, &w.ql, &w.qm,
-                            &pg, &pz, &cgs, &stats, &kk, &NN, &BB, &nb};
+                            &pg, &pz, &cgs, &stats, &kk, &NN, &BB, &nb, &i4n, &i4t, &PP};
             const int grid = std::min(B * kNblk, g.cg_coop_blocks);
             CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cg_fused_kernel), dim3(grid), dim3(kVecThreads),
                                            args, 0, s));

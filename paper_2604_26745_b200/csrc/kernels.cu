@@ -474,7 +474,8 @@ __global__ void scalar_kernel(int op, int k, const double* p0, const double* p1,
 __global__ void cg_fused_kernel(const double2* __restrict__ part, int G, float alpha, float beta_h,
                                 const float* betav, float* sl, float* sm, float* zl, float* zm, float* pl,
                                 float* pm, float* ql, float* qm, double* pg, double* pz, CGState* st,
-                                pget_gn_stats* stats, int k, int N, int B, int nblk)
+                                pget_gn_stats* stats, int k, int N, int B, int nblk, float4* img4n, float4* img4t,
+                                int P)
 {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
@@ -565,8 +566,14 @@ __global__ void cg_fused_kernel(const double2* __restrict__ part, int G, float a
             const float bc = static_cast<float>(bcg);
             for (size_t e = static_cast<size_t>(j) * blockDim.x + threadIdx.x; e < n2; e += stride) {
                 const size_t q = base + e;
-                pl[q] = fmaf(bc, pl[q], zl[q]);
-                pm[q] = fmaf(bc, pm[q], zm[q]);
+                const float p1 = fmaf(bc, pl[q], zl[q]), p2 = fmaf(bc, pm[q], zm[q]);
+                pl[q] = p1;
+                pm[q] = p2;
+                if (img4n) {   // the next GN product's packed (dlam, dmu) halves, both orientations (pack4)
+                    const int i = static_cast<int>(e % N) + kHalo, jj = static_cast<int>(e / N) + kHalo;
+                    reinterpret_cast<float2*>(img4n + (static_cast<size_t>(m) * P + jj) * P + i)[1] = make_float2(p1, p2);
+                    reinterpret_cast<float2*>(img4t + (static_cast<size_t>(m) * P + i) * P + jj)[1] = make_float2(p1, p2);
+                }
             }
         }
         if (j == 0 && threadIdx.x == 0) st_out[m] = c;   // carried over (stopped members keep theirs)

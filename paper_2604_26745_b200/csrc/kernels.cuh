@@ -94,7 +94,7 @@ __global__ void cg_update2_kernel(const float* zl, const float* zm, float* pl, f
 __global__ void cg_fused_kernel(const double2* part, int G, float alpha, float beta_h, const float* betav, float* sl,
                                 float* sm, float* zl, float* zm, float* pl, float* pm, float* ql, float* qm,
                                 double* pg, double* pz, CGState* st, pget_gn_stats* stats, int k, int N, int B,
-                                int nblk);
+                                int nblk, float4* img4n, float4* img4t, int P);
 __global__ void dotsq_kernel(const float* a, const float* b, double* pdot, double* psq, int nper);
 __global__ void lapdot_kernel(const float* ul, const float* um, const float* sl, const float* sm, double* pdot,
                               double* psq, int N);
