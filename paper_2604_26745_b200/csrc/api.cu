@@ -142,7 +142,9 @@ ProjCfg proj_cfg(const Geometry& g, int mode)
     {
         const int tiles = ((g.desc.n_px + 31) / 32) * ((g.desc.n_px + 31) / 32);
         const int64_t want = (2LL * g.sm_count + int64_t(tiles) * g.desc.batch - 1) / (int64_t(tiles) * g.desc.batch);
-        c.G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(want, std::max(1, S.max_slots_member))));
+        int64_t wg = want;
+        if (const char* ev = std::getenv("PGET_RED_G")) wg = std::max(1, std::atoi(ev));   // experiment
+        c.G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(wg, std::max(1, S.max_slots_member))));
     }
     return c;
 }
