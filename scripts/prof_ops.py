@@ -1,6 +1,10 @@
-"""Run each projector mode once on a config (for ncu captures): forward, JVP, VJP, GN apply."""
+"""Run each projector mode once on a config (for ncu captures): forward, JVP, VJP, GN apply (through
+the coefficient cache, as the LM iteration runs it: VJP-mode phase A, cache build, GN-mode phase A,
+scatter weights, cached scatter)."""
 import os
 import sys
+
+os.environ.setdefault("PGET_GN_APPLY_CACHED", "1")
 
 import numpy as np
 import torch
