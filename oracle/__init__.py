@@ -63,7 +63,37 @@ def _load():
         _lib.orc_ray_adjoint.argtypes = [C.c_int, P, P, C.c_double, P, P]
         _lib.orc_ray_adjoint.restype = None
         _lib.orc_threads.restype = C.c_int
+        _lib.orc_set_prior.argtypes = [P, P, C.c_double, C.c_double]
+        _lib.orc_set_prior.restype = None
     return _lib
+
+
+class _Prior:
+    """O10 geometry priors for the duration of one oracle call: prior = (mask_lam, mask_mu, alpha1,
+    alpha2) with masks [B][N][N] (or None), member = the batch member of a per-member call."""
+
+    def __init__(self, g, prior, member=None):
+        self.lib, self.keep = _load(), []
+        self.args = (None, None, 0.0, 0.0)
+        if prior is not None:
+            m1, m2, a1, a2 = prior
+            shp = img_shape(g)
+
+            def arr(m):
+                if m is None:
+                    return None
+                a = _f64(m).reshape(shp)
+                a = np.ascontiguousarray(a if member is None else a[member])
+                self.keep.append(a)
+                return _p(a)
+            self.args = (arr(m1), arr(m2), float(a1), float(a2))
+
+    def __enter__(self):
+        self.lib.orc_set_prior(*self.args)
+        return self
+
+    def __exit__(self, *exc):
+        self.lib.orc_set_prior(None, None, 0.0, 0.0)
 
 
 def _desc(g: dict) -> _Desc:
@@ -150,28 +180,30 @@ def laplacian(u):
     return out
 
 
-def apply_H(g, lam, mu, alpha, beta, p_lam, p_mu):
+def apply_H(g, lam, mu, alpha, beta, p_lam, p_mu, prior=None):
     lib = _load()
     d = _desc(g)
     lam, mu = _f64(lam), _f64(mu)
     p = np.concatenate([_f64(p_lam).ravel(), _f64(p_mu).ravel()])
     out = np.zeros_like(p)
-    rc = lib.orc_apply_H(C.byref(d), _p(lam), _p(mu), alpha, beta, _p(p), _p(out))
+    with _Prior(g, prior):
+        rc = lib.orc_apply_H(C.byref(d), _p(lam), _p(mu), alpha, beta, _p(p), _p(out))
     assert rc == 0
     n = p.size // 2
     return out[:n].reshape(img_shape(g)), out[n:].reshape(img_shape(g))
 
 
-def gn_cg_step(g, lam, mu, y, alpha, beta, n_cg):
-    """One LM iteration (O7).  Returns (s_lam, s_mu, stats dict)."""
+def gn_cg_step(g, lam, mu, y, alpha, beta, n_cg, prior=None):
+    """One LM iteration (O7; with the O10 priors).  Returns (s_lam, s_mu, stats dict)."""
     lib = _load()
     d = _desc(g)
     lam, mu, y = _f64(lam), _f64(mu), _f64(y)
     sl = np.zeros(img_shape(g))
     sm = np.zeros(img_shape(g))
     st = np.zeros(ST_CG + n_cg + 1)
-    rc = lib.orc_gn_cg_step(C.byref(d), _p(lam), _p(mu), _p(y), float(alpha), float(beta), int(n_cg),
-                            _p(sl), _p(sm), _p(st))
+    with _Prior(g, prior):
+        rc = lib.orc_gn_cg_step(C.byref(d), _p(lam), _p(mu), _p(y), float(alpha), float(beta), int(n_cg),
+                                _p(sl), _p(sm), _p(st))
     assert rc == 0, rc
     return sl, sm, stats_dict(st, n_cg)
 
@@ -198,7 +230,7 @@ def ray_adjoint(lam_s, mu_s, delta):
     return dl, dm
 
 
-def safeguard(g, lam, mu, y, s_lam, s_mu, c_lam, c_mu, alpha, kappa=0.1):
+def safeguard(g, lam, mu, y, s_lam, s_mu, c_lam, c_mu, alpha, kappa=0.1, prior=None):
     """Prop. 1 safeguard (O8), per batch member.  Returns ((u_next_lam, u_next_mu), [dict per member])."""
     lib = _load()
     B = int(g.get("batch", 1))
@@ -213,8 +245,9 @@ def safeguard(g, lam, mu, y, s_lam, s_mu, c_lam, c_mu, alpha, kappa=0.1):
         ym = np.ascontiguousarray(ys[m])
         un = np.zeros(2 * l.size)
         out = np.zeros(7)
-        rc = lib.orc_safeguard(C.byref(d), _p(l), _p(u), _p(ym), _p(sl), _p(sm), _p(cl), _p(cm), float(alpha),
-                               float(kappa), _p(un), _p(out))
+        with _Prior(g, prior, m):
+            rc = lib.orc_safeguard(C.byref(d), _p(l), _p(u), _p(ym), _p(sl), _p(sm), _p(cl), _p(cm), float(alpha),
+                                   float(kappa), _p(un), _p(out))
         assert rc == 0, rc
         nl[m] = un[:l.size].reshape(l.shape)
         nm[m] = un[l.size:].reshape(l.shape)
@@ -223,7 +256,7 @@ def safeguard(g, lam, mu, y, s_lam, s_mu, c_lam, c_mu, alpha, kappa=0.1):
     return (nl, nm), res
 
 
-def lm_solve(g, lam, mu, y, n_iter, n_cg, alpha0, alpha_decay=5.0, k_freeze=0, beta0=0.0, box=None):
+def lm_solve(g, lam, mu, y, n_iter, n_cg, alpha0, alpha_decay=5.0, k_freeze=0, beta0=0.0, box=None, prior=None):
     """O9: n_iter LM iterations per batch member.  Returns ((lam, mu), [[stats dict per iteration]
     per member])."""
     lib = _load()
@@ -238,9 +271,10 @@ def lm_solve(g, lam, mu, y, n_iter, n_cg, alpha0, alpha_decay=5.0, k_freeze=0, b
         l = np.ascontiguousarray(lam_o[m])
         u = np.ascontiguousarray(mu_o[m])
         st = np.zeros(n_iter * (ST_CG + n_cg + 1))
-        rc = lib.orc_lm_solve(C.byref(d), _p(l), _p(u), _p(np.ascontiguousarray(ys[m])), int(n_iter), int(n_cg),
-                              float(alpha0), float(alpha_decay), int(k_freeze), float(beta0),
-                              None if bx is None else _p(bx), _p(st))
+        with _Prior(g, prior, m):
+            rc = lib.orc_lm_solve(C.byref(d), _p(l), _p(u), _p(np.ascontiguousarray(ys[m])), int(n_iter),
+                                  int(n_cg), float(alpha0), float(alpha_decay), int(k_freeze), float(beta0),
+                                  None if bx is None else _p(bx), _p(st))
         assert rc == 0, rc
         lam_o[m], mu_o[m] = l, u
         row = ST_CG + n_cg + 1

@@ -20,6 +20,10 @@
  *       -- PAPER.md:160-180 eq:m-function, eq:LMA-step; PAPER.md:248 eq:rho_agreement
  *       -- inner solver: plain CG (reading Q12) instead of the paper's SGP.
  *   LM solve: alpha continuation, beta schedule, box projection -- PAPER.md:144-182, 288 (O9, N1)
+ *   geometry priors (O10, N1): f += alpha1/2 ||P1 lam||^2 + alpha2/2 ||P2 mu||^2, P1, P2 diagonal
+ *       masks -- PAPER.md:146-148 eq:lma_objective (reading R-prior), continued with alpha
+ *       (alpha^(k) = (alpha1, alpha2) / 5^k); set by orc_set_prior, used by every
+ *       function below that evaluates f, its gradient, H or m_k (not thread-safe: test use only)
  *   safeguard u_{k+1} = u~ iff m_k(s~) <= m_k(s_k) and rho_k(s~) > kappa
  *       -- PAPER.md:241-258 Prop. 1 eq:uk+1_condition; Algorithm 2 PAPER.md:290-313 (O8, N2)
  *
@@ -431,6 +435,44 @@ static double dot(const double* a, const double* b, size_t n)
     return s;
 }
 
+/* ------------------------------------------------------------------ O10 geometry priors */
+/* P1 = diag(m1), P2 = diag(m2) over [batch][N][N]; a1, a2 the weights at alpha^(0); scale the
+ * continuation factor alpha_k / alpha_0 (orc_lm_solve sets it per iteration). */
+static struct {
+    const double *m1, *m2;
+    double a1, a2, scale;
+} g_prior = {NULL, NULL, 0.0, 0.0, 1.0};
+
+void orc_set_prior(const double* m1, const double* m2, double a1, double a2)
+{
+    g_prior.m1 = m1;
+    g_prior.m2 = m2;
+    g_prior.a1 = m1 ? a1 : 0.0;
+    g_prior.a2 = m2 ? a2 : 0.0;
+    g_prior.scale = 1.0;
+}
+
+/* alpha1/2 ||P1 x_lam||^2 + alpha2/2 ||P2 x_mu||^2 at the current continuation scale */
+static double prior_value(const double* xl, const double* xm, size_t npx)
+{
+    double v = 0.0;
+    for (size_t k = 0; k < npx; ++k) {
+        if (g_prior.m1) v += 0.5 * g_prior.a1 * g_prior.scale * (g_prior.m1[k] * xl[k]) * (g_prior.m1[k] * xl[k]);
+        if (g_prior.m2) v += 0.5 * g_prior.a2 * g_prior.scale * (g_prior.m2[k] * xm[k]) * (g_prior.m2[k] * xm[k]);
+    }
+    return v;
+}
+
+/* out += P^T P x, weighted: out_lam += alpha1 m1^2 x_lam, out_mu += alpha2 m2^2 x_mu (the gradient of
+ * prior_value, and its Hessian applied to x) */
+static void prior_apply(const double* xl, const double* xm, double* ol, double* om, size_t npx)
+{
+    for (size_t k = 0; k < npx; ++k) {
+        if (g_prior.m1) ol[k] += g_prior.a1 * g_prior.scale * g_prior.m1[k] * g_prior.m1[k] * xl[k];
+        if (g_prior.m2) om[k] += g_prior.a2 * g_prior.scale * g_prior.m2[k] * g_prior.m2[k] * xm[k];
+    }
+}
+
 /* ------------------------------------------------------------------ O7 GN-CG step + LM wrap */
 /* Stats layout (double[16 + n_cg + 1]):
  *  0 f(u)   1 1/2||r||^2   2 R(u)   3 ||b||   4 pred = m(0)-m(s)   5 f(u+s)   6 rho
@@ -457,6 +499,7 @@ static int apply_H(hctx* H, const double* p, double* out)
         orc_laplacian(H->g->n_px, H->g->batch, H->tl, H->tm);
         for (size_t k = 0; k < n; ++k) out[f * n + k] += H->alpha * H->tm[k] + H->beta * p[f * n + k];
     }
+    prior_apply(p, p + n, out, out + n, n);   /* + P^T P p (O10) */
     return 0;
 }
 
@@ -474,6 +517,7 @@ static double objective(const orc_desc* g, const double* lam, const double* mu, 
     orc_laplacian(g->n_px, g->batch, mu, tl);
     q += dot(tl, tl, npx);
     *reg = 0.5 * alpha * q;                                       /* R(u) = alpha/2 (||L lam||^2 + ||L mu||^2) */
+    *reg += prior_value(lam, mu, npx);                            /* + alpha1/2 ||P1 lam||^2 + alpha2/2 ||P2 mu||^2 */
     return *misfit + *reg;
 }
 
@@ -520,6 +564,13 @@ static int lm_step(const orc_desc* g, const double* lam, const double* mu, const
         orc_laplacian(g->n_px, g->batch, tl, tm);
         for (size_t k = 0; k < npx; ++k) bvec[f * npx + k] = -(bvec[f * npx + k] + alpha * tm[k]);
     }
+    {   /* - P^T P u (O10) */
+        double* gp = (double*)calloc(2 * npx, sizeof(double));
+        if (!gp) return -2;
+        prior_apply(lam, mu, gp, gp + npx, npx);
+        for (size_t k = 0; k < 2 * npx; ++k) bvec[k] -= gp[k];
+        free(gp);
+    }
     stats[0] = f0; stats[1] = misfit; stats[2] = reg; stats[3] = sqrt(dot(bvec, bvec, n2));
 
     /* 5: CG from s0 = 0 on H s = b */
@@ -562,8 +613,9 @@ static int lm_step(const orc_desc* g, const double* lam, const double* mu, const
         ls2 += dot(tl, tl, npx);
     }
     double bs = dot(bvec, s, n2);
-    double pred = bs - 0.5 * (js2 + alpha * ls2);
-    stats[4] = pred; stats[12] = js2; stats[13] = alpha * ls2; stats[14] = bs;
+    double ps2 = 2.0 * prior_value(s, s + npx, npx);              /* ||P s||^2, weighted (O10) */
+    double pred = bs - 0.5 * (js2 + alpha * ls2 + ps2);
+    stats[4] = pred; stats[12] = js2; stats[13] = alpha * ls2 + ps2; stats[14] = bs;
 
     /* 7: f(u+s), rho */
     for (size_t i = 0; i < npx; ++i) { ut[i] = lam[i] + s[i]; ut[npx + i] = mu[i] + s[npx + i]; }
@@ -610,6 +662,17 @@ static double model_m(const orc_desc* g, const double* lam, const double* mu, co
         half_rr += 0.5 * alpha * dot(tl, tl, npx);
         cross += alpha * dot(tm, tl, npx);
         half_ss += 0.5 * alpha * dot(tm, tm, npx);
+    }
+    /* the prior rows of F~ (O10): sqrt(alpha1) P1 lam, sqrt(alpha2) P2 mu, linear in u */
+    half_rr += prior_value(lam, mu, npx);
+    half_ss += prior_value(sl, sm, npx);
+    {
+        double* gp = (double*)calloc(2 * npx, sizeof(double));
+        if (gp) {
+            prior_apply(lam, mu, gp, gp + npx, npx);
+            cross += dot(gp, sl, npx) + dot(gp + npx, sm, npx);
+            free(gp);
+        }
     }
     return half_rr + cross + half_ss;
 }
@@ -668,13 +731,14 @@ int orc_lm_solve(const orc_desc* g, double* lam, double* mu, const double* y, in
     if (!sl || !sm) return -2;
     if (box)
         for (size_t i = 0; i < npx; ++i) { lam[i] = clampd(lam[i], box[0], box[1]); mu[i] = clampd(mu[i], box[2], box[3]); }
-    double alpha = alpha0, beta = beta0;
+    double alpha = alpha0, beta = beta0, pscale = 1.0;
     const int row = ST_CG + n_cg + 1;
     for (int k = 0; k < n_iter; ++k) {
-        if (k > 0 && k <= k_freeze) alpha /= decay;
+        if (k > 0 && k <= k_freeze) { alpha /= decay; pscale /= decay; }   /* (alpha, alpha1, alpha2) / decay^k */
+        g_prior.scale = pscale;
         double* st = stats + (size_t)k * row;
         int rc = lm_step(g, lam, mu, y, alpha, beta, n_cg, box, sl, sm, st);
-        if (rc) { free(sl); free(sm); return rc; }
+        if (rc) { g_prior.scale = 1.0; free(sl); free(sm); return rc; }
         if (st[7] != 0.0)
             for (size_t i = 0; i < npx; ++i) {
                 double a = lam[i] + sl[i], b = mu[i] + sm[i];
@@ -684,6 +748,7 @@ int orc_lm_solve(const orc_desc* g, double* lam, double* mu, const double* y, in
             }
         beta = st[8];
     }
+    g_prior.scale = 1.0;
     free(sl); free(sm);
     return 0;
 }

@@ -22,7 +22,7 @@ import numpy as np
 __all__ = [
     "CONFIGS", "Config", "geometry_desc", "make_phantom", "make_phantom_prime",
     "rod_directions", "white_directions", "white_weights", "initial_guess",
-    "poisson_noise", "rng_for", "disk_phantom",
+    "poisson_noise", "rng_for", "disk_phantom", "prior_masks",
 ]
 
 
@@ -229,6 +229,26 @@ def white_directions(shape, seed: int):
 def white_weights(shape, seed: int):
     """w ~ N(0,1) sinogram-shaped weights (rel-L2/adjoint only)."""
     return rng_for(seed).standard_normal(size=shape).astype(np.float32)
+
+
+def prior_masks(cfg: Config | int, n_px: int | None = None, margin_px: float = 1.0):
+    """Geometry-prior masks (P1 = diag(m_lam), P2 = diag(m_mu), reading R-prior):
+    1 on pixels whose centre lies farther than the rod radius + margin_px pixels from every lattice
+    position of the configuration (rod or not: no position is assumed filled a priori), else 0.
+    float32 [B][N][N], the same for both parts and every member."""
+    if isinstance(cfg, int):
+        cfg = CONFIGS[cfg]
+    n = n_px or cfg.n_px
+    centres, radius, _ = _lattice(cfg.lattice)
+    h = 2.0 / n
+    c = -1.0 + (np.arange(n) + 0.5) * h
+    near = np.zeros((n, n), dtype=bool)
+    r = radius + margin_px * h
+    for (cx, cy) in centres:
+        near |= (c[None, :] - cx) ** 2 + (c[:, None] - cy) ** 2 <= r * r
+    m = np.where(near, 0.0, 1.0).astype(np.float32)
+    m = np.broadcast_to(m, (cfg.batch, n, n)).copy()
+    return m, m.copy()
 
 
 def initial_guess(n_px: int, batch: int = 1):
