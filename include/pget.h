@@ -189,6 +189,28 @@ pget_status pget_geometry_info(pget_geometry g, pget_geometry_info_t* out);
 size_t pget_table_bytes(pget_geometry g, int table_id);                    /* 0 for a bad id */
 pget_status pget_geometry_export(pget_geometry g, int table_id, void* host_dst, size_t bytes);
 
+/* Geometry priors P1, P2 of eq:lma_objective (reading R-prior
+ * in DESIGN.md): penalties of the emission and attenuation outside the expected rod locations, as
+ * diagonal masks,
+ *     f(u) += alpha1/2 ||P1 lam||^2 + alpha2/2 ||P2 mu||^2,   P1 = diag(mask_lam), P2 = diag(mask_mu),
+ * so the gradient gains (alpha1 mask_lam^2 lam, alpha2 mask_mu^2 mu), H gains that diagonal and m_k
+ * the stacked rows sqrt(alpha1) P1 lam, sqrt(alpha2) P2 mu.  pget_lm_solve continues them with alpha
+ * (alpha^(k) = (alpha1, alpha2) / 5^k).
+ * mask_lam / mask_mu: device fp32 images [batch][N][N] (row = y) or NULL (that term off);
+ * alpha1, alpha2: finite and >= 0. */
+typedef struct {
+    const float* mask_lam;
+    const float* mask_mu;
+    float alpha1, alpha2;
+} pget_prior;
+
+/* Attach the priors to the handle: every later pget_gn_apply, pget_gn_cg_step, pget_lm_solve and
+ * pget_safeguard on g includes them until pget_set_prior(g, NULL) clears them.  The handle keeps
+ * the two device pointers (the caller keeps the masks alive and unchanged while set); it does not
+ * copy them.  Not to be called while calls on g are in flight on another thread.
+ * Errors: PGET_ERR_INVALID_ARGUMENT for a NULL/host-only handle or a negative / non-finite weight. */
+pget_status pget_set_prior(pget_geometry g, const pget_prior* prior);
+
 /* Workspace bytes needed by `op` (PGET_OP_*); 0 for a bad op. */
 size_t pget_workspace_bytes(pget_geometry g, int op);
 
@@ -206,7 +228,8 @@ pget_status pget_vjp(pget_geometry g, const float* lam, const float* mu, const f
                      float* g_lam, float* g_mu, void* ws, size_t ws_bytes, pget_stream_t stream);
 
 /* (q_lam, q_mu) = H p = J^T J p + alpha L^T L p + beta p at u = (lam, mu): the GN normal
- * operator of eq:LMA-step with the Laplacian penalty (reading Q10). */
+ * operator of eq:LMA-step with the Laplacian penalty (reading Q10); plus the
+ * diagonal of the priors when pget_set_prior attached them. */
 pget_status pget_gn_apply(pget_geometry g, const float* lam, const float* mu, const float* p_lam,
                           const float* p_mu, float alpha, float beta, float* q_lam, float* q_mu,
                           void* ws, size_t ws_bytes, pget_stream_t stream);

@@ -28,7 +28,7 @@ OPS = {"forward": 0, "jvp": 1, "vjp": 2, "gn_cg_step": 3, "gn_apply": 4, "safegu
 EXPORTED = ["pget_status_string", "pget_last_error_message", "pget_geometry_create", "pget_geometry_destroy",
             "pget_geometry_info", "pget_table_bytes", "pget_geometry_export", "pget_workspace_bytes",
             "pget_forward", "pget_jvp", "pget_vjp", "pget_gn_apply", "pget_gn_cg_step", "pget_safeguard", "pget_lm_solve", "pget_profile_begin",
-            "pget_profile_end"]
+            "pget_profile_end", "pget_set_prior", "pget_schedule_check"]
 MODES = ("forward", "jvp", "vjp", "gn")
 
 
@@ -68,6 +68,10 @@ class LMParams(C.Structure):
     _fields_ = [("n_iter", C.c_int32), ("n_cg", C.c_int32), ("alpha0", C.c_float), ("alpha_decay", C.c_float),
                 ("k_freeze", C.c_int32), ("beta0", C.c_float), ("lam_lo", C.c_float), ("lam_hi", C.c_float),
                 ("mu_lo", C.c_float), ("mu_hi", C.c_float), ("flags", C.c_uint32), ("pad_", C.c_int32)]
+
+
+class Prior(C.Structure):
+    _fields_ = [("mask_lam", C.c_void_p), ("mask_mu", C.c_void_p), ("alpha1", C.c_float), ("alpha2", C.c_float)]
 
 
 class SafeguardStats(C.Structure):
@@ -113,10 +117,11 @@ def lib():
         L.pget_safeguard.argtypes = [P, P, P, P, P, P, P, P, C.c_float, C.c_float, P, P, P, P, S, P]
         L.pget_lm_solve.argtypes = [P, P, P, P, C.POINTER(LMParams), P, P, S, P]
         L.pget_schedule_check.argtypes = [P]
+        L.pget_set_prior.argtypes = [P, C.POINTER(Prior)]
         L.pget_profile_begin.argtypes = [C.c_int32]
         L.pget_profile_end.argtypes = [P, P, P]
         for n in ("pget_profile_begin", "pget_profile_end", "pget_geometry_create", "pget_geometry_destroy", "pget_geometry_info", "pget_geometry_export",
-                  "pget_forward", "pget_jvp", "pget_vjp", "pget_gn_apply", "pget_gn_cg_step", "pget_safeguard", "pget_lm_solve", "pget_schedule_check"):
+                  "pget_forward", "pget_jvp", "pget_vjp", "pget_gn_apply", "pget_gn_cg_step", "pget_safeguard", "pget_lm_solve", "pget_schedule_check", "pget_set_prior"):
             getattr(L, n).restype = C.c_int
         _lib = L
     return _lib
@@ -190,6 +195,22 @@ class Geometry:
         out = np.zeros(nbytes // np.dtype(dt).itemsize, dtype=dt)
         _check(lib().pget_geometry_export(self._h, tid, out.ctypes.data_as(C.c_void_p), nbytes), "export")
         return out
+
+    def set_prior(self, mask_lam=None, mask_mu=None, alpha1=0.0, alpha2=0.0):
+        """Attach the geometry priors P1 = diag(mask_lam), P2 = diag(mask_mu) (pget_set_prior): later
+        GN / LM / safeguard calls add alpha1/2 ||P1 lam||^2 + alpha2/2 ||P2 mu||^2 to f.  Masks are
+        contiguous fp32 CUDA tensors of img_shape (kept referenced here); all None clears."""
+        if mask_lam is None and mask_mu is None:
+            _check(lib().pget_set_prior(self._h, None), "pget_set_prior")
+            self._prior = None
+            return
+        for m in (mask_lam, mask_mu):
+            if m is not None:
+                _f32(m, self.img_shape, "mask")
+        pr = Prior(mask_lam.data_ptr() if mask_lam is not None else None,
+                   mask_mu.data_ptr() if mask_mu is not None else None, float(alpha1), float(alpha2))
+        _check(lib().pget_set_prior(self._h, C.byref(pr)), "pget_set_prior")
+        self._prior = (mask_lam, mask_mu)
 
     def schedule_check(self):
         """Host-side consistency check of the handle's static schedules (raises on a violation)."""

@@ -460,7 +460,7 @@ WS carve(const Geometry& g, int op, char* base)
         w.dysino = reinterpret_cast<float*>(take(ns * sizeof(float)));
         float** vecs[] = {&w.bl, &w.bm, &w.zl, &w.zm, &w.pl, &w.pm, &w.ql, &w.qm, &w.ul, &w.um};
         for (float** v : vecs) *v = reinterpret_cast<float*>(take(n2 * sizeof(float)));
-        w.part = reinterpret_cast<double*>(take(8 * B * kNblk * sizeof(double)));
+        w.part = reinterpret_cast<double*>(take(9 * B * kNblk * sizeof(double)));   // [8]: priors
         w.cg = reinterpret_cast<CGState*>(take(2 * B * sizeof(CGState)));   // double-buffered (cg_fused_kernel)
         if (op == PGET_OP_LM_SOLVE) {   // the step, per-member beta
             w.sl = reinterpret_cast<float*>(take(n2 * sizeof(float)));
@@ -473,7 +473,7 @@ WS carve(const Geometry& g, int op, char* base)
         w.dysino = reinterpret_cast<float*>(take(ns * sizeof(float)));
         w.zl = reinterpret_cast<float*>(take(n2 * sizeof(float)));
         w.zm = reinterpret_cast<float*>(take(n2 * sizeof(float)));
-        w.part = reinterpret_cast<double*>(take(12 * B * kNblk * sizeof(double)));
+        w.part = reinterpret_cast<double*>(take(18 * B * kNblk * sizeof(double)));   // [12..17]: priors
     }
     w.bytes = off;
     return w;
@@ -831,6 +831,17 @@ static pget_status proj_adjoint(const Geometry& g, const WS& w, int mode, const 
 
 // GN with cached Jacobian entries: args shared by the three kernels (phase-B units,
 // groups, stage list and launch shape of the segmented adjoint)
+// the priors attached to the handle, weights times the LM continuation factor
+static PriorArgs prior_args(const Geometry& g, float scale)
+{
+    PriorArgs p;
+    p.m1 = g.prior_m1;
+    p.m2 = g.prior_m2;
+    p.a1 = g.prior_a1 * scale;
+    p.a2 = g.prior_a2 * scale;
+    return p;
+}
+
 static ProjArgs gnc_args(const Geometry& g, const WS& w)
 {
     const Schedule& S = g.sch[kSchedAdj];
@@ -1064,7 +1075,7 @@ pget_status pget_vjp(pget_geometry h, const float* lam, const float* mu, const f
     if ((st = proj_adjoint(g, w, MODE_VJP, wv, s))) return st;
     finish_kernel<<<dim3(vec_grid(static_cast<size_t>(N) * N), B), kVecThreads, 0, s>>>(
         w.gacc, proj_cfg(g, MODE_VJP).G, nullptr, nullptr, 0.f, 0.f, 1.f, g_lam, g_mu, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-        nullptr, nullptr, nullptr, N); note();
+        nullptr, nullptr, nullptr, N, PriorArgs{}); note();
     CK(cudaGetLastError());
     return PGET_OK;
 }
@@ -1104,7 +1115,7 @@ pget_status pget_gn_apply(pget_geometry h, const float* lam, const float* mu, co
     }
     finish_kernel<<<dim3(vec_grid(static_cast<size_t>(N) * N), B), kVecThreads, 0, s>>>(
         w.gacc, proj_cfg(g, MODE_GN).G, p_lam, p_mu, alpha, beta, 1.f, q_lam, q_mu, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-        nullptr, nullptr, nullptr, N); note();
+        nullptr, nullptr, nullptr, N, prior_args(g, 1.f)); note();
     CK(cudaGetLastError());
     return PGET_OK;
 }
@@ -1115,15 +1126,19 @@ pget_status pget_gn_apply(pget_geometry h, const float* lam, const float* mu, co
 static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const float* mu,
                               const float* y_meas, float alpha, float beta, const float* betav, int32_t n_cg,
                               uint32_t flags, float* s_lam, float* s_mu, pget_gn_stats* stats, const float4* box,
-                              cudaStream_t s)
+                              cudaStream_t s, float pscale = 1.f)
 {
     pget_status st;
     const int N = g.desc.n_px, B = g.desc.batch;
     const int n2 = N * N;
     const int nsper = g.n_ab * g.desc.n_det;
     const dim3 vg(kNblk, B);
-    double* P[8];
-    for (int k = 0; k < 8; ++k) P[k] = w.part + static_cast<size_t>(k) * B * kNblk;
+    double* P[9];
+    for (int k = 0; k < 9; ++k) P[k] = w.part + static_cast<size_t>(k) * B * kNblk;
+    // priors (pget_set_prior) at the continuation scale pscale; P[8] holds their value partials
+    const PriorArgs pr = prior_args(g, pscale);
+    const bool has_prior = pr.m1 || pr.m2;
+    double* Pp = has_prior ? P[8] : nullptr;
     const int sgrid = (B + 127) / 128;
     const int Gv = proj_cfg(g, MODE_VJP).G, Gg = proj_cfg(g, MODE_GN).G;
 
@@ -1132,16 +1147,17 @@ static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const f
     if ((st = fwd_out(g, w, w.ysino, s))) return st;
     residual_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, y_meas, P[0], nsper); note();
     regsq_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, P[1], N); note();
+    if (has_prior) priorsq_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, pr, Pp, N); note();
     CK(cudaGetLastError());
-    // 3: b = -(J^T r + alpha L^T L u); z = p = b; s = 0; ||b||^2
+    // 3: b = -(J^T r + alpha L^T L u (+ P^T P u)); z = p = b; s = 0; ||b||^2
     const bool cached = g.adj_seg && g.gn_cached;
     // the gradient VJP also writes the GN Jacobian-entry cache (fused cache build)
     // F(u) above was the segmented forward: its phase-A partials of u are the VJP's phase A
     if ((st = proj_adjoint(g, w, MODE_VJP, w.ysino, s, cached && n_cg > 0, g.adj_seg && g.fwd_seg))) return st;
     finish_kernel<<<vg, kVecThreads, 0, s>>>(w.gacc, Gv, lam, mu, alpha, 0.f, -1.f, w.bl, w.bm, w.bl, w.bm, P[2], w.zl,
-                                            w.zm, w.pl, w.pm, s_lam, s_mu, N); note();
+                                            w.zm, w.pl, w.pm, s_lam, s_mu, N, pr); note();
     CK(cudaGetLastError());
-    scalar_kernel<<<sgrid, 128, 0, s>>>(SC_INIT, 0, P[0], P[1], P[2], kNblk, w.cg, stats, B, alpha, beta, betav); note();
+    scalar_kernel<<<sgrid, 128, 0, s>>>(SC_INIT, 0, P[0], P[1], P[2], kNblk, w.cg, stats, B, alpha, beta, betav, Pp); note();
     CK(cudaGetLastError());
 
     // 5: CG
@@ -1164,8 +1180,9 @@ static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const f
             const bool mirror = k + 1 < n_cg && (!cached || g.gn_hybrid);
             float4* i4n = mirror ? w.img4[0] : nullptr;
             float4* i4t = mirror ? w.img4[1] : nullptr;
+            PriorArgs prv = pr;
             void* args[] = {&w.gacc, &GG, &al, &be, &bv, &s_lam, &s_mu, &w.zl, &w.zm, &w.pl, &w.pm, &w.ql, &w.qm,
-                            &pg, &pz, &cgs, &stats, &kk, &NN, &BB, &nb, &i4n, &i4t, &PP};
+                            &pg, &pz, &cgs, &stats, &kk, &NN, &BB, &nb, &i4n, &i4t, &PP, &prv};
             const int grid = std::min(B * kNblk, g.cg_coop_blocks);
             CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cg_fused_kernel), dim3(grid), dim3(kVecThreads),
                                            args, 0, s));
@@ -1208,8 +1225,9 @@ static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const f
         sumsq_kernel<<<vg, kVecThreads, 0, s>>>(w.dysino, P[5], nsper); note();
     }
     regsq_kernel<<<vg, kVecThreads, 0, s>>>(s_lam, s_mu, P[6], N); note();
+    if (has_prior) priorsq_kernel<<<vg, kVecThreads, 0, s>>>(s_lam, s_mu, pr, Pp, N); note();
     dot2_kernel<<<vg, kVecThreads, 0, s>>>(w.bl, w.bm, s_lam, s_mu, P[7], n2); note();
-    scalar_kernel<<<sgrid, 128, 0, s>>>(SC_PRED, 0, P[5], P[6], P[7], kNblk, w.cg, stats, B, alpha, beta, betav); note();
+    scalar_kernel<<<sgrid, 128, 0, s>>>(SC_PRED, 0, P[5], P[6], P[7], kNblk, w.cg, stats, B, alpha, beta, betav, Pp); note();
     CK(cudaGetLastError());
     // 7-8: f(u+s), rho, accept, beta_next
     if (flags & PGET_GN_EVAL_TRIAL) {
@@ -1217,7 +1235,8 @@ static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const f
         if ((st = fwd_out(g, w, w.ysino, s))) return st;
         residual_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, y_meas, P[0], nsper); note();
         regsq_kernel<<<vg, kVecThreads, 0, s>>>(w.ul, w.um, P[1], N); note();
-        scalar_kernel<<<sgrid, 128, 0, s>>>(SC_TRIAL, 0, P[0], P[1], nullptr, kNblk, w.cg, stats, B, alpha, beta, betav); note();
+        if (has_prior) priorsq_kernel<<<vg, kVecThreads, 0, s>>>(w.ul, w.um, pr, Pp, N); note();
+        scalar_kernel<<<sgrid, 128, 0, s>>>(SC_TRIAL, 0, P[0], P[1], nullptr, kNblk, w.cg, stats, B, alpha, beta, betav, Pp); note();
         CK(cudaGetLastError());
     }
     return PGET_OK;
@@ -1268,12 +1287,16 @@ pget_status pget_lm_solve(pget_geometry h, float* lam, float* mu, const float* y
         clamp_kernel<<<vec_grid(n), kVecThreads, 0, s>>>(lam, mu, n, box.x, box.y, box.z, box.w); note();
         CK(cudaGetLastError());
     }
-    double alpha = p.alpha0;
+    double alpha = p.alpha0, pscale = 1.0;
     for (int k = 0; k < p.n_iter; ++k) {
-        if (k > 0 && k <= p.k_freeze) alpha /= p.alpha_decay;   // alpha_k = alpha0 / decay^min(k, k_freeze)
+        if (k > 0 && k <= p.k_freeze) {   // (alpha, alpha1, alpha2)_k = (alpha, alpha1, alpha2)_0 / decay^min(k, k_freeze)
+            alpha /= p.alpha_decay;
+            pscale /= p.alpha_decay;
+        }
         pget_gn_stats* sk = stats + static_cast<size_t>(k) * B;
         if ((st = gn_cg_impl(g, w, lam, mu, y_meas, static_cast<float>(alpha), 0.f, w.beta, p.n_cg,
-                             PGET_GN_EVAL_TRIAL, w.sl, w.sm, sk, use_box ? &box : nullptr, s)))
+                             PGET_GN_EVAL_TRIAL, w.sl, w.sm, sk, use_box ? &box : nullptr, s,
+                             static_cast<float>(pscale))))
             return st;
         lm_update_kernel<<<dim3(vec_grid(n2), B), kVecThreads, 0, s>>>(lam, mu, w.ul, w.um, sk, w.beta, n2); note();
         CK(cudaGetLastError());
@@ -1304,8 +1327,8 @@ pget_status pget_safeguard(pget_geometry h, const float* lam, const float* mu, c
     const int n2 = N * N;
     const int nsper = g.n_ab * g.desc.n_det;
     const dim3 vg(kNblk, B);
-    double* P[12];
-    for (int k = 0; k < 12; ++k) P[k] = w.part + static_cast<size_t>(k) * B * kNblk;
+    double* P[18];
+    for (int k = 0; k < 18; ++k) P[k] = w.part + static_cast<size_t>(k) * B * kNblk;
     const size_t nimg = static_cast<size_t>(B) * n2;
     // s~ = u~ - u;  F(u) and J s~ in one JVP launch
     diff2_kernel<<<vec_grid(nimg), kVecThreads, 0, s>>>(cand_lam, cand_mu, lam, mu, w.zl, w.zm, nimg); note();
@@ -1328,10 +1351,38 @@ pget_status pget_safeguard(pget_geometry h, const float* lam, const float* mu, c
     if ((st = proj_out(g, w, MODE_FWD, w.ysino, nullptr, s))) return st;
     residual_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, y_meas, P[10], nsper); note();
     regsq_kernel<<<vg, kVecThreads, 0, s>>>(cand_lam, cand_mu, P[11], N); note();
-    guard_scalar_kernel<<<(B + 127) / 128, 128, 0, s>>>(w.part, kNblk, B, alpha, kappa, stats); note();
+    // priors (pget_set_prior): the rows sqrt(a1) P1 lam, sqrt(a2) P2 mu of F~ in f, m_k(s~), m_k(s_k), f(u~)
+    const PriorArgs pr = prior_args(g, 1.f);
+    const bool has_prior = pr.m1 || pr.m2;
+    if (has_prior) {
+        priorsq_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, pr, P[12], N); note();
+        priordot_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, w.zl, w.zm, pr, P[13], P[14], N); note();
+        priordot_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, s_lam, s_mu, pr, P[15], P[16], N); note();
+        priorsq_kernel<<<vg, kVecThreads, 0, s>>>(cand_lam, cand_mu, pr, P[17], N); note();
+    }
+    guard_scalar_kernel<<<(B + 127) / 128, 128, 0, s>>>(w.part, kNblk, B, alpha, kappa, stats, has_prior ? 1 : 0); note();
     guard_select_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, s_lam, s_mu, cand_lam, cand_mu, stats, u_next_lam,
                                                   u_next_mu, n2); note();
     CK(cudaGetLastError());
+    return PGET_OK;
+}
+
+pget_status pget_set_prior(pget_geometry h, const pget_prior* prior)
+{
+    if (!h) return fail(PGET_ERR_INVALID_ARGUMENT, "NULL geometry handle");
+    if (h->g.device < 0) return fail(PGET_ERR_INVALID_ARGUMENT, "pget_set_prior: host-only handle");
+    Geometry& g = h->g;
+    if (!prior) {
+        g.prior_m1 = g.prior_m2 = nullptr;
+        g.prior_a1 = g.prior_a2 = 0.f;
+        return PGET_OK;
+    }
+    if (!std::isfinite(prior->alpha1) || !std::isfinite(prior->alpha2) || prior->alpha1 < 0.f || prior->alpha2 < 0.f)
+        return fail(PGET_ERR_INVALID_ARGUMENT, "pget_set_prior: alpha1, alpha2 must be finite and >= 0");
+    g.prior_m1 = prior->mask_lam;
+    g.prior_m2 = prior->mask_mu;
+    g.prior_a1 = prior->mask_lam ? prior->alpha1 : 0.f;
+    g.prior_a2 = prior->mask_mu ? prior->alpha2 : 0.f;
     return PGET_OK;
 }
 

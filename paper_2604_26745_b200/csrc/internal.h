@@ -182,6 +182,10 @@ struct Geometry {
     // pget_gn_apply through the cache too (one product per call: building the cache costs more than
     // it saves; tests set PGET_GN_APPLY_CACHED=1 to pin the cached product at the operator tolerance)
     bool gn_apply_cached = false;
+    // geometry priors attached by pget_set_prior (caller-owned device masks; null = off)
+    const float* prior_m1 = nullptr;
+    const float* prior_m2 = nullptr;
+    float prior_a1 = 0.f, prior_a2 = 0.f;
     int cellmax = 1;        // max consecutive samples of one ray inside one pixel cell
     double cache_max_gb = 48.0;   // larger caches fall back to the recomputing GN product (config 5: 25 GB)
     bool gn_hybrid = true;   // cached scatter with the recomputed (J p) (PGET_GN_CACHE=1)

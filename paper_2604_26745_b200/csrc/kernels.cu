@@ -97,6 +97,13 @@ __device__ __forceinline__ float lap_at(const float* __restrict__ x, int N, int 
     return s;
 }
 
+// (P1^T P1 x_lam, P2^T P2 x_mu) weighted, added to (ol, om) at element k of [B][N][N] (priors)
+__device__ __forceinline__ void prior_op(const PriorArgs& pr, size_t k, float xl, float xm, float& ol, float& om)
+{
+    if (pr.m1) { const float m = pr.m1[k]; ol += pr.a1 * (m * m) * xl; }
+    if (pr.m2) { const float m = pr.m2[k]; om += pr.a2 * (m * m) * xm; }
+}
+
 __device__ __forceinline__ float lap2_at(const float* __restrict__ x, int N, int j, int i)
 {
     return 4.f * lap_at(x, N, j, i) - lap_at(x, N, j, i - 1) - lap_at(x, N, j, i + 1) -
@@ -111,7 +118,7 @@ __global__ void finish_kernel(const double2* __restrict__ part, int G, const flo
                               const float* __restrict__ xm, float alpha, float beta, float sign,
                               float* outl, float* outm, const float* __restrict__ dotl,
                               const float* __restrict__ dotm, double* partial, float* copy1l, float* copy1m,
-                              float* copy2l, float* copy2m, float* zerol, float* zerom, int N)
+                              float* copy2l, float* copy2m, float* zerol, float* zerom, int N, PriorArgs pr)
 {
     __shared__ double sh[32];
     const int m = blockIdx.y;
@@ -141,6 +148,7 @@ __global__ void finish_kernel(const double2* __restrict__ part, int G, const flo
             const float* pm = xm + base;
             ol += alpha * lap2_at(pl, N, j, i) + beta * pl[e];
             om += alpha * lap2_at(pm, N, j, i) + beta * pm[e];
+            prior_op(pr, base + e, pl[e], pm[e], ol, om);
         }
         ol *= sign;
         om *= sign;
@@ -202,6 +210,53 @@ __global__ void regsq_kernel(const float* __restrict__ xl, const float* __restri
     }
     const double t = block_sum(s, sh);
     if (threadIdx.x == 0) partial[m * gridDim.x + blockIdx.x] = t;
+}
+
+// priors: partial sum a1 (m1 x_lam)^2 + a2 (m2 x_mu)^2 (twice the penalty)
+__global__ void priorsq_kernel(const float* __restrict__ xl, const float* __restrict__ xm, PriorArgs pr,
+                               double* partial, int N)
+{
+    __shared__ double sh[32];
+    const int m = blockIdx.y;
+    const size_t n2 = static_cast<size_t>(N) * N;
+    double s = 0.0;
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n2;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const size_t k = m * n2 + e;
+        if (pr.m1) { const double a = static_cast<double>(pr.m1[k]) * xl[k]; s += static_cast<double>(pr.a1) * a * a; }
+        if (pr.m2) { const double a = static_cast<double>(pr.m2[k]) * xm[k]; s += static_cast<double>(pr.a2) * a * a; }
+    }
+    const double t = block_sum(s, sh);
+    if (threadIdx.x == 0) partial[m * gridDim.x + blockIdx.x] = t;
+}
+
+// priors: partials sum a m^2 u s (pdot) and sum a (m s)^2 (psq) over both parts
+__global__ void priordot_kernel(const float* __restrict__ ul, const float* __restrict__ um,
+                                const float* __restrict__ sl, const float* __restrict__ sm, PriorArgs pr,
+                                double* pdot, double* psq, int N)
+{
+    __shared__ double sh[32];
+    const int m = blockIdx.y;
+    const size_t n2 = static_cast<size_t>(N) * N;
+    double d = 0.0, q = 0.0;
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n2;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const size_t k = m * n2 + e;
+        if (pr.m1) {
+            const double w = static_cast<double>(pr.a1) * pr.m1[k] * pr.m1[k];
+            d += w * ul[k] * sl[k];
+            q += w * sl[k] * sl[k];
+        }
+        if (pr.m2) {
+            const double w = static_cast<double>(pr.a2) * pr.m2[k] * pr.m2[k];
+            d += w * um[k] * sm[k];
+            q += w * sm[k] * sm[k];
+        }
+    }
+    const double td = block_sum(d, sh);
+    if (threadIdx.x == 0) pdot[m * gridDim.x + blockIdx.x] = td;
+    const double tq = block_sum(q, sh);
+    if (threadIdx.x == 0) psq[m * gridDim.x + blockIdx.x] = tq;
 }
 
 // partial <a, b> over both parts
@@ -325,18 +380,21 @@ __global__ void diff2_kernel(const float* __restrict__ al, const float* __restri
 // one thread per member.  P: [0] 1/2||r||^2  [1] ||Lu||^2  [2] <r,Js~>  [3] ||Js~||^2  [4] <Lu,Ls~>
 // [5] ||Ls~||^2  [6..9] the same four for s_k  [10] 1/2||F(u~)-y||^2  [11] ||Lu~||^2
 __global__ void guard_scalar_kernel(const double* P, int nblk, int B, double alpha, double kappa,
-                                    pget_safeguard_stats* out)
+                                    pget_safeguard_stats* out, int has_prior)
 {
     const int m = blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= B) return;
     auto v = [&](int k) { return psum(P + static_cast<size_t>(k) * B * nblk, m, nblk); };
+    // priors (the rows sqrt(a1) P1 lam, sqrt(a2) P2 mu of F~): 12 sum a (m u)^2, 13/14 <u, s~>_P and
+    // ||s~||_P^2, 15/16 the same for s_k, 17 sum a (m u~)^2
+    auto w = [&](int k) { return has_prior ? v(k) : 0.0; };
     pget_safeguard_stats S;
-    S.f = v(0) + 0.5 * alpha * v(1);
-    S.m_cand = S.f + v(2) + alpha * v(4) + 0.5 * (v(3) + alpha * v(5));
-    S.m_lm = S.f + v(6) + alpha * v(8) + 0.5 * (v(7) + alpha * v(9));
+    S.f = v(0) + 0.5 * alpha * v(1) + 0.5 * w(12);
+    S.m_cand = S.f + v(2) + alpha * v(4) + w(13) + 0.5 * (v(3) + alpha * v(5) + w(14));
+    S.m_lm = S.f + v(6) + alpha * v(8) + w(15) + 0.5 * (v(7) + alpha * v(9) + w(16));
     S.pred_cand = S.f - S.m_cand;
     S.pred_lm = S.f - S.m_lm;
-    S.f_cand = v(10) + 0.5 * alpha * v(11);
+    S.f_cand = v(10) + 0.5 * alpha * v(11) + 0.5 * w(17);
     S.rho_cand = S.pred_cand != 0.0 ? (S.f - S.f_cand) / S.pred_cand : 0.0;
     S.kappa = kappa;
     S.accepted = (S.m_cand <= S.m_lm && S.pred_cand > 0.0 && S.rho_cand > kappa) ? 1 : 0;
@@ -407,7 +465,7 @@ __global__ void fill_kernel(float* x, float v, int n)
 // Scalar steps of the LM iteration (one thread per member).
 __global__ void scalar_kernel(int op, int k, const double* p0, const double* p1, const double* p2, int nblk,
                               CGState* st, pget_gn_stats* stats, int B, double alpha, double beta_h,
-                              const float* betav)
+                              const float* betav, const double* pp)
 {
     const int m = blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= B) return;
@@ -418,6 +476,7 @@ __global__ void scalar_kernel(int op, int k, const double* p0, const double* p1,
         const double mis = psum(p0, m, nblk), lq = psum(p1, m, nblk), bb = psum(p2, m, nblk);
         S.misfit = mis;
         S.reg = 0.5 * alpha * lq;
+        if (pp) S.reg += 0.5 * psum(pp, m, nblk);   // priors: pp = sum a (m x)^2 of u
         S.f = mis + S.reg;
         S.grad_norm = sqrt(bb);
         S.cg_res[0] = sqrt(bb);
@@ -450,10 +509,12 @@ __global__ void scalar_kernel(int op, int k, const double* p0, const double* p1,
         const double js2 = psum(p0, m, nblk), ls2 = psum(p1, m, nblk), bs = psum(p2, m, nblk);
         S.js2 = js2;
         S.als2 = alpha * ls2;
+        if (pp) S.als2 += psum(pp, m, nblk);   // priors of s
         S.bs = bs;
-        S.pred = bs - 0.5 * (js2 + alpha * ls2);
+        S.pred = bs - 0.5 * (js2 + S.als2);
     } else if (op == SC_TRIAL) {     // p0: 1/2||r(u+s)||^2, p1: ||L(u+s)||^2
-        const double f1 = psum(p0, m, nblk) + 0.5 * alpha * psum(p1, m, nblk);
+        double f1 = psum(p0, m, nblk) + 0.5 * alpha * psum(p1, m, nblk);
+        if (pp) f1 += 0.5 * psum(pp, m, nblk);   // priors of u + s
         S.f_trial = f1;
         S.rho = (S.f - f1) / S.pred;
         S.accepted = S.rho > 0.1;
@@ -475,7 +536,7 @@ __global__ void cg_fused_kernel(const double2* __restrict__ part, int G, float a
                                 const float* betav, float* sl, float* sm, float* zl, float* zm, float* pl,
                                 float* pm, float* ql, float* qm, double* pg, double* pz, CGState* st,
                                 pget_gn_stats* stats, int k, int N, int B, int nblk, float4* img4n, float4* img4t,
-                                int P)
+                                int P, PriorArgs pr)
 {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
@@ -514,8 +575,9 @@ __global__ void cg_fused_kernel(const double2* __restrict__ part, int G, float a
                 }
                 const float* xl = pl + base;
                 const float* xm = pm + base;
-                const float ol = static_cast<float>(a.x) + alpha * lap2_at(xl, N, jj, i) + beta * xl[e];
-                const float om = static_cast<float>(a.y) + alpha * lap2_at(xm, N, jj, i) + beta * xm[e];
+                float ol = static_cast<float>(a.x) + alpha * lap2_at(xl, N, jj, i) + beta * xl[e];
+                float om = static_cast<float>(a.y) + alpha * lap2_at(xm, N, jj, i) + beta * xm[e];
+                prior_op(pr, base + e, xl[e], xm[e], ol, om);
                 ql[base + e] = ol;
                 qm[base + e] = om;
                 dsum += static_cast<double>(ol) * xl[e] + static_cast<double>(om) * xm[e];

@@ -64,6 +64,14 @@ struct CGState {
 };
 
 
+// geometry priors P1, P2 (pget_set_prior): weights already scaled by the LM continuation; a null mask
+// switches its term off
+struct PriorArgs {
+    const float* m1;
+    const float* m2;
+    float a1, a2;
+};
+
 __global__ void pack2_kernel(const float* lam, const float* mu, const float* slam, const float* smu, float2* out,
                              float2* outT, float* ut_lam, float* ut_mu, int N, int P, int B, int has_box,
                              float4 box);
@@ -81,10 +89,13 @@ __global__ void reduce_slots_kernel(const float2* slots, double2* part, int N, i
 __global__ void finish_kernel(const double2* part, int G, const float* xl, const float* xm, float alpha, float beta,
                               float sign, float* outl, float* outm, const float* dotl, const float* dotm,
                               double* partial, float* copy1l, float* copy1m, float* copy2l, float* copy2m,
-                              float* zerol, float* zerom, int N);
+                              float* zerol, float* zerom, int N, PriorArgs pr);
 __global__ void residual_kernel(float* y, const float* ymeas, double* partial, int nper);
 __global__ void sumsq_kernel(const float* x, double* partial, int nper);
 __global__ void regsq_kernel(const float* xl, const float* xm, double* partial, int N);
+__global__ void priorsq_kernel(const float* xl, const float* xm, PriorArgs pr, double* partial, int N);
+__global__ void priordot_kernel(const float* ul, const float* um, const float* sl, const float* sm, PriorArgs pr,
+                                double* pdot, double* psq, int N);
 __global__ void dot2_kernel(const float* al, const float* am, const float* bl, const float* bm, double* partial,
                             int n2);
 __global__ void cg_update1_kernel(float* sl, float* sm, float* zl, float* zm, const float* pl, const float* pm,
@@ -94,20 +105,20 @@ __global__ void cg_update2_kernel(const float* zl, const float* zm, float* pl, f
 __global__ void cg_fused_kernel(const double2* part, int G, float alpha, float beta_h, const float* betav, float* sl,
                                 float* sm, float* zl, float* zm, float* pl, float* pm, float* ql, float* qm,
                                 double* pg, double* pz, CGState* st, pget_gn_stats* stats, int k, int N, int B,
-                                int nblk, float4* img4n, float4* img4t, int P);
+                                int nblk, float4* img4n, float4* img4t, int P, PriorArgs pr);
 __global__ void dotsq_kernel(const float* a, const float* b, double* pdot, double* psq, int nper);
 __global__ void lapdot_kernel(const float* ul, const float* um, const float* sl, const float* sm, double* pdot,
                               double* psq, int N);
 __global__ void diff2_kernel(const float* al, const float* am, const float* bl, const float* bm, float* ol,
                              float* om, size_t n);
 __global__ void guard_scalar_kernel(const double* P, int nblk, int B, double alpha, double kappa,
-                                    pget_safeguard_stats* out);
+                                    pget_safeguard_stats* out, int has_prior);
 __global__ void guard_select_kernel(const float* ul, const float* um, const float* sl, const float* sm,
                                     const float* cl, const float* cm, const pget_safeguard_stats* st, float* ol,
                                     float* om, int n2);
 __global__ void scalar_kernel(int op, int k, const double* p0, const double* p1, const double* p2, int nblk,
                               CGState* st, pget_gn_stats* stats, int B, double alpha, double beta_h,
-                              const float* betav);
+                              const float* betav, const double* pp = nullptr);
 
 }  // namespace pget
 

@@ -54,7 +54,7 @@ def _candidates(l0, m0, sl, sm, lt, mt, seed, more=None):
     return out
 
 
-def _check(pg, gd, g, lam, mu, y, sl, sm, lt, mt, alpha, seed=11, kappa=0.1, more=None):
+def _check(pg, gd, g, lam, mu, y, sl, sm, lt, mt, alpha, seed=11, kappa=0.1, more=None, prior=None):
     f32 = lambda a: np.asarray(a, dtype=np.float32)
     lam, mu, y, sl, sm = f32(lam), f32(mu), f32(y), f32(sl), f32(sm)
     B = gd["batch"]
@@ -64,7 +64,7 @@ def _check(pg, gd, g, lam, mu, y, sl, sm, lt, mt, alpha, seed=11, kappa=0.1, mor
         cl, cm = f32(cl), f32(cm)
         (ul, um), S = pg.safeguard(g, dev(lam), dev(mu), dev(y), dev(sl), dev(sm), dev(cl), dev(cm), alpha, kappa)
         torch.cuda.synchronize()
-        (ol, om), So = O.safeguard(gd, lam, mu, y, sl, sm, cl, cm, alpha, kappa)
+        (ol, om), So = O.safeguard(gd, lam, mu, y, sl, sm, cl, cm, alpha, kappa, prior=prior)
         r = O.forward(gd, lam, mu) - y
         js_c = O.jvp(gd, lam, mu, cl - lam, cm - mu)
         js_l = O.jvp(gd, lam, mu, sl, sm)
