@@ -366,9 +366,6 @@ struct RayB {   // per-ray constants of sweep B
 // PAIRED adds the opposite-bank ray of the same line (its detector at the low-i end):
 //   E'_i = e^{-(S - A_i)},  a_lam += w'_r Delta E'_i,  a_mu += -w'_r Delta^2 (Q'_i + lam_i E'_i / 2),
 //   Q'_i = sum_{k>i} lam_k E'_k  (samples farther from that detector, already visited).
-#ifndef PGET_GNB_L1PF
-#define PGET_GNB_L1PF 0   // gnb_kernel: L1 prefetch distance in entry rows (0: none; experiment)
-#endif
 #ifndef PGET_PF_DIST
 #define PGET_PF_DIST 8   // samples between a cache entry's L2 prefetch and its use (4: +4 %, 16: +0.6 %, 32: +3 %, none: +3 % LM; scripts/pf_exp.sh)
 #endif
@@ -1520,7 +1517,7 @@ __device__ __forceinline__ void walk_jvpc(const float2* __restrict__ img, int P,
 // two, |value * S| < 2^22 by construction, see gnb_kernel), rounded to integers with the
 // 1.5 * 2^23 magic-number FFMA and added.  Integer addition is associative, so the result does not
 // depend on the order in which warps and lanes add.
-static_assert(PGET_PF_DIST + 4 <= kCachePadRows && PGET_GNB_L1PF <= kCachePadRows, "cache read-ahead exceeds the padding");
+static_assert(PGET_PF_DIST + 4 <= kCachePadRows, "cache read-ahead exceeds the padding");
 __device__ __forceinline__ void red_s32(uint32_t addr, int v)
 {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
@@ -1571,9 +1568,6 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
         const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;
         const float2 av = make_float2(fmaf(wr, c.x, wr1 * c.z), fmaf(wr, c.y, wr1 * c.w));
         asm volatile("prefetch.global.L2 [%0];" ::"l"(p + PGET_PF_DIST * 32));
-#if PGET_GNB_L1PF > 0
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(p + PGET_GNB_L1PF * 32));
-#endif
         c = __ldg(p + 4 * 32);
         p += 32;
         const float2 tv = __fmul2_rn(av, make_float2(fv, fv));         // row j0+1
