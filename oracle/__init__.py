@@ -50,8 +50,10 @@ def _load():
             ("orc_jvp", [P] * 7), ("orc_vjp", [P] * 6), ("orc_n_t", [P]),
             ("orc_gn_cg_step", [P, P, P, P, C.c_double, C.c_double, C.c_int, P, P, P]),
             ("orc_apply_H", [P, P, P, C.c_double, C.c_double, P, P]),
+            ("orc_lm_step_box", [P, P, P, P, C.c_double, C.c_double, C.c_int, P, C.c_int, P, P, P]),
             ("orc_safeguard", [P, P, P, P, P, P, P, P, C.c_double, C.c_double, P, P]),
-            ("orc_lm_solve", [P, P, P, P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_double, P, P]),
+            ("orc_lm_solve", [P, P, P, P, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int, C.c_double, P, C.c_int,
+                              P]),
         ]:
             f = getattr(_lib, name)
             f.argtypes = args
@@ -208,6 +210,22 @@ def gn_cg_step(g, lam, mu, y, alpha, beta, n_cg, prior=None):
     return sl, sm, stats_dict(st, n_cg)
 
 
+def lm_step_box(g, lam, mu, y, alpha, beta, n_it, box, inner="sgp", prior=None):
+    """One LM iteration inside a box: CG + projection (inner="cg") or SGP (O11).  Returns (s_lam, s_mu,
+    stats dict)."""
+    lib = _load()
+    d = _desc(g)
+    lam, mu, y = _f64(lam), _f64(mu), _f64(y)
+    bx = np.ascontiguousarray(box, dtype=np.float64)
+    sl, sm = np.zeros(img_shape(g)), np.zeros(img_shape(g))
+    st = np.zeros(ST_CG + n_it + 1)
+    with _Prior(g, prior):
+        rc = lib.orc_lm_step_box(C.byref(d), _p(lam), _p(mu), _p(y), float(alpha), float(beta), int(n_it), _p(bx),
+                                 int(inner == "sgp"), _p(sl), _p(sm), _p(st))
+    assert rc == 0, rc
+    return sl, sm, stats_dict(st, n_it)
+
+
 def stats_dict(st, n_cg):
     return dict(f=st[0], misfit=st[1], reg=st[2], grad_norm=st[3], pred=st[4], f_trial=st[5],
                 rho=st[6], accepted=bool(st[7]), beta_next=st[8], n_cg_done=int(st[9]),
@@ -256,9 +274,11 @@ def safeguard(g, lam, mu, y, s_lam, s_mu, c_lam, c_mu, alpha, kappa=0.1, prior=N
     return (nl, nm), res
 
 
-def lm_solve(g, lam, mu, y, n_iter, n_cg, alpha0, alpha_decay=5.0, k_freeze=0, beta0=0.0, box=None, prior=None):
-    """O9: n_iter LM iterations per batch member.  Returns ((lam, mu), [[stats dict per iteration]
-    per member])."""
+def lm_solve(g, lam, mu, y, n_iter, n_cg, alpha0, alpha_decay=5.0, k_freeze=0, beta0=0.0, box=None, prior=None,
+             inner="cg"):
+    """O9: n_iter LM iterations per batch member (inner solver "cg", or "sgp" (O11) with a box).
+    Returns ((lam, mu), [[stats dict per iteration] per member])."""
+    assert inner in ("cg", "sgp") and (inner == "cg" or box is not None)
     lib = _load()
     B = int(g.get("batch", 1))
     shp = img_shape(g)
@@ -274,7 +294,7 @@ def lm_solve(g, lam, mu, y, n_iter, n_cg, alpha0, alpha_decay=5.0, k_freeze=0, b
         with _Prior(g, prior, m):
             rc = lib.orc_lm_solve(C.byref(d), _p(l), _p(u), _p(np.ascontiguousarray(ys[m])), int(n_iter),
                                   int(n_cg), float(alpha0), float(alpha_decay), int(k_freeze), float(beta0),
-                                  None if bx is None else _p(bx), _p(st))
+                                  None if bx is None else _p(bx), int(inner == "sgp"), _p(st))
         assert rc == 0, rc
         lam_o[m], mu_o[m] = l, u
         row = ST_CG + n_cg + 1

@@ -20,6 +20,9 @@
  *       -- PAPER.md:160-180 eq:m-function, eq:LMA-step; PAPER.md:248 eq:rho_agreement
  *       -- inner solver: plain CG (reading Q12) instead of the paper's SGP.
  *   LM solve: alpha continuation, beta schedule, box projection -- PAPER.md:144-182, 288 (O9, N1)
+ *   SGP inner solver (O11, N1): the box-constrained LM subproblem by gradient projection with
+ *       Barzilai-Borwein steps and an exact line search -- PAPER.md:177 (bonettini2008scaled),
+ *       identity scaling (reading R-SGP)
  *   geometry priors (O10, N1): f += alpha1/2 ||P1 lam||^2 + alpha2/2 ||P2 mu||^2, P1, P2 diagonal
  *       masks -- PAPER.md:146-148 eq:lma_objective (reading R-prior), continued with alpha
  *       (alpha^(k) = (alpha1, alpha2) / 5^k); set by orc_set_prior, used by every
@@ -524,18 +527,26 @@ static double objective(const orc_desc* g, const double* lam, const double* mu, 
 /* One LM iteration; box (NULL or {lam_lo, lam_hi, mu_lo, mu_hi}) replaces the CG step by the step
  * actually taken inside the box, s' = clamp(u + s) - u, before pred and the trial (reading R-N1). */
 static int lm_step(const orc_desc* g, const double* lam, const double* mu, const double* y, double alpha,
-                   double beta, int n_cg, const double* box, double* s_lam, double* s_mu, double* stats);
+                   double beta, int n_cg, const double* box, int sgp, double* s_lam, double* s_mu, double* stats);
 
 int orc_gn_cg_step(const orc_desc* g, const double* lam, const double* mu, const double* y,
                    double alpha, double beta, int n_cg, double* s_lam, double* s_mu, double* stats)
 {
-    return lm_step(g, lam, mu, y, alpha, beta, n_cg, NULL, s_lam, s_mu, stats);
+    return lm_step(g, lam, mu, y, alpha, beta, n_cg, NULL, 0, s_lam, s_mu, stats);
 }
 
 static double clampd(double x, double lo, double hi) { return x < lo ? lo : (x > hi ? hi : x); }
 
+/* One LM iteration with the box {lam_lo, lam_hi, mu_lo, mu_hi}: CG then projection (sgp = 0, reading
+ * R-N1) or the SGP inner solver (sgp = 1, O11).  Stats as orc_gn_cg_step. */
+int orc_lm_step_box(const orc_desc* g, const double* lam, const double* mu, const double* y, double alpha,
+                    double beta, int n_it, const double* box, int sgp, double* s_lam, double* s_mu, double* stats)
+{
+    return lm_step(g, lam, mu, y, alpha, beta, n_it, box, sgp, s_lam, s_mu, stats);
+}
+
 static int lm_step(const orc_desc* g, const double* lam, const double* mu, const double* y, double alpha,
-                   double beta, int n_cg, const double* box, double* s_lam, double* s_mu, double* stats)
+                   double beta, int n_cg, const double* box, int sgp, double* s_lam, double* s_mu, double* stats)
 {
     size_t npx = (size_t)g->batch * g->n_px * g->n_px;
     size_t ns = (size_t)g->batch * g->n_angles * g->n_banks * g->n_det;
@@ -573,8 +584,48 @@ static int lm_step(const orc_desc* g, const double* lam, const double* mu, const
     }
     stats[0] = f0; stats[1] = misfit; stats[2] = reg; stats[3] = sqrt(dot(bvec, bvec, n2));
 
-    /* 5: CG from s0 = 0 on H s = b */
     hctx H = {g, lam, mu, alpha, beta, npx, ys, tl, tm};
+    if (sgp && box) {
+        /* 5': SGP (O11) on min q(s) = 1/2 s^T H s - b^T s over {s : u + s in box}, from s0 = 0 (u in
+         * the box).  gq = H s - b; d = P(u + s - a gq) - u - s (projection onto the box); stop when
+         * <gq, d> >= 0; lam_k = min(1, -<gq,d> / <d,Hd>) (exact minimiser of q on the segment, which
+         * stays feasible); s += lam_k d, gq += lam_k H d; a alternates the two Barzilai-Borwein
+         * lengths <ds,ds>/<ds,dg> and <ds,dg>/<dg,dg> (ds = lam_k d, dg = lam_k H d), clamped to
+         * [1e-10, 1e10]; a_0 = 1.  stats[ST_CG + k] = ||d_k||. */
+        double* gq = z;
+        double* d = p;
+        for (size_t i = 0; i < n2; ++i) gq[i] = -bvec[i];
+        double a = 1.0, beta_min2 = 0.0;
+        int k;
+        for (k = 0; k < n_cg; ++k) {
+            for (size_t i = 0; i < npx; ++i) {
+                d[i] = clampd(lam[i] + s[i] - a * gq[i], box[0], box[1]) - lam[i] - s[i];
+                d[npx + i] = clampd(mu[i] + s[npx + i] - a * gq[npx + i], box[2], box[3]) - mu[i] - s[npx + i];
+            }
+            double gd = dot(gq, d, n2), dd = dot(d, d, n2);
+            stats[ST_CG + k] = sqrt(dd);
+            if (!(gd < 0.0)) { stats[10] = 1.0; break; }
+            apply_H(&H, d, q);
+            double dHd = dot(d, q, n2);
+            if (k == 0) beta_min2 = 1e-3 * dHd / dd;
+            double lk = dHd > 0.0 ? fmin(1.0, -gd / dHd) : 1.0;
+            for (size_t i = 0; i < n2; ++i) { s[i] += lk * d[i]; gq[i] += lk * q[i]; }
+            double sy = lk * lk * dHd, ss = lk * lk * dd, yy = lk * lk * dot(q, q, n2);
+            double an = (k % 2 == 0) ? (sy > 0.0 ? ss / sy : 1e10) : (yy > 0.0 ? sy / yy : 1e10);
+            a = an < 1e-10 ? 1e-10 : (an > 1e10 ? 1e10 : an);
+        }
+        if (k == n_cg) {
+            for (size_t i = 0; i < npx; ++i) {
+                d[i] = clampd(lam[i] + s[i] - a * gq[i], box[0], box[1]) - lam[i] - s[i];
+                d[npx + i] = clampd(mu[i] + s[npx + i] - a * gq[npx + i], box[2], box[3]) - mu[i] - s[npx + i];
+            }
+            stats[ST_CG + n_cg] = sqrt(dot(d, d, n2));
+        }
+        stats[9] = k;
+        stats[11] = beta_min2;
+        goto step_done;
+    }
+    /* 5: CG from s0 = 0 on H s = b */
     memcpy(z, bvec, sizeof(double) * n2);
     memcpy(p, bvec, sizeof(double) * n2);
     double zeta = dot(z, z, n2);
@@ -597,8 +648,9 @@ static int lm_step(const orc_desc* g, const double* lam, const double* mu, const
     }
     stats[9] = k;
     stats[11] = beta_min;
+step_done:
 
-    /* (N1) the step actually taken inside the box */
+    /* (N1) the step actually taken inside the box (a no-op for the feasible SGP step) */
     if (box)
         for (size_t i = 0; i < npx; ++i) {
             s[i] = clampd(lam[i] + s[i], box[0], box[1]) - lam[i];
@@ -723,7 +775,8 @@ int orc_safeguard(const orc_desc* g, const double* lam, const double* mu, const 
  * u_k; with a box the initial guess is clamped and every step projected (lm_step).  lam, mu updated
  * in place; stats: n_iter rows of (ST_CG + n_cg + 1) doubles as orc_gn_cg_step's. */
 int orc_lm_solve(const orc_desc* g, double* lam, double* mu, const double* y, int n_iter, int n_cg,
-                 double alpha0, double decay, int k_freeze, double beta0, const double* box, double* stats)
+                 double alpha0, double decay, int k_freeze, double beta0, const double* box, int sgp,
+                 double* stats)
 {
     size_t npx = (size_t)g->batch * g->n_px * g->n_px;
     double* sl = (double*)malloc(sizeof(double) * npx);
@@ -737,7 +790,7 @@ int orc_lm_solve(const orc_desc* g, double* lam, double* mu, const double* y, in
         if (k > 0 && k <= k_freeze) { alpha /= decay; pscale /= decay; }   /* (alpha, alpha1, alpha2) / decay^k */
         g_prior.scale = pscale;
         double* st = stats + (size_t)k * row;
-        int rc = lm_step(g, lam, mu, y, alpha, beta, n_cg, box, sl, sm, st);
+        int rc = lm_step(g, lam, mu, y, alpha, beta, n_cg, box, sgp, sl, sm, st);
         if (rc) { g_prior.scale = 1.0; free(sl); free(sm); return rc; }
         if (st[7] != 0.0)
             for (size_t i = 0; i < npx; ++i) {

@@ -709,3 +709,79 @@ def test_p15_prior_pulls_masked_emission_down():
     (l_b, _), _ = O.lm_solve(g, l0, m0, y, 4, 8, 1e-3, beta0=0.01, prior=(m1, m2, 50.0, 0.0))
     out = m1 == 1.0
     assert np.sum(l_b[out] ** 2) < 0.5 * np.sum(l_a[out] ** 2)
+
+
+# ----------------------------------------------------------------------------- P16 SGP inner solver (O11, N1)
+def _sgp_case(n_px=8, n_angles=6):
+    g = P.geometry_desc(2, n_px=n_px, n_angles=n_angles)
+    lt, mt = P.make_phantom(2, n_px=n_px)
+    y = O.forward(g, lt, mt)
+    l0, m0 = P.initial_guess(n_px)
+    return g, y, (l0.astype(np.float64), m0.astype(np.float64))
+
+
+def _grad_b(g, l0, m0, y, alpha):
+    """b = -grad f(u) from a one-step CG solve (s = a b with a = <b,b>/<b,Hb>), independent of SGP."""
+    sl, sm, st = O.gn_cg_step(g, l0, m0, y, alpha, 0.0, 1)
+    a = np.sqrt(np.sum(sl ** 2) + np.sum(sm ** 2)) / st["grad_norm"]
+    return sl / a, sm / a
+
+
+def test_p16_sgp_iterates_feasible_and_monotone():
+    """u + s stays in the box; with beta = 0, pred = -q(s) and the exact line search makes q decrease
+    at every iteration."""
+    g, y, (l0, m0) = _sgp_case()
+    box = (0.0, 0.9, 0.0, 0.35)
+    preds = []
+    for n in range(1, 8):
+        sl, sm, st = O.lm_step_box(g, l0, m0, y, 1e-3, 0.0, n, box)
+        assert np.all(l0 + sl >= box[0] - 1e-15) and np.all(l0 + sl <= box[1] + 1e-15)
+        assert np.all(m0 + sm >= box[2] - 1e-15) and np.all(m0 + sm <= box[3] + 1e-15)
+        preds.append(st["pred"])
+    assert all(b >= a - 1e-12 * abs(a) for a, b in zip(preds, preds[1:])), preds
+    assert preds[-1] > preds[0] > 0
+
+
+def test_p16_sgp_matches_lbfgsb_on_the_box_qp():
+    """Converged SGP = the minimiser of q(s) = 1/2 s^T H s - b^T s over the box from scipy's L-BFGS-B
+    (H p through O.apply_H, b from an independent CG step)."""
+    from scipy.optimize import minimize
+    g, y, (l0, m0) = _sgp_case()
+    alpha = 1e-3
+    box = (0.0, 0.9, 0.0, 0.35)
+    bl, bm = _grad_b(g, l0, m0, y, alpha)
+    b = np.concatenate([bl.ravel(), bm.ravel()])
+    n = bl.size
+
+    def q_and_grad(x):
+        hl, hm = O.apply_H(g, l0, m0, alpha, 0.0, x[:n].reshape(bl.shape), x[n:].reshape(bl.shape))
+        hx = np.concatenate([hl.ravel(), hm.ravel()])
+        return 0.5 * x @ hx - b @ x, hx - b
+    lo = np.concatenate([box[0] - l0.ravel(), box[2] - m0.ravel()])
+    hi = np.concatenate([box[1] - l0.ravel(), box[3] - m0.ravel()])
+    ref = minimize(q_and_grad, np.zeros(2 * n), jac=True, method="L-BFGS-B", bounds=list(zip(lo, hi)),
+                   options=dict(maxiter=5000, ftol=1e-15, gtol=1e-12))
+    # alpha = 1e-3 leaves H ill-conditioned: gradient projection needs ~3000 iterations here
+    sl, sm, st = O.lm_step_box(g, l0, m0, y, alpha, 0.0, 3000, box)
+    x = np.concatenate([sl.ravel(), sm.ravel()])
+    assert q_and_grad(x)[0] <= ref.fun + 1e-10 * abs(ref.fun)
+    assert np.linalg.norm(x - ref.x) <= 1e-4 * np.linalg.norm(ref.x)
+    assert np.any(np.isclose(x, lo)) or np.any(np.isclose(x, hi))      # the box binds
+
+
+def test_p16_sgp_without_binding_box_is_the_newton_step():
+    """A box far away: SGP converges to the unconstrained minimiser H^{-1} b, as CG does."""
+    g, y, (l0, m0) = _sgp_case()
+    box = (-1e3, 1e3, -1e3, 1e3)
+    sl, sm, _ = O.lm_step_box(g, l0, m0, y, 1e-3, 0.0, 3000, box)
+    cl, cm, _ = O.gn_cg_step(g, l0, m0, y, 1e-3, 0.0, 400)
+    x, c = np.concatenate([sl.ravel(), sm.ravel()]), np.concatenate([cl.ravel(), cm.ravel()])
+    assert np.linalg.norm(x - c) <= 1e-4 * np.linalg.norm(c)
+
+
+def test_p16_lm_solve_with_sgp_decreases_f_inside_the_box():
+    g, y, (l0, m0) = _sgp_case(n_px=16, n_angles=8)
+    box = (0.0, 1.6, 0.0, 0.6)
+    (lk, mk), [sts] = O.lm_solve(g, l0, m0, y, 5, 10, 1e-3, beta0=0.01, box=box, inner="sgp")
+    assert sts[-1]["f_trial"] < 0.2 * sts[0]["f"]
+    assert lk.min() >= box[0] and lk.max() <= box[1] and mk.min() >= box[2] and mk.max() <= box[3]
