@@ -146,6 +146,10 @@ typedef struct {
 
 /* Parameters of pget_lm_solve (host struct).  (PAPER.md:144-182, 288.) */
 #define PGET_LM_BOX 1u   /* project every iterate onto [lam_lo, lam_hi] x [mu_lo, mu_hi] */
+#define PGET_LM_SGP 2u   /* with PGET_LM_BOX: solve each step's box-constrained subproblem by scaled gradient
+                          * projection (identity scaling, Barzilai-Borwein lengths, exact line
+                          * search, n_cg iterations; stats cg_res = ||d_k||, the projected-gradient step)
+                          * instead of CG followed by the projection */
 typedef struct {
     int32_t n_iter;       /* LM iterations                                                    */
     int32_t n_cg;         /* CG steps per iteration, 0 <= n_cg <= PGET_MAX_CG                  */
@@ -154,7 +158,7 @@ typedef struct {
     int32_t k_freeze;     /* iteration from which alpha stays fixed                            */
     float beta0;          /* initial LM parameter of every member                              */
     float lam_lo, lam_hi, mu_lo, mu_hi;   /* the box (PGET_LM_BOX)                              */
-    uint32_t flags;       /* PGET_LM_BOX                                                       */
+    uint32_t flags;       /* PGET_LM_BOX, PGET_LM_SGP                                          */
     int32_t pad_;
 } pget_lm_params;
 

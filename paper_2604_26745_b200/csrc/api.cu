@@ -1126,7 +1126,7 @@ pget_status pget_gn_apply(pget_geometry h, const float* lam, const float* mu, co
 static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const float* mu,
                               const float* y_meas, float alpha, float beta, const float* betav, int32_t n_cg,
                               uint32_t flags, float* s_lam, float* s_mu, pget_gn_stats* stats, const float4* box,
-                              cudaStream_t s, float pscale = 1.f)
+                              cudaStream_t s, float pscale = 1.f, bool sgp = false)
 {
     pget_status st;
     const int N = g.desc.n_px, B = g.desc.batch;
@@ -1161,7 +1161,35 @@ static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const f
     CK(cudaGetLastError());
 
     // 5: CG
-    for (int k = 0; k < n_cg; ++k) {
+    if (sgp && box) {   // 5': SGP (O11) instead of CG: s stays inside the box
+        const size_t nimg = static_cast<size_t>(B) * n2;
+        sgp_init_kernel<<<vec_grid(nimg), kVecThreads, 0, s>>>(w.bl, w.bm, w.zl, w.zm, w.cg, n2, B); note();
+        CK(cudaGetLastError());
+        for (int k = 0; k <= n_cg; ++k) {
+            // d = P(u + s - a g) - u - s into (pl, pm); the last pass only reports ||d||
+            sgp_dir_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, s_lam, s_mu, w.zl, w.zm, w.cg, *box, w.pl, w.pm, P[3],
+                                                      P[4], n2); note();
+            CK(cudaGetLastError());
+            if (k == n_cg) {
+                sgp_scalar_kernel<<<sgrid, 128, 0, s>>>(k, 1, P[3], P[4], nullptr, nullptr, kNblk, w.cg, stats, B); note();
+                break;
+            }
+            if (cached) {   // q = H d
+                if ((st = gnc_product(g, w, lam, mu, w.pl, w.pm, s))) return st;
+            } else {
+                if ((st = pack4(g, w, lam, mu, w.pl, w.pm, s))) return st;
+                if ((st = proj_adjoint(g, w, MODE_GN, nullptr, s))) return st;
+            }
+            finish_kernel<<<vg, kVecThreads, 0, s>>>(w.gacc, Gg, w.pl, w.pm, alpha, beta, 1.f, w.ql, w.qm, w.pl, w.pm,
+                                                    P[5], nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, N, pr,
+                                                    betav); note();
+            dot2_kernel<<<vg, kVecThreads, 0, s>>>(w.ql, w.qm, w.ql, w.qm, P[6], n2); note();
+            sgp_scalar_kernel<<<sgrid, 128, 0, s>>>(k, 0, P[3], P[4], P[5], P[6], kNblk, w.cg, stats, B); note();
+            sgp_update_kernel<<<vg, kVecThreads, 0, s>>>(s_lam, s_mu, w.zl, w.zm, w.pl, w.pm, w.ql, w.qm, w.cg, n2); note();
+            CK(cudaGetLastError());
+        }
+    }
+    for (int k = 0; k < n_cg && !(sgp && box); ++k) {
         // p of step k > 0 was packed by step k-1's fused CG kernel
         const bool packed = k > 0 && (!cached || g.gn_hybrid);
         if (cached) {
@@ -1276,6 +1304,9 @@ pget_status pget_lm_solve(pget_geometry h, float* lam, float* mu, const float* y
     const bool use_box = (p.flags & PGET_LM_BOX) != 0;
     if (use_box && !(p.lam_lo <= p.lam_hi && p.mu_lo <= p.mu_hi))
         return fail(PGET_ERR_INVALID_ARGUMENT, "pget_lm_solve: empty box");
+    const bool use_sgp = (p.flags & PGET_LM_SGP) != 0;
+    if (use_sgp && !use_box) return fail(PGET_ERR_INVALID_ARGUMENT, "pget_lm_solve: PGET_LM_SGP needs PGET_LM_BOX");
+    if (p.flags & ~(PGET_LM_BOX | PGET_LM_SGP)) return fail(PGET_ERR_INVALID_ARGUMENT, "pget_lm_solve: unknown flags");
     const Geometry& g = h->g;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int N = g.desc.n_px, B = g.desc.batch, n2 = N * N;
@@ -1296,7 +1327,7 @@ pget_status pget_lm_solve(pget_geometry h, float* lam, float* mu, const float* y
         pget_gn_stats* sk = stats + static_cast<size_t>(k) * B;
         if ((st = gn_cg_impl(g, w, lam, mu, y_meas, static_cast<float>(alpha), 0.f, w.beta, p.n_cg,
                              PGET_GN_EVAL_TRIAL, w.sl, w.sm, sk, use_box ? &box : nullptr, s,
-                             static_cast<float>(pscale))))
+                             static_cast<float>(pscale), use_sgp)))
             return st;
         lm_update_kernel<<<dim3(vec_grid(n2), B), kVecThreads, 0, s>>>(lam, mu, w.ul, w.um, sk, w.beta, n2); note();
         CK(cudaGetLastError());

@@ -118,7 +118,8 @@ __global__ void finish_kernel(const double2* __restrict__ part, int G, const flo
                               const float* __restrict__ xm, float alpha, float beta, float sign,
                               float* outl, float* outm, const float* __restrict__ dotl,
                               const float* __restrict__ dotm, double* partial, float* copy1l, float* copy1m,
-                              float* copy2l, float* copy2m, float* zerol, float* zerom, int N, PriorArgs pr)
+                              float* copy2l, float* copy2m, float* zerol, float* zerom, int N, PriorArgs pr,
+                              const float* betav)
 {
     __shared__ double sh[32];
     const int m = blockIdx.y;
@@ -146,8 +147,9 @@ __global__ void finish_kernel(const double2* __restrict__ part, int G, const flo
         if (xl) {
             const float* pl = xl + base;
             const float* pm = xm + base;
-            ol += alpha * lap2_at(pl, N, j, i) + beta * pl[e];
-            om += alpha * lap2_at(pm, N, j, i) + beta * pm[e];
+            const float bt = betav ? betav[m] : beta;   // per-member LM parameter (LM solve)
+            ol += alpha * lap2_at(pl, N, j, i) + bt * pl[e];
+            om += alpha * lap2_at(pm, N, j, i) + bt * pm[e];
             prior_op(pr, base + e, pl[e], pm[e], ol, om);
         }
         ol *= sign;
@@ -525,6 +527,99 @@ __global__ void scalar_kernel(int op, int k, const double* p0, const double* p1,
     }
 }
 
+
+// ---- SGP inner solver (O11): gradient projection on the box with Barzilai-Borwein
+// lengths and an exact line search, from s = 0; g = H s - b.
+__global__ void sgp_init_kernel(const float* __restrict__ bl, const float* __restrict__ bm, float* gl, float* gm,
+                                CGState* st, int n2, int B)
+{
+    const size_t n = static_cast<size_t>(B) * n2;
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        gl[e] = -bl[e];
+        gm[e] = -bm[e];
+    }
+    if (blockIdx.x == 0)
+        for (int m = threadIdx.x; m < B; m += blockDim.x) st[m] = CGState{0.0, 1.0, 0.0, 0, 0};
+}
+
+// d = P_box(u + s - a g) - u - s; partials <g, d>, <d, d> (zero for a stopped member)
+__global__ void sgp_dir_kernel(const float* __restrict__ ul, const float* __restrict__ um,
+                               const float* __restrict__ sl, const float* __restrict__ sm,
+                               const float* __restrict__ gl, const float* __restrict__ gm, const CGState* st,
+                               float4 box, float* dl, float* dm, double* pgd, double* pdd, int n2)
+{
+    __shared__ double sh[32];
+    const int m = blockIdx.y;
+    const size_t base = static_cast<size_t>(m) * n2;
+    const bool run = !st[m].stop;
+    const float a = static_cast<float>(st[m].a);
+    double gd = 0.0, dd = 0.0;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n2; e += gridDim.x * blockDim.x) {
+        const size_t k = base + e;
+        float d1 = 0.f, d2 = 0.f;
+        if (run) {
+            const float x1 = ul[k] + sl[k], x2 = um[k] + sm[k];
+            d1 = fminf(fmaxf(fmaf(-a, gl[k], x1), box.x), box.y) - x1;
+            d2 = fminf(fmaxf(fmaf(-a, gm[k], x2), box.z), box.w) - x2;
+            gd += static_cast<double>(gl[k]) * d1 + static_cast<double>(gm[k]) * d2;
+            dd += static_cast<double>(d1) * d1 + static_cast<double>(d2) * d2;
+        }
+        dl[k] = d1;
+        dm[k] = d2;
+    }
+    const double t1 = block_sum(gd, sh);
+    if (threadIdx.x == 0) pgd[m * gridDim.x + blockIdx.x] = t1;
+    const double t2 = block_sum(dd, sh);
+    if (threadIdx.x == 0) pdd[m * gridDim.x + blockIdx.x] = t2;
+}
+
+// per member: stop when <g, d> >= 0; else lam = min(1, -<g,d>/<d,Hd>), the next BB length (BB1 after
+// even steps, BB2 after odd ones, clamped to [1e-10, 1e10]); final_: only ||d|| of the last direction
+__global__ void sgp_scalar_kernel(int k, int final_, const double* pgd, const double* pdd, const double* pdhd,
+                                  const double* pqq, int nblk, CGState* st, pget_gn_stats* stats, int B)
+{
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m >= B) return;
+    CGState& c = st[m];
+    pget_gn_stats& S = stats[m];
+    if (c.stop) return;
+    const double gd = psum(pgd, m, nblk), dd = psum(pdd, m, nblk);
+    S.cg_res[k] = sqrt(dd);
+    if (final_) return;
+    if (!(gd < 0.0)) {
+        c.stop = 1;
+        S.breakdown = 1;
+        S.n_cg_done = k;
+        return;
+    }
+    const double dhd = psum(pdhd, m, nblk), qq = psum(pqq, m, nblk);
+    if (k == 0) S.beta_min = 1e-3 * dhd / dd;
+    const double lam = dhd > 0.0 ? fmin(1.0, -gd / dhd) : 1.0;
+    c.bcg = lam;
+    const double sy = lam * lam * dhd, ss = lam * lam * dd, yy = lam * lam * qq;
+    double an = (k % 2 == 0) ? (sy > 0.0 ? ss / sy : 1e10) : (yy > 0.0 ? sy / yy : 1e10);
+    c.a = an < 1e-10 ? 1e-10 : (an > 1e10 ? 1e10 : an);
+    S.n_cg_done = k + 1;
+}
+
+// s += lam d, g += lam H d (members not stopped)
+__global__ void sgp_update_kernel(float* sl, float* sm, float* gl, float* gm, const float* __restrict__ dl,
+                                  const float* __restrict__ dm, const float* __restrict__ ql,
+                                  const float* __restrict__ qm, const CGState* st, int n2)
+{
+    const int m = blockIdx.y;
+    if (st[m].stop) return;
+    const float lam = static_cast<float>(st[m].bcg);
+    const size_t base = static_cast<size_t>(m) * n2;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n2; e += gridDim.x * blockDim.x) {
+        const size_t k = base + e;
+        sl[k] = fmaf(lam, dl[k], sl[k]);
+        sm[k] = fmaf(lam, dm[k], sm[k]);
+        gl[k] = fmaf(lam, ql[k], gl[k]);
+        gm[k] = fmaf(lam, qm[k], gm[k]);
+    }
+}
 
 // One CG step after the GN projector, fused into a single cooperative launch (grid-wide syncs):
 //   q = H p  (the G fp64 slot partials + alpha L^T L p + beta p),   gamma = <p, q>,

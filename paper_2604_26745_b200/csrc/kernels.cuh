@@ -89,10 +89,19 @@ __global__ void reduce_slots_kernel(const float2* slots, double2* part, int N, i
 __global__ void finish_kernel(const double2* part, int G, const float* xl, const float* xm, float alpha, float beta,
                               float sign, float* outl, float* outm, const float* dotl, const float* dotm,
                               double* partial, float* copy1l, float* copy1m, float* copy2l, float* copy2m,
-                              float* zerol, float* zerom, int N, PriorArgs pr);
+                              float* zerol, float* zerom, int N, PriorArgs pr, const float* betav = nullptr);
 __global__ void residual_kernel(float* y, const float* ymeas, double* partial, int nper);
 __global__ void sumsq_kernel(const float* x, double* partial, int nper);
 __global__ void regsq_kernel(const float* xl, const float* xm, double* partial, int N);
+// SGP inner solver (O11): CGState carries a = the Barzilai-Borwein length, bcg = the line-search step
+__global__ void sgp_init_kernel(const float* bl, const float* bm, float* gl, float* gm, CGState* st, int n2, int B);
+__global__ void sgp_dir_kernel(const float* ul, const float* um, const float* sl, const float* sm, const float* gl,
+                               const float* gm, const CGState* st, float4 box, float* dl, float* dm, double* pgd,
+                               double* pdd, int n2);
+__global__ void sgp_scalar_kernel(int k, int final_, const double* pgd, const double* pdd, const double* pdhd,
+                                  const double* pqq, int nblk, CGState* st, pget_gn_stats* stats, int B);
+__global__ void sgp_update_kernel(float* sl, float* sm, float* gl, float* gm, const float* dl, const float* dm,
+                                  const float* ql, const float* qm, const CGState* st, int n2);
 __global__ void priorsq_kernel(const float* xl, const float* xm, PriorArgs pr, double* partial, int N);
 __global__ void priordot_kernel(const float* ul, const float* um, const float* sl, const float* sm, PriorArgs pr,
                                 double* pdot, double* psq, int N);

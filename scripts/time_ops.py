@@ -36,6 +36,12 @@ if "--solve" in sys.argv:   # a 10-iteration LM solve (N1) from u0 with a box, r
         return pg.lm_solve(g, ls, ms, y, 10, 20, alpha0=1e-2, alpha_decay=5.0, k_freeze=3, beta0=0.0,
                            box=(0.0, 2.0, 0.0, 1.0))
     ops["solve10"] = solve
+    if "--sgp" in sys.argv:   # the same solve with the SGP inner solver (PGET_LM_SGP)
+        def solve_sgp():
+            ls.copy_(torch.from_numpy(l0h)); ms.copy_(torch.from_numpy(m0h))
+            return pg.lm_solve(g, ls, ms, y, 10, 20, alpha0=1e-2, alpha_decay=5.0, k_freeze=3, beta0=0.0,
+                               box=(0.0, 2.0, 0.0, 1.0), sgp=True)
+        ops["solve10_sgp"] = solve_sgp
 nom = g.info["n_samples_nominal"]
 out = {}
 for name, f in ops.items():

@@ -81,3 +81,40 @@ def test_lm_solve_errors(pg):
         pg.lm_solve(g, lam, mu, yd, 1, 4, alpha_decay=0.5)
     with pytest.raises(RuntimeError, match="n_cg"):
         pg.lm_solve(g, lam, mu, yd, 1, 10_000)
+
+
+def test_lm_solve_sgp_parity(pg):
+    """PGET_LM_SGP (O11): the box-constrained steps by gradient projection with
+    Barzilai-Borwein lengths.  Same pins as the CG solve (reading R-LM: the inner iterations amplify
+    fp32-level differences), plus the SGP-specific ones: every iterate inside the box, the first
+    projected-gradient step ||d_0|| at 1e-5 (it precedes any GN product)."""
+    gd, y, l0, m0 = _problem()
+    box = (0.0, 1.5, 0.0, 0.6)
+    kw = dict(n_iter=4, n_cg=8, alpha0=1e-2, alpha_decay=5.0, k_freeze=2, beta0=0.1)
+    g = pg.Geometry(gd)
+    lam, mu = dev(l0), dev(m0)
+    S = pg.lm_solve(g, lam, mu, dev(y), box=box, sgp=True, **kw)
+    torch.cuda.synchronize()
+    (lo, mo), So = O.lm_solve(gd, l0, m0, y, kw["n_iter"], kw["n_cg"], kw["alpha0"], kw["alpha_decay"],
+                              kw["k_freeze"], kw["beta0"], box=box, inner="sgp")
+    lam, mu = lam.cpu().numpy(), mu.cpu().numpy()
+    for m in range(gd["batch"]):
+        for key in ("f", "misfit", "reg", "grad_norm"):
+            assert abs(S[0][m][key] - So[m][0][key]) <= 1e-5 * abs(So[m][0][key]), key
+        assert abs(S[0][m]["cg_res"][0] - So[m][0]["cg_res"][0]) <= 1e-5 * So[m][0]["cg_res"][0]
+        for k in range(kw["n_iter"]):
+            a, o = S[k][m], So[m][k]
+            assert abs(a["f"] - o["f"]) <= (1e-5 if k == 0 else 0.1) * abs(o["f"]), (m, k)
+            if abs(o["rho"] - 0.1) > 0.02:
+                assert a["accepted"] == o["accepted"], (m, k, a["rho"], o["rho"])
+        assert rel_l2(lam[m].astype(np.float64), lo[m]) <= 5e-2
+        assert rel_l2(mu[m].astype(np.float64), mo[m]) <= 5e-2
+        assert S[-1][m]["f_trial"] < S[0][m]["f"]
+    assert lam.min() >= box[0] and lam.max() <= box[1] and mu.min() >= box[2] and mu.max() <= box[3]
+
+
+def test_lm_solve_sgp_needs_box(pg):
+    gd, y, l0, m0 = _problem(batch=1, n_px=16)
+    g = pg.Geometry(gd)
+    with pytest.raises(RuntimeError, match="PGET_LM_SGP"):
+        pg.lm_solve(g, dev(l0), dev(m0), dev(y), 1, 4, sgp=True)
