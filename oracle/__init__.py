@@ -66,6 +66,8 @@ def _load():
         _lib.orc_ray_adjoint.restype = None
         _lib.orc_threads.restype = C.c_int
         _lib.orc_set_prior.argtypes = [P, P, C.c_double, C.c_double]
+        _lib.orc_project.argtypes = [P, P, C.c_size_t, P]
+        _lib.orc_project.restype = None
         _lib.orc_set_prior.restype = None
     return _lib
 
@@ -216,7 +218,7 @@ def lm_step_box(g, lam, mu, y, alpha, beta, n_it, box, inner="sgp", prior=None):
     lib = _load()
     d = _desc(g)
     lam, mu, y = _f64(lam), _f64(mu), _f64(y)
-    bx = np.ascontiguousarray(box, dtype=np.float64)
+    bx = _box5(box)
     sl, sm = np.zeros(img_shape(g)), np.zeros(img_shape(g))
     st = np.zeros(ST_CG + n_it + 1)
     with _Prior(g, prior):
@@ -224,6 +226,20 @@ def lm_step_box(g, lam, mu, y, alpha, beta, n_it, box, inner="sgp", prior=None):
                                  int(inner == "sgp"), _p(sl), _p(sm), _p(st))
     assert rc == 0, rc
     return sl, sm, stats_dict(st, n_it)
+
+
+def _box5(box):
+    """(lam_lo, lam_hi, mu_lo, mu_hi[, c]) -> the oracle's 5-vector; c > 0 adds lam <= c mu (O12)."""
+    b = list(box) + [0.0] * (5 - len(box))
+    return np.ascontiguousarray(b, dtype=np.float64)
+
+
+def project(lam, mu, box):
+    """O12: the per-pixel Euclidean projection of (lam, mu) onto the LM solve's feasible set."""
+    lib = _load()
+    l, m = _f64(lam).copy(), _f64(mu).copy()
+    lib.orc_project(_p(l), _p(m), l.size, _p(_box5(box)))
+    return l, m
 
 
 def stats_dict(st, n_cg):
@@ -285,7 +301,7 @@ def lm_solve(g, lam, mu, y, n_iter, n_cg, alpha0, alpha_decay=5.0, k_freeze=0, b
     lam_o, mu_o = _f64(lam).reshape(shp).copy(), _f64(mu).reshape(shp).copy()
     ys = _f64(y).reshape(B, -1)
     d = _desc(dict(g, batch=1))
-    bx = None if box is None else np.ascontiguousarray(box, dtype=np.float64)
+    bx = None if box is None else _box5(box)
     out = []
     for m in range(B):
         l = np.ascontiguousarray(lam_o[m])

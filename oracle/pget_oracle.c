@@ -537,6 +537,33 @@ int orc_gn_cg_step(const orc_desc* g, const double* lam, const double* mu, const
 
 static double clampd(double x, double lo, double hi) { return x < lo ? lo : (x > hi ? hi : x); }
 
+/* Euclidean projection of one pixel's (lam, mu) onto the feasible set of the LM solve (O12, N1):
+ * the box [box0, box1] x [box2, box3] and, when box4 = c > 0, the linear constraint lam <= c mu ("low
+ * attenuation but highly emitting materials are not allowed"; reading R-lin).  If the
+ * box projection satisfies lam <= c mu it is the projection; otherwise the projection lies on the
+ * line lam = c mu, at the line parameter t* = (c lam + mu) / (c^2 + 1) clamped to the line's segment
+ * inside the box. */
+static void projK(double* l, double* m, const double* box)
+{
+    double pl = clampd(*l, box[0], box[1]), pm = clampd(*m, box[2], box[3]);
+    const double c = box[4];
+    if (c > 0.0 && pl > c * pm) {
+        double t = (c * *l + *m) / (c * c + 1.0);
+        double tlo = fmax(box[0] / c, box[2]), thi = fmin(box[1] / c, box[3]);
+        t = clampd(t, tlo, thi);
+        pl = c * t;
+        pm = t;
+    }
+    *l = pl;
+    *m = pm;
+}
+
+/* the projection of whole images (test entry point) */
+void orc_project(double* lam, double* mu, size_t n, const double* box)
+{
+    for (size_t i = 0; i < n; ++i) projK(&lam[i], &mu[i], box);
+}
+
 /* One LM iteration with the box {lam_lo, lam_hi, mu_lo, mu_hi}: CG then projection (sgp = 0, reading
  * R-N1) or the SGP inner solver (sgp = 1, O11).  Stats as orc_gn_cg_step. */
 int orc_lm_step_box(const orc_desc* g, const double* lam, const double* mu, const double* y, double alpha,
@@ -599,8 +626,10 @@ static int lm_step(const orc_desc* g, const double* lam, const double* mu, const
         int k;
         for (k = 0; k < n_cg; ++k) {
             for (size_t i = 0; i < npx; ++i) {
-                d[i] = clampd(lam[i] + s[i] - a * gq[i], box[0], box[1]) - lam[i] - s[i];
-                d[npx + i] = clampd(mu[i] + s[npx + i] - a * gq[npx + i], box[2], box[3]) - mu[i] - s[npx + i];
+                double pl = lam[i] + s[i] - a * gq[i], pm = mu[i] + s[npx + i] - a * gq[npx + i];
+                projK(&pl, &pm, box);
+                d[i] = pl - lam[i] - s[i];
+                d[npx + i] = pm - mu[i] - s[npx + i];
             }
             double gd = dot(gq, d, n2), dd = dot(d, d, n2);
             stats[ST_CG + k] = sqrt(dd);
@@ -616,8 +645,10 @@ static int lm_step(const orc_desc* g, const double* lam, const double* mu, const
         }
         if (k == n_cg) {
             for (size_t i = 0; i < npx; ++i) {
-                d[i] = clampd(lam[i] + s[i] - a * gq[i], box[0], box[1]) - lam[i] - s[i];
-                d[npx + i] = clampd(mu[i] + s[npx + i] - a * gq[npx + i], box[2], box[3]) - mu[i] - s[npx + i];
+                double pl = lam[i] + s[i] - a * gq[i], pm = mu[i] + s[npx + i] - a * gq[npx + i];
+                projK(&pl, &pm, box);
+                d[i] = pl - lam[i] - s[i];
+                d[npx + i] = pm - mu[i] - s[npx + i];
             }
             stats[ST_CG + n_cg] = sqrt(dot(d, d, n2));
         }
@@ -653,8 +684,10 @@ step_done:
     /* (N1) the step actually taken inside the box (a no-op for the feasible SGP step) */
     if (box)
         for (size_t i = 0; i < npx; ++i) {
-            s[i] = clampd(lam[i] + s[i], box[0], box[1]) - lam[i];
-            s[npx + i] = clampd(mu[i] + s[npx + i], box[2], box[3]) - mu[i];
+            double pl = lam[i] + s[i], pm = mu[i] + s[npx + i];
+            projK(&pl, &pm, box);
+            s[i] = pl - lam[i];
+            s[npx + i] = pm - mu[i];
         }
     /* 6: pred = <b,s> - 1/2(||Js||^2 + alpha||Ls||^2) */
     orc_jvp(g, lam, mu, s, s + npx, NULL, ys);
@@ -673,8 +706,7 @@ step_done:
     for (size_t i = 0; i < npx; ++i) { ut[i] = lam[i] + s[i]; ut[npx + i] = mu[i] + s[npx + i]; }
     if (box)
         for (size_t i = 0; i < npx; ++i) {
-            ut[i] = clampd(ut[i], box[0], box[1]);
-            ut[npx + i] = clampd(ut[npx + i], box[2], box[3]);
+            projK(&ut[i], &ut[npx + i], box);
         }
     double mis2, reg2;
     double f1 = objective(g, ut, ut + npx, y, alpha, &mis2, &reg2, r, tl);
@@ -783,7 +815,7 @@ int orc_lm_solve(const orc_desc* g, double* lam, double* mu, const double* y, in
     double* sm = (double*)malloc(sizeof(double) * npx);
     if (!sl || !sm) return -2;
     if (box)
-        for (size_t i = 0; i < npx; ++i) { lam[i] = clampd(lam[i], box[0], box[1]); mu[i] = clampd(mu[i], box[2], box[3]); }
+        for (size_t i = 0; i < npx; ++i) projK(&lam[i], &mu[i], box);
     double alpha = alpha0, beta = beta0, pscale = 1.0;
     const int row = ST_CG + n_cg + 1;
     for (int k = 0; k < n_iter; ++k) {
@@ -795,7 +827,7 @@ int orc_lm_solve(const orc_desc* g, double* lam, double* mu, const double* y, in
         if (st[7] != 0.0)
             for (size_t i = 0; i < npx; ++i) {
                 double a = lam[i] + sl[i], b = mu[i] + sm[i];
-                if (box) { a = clampd(a, box[0], box[1]); b = clampd(b, box[2], box[3]); }
+                if (box) projK(&a, &b, box);
                 lam[i] = a;
                 mu[i] = b;
             }

@@ -785,3 +785,45 @@ def test_p16_lm_solve_with_sgp_decreases_f_inside_the_box():
     (lk, mk), [sts] = O.lm_solve(g, l0, m0, y, 5, 10, 1e-3, beta0=0.01, box=box, inner="sgp")
     assert sts[-1]["f_trial"] < 0.2 * sts[0]["f"]
     assert lk.min() >= box[0] and lk.max() <= box[1] and mk.min() >= box[2] and mk.max() <= box[3]
+
+
+# ----------------------------------------------------------------------------- P17 linear constraint lam <= c mu (O12, N1)
+def test_p17_projection_is_the_euclidean_projection():
+    """Variational inequality <x - P x, z - P x> <= 0 for every feasible z (which characterises the
+    projection onto a convex set), feasibility, idempotence; c = 0 is the plain box clamp."""
+    rng = np.random.default_rng(17)
+    box = (0.0, 2.0, 0.0, 1.0, 2.5)
+    x = rng.uniform(-1.0, 3.0, size=4000)
+    y = rng.uniform(-0.5, 1.5, size=4000)
+    pl, pm = O.project(x, y, box)
+    assert np.all((pl >= 0) & (pl <= 2) & (pm >= 0) & (pm <= 1) & (pl <= 2.5 * pm + 1e-12))
+    zl = rng.uniform(0, 2, size=20000)
+    zm = rng.uniform(0, 1, size=20000)
+    ok = zl <= 2.5 * zm
+    zl, zm = zl[ok][:3000], zm[ok][:3000]
+    vi = (x - pl)[:, None] * (zl[None, :] - pl[:, None]) + (y - pm)[:, None] * (zm[None, :] - pm[:, None])
+    assert vi.max() <= 1e-12
+    ql, qm = O.project(pl, pm, box)
+    np.testing.assert_allclose(ql, pl, rtol=0, atol=1e-15)
+    np.testing.assert_allclose(qm, pm, rtol=0, atol=1e-15)
+    cl, cm = O.project(x, y, box[:4])
+    np.testing.assert_array_equal(cl, np.clip(x, 0, 2))
+    np.testing.assert_array_equal(cm, np.clip(y, 0, 1))
+    assert np.any(pl == 2.5 * pm) and np.any(pl < 2.5 * pm)        # the constraint binds somewhere
+
+
+def test_p17_lm_solve_respects_the_constraint():
+    """Every LM iterate (CG + projection, and SGP) satisfies lam <= c mu; a non-binding c changes
+    nothing (bitwise)."""
+    g, y, (l0, m0) = _sgp_case(n_px=16, n_angles=8)
+    for inner in ("cg", "sgp"):
+        (lk, mk), [sts] = O.lm_solve(g, l0, m0, y, 4, 8, 1e-3, beta0=0.01, box=(0.0, 1.6, 0.0, 0.6, 3.0),
+                                     inner=inner)
+        assert np.all(lk <= 3.0 * mk + 1e-12) and sts[-1]["f_trial"] < sts[0]["f"]
+        assert np.any(np.isclose(lk, 3.0 * mk) & (lk > 0))
+        # mu >= 0.01 in the box, so lam <= 1e6 mu never binds
+        (la, ma), [sa] = O.lm_solve(g, l0, m0, y, 3, 6, 1e-3, beta0=0.01, box=(0.0, 1.6, 0.01, 0.6), inner=inner)
+        (lb, mb), [sb] = O.lm_solve(g, l0, m0, y, 3, 6, 1e-3, beta0=0.01, box=(0.0, 1.6, 0.01, 0.6, 1e6),
+                                    inner=inner)
+        np.testing.assert_array_equal(la, lb)
+        assert [s["f"] for s in sa] == [s["f"] for s in sb]
