@@ -159,7 +159,9 @@ typedef struct {
     float beta0;          /* initial LM parameter of every member                              */
     float lam_lo, lam_hi, mu_lo, mu_hi;   /* the box (PGET_LM_BOX)                              */
     uint32_t flags;       /* PGET_LM_BOX, PGET_LM_SGP                                          */
-    int32_t pad_;
+    float lam_per_mu;     /* > 0 (with PGET_LM_BOX): also lam <= lam_per_mu * mu in every projection ("low
+                           * attenuation but highly emitting materials are not allowed", PAPER.md:148;
+                           * reading R-lin); 0 = off                                               */
 } pget_lm_params;
 
 /* Device-resident result of the Prop. 1 safeguard check, per batch member (array of `batch`).

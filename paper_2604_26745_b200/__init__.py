@@ -68,7 +68,7 @@ PGET_LM_SGP = 2
 class LMParams(C.Structure):
     _fields_ = [("n_iter", C.c_int32), ("n_cg", C.c_int32), ("alpha0", C.c_float), ("alpha_decay", C.c_float),
                 ("k_freeze", C.c_int32), ("beta0", C.c_float), ("lam_lo", C.c_float), ("lam_hi", C.c_float),
-                ("mu_lo", C.c_float), ("mu_hi", C.c_float), ("flags", C.c_uint32), ("pad_", C.c_int32)]
+                ("mu_lo", C.c_float), ("mu_hi", C.c_float), ("flags", C.c_uint32), ("lam_per_mu", C.c_float)]
 
 
 class Prior(C.Structure):
@@ -356,15 +356,15 @@ def safeguard(g: Geometry, lam, mu, y_meas, s_lam, s_mu, cand_lam, cand_mu, alph
 
 
 def lm_solve(g: Geometry, lam, mu, y_meas, n_iter, n_cg=20, alpha0=1e-3, alpha_decay=5.0, k_freeze=0, beta0=0.0,
-             box=None, sgp=False, ws=None, stream=None):
+             box=None, sgp=False, lam_per_mu=0.0, ws=None, stream=None):
     """Full LM solve (pget_lm_solve): lam, mu are updated in place.  box = (lam_lo, lam_hi, mu_lo, mu_hi)
-    or None; sgp: the box-constrained steps by SGP (PGET_LM_SGP).  Returns [[stats dict per member] per
-    iteration]."""
+    or None; sgp: the box-constrained steps by SGP (PGET_LM_SGP); lam_per_mu > 0 adds lam <= lam_per_mu mu
+    to the box.  Returns [[stats dict per member] per iteration]."""
     import torch
     _f32(lam, g.img_shape, "lam"); _f32(mu, g.img_shape, "mu"); _f32(y_meas, g.sino_shape, "y_meas")
     p = LMParams(int(n_iter), int(n_cg), float(alpha0), float(alpha_decay), int(k_freeze), float(beta0),
                  *(float(x) for x in (box if box is not None else (0.0, 0.0, 0.0, 0.0))),
-                 (PGET_LM_BOX if box is not None else 0) | (PGET_LM_SGP if sgp else 0), 0)
+                 (PGET_LM_BOX if box is not None else 0) | (PGET_LM_SGP if sgp else 0), float(lam_per_mu))
     B = g.info["batch"]
     buf = torch.zeros(max(1, n_iter) * B * C.sizeof(GNStats), dtype=torch.uint8, device=lam.device)
     ws = g.workspace("lm_solve") if ws is None else ws

@@ -775,12 +775,12 @@ size_t pget_workspace_bytes(pget_geometry h, int op)
 
 // ---- building blocks (all enqueued on s)
 static pget_status pack2(const Geometry& g, const WS& w, const float* lam, const float* mu, const float* slam,
-                         const float* smu, float* ul, float* um, cudaStream_t s, const float4* box = nullptr)
+                         const float* smu, float* ul, float* um, cudaStream_t s, const BoxK* box = nullptr)
 {
     const size_t img = static_cast<size_t>(g.desc.batch) * g.P * g.P;
     pack2_kernel<<<vec_grid(img), kVecThreads, 0, s>>>(lam, mu, slam, smu, w.img2[0], w.img2[1], ul, um,
                                                       g.desc.n_px, g.P, g.desc.batch, box ? 1 : 0,
-                                                      box ? *box : make_float4(0.f, 0.f, 0.f, 0.f)); note();
+                                                      box ? *box : BoxK{make_float4(0.f, 0.f, 0.f, 0.f), 0.f}); note();
     CK(cudaGetLastError());
     return PGET_OK;
 }
@@ -1125,7 +1125,7 @@ pget_status pget_gn_apply(pget_geometry h, const float* lam, const float* mu, co
 // pred and the trial (reading R-N1).
 static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const float* mu,
                               const float* y_meas, float alpha, float beta, const float* betav, int32_t n_cg,
-                              uint32_t flags, float* s_lam, float* s_mu, pget_gn_stats* stats, const float4* box,
+                              uint32_t flags, float* s_lam, float* s_mu, pget_gn_stats* stats, const BoxK* box,
                               cudaStream_t s, float pscale = 1.f, bool sgp = false)
 {
     pget_status st;
@@ -1221,8 +1221,7 @@ static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const f
     // (N1) the step actually taken inside the box: s <- clamp(u + s) - u
     if (box) {
         const size_t n = static_cast<size_t>(B) * n2;
-        project_step_kernel<<<vec_grid(n), kVecThreads, 0, s>>>(lam, mu, s_lam, s_mu, n, box->x, box->y, box->z,
-                                                                box->w); note();
+        project_step_kernel<<<vec_grid(n), kVecThreads, 0, s>>>(lam, mu, s_lam, s_mu, n, *box); note();
         CK(cudaGetLastError());
     }
     // 6: pred = <b,s> - 1/2(||Js||^2 + alpha ||Ls||^2); ||Js||^2 from the paired GN-mode phase A of
@@ -1306,16 +1305,20 @@ pget_status pget_lm_solve(pget_geometry h, float* lam, float* mu, const float* y
         return fail(PGET_ERR_INVALID_ARGUMENT, "pget_lm_solve: empty box");
     const bool use_sgp = (p.flags & PGET_LM_SGP) != 0;
     if (use_sgp && !use_box) return fail(PGET_ERR_INVALID_ARGUMENT, "pget_lm_solve: PGET_LM_SGP needs PGET_LM_BOX");
+    if (!std::isfinite(p.lam_per_mu) || p.lam_per_mu < 0.f || (p.lam_per_mu > 0.f && !use_box))
+        return fail(PGET_ERR_INVALID_ARGUMENT, "pget_lm_solve: lam_per_mu must be finite, >= 0, and needs PGET_LM_BOX");
+    if (p.lam_per_mu > 0.f && p.lam_lo > p.lam_per_mu * p.mu_hi)
+        return fail(PGET_ERR_INVALID_ARGUMENT, "pget_lm_solve: lam <= lam_per_mu mu excludes the whole box");
     if (p.flags & ~(PGET_LM_BOX | PGET_LM_SGP)) return fail(PGET_ERR_INVALID_ARGUMENT, "pget_lm_solve: unknown flags");
     const Geometry& g = h->g;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int N = g.desc.n_px, B = g.desc.batch, n2 = N * N;
-    const float4 box = make_float4(p.lam_lo, p.lam_hi, p.mu_lo, p.mu_hi);
+    const BoxK box{make_float4(p.lam_lo, p.lam_hi, p.mu_lo, p.mu_hi), p.lam_per_mu};
     fill_kernel<<<(B + 127) / 128, 128, 0, s>>>(w.beta, p.beta0, B); note();
     CK(cudaGetLastError());
     if (use_box) {   // the initial guess itself is projected onto the box
         const size_t n = static_cast<size_t>(B) * n2;
-        clamp_kernel<<<vec_grid(n), kVecThreads, 0, s>>>(lam, mu, n, box.x, box.y, box.z, box.w); note();
+        clamp_kernel<<<vec_grid(n), kVecThreads, 0, s>>>(lam, mu, n, box); note();
         CK(cudaGetLastError());
     }
     double alpha = p.alpha0, pscale = 1.0;

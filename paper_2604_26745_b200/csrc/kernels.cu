@@ -14,10 +14,25 @@ namespace pget {
 // ------------------------------------------------------------------------------------------
 // image packing: padded P x P images with a zero halo of kHalo pixels, in the normal and in the
 // transposed orientation (orientation class 1 of the projector samples the transposed copy).
+// Euclidean projection of one pixel's (lam, mu) onto the feasible set (oracle O12): the box, then, if
+// lam > c mu, the closest point of the segment of the line lam = c mu inside the box
+__device__ __forceinline__ void proj_k(float& l, float& m, const BoxK& k)
+{
+    float pl = fminf(fmaxf(l, k.b.x), k.b.y), pm = fminf(fmaxf(m, k.b.z), k.b.w);
+    if (k.c > 0.f && pl > k.c * pm) {
+        float t = (k.c * l + m) / (k.c * k.c + 1.f);
+        t = fminf(fmaxf(t, fmaxf(k.b.x / k.c, k.b.z)), fminf(k.b.y / k.c, k.b.w));
+        pl = k.c * t;
+        pm = t;
+    }
+    l = pl;
+    m = pm;
+}
+
 __global__ void pack2_kernel(const float* __restrict__ lam, const float* __restrict__ mu,
                              const float* __restrict__ slam, const float* __restrict__ smu, float2* out,
                              float2* outT, float* ut_lam, float* ut_mu, int N, int P, int B, int has_box,
-                             float4 box)
+                             BoxK box)
 {
     // has_box: box = (lam_lo, lam_hi, mu_lo, mu_hi) clamps the trial point u + s
     const size_t total = static_cast<size_t>(B) * P * P;
@@ -34,10 +49,7 @@ __global__ void pack2_kernel(const float* __restrict__ lam, const float* __restr
             if (slam) {
                 val.x += slam[src];
                 val.y += smu[src];
-                if (has_box) {
-                    val.x = fminf(fmaxf(val.x, box.x), box.y);
-                    val.y = fminf(fmaxf(val.y, box.z), box.w);
-                }
+                if (has_box) proj_k(val.x, val.y, box);
                 ut_lam[src] = val.x;
                 ut_mu[src] = val.y;
             }
@@ -424,12 +436,14 @@ __global__ void guard_select_kernel(const float* __restrict__ ul, const float* _
 // ---- full LM solve
 // box projection of the LM step: s <- clamp(u + s) - u (the step actually taken, reading R-N1)
 __global__ void project_step_kernel(const float* __restrict__ ul, const float* __restrict__ um, float* sl, float* sm,
-                                    size_t n, float llo, float lhi, float mlo, float mhi)
+                                    size_t n, BoxK box)
 {
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        sl[e] = fminf(fmaxf(ul[e] + sl[e], llo), lhi) - ul[e];
-        sm[e] = fminf(fmaxf(um[e] + sm[e], mlo), mhi) - um[e];
+        float a = ul[e] + sl[e], b = um[e] + sm[e];
+        proj_k(a, b, box);
+        sl[e] = a - ul[e];
+        sm[e] = b - um[e];
     }
 }
 
@@ -449,12 +463,14 @@ __global__ void lm_update_kernel(float* ul, float* um, const float* __restrict__
     if (blockIdx.x == 0 && threadIdx.x == 0) betav[m] = static_cast<float>(stats[m].beta_next);
 }
 
-__global__ void clamp_kernel(float* ul, float* um, size_t n, float llo, float lhi, float mlo, float mhi)
+__global__ void clamp_kernel(float* ul, float* um, size_t n, BoxK box)
 {
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        ul[e] = fminf(fmaxf(ul[e], llo), lhi);
-        um[e] = fminf(fmaxf(um[e], mlo), mhi);
+        float a = ul[e], b = um[e];
+        proj_k(a, b, box);
+        ul[e] = a;
+        um[e] = b;
     }
 }
 
@@ -547,7 +563,7 @@ __global__ void sgp_init_kernel(const float* __restrict__ bl, const float* __res
 __global__ void sgp_dir_kernel(const float* __restrict__ ul, const float* __restrict__ um,
                                const float* __restrict__ sl, const float* __restrict__ sm,
                                const float* __restrict__ gl, const float* __restrict__ gm, const CGState* st,
-                               float4 box, float* dl, float* dm, double* pgd, double* pdd, int n2)
+                               BoxK box, float* dl, float* dm, double* pgd, double* pdd, int n2)
 {
     __shared__ double sh[32];
     const int m = blockIdx.y;
@@ -560,8 +576,10 @@ __global__ void sgp_dir_kernel(const float* __restrict__ ul, const float* __rest
         float d1 = 0.f, d2 = 0.f;
         if (run) {
             const float x1 = ul[k] + sl[k], x2 = um[k] + sm[k];
-            d1 = fminf(fmaxf(fmaf(-a, gl[k], x1), box.x), box.y) - x1;
-            d2 = fminf(fmaxf(fmaf(-a, gm[k], x2), box.z), box.w) - x2;
+            float y1 = fmaf(-a, gl[k], x1), y2 = fmaf(-a, gm[k], x2);
+            proj_k(y1, y2, box);
+            d1 = y1 - x1;
+            d2 = y2 - x2;
             gd += static_cast<double>(gl[k]) * d1 + static_cast<double>(gm[k]) * d2;
             dd += static_cast<double>(d1) * d1 + static_cast<double>(d2) * d2;
         }

@@ -66,6 +66,12 @@ struct CGState {
 
 // geometry priors P1, P2 (pget_set_prior): weights already scaled by the LM continuation; a null mask
 // switches its term off
+// the LM solve's feasible set (N1): box (lam_lo, lam_hi, mu_lo, mu_hi) and, for c > 0, lam <= c mu
+struct BoxK {
+    float4 b;
+    float c;
+};
+
 struct PriorArgs {
     const float* m1;
     const float* m2;
@@ -74,13 +80,12 @@ struct PriorArgs {
 
 __global__ void pack2_kernel(const float* lam, const float* mu, const float* slam, const float* smu, float2* out,
                              float2* outT, float* ut_lam, float* ut_mu, int N, int P, int B, int has_box,
-                             float4 box);
-__global__ void project_step_kernel(const float* ul, const float* um, float* sl, float* sm, size_t n, float llo,
-                                    float lhi, float mlo, float mhi);
+                             BoxK box);
+__global__ void project_step_kernel(const float* ul, const float* um, float* sl, float* sm, size_t n, BoxK box);
 __global__ void lm_update_kernel(float* ul, float* um, const float* tl, const float* tm, const pget_gn_stats* stats,
                                  float* betav, int n2);
 __global__ void fill_kernel(float* x, float v, int n);
-__global__ void clamp_kernel(float* ul, float* um, size_t n, float llo, float lhi, float mlo, float mhi);
+__global__ void clamp_kernel(float* ul, float* um, size_t n, BoxK box);
 __global__ void pack4_kernel(const float* lam, const float* mu, const float* dl, const float* dm, float4* out,
                              float4* outT, int N, int P, int B);
 __global__ void reduce_slots_kernel(const float2* slots, double2* part, int N, int Ns, int B, int G,
@@ -96,7 +101,7 @@ __global__ void regsq_kernel(const float* xl, const float* xm, double* partial, 
 // SGP inner solver (O11): CGState carries a = the Barzilai-Borwein length, bcg = the line-search step
 __global__ void sgp_init_kernel(const float* bl, const float* bm, float* gl, float* gm, CGState* st, int n2, int B);
 __global__ void sgp_dir_kernel(const float* ul, const float* um, const float* sl, const float* sm, const float* gl,
-                               const float* gm, const CGState* st, float4 box, float* dl, float* dm, double* pgd,
+                               const float* gm, const CGState* st, BoxK box, float* dl, float* dm, double* pgd,
                                double* pdd, int n2);
 __global__ void sgp_scalar_kernel(int k, int final_, const double* pgd, const double* pdd, const double* pdhd,
                                   const double* pqq, int nblk, CGState* st, pget_gn_stats* stats, int B);

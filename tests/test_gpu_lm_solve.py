@@ -118,3 +118,33 @@ def test_lm_solve_sgp_needs_box(pg):
     g = pg.Geometry(gd)
     with pytest.raises(RuntimeError, match="PGET_LM_SGP"):
         pg.lm_solve(g, dev(l0), dev(m0), dev(y), 1, 4, sgp=True)
+
+
+@pytest.mark.parametrize("sgp", [False, True])
+def test_lm_solve_linear_constraint(pg, sgp):
+    """lam <= c mu in every projection (O12, reading R-lin), with CG + projection and with
+    SGP: parity pins as above, and every final iterate inside the feasible set."""
+    gd, y, l0, m0 = _problem()
+    box, c = (0.0, 1.5, 0.0, 0.6), 3.0
+    kw = dict(n_iter=4, n_cg=8, alpha0=1e-2, alpha_decay=5.0, k_freeze=2, beta0=0.1)
+    g = pg.Geometry(gd)
+    lam, mu = dev(l0), dev(m0)
+    S = pg.lm_solve(g, lam, mu, dev(y), box=box, sgp=sgp, lam_per_mu=c, **kw)
+    torch.cuda.synchronize()
+    (lo, mo), So = O.lm_solve(gd, l0, m0, y, kw["n_iter"], kw["n_cg"], kw["alpha0"], kw["alpha_decay"],
+                              kw["k_freeze"], kw["beta0"], box=box + (c,), inner="sgp" if sgp else "cg")
+    lam, mu = lam.cpu().numpy(), mu.cpu().numpy()
+    for m in range(gd["batch"]):
+        for key in ("f", "misfit", "reg", "grad_norm"):
+            assert abs(S[0][m][key] - So[m][0][key]) <= 1e-5 * abs(So[m][0][key]), key
+        for k in range(kw["n_iter"]):
+            a, o = S[k][m], So[m][k]
+            assert abs(a["f"] - o["f"]) <= (1e-5 if k == 0 else 0.1) * abs(o["f"]), (m, k)
+            if abs(o["rho"] - 0.1) > 0.02:
+                assert a["accepted"] == o["accepted"], (m, k)
+        assert rel_l2(lam[m].astype(np.float64), lo[m]) <= 5e-2
+        assert rel_l2(mu[m].astype(np.float64), mo[m]) <= 5e-2
+    assert np.all(lam <= c * mu + 1e-6 * c) and lam.min() >= box[0] and mu.max() <= box[3]
+    assert np.any(np.isclose(lam, c * mu, rtol=1e-5, atol=0) & (lam > 0))   # the constraint binds
+    with pytest.raises(RuntimeError, match="lam_per_mu"):
+        pg.lm_solve(g, dev(l0), dev(m0), dev(y), 1, 4, lam_per_mu=3.0)
