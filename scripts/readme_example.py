@@ -1,3 +1,8 @@
+"""The README usage example, run as a script (checks that it stays runnable)."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch, paper_2604_26745_b200 as pg, pget_data as P
 g = pg.Geometry(P.geometry_desc(2))
 lam, mu = (torch.from_numpy(a).cuda() for a in P.make_phantom(2))
