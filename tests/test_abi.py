@@ -93,6 +93,18 @@ def test_compute_on_host_only_handle_fails_cleanly():
     assert pg.lib().pget_table_bytes(g.handle, 42) == 0
     for op in pg.OPS:
         assert g.workspace_bytes(op) > 0
+    pr = pg.Prior(None, None, 1.0, 1.0)
+    assert pg.lib().pget_set_prior(g.handle, C.byref(pr)) == 1      # host-only handle
+    assert pg.lib().pget_set_prior(None, None) == 1
+
+
+def test_host_struct_layouts():
+    """The C structs the binding mirrors keep their sizes (pget.h): the LM parameters (48 B, the last
+    field lam_per_mu replaced a pad), the prior, the safeguard statistics."""
+    import ctypes as C
+    assert C.sizeof(pg.LMParams) == 48
+    assert C.sizeof(pg.Prior) == 24
+    assert C.sizeof(pg.SafeguardStats) == 72
 
 
 @pytest.mark.parametrize("gd", [P.geometry_desc(c) for c in (1, 2, 3, 4)] + [

@@ -366,3 +366,15 @@ def test_lm_iteration_cuda_graph_capture(pg):
     gr.replay()
     torch.cuda.synchronize()
     assert torch.equal(sl, ref_s) and torch.equal(st, ref_st)
+
+
+@pytest.mark.parametrize("cached", [False, True])
+def test_gn_apply_zero_direction(pg, cached, monkeypatch):
+    """H 0 = 0 exactly on both GN paths (the fixed-point scatter's scale bounds are 0 then)."""
+    monkeypatch.setenv("PGET_GN_APPLY_CACHED", "1" if cached else "0")
+    gd = P.geometry_desc(2)
+    g = pg.Geometry(gd)
+    lam, mu = P.initial_guess(gd["n_px"])
+    z = np.zeros_like(lam)
+    ql, qm = pg.gn_apply(g, dev(lam), dev(mu), dev(z), dev(z), 1e-3, 0.5)
+    assert not host(ql).any() and not host(qm).any()
