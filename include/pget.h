@@ -137,7 +137,7 @@ typedef struct {
     double js2;           /* ||Js||^2                                                         */
     double als2;          /* alpha ||Ls||^2                                                   */
     double bs;            /* <b, s>                                                           */
-    int32_t accepted;     /* rho > eta = 0.1             (PGET_GN_EVAL_TRIAL)                 */
+    int32_t accepted;     /* pred > 0 and rho > eta = 0.1 (PGET_GN_EVAL_TRIAL; reading R-accept)  */
     int32_t n_cg_done;    /* CG steps performed                                               */
     int32_t breakdown;    /* 0 none, 1 zeta == 0, 2 <p,Hp> <= 0                              */
     int32_t pad_;
@@ -243,7 +243,7 @@ pget_status pget_gn_apply(pget_geometry g, const float* lam, const float* mu, co
 /* One LM iteration at u = (lam, mu) for measurements y_meas:
  * r = F(u) - y; b = -(J^T r + alpha L^T L u); n_cg CG steps from s = 0 on
  * (J^T J + alpha L^T L + beta I) s = b; pred; with PGET_GN_EVAL_TRIAL also f(u+s),
- * rho, accept (rho > 0.1) and beta_next.  Writes s to (s_lam, s_mu) and `batch`
+ * rho, accept (pred > 0 and rho > 0.1, reading R-accept) and beta_next.  Writes s to (s_lam, s_mu) and `batch`
  * pget_gn_stats structs to stats_dev (device memory).  0 <= n_cg <= PGET_MAX_CG. */
 pget_status pget_gn_cg_step(pget_geometry g, const float* lam, const float* mu, const float* y_meas,
                             float alpha, float beta, int32_t n_cg, uint32_t flags, float* s_lam,
@@ -252,11 +252,19 @@ pget_status pget_gn_cg_step(pget_geometry g, const float* lam, const float* mu, 
 
 /* Full LM solve (the paper's deterministic LMA iterated; the alpha continuation
  * alpha_k = alpha0 / 5^k frozen later), per batch member, on the device: for
- * k = 0..n_iter-1 one pget_gn_cg_step at (u_k, alpha_k, beta_k) with PGET_GN_EVAL_TRIAL, where with
- * PGET_LM_BOX the CG step is first replaced by s' = clamp(u_k + s) - u_k (pred and rho then refer to
- * s'; reading R-N1: a projected step instead of the paper's scaled gradient projection); then
- * u_{k+1} = u_k + s' if rho > 0.1 (accepted) else u_k, and beta_{k+1} = beta_next (x10 on reject, at
- * least beta_min; x0.2 if rho > 0.75).  With PGET_LM_BOX the initial guess is clamped first.
+ * k = 0..n_iter-1 one LM iteration at (u_k, alpha_k, beta_k) with PGET_GN_EVAL_TRIAL.  The feasible
+ * set (PGET_LM_BOX) is the box [lam_lo, lam_hi] x [mu_lo, mu_hi], intersected with lam <= c mu when
+ * lam_per_mu = c > 0 (reading R-lin); P denotes the per-pixel Euclidean projection onto
+ * it.  The inner solver is either
+ *   - CG (default; reading R-N1): n_cg CG steps on the unconstrained normal equations, then the step
+ *     is replaced by the step actually taken, s' = P(u_k + s) - u_k; or
+ *   - scaled gradient projection (PGET_LM_SGP, the paper's solver; reading R-SGP):
+ *     n_cg projected-gradient iterations on the box-constrained quadratic model, whose iterates stay
+ *     feasible, so s' = s.
+ * pred, rho and the trial point refer to s' (the trial point u_k + s' is feasible).  Then
+ * u_{k+1} = u_k + s' if pred > 0 and rho > 0.1 (accepted, reading R-accept) else u_k, and
+ * beta_{k+1} = beta_next (x10 on reject, at least beta_min; x0.2 if rho > 0.75).  With PGET_LM_BOX the
+ * initial guess is projected first, so every iterate is feasible.
  * lam, mu: device images, updated in place.  stats_dev: n_iter * batch pget_gn_stats records, iteration-major,
  * receiving every iteration's statistics.  Workspace: pget_workspace_bytes(g, PGET_OP_LM_SOLVE).
  * No host synchronisation; errors as for pget_gn_cg_step. */
@@ -278,6 +286,15 @@ pget_status pget_safeguard(pget_geometry g, const float* lam, const float* mu, c
                            const float* cand_mu, float alpha, float kappa, float* u_next_lam,
                            float* u_next_mu, pget_safeguard_stats* stats_dev, void* ws,
                            size_t ws_bytes, pget_stream_t stream);
+
+/* Diagnostic (tests): where the CG vectors of an LM iteration live inside its workspace.  For op
+ * PGET_OP_GN_CG_STEP, region PGET_WS_P_LAM / P_MU is the CG direction p and PGET_WS_Q_LAM / Q_MU the
+ * product q = H p of the last CG step, each [batch][N][N] fp32 at ws + *offset.  After a call with
+ * n_cg = k >= 1 they hold p_k and q_{k-1} = H p_{k-1} (with n_cg = 0: p_0 = b), so a caller can pin
+ * the operator the CG loop applies, step by step.  PGET_OK, or
+ * PGET_ERR_INVALID_ARGUMENT for a bad op / region.  Host-side, no device access. */
+enum { PGET_WS_P_LAM = 0, PGET_WS_P_MU = 1, PGET_WS_Q_LAM = 2, PGET_WS_Q_MU = 3 };
+pget_status pget_workspace_region(pget_geometry g, int op, int region, size_t* offset, size_t* bytes);
 
 /* Diagnostic: checks on the host that the handle's static schedules are consistent (every
  * (member, angle-bank, detector) of the forward/JVP schedules covered once; the adjoint's row

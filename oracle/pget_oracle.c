@@ -712,8 +712,10 @@ step_done:
     double f1 = objective(g, ut, ut + npx, y, alpha, &mis2, &reg2, r, tl);
     double rho = (f0 - f1) / pred;
     stats[5] = f1; stats[6] = rho;
-    /* 8: accept iff rho > eta = 0.1; beta update x10 (reject) / x0.2 (rho > 0.75) */
-    int acc = rho > 0.1;
+    /* 8: accept iff pred > 0 and rho > eta = 0.1 (reading R-accept: rho compares the actual with the
+     *    predicted decrease, PAPER.md:248 eq:rho_agreement, and only a positive predicted decrease makes
+     *    rho > eta a decrease of f); beta update x10 (reject) / x0.2 (rho > 0.75) */
+    int acc = pred > 0.0 && rho > 0.1;
     double bn = beta;
     if (!acc) bn = (10.0 * beta > beta_min) ? 10.0 * beta : beta_min;
     else if (rho > 0.75) bn = 0.2 * beta;

@@ -118,11 +118,13 @@ def lib():
         L.pget_safeguard.argtypes = [P, P, P, P, P, P, P, P, C.c_float, C.c_float, P, P, P, P, S, P]
         L.pget_lm_solve.argtypes = [P, P, P, P, C.POINTER(LMParams), P, P, S, P]
         L.pget_schedule_check.argtypes = [P]
+        L.pget_workspace_region.argtypes = [P, C.c_int, C.c_int, C.POINTER(S), C.POINTER(S)]
         L.pget_set_prior.argtypes = [P, C.POINTER(Prior)]
         L.pget_profile_begin.argtypes = [C.c_int32]
         L.pget_profile_end.argtypes = [P, P, P]
         for n in ("pget_profile_begin", "pget_profile_end", "pget_geometry_create", "pget_geometry_destroy", "pget_geometry_info", "pget_geometry_export",
-                  "pget_forward", "pget_jvp", "pget_vjp", "pget_gn_apply", "pget_gn_cg_step", "pget_safeguard", "pget_lm_solve", "pget_schedule_check", "pget_set_prior"):
+                  "pget_forward", "pget_jvp", "pget_vjp", "pget_gn_apply", "pget_gn_cg_step", "pget_safeguard", "pget_lm_solve", "pget_schedule_check", "pget_set_prior",
+                  "pget_workspace_region"):
             getattr(L, n).restype = C.c_int
         _lib = L
     return _lib
@@ -213,6 +215,13 @@ class Geometry:
         _check(lib().pget_set_prior(self._h, C.byref(pr)), "pget_set_prior")
         self._prior = (mask_lam, mask_mu)
 
+    def workspace_region(self, op: str, region: int):
+        """(offset, bytes) of a CG vector inside `op`'s workspace (pget_workspace_region; tests)."""
+        off, n = C.c_size_t(), C.c_size_t()
+        _check(lib().pget_workspace_region(self._h, OPS[op], int(region), C.byref(off), C.byref(n)),
+               "pget_workspace_region")
+        return off.value, n.value
+
     def schedule_check(self):
         """Host-side consistency check of the handle's static schedules (raises on a violation)."""
         _check(lib().pget_schedule_check(self._h), "pget_schedule_check")
@@ -232,11 +241,15 @@ class Geometry:
 
 
 def _f32(t, shape, what):
+    """A contiguous float32 CUDA tensor of exactly `shape` ([B][N][N] images, [B][n_angles][n_banks][n_det]
+    sinograms); with batch 1 the leading batch axis may be omitted.  Anything else raises: the C ABI
+    reads raw pointers, so a tensor of the right size in another layout would be misread."""
     import torch
     if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
         raise TypeError(f"{what}: expected a contiguous float32 CUDA tensor")
-    if tuple(t.shape) != tuple(shape) and t.numel() != int(np.prod(shape)):
-        raise ValueError(f"{what}: shape {tuple(t.shape)} != {tuple(shape)}")
+    shape = tuple(shape)
+    if tuple(t.shape) != shape and not (shape[0] == 1 and tuple(t.shape) == shape[1:]):
+        raise ValueError(f"{what}: shape {tuple(t.shape)} != {shape}")
     return t
 
 
@@ -245,6 +258,7 @@ def forward(g: Geometry, lam, mu, y=None, ws=None, stream=None):
     _f32(lam, g.img_shape, "lam"); _f32(mu, g.img_shape, "mu")
     if y is None:
         y = torch.empty(g.sino_shape, dtype=torch.float32, device=lam.device)
+    _f32(y, g.sino_shape, "y")
     ws = g.workspace("forward") if ws is None else ws
     _check(lib().pget_forward(g.handle, _ptr(lam), _ptr(mu), _ptr(y), _ptr(ws), ws.numel(), _stream(stream)),
            "pget_forward")
@@ -259,6 +273,9 @@ def jvp(g: Geometry, lam, mu, dlam, dmu, want_y=False, y=None, dy=None, ws=None,
         dy = torch.empty(g.sino_shape, dtype=torch.float32, device=lam.device)
     if want_y and y is None:
         y = torch.empty(g.sino_shape, dtype=torch.float32, device=lam.device)
+    _f32(dy, g.sino_shape, "dy")
+    if want_y:
+        _f32(y, g.sino_shape, "y")
     ws = g.workspace("jvp") if ws is None else ws
     _check(lib().pget_jvp(g.handle, _ptr(lam), _ptr(mu), _ptr(dlam), _ptr(dmu), _ptr(y) if want_y else None,
                           _ptr(dy), _ptr(ws), ws.numel(), _stream(stream)), "pget_jvp")
@@ -271,6 +288,7 @@ def vjp(g: Geometry, lam, mu, w, g_lam=None, g_mu=None, ws=None, stream=None):
     if g_lam is None:
         g_lam = torch.empty(g.img_shape, dtype=torch.float32, device=lam.device)
         g_mu = torch.empty(g.img_shape, dtype=torch.float32, device=lam.device)
+    _f32(g_lam, g.img_shape, "g_lam"); _f32(g_mu, g.img_shape, "g_mu")
     ws = g.workspace("vjp") if ws is None else ws
     _check(lib().pget_vjp(g.handle, _ptr(lam), _ptr(mu), _ptr(w), _ptr(g_lam), _ptr(g_mu), _ptr(ws), ws.numel(),
                           _stream(stream)), "pget_vjp")
@@ -279,6 +297,8 @@ def vjp(g: Geometry, lam, mu, w, g_lam=None, g_mu=None, ws=None, stream=None):
 
 def gn_apply(g: Geometry, lam, mu, p_lam, p_mu, alpha, beta, ws=None, stream=None):
     import torch
+    for t, n in ((lam, "lam"), (mu, "mu"), (p_lam, "p_lam"), (p_mu, "p_mu")):
+        _f32(t, g.img_shape, n)
     q_lam = torch.empty(g.img_shape, dtype=torch.float32, device=lam.device)
     q_mu = torch.empty_like(q_lam)
     ws = g.workspace("gn_apply") if ws is None else ws
@@ -310,6 +330,7 @@ def gn_cg_step(g: Geometry, lam, mu, y_meas, alpha, beta, n_cg, flags=PGET_GN_EV
     if s_lam is None:
         s_lam = torch.empty(g.img_shape, dtype=torch.float32, device=lam.device)
         s_mu = torch.empty_like(s_lam)
+    _f32(s_lam, g.img_shape, "s_lam"); _f32(s_mu, g.img_shape, "s_mu")
     if stats is None:
         stats = stats_buffer(g, lam.device)
     ws = g.workspace("gn_cg_step") if ws is None else ws

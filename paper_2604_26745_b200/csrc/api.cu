@@ -481,11 +481,22 @@ WS carve(const Geometry& g, int op, char* base)
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-pget_status check_ptrs(std::initializer_list<const void*> ptrs, const char* what)
+// every pointer argument: non-NULL, 16-byte aligned, CUDA device (or managed) memory of the handle's device
+pget_status check_ptrs(std::initializer_list<const void*> ptrs, const char* what, int device)
 {
     for (const void* p : ptrs) {
         if (!p) return fail(PGET_ERR_INVALID_ARGUMENT, std::string(what) + ": NULL device pointer");
         if (!aligned16(p)) return fail(PGET_ERR_ALIGNMENT, std::string(what) + ": pointer not 16-byte aligned");
+        cudaPointerAttributes at;
+        if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+            cudaGetLastError();   // clear the sticky-free error state of the failed query
+            return fail(PGET_ERR_INVALID_ARGUMENT, std::string(what) + ": pointer is not CUDA memory");
+        }
+        if (at.type == cudaMemoryTypeManaged) continue;
+        if (at.type != cudaMemoryTypeDevice)
+            return fail(PGET_ERR_INVALID_ARGUMENT, std::string(what) + ": pointer is not device memory");
+        if (at.device != device)
+            return fail(PGET_ERR_INVALID_ARGUMENT, std::string(what) + ": pointer on another device");
     }
     return PGET_OK;
 }
@@ -1040,7 +1051,7 @@ pget_status pget_forward(pget_geometry h, const float* lam, const float* mu, flo
     WS w;
     pget_status st = check_common(h, PGET_OP_FORWARD, ws, ws_bytes, &w);
     if (st) return st;
-    if ((st = check_ptrs({lam, mu, y}, "pget_forward"))) return st;
+    if ((st = check_ptrs({lam, mu, y}, "pget_forward", h->g.device))) return st;
     const Geometry& g = h->g;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if ((st = pack2(g, w, lam, mu, nullptr, nullptr, nullptr, nullptr, s))) return st;
@@ -1053,7 +1064,7 @@ pget_status pget_jvp(pget_geometry h, const float* lam, const float* mu, const f
     WS w;
     pget_status st = check_common(h, PGET_OP_JVP, ws, ws_bytes, &w);
     if (st) return st;
-    if ((st = check_ptrs({lam, mu, dlam, dmu, dy}, "pget_jvp"))) return st;
+    if ((st = check_ptrs({lam, mu, dlam, dmu, dy}, "pget_jvp", h->g.device))) return st;
     if (y && !aligned16(y)) return fail(PGET_ERR_ALIGNMENT, "pget_jvp: y not 16-byte aligned");
     const Geometry& g = h->g;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -1067,7 +1078,7 @@ pget_status pget_vjp(pget_geometry h, const float* lam, const float* mu, const f
     WS w;
     pget_status st = check_common(h, PGET_OP_VJP, ws, ws_bytes, &w);
     if (st) return st;
-    if ((st = check_ptrs({lam, mu, wv, g_lam, g_mu}, "pget_vjp"))) return st;
+    if ((st = check_ptrs({lam, mu, wv, g_lam, g_mu}, "pget_vjp", h->g.device))) return st;
     const Geometry& g = h->g;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int N = g.desc.n_px, B = g.desc.batch;
@@ -1087,7 +1098,7 @@ pget_status pget_gn_apply(pget_geometry h, const float* lam, const float* mu, co
     WS w;
     pget_status st = check_common(h, PGET_OP_GN_APPLY, ws, ws_bytes, &w);
     if (st) return st;
-    if ((st = check_ptrs({lam, mu, p_lam, p_mu, q_lam, q_mu}, "pget_gn_apply"))) return st;
+    if ((st = check_ptrs({lam, mu, p_lam, p_mu, q_lam, q_mu}, "pget_gn_apply", h->g.device))) return st;
     if (!std::isfinite(alpha) || !std::isfinite(beta) || alpha < 0.f || beta < 0.f)
         return fail(PGET_ERR_INVALID_ARGUMENT, "alpha, beta must be finite and >= 0");
     const Geometry& g = h->g;
@@ -1276,7 +1287,7 @@ pget_status pget_gn_cg_step(pget_geometry h, const float* lam, const float* mu, 
     WS w;
     pget_status st = check_common(h, PGET_OP_GN_CG_STEP, ws, ws_bytes, &w);
     if (st) return st;
-    if ((st = check_ptrs({lam, mu, y_meas, s_lam, s_mu, stats}, "pget_gn_cg_step"))) return st;
+    if ((st = check_ptrs({lam, mu, y_meas, s_lam, s_mu, stats}, "pget_gn_cg_step", h->g.device))) return st;
     if (n_cg < 0 || n_cg > PGET_MAX_CG) return fail(PGET_ERR_INVALID_ARGUMENT, "n_cg out of [0, PGET_MAX_CG]");
     if (!std::isfinite(alpha) || !std::isfinite(beta) || alpha < 0.f || beta < 0.f)
         return fail(PGET_ERR_INVALID_ARGUMENT, "alpha, beta must be finite and >= 0");
@@ -1292,7 +1303,7 @@ pget_status pget_lm_solve(pget_geometry h, float* lam, float* mu, const float* y
     WS w;
     pget_status st = check_common(h, PGET_OP_LM_SOLVE, ws, ws_bytes, &w);
     if (st) return st;
-    if ((st = check_ptrs({lam, mu, y_meas, stats}, "pget_lm_solve"))) return st;
+    if ((st = check_ptrs({lam, mu, y_meas, stats}, "pget_lm_solve", h->g.device))) return st;
     if (!prm) return fail(PGET_ERR_INVALID_ARGUMENT, "pget_lm_solve: NULL params");
     const pget_lm_params p = *prm;
     if (p.n_iter < 0 || p.n_cg < 0 || p.n_cg > PGET_MAX_CG || p.k_freeze < 0)
@@ -1347,8 +1358,7 @@ pget_status pget_safeguard(pget_geometry h, const float* lam, const float* mu, c
     WS w;
     pget_status st = check_common(h, PGET_OP_SAFEGUARD, ws, ws_bytes, &w);
     if (st) return st;
-    if ((st = check_ptrs({lam, mu, y_meas, s_lam, s_mu, cand_lam, cand_mu, u_next_lam, u_next_mu, stats},
-                         "pget_safeguard")))
+    if ((st = check_ptrs({lam, mu, y_meas, s_lam, s_mu, cand_lam, cand_mu, u_next_lam, u_next_mu, stats}, "pget_safeguard", h->g.device)))
         return st;
     if (!std::isfinite(alpha) || alpha < 0.f) return fail(PGET_ERR_INVALID_ARGUMENT, "alpha must be finite and >= 0");
     if (!std::isfinite(kappa) || !(kappa > 0.f)) return fail(PGET_ERR_INVALID_ARGUMENT, "kappa must be finite and > 0");
@@ -1532,6 +1542,24 @@ pget_status pget_schedule_check(pget_geometry h)
     for (int c : rseen)
         if (c != 1) return bad("comb groups do not cover every ray once");
     (void)J;
+    return PGET_OK;
+}
+
+pget_status pget_workspace_region(pget_geometry h, int op, int region, size_t* offset, size_t* bytes)
+{
+    if (!h || !offset || !bytes) return fail(PGET_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (op != PGET_OP_GN_CG_STEP) return fail(PGET_ERR_INVALID_ARGUMENT, "pget_workspace_region: op");
+    const WS w = carve(h->g, op, reinterpret_cast<char*>(uintptr_t(1) << 40));
+    const float* p = nullptr;
+    switch (region) {
+    case PGET_WS_P_LAM: p = w.pl; break;
+    case PGET_WS_P_MU: p = w.pm; break;
+    case PGET_WS_Q_LAM: p = w.ql; break;
+    case PGET_WS_Q_MU: p = w.qm; break;
+    default: return fail(PGET_ERR_INVALID_ARGUMENT, "pget_workspace_region: region");
+    }
+    *offset = static_cast<size_t>(reinterpret_cast<uintptr_t>(p) - (uintptr_t(1) << 40));
+    *bytes = static_cast<size_t>(h->g.desc.batch) * h->g.desc.n_px * h->g.desc.n_px * sizeof(float);
     return PGET_OK;
 }
 

@@ -535,7 +535,7 @@ __global__ void scalar_kernel(int op, int k, const double* p0, const double* p1,
         if (pp) f1 += 0.5 * psum(pp, m, nblk);   // priors of u + s
         S.f_trial = f1;
         S.rho = (S.f - f1) / S.pred;
-        S.accepted = S.rho > 0.1;
+        S.accepted = S.pred > 0.0 && S.rho > 0.1;   // reading R-accept
         double bn = beta;
         if (!S.accepted) bn = (10.0 * beta > S.beta_min) ? 10.0 * beta : S.beta_min;
         else if (S.rho > 0.75) bn = 0.2 * beta;

@@ -26,6 +26,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
+#include <mutex>
+#include <utility>
+
 #include "internal.h"
 #include "kernels.cuh"
 
@@ -2038,20 +2042,38 @@ cudaError_t launch_gnc(int phase, bool paired, const ProjArgs& A, int grid, int 
     return cudaGetLastError();
 }
 
+// Dynamic shared-memory limits are a per-(device, kernel) process-wide attribute: only ever raised, so a
+// handle created later with a smaller configuration never lowers the limit an earlier (larger) handle
+// relies on (handles are immutable and usable side by side, include/pget.h).
+static std::mutex g_smem_mu;
+static std::map<std::pair<int, const void*>, int> g_smem_hw;
+template <class F>
+static cudaError_t raise_smem(F* fn, int v)
+{
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lk(g_smem_mu);
+    int& hw = g_smem_hw[{dev, reinterpret_cast<const void*>(fn)}];
+    if (v <= hw) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
+    if (e == cudaSuccess) hw = v;
+    return e;
+}
+
 cudaError_t set_gnc_smem_limit(size_t smem)
 {
     const int v = static_cast<int>(smem);
-    const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(lin_kernel<true>, a, v))) return e;
-    if ((e = cudaFuncSetAttribute(lin_kernel<false>, a, v))) return e;
-    if ((e = cudaFuncSetAttribute(jvpc_kernel, a, v))) return e;
-    if ((e = cudaFuncSetAttribute(gnb_kernel<true, false>, a, v))) return e;
-    if ((e = cudaFuncSetAttribute(gnb_kernel<true, true>, a, v))) return e;
-    if ((e = cudaFuncSetAttribute(gnb_kernel<false, true>, a, v))) return e;
-    if ((e = cudaFuncSetAttribute(jsq_kernel<true>, a, v))) return e;
-    if ((e = cudaFuncSetAttribute(jsq_kernel<false>, a, v))) return e;
-    return cudaFuncSetAttribute(gnb_kernel<false, false>, a, v);
+    if ((e = raise_smem(lin_kernel<true>, v))) return e;
+    if ((e = raise_smem(lin_kernel<false>, v))) return e;
+    if ((e = raise_smem(jvpc_kernel, v))) return e;
+    if ((e = raise_smem(gnb_kernel<true, false>, v))) return e;
+    if ((e = raise_smem(gnb_kernel<true, true>, v))) return e;
+    if ((e = raise_smem(gnb_kernel<false, true>, v))) return e;
+    if ((e = raise_smem(jsq_kernel<true>, v))) return e;
+    if ((e = raise_smem(jsq_kernel<false>, v))) return e;
+    return raise_smem(gnb_kernel<false, false>, v);
 }
 
 // ------------------------------------------------------------------------------------------ reduction
@@ -2199,27 +2221,26 @@ template <int MODE>
 static cudaError_t seg_attr_mode(int phase, size_t smem)
 {
     const int v = static_cast<int>(smem);
-    const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
     cudaError_t e;
     if (phase == 0) {
-        if ((e = cudaFuncSetAttribute(seg_a_kernel<MODE, 1, true>, a, v))) return e;
-        if ((e = cudaFuncSetAttribute(seg_a_kernel<MODE, 2, true>, a, v))) return e;
-        if ((e = cudaFuncSetAttribute(seg_a_kernel<MODE, 1, false>, a, v))) return e;
-        return cudaFuncSetAttribute(seg_a_kernel<MODE, 2, false>, a, v);
+        if ((e = raise_smem(seg_a_kernel<MODE, 1, true>, v))) return e;
+        if ((e = raise_smem(seg_a_kernel<MODE, 2, true>, v))) return e;
+        if ((e = raise_smem(seg_a_kernel<MODE, 1, false>, v))) return e;
+        return raise_smem(seg_a_kernel<MODE, 2, false>, v);
     }
-    if ((e = cudaFuncSetAttribute(seg_b_kernel<MODE, true, false>, a, v))) return e;
-    if ((e = cudaFuncSetAttribute(seg_b_kernel<MODE, false, false>, a, v))) return e;
-    if ((e = cudaFuncSetAttribute(seg_b_kernel<MODE, true, MODE == MODE_VJP>, a, v))) return e;
-    return cudaFuncSetAttribute(seg_b_kernel<MODE, false, MODE == MODE_VJP>, a, v);
+    if ((e = raise_smem(seg_b_kernel<MODE, true, false>, v))) return e;
+    if ((e = raise_smem(seg_b_kernel<MODE, false, false>, v))) return e;
+    if ((e = raise_smem(seg_b_kernel<MODE, true, MODE == MODE_VJP>, v))) return e;
+    return raise_smem(seg_b_kernel<MODE, false, MODE == MODE_VJP>, v);
 }
 
 cudaError_t set_seg_smem_limit(int phase, int mode, size_t smem)
 {
     if (mode == MODE_JVP) {
         const int v = static_cast<int>(smem);
-        cudaError_t e = cudaFuncSetAttribute(seg_a_kernel<MODE_JVP, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
+        cudaError_t e = raise_smem(seg_a_kernel<MODE_JVP, 1, false>, v);
         if (e) return e;
-        return cudaFuncSetAttribute(seg_a_kernel<MODE_JVP, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
+        return raise_smem(seg_a_kernel<MODE_JVP, 2, false>, v);
     }
     if (mode == MODE_VJP) return seg_attr_mode<MODE_VJP>(phase, smem);
     if (mode == MODE_GN) return seg_attr_mode<MODE_GN>(phase, smem);
@@ -2235,10 +2256,10 @@ static cudaError_t attr_mode(size_t smem)
     constexpr bool CP = MODE != MODE_JVP;
     const int v = static_cast<int>(smem);
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(proj_kernel<MODE, 1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, v))) return e;
-    if ((e = cudaFuncSetAttribute(proj_kernel<MODE, 2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, v))) return e;
-    if ((e = cudaFuncSetAttribute(proj_kernel<MODE, 1, CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, v))) return e;
-    return cudaFuncSetAttribute(proj_kernel<MODE, 2, CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
+    if ((e = raise_smem(proj_kernel<MODE, 1, false>, v))) return e;
+    if ((e = raise_smem(proj_kernel<MODE, 2, false>, v))) return e;
+    if ((e = raise_smem(proj_kernel<MODE, 1, CP>, v))) return e;
+    return raise_smem(proj_kernel<MODE, 2, CP>, v);
 }
 
 cudaError_t set_proj_smem_limit(int mode, size_t smem)

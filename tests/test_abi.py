@@ -122,3 +122,22 @@ def test_static_schedules_consistent(gd):
     stages, slots, reduce lists, coefficient-cache layout, comb groups) pass pget_schedule_check."""
     g = pg.Geometry(gd, device=-1)
     g.schedule_check()
+
+
+def test_workspace_regions_inside_and_disjoint():
+    """pget_workspace_region: the CG vectors p, q of an LM iteration are four disjoint image-sized
+    regions inside the workspace the call asks for."""
+    gd = P.geometry_desc(2)
+    g = pg.Geometry(gd, device=-1)
+    total = g.workspace_bytes("gn_cg_step")
+    spans = [g.workspace_region("gn_cg_step", r) for r in range(4)]
+    img = int(np.prod(g.img_shape)) * 4
+    for off, n in spans:
+        assert n == img and off % 16 == 0 and off + n <= total
+    spans.sort()
+    for (a, n), (b, _) in zip(spans, spans[1:]):
+        assert a + n <= b
+    with pytest.raises(RuntimeError):
+        g.workspace_region("forward", 0)
+    with pytest.raises(RuntimeError):
+        g.workspace_region("gn_cg_step", 7)

@@ -346,6 +346,61 @@ def test_p11_cg_equals_dense_solve():
     assert abs(st["pred"] - (m(np.zeros_like(s)) - m(s))) <= 1e-9 * abs(st["pred"])
 
 
+def test_p11_cg_equals_dense_solve_with_priors():
+    """With the O10 priors (diagonal masks m1, m2, weights a1, a2) the LM step solves
+    (J^T J + alpha L^T L + diag(a1 m1^2, a2 m2^2) + beta I) s = b with b = -(J^T r + alpha L^T L u +
+    (a1 m1^2 lam, a2 m2^2 mu)), and pred = m(0) - m(s) for the model with the prior rows
+    sqrt(a1) m1 lam, sqrt(a2) m2 mu of F~ (eq:m-function).  Every matrix
+    here is built in numpy from JVP columns and the masks; a dropped or doubled prior term in the
+    oracle's b, H, or pred (its ps2 = 2 prior_value(s)) fails one of the three checks."""
+    N = 6
+    g = dict(n_px=N, n_angles=6, n_banks=2, n_det=9, n_subrays=2, subray_sigma=0.4, step_px=0.5,
+             bank1_shift=0.0, batch=1)
+    rng = np.random.default_rng(7)
+    lam, mu = rng.uniform(0.3, 1.2, (1, N, N)), rng.uniform(0.1, 0.5, (1, N, N))
+    y = O.forward(g, rng.uniform(0.3, 1.2, (1, N, N)), rng.uniform(0.1, 0.5, (1, N, N)))
+    m1 = (rng.uniform(size=(1, N, N)) < 0.5).astype(np.float64)
+    m2 = (rng.uniform(size=(1, N, N)) < 0.5).astype(np.float64)
+    a1, a2 = 0.7, 3.0
+    alpha, beta = 1e-2, 0.05
+    Jd, Ld, H = _dense_H(g, lam, mu, alpha, beta)
+    D = np.concatenate([a1 * m1.ravel() ** 2, a2 * m2.ravel() ** 2])
+    H = H + np.diag(D)
+    r = (O.forward(g, lam, mu) - y).ravel()
+    u = np.concatenate([lam.ravel(), mu.ravel()])
+    b = -(Jd.T @ r + alpha * Ld.T @ (Ld @ u) + D * u)
+    s_ref = np.linalg.solve(H, b)
+    pr = (m1, m2, a1, a2)
+    sl, sm, st = O.gn_cg_step(g, lam, mu, y, alpha, beta, 200, prior=pr)
+    s = np.concatenate([sl.ravel(), sm.ravel()])
+    assert rel_l2(s, s_ref) <= 1e-8
+    assert abs(st["grad_norm"] - np.linalg.norm(b)) <= 1e-10 * np.linalg.norm(b)
+
+    def m(sv):
+        return (0.5 * np.sum((r + Jd @ sv) ** 2) + 0.5 * alpha * np.sum((Ld @ (u + sv)) ** 2)
+                + 0.5 * np.sum(D * (u + sv) ** 2))
+    s0 = np.zeros_like(s)
+    assert abs(st["f"] - m(s0)) <= 1e-12 * st["f"]
+    assert abs(st["pred"] - (m(s0) - m(s))) <= 1e-9 * abs(st["pred"])
+    # the same at a truncated CG iterate (s not the minimiser, so pred's quadratic term is tested
+    # separately from <b, s>): 3 CG steps
+    sl, sm, st = O.gn_cg_step(g, lam, mu, y, alpha, beta, 3, prior=pr)
+    s = np.concatenate([sl.ravel(), sm.ravel()])
+    assert abs(st["pred"] - (m(s0) - m(s))) <= 1e-9 * abs(st["pred"])
+    assert abs(st["als2"] - (alpha * np.sum((Ld @ s) ** 2) + np.sum(D * s ** 2))) <= 1e-9 * st["als2"]
+
+
+def test_p12_reject_when_pred_not_positive():
+    """Reading R-accept: rho = (f(u) - f(u+s)) / pred is the ratio of the actual to the predicted
+    decrease (eq:rho_agreement); a box that clips the CG step hard makes pred < 0, and
+    a step that then raises f has rho > eta although it is no decrease.  Such a step is rejected."""
+    g, _, y, (l0, m0) = _tiny_lm()
+    sl, sm, st = O.lm_step_box(g, l0, m0, y, 1e-3, 0.0, 8, (0.7, 0.9, 0.28, 0.31), inner="cg")
+    assert st["pred"] < 0 and st["f_trial"] > st["f"] and st["rho"] > 0.1   # the old rule accepted it
+    assert not st["accepted"]
+    assert st["beta_next"] == max(0.0, st["beta_min"])
+
+
 def test_p11_cg_recurrence_residuals():
     N = 8
     g = dict(n_px=N, n_angles=8, n_banks=2, n_det=11, n_subrays=2, subray_sigma=0.4, step_px=0.5,
