@@ -3,11 +3,15 @@
 "ray-samples/s for fwd/JVP/VJP and ms per LM iteration at 1 B200 vs roofline").
 
 One step = one pass of the whole hot path over one
-batch of synthetic config-2 input (BASELINE.json configs[1]: 9x9 lattice, N=128,
-360 angles, 2x91 detectors, J=5, Poisson noise at 1e4 peak):
+batch of synthetic config-4 input (BASELINE.json configs[3], the largest single-GPU
+configuration with an LM iteration: hexagonal 127-rod assembly, N=256, 720 angles,
+2x91 detectors, J=9, Poisson noise at 1e4 peak):
     forward(u) + JVP(u; du) + VJP(u; w) + one LM iteration (20 CG steps, alpha=1e-3,
     beta=0, trial evaluation)
 value = nominal ray-sample passes per step x steps x ranks / max-over-ranks device time.
+The same JSON line carries `per_config`: forward / JVP / VJP ray-samples/s, ms per LM
+iteration and the per-kernel roofline fractions of configs 1-5 (the north star's
+"throughput on the five synthetic assemblies"), with config 5's HBM GB/s.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 Multi-GPU (torchrun): every rank runs an independent replica (the assemblies are
@@ -28,8 +32,33 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "ray-samples/s for fwd/JVP/VJP and ms per LM iteration at 1 B200 vs roofline"
-SMEM_B_PER_CLK_SM = 128          # guide: smem/L1 crossbar bytes per clock per SM
+SMEM_B_PER_CLK_SM = 128          # guide: smem/L1 crossbar bytes per clock per SM (fallback)
 N_SM = 148
+REF_ANGLES = {1: 90, 2: 36, 3: 18, 4: 18, 5: 36}   # oracle sample per config: ~1-3 s of host time per step
+
+
+def smem_peak():
+    """Shared-memory data-path peak per SM per clock: the measured LDS.128 figure
+    (scripts/micro/smem_bw.cu, profiles/smem_peak.json) when committed, else the guide's nominal 128 B."""
+    p = os.path.join(ROOT, "profiles", "smem_peak.json")
+    try:
+        d = json.load(open(p))
+        return float(d["bytes_per_clk_per_sm"]), f"measured LDS.128 peak {d['bytes_per_clk_per_sm']:.1f} B/clk/SM (profiles/smem_peak.json)"
+    except Exception:
+        return float(SMEM_B_PER_CLK_SM), "nominal 128 B/clk/SM (B200_PROFILING guide)"
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or None
+
+
 # algorithmic shared-memory bytes per nominal ray-sample (SURVEY.md §8(d) table; DESIGN.md)
 ALG_BYTES = {"forward": 32, "jvp": 64, "vjp": 32 + 32 + 64, "gn": 64 + 32 + 64}
 
@@ -125,7 +154,7 @@ def reference_arm(args, rank, world):
     import oracle as O
     import pget_data as P
     cfg = P.CONFIGS[args.config]
-    sample = cpu_sample(cfg, args.ref_angles)
+    sample = cpu_sample(cfg, args.ref_angles or REF_ANGLES[cfg.cid])
     times = []
     for k in range(args.warmup + args.steps):
         dt, n = run_oracle_step(O, P, cfg, sample)
@@ -139,7 +168,8 @@ def reference_arm(args, rank, world):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload(cfg), "sample": sample["desc"]},
         "cpu_baseline": {"value": value, "unit": "ray-samples/s", "cores": O.threads(), "kind": "oracle",
-                         "sample": sample["desc"]},
+                         "sample": sample["desc"], "cpu_model": cpu_model(),
+                         "omp_num_threads": os.environ.get("OMP_NUM_THREADS")},
         "e2e": {"value": value, "unit": "ray-samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -199,14 +229,105 @@ def roofline_ncu(cid, dom):
         return None
 
 
+def measure_config(pg, P, cid, flush, sm_mhz, reps=5):
+    """Per-config block (not the headline value): forward / JVP / VJP nominal ray-samples/s and ms per
+    LM iteration (median over reps of CUDA-event timings on the current stream, L2 flushed before each
+    op), the projector launches' algorithmic roofline fractions (bytes per traced sample of
+    ALG_BYTES x traced samples / average launch time / shared-memory peak), and for config 5 (the
+    batched case) the HBM GB/s of the operations' algorithmic bytes (inputs read + outputs written)."""
+    import torch
+    cfg = P.CONFIGS[cid]
+    gd = P.geometry_desc(cid)
+    g = pg.Geometry(gd)
+    nominal, traced, traced_j = (g.info[k] for k in ("n_samples_nominal", "n_samples_traced", "n_samples_traced_jvp"))
+    dev = lambda x: torch.from_numpy(np.ascontiguousarray(x, np.float32)).cuda()
+    lam, mu = map(dev, P.make_phantom(cid))
+    dl, dm = map(dev, P.rod_directions(cid))
+    lp, mp = map(dev, P.make_phantom_prime(cid))
+    l0, m0 = map(dev, P.initial_guess(cfg.n_px, cfg.batch))
+    y_clean = pg.forward(g, lam, mu)
+    w = (pg.forward(g, lp, mp) - y_clean).contiguous()
+    y_meas = dev(P.poisson_noise(y_clean.cpu().numpy(), cfg.noise_peak or 1e4, cfg.seed))
+    y, dy = torch.empty(g.sino_shape, device="cuda"), torch.empty(g.sino_shape, device="cuda")
+    gl, gm = torch.empty(g.img_shape, device="cuda"), torch.empty(g.img_shape, device="cuda")
+    sl, sm = torch.empty(g.img_shape, device="cuda"), torch.empty(g.img_shape, device="cuda")
+    stats = pg.stats_buffer(g)
+    ops = {
+        "forward": lambda: pg.forward(g, lam, mu, y=y),
+        "jvp": lambda: pg.jvp(g, lam, mu, dl, dm, dy=dy),
+        "vjp": lambda: pg.vjp(g, lam, mu, w, g_lam=gl, g_mu=gm),
+        "lm": lambda: pg.gn_cg_step(g, l0, m0, y_meas, cfg.alpha, 0.0, cfg.n_cg, pg.PGET_GN_EVAL_TRIAL, s_lam=sl,
+                                    s_mu=sm, stats=stats),
+    }
+    nrep = {k: (max(2, reps // 2) if (k == "lm" and cid in (4, 5)) else reps) for k in ops}
+    ms = {}
+    for k, f in ops.items():
+        f()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(nrep[k]):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            f()
+            b.record()
+            b.synchronize()
+            ts.append(a.elapsed_time(b))
+        ms[k] = statistics.median(ts)
+    # per projector launch (CUDA events around each launch inside the library), one more pass
+    pg.profile_begin(256)
+    for k in ("forward", "jvp", "vjp"):
+        flush.zero_()
+        ops[k]()
+    torch.cuda.synchronize()
+    prof = pg.profile_end()
+    pg.profile_begin(256)
+    ops["lm"]()
+    torch.cuda.synchronize()
+    prof_lm = pg.profile_end()
+    bpc, _ = smem_peak()
+    peak = bpc * N_SM * sm_mhz * 1e6
+    kern = {}
+    for mode, pr in (("forward", prof), ("jvp", prof), ("vjp", prof), ("gn", prof_lm)):
+        n = pr["launches"][mode]
+        if not n:
+            continue
+        lms = pr["ms"][mode] / n
+        units = traced_j if mode == "jvp" else traced
+        ach = ALG_BYTES[mode] * units / (lms * 1e-3)
+        kern[mode] = {"launch_ms": lms, "alg_bytes_per_traced_sample": ALG_BYTES[mode], "traced_samples": units,
+                      "achieved_GBps": ach / 1e9, "frac": ach / peak}
+    out = {
+        "workload": f"{cfg.lattice} N={cfg.n_px} angles={cfg.n_angles} J={cfg.n_subrays} B={cfg.batch}",
+        "nominal_samples_per_pass": nominal, "traced_samples_per_pass": traced, "traced_samples_jvp": traced_j,
+        "forward_ms": ms["forward"], "jvp_ms": ms["jvp"], "vjp_ms": ms["vjp"], "lm_ms": ms["lm"],
+        "forward_samples_per_s": nominal / (ms["forward"] * 1e-3),
+        "jvp_samples_per_s": nominal / (ms["jvp"] * 1e-3),
+        "vjp_samples_per_s": nominal / (ms["vjp"] * 1e-3),
+        "lm_samples_per_s": nominal * (3 + 2 * cfg.n_cg) / (ms["lm"] * 1e-3),
+        "kernels": kern,
+        "reps": nrep,
+    }
+    if cfg.batch > 1:
+        img, sino = 4 * int(np.prod(g.img_shape)), 4 * int(np.prod(g.sino_shape))
+        byts = {"forward": 2 * img + sino, "jvp": 4 * img + sino, "vjp": 2 * img + sino + 2 * img}
+        tot = sum(byts.values())
+        t = (ms["forward"] + ms["jvp"] + ms["vjp"]) * 1e-3
+        out["hbm"] = {"alg_bytes_fwd_jvp_vjp": tot, "GBps": tot / t / 1e9,
+                      "basis": "inputs read + outputs written once per op (lam, mu, dlam, dmu, w; y, dy, g_lam, g_mu)"}
+    del g
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2)
-    ap.add_argument("--ref-angles", type=int, default=36)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--ref-angles", type=int, default=0, help="oracle sample angles (0: per-config default)")
+    ap.add_argument("--no-per-config", action="store_true", help="skip the configs 1-5 block")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the step directly instead of a CUDA graph")
@@ -391,7 +512,8 @@ def main():
     units = traced                                      # samples one launch actually evaluates
     achieved_gbs = ALG_BYTES[dom] * units / (per_launch_ms * 1e-3) / 1e9
     sm_mhz = (clk or {}).get("sm_mhz") or 1965.0
-    peak_gbs = SMEM_B_PER_CLK_SM * N_SM * sm_mhz * 1e6 / 1e9
+    bpc, peak_src = smem_peak()
+    peak_gbs = bpc * N_SM * sm_mhz * 1e6 / 1e9
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
@@ -403,10 +525,19 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import oracle as O
-        s = cpu_sample(cfg, args.ref_angles)
+        s = cpu_sample(cfg, args.ref_angles or REF_ANGLES[cfg.cid])
         dt, n = run_oracle_step(O, P, cfg, s)
         cpu = {"value": n / dt, "unit": "ray-samples/s", "cores": O.threads(), "kind": "oracle",
-               "sample": s["desc"]}
+               "sample": s["desc"], "cpu_model": cpu_model(), "omp_num_threads": os.environ.get("OMP_NUM_THREADS")}
+
+    per_config = None
+    if rank == 0 and world == 1 and not args.no_per_config:
+        del ws
+        torch.cuda.empty_cache()
+        per_config = {}
+        for cid in (1, 2, 3, 4, 5):
+            per_config[f"config {cid}"] = measure_config(pg, P, cid, flush, sm_mhz)
+            torch.cuda.empty_cache()
 
     if rank == 0:
         value = job_rate(samples_per_step, args.steps, world, total_ms)
@@ -434,7 +565,7 @@ def main():
                                     "vjp": "vjp: seg_a_kernel + seg_b_kernel (segmented adjoint, one launch pair)"}.get(dom, f"proj_kernel<{dom}>")),
                          "achieved": achieved_gbs, "peak": peak_gbs, "unit": "GB/s", "frac": achieved_gbs / peak_gbs,
                          "traffic": traffic,
-                         "peak_basis": f"128 B/clk/SM x 148 SMs x {sm_mhz:.0f} MHz (median SM clock under load)",
+                         "peak_basis": f"{peak_src} x 148 SMs x {sm_mhz:.0f} MHz (median SM clock under load)",
                          "alg_bytes_per_sample": ALG_BYTES[dom], "units_per_launch": units,
                          "launch_ms": per_launch_ms},
             "roofline_ncu": roofline_ncu(cfg.cid, dom),
@@ -446,8 +577,9 @@ def main():
                 "bound_ms": nominal * (2 * 32 + 21 * 96 + 20 * 64) / (peak_gbs * 1e9) * 1e3,
                 "measured_ms": phase["lm"] / K,
                 "frac": (nominal * (2 * 32 + 21 * 96 + 20 * 64) / (peak_gbs * 1e9) * 1e3) / (phase["lm"] / K),
-                "basis": "SURVEY.md 8(d): nominal samples x 3360 B at 128 B/clk/SM x 148 SMs x SM clock"},
+                "basis": f"SURVEY.md 8(d): nominal samples x 3360 B at {peak_src} x 148 SMs x SM clock"},
             "cpu_baseline": cpu,
+            "per_config": per_config,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk,

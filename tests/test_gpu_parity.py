@@ -458,3 +458,44 @@ def test_host_pointer_rejected(pg):
                                C.c_void_p(y.data_ptr()), C.c_void_p(ws.data_ptr()), ws.numel(), None)
     assert rc == 1          # PGET_ERR_INVALID_ARGUMENT
     assert b"device memory" in pg.lib().pget_last_error_message()
+
+
+# ----------------------------------------------------------------------------------- high optical depth (Q19)
+@pytest.mark.parametrize("scale", [20.0, 80.0, 130.0])
+def test_high_optical_depth(pg, scale):
+    """real fuel reaches optical depths >> 1 (mu ~ 0.12-0.14 /mm across
+    a 150 mm assembly); the configs' mu scaled by 20 / 80 / 130 gives a largest line optical depth S of
+    ~15 / ~60 / ~97 on the config-2 phantom.  The line-paired paths accumulate sum lam e^{+A} for the
+    opposite bank (DESIGN.md R-depth): forward, JVP, VJP and the GN operator (both GN paths) must keep
+    the north-star tolerances there; the JVP is graded on its own rod-wise directions."""
+    cid = 2
+    gd = P.geometry_desc(cid)
+    cfg = P.CONFIGS[cid]
+    lam, mu, dl, dm, lp, mp = inputs(cid)
+    mu = (mu * np.float32(scale)).astype(np.float32)
+    dm = (dm * np.float32(scale)).astype(np.float32)
+    g = pg.Geometry(gd)
+    y_o, dy_o = O.jvp(gd, lam, mu, dl, dm, with_y=True)
+    y = host(pg.forward(g, dev(lam), dev(mu)))
+    assert np.isfinite(y).all()
+    assert_parity(y, y_o, f"mu x{scale} forward")
+    _, dy = pg.jvp(g, dev(lam), dev(mu), dev(dl), dev(dm), want_y=True)
+    assert_parity(host(dy), dy_o, f"mu x{scale} jvp")
+    w = (O.forward(gd, lp, mu) - y_o).astype(np.float32)
+    gl, gm = pg.vjp(g, dev(lam), dev(mu), dev(w))
+    gl_o, gm_o = O.vjp(gd, lam, mu, w)
+    assert_parity(host(gl), gl_o, f"mu x{scale} vjp.lam")
+    assert_parity(host(gm), gm_o, f"mu x{scale} vjp.mu")
+    ql_o, qm_o = O.apply_H(gd, lam, mu, cfg.alpha, 0.25, dl, dm)
+    o = np.concatenate([ql_o.ravel(), qm_o.ravel()])
+    for cached in ("0", "1"):
+        import os
+        os.environ["PGET_GN_APPLY_CACHED"] = cached
+        try:
+            g2 = pg.Geometry(gd)
+            ql, qm = pg.gn_apply(g2, dev(lam), dev(mu), dev(dl), dev(dm), cfg.alpha, 0.25)
+        finally:
+            os.environ.pop("PGET_GN_APPLY_CACHED", None)
+        x = np.concatenate([host(ql).ravel(), host(qm).ravel()])
+        assert np.isfinite(x).all()
+        assert rel_l2(x, o) <= TOL_L2, (cached, rel_l2(x, o))
