@@ -94,7 +94,7 @@ ProjCfg proj_cfg(const Geometry& g, int mode)
     const int cps = proj_ctas_per_sm(mode);
     c.kind = sched_kind(mode);
     const Schedule& S = g.sch[c.kind];
-    c.paired = g.dup && mode != MODE_JVP;
+    c.paired = g.pair && mode != MODE_JVP;
     const bool hasB = mode == MODE_VJP || mode == MODE_GN;
     const bool nf4 = mode == MODE_JVP || mode == MODE_GN;
     // Warps per CTA and ray groups per warp.  Every warp of a band should carry the same number of
@@ -347,7 +347,7 @@ pget_status run_seg(const Geometry& g, int mode, ProjArgs A, float* segp, cudaSt
     A.stage_bytes = c.stageA;
     // have_a: segp already holds this u's VJP-mode phase-A partials (the segmented forward of the same
     // u wrote them), so only phase B runs
-    cudaError_t e = have_a ? cudaSuccess : launch_seg(0, mode, c.maxgA, g.dup, A, c.gridA, (c.WA + 1) * 32, c.smemA, s);
+    cudaError_t e = have_a ? cudaSuccess : launch_seg(0, mode, c.maxgA, g.pair, A, c.gridA, (c.WA + 1) * 32, c.smemA, s);
     if (e == cudaSuccess) {
         A.units = S.d_unitsB;
         A.u_begin = S.d_ub_begin;
@@ -361,7 +361,7 @@ pget_status run_seg(const Geometry& g, int mode, ProjArgs A, float* segp, cudaSt
         A.off_gsh = c.off_gsh;
         A.off_rsc = c.off_rsc;
         A.off_q1 = c.off_q1;
-        e = launch_seg(1, mode, 1, g.dup, A, c.gridB, c.WB * 32, c.smemB, s);
+        e = launch_seg(1, mode, 1, g.pair, A, c.gridB, c.WB * 32, c.smemB, s);
     }
     if (eb) cudaEventRecord(eb, s);
     if (e != cudaSuccess) return cuda_fail(e, "segmented projector launch");
@@ -586,6 +586,7 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     Geometry& g = h->g;
     if (g.desc.n_px > 2048) { delete h; return fail(PGET_ERR_INVALID_ARGUMENT, "n_px > 2048 not supported"); }
     g.device = device;
+    if (const char* ev = std::getenv("PGET_NO_PAIR")) g.pair = g.pair && std::atoi(ev) == 0;   // experiments
     if (device < 0) {   // host-only handle: tables, info and the host schedules; no device tables, no compute
         std::vector<RayP> rays;
         build_ray_params(g, &rays);
@@ -670,7 +671,7 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
         up(&g.d_tabsJ, g.task_ab);
     }
     if (g.adj_seg && e == cudaSuccess) {   // traced angle-banks of the adjoint schedule (segmented forward)
-        const std::vector<int32_t>& lst = g.dup ? g.task_ab_p : g.task_ab;
+        const std::vector<int32_t>& lst = g.pair ? g.task_ab_p : g.task_ab;
         e = cudaMalloc(&g.d_tabsA, std::max<size_t>(1, lst.size()) * sizeof(int32_t));
         if (e == cudaSuccess && !lst.empty())
             e = cudaMemcpy(g.d_tabsA, lst.data(), lst.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
@@ -723,7 +724,7 @@ pget_status pget_geometry_info(pget_geometry h, pget_geometry_info_t* o)
     const pget_geometry_desc& d = g.desc;
     o->n_rays = static_cast<int64_t>(d.batch) * g.n_ab * g.R;
     o->n_samples_nominal = g.n_samples_nominal;
-    o->n_samples_traced = g.dup ? g.n_samples_traced_p : g.n_samples_traced;
+    o->n_samples_traced = g.pair ? g.n_samples_traced_p : g.n_samples_traced;
     o->n_samples_traced_jvp = g.n_samples_traced;
     o->angle_banks_merged = g.dup ? 1 : 0;
     o->pad_ = 0;
@@ -894,7 +895,7 @@ static pget_status gnc_build(const Geometry& g, const WS& w, cudaStream_t s)
 {
     const SegCfg c = seg_cfg(g);
     if (w.gscale) CK(cudaMemsetAsync(w.gscale, 0, static_cast<size_t>(g.desc.batch) * g.sch[kSchedAdj].ntab * 8 * sizeof(float), s));
-    cudaError_t e = launch_gnc(0, g.dup, gnc_args(g, w), c.gridB, c.WB * 32, c.smemB, s);
+    cudaError_t e = launch_gnc(0, g.pair, gnc_args(g, w), c.gridB, c.WB * 32, c.smemB, s);
     note();
     if (e != cudaSuccess) return cuda_fail(e, "lin_kernel launch");
     return PGET_OK;
@@ -939,17 +940,17 @@ static pget_status gnc_product(const Geometry& g, const WS& w, const float* lam,
         Aa.RbA = c.RbA;
         Aa.passesA = c.passesA;
         Aa.stage_bytes = c.stageA;
-        e = launch_seg(0, MODE_GN, c.maxgA, g.dup, Aa, c.gridA, (c.WA + 1) * 32, c.smemA, s);
-        if (e == cudaSuccess) e = launch_gnw(g.dup, A, g.d_tabsA, S.ntab, g.desc.batch, s);
+        e = launch_seg(0, MODE_GN, c.maxgA, g.pair, Aa, c.gridA, (c.WA + 1) * 32, c.smemA, s);
+        if (e == cudaSuccess) e = launch_gnw(g.pair, A, g.d_tabsA, S.ntab, g.desc.batch, s);
     } else {
-        e = launch_gnc(1, g.dup, A, c.gridB, c.WB * 32, c.smemB, s);
+        e = launch_gnc(1, g.pair, A, c.gridB, c.WB * 32, c.smemB, s);
     }
     if (e == cudaSuccess) {
         ProjArgs Ag = A;
         Ag.RbB = c.RbG;
         Ag.off_wacc = c.off_waccG;
         Ag.off_rout = c.off_routG;
-        e = launch_gnc(2, g.dup, Ag, c.gridB, c.WB * 32, c.smemG, s);
+        e = launch_gnc(2, g.pair, Ag, c.gridB, c.WB * 32, c.smemG, s);
     }
     if (eb) cudaEventRecord(eb, s);
     if (e != cudaSuccess) return cuda_fail(e, "cached GN launch");
@@ -997,9 +998,9 @@ static pget_status fwd_out(const Geometry& g, const WS& w, float* y, cudaStream_
         }
     }
     if (ea) cudaEventRecord(ea, s);
-    cudaError_t e = launch_seg(0, MODE_VJP, c.maxgA, g.dup, A, c.gridA, (c.WA + 1) * 32, c.smemA, s);
-    const int ntab = static_cast<int>((g.dup ? g.task_ab_p : g.task_ab).size());
-    if (e == cudaSuccess) e = launch_fwd_combine(g.dup, A, g.d_tabsA, ntab, g.desc.batch, s);
+    cudaError_t e = launch_seg(0, MODE_VJP, c.maxgA, g.pair, A, c.gridA, (c.WA + 1) * 32, c.smemA, s);
+    const int ntab = static_cast<int>((g.pair ? g.task_ab_p : g.task_ab).size());
+    if (e == cudaSuccess) e = launch_fwd_combine(g.pair, A, g.d_tabsA, ntab, g.desc.batch, s);
     if (eb) cudaEventRecord(eb, s);
     if (e != cudaSuccess) return cuda_fail(e, "segmented forward launch");
     return PGET_OK;
@@ -1116,7 +1117,7 @@ pget_status pget_gn_apply(pget_geometry h, const float* lam, const float* mu, co
         A.RbA = c.RbA;
         A.passesA = c.passesA;
         A.stage_bytes = c.stageA;
-        CK(launch_seg(0, MODE_VJP, c.maxgA, g.dup, A, c.gridA, (c.WA + 1) * 32, c.smemA, s));
+        CK(launch_seg(0, MODE_VJP, c.maxgA, g.pair, A, c.gridA, (c.WA + 1) * 32, c.smemA, s));
         note();
         if ((st = gnc_build(g, w, s))) return st;
         if ((st = gnc_product(g, w, lam, mu, p_lam, p_mu, s))) return st;
@@ -1251,10 +1252,10 @@ static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const f
         Aa.RbA = c.RbA;
         Aa.passesA = c.passesA;
         Aa.stage_bytes = c.stageA;
-        CK(launch_seg(0, MODE_GN, c.maxgA, g.dup, Aa, c.gridA, (c.WA + 1) * 32, c.smemA, s));
+        CK(launch_seg(0, MODE_GN, c.maxgA, g.pair, Aa, c.gridA, (c.WA + 1) * 32, c.smemA, s));
         note();
         double* sq = reinterpret_cast<double*>(w.ysino);   // per (member, angle-bank); ysino is free here
-        CK(launch_jsq(g.dup, A, sq, c.gridB, c.WB * 32, c.smemB, s));
+        CK(launch_jsq(g.pair, A, sq, c.gridB, c.WB * 32, c.smemB, s));
         note();
         CK(launch_jsq_member(sq, S.ntab, B, kNblk, P[5], s));
         note();
@@ -1442,7 +1443,7 @@ pget_status pget_schedule_check(pget_geometry h)
     // fused kinds: every (member, traced angle-bank, detector) covered exactly once
     for (int k = 0; k < 2; ++k) {
         const Schedule& S = g.sch[k];
-        const bool paired = g.dup && k != kSchedJvp;
+        const bool paired = g.pair && k != kSchedJvp;
         const std::vector<int32_t>& list = paired ? g.task_ab_p : g.task_ab;
         std::map<std::pair<int, int>, std::vector<int>> cover;
         for (const TaskD& t : S.tasks) {
@@ -1460,7 +1461,7 @@ pget_status pget_schedule_check(pget_geometry h)
     if (!g.adj_seg) return PGET_OK;
     const Schedule& S = g.sch[kSchedAdj];
     const int K = S.K, ntab = S.ntab, ngB = S.max_gB;
-    const std::vector<int32_t>& list = g.dup ? g.task_ab_p : g.task_ab;
+    const std::vector<int32_t>& list = g.pair ? g.task_ab_p : g.task_ab;
     if (K < 1 || S.seg_rows.size() != static_cast<size_t>(K) + 1 || S.seg_rows.front() != 0 ||
         S.seg_rows.back() != g.P - 1)
         return bad("segment rows");

@@ -140,6 +140,7 @@ pget_status build_geometry(const pget_geometry_desc* d, Geometry* g, std::string
         g->orient[ab] = std::fabs(c) > std::fabs(s) ? 1 : 0;
     }
     g->dup = (nA % 2 == 0) && nB == 2 && d->bank1_shift == 0.0;
+    g->pair = g->dup;
     auto traced = [&](int ab) { return !g->dup || (ab / nB) < nA / 2; };
     for (int cls = 0; cls < 2; ++cls)
         for (int ab = 0; ab < g->n_ab; ++ab)

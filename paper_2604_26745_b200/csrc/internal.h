@@ -149,6 +149,9 @@ struct Geometry {
     // Line pairing (with dup): bank 1 of angle a traces the lines of bank 0 of angle a in the opposite
     // direction (phi + pi, mirrored offsets), so the forward, VJP and GN projectors trace only the
     // bank-0 angle-banks with a < n_A/2 and evaluate both directions per traversal.
+    // pair == false (PGET_NO_PAIR=1, or a model variant whose opposite-direction attenuation does not
+    // factor, N3) keeps the duplicate merging but traces both banks of every traced angle separately
+    bool pair = false;
     std::vector<int32_t> task_ab_p;   // bank-0 traced angle-banks (class 0, then class 1); empty without dup
     int n_class0_p = 0;
     int64_t n_samples_traced_p = 0;

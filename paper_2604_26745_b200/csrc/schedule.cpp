@@ -50,7 +50,7 @@ static void comb_groups(int r_lo, int r_hi, int S, std::vector<int32_t>* out)
 void build_schedule(const Geometry& g, int kind, int C, Schedule* S)
 {
     const bool adjoint = kind == kSchedAdj;
-    const bool paired = g.dup && kind != kSchedJvp;
+    const bool paired = g.pair && kind != kSchedJvp;
     const std::vector<int32_t>& list = paired ? g.task_ab_p : g.task_ab;
     const int B = g.desc.batch, nd = g.desc.n_det, J = g.desc.n_subrays;
     const int ntab = static_cast<int>(list.size());
@@ -201,7 +201,7 @@ void build_schedule(const Geometry& g, int kind, int C, Schedule* S)
 // order so that consecutive units of one (member, class) share a partial slot (<= kSlotTasks).
 void build_adj_schedule(const Geometry& g, const std::vector<RayP>& rays, int CA, int C, Schedule* S, bool unpaired)
 {
-    const bool paired = g.dup && !unpaired;   // unpaired: the standalone JVP (every traced angle-bank)
+    const bool paired = g.pair && !unpaired;   // unpaired: the standalone JVP (every traced angle-bank)
     const std::vector<int32_t>& list = paired ? g.task_ab_p : g.task_ab;
     const int B = g.desc.batch, R = g.R;
     const int ntab = static_cast<int>(list.size());

@@ -81,17 +81,24 @@ def full(rep):
 
 
 def main():
+    # usage: ncu_summary.py TAG LAUNCH_LIST.csv [FULL.ncu-rep|-] [CONFIG_ID]
     tag = sys.argv[1]
-    lst, rep = sys.argv[2], sys.argv[3]
+    lst, rep = sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else "-"
+    cid = int(sys.argv[4]) if len(sys.argv) > 4 else 2
     lines = [f"# ncu summary, round {tag}", "",
              "Launch list: `ncu --metrics gpu__time_duration.sum --clock-control none` of "
-             "`python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e` (config 2; cold-cache, "
-             "serialised launches: compare shares, not absolute times).", ""]
+             f"`python bench.py --config {cid} --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-per-config` "
+             f"(config {cid}; cold-cache, serialised launches: compare shares, not absolute times).", ""]
     tab, n, T = launches(lst)
     lines += [f"{n} launches, {T / 1e3:.2f} ms total.", ""] + tab + [""]
+    if rep == "-":
+        out = os.path.join(ROOT, "profiles", f"ncu_summary_{tag}.md")
+        open(out, "w").write("\n".join(lines) + "\n")
+        print(out)
+        return
     lines += ["Full capture: `ncu --set full --clock-control none --import-source on -k regex:\"proj_kernel|seg_|lin_kernel|gnb_kernel\" -c 8 "
-              "python scripts/prof_ops.py 2 1` (one launch of each projector kernel, config 2: forward and JVP "
-              "fused, VJP as segmented phases A and B, GN as the VJP-mode phase A + cache build (lin) + GN-mode phase A + cached scatter (gnb)).", ""]
+              f"python scripts/prof_ops.py {cid} 1` (one launch of each projector kernel, config {cid}: forward "
+              "fused, JVP segmented, VJP as segmented phases A and B, GN as the VJP-mode phase A + cache build (lin) + GN-mode phase A + cached scatter (gnb)).", ""]
     res = full(rep)
     labs = [lab for _, lab in KEYS]
     lines.append("| metric | " + " | ".join(m for m, _, _ in res) + " |")
@@ -125,11 +132,15 @@ def main():
                      "sm_sol_pct": num("SM SOL %"), "issue_active_pct": num("issue active %"),
                      "l1_smem_pct": num("L1/smem throughput %"), "fma_pipe_pct": num("FMA pipe %"),
                      "xu_pipe_pct": num("XU (MUFU) %")}
-    json.dump({"cfg2": sol, "source": f"profiles/ncu_summary_{tag}.md"},
-              open(os.path.join(ROOT, "profiles", "ncu_sol.json"), "w"), indent=1)
+    sp = os.path.join(ROOT, "profiles", "ncu_sol.json")
+    olds = json.load(open(sp)) if os.path.exists(sp) else {}
+    olds[f"cfg{cid}"] = sol
+    olds.setdefault("sources", {})[f"cfg{cid}"] = f"profiles/ncu_summary_{tag}.md"
+    olds["source"] = f"profiles/ncu_summary_{tag}.md"
+    json.dump(olds, open(sp, "w"), indent=1)
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     old = json.load(open(tp)) if os.path.exists(tp) else {}
-    old["cfg2"] = traffic
+    old[f"cfg{cid}"] = traffic
     old["source"] = f"profiles/ncu_summary_{tag}.md (ncu --set full, dram__bytes_read.sum + dram__bytes_write.sum per launch)"
     json.dump(old, open(tp, "w"), indent=1)
     print(out)
