@@ -36,7 +36,8 @@ def build(force: bool = False) -> str:
 class _Desc(C.Structure):
     _fields_ = [("n_px", C.c_int), ("n_angles", C.c_int), ("n_banks", C.c_int),
                 ("n_det", C.c_int), ("n_subrays", C.c_int), ("subray_sigma", C.c_double),
-                ("step_px", C.c_double), ("bank1_shift", C.c_double), ("batch", C.c_int)]
+                ("step_px", C.c_double), ("bank1_shift", C.c_double), ("batch", C.c_int),
+                ("det_radius", C.c_double), ("c_slope", C.c_double), ("r_slope", C.c_double)]
 
 
 def _load():
@@ -47,7 +48,7 @@ def _load():
         P = C.c_void_p
         for name, args in [
             ("orc_tables", [P] * 8), ("orc_forward", [P] * 4), ("orc_forward_naive", [P] * 4),
-            ("orc_jvp", [P] * 7), ("orc_vjp", [P] * 6), ("orc_n_t", [P]),
+            ("orc_jvp", [P] * 7), ("orc_vjp", [P] * 6), ("orc_n_t", [P]), ("orc_variant_tables", [P] * 3),
             ("orc_gn_cg_step", [P, P, P, P, C.c_double, C.c_double, C.c_int, P, P, P]),
             ("orc_apply_H", [P, P, P, C.c_double, C.c_double, P, P]),
             ("orc_lm_step_box", [P, P, P, P, C.c_double, C.c_double, C.c_int, P, C.c_int, P, P, P]),
@@ -103,7 +104,8 @@ class _Prior:
 def _desc(g: dict) -> _Desc:
     return _Desc(int(g["n_px"]), int(g["n_angles"]), int(g.get("n_banks", 2)), int(g.get("n_det", 91)),
                  int(g.get("n_subrays", 1)), float(g.get("subray_sigma", 0.4)),
-                 float(g.get("step_px", 0.5)), float(g.get("bank1_shift", 0.0)), int(g.get("batch", 1)))
+                 float(g.get("step_px", 0.5)), float(g.get("bank1_shift", 0.0)), int(g.get("batch", 1)),
+                 float(g.get("det_radius", 0.0)), float(g.get("c_slope", 0.0)), float(g.get("r_slope", 0.0)))
 
 
 def _f64(a):
@@ -112,6 +114,18 @@ def _f64(a):
 
 def _p(a):
     return a.ctypes.data_as(C.c_void_p)
+
+
+def variant_tables(g: dict) -> dict:
+    """O13 tables of the model variant (N3): c_i [n_t] and W_j(d_i) [J][n_t]."""
+    lib = _load()
+    d = _desc(g)
+    n_t = lib.orc_n_t(C.byref(d))
+    Cv = np.zeros(n_t)
+    W = np.zeros((int(g.get("n_subrays", 1)), n_t))
+    rc = lib.orc_variant_tables(C.byref(d), _p(Cv), _p(W))
+    assert rc == 0, rc
+    return {"c": Cv, "w": W}
 
 
 def threads() -> int:

@@ -29,6 +29,12 @@
  *       function below that evaluates f, its gradient, H or m_k (not thread-safe: test use only)
  *   safeguard u_{k+1} = u~ iff m_k(s~) <= m_k(s_k) and rho_k(s~) > kappa
  *       -- PAPER.md:241-258 Prop. 1 eq:uk+1_condition; Algorithm 2 PAPER.md:290-313 (O8, N2)
+ *   model variant (O13, N3): the collimator response r_{m,n} and the vertical opening-angle correction
+ *       c_{m,n} >= 1 of eq:d_fwd_model, as functions of the emission point's
+ *       distance to the detector d = det_radius - t (reading R-N3):
+ *         y = sum_j sum_i W_j(d_i) Delta lam_i exp(-c_i A_i),  c_i = 1 + c_slope d_i,
+ *         W_j(d) = exp(-delta_j^2 / (2 sigma(d)^2)) / sum_k exp(-delta_k^2 / (2 sigma(d)^2)),
+ *         sigma(d) = subray_sigma * pitch * (1 + r_slope d);   on iff det_radius > 0
  *
  * Parity pins: tests/test_oracle.py (P1-P12 of SURVEY.md §8(c.4)); DESIGN.md "Oracle".
  * Compile: gcc -O2 -fopenmp -ffp-contract=off -fPIC -shared (no fast-math).
@@ -44,6 +50,7 @@ typedef struct {
     int n_px, n_angles, n_banks, n_det, n_subrays;
     double subray_sigma, step_px, bank1_shift;
     int batch;
+    double det_radius, c_slope, r_slope;   /* O13 model variant (N3); det_radius <= 0: off */
 } orc_desc;
 
 /* ------------------------------------------------------------------ O1 geometry */
@@ -204,24 +211,80 @@ static void o2_scatter(double* img, int N, double u, double v, double val)
 typedef struct {
     orc_lattice L;
     double w[64];
+    int var;          /* O13 variant on */
+    double* C;        /* [n_t]    c_i                   */
+    double* W;        /* [J][n_t] W_j(d_i)              */
 } orc_ctx;
+
+/* O13 tables (variant): distance of lattice sample i to the detector d_i = det_radius - t_i,
+ * c_i = 1 + c_slope d_i, W_j(d_i) the normalised Gaussian sub-ray response of width
+ * sigma(d_i) = subray_sigma * pitch * (1 + r_slope d_i) */
+static void o13_tables(const orc_desc* g, const orc_lattice* L, double* C, double* W)
+{
+    int J = g->n_subrays;
+    double p = 2.0 / (g->n_det - 1);
+    for (int i = 0; i < L->n_t; ++i) {
+        double t = -L->T + (i + 0.5) * L->delta;
+        double d = g->det_radius - t;
+        C[i] = 1.0 + g->c_slope * d;
+        double sp = g->subray_sigma * p * (1.0 + g->r_slope * d);
+        double sum = 0.0;
+        for (int j = 0; j < J; ++j) {
+            double dj = (double)(2 * j + 1 - J) / (double)(2 * J) * p;
+            W[(size_t)j * L->n_t + i] = exp(-(dj * dj) / (2.0 * sp * sp));
+            sum += W[(size_t)j * L->n_t + i];
+        }
+        for (int j = 0; j < J; ++j) W[(size_t)j * L->n_t + i] = W[(size_t)j * L->n_t + i] / sum;
+    }
+}
+
+static void ctx_free(orc_ctx* cx)
+{
+    free(cx->C);
+    free(cx->W);
+    cx->C = cx->W = NULL;
+}
 
 static int ctx_init(const orc_desc* g, orc_ctx* cx)
 {
+    cx->C = cx->W = NULL;
+    cx->var = 0;
     if (g->n_subrays > 64 || g->n_subrays < 1 || g->n_det < 2 || g->n_px < 2 || g->n_angles < 1 ||
         g->n_banks < 1 || g->n_banks > 2 || g->step_px <= 0.0)
         return -1;
     cx->L = o1_lattice(g);
     o1_weights(g, cx->w);
+    if (g->det_radius > 0.0) {
+        if (g->det_radius < cx->L.T || g->c_slope < 0.0 || g->r_slope < 0.0) return -1;
+        cx->var = 1;
+        cx->C = (double*)malloc(sizeof(double) * cx->L.n_t);
+        cx->W = (double*)malloc(sizeof(double) * cx->L.n_t * g->n_subrays);
+        if (!cx->C || !cx->W) { ctx_free(cx); return -2; }
+        o13_tables(g, &cx->L, cx->C, cx->W);
+    }
+    return 0;
+}
+
+/* Export the O13 tables (pin P18 and the bit-exact comparison with the library). */
+int orc_variant_tables(const orc_desc* g, double* C, double* W)
+{
+    orc_ctx cx;
+    if (ctx_init(g, &cx)) return -1;
+    if (!cx.var) { ctx_free(&cx); return -3; }
+    memcpy(C, cx.C, sizeof(double) * cx.L.n_t);
+    memcpy(W, cx.W, sizeof(double) * cx.L.n_t * g->n_subrays);
+    ctx_free(&cx);
     return 0;
 }
 
 /* O3/O4 for one ray.  Returns g_ray; *dg_ray (if dlam) gets the JVP.
  * A_i = Delta*(1/2 mu_i + sum_{k>i} mu_k);  g = Delta * sum_i lam_i exp(-A_i)
  * dA_i = Delta*(1/2 dmu_i + sum_{k>i} dmu_k); dg = Delta * sum_i (dlam_i - lam_i dA_i) exp(-A_i) */
+/* O13 (Cv, Wv non-NULL): g = Delta sum_i W_i lam_i exp(-c_i A_i),
+ * dg = Delta sum_i W_i (dlam_i - lam_i c_i dA_i) exp(-c_i A_i)   (eq:d_fwd_model with r, c; eq:frechet) */
 static double ray_fwd(const orc_lattice* L, int N, const double* lam, const double* mu,
                       const double* dlam, const double* dmu, double c, double s, double sigma,
-                      int ilo, int ihi, double* dg_ray)
+                      int ilo, int ihi, double* dg_ray, const double* Cv, const double* Wv)
 {
     double g = 0.0, dg = 0.0;
     double sum_mu = 0.0, sum_dmu = 0.0;      /* sum_{k>i} over samples nearer the detector */
@@ -230,12 +293,14 @@ static double ray_fwd(const orc_lattice* L, int N, const double* lam, const doub
         o2_pos(L, c, s, sigma, i, &u, &v);
         double li = o2_sample(lam, N, u, v), mi = o2_sample(mu, N, u, v);
         double A = L->delta * (0.5 * mi + sum_mu);
-        double E = exp(-A);
-        g += li * E;
+        double ci = Cv ? Cv[i] : 1.0, wi = Wv ? Wv[i] : 1.0;
+        double E = Cv ? exp(-ci * A) : exp(-A);
+        g += Wv ? wi * li * E : li * E;
         if (dlam) {
             double dli = o2_sample(dlam, N, u, v), dmi = o2_sample(dmu, N, u, v);
             double dA = L->delta * (0.5 * dmi + sum_dmu);
-            dg += (dli - li * dA) * E;
+            if (Cv) dg += wi * (dli - li * ci * dA) * E;
+            else dg += (dli - li * dA) * E;
             sum_dmu += dmi;
         }
         sum_mu += mi;
@@ -266,9 +331,11 @@ static double ray_fwd_naive(const orc_lattice* L, int N, const double* lam, cons
 
 /* O5 for one ray with adjoint weight wr:
  * a_lam(i) = wr*Delta*E_i; a_mu(i) = -wr*Delta^2*(sum_{k<i} lam_k E_k + 1/2 lam_i E_i) */
+/* O13 (Cv, Wv non-NULL): a_lam(i) = wr Delta W_i E_i, a_mu(i) = -wr Delta^2 (sum_{k<i} W_k lam_k c_k E_k
+ * + 1/2 W_i lam_i c_i E_i) with E_i = exp(-c_i A_i) (the transpose of the O13 JVP) */
 static void ray_vjp(const orc_lattice* L, int N, const double* lam, const double* mu, double wr,
                     double c, double s, double sigma, int ilo, int ihi, double* glam, double* gmu,
-                    double* buf)
+                    double* buf, const double* Cv, const double* Wv)
 {
     int n = ihi - ilo + 1;
     if (n <= 0) return;
@@ -280,15 +347,16 @@ static void ray_vjp(const orc_lattice* L, int N, const double* lam, const double
         o2_pos(L, c, s, sigma, i, &u, &v);
         double mi = o2_sample(mu, N, u, v);
         ls[i - ilo] = o2_sample(lam, N, u, v);
-        E[i - ilo] = exp(-L->delta * (0.5 * mi + sum_mu));
+        if (Cv) E[i - ilo] = exp(-Cv[i] * (L->delta * (0.5 * mi + sum_mu)));
+        else E[i - ilo] = exp(-L->delta * (0.5 * mi + sum_mu));
         sum_mu += mi;
     }
     double prefix = 0.0;       /* sum_{k<i} lam_k E_k (samples farther from the detector) */
     for (int i = ilo; i <= ihi; ++i) {
         double u, v;
         o2_pos(L, c, s, sigma, i, &u, &v);
-        double le = ls[i - ilo] * E[i - ilo];
-        double al = wr * L->delta * E[i - ilo];
+        double le = Cv ? Wv[i] * ls[i - ilo] * Cv[i] * E[i - ilo] : ls[i - ilo] * E[i - ilo];
+        double al = Cv ? wr * L->delta * Wv[i] * E[i - ilo] : wr * L->delta * E[i - ilo];
         double am = -wr * L->delta * L->delta * (prefix + 0.5 * le);
         o2_scatter(glam, N, u, v, al);
         o2_scatter(gmu, N, u, v, am);
@@ -315,6 +383,7 @@ static int fwd_impl(const orc_desc* g, const double* lam, const double* mu, cons
 {
     orc_ctx cx;
     if (ctx_init(g, &cx)) return -1;
+    if (naive && cx.var) { ctx_free(&cx); return -1; }
     int N = g->n_px, nA = g->n_angles, nB = g->n_banks, nd = g->n_det, J = g->n_subrays;
     long n_ab = (long)g->batch * nA * nB;
     size_t npx = (size_t)N * N;
@@ -338,14 +407,21 @@ static int fwd_impl(const orc_desc* g, const double* lam, const double* mu, cons
                 if (naive)
                     gj = ray_fwd_naive(&cx.L, N, l, u, c, s, sigma, ilo, ihi);
                 else
-                    gj = ray_fwd(&cx.L, N, l, u, dl, du, c, s, sigma, ilo, ihi, dl ? &dgj : NULL);
-                acc += cx.w[j] * gj;                 /* y = sum_j w_j g_ray */
-                dacc += cx.w[j] * dgj;
+                    gj = ray_fwd(&cx.L, N, l, u, dl, du, c, s, sigma, ilo, ihi, dl ? &dgj : NULL,
+                                 cx.var ? cx.C : NULL, cx.var ? cx.W + (size_t)j * cx.L.n_t : NULL);
+                if (cx.var) {                        /* O13: the response is inside the ray sum */
+                    acc += gj;
+                    dacc += dgj;
+                } else {
+                    acc += cx.w[j] * gj;             /* y = sum_j w_j g_ray */
+                    dacc += cx.w[j] * dgj;
+                }
             }
             if (y) y[q * nd + d] = acc;
             if (dy) dy[q * nd + d] = dacc;
         }
     }
+    ctx_free(&cx);
     return 0;
 }
 
@@ -378,7 +454,7 @@ int orc_vjp(const orc_desc* g, const double* lam, const double* mu, const double
     memset(gmu, 0, sizeof(double) * npx * g->batch);
     for (int m = 0; m < g->batch; ++m) {
         double* priv = (double*)calloc((size_t)nth * 2 * npx, sizeof(double));
-        if (!priv) return -2;
+        if (!priv) { ctx_free(&cx); return -2; }
         const double* l = lam + m * npx;
         const double* u = mu + m * npx;
 #pragma omp parallel
@@ -401,7 +477,11 @@ int orc_vjp(const orc_desc* g, const double* lam, const double* mu, const double
                         double sigma = o1_offset(g, b, d, j);
                         int ilo, ihi;
                         o1_clip(g, &cx.L, c, s, sigma, &ilo, &ihi);
-                        ray_vjp(&cx.L, N, l, u, cx.w[j] * wd, c, s, sigma, ilo, ihi, gl, gm, buf);
+                        if (cx.var)   /* O13: the response W_j(d_i) is inside the ray sum */
+                            ray_vjp(&cx.L, N, l, u, wd, c, s, sigma, ilo, ihi, gl, gm, buf, cx.C,
+                                    cx.W + (size_t)j * cx.L.n_t);
+                        else
+                            ray_vjp(&cx.L, N, l, u, cx.w[j] * wd, c, s, sigma, ilo, ihi, gl, gm, buf, NULL, NULL);
                     }
                 }
             }
@@ -414,6 +494,7 @@ int orc_vjp(const orc_desc* g, const double* lam, const double* mu, const double
             }
         free(priv);
     }
+    ctx_free(&cx);
     return 0;
 }
 

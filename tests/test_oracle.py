@@ -882,3 +882,177 @@ def test_p17_lm_solve_respects_the_constraint():
                                     inner=inner)
         np.testing.assert_array_equal(la, lb)
         assert [s["f"] for s in sa] == [s["f"] for s in sb]
+
+
+# ----------------------------------------------------------------------------- P18 model variant (O13, N3)
+# the collimator response r and the vertical correction c of eq:d_fwd_model as
+# functions of the emission point's distance to the detector (reading R-N3)
+VAR = dict(det_radius=1.6, c_slope=0.05, r_slope=0.35)
+
+
+def test_p18_tables():
+    """c_i = 1 + c_slope d_i >= 1 grows with the distance d_i = det_radius - t_i to the detector (PAPER.md:141:
+    'c >= 1 ... far-away emissions'); the response W_j(d) sums to 1 over the sub-rays at every distance
+    (a probability split over the detector's sub-rays), is symmetric in j, and widens with d."""
+    g = small(n_px=32, J=5, **VAR)
+    t = O.tables(g)
+    h, delta, T = t["tlat"]
+    v = O.variant_tables(g)
+    n_t = v["c"].size
+    ti = -T + (np.arange(n_t) + 0.5) * delta
+    d = VAR["det_radius"] - ti
+    assert np.all(d > 0)
+    np.testing.assert_allclose(v["c"], 1 + VAR["c_slope"] * d, rtol=1e-15)
+    assert np.all(np.diff(v["c"]) < 0) and v["c"].min() >= 1.0
+    W = v["w"]
+    assert np.abs(W.sum(0) - 1).max() <= 4e-16
+    assert np.array_equal(W, W[::-1])
+    assert np.all(np.diff(W[2]) > 0)            # the centre sub-ray's share shrinks with distance (i up = nearer)
+    # the centre share at distance 0 is the base model's weight at sigma0
+    g0 = small(n_px=32, J=5, det_radius=1.6, c_slope=0.0, r_slope=0.0)
+    np.testing.assert_allclose(O.variant_tables(g0)["w"][:, 0], t["weights"], rtol=1e-15)
+
+
+def test_p18_reduces_to_base_model():
+    """Slopes 0: the variant's code path reproduces the base model (the response moves inside the ray
+    sum: 1e-13 rel); mu = 0: c drops out exactly (exp(-c 0) = 1), whatever its slope."""
+    g = small(n_px=20, J=3)
+    lam, mu = rand_img(g, 1, 0, 1.5), rand_img(g, 2, 0, 0.6)
+    dl, dm = rand_img(g, 3, -1, 1), rand_img(g, 4, -0.1, 0.1)
+    g0 = dict(g, det_radius=1.6, c_slope=0.0, r_slope=0.0)
+    y, dy = O.jvp(g, lam, mu, dl, dm, with_y=True)
+    y0, dy0 = O.jvp(g0, lam, mu, dl, dm, with_y=True)
+    assert rel_l2(y0, y) <= 1e-13 and rel_l2(dy0, dy) <= 1e-13
+    w = np.random.default_rng(5).standard_normal(O.sino_shape(g))
+    gl, gm = O.vjp(g, lam, mu, w)
+    gl0, gm0 = O.vjp(g0, lam, mu, w)
+    assert rel_l2(gl0, gl) <= 1e-13 and rel_l2(gm0, gm) <= 1e-13
+    z = np.zeros_like(mu)
+    ya = O.forward(dict(g, det_radius=1.6, c_slope=0.0, r_slope=0.3), lam, z)
+    yb = O.forward(dict(g, det_radius=1.6, c_slope=0.4, r_slope=0.3), lam, z)
+    assert np.array_equal(ya, yb)
+
+
+def test_p18_c_attenuated_disk_closed_form():
+    """c alone (J = 1, so W = 1): uniform disk lam0 = 1, mu0 = 0.5, R = 0.5, chord [-l, l] along the ray,
+    g(s) = int_{-l}^{l} exp(-c(t) mu0 (l - t)) dt with c(t) = 1 + c_slope (det_radius - t): the correction
+    multiplies the whole path from the emission point to the detector (eq:d_fwd_model).  Quadrature by
+    scipy; first-order convergence in h as P4."""
+    from scipy.integrate import quad
+    D, kc, mu0, R = 1.6, 0.2, 0.5, 0.5
+    means = []
+    for N in (128, 256):
+        g = dict(_disk_geom(N), det_radius=D, c_slope=kc, r_slope=0.0)
+        lam, mu = P.disk_phantom(N, R, 1.0, mu0)
+        y = O.forward(g, lam, mu)[0]
+        s = O.tables(g)["offsets"][0, :, 0]
+        sel = np.abs(s) <= 0.9 * R
+        ref = []
+        for sv in s[sel]:
+            l = math.sqrt(R * R - sv * sv)
+            ref.append(quad(lambda t: math.exp(-(1 + kc * (D - t)) * mu0 * (l - t)), -l, l, epsabs=1e-13)[0])
+        ref = np.array(ref)
+        err = np.abs(y[:, 0, sel] - ref) / ref
+        assert err.max() <= 1.5e-2
+        means.append(err.mean())
+        # the wrong reading c(t) = 1 + c_slope (det_radius + t) (distance from the far side) is far off
+        wrong = np.array([quad(lambda t: math.exp(-(1 + kc * (D + t)) * mu0 * (l - t)), -l, l)[0]
+                          for l in np.sqrt(R * R - s[sel] ** 2)])
+        assert (np.abs(y[:, 0, sel] - wrong) / wrong).mean() > 5 * err.mean()
+    assert means[0] / means[1] >= 1.5
+
+
+def test_p18_r_uniform_disk_closed_form():
+    """r alone (mu = 0, J = 5): a uniform emitting disk gives y_d = sum_j int_{chord_j} W_j(det_radius - t) dt
+    with the sub-ray offsets of O1 (scipy quadrature over each sub-ray's chord; first-order convergence)."""
+    from scipy.integrate import quad
+    D, kr, R, J = 1.6, 0.6, 0.5, 5
+    p = 2.0 / 90
+    s0 = 0.4 * p
+    dj = np.array([(2 * j + 1 - J) / (2 * J) * p for j in range(J)])
+
+    def Wj(j, d):
+        q = np.exp(-dj ** 2 / (2 * (s0 * (1 + kr * d)) ** 2))
+        return q[j] / q.sum()
+    means = []
+    for N in (128, 256):
+        g = dict(_disk_geom(N), n_subrays=J, det_radius=D, c_slope=0.0, r_slope=kr)
+        lam, mu = P.disk_phantom(N, R, 1.0, 0.0)
+        y = O.forward(g, lam, mu)[0]
+        s = O.tables(g)["offsets"][0, :, J // 2]
+        sel = np.abs(s) <= 0.85 * R
+        ref = []
+        for sv in s[sel]:
+            tot = 0.0
+            for j in range(J):
+                l = math.sqrt(max(R * R - (sv + dj[j]) ** 2, 0.0))
+                tot += quad(lambda t: Wj(j, D - t), -l, l, epsabs=1e-14)[0]
+            ref.append(tot)
+        ref = np.array(ref)
+        err = np.abs(y[:, 0, sel] - ref) / ref
+        assert err.max() <= 1.5e-2
+        means.append(err.mean())
+    assert means[0] / means[1] >= 1.5
+
+
+def test_p18_r_invariant_for_fields_constant_across_rays():
+    """theta = 0 rays run along x; an emission field that depends on x only is seen identically by every
+    sub-ray of a detector, so sum_j W_j(d) = 1 makes the detector reading independent of r_slope
+    (catches a response that is not normalised per distance, or applied per ray instead of per sample)."""
+    N = 32
+    g = dict(n_px=N, n_angles=4, n_banks=2, n_det=9, n_subrays=5, subray_sigma=0.4, step_px=0.5,
+             bank1_shift=0.0, batch=1, det_radius=1.6, c_slope=0.0)
+    x = np.random.default_rng(3).uniform(0.2, 1.5, N)
+    lam = np.tile(x, (N, 1))[None]              # lam[j][i] = x[i]: constant along y
+    mu = np.zeros_like(lam)
+    ya = O.forward(dict(g, r_slope=0.0), lam, mu)[0]
+    yb = O.forward(dict(g, r_slope=0.8), lam, mu)[0]
+    inner = slice(1, 8)                         # detectors whose sub-rays all lie inside the grid
+    assert np.abs(ya[0, 0, inner] - yb[0, 0, inner]).max() <= 1e-13 * np.abs(ya).max()
+    assert np.abs(ya[1, 0] - yb[1, 0]).max() > 1e-4 * np.abs(ya).max()   # at 90 deg the field varies across rays
+
+
+def test_p18_c_lowers_every_reading():
+    """mu > 0 everywhere: a larger vertical correction lengthens every path, so every reading falls."""
+    g = small(n_px=20, J=3)
+    lam, mu = rand_img(g, 1, 0.2, 1.5), rand_img(g, 2, 0.1, 0.6)
+    ya = O.forward(dict(g, det_radius=1.6, c_slope=0.02, r_slope=0.2), lam, mu)
+    yb = O.forward(dict(g, det_radius=1.6, c_slope=0.08, r_slope=0.2), lam, mu)
+    assert np.all(yb < ya)
+
+
+def test_p18_jvp_central_differences():
+    g = small(n_px=24, n_angles=10, J=3, n_det=11, **VAR)
+    lam, mu = rand_img(g, 10, 0, 1.5), rand_img(g, 11, 0, 0.6)
+    un = math.sqrt(np.sum(lam ** 2) + np.sum(mu ** 2))
+    for k in range(20):
+        rng = np.random.default_rng(200 + k)
+        dl = rng.uniform(-1, 1, lam.shape)
+        dm = rng.uniform(-0.1, 0.1, mu.shape)
+        eps = 1e-6 * un / math.sqrt(np.sum(dl ** 2) + np.sum(dm ** 2))
+        fd = (O.forward(g, lam + eps * dl, mu + eps * dm) - O.forward(g, lam - eps * dl, mu - eps * dm)) / (2 * eps)
+        assert rel_l2(O.jvp(g, lam, mu, dl, dm), fd) <= 1e-7
+
+
+def test_p18_adjoint_identity_and_dense_transpose():
+    g = small(n_px=12, n_angles=6, J=2, n_det=9, **VAR)
+    for k in range(100):
+        rng = np.random.default_rng(3000 + k)
+        lam = rng.uniform(0, 1.5, O.img_shape(g))
+        mu = rng.uniform(0, 0.6, O.img_shape(g))
+        vl, vm = rng.standard_normal(O.img_shape(g)), rng.standard_normal(O.img_shape(g))
+        w = rng.standard_normal(O.sino_shape(g))
+        jv = O.jvp(g, lam, mu, vl, vm)
+        gl, gm = O.vjp(g, lam, mu, w)
+        assert abs(np.sum(jv * w) - np.sum(vl * gl) - np.sum(vm * gm)) <= 1e-10 * np.linalg.norm(jv) * np.linalg.norm(w)
+    g = dict(n_px=8, n_angles=4, n_banks=2, n_det=5, n_subrays=3, subray_sigma=0.4, step_px=0.5,
+             bank1_shift=0.0, batch=1, **dict(VAR, det_radius=2.0))   # det_radius >= T = 1.75 at N = 8
+    rng = np.random.default_rng(6)
+    lam, mu = rng.uniform(0.2, 1.5, (1, 8, 8)), rng.uniform(0.1, 0.6, (1, 8, 8))
+    npx = 64
+    Jd = np.stack([O.jvp(g, lam, mu, e[:npx].reshape(1, 8, 8), e[npx:].reshape(1, 8, 8)).ravel()
+                   for e in np.eye(2 * npx)], axis=1)
+    ns = Jd.shape[0]
+    JT = np.stack([np.concatenate([x.ravel() for x in O.vjp(g, lam, mu, e.reshape(O.sino_shape(g)))])
+                   for e in np.eye(ns)], axis=0)
+    assert np.abs(JT - Jd).max() <= 1e-12 * np.abs(Jd).max()
