@@ -81,6 +81,18 @@ typedef struct {
     double step_px;       /* > 0: sample step Delta in pixels (0.5)                        */
     double bank1_shift;   /* bank-1 offset shift in pitches (0 for the configs)            */
     int32_t batch;        /* >= 1 independent image pairs per call                         */
+    /* Model variant (eq:d_fwd_model; reading R-N3): the
+     * collimator response r_{m,n} and the vertical opening-angle correction c_{m,n} >= 1 as functions of
+     * the emission point's distance to the detector, d_i = det_radius - t_i:
+     *     y = sum_j sum_i W_j(d_i) Delta lam_i exp(-c_i A_i),   c_i = 1 + c_slope d_i,
+     *     W_j(d) = exp(-delta_j^2/(2 sigma(d)^2)) / sum_k exp(-delta_k^2/(2 sigma(d)^2)),
+     *     sigma(d) = subray_sigma * pitch * (1 + r_slope d).
+     * det_radius <= 0: off (the base model above).  On: det_radius >= T, slopes >= 0 and finite.  The
+     * variant runs unpaired, unsegmented and without the GN coefficient cache (its attenuation does not
+     * factor along a ray), so it is several times slower than the base model. */
+    double det_radius;    /* distance from the rotation centre to the detector face (domain units) */
+    double c_slope;       /* c_i = 1 + c_slope d_i                                          */
+    double r_slope;       /* sigma(d) = sigma_0 (1 + r_slope d)                              */
 } pget_geometry_desc;
 
 typedef struct {
@@ -111,7 +123,9 @@ enum {
     PGET_TABLE_OFFSETS = 2, /* double [n_banks][n_det][n_subrays]        sigma_{b,d,j}        */
     PGET_TABLE_WEIGHTS = 3, /* double [n_subrays]                        w_j                  */
     PGET_TABLE_TLAT = 4,    /* double [3]                                (h, Delta, T)        */
-    PGET_TABLE_CLIP = 5     /* int32  [n_angles][n_banks][n_det][n_subrays][2]  (i_lo, i_hi); empty ray = (0,-1) */
+    PGET_TABLE_CLIP = 5,    /* int32  [n_angles][n_banks][n_det][n_subrays][2]  (i_lo, i_hi); empty ray = (0,-1) */
+    PGET_TABLE_VAR_C = 6,   /* double [n_t]                              c_i (model variant; 0 bytes when off) */
+    PGET_TABLE_VAR_W = 7    /* double [n_subrays][n_t]                   W_j(d_i) (model variant)            */
 };
 
 /* Operation ids for pget_workspace_bytes. */

@@ -23,7 +23,7 @@ __all__ = ["Geometry", "forward", "jvp", "vjp", "gn_apply", "gn_cg_step", "safeg
 
 PGET_GN_EVAL_TRIAL = 1
 PGET_MAX_CG = 256
-TABLES = {"angles": 0, "dirs": 1, "offsets": 2, "weights": 3, "tlat": 4, "clip": 5}
+TABLES = {"angles": 0, "dirs": 1, "offsets": 2, "weights": 3, "tlat": 4, "clip": 5, "var_c": 6, "var_w": 7}
 OPS = {"forward": 0, "jvp": 1, "vjp": 2, "gn_cg_step": 3, "gn_apply": 4, "safeguard": 5, "lm_solve": 6}
 EXPORTED = ["pget_status_string", "pget_last_error_message", "pget_geometry_create", "pget_geometry_destroy",
             "pget_geometry_info", "pget_table_bytes", "pget_geometry_export", "pget_workspace_bytes",
@@ -35,7 +35,8 @@ MODES = ("forward", "jvp", "vjp", "gn")
 class _Desc(C.Structure):
     _fields_ = [("n_px", C.c_int32), ("n_angles", C.c_int32), ("n_banks", C.c_int32), ("n_det", C.c_int32),
                 ("n_subrays", C.c_int32), ("subray_sigma", C.c_double), ("step_px", C.c_double),
-                ("bank1_shift", C.c_double), ("batch", C.c_int32)]
+                ("bank1_shift", C.c_double), ("batch", C.c_int32), ("det_radius", C.c_double),
+                ("c_slope", C.c_double), ("r_slope", C.c_double)]
 
 
 class _Info(C.Structure):
@@ -157,7 +158,8 @@ class Geometry:
         self.device = int(device)           # device < 0: host-only handle (tables/info only)
         d = _Desc(int(desc["n_px"]), int(desc["n_angles"]), int(desc.get("n_banks", 2)), int(desc.get("n_det", 91)),
                   int(desc.get("n_subrays", 1)), float(desc.get("subray_sigma", 0.4)),
-                  float(desc.get("step_px", 0.5)), float(desc.get("bank1_shift", 0.0)), int(desc.get("batch", 1)))
+                  float(desc.get("step_px", 0.5)), float(desc.get("bank1_shift", 0.0)), int(desc.get("batch", 1)),
+                  float(desc.get("det_radius", 0.0)), float(desc.get("c_slope", 0.0)), float(desc.get("r_slope", 0.0)))
         h = C.c_void_p()
         _check(lib().pget_geometry_create(C.byref(d), self.device, C.byref(h)), "pget_geometry_create")
         self._h = h

@@ -259,7 +259,9 @@ ProjArgs base_args(const Geometry& g, const ProjCfg& c)
     A.tasks = S.d_tasks;
     A.cta_begin = S.d_cta_begin;
     A.groups = S.d_groups;
-    A.w = g.d_w;
+    A.w = g.var ? g.d_ones : g.d_w;   // variant: the response W_j(d_i) is inside the ray sums (A.var_cw)
+    A.var_cw = static_cast<const float2*>(g.d_var_cw);
+    A.n_t = g.n_t;
     A.N = g.desc.n_px;
     A.Ns = slot_pitch(g);
     A.P = g.P;
@@ -528,8 +530,12 @@ void free_device_tables(Geometry* g)
 {
     cudaFree(g->d_rays);
     cudaFree(g->d_w);
+    cudaFree(g->d_ones);
+    cudaFree(g->d_var_cw);
     g->d_rays = nullptr;
     g->d_w = nullptr;
+    g->d_ones = nullptr;
+    g->d_var_cw = nullptr;
     for (Schedule& S : g->sch) {
         cudaFree(S.d_cta_begin); cudaFree(S.d_tasks); cudaFree(S.d_groups); cudaFree(S.d_red_off); cudaFree(S.d_red_slot);
         S.d_cta_begin = nullptr; S.d_tasks = nullptr; S.d_groups = nullptr; S.d_red_off = nullptr; S.d_red_slot = nullptr;
@@ -587,7 +593,16 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     if (g.desc.n_px > 2048) { delete h; return fail(PGET_ERR_INVALID_ARGUMENT, "n_px > 2048 not supported"); }
     g.device = device;
     if (const char* ev = std::getenv("PGET_NO_PAIR")) g.pair = g.pair && std::atoi(ev) == 0;   // experiments
+    // the model variant (N3): its attenuation exp(-c_i A_i) does not factor along a ray, so it runs the
+    // whole-ray (fused) projectors, unpaired, with the recomputed GN product
+    auto variant_paths = [&g]() {
+        if (!g.var) return;
+        g.adj_seg = g.jvp_seg = g.fwd_seg = false;
+        g.gn_cached = false;
+        g.pair = false;
+    };
     if (device < 0) {   // host-only handle: tables, info and the host schedules; no device tables, no compute
+        variant_paths();
         std::vector<RayP> rays;
         build_ray_params(g, &rays);
         build_host_schedules(g, rays);
@@ -626,6 +641,7 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     if (const char* ev = std::getenv("PGET_SEGA_W")) g.segA_W = std::max(1, std::min(15, std::atoi(ev)));
     if (const char* ev = std::getenv("PGET_SEGA_CPS")) g.segA_cps = std::max(1, std::min(4, std::atoi(ev)));
     if ((g.segA_W + 1) * 32 * g.segA_cps > 2048) g.segA_cps = 2048 / ((g.segA_W + 1) * 32);
+    variant_paths();
     // the coefficient cache while it stays well inside HBM (config 2: 0.4 GB, config 4: 2.7 GB,
     // config 5's 64 assemblies: 25 GB of 180; measured: config 5 LM iteration 307 -> 210 ms)
     build_host_schedules(g, rays);
@@ -677,6 +693,18 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
             e = cudaMemcpy(g.d_tabsA, lst.data(), lst.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
     }
     if (e == cudaSuccess) e = cudaMalloc(&g.d_w, g.wf.size() * sizeof(float));
+    if (e == cudaSuccess && g.var) {   // the variant's tables as float (W_j(d_i), c_i) and unit weights
+        std::vector<float2> cw(g.var_w.size());
+        for (int j = 0; j < g.desc.n_subrays; ++j)
+            for (int i = 0; i < g.n_t; ++i)
+                cw[static_cast<size_t>(j) * g.n_t + i] =
+                    make_float2(static_cast<float>(g.var_w[static_cast<size_t>(j) * g.n_t + i]), static_cast<float>(g.var_c[i]));
+        const std::vector<float> ones(g.wf.size(), 1.0f);
+        e = cudaMalloc(&g.d_var_cw, cw.size() * sizeof(float2));
+        if (e == cudaSuccess) e = cudaMemcpy(g.d_var_cw, cw.data(), cw.size() * sizeof(float2), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMalloc(&g.d_ones, ones.size() * sizeof(float));
+        if (e == cudaSuccess) e = cudaMemcpy(g.d_ones, ones.data(), ones.size() * sizeof(float), cudaMemcpyHostToDevice);
+    }
     if (e == cudaSuccess) e = cudaMemcpy(g.d_rays, rays.data(), rays.size() * sizeof(RayP), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(g.d_w, g.wf.data(), g.wf.size() * sizeof(float), cudaMemcpyHostToDevice);
     for (int mode = 0; mode < 4 && e == cudaSuccess; ++mode) {
@@ -754,6 +782,8 @@ size_t pget_table_bytes(pget_geometry h, int id)
     case PGET_TABLE_WEIGHTS: return g.weights.size() * sizeof(double);
     case PGET_TABLE_TLAT: return 3 * sizeof(double);
     case PGET_TABLE_CLIP: return g.clip.size() * sizeof(int32_t);
+    case PGET_TABLE_VAR_C: return g.var_c.size() * sizeof(double);
+    case PGET_TABLE_VAR_W: return g.var_w.size() * sizeof(double);
     }
     return 0;
 }
@@ -774,6 +804,8 @@ pget_status pget_geometry_export(pget_geometry h, int id, void* dst, size_t byte
     case PGET_TABLE_WEIGHTS: src = g.weights.data(); break;
     case PGET_TABLE_TLAT: src = tl; break;
     case PGET_TABLE_CLIP: src = g.clip.data(); break;
+    case PGET_TABLE_VAR_C: src = g.var_c.data(); break;
+    case PGET_TABLE_VAR_W: src = g.var_w.data(); break;
     }
     std::memcpy(dst, src, need);
     return PGET_OK;

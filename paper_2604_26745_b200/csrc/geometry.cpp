@@ -35,6 +35,11 @@ pget_status build_geometry(const pget_geometry_desc* d, Geometry* g, std::string
         *err = buf;
         return PGET_ERR_INVALID_ARGUMENT;
     }
+    if (!std::isfinite(d->det_radius) || !std::isfinite(d->c_slope) || !std::isfinite(d->r_slope) ||
+        (d->det_radius > 0.0 && (d->c_slope < 0.0 || d->r_slope < 0.0))) {
+        *err = "invalid model variant (det_radius, c_slope, r_slope must be finite; slopes >= 0)";
+        return PGET_ERR_INVALID_ARGUMENT;
+    }
     g->desc = *d;
     const int N = d->n_px, nA = d->n_angles, nB = d->n_banks, nd = d->n_det, J = d->n_subrays;
 
@@ -83,6 +88,36 @@ pget_status build_geometry(const pget_geometry_desc* d, Geometry* g, std::string
     }
     g->wf.resize(J);
     for (int j = 0; j < J; ++j) g->wf[j] = static_cast<float>(g->weights[j]);
+
+    // model variant (N3, reading R-N3): d_i = det_radius - t_i, c_i = 1 + c_slope d_i, W_j(d_i) the
+    // normalised Gaussian response of width sigma p (1 + r_slope d_i) (the O1-style fp64 text order)
+    g->var = d->det_radius > 0.0;
+    g->var_c.clear();
+    g->var_w.clear();
+    if (g->var) {
+        if (d->det_radius < g->T) {
+            std::snprintf(buf, sizeof buf, "det_radius %g < T %g: a sample would lie behind the detector",
+                          d->det_radius, g->T);
+            *err = buf;
+            return PGET_ERR_INVALID_ARGUMENT;
+        }
+        g->var_c.resize(g->n_t);
+        g->var_w.resize(static_cast<size_t>(J) * g->n_t);
+        for (int i = 0; i < g->n_t; ++i) {
+            const double t = -g->T + (i + 0.5) * g->delta;
+            const double dd = d->det_radius - t;
+            g->var_c[i] = 1.0 + d->c_slope * dd;
+            const double sp = d->subray_sigma * p * (1.0 + d->r_slope * dd);
+            double sum = 0.0;
+            for (int j = 0; j < J; ++j) {
+                const double dj = static_cast<double>(2 * j + 1 - J) / static_cast<double>(2 * J) * p;
+                g->var_w[static_cast<size_t>(j) * g->n_t + i] = std::exp(-(dj * dj) / (2.0 * sp * sp));
+                sum += g->var_w[static_cast<size_t>(j) * g->n_t + i];
+            }
+            for (int j = 0; j < J; ++j)
+                g->var_w[static_cast<size_t>(j) * g->n_t + i] = g->var_w[static_cast<size_t>(j) * g->n_t + i] / sum;
+        }
+    }
 
     // clip: slab test of x(t) = sigma omega_perp + t omega against |x|,|y| <= 1 + h/2
     const double bb = 1.0 + g->h / 2.0;
@@ -140,7 +175,7 @@ pget_status build_geometry(const pget_geometry_desc* d, Geometry* g, std::string
         g->orient[ab] = std::fabs(c) > std::fabs(s) ? 1 : 0;
     }
     g->dup = (nA % 2 == 0) && nB == 2 && d->bank1_shift == 0.0;
-    g->pair = g->dup;
+    g->pair = g->dup && !g->var;   // the variant's opposite-direction attenuation does not factor
     auto traced = [&](int ab) { return !g->dup || (ab / nB) < nA / 2; };
     for (int cls = 0; cls < 2; ++cls)
         for (int ab = 0; ab < g->n_ab; ++ab)

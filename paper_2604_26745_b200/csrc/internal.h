@@ -135,6 +135,9 @@ struct Geometry {
     int n_t;
     std::vector<double> angles, dirs, offsets, weights;
     std::vector<int32_t> clip;
+    // model variant (N3, reading R-N3; desc.det_radius > 0): c_i [n_t], W_j(d_i) [J][n_t]
+    bool var = false;
+    std::vector<double> var_c, var_w;
     int64_t n_samples_nominal;
     int64_t n_samples_traced = 0;
     // launch geometry
@@ -165,6 +168,8 @@ struct Geometry {
     // device tables
     RayP* d_rays = nullptr;       // [n_ab][R] oriented frame
     float* d_w = nullptr;         // [J] float weights
+    float* d_ones = nullptr;      // [J] ones: the variant's response sits inside the ray sums
+    void* d_var_cw = nullptr;     // [J][n_t] float2 (W_j(d_i), c_i) (model variant)
     std::vector<float> wf;        // host copy of the float weights
     int sm_count = 148;
     int cg_coop_blocks = 148;   // co-resident blocks of cg_fused_kernel (cooperative launch bound)

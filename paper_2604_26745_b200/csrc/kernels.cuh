@@ -47,6 +47,8 @@ struct ProjArgs {
     float* gw;              // [B * ntab][2][R] GN scatter weights (w_r, w'_r) of gnw_kernel, or null
     float* gscale;          // [B * ntab][8] fixed-point scale bounds of the cached scatter (null: float path)
     int cellmax;            // max consecutive samples of a ray in one pixel cell
+    const float2* var_cw;   // model variant (N3): [J][n_t] (W_j(d_i), c_i), null when off
+    int n_t;
 };
 
 constexpr int kSegFields = 9;

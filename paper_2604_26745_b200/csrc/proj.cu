@@ -279,10 +279,12 @@ struct SmpA {   // one sample of a ray in sweep A: its corners (prefetched) and 
     float fu, fv;
 };
 
-template <int MODE, bool PAIRED>
+// VAR (model variant N3, reading R-N3): cw is the lane's row [n_t] of (W_j(d_i), c_i); E_i = e^{-c_i A_i},
+// the forward / JVP sums carry W_j(d_i), the adjoint's G carries W c (G_c = sum W lam c E).
+template <int MODE, bool PAIRED, bool VAR = false>
 __device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int P, int r0, int r1, int ilo,
                                        int64_t dU, int64_t dV, float cf, float ch, float dl, float dlh, int& i,
-                                       int64_t& u, int64_t& v, StateA& st)
+                                       int64_t& u, int64_t& v, StateA& st, const float2* __restrict__ cw = nullptr)
 {
     using TR = ModeTraits<MODE>;
     using Cn = typename CornerT<TR::NF4>::T;
@@ -321,14 +323,22 @@ __device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int
             arg = fmaf(mu, ch, x_.s);
             x_.s = fmaf(mu, cf, x_.s);
         }
-        const float E = ex2(arg);      // exp(-Delta(mu_i/2 + sum_{k>i} mu_k))
-        if constexpr (TR::COMP_G) kahan(x_.g, x_.gc, lam * E);
-        else x_.g = fmaf(lam, E, x_.g);
+        float cv = 1.f, wv = 1.f;      // VAR: c_i, W_j(d_i)
+        if constexpr (VAR) {
+            const float2 t = __ldg(cw + i);
+            wv = t.x;
+            cv = t.y;
+        }
+        const float E = VAR ? ex2(cv * arg) : ex2(arg);   // exp(-c_i Delta(mu_i/2 + sum_{k>i} mu_k))
+        const float lg = VAR ? lam * (TR::HAS_B ? wv * cv : wv) : lam;
+        if constexpr (TR::COMP_G) kahan(x_.g, x_.gc, lg * E);
+        else x_.g = fmaf(lg, E, x_.g);
         float dA = 0.f;
         if constexpr (TR::NF4) {
             dA = fmaf(dmu, dlh, x_.ds);   // Delta (dmu_i/2 + sum_{k>i} dmu_k)
-            if constexpr (TR::COMP_J) kahan(x_.dg, x_.dgc, fmaf(-lam, dA, dlam) * E);
-            else x_.dg = fmaf(fmaf(-lam, dA, dlam), E, x_.dg);
+            const float jt = VAR ? wv * fmaf(-lam * cv, dA, dlam) : fmaf(-lam, dA, dlam);
+            if constexpr (TR::COMP_J) kahan(x_.dg, x_.dgc, jt * E);
+            else x_.dg = fmaf(jt, E, x_.dg);
             x_.ds = fmaf(dmu, dl, x_.ds);
         }
         if constexpr (PAIRED && (MODE == MODE_FWD || MODE == MODE_VJP)) {   // VJP: segmented phase A only
@@ -383,12 +393,14 @@ struct RayB {   // per-ray constants of sweep B
 // CACHE (the LM wrap's gradient VJP): rb holds the unit-weight constants; every sample's Jacobian
 // entries (alpha, beta, alpha', beta') go to the lane's cache block (row k) and the scatter weights
 // are w_r (alpha, beta) + w'_r (alpha', beta') -- the cache build of lin_kernel fused into the VJP.
-template <bool PAIRED, bool COMP, bool CACHE = false>
+// VAR (model variant N3): cw is the lane's row of (W_j(d_i), c_i): a_lam(i) = w_r Delta W_i E_i,
+// a_mu(i) = -w_r Delta^2 (sum_{k<i} W_k lam_k c_k E_k + W_i lam_i c_i E_i / 2), E_i = e^{-c_i A_i}
+template <bool PAIRED, bool COMP, bool CACHE = false, bool VAR = false>
 __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* __restrict__ acc, int P, int r0,
                                        int r1, int abase, int sP, int ilo, int64_t dU, int64_t dV, float cf, float ch,
                                        const RayB& rb, int& i, int64_t& u, int64_t& v, StateB& st,
                                        float wr = 0.f, float wr1 = 0.f, float4* cl = nullptr, int* kp = nullptr,
-                                       float2* emax = nullptr)
+                                       float2* emax = nullptr, const float2* __restrict__ cw = nullptr)
 {
     int iv = hi32(v), iu = hi32(u);
     if (i < ilo || iv < r0 || iv >= r1) return;
@@ -421,9 +433,15 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
         }
         const float2 x = bilerp2(q00, q01, q10, q11, fu, fv);
         const float arg_hi = fmaf(x.y, ch, x_.s);
-        const float E = ex2(arg_hi - x_.sc);
-        const float le = x.x * E;
-        float al = rb.kl * E;
+        float cv = 1.f, wv = 1.f;
+        if constexpr (VAR) {
+            const float2 t = __ldg(cw + i);
+            wv = t.x;
+            cv = t.y;
+        }
+        const float E = VAR ? ex2(cv * (arg_hi - x_.sc)) : ex2(arg_hi - x_.sc);
+        const float le = VAR ? x.x * (wv * cv) * E : x.x * E;
+        float al = VAR ? rb.kl * (wv * E) : rb.kl * E;
         float am = rb.km * (((rb.G - x_.q) - (rb.Gc - x_.qc)) - 0.5f * le);
         if constexpr (CACHE) {   // unit-weight entries: store, then weight
             float4 cv = make_float4(al, am, 0.f, 0.f);
@@ -512,7 +530,7 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
 }
 
 // ------------------------------------------------------------------------------------------ kernel
-template <int MODE, int MAXG, bool PAIRED>
+template <int MODE, int MAXG, bool PAIRED, bool VAR = false>
 __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MINB) proj_kernel(ProjArgs A)
 {
     using TR = ModeTraits<MODE>;
@@ -567,10 +585,12 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
             int rr[MAXG], ii[MAXG], ilo[MAXG];
             int64_t uu[MAXG], vv[MAXG];
             StateA st[MAXG];
+            const float2* cwa[MAXG];
 #pragma unroll
             for (int k = 0; k < MAXG; ++k) {
                 const int r = prl + ((pass * MAXG + k) * W + warp) * 32 + lane;
                 rr[k] = r < prh ? r : -1;
+                cwa[k] = VAR && rr[k] >= 0 ? A.var_cw + static_cast<size_t>(rr[k] % J) * A.n_t : nullptr;
                 ii[k] = -1; ilo[k] = 0; uu[k] = 0; vv[k] = 0;
                 if (rr[k] >= 0) {
                     const RayP rp = rays[rr[k]];
@@ -589,7 +609,8 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                 const unsigned char* sb = stage0 + b * A.stage_bytes;
 #pragma unroll
                 for (int k = 0; k < MAXG; ++k)
-                    walk_a<MODE, PAIRED>(sb, P, r0, r1, ilo[k], dU, dV, cf, ch, dl, dlh, ii[k], uu[k], vv[k], st[k]);
+                    walk_a<MODE, PAIRED, VAR>(sb, P, r0, r1, ilo[k], dU, dV, cf, ch, dl, dlh, ii[k], uu[k], vv[k], st[k],
+                                              cwa[k]);
                 __syncthreads();   // stage buffer b consumed
                 if (tid == 0 && s + 2 < n_stages) issue_stage<MODE>(A, t0, ns_task, s + 2, stage0 + b * A.stage_bytes, &mbar[b]);
                 ++s;
@@ -671,10 +692,12 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
             int64_t uu[MAXG], vv[MAXG];
             RayB rb[MAXG];
             StateB st[MAXG];
+            const float2* cwb[MAXG];
 #pragma unroll
             for (int k = 0; k < MAXG; ++k) {
                 const int grp = ti.gbeg + (pass * MAXG + k) * W + warp;
                 const int r = grp < ti.gend ? A.groups[grp * 32 + lane] : -1;
+                cwb[k] = VAR && r >= 0 ? A.var_cw + static_cast<size_t>(r % J) * A.n_t : nullptr;
                 ii[k] = -1; ilo[k] = 0; uu[k] = 0; vv[k] = 0;
                 rb[k] = RayB{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
                 st[k] = StateB{0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -717,8 +740,9 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                 const int abase = flip ? A.RbB * P : 0, sP = flip ? -P : P;
 #pragma unroll
                 for (int k = 0; k < MAXG; ++k)
-                    walk_b<PAIRED, TR::COMP_S>(sb, wacc, P, r0, r1, abase, sP, ilo[k], dU, dV, cf, ch, rb[k], ii[k], uu[k], vv[k],
-                                   st[k]);
+                    walk_b<PAIRED, TR::COMP_S, false, VAR>(sb, wacc, P, r0, r1, abase, sP, ilo[k], dU, dV, cf, ch, rb[k],
+                                                           ii[k], uu[k], vv[k], st[k], 0.f, 0.f, nullptr, nullptr,
+                                                           nullptr, cwb[k]);
                 __syncthreads();   // stage buffer b and every warp ring consumed
                 if (tid == 0 && s + 2 < n_stages) issue_stage<MODE>(A, t0, ns_task, s + 2, stage0 + b * A.stage_bytes, &mbar[b]);
                 ++s;
@@ -1526,6 +1550,22 @@ __device__ __forceinline__ void red_s32(uint32_t addr, int v)
 {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
+// (lambda, mu) fixed-point pair as one signed 64-bit addend: lo + hi 2^32 (int64 arithmetic), so a sum
+// of such addends is sum(lo) + sum(hi) 2^32 exactly, and both halves decode when |sum(lo)| < 2^31
+__device__ __forceinline__ void red_s64(uint32_t addr, int lo, int hi)
+{
+    const unsigned long long v =
+        static_cast<unsigned long long>((static_cast<long long>(hi) << 32) + static_cast<long long>(lo));
+    asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
+}
+__device__ __forceinline__ int2 unpack_s64(long long x)
+{
+    const int lo = static_cast<int>(x & 0xffffffffLL);
+    return make_int2(lo, static_cast<int>((x - lo) >> 32));
+}
+#ifndef PGET_GNB_MODE
+#define PGET_GNB_MODE 0   // experiments: bit 0 no same-cell merging (flush every sample), bit 1 packed 64-bit adds
+#endif
 template <bool INTACC>
 __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0, int r1, int abase, int sP, int ilo,
                                          int64_t dU, int64_t dV, float wr, float wr1, int& i, int64_t& u, int64_t& v,
@@ -1537,7 +1577,16 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
     float2 p00 = make_float2(0.f, 0.f), p01 = p00, p10 = p00, p11 = p00;
     const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(acc));
     auto rmw = [&](int off, float2 a, float2 b, float2 c, float2 d) {
-        if constexpr (INTACC) {
+        if constexpr (INTACC && (PGET_GNB_MODE & 2)) {
+            const float2 mg = make_float2(12582912.f, 12582912.f);   // 1.5 * 2^23
+            const float2 ta = __ffma2_rn(a, S, mg), tb = __ffma2_rn(b, S, mg);
+            const float2 tc = __ffma2_rn(c, S, mg), td = __ffma2_rn(d, S, mg);
+            const uint32_t a0 = sbase + static_cast<uint32_t>(off * 8), a1 = sbase + static_cast<uint32_t>((off + sP) * 8);
+            red_s64(a0, __float_as_int(ta.x) - 0x4B400000, __float_as_int(ta.y) - 0x4B400000);
+            red_s64(a0 + 8, __float_as_int(tb.x) - 0x4B400000, __float_as_int(tb.y) - 0x4B400000);
+            red_s64(a1, __float_as_int(tc.x) - 0x4B400000, __float_as_int(tc.y) - 0x4B400000);
+            red_s64(a1 + 8, __float_as_int(td.x) - 0x4B400000, __float_as_int(td.y) - 0x4B400000);
+        } else if constexpr (INTACC) {
             const float2 mg = make_float2(12582912.f, 12582912.f);   // 1.5 * 2^23
             const float2 ta = __ffma2_rn(a, S, mg), tb = __ffma2_rn(b, S, mg);
             const float2 tc = __ffma2_rn(c, S, mg), td = __ffma2_rn(d, S, mg);
@@ -1580,7 +1629,9 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
         const float2 c10 = __ffma2_rn(c11, make_float2(-1.f, -1.f), tv);
         const float2 c01 = __fmul2_rn(bv, make_float2(fu, fu));
         const float2 c00 = __ffma2_rn(c01, make_float2(-1.f, -1.f), bv);
-        if (aoff != poff) {
+        if constexpr (PGET_GNB_MODE & 1) {   // experiment: every sample added at once (no divergent merge)
+            rmw(aoff, c00, c01, c10, c11);
+        } else if (aoff != poff) {
             if (poff >= 0 && (PGET_ABLATE != 1 || p00.x == 12345.f)) rmw(poff, p00, p01, p10, p11);   // ABLATE 1: no scatter
             poff = aoff;
             p00 = c00; p01 = c01; p10 = c10; p11 = c11;
@@ -1598,7 +1649,7 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
     };
     while (step(c0) && step(c1) && step(c2) && step(c3)) {
     }
-    rmw(poff, p00, p01, p10, p11);
+    if constexpr (!(PGET_GNB_MODE & 1)) rmw(poff, p00, p01, p10, p11);
     ck = p;
 }
 
@@ -1931,7 +1982,14 @@ __global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
                     const int lr = flip ? r0 + Rb - rw : rw - r0;
                     PGET_CHECK(lr >= 0 && lr < RB1);
                     float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if constexpr (INTACC) {
+                    if constexpr (INTACC && (PGET_GNB_MODE & 2)) {
+                        long long* el = reinterpret_cast<long long*>(wacc_all) + static_cast<size_t>(lr) * P + 2 * q;
+                        const int2 x0 = unpack_s64(el[0]), x1 = unpack_s64(el[1]);
+                        el[0] = 0;
+                        el[1] = 0;
+                        sum = make_float4(static_cast<float>(x0.x) * iS.x, static_cast<float>(x0.y) * iS.y,
+                                          static_cast<float>(x1.x) * iS.x, static_cast<float>(x1.y) * iS.y);
+                    } else if constexpr (INTACC) {
                         int2* el = reinterpret_cast<int2*>(wacc_all) + static_cast<size_t>(lr) * (P / 2) + q;
                         int2* em = el + static_cast<size_t>(RB1) * (P / 2);   // mu plane
                         const int2 xl = *el, xm = *em;
@@ -2155,7 +2213,10 @@ static cudaError_t launch_mode(int maxg, bool paired, const ProjArgs& A, int gri
                                cudaStream_t s)
 {
     constexpr bool CP = MODE != MODE_JVP;   // the JVP is never line-paired
-    if (paired && CP) {
+    if (A.var_cw) {   // model variant (N3): unpaired only
+        if (maxg == 1) proj_kernel<MODE, 1, false, true><<<grid, block, smem, s>>>(A);
+        else proj_kernel<MODE, 2, false, true><<<grid, block, smem, s>>>(A);
+    } else if (paired && CP) {
         if (maxg == 1) proj_kernel<MODE, 1, CP><<<grid, block, smem, s>>>(A);
         else proj_kernel<MODE, 2, CP><<<grid, block, smem, s>>>(A);
     } else {
@@ -2259,6 +2320,8 @@ static cudaError_t attr_mode(size_t smem)
     if ((e = raise_smem(proj_kernel<MODE, 1, false>, v))) return e;
     if ((e = raise_smem(proj_kernel<MODE, 2, false>, v))) return e;
     if ((e = raise_smem(proj_kernel<MODE, 1, CP>, v))) return e;
+    if ((e = raise_smem(proj_kernel<MODE, 1, false, true>, v))) return e;
+    if ((e = raise_smem(proj_kernel<MODE, 2, false, true>, v))) return e;
     return raise_smem(proj_kernel<MODE, 2, CP>, v);
 }
 

@@ -141,3 +141,33 @@ def test_workspace_regions_inside_and_disjoint():
         g.workspace_region("forward", 0)
     with pytest.raises(RuntimeError):
         g.workspace_region("gn_cg_step", 7)
+
+
+VAR_GEOMS = [dict(P.geometry_desc(c), det_radius=1.6, c_slope=0.05, r_slope=0.35) for c in (2, 4)] + [
+    dict(n_px=16, n_angles=7, n_banks=1, n_det=5, n_subrays=9, subray_sigma=0.3, step_px=0.37, bank1_shift=0.0,
+         batch=3, det_radius=2.0, c_slope=0.2, r_slope=1.0)]
+
+
+@pytest.mark.parametrize("gd", VAR_GEOMS)
+def test_variant_tables_bit_exact_with_oracle(gd):
+    """Model variant (N3, reading R-N3): the library's c_i and W_j(d_i) equal the oracle's O13 tables bit
+    for bit; the variant disables line pairing (its attenuation does not factor along a line)."""
+    g = pg.Geometry(gd, device=-1)
+    v = O.variant_tables(gd)
+    assert _same_bits(g.export("var_c"), v["c"])
+    assert _same_bits(g.export("var_w").reshape(v["w"].shape), v["w"])
+    base = pg.Geometry(dict(gd, det_radius=0.0), device=-1)
+    assert g.info["n_samples_traced"] >= base.info["n_samples_traced"]
+    if base.info["angle_banks_merged"]:
+        assert g.info["n_samples_traced"] == 2 * base.info["n_samples_traced"]   # unpaired
+    assert g.export("var_c").size > 0 and base.export("var_c").size == 0
+
+
+def test_variant_desc_validation():
+    import ctypes as C
+    bad = [dict(P.geometry_desc(2), det_radius=1.0, c_slope=0.1),          # det_radius < T
+           dict(P.geometry_desc(2), det_radius=1.6, c_slope=-0.1),         # negative slope
+           dict(P.geometry_desc(2), det_radius=1.6, r_slope=float("nan"))]
+    for gd in bad:
+        with pytest.raises(RuntimeError, match="INVALID_ARGUMENT"):
+            pg.Geometry(gd, device=-1)
