@@ -266,7 +266,28 @@ struct CornerT<false> {
 struct StateA {
     float s, sc, g, gc, ds, dg, dgc;
     float p1, p1c, p2, p2c, p3, p3c;   // PAIRED: sums over e^{+A_i} for the reverse-direction ray
+    // PAIRED (reading R-depth): s, sc and p1..p3 are local to the current band; Lb, Lbc is the depth
+    // before the band and R1..R3 the reverse-direction sums rebased to the current depth,
+    // R_k = 2^{L} sum_{visited} (.) 2^{-L_i} <= sum (.), folded in at every band end (fold_a)
+    float Lb, Lbc, R1, R2, R3;
 };
+
+// PAIRED: close a band.  The reverse-direction sums of the band (relative to the band start, whose
+// exponents 2^{-s_local} stay small) join the rebased totals, the band depth joins Lb, and the band
+// accumulators restart: no exponent ever exceeds a band's optical depth, so sum lam e^{+A} neither
+// overflows nor loses the precision of a large fp32 depth (DESIGN.md R-depth).
+__device__ __forceinline__ void fold_a(StateA& q)
+{
+    const float sb = q.s - q.sc;   // the band's depth (log2 units, <= 0)
+    const float eb = ex2(sb);
+    q.R1 = eb * (q.R1 + (q.p1 - q.p1c));
+    q.R2 = eb * (q.R2 + (q.p2 - q.p2c));
+    q.R3 = eb * (q.R3 + (q.p3 - q.p3c));
+    kahan(q.Lb, q.Lbc, q.s);
+    kahan(q.Lb, q.Lbc, -q.sc);
+    q.s = q.sc = 0.f;
+    q.p1 = q.p1c = q.p2 = q.p2c = q.p3 = q.p3c = 0.f;
+}
 
 // Sweep A: forward (+ JVP) recurrence, detector end first.
 // PAIRED (line pairing): the same traversal also accumulates, for the ray of
@@ -329,7 +350,8 @@ __device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int
             wv = t.x;
             cv = t.y;
         }
-        const float E = VAR ? ex2(cv * arg) : ex2(arg);   // exp(-c_i Delta(mu_i/2 + sum_{k>i} mu_k))
+        // exp(-c_i Delta(mu_i/2 + sum_{k>i} mu_k)); PAIRED: arg is band-local, Lb the depth before the band
+        const float E = VAR ? ex2(cv * arg) : (PAIRED ? ex2(arg + x_.Lb) : ex2(arg));
         const float lg = VAR ? lam * (TR::HAS_B ? wv * cv : wv) : lam;
         if constexpr (TR::COMP_G) kahan(x_.g, x_.gc, lg * E);
         else x_.g = fmaf(lg, E, x_.g);
@@ -598,7 +620,7 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                     uu[k] = rp.U0 + static_cast<int64_t>(rp.ihi) * dU;
                     vv[k] = rp.V0 + static_cast<int64_t>(rp.ihi) * dV;
                 }
-                st[k] = StateA{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                st[k] = StateA{};
             }
             for (int kb = 0; kb < A.nbA; ++kb) {
                 const int band = ti.dir > 0 ? A.nbA - 1 - kb : kb;
@@ -608,9 +630,11 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                 mbar_wait(&mbar[b], static_cast<uint32_t>((s >> 1) & 1));
                 const unsigned char* sb = stage0 + b * A.stage_bytes;
 #pragma unroll
-                for (int k = 0; k < MAXG; ++k)
+                for (int k = 0; k < MAXG; ++k) {
                     walk_a<MODE, PAIRED, VAR>(sb, P, r0, r1, ilo[k], dU, dV, cf, ch, dl, dlh, ii[k], uu[k], vv[k], st[k],
                                               cwa[k]);
+                    if (PAIRED) fold_a(st[k]);
+                }
                 __syncthreads();   // stage buffer b consumed
                 if (tid == 0 && s + 2 < n_stages) issue_stage<MODE>(A, t0, ns_task, s + 2, stage0 + b * A.stage_bytes, &mbar[b]);
                 ++s;
@@ -623,15 +647,15 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                 const StateA& q = st[k];
                 if (MODE == MODE_FWD) {
                     rout[r] = A.delta * q.g;
-                    if (PAIRED) rout[R + r] = A.delta * ex2(q.s) * q.p2;   // e^{-S} sum lam e^{A}
+                    if (PAIRED) rout[R + r] = A.delta * q.R2;   // e^{-S} sum lam e^{A} (rebased, fold_a)
                 }
                 if (MODE == MODE_JVP) { rout[r] = A.delta * q.g; rout[R + r] = A.delta * (q.dg - q.dgc); }
-                if (MODE == MODE_VJP || MODE == MODE_GN) gsh[r] = make_float4(q.g, q.gc, q.s, q.sc);
+                if (MODE == MODE_VJP || MODE == MODE_GN)
+                    gsh[r] = PAIRED ? make_float4(q.g, q.gc, q.Lb, q.Lbc) : make_float4(q.g, q.gc, q.s, q.sc);
                 if (MODE == MODE_GN) {
                     rout[r] = A.delta * (q.dg - q.dgc);
                     if (PAIRED)   // opposite bank: e^{-S} (sum dlam e^A - dS sum lam e^A + sum lam dA e^A)
-                        rout[R + r] = A.delta * ex2(q.s - q.sc) *
-                                      (((q.p1 - q.p1c) + (q.p3 - q.p3c)) - q.ds * (q.p2 - q.p2c));
+                        rout[R + r] = A.delta * ((q.R1 + q.R3) - q.ds * q.R2);
                 }
             }
         }
@@ -915,7 +939,7 @@ __global__ void __launch_bounds__(512, 1) seg_a_kernel(ProjArgs A)   // W consum
                     uu[k] = rp.U0 + static_cast<int64_t>(ii[k]) * dU;
                     vv[k] = rp.V0 + static_cast<int64_t>(ii[k]) * dV;
                 }
-                st[k] = StateA{0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+                st[k] = StateA{};
             }
             for (int j = 0; j < ui.nb; ++j) {
                 int r0, r1;
@@ -924,8 +948,10 @@ __global__ void __launch_bounds__(512, 1) seg_a_kernel(ProjArgs A)   // W consum
                 mbar_wait(&full[b], static_cast<uint32_t>((s / kSegAStages) & 1));
                 const unsigned char* sbuf = stage0 + b * A.stage_bytes;
 #pragma unroll
-                for (int k = 0; k < MAXG; ++k)
+                for (int k = 0; k < MAXG; ++k) {
                     walk_a<MODE, PAIRED>(sbuf, P, r0, r1, ilo[k], dU, dV, cf, ch, dl, dlh, ii[k], uu[k], vv[k], st[k]);
+                    if (PAIRED) fold_a(st[k]);
+                }
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&empty[b]);   // this warp is done with buffer b
                 ++s;
@@ -935,22 +961,25 @@ __global__ void __launch_bounds__(512, 1) seg_a_kernel(ProjArgs A)   // W consum
                 const int r = rr[k];
                 if (r < 0) continue;
                 const StateA& q = st[k];
-                part[0 * R + r] = q.s;
-                part[1 * R + r] = q.sc;
+                // PAIRED: the unit's depth is Lb (every band folded) and the reverse-direction sums are
+                // rebased to the unit's end (R_k = 2^{s_unit} p_k): the combines scale them by
+                // 2^{-(depth after the unit)}
+                part[0 * R + r] = PAIRED ? q.Lb : q.s;
+                part[1 * R + r] = PAIRED ? q.Lbc : q.sc;
                 part[2 * R + r] = q.g;
                 part[3 * R + r] = q.gc;
                 if (MODE == MODE_GN) {
                     part[4 * R + r] = q.ds;
                     part[5 * R + r] = q.dg - q.dgc;
-                    part[6 * R + r] = q.p1;
-                    part[8 * R + r] = q.p3;
+                    part[6 * R + r] = PAIRED ? q.R1 : q.p1;
+                    part[8 * R + r] = PAIRED ? q.R3 : q.p3;
                 }
                 if (MODE == MODE_JVP) {   // the compensated JVP sum kept as its pair
                     part[4 * R + r] = q.ds;
                     part[5 * R + r] = q.dg;
                     part[6 * R + r] = q.dgc;
                 }
-                if (PAIRED) part[7 * R + r] = q.p2;
+                if (PAIRED) part[7 * R + r] = q.R2;
             }
         }
     }
@@ -1020,8 +1049,8 @@ __global__ void __launch_bounds__(256) fwd_combine_kernel(ProjArgs A, const int3
         for (int q = 0; q < K; ++q) {
             const float* pq = part0 + static_cast<size_t>(dir > 0 ? K - 1 - q : q) * kSegFields * R;
             y += exp2(L) * (static_cast<double>(pq[2 * R + r]) - pq[3 * R + r]);
-            if (PAIRED) p2 += exp2(-L) * pq[7 * R + r];
             L += static_cast<double>(pq[0 * R + r]) - pq[1 * R + r];
+            if (PAIRED) p2 += exp2(-L) * pq[7 * R + r];   // rebased to the unit's end (seg_a_kernel)
         }
         ry[r] = static_cast<float>(A.delta * y);
         if (PAIRED) ry[R + r] = static_cast<float>(A.delta * exp2(L) * p2);
@@ -1167,7 +1196,7 @@ __global__ void __launch_bounds__(512, 1) seg_b_kernel(ProjArgs A)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 if (q >= qme && q < K) T += exp2(Lb[q] - Lme) * gq[q];
-                if (PAIRED && q < qme) Qoff += exp2(LK - Lb[q]) * p2q[q];
+                if (PAIRED && q < qme) Qoff += exp2(LK - Lb[q + 1]) * p2q[q];   // rebased R2
             }
             const double Sl = LK - Lme;
             const float Th = static_cast<float>(T), Sh = static_cast<float>(Sl), Qh = static_cast<float>(Qoff);
@@ -1182,7 +1211,7 @@ __global__ void __launch_bounds__(512, 1) seg_b_kernel(ProjArgs A)
                     if (q < K) {
                         dG += exp2(Lb[q]) * (dgq[q] - dLb[q] * gq[q]);
                         if (PAIRED) {
-                            const double e = exp2(-Lb[q]);
+                            const double e = exp2(-Lb[q + 1]);   // rebased R1..R3
                             P1 += e * p1q[q];
                             P2 += e * p2q[q];
                             P3 += e * (p3q[q] + dLb[q] * p2q[q]);
@@ -1366,7 +1395,7 @@ __device__ __forceinline__ void seg_constants(const ProjArgs& A, const UnitInfo&
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         if (q >= qme && q < K) T += exp2(Lb[q] - Lme) * gq[q];
-        if (PAIRED && q < qme) Qoff += exp2(LK - Lb[q]) * p2q[q];
+        if (PAIRED && q < qme) Qoff += exp2(LK - Lb[q + 1]) * p2q[q];   // rebased R2
     }
     const double Sl = LK - Lme;
     const float Th = static_cast<float>(T), Sh = static_cast<float>(Sl), Qh = static_cast<float>(Qoff);
@@ -1413,7 +1442,7 @@ __device__ __forceinline__ void gn_rout_from_seg(const ProjArgs& A, int canon0, 
         if (q < K) {
             dG += exp2(Lb[q]) * (dgq[q] - dLb[q] * gq[q]);
             if (PAIRED) {
-                const double e = exp2(-Lb[q]);
+                const double e = exp2(-Lb[q + 1]);   // rebased R1..R3 (seg_a_kernel)
                 P1 += e * p1q[q];
                 P2 += e * p2q[q];
                 P3 += e * (p3q[q] + dLb[q] * p2q[q]);
@@ -1550,43 +1579,41 @@ __device__ __forceinline__ void red_s32(uint32_t addr, int v)
 {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
-// (lambda, mu) fixed-point pair as one signed 64-bit addend: lo + hi 2^32 (int64 arithmetic), so a sum
-// of such addends is sum(lo) + sum(hi) 2^32 exactly, and both halves decode when |sum(lo)| < 2^31
-__device__ __forceinline__ void red_s64(uint32_t addr, int lo, int hi)
-{
-    const unsigned long long v =
-        static_cast<unsigned long long>((static_cast<long long>(hi) << 32) + static_cast<long long>(lo));
-    asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(addr), "l"(v) : "memory");
-}
-__device__ __forceinline__ int2 unpack_s64(long long x)
-{
-    const int lo = static_cast<int>(x & 0xffffffffLL);
-    return make_int2(lo, static_cast<int>((x - lo) >> 32));
-}
 #ifndef PGET_GNB_MODE
-#define PGET_GNB_MODE 0   // experiments: bit 0 no same-cell merging (flush every sample), bit 1 packed 64-bit adds
+#define PGET_GNB_MODE 0   // experiments: bit 2 half-width entry stream (timing ablation), bit 3 L2 evict-first loads
 #endif
+__device__ __forceinline__ float4 ld_entry_ef(const float4* q, uint64_t pol)
+{
+    float4 r;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(q), "l"(pol));
+    return r;
+}
 template <bool INTACC>
 __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0, int r1, int abase, int sP, int ilo,
                                          int64_t dU, int64_t dV, float wr, float wr1, int& i, int64_t& u, int64_t& v,
-                                         const float4*& ck, const float4* cend, float2 S, uint32_t planeB)
+                                         const float4*& ck, const float4* cend, float2 S, uint32_t planeB,
+                                         const float4* cbase = nullptr)
 {
+    [[maybe_unused]] uint64_t pol = 0;
+    if constexpr (PGET_GNB_MODE & 8) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    auto LD = [&](const float4* q) -> float4 {
+        if constexpr (PGET_GNB_MODE & 4) {   // timing ablation: half the bytes per entry (values wrong)
+            const float2 h = __ldg(reinterpret_cast<const float2*>(cbase) + (q - cbase));
+            return make_float4(h.x, h.y, 0.f, 0.f);
+        } else if constexpr (PGET_GNB_MODE & 8) {
+            return ld_entry_ef(q, pol);
+        } else {
+            return __ldg(q);
+        }
+    };
     const int iv0 = hi32(v);
     if (i < ilo || iv0 < r0 || iv0 >= r1) return;
     int poff = -1;
     float2 p00 = make_float2(0.f, 0.f), p01 = p00, p10 = p00, p11 = p00;
     const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(acc));
     auto rmw = [&](int off, float2 a, float2 b, float2 c, float2 d) {
-        if constexpr (INTACC && (PGET_GNB_MODE & 2)) {
-            const float2 mg = make_float2(12582912.f, 12582912.f);   // 1.5 * 2^23
-            const float2 ta = __ffma2_rn(a, S, mg), tb = __ffma2_rn(b, S, mg);
-            const float2 tc = __ffma2_rn(c, S, mg), td = __ffma2_rn(d, S, mg);
-            const uint32_t a0 = sbase + static_cast<uint32_t>(off * 8), a1 = sbase + static_cast<uint32_t>((off + sP) * 8);
-            red_s64(a0, __float_as_int(ta.x) - 0x4B400000, __float_as_int(ta.y) - 0x4B400000);
-            red_s64(a0 + 8, __float_as_int(tb.x) - 0x4B400000, __float_as_int(tb.y) - 0x4B400000);
-            red_s64(a1, __float_as_int(tc.x) - 0x4B400000, __float_as_int(tc.y) - 0x4B400000);
-            red_s64(a1 + 8, __float_as_int(td.x) - 0x4B400000, __float_as_int(td.y) - 0x4B400000);
-        } else if constexpr (INTACC) {
+        if constexpr (INTACC) {
             const float2 mg = make_float2(12582912.f, 12582912.f);   // 1.5 * 2^23
             const float2 ta = __ffma2_rn(a, S, mg), tb = __ffma2_rn(b, S, mg);
             const float2 tc = __ffma2_rn(c, S, mg), td = __ffma2_rn(d, S, mg);
@@ -1609,7 +1636,7 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
         }
     };
     const float4* p = ck;
-    float4 c0 = __ldg(p), c1 = __ldg(p + 32), c2 = __ldg(p + 64), c3 = __ldg(p + 96);
+    float4 c0 = LD(p), c1 = LD(p + 32), c2 = LD(p + 64), c3 = LD(p + 96);
     int iv = iv0;
     auto step = [&](float4& c) -> bool {
         const int aoff = abase + (iv - r0) * sP + hi32(u);
@@ -1620,8 +1647,11 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
         const int iv2 = hi32(v2);
         const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;
         const float2 av = make_float2(fmaf(wr, c.x, wr1 * c.z), fmaf(wr, c.y, wr1 * c.w));
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(p + PGET_PF_DIST * 32));
-        c = __ldg(p + 4 * 32);
+        if constexpr (PGET_GNB_MODE & 4)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const float2*>(cbase) + (p - cbase) + PGET_PF_DIST * 32));
+        else
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(p + PGET_PF_DIST * 32));
+        c = LD(p + 4 * 32);
         p += 32;
         const float2 tv = __fmul2_rn(av, make_float2(fv, fv));         // row j0+1
         const float2 bv = __ffma2_rn(tv, make_float2(-1.f, -1.f), av); // row j0
@@ -1629,9 +1659,7 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
         const float2 c10 = __ffma2_rn(c11, make_float2(-1.f, -1.f), tv);
         const float2 c01 = __fmul2_rn(bv, make_float2(fu, fu));
         const float2 c00 = __ffma2_rn(c01, make_float2(-1.f, -1.f), bv);
-        if constexpr (PGET_GNB_MODE & 1) {   // experiment: every sample added at once (no divergent merge)
-            rmw(aoff, c00, c01, c10, c11);
-        } else if (aoff != poff) {
+        if (aoff != poff) {
             if (poff >= 0 && (PGET_ABLATE != 1 || p00.x == 12345.f)) rmw(poff, p00, p01, p10, p11);   // ABLATE 1: no scatter
             poff = aoff;
             p00 = c00; p01 = c01; p10 = c10; p11 = c11;
@@ -1649,7 +1677,7 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
     };
     while (step(c0) && step(c1) && step(c2) && step(c3)) {
     }
-    if constexpr (!(PGET_GNB_MODE & 1)) rmw(poff, p00, p01, p10, p11);
+    rmw(poff, p00, p01, p10, p11);
     ck = p;
 }
 
@@ -1961,7 +1989,7 @@ __global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
                 const int abase = flip ? Rb * P : 0, sP = flip ? -P : P;
                 if (PGET_ABLATE != 3)   // 3: no walk
                     walk_gnb<INTACC>(wacc, P, r0, r1, abase, sP, ilo, dU, dV, wr, wr1, ii, uu, vv, cl, cend, S,
-                                     static_cast<uint32_t>(RB1 * P * 4));
+                                     static_cast<uint32_t>(RB1 * P * 4), A.cache);
                 __syncthreads();   // every warp ring complete
                 const bool last = j == ui.nb - 1;
                 const int carry = last ? -1 : (ui.dir > 0 ? r0 : r1);
@@ -1982,14 +2010,7 @@ __global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
                     const int lr = flip ? r0 + Rb - rw : rw - r0;
                     PGET_CHECK(lr >= 0 && lr < RB1);
                     float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if constexpr (INTACC && (PGET_GNB_MODE & 2)) {
-                        long long* el = reinterpret_cast<long long*>(wacc_all) + static_cast<size_t>(lr) * P + 2 * q;
-                        const int2 x0 = unpack_s64(el[0]), x1 = unpack_s64(el[1]);
-                        el[0] = 0;
-                        el[1] = 0;
-                        sum = make_float4(static_cast<float>(x0.x) * iS.x, static_cast<float>(x0.y) * iS.y,
-                                          static_cast<float>(x1.x) * iS.x, static_cast<float>(x1.y) * iS.y);
-                    } else if constexpr (INTACC) {
+                    if constexpr (INTACC) {
                         int2* el = reinterpret_cast<int2*>(wacc_all) + static_cast<size_t>(lr) * (P / 2) + q;
                         int2* em = el + static_cast<size_t>(RB1) * (P / 2);   // mu plane
                         const int2 xl = *el, xm = *em;
