@@ -791,8 +791,9 @@ size_t pget_table_bytes(pget_geometry h, int id)
 pget_status pget_geometry_export(pget_geometry h, int id, void* dst, size_t bytes)
 {
     if (!h || !dst) return fail(PGET_ERR_INVALID_ARGUMENT, "NULL argument");
+    if (id < PGET_TABLE_ANGLES || id > PGET_TABLE_VAR_W) return fail(PGET_ERR_INVALID_ARGUMENT, "bad table id");
     const size_t need = pget_table_bytes(h, id);
-    if (need == 0) return fail(PGET_ERR_INVALID_ARGUMENT, "bad table id");
+    if (need == 0) return PGET_OK;   // an empty table (the model variant's when it is off)
     if (bytes < need) return fail(PGET_ERR_SHAPE, "destination too small");
     const Geometry& g = h->g;
     const double tl[3] = {g.h, g.delta, g.T};
