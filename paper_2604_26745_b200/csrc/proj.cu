@@ -300,6 +300,18 @@ struct SmpA {   // one sample of a ray in sweep A: its corners (prefetched) and 
     float fu, fv;
 };
 
+// number of samples a walk takes inside one band: i, i-1, ... while i' >= ilo and the sample row stays in
+// [r0, r1) (v_{i-k} = v - k dV; dV != 0 in the oriented frame) -- computed once per band so the sample
+// loop tests a counter instead of three bounds
+__device__ __forceinline__ int band_steps(int i, int ilo, int64_t v, int64_t dV, int r0, int r1)
+{
+    const int64_t num = dV > 0 ? v - (static_cast<int64_t>(r0) << 32)
+                               : ((static_cast<int64_t>(r1) << 32) - 1) - v;   // >= 0: v is inside
+    const int64_t k = num / (dV > 0 ? dV : -dV);                                  // further steps inside
+    const int64_t n = i - ilo + 1;
+    return static_cast<int>(k + 1 < n ? k + 1 : n);
+}
+
 // VAR (model variant N3, reading R-N3): cw is the lane's row [n_t] of (W_j(d_i), c_i); E_i = e^{-c_i A_i},
 // the forward / JVP sums carry W_j(d_i), the adjoint's G carries W c (G_c = sum W lam c E).
 template <int MODE, bool PAIRED, bool VAR = false>
@@ -311,6 +323,7 @@ __device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int
     using Cn = typename CornerT<TR::NF4>::T;
     const int iv0 = hi32(v);
     if (i < ilo || iv0 < r0 || iv0 >= r1) return;
+    int n = band_steps(i, ilo, v, dV, r0, r1);
     const Cn* img = reinterpret_cast<const Cn*>(sb);
     auto load = [&](SmpA<TR::NF4>& x, int64_t uu, int64_t vv, int ivv) {
         const int o = (ivv - r0) * P + hi32(uu);
@@ -325,7 +338,7 @@ __device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int
         const int i2 = i - 1;
         const int64_t u2 = u - dU, v2 = v - dV;
         const int iv2 = hi32(v2);
-        const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;
+        const bool nxt = --n != 0;
         if (nxt) load(nx, u2, v2, iv2);
         float lam, mu, dlam = 0.f, dmu = 0.f;
         if constexpr (TR::NF4) {
@@ -426,6 +439,7 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
 {
     int iv = hi32(v), iu = hi32(u);
     if (i < ilo || iv < r0 || iv >= r1) return;
+    int n = band_steps(i, ilo, v, dV, r0, r1);
     int o = (iv - r0) * P + iu;
     float2 q00 = img[o], q01 = img[o + 1], q10 = img[o + P], q11 = img[o + P + 1];
     float fu = frac23(u), fv = frac23(v);
@@ -445,7 +459,7 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
         const int i2 = i - 1;
         const int64_t u2 = u - dU, v2 = v - dV;
         const int iv2 = hi32(v2);
-        const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;
+        const bool nxt = --n != 0;
         float2 n00, n01, n10, n11;
         int o2 = o;
         if (nxt) {
@@ -1461,6 +1475,7 @@ __device__ __forceinline__ void walk_lin(const float2* __restrict__ img, int P, 
 {
     int iv = hi32(v), iu = hi32(u);
     if (i < ilo || iv < r0 || iv >= r1) return;
+    int n = band_steps(i, ilo, v, dV, r0, r1);
     int o = (iv - r0) * P + iu;
     float2 q00 = img[o], q01 = img[o + 1], q10 = img[o + P], q11 = img[o + P + 1];
     float fu = frac23(u), fv = frac23(v);
@@ -1469,7 +1484,7 @@ __device__ __forceinline__ void walk_lin(const float2* __restrict__ img, int P, 
         const int i2 = i - 1;
         const int64_t u2 = u - dU, v2 = v - dV;
         const int iv2 = hi32(v2);
-        const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;
+        const bool nxt = --n != 0;
         float2 n00, n01, n10, n11;
         int o2 = o;
         if (nxt) {
@@ -1579,38 +1594,14 @@ __device__ __forceinline__ void red_s32(uint32_t addr, int v)
 {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
-#ifndef PGET_GNB_MODE
-#define PGET_GNB_MODE 0   // experiments: bit 2 half-width entry stream (timing ablation), bit 3 L2 evict-first loads
-#endif
-__device__ __forceinline__ float4 ld_entry_ef(const float4* q, uint64_t pol)
-{
-    float4 r;
-    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
-                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(q), "l"(pol));
-    return r;
-}
 template <bool INTACC>
 __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0, int r1, int abase, int sP, int ilo,
                                          int64_t dU, int64_t dV, float wr, float wr1, int& i, int64_t& u, int64_t& v,
-                                         const float4*& ck, const float4* cend, float2 S, uint32_t planeB,
-                                         const float4* cbase = nullptr)
+                                         const float4*& ck, const float4* cend, float2 S, uint32_t planeB)
 {
-    [[maybe_unused]] uint64_t pol = 0;
-    if constexpr (PGET_GNB_MODE & 8) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    auto LD = [&](const float4* q) -> float4 {
-        if constexpr (PGET_GNB_MODE & 4) {   // timing ablation: half the bytes per entry (values wrong)
-            const float2 h = __ldg(reinterpret_cast<const float2*>(cbase) + (q - cbase));
-            return make_float4(h.x, h.y, 0.f, 0.f);
-        } else if constexpr (PGET_GNB_MODE & 8) {
-            return ld_entry_ef(q, pol);
-        } else {
-            return __ldg(q);
-        }
-    };
     const int iv0 = hi32(v);
     if (i < ilo || iv0 < r0 || iv0 >= r1) return;
-    int poff = -1;
-    float2 p00 = make_float2(0.f, 0.f), p01 = p00, p10 = p00, p11 = p00;
+    int n = band_steps(i, ilo, v, dV, r0, r1);
     const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(acc));
     auto rmw = [&](int off, float2 a, float2 b, float2 c, float2 d) {
         if constexpr (INTACC) {
@@ -1635,24 +1626,23 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
             pa[sP + 1] = make_float2(t11.x + d.x, t11.y + d.y);
         }
     };
-    const float4* p = ck;
-    float4 c0 = LD(p), c1 = LD(p + 32), c2 = LD(p + 64), c3 = LD(p + 96);
+    // the pending cell starts as the first sample's (valid address, zero sums): no first-time test
     int iv = iv0;
+    int poff = abase + (iv - r0) * sP + hi32(u);
+    const float2 z2 = make_float2(0.f, 0.f);
+    float2 p00 = z2, p01 = z2, p10 = z2, p11 = z2;
+    const float4* const p0 = ck;
+    int k = 0;   // entry row of the current sample, relative to p0
+    float4 c0 = __ldg(p0), c1 = __ldg(p0 + 32), c2 = __ldg(p0 + 64), c3 = __ldg(p0 + 96);
+    const float2 w2 = make_float2(wr, wr), w12 = make_float2(wr1, wr1);
     auto step = [&](float4& c) -> bool {
         const int aoff = abase + (iv - r0) * sP + hi32(u);
-        PGET_CHECK(hi32(u) >= 0 && hi32(u) + 1 < P && iv >= r0 && iv < r1 && p < cend);
+        PGET_CHECK(hi32(u) >= 0 && hi32(u) + 1 < P && iv >= r0 && iv < r1 && p0 + k * 32 < cend);
         const float fu = frac23(u), fv = frac23(v);
-        const int i2 = i - 1;
-        const int64_t u2 = u - dU, v2 = v - dV;
-        const int iv2 = hi32(v2);
-        const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;
-        const float2 av = make_float2(fmaf(wr, c.x, wr1 * c.z), fmaf(wr, c.y, wr1 * c.w));
-        if constexpr (PGET_GNB_MODE & 4)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const float2*>(cbase) + (p - cbase) + PGET_PF_DIST * 32));
-        else
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(p + PGET_PF_DIST * 32));
-        c = LD(p + 4 * 32);
-        p += 32;
+        const float2 av = __ffma2_rn(w2, make_float2(c.x, c.y), __fmul2_rn(w12, make_float2(c.z, c.w)));
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + ((k + PGET_PF_DIST) << 5)));
+        c = __ldg(p0 + ((k + 4) << 5));
+        ++k;
         const float2 tv = __fmul2_rn(av, make_float2(fv, fv));         // row j0+1
         const float2 bv = __ffma2_rn(tv, make_float2(-1.f, -1.f), av); // row j0
         const float2 c11 = __fmul2_rn(tv, make_float2(fu, fu));
@@ -1660,25 +1650,25 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
         const float2 c01 = __fmul2_rn(bv, make_float2(fu, fu));
         const float2 c00 = __ffma2_rn(c01, make_float2(-1.f, -1.f), bv);
         if (aoff != poff) {
-            if (poff >= 0 && (PGET_ABLATE != 1 || p00.x == 12345.f)) rmw(poff, p00, p01, p10, p11);   // ABLATE 1: no scatter
+            if (PGET_ABLATE != 1 || p00.x == 12345.f) rmw(poff, p00, p01, p10, p11);   // ABLATE 1: no scatter
             poff = aoff;
             p00 = c00; p01 = c01; p10 = c10; p11 = c11;
         } else {
-            p00.x += c00.x; p00.y += c00.y;
-            p01.x += c01.x; p01.y += c01.y;
-            p10.x += c10.x; p10.y += c10.y;
-            p11.x += c11.x; p11.y += c11.y;
+            p00 = __fadd2_rn(p00, c00);
+            p01 = __fadd2_rn(p01, c01);
+            p10 = __fadd2_rn(p10, c10);
+            p11 = __fadd2_rn(p11, c11);
         }
-        i = i2;
-        u = u2;
-        v = v2;
-        iv = iv2;
-        return nxt;
+        u -= dU;
+        v -= dV;
+        iv = hi32(v);
+        return --n != 0;
     };
     while (step(c0) && step(c1) && step(c2) && step(c3)) {
     }
     rmw(poff, p00, p01, p10, p11);
-    ck = p;
+    i -= k;
+    ck = p0 + (k << 5);
 }
 
 // per-unit lane setup shared by the three kernels: the lane's ray of comb group grp, its entry
@@ -1989,7 +1979,7 @@ __global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
                 const int abase = flip ? Rb * P : 0, sP = flip ? -P : P;
                 if (PGET_ABLATE != 3)   // 3: no walk
                     walk_gnb<INTACC>(wacc, P, r0, r1, abase, sP, ilo, dU, dV, wr, wr1, ii, uu, vv, cl, cend, S,
-                                     static_cast<uint32_t>(RB1 * P * 4), A.cache);
+                                     static_cast<uint32_t>(RB1 * P * 4));
                 __syncthreads();   // every warp ring complete
                 const bool last = j == ui.nb - 1;
                 const int carry = last ? -1 : (ui.dir > 0 ? r0 : r1);
