@@ -455,6 +455,9 @@ WS carve(const Geometry& g, int op, char* base)
                 w.gscale = reinterpret_cast<float*>(take(static_cast<size_t>(B) * S.ntab * 8 * sizeof(float)));
         }
     }
+    if ((op == PGET_OP_FORWARD || guard) && g.adj_seg && g.fwd_seg)   // the segmented forward's partials
+        w.segp = reinterpret_cast<float*>(take(static_cast<size_t>(g.sch[kSchedAdj].n_canon) * kSegFields *
+                                               g.R * sizeof(float)));
     if ((op == PGET_OP_JVP || guard) && g.adj_seg && g.jvp_seg)
         w.segpJ = reinterpret_cast<float*>(take(static_cast<size_t>(g.schJ.n_canon) * kSegFields * g.R * sizeof(float)));
     if (op == PGET_OP_GN_CG_STEP || op == PGET_OP_LM_SOLVE) {
@@ -1089,7 +1092,7 @@ pget_status pget_forward(pget_geometry h, const float* lam, const float* mu, flo
     const Geometry& g = h->g;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if ((st = pack2(g, w, lam, mu, nullptr, nullptr, nullptr, nullptr, s))) return st;
-    return proj_out(g, w, MODE_FWD, y, nullptr, s);   // fused: faster standalone on configs 2, 3, 5
+    return fwd_out(g, w, y, s);   // the warp-specialised segmented phase A + fp64 combine (fused: variant only)
 }
 
 pget_status pget_jvp(pget_geometry h, const float* lam, const float* mu, const float* dlam, const float* dmu,
@@ -1426,7 +1429,7 @@ pget_status pget_safeguard(pget_geometry h, const float* lam, const float* mu, c
     CK(cudaGetLastError());
     // f(u~)
     if ((st = pack2(g, w, cand_lam, cand_mu, nullptr, nullptr, nullptr, nullptr, s))) return st;
-    if ((st = proj_out(g, w, MODE_FWD, w.ysino, nullptr, s))) return st;
+    if ((st = fwd_out(g, w, w.ysino, s))) return st;
     residual_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, y_meas, P[10], nsper); note();
     regsq_kernel<<<vg, kVecThreads, 0, s>>>(cand_lam, cand_mu, P[11], N); note();
     // priors (pget_set_prior): the rows sqrt(a1) P1 lam, sqrt(a2) P2 mu of F~ in f, m_k(s~), m_k(s_k), f(u~)

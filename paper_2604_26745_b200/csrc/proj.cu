@@ -307,7 +307,12 @@ __device__ __forceinline__ int band_steps(int i, int ilo, int64_t v, int64_t dV,
 {
     const int64_t num = dV > 0 ? v - (static_cast<int64_t>(r0) << 32)
                                : ((static_cast<int64_t>(r1) << 32) - 1) - v;   // >= 0: v is inside
-    const int64_t k = num / (dV > 0 ? dV : -dV);                                  // further steps inside
+    const int64_t adV = dV > 0 ? dV : -dV;
+    // further steps inside = floor(num / |dV|): a double quotient (both exact below 2^53), fixed up
+    // exactly (a 64-bit integer division is a long subroutine, and a band is only tens of samples)
+    int64_t k = static_cast<int64_t>(__ddiv_rz(static_cast<double>(num), static_cast<double>(adV)));
+    if ((k + 1) * adV <= num) ++k;
+    else if (k * adV > num) --k;
     const int64_t n = i - ilo + 1;
     return static_cast<int>(k + 1 < n ? k + 1 : n);
 }
@@ -439,7 +444,6 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
 {
     int iv = hi32(v), iu = hi32(u);
     if (i < ilo || iv < r0 || iv >= r1) return;
-    int n = band_steps(i, ilo, v, dV, r0, r1);
     int o = (iv - r0) * P + iu;
     float2 q00 = img[o], q01 = img[o + 1], q10 = img[o + P], q11 = img[o + P + 1];
     float fu = frac23(u), fv = frac23(v);
@@ -459,7 +463,7 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
         const int i2 = i - 1;
         const int64_t u2 = u - dU, v2 = v - dV;
         const int iv2 = hi32(v2);
-        const bool nxt = --n != 0;
+        const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;   // sweep-B bands are a few rows: no band_steps
         float2 n00, n01, n10, n11;
         int o2 = o;
         if (nxt) {
@@ -1475,7 +1479,6 @@ __device__ __forceinline__ void walk_lin(const float2* __restrict__ img, int P, 
 {
     int iv = hi32(v), iu = hi32(u);
     if (i < ilo || iv < r0 || iv >= r1) return;
-    int n = band_steps(i, ilo, v, dV, r0, r1);
     int o = (iv - r0) * P + iu;
     float2 q00 = img[o], q01 = img[o + 1], q10 = img[o + P], q11 = img[o + P + 1];
     float fu = frac23(u), fv = frac23(v);
@@ -1484,7 +1487,7 @@ __device__ __forceinline__ void walk_lin(const float2* __restrict__ img, int P, 
         const int i2 = i - 1;
         const int64_t u2 = u - dU, v2 = v - dV;
         const int iv2 = hi32(v2);
-        const bool nxt = --n != 0;
+        const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;   // sweep-B bands are a few rows: no band_steps
         float2 n00, n01, n10, n11;
         int o2 = o;
         if (nxt) {
