@@ -229,7 +229,7 @@ def roofline_ncu(cid, dom):
         return None
 
 
-def measure_config(pg, P, cid, flush, sm_mhz, reps=5):
+def measure_config(pg, P, cid, flush, sm_mhz, reps=5, **desc_over):
     """Per-config block (not the headline value): forward / JVP / VJP nominal ray-samples/s and ms per
     LM iteration (median over reps of CUDA-event timings on the current stream, L2 flushed before each
     op), the projector launches' algorithmic roofline fractions (bytes per traced sample of
@@ -237,7 +237,7 @@ def measure_config(pg, P, cid, flush, sm_mhz, reps=5):
     batched case) the HBM GB/s of the operations' algorithmic bytes (inputs read + outputs written)."""
     import torch
     cfg = P.CONFIGS[cid]
-    gd = P.geometry_desc(cid)
+    gd = P.geometry_desc(cid, **desc_over)
     g = pg.Geometry(gd)
     nominal, traced, traced_j = (g.info[k] for k in ("n_samples_nominal", "n_samples_traced", "n_samples_traced_jvp"))
     dev = lambda x: torch.from_numpy(np.ascontiguousarray(x, np.float32)).cuda()
@@ -298,7 +298,8 @@ def measure_config(pg, P, cid, flush, sm_mhz, reps=5):
         kern[mode] = {"launch_ms": lms, "alg_bytes_per_traced_sample": ALG_BYTES[mode], "traced_samples": units,
                       "achieved_GBps": ach / 1e9, "frac": ach / peak}
     out = {
-        "workload": f"{cfg.lattice} N={cfg.n_px} angles={cfg.n_angles} J={cfg.n_subrays} B={cfg.batch}",
+        "workload": f"{cfg.lattice} N={cfg.n_px} angles={cfg.n_angles} J={cfg.n_subrays} B={cfg.batch}"
+                    + "".join(f" {k}={v}" for k, v in desc_over.items()),
         "nominal_samples_per_pass": nominal, "traced_samples_per_pass": traced, "traced_samples_jvp": traced_j,
         "forward_ms": ms["forward"], "jvp_ms": ms["jvp"], "vjp_ms": ms["vjp"], "lm_ms": ms["lm"],
         "forward_samples_per_s": nominal / (ms["forward"] * 1e-3),
@@ -537,6 +538,12 @@ def main():
         per_config = {}
         for cid in (1, 2, 3, 4, 5):
             per_config[f"config {cid}"] = measure_config(pg, P, cid, flush, sm_mhz)
+            torch.cuda.empty_cache()
+        # the paper's own detector geometry: the banks interleaved by half a pitch, where
+        # neither the duplicate angle-banks nor the line pairing apply (every nominal sample is traced)
+        for cid in (2, 4):
+            per_config[f"config {cid} interleaved banks"] = measure_config(pg, P, cid, flush, sm_mhz,
+                                                                           bank1_shift=0.5)
             torch.cuda.empty_cache()
 
     if rank == 0:

@@ -41,6 +41,8 @@
  * pget_last_error_message() (thread-local).  Kernel launch failures return
  * PGET_ERR_CUDA.  No C++ exception crosses this interface; nothing aborts.
  *
+ * Tracing: every compute entry point is an NVTX range named after it (Nsight Systems, ncu --nvtx).
+ *
  * Threading: a handle is immutable after creation; concurrent calls on
  * different streams are safe when their workspaces and outputs differ.
  */
@@ -318,6 +320,12 @@ pget_status pget_workspace_region(pget_geometry g, int op, int region, size_t* o
  * handles (device < 0).  PGET_OK or PGET_ERR_INVALID_ARGUMENT with the violated rule in
  * pget_last_error_message(). */
 pget_status pget_schedule_check(pget_geometry g);
+
+/* Failure detection: scans n floats of device array x for NaN / infinity on `stream`,
+ * then synchronises it.  PGET_OK if all are finite, PGET_ERR_NOT_FINITE otherwise (for example the
+ * output of a call fed non-finite inputs).  flag_dev: one device int32 of scratch (caller-owned).
+ * A diagnostic: unlike the compute calls it waits for the stream. */
+pget_status pget_check_finite(const float* x, size_t n, int32_t* flag_dev, pget_stream_t stream);
 
 /* Tracing.  Between pget_profile_begin and pget_profile_end every kernel the library
  * launches (on any stream, from any thread) is counted, and each projector launch is

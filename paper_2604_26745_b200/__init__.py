@@ -121,11 +121,12 @@ def lib():
         L.pget_schedule_check.argtypes = [P]
         L.pget_workspace_region.argtypes = [P, C.c_int, C.c_int, C.POINTER(S), C.POINTER(S)]
         L.pget_set_prior.argtypes = [P, C.POINTER(Prior)]
+        L.pget_check_finite.argtypes = [P, S, P, P]
         L.pget_profile_begin.argtypes = [C.c_int32]
         L.pget_profile_end.argtypes = [P, P, P]
         for n in ("pget_profile_begin", "pget_profile_end", "pget_geometry_create", "pget_geometry_destroy", "pget_geometry_info", "pget_geometry_export",
                   "pget_forward", "pget_jvp", "pget_vjp", "pget_gn_apply", "pget_gn_cg_step", "pget_safeguard", "pget_lm_solve", "pget_schedule_check", "pget_set_prior",
-                  "pget_workspace_region"):
+                  "pget_workspace_region", "pget_check_finite"):
             getattr(L, n).restype = C.c_int
         _lib = L
     return _lib
@@ -340,6 +341,16 @@ def gn_cg_step(g: Geometry, lam, mu, y_meas, alpha, beta, n_cg, flags=PGET_GN_EV
                                  int(flags), _ptr(s_lam), _ptr(s_mu), _ptr(stats), _ptr(ws), ws.numel(),
                                  _stream(stream)), "pget_gn_cg_step")
     return s_lam, s_mu, stats
+
+
+def check_finite(t, stream=None):
+    """Raise RuntimeError (PGET_ERR_NOT_FINITE) if the float32 CUDA tensor t holds a NaN or an infinity
+    (pget_check_finite; synchronises the stream)."""
+    import torch
+    if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()):
+        raise TypeError("check_finite: expected a contiguous float32 CUDA tensor")
+    flag = torch.empty(1, dtype=torch.int32, device=t.device)
+    _check(lib().pget_check_finite(_ptr(t), t.numel(), _ptr(flag), _stream(stream)), "pget_check_finite")
 
 
 def profile_begin(max_launches: int = 4096):

@@ -18,6 +18,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.h"
 #include "kernels.cuh"
 
@@ -26,6 +28,15 @@ using namespace pget;
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range around every public entry point (SURVEY.md §5 tracing): visible in Nsight Systems / ncu
+// --nvtx; a no-op without an attached tool (NVTX v3 is header-only)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // ---- tracing (pget_profile_begin / pget_profile_end)
 struct ProfRec {
@@ -585,6 +596,7 @@ const char* pget_last_error_message(void) { return g_err.c_str(); }
 
 pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pget_geometry* out)
 {
+    NvtxRange nvtx_("pget_geometry_create");
     if (!out) return fail(PGET_ERR_INVALID_ARGUMENT, "out is NULL");
     *out = nullptr;
     pget_geometry h = new (std::nothrow) pget_geometry_s;
@@ -826,7 +838,7 @@ static pget_status pack2(const Geometry& g, const WS& w, const float* lam, const
                          const float* smu, float* ul, float* um, cudaStream_t s, const BoxK* box = nullptr)
 {
     const size_t img = static_cast<size_t>(g.desc.batch) * g.P * g.P;
-    pack2_kernel<<<vec_grid(img), kVecThreads, 0, s>>>(lam, mu, slam, smu, w.img2[0], w.img2[1], ul, um,
+    launch_k(pack2_kernel, vec_grid(img), kVecThreads, 0, s, lam, mu, slam, smu, w.img2[0], w.img2[1], ul, um,
                                                       g.desc.n_px, g.P, g.desc.batch, box ? 1 : 0,
                                                       box ? *box : BoxK{make_float4(0.f, 0.f, 0.f, 0.f), 0.f}); note();
     CK(cudaGetLastError());
@@ -837,7 +849,7 @@ static pget_status pack4(const Geometry& g, const WS& w, const float* lam, const
                          const float* dm, cudaStream_t s)
 {
     const size_t img = static_cast<size_t>(g.desc.batch) * g.P * g.P;
-    pack4_kernel<<<vec_grid(img), kVecThreads, 0, s>>>(lam, mu, dl, dm, w.img4[0], w.img4[1], g.desc.n_px, g.P,
+    launch_k(pack4_kernel, vec_grid(img), kVecThreads, 0, s, lam, mu, dl, dm, w.img4[0], w.img4[1], g.desc.n_px, g.P,
                                                       g.desc.batch); note();
     CK(cudaGetLastError());
     return PGET_OK;
@@ -870,7 +882,7 @@ static pget_status proj_adjoint(const Geometry& g, const WS& w, int mode, const 
     if (st) return st;
     const int N = g.desc.n_px;
     const dim3 grid((N + 31) / 32, (N + 31) / 32, g.desc.batch * c.G);
-    reduce_slots_kernel<<<grid, dim3(32, 8), 0, s>>>(w.slots, w.gacc, N, slot_pitch(g), g.desc.batch, c.G,
+    launch_k(reduce_slots_kernel, grid, dim3(32, 8), 0, s, w.slots, w.gacc, N, slot_pitch(g), g.desc.batch, c.G,
                                                     g.sch[kSchedAdj].d_red_off, g.sch[kSchedAdj].d_red_slot,
                                                     g.sch[kSchedAdj].d_slot_lo, g.sch[kSchedAdj].d_slot_hi); note();
     CK(cudaGetLastError());
@@ -993,7 +1005,7 @@ static pget_status gnc_product(const Geometry& g, const WS& w, const float* lam,
     const ProjCfg pc = proj_cfg(g, MODE_GN);
     const int N = g.desc.n_px;
     const dim3 grid((N + 31) / 32, (N + 31) / 32, g.desc.batch * pc.G);
-    reduce_slots_kernel<<<grid, dim3(32, 8), 0, s>>>(w.slots, w.gacc, N, slot_pitch(g), g.desc.batch, pc.G,
+    launch_k(reduce_slots_kernel, grid, dim3(32, 8), 0, s, w.slots, w.gacc, N, slot_pitch(g), g.desc.batch, pc.G,
                                                     g.sch[kSchedAdj].d_red_off, g.sch[kSchedAdj].d_red_slot,
                                                     g.sch[kSchedAdj].d_slot_lo, g.sch[kSchedAdj].d_slot_hi); note();
     CK(cudaGetLastError());
@@ -1085,6 +1097,7 @@ static pget_status jvp_out(const Geometry& g, const WS& w, float* y, float* dy, 
 pget_status pget_forward(pget_geometry h, const float* lam, const float* mu, float* y, void* ws, size_t ws_bytes,
                          pget_stream_t stream)
 {
+    NvtxRange nvtx_("pget_forward");
     WS w;
     pget_status st = check_common(h, PGET_OP_FORWARD, ws, ws_bytes, &w);
     if (st) return st;
@@ -1098,6 +1111,7 @@ pget_status pget_forward(pget_geometry h, const float* lam, const float* mu, flo
 pget_status pget_jvp(pget_geometry h, const float* lam, const float* mu, const float* dlam, const float* dmu,
                      float* y, float* dy, void* ws, size_t ws_bytes, pget_stream_t stream)
 {
+    NvtxRange nvtx_("pget_jvp");
     WS w;
     pget_status st = check_common(h, PGET_OP_JVP, ws, ws_bytes, &w);
     if (st) return st;
@@ -1112,6 +1126,7 @@ pget_status pget_jvp(pget_geometry h, const float* lam, const float* mu, const f
 pget_status pget_vjp(pget_geometry h, const float* lam, const float* mu, const float* wv, float* g_lam, float* g_mu,
                      void* ws, size_t ws_bytes, pget_stream_t stream)
 {
+    NvtxRange nvtx_("pget_vjp");
     WS w;
     pget_status st = check_common(h, PGET_OP_VJP, ws, ws_bytes, &w);
     if (st) return st;
@@ -1121,9 +1136,9 @@ pget_status pget_vjp(pget_geometry h, const float* lam, const float* mu, const f
     const int N = g.desc.n_px, B = g.desc.batch;
     if ((st = pack2(g, w, lam, mu, nullptr, nullptr, nullptr, nullptr, s))) return st;
     if ((st = proj_adjoint(g, w, MODE_VJP, wv, s))) return st;
-    finish_kernel<<<dim3(vec_grid(static_cast<size_t>(N) * N), B), kVecThreads, 0, s>>>(
+    launch_k(finish_kernel, dim3(vec_grid(static_cast<size_t>(N) * N), B), kVecThreads, 0, s, 
         w.gacc, proj_cfg(g, MODE_VJP).G, nullptr, nullptr, 0.f, 0.f, 1.f, g_lam, g_mu, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-        nullptr, nullptr, nullptr, N, PriorArgs{}); note();
+        nullptr, nullptr, nullptr, N, PriorArgs{}, nullptr); note();
     CK(cudaGetLastError());
     return PGET_OK;
 }
@@ -1132,6 +1147,7 @@ pget_status pget_gn_apply(pget_geometry h, const float* lam, const float* mu, co
                           float alpha, float beta, float* q_lam, float* q_mu, void* ws, size_t ws_bytes,
                           pget_stream_t stream)
 {
+    NvtxRange nvtx_("pget_gn_apply");
     WS w;
     pget_status st = check_common(h, PGET_OP_GN_APPLY, ws, ws_bytes, &w);
     if (st) return st;
@@ -1161,9 +1177,9 @@ pget_status pget_gn_apply(pget_geometry h, const float* lam, const float* mu, co
         if ((st = pack4(g, w, lam, mu, p_lam, p_mu, s))) return st;
         if ((st = proj_adjoint(g, w, MODE_GN, nullptr, s))) return st;
     }
-    finish_kernel<<<dim3(vec_grid(static_cast<size_t>(N) * N), B), kVecThreads, 0, s>>>(
+    launch_k(finish_kernel, dim3(vec_grid(static_cast<size_t>(N) * N), B), kVecThreads, 0, s, 
         w.gacc, proj_cfg(g, MODE_GN).G, p_lam, p_mu, alpha, beta, 1.f, q_lam, q_mu, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-        nullptr, nullptr, nullptr, N, prior_args(g, 1.f)); note();
+        nullptr, nullptr, nullptr, N, prior_args(g, 1.f), nullptr); note();
     CK(cudaGetLastError());
     return PGET_OK;
 }
@@ -1193,33 +1209,33 @@ static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const f
     // 1-2: r = F(u) - y, 1/2||r||^2, ||Lu||^2   (u packed once for the whole iteration)
     if ((st = pack2(g, w, lam, mu, nullptr, nullptr, nullptr, nullptr, s))) return st;
     if ((st = fwd_out(g, w, w.ysino, s))) return st;
-    residual_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, y_meas, P[0], nsper); note();
-    regsq_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, P[1], N); note();
-    if (has_prior) priorsq_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, pr, Pp, N); note();
+    launch_k(residual_kernel, vg, kVecThreads, 0, s, w.ysino, y_meas, P[0], nsper); note();
+    launch_k(regsq_kernel, vg, kVecThreads, 0, s, lam, mu, P[1], N); note();
+    if (has_prior) launch_k(priorsq_kernel, vg, kVecThreads, 0, s, lam, mu, pr, Pp, N); note();
     CK(cudaGetLastError());
     // 3: b = -(J^T r + alpha L^T L u (+ P^T P u)); z = p = b; s = 0; ||b||^2
     const bool cached = g.adj_seg && g.gn_cached;
     // the gradient VJP also writes the GN Jacobian-entry cache (fused cache build)
     // F(u) above was the segmented forward: its phase-A partials of u are the VJP's phase A
     if ((st = proj_adjoint(g, w, MODE_VJP, w.ysino, s, cached && n_cg > 0, g.adj_seg && g.fwd_seg))) return st;
-    finish_kernel<<<vg, kVecThreads, 0, s>>>(w.gacc, Gv, lam, mu, alpha, 0.f, -1.f, w.bl, w.bm, w.bl, w.bm, P[2], w.zl,
-                                            w.zm, w.pl, w.pm, s_lam, s_mu, N, pr); note();
+    launch_k(finish_kernel, vg, kVecThreads, 0, s, w.gacc, Gv, lam, mu, alpha, 0.f, -1.f, w.bl, w.bm, w.bl, w.bm, P[2], w.zl,
+                                            w.zm, w.pl, w.pm, s_lam, s_mu, N, pr, nullptr); note();
     CK(cudaGetLastError());
-    scalar_kernel<<<sgrid, 128, 0, s>>>(SC_INIT, 0, P[0], P[1], P[2], kNblk, w.cg, stats, B, alpha, beta, betav, Pp); note();
+    launch_k(scalar_kernel, sgrid, 128, 0, s, SC_INIT, 0, P[0], P[1], P[2], kNblk, w.cg, stats, B, alpha, beta, betav, Pp); note();
     CK(cudaGetLastError());
 
     // 5: CG
     if (sgp && box) {   // 5': SGP (O11) instead of CG: s stays inside the box
         const size_t nimg = static_cast<size_t>(B) * n2;
-        sgp_init_kernel<<<vec_grid(nimg), kVecThreads, 0, s>>>(w.bl, w.bm, w.zl, w.zm, w.cg, n2, B); note();
+        launch_k(sgp_init_kernel, vec_grid(nimg), kVecThreads, 0, s, w.bl, w.bm, w.zl, w.zm, w.cg, n2, B); note();
         CK(cudaGetLastError());
         for (int k = 0; k <= n_cg; ++k) {
             // d = P(u + s - a g) - u - s into (pl, pm); the last pass only reports ||d||
-            sgp_dir_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, s_lam, s_mu, w.zl, w.zm, w.cg, *box, w.pl, w.pm, P[3],
+            launch_k(sgp_dir_kernel, vg, kVecThreads, 0, s, lam, mu, s_lam, s_mu, w.zl, w.zm, w.cg, *box, w.pl, w.pm, P[3],
                                                       P[4], n2); note();
             CK(cudaGetLastError());
             if (k == n_cg) {
-                sgp_scalar_kernel<<<sgrid, 128, 0, s>>>(k, 1, P[3], P[4], nullptr, nullptr, kNblk, w.cg, stats, B); note();
+                launch_k(sgp_scalar_kernel, sgrid, 128, 0, s, k, 1, P[3], P[4], nullptr, nullptr, kNblk, w.cg, stats, B); note();
                 break;
             }
             if (cached) {   // q = H d
@@ -1228,12 +1244,12 @@ static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const f
                 if ((st = pack4(g, w, lam, mu, w.pl, w.pm, s))) return st;
                 if ((st = proj_adjoint(g, w, MODE_GN, nullptr, s))) return st;
             }
-            finish_kernel<<<vg, kVecThreads, 0, s>>>(w.gacc, Gg, w.pl, w.pm, alpha, beta, 1.f, w.ql, w.qm, w.pl, w.pm,
+            launch_k(finish_kernel, vg, kVecThreads, 0, s, w.gacc, Gg, w.pl, w.pm, alpha, beta, 1.f, w.ql, w.qm, w.pl, w.pm,
                                                     P[5], nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, N, pr,
                                                     betav); note();
-            dot2_kernel<<<vg, kVecThreads, 0, s>>>(w.ql, w.qm, w.ql, w.qm, P[6], n2); note();
-            sgp_scalar_kernel<<<sgrid, 128, 0, s>>>(k, 0, P[3], P[4], P[5], P[6], kNblk, w.cg, stats, B); note();
-            sgp_update_kernel<<<vg, kVecThreads, 0, s>>>(s_lam, s_mu, w.zl, w.zm, w.pl, w.pm, w.ql, w.qm, w.cg, n2); note();
+            launch_k(dot2_kernel, vg, kVecThreads, 0, s, w.ql, w.qm, w.ql, w.qm, P[6], n2); note();
+            launch_k(sgp_scalar_kernel, sgrid, 128, 0, s, k, 0, P[3], P[4], P[5], P[6], kNblk, w.cg, stats, B); note();
+            launch_k(sgp_update_kernel, vg, kVecThreads, 0, s, s_lam, s_mu, w.zl, w.zm, w.pl, w.pm, w.ql, w.qm, w.cg, n2); note();
             CK(cudaGetLastError());
         }
     }
@@ -1269,7 +1285,7 @@ static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const f
     // (N1) the step actually taken inside the box: s <- clamp(u + s) - u
     if (box) {
         const size_t n = static_cast<size_t>(B) * n2;
-        project_step_kernel<<<vec_grid(n), kVecThreads, 0, s>>>(lam, mu, s_lam, s_mu, n, *box); note();
+        launch_k(project_step_kernel, vec_grid(n), kVecThreads, 0, s, lam, mu, s_lam, s_mu, n, *box); note();
         CK(cudaGetLastError());
     }
     // 6: pred = <b,s> - 1/2(||Js||^2 + alpha ||Ls||^2); ||Js||^2 from the paired GN-mode phase A of
@@ -1297,21 +1313,21 @@ static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const f
         note();
     } else {
         if ((st = proj_out(g, w, MODE_JVP, nullptr, w.dysino, s))) return st;
-        sumsq_kernel<<<vg, kVecThreads, 0, s>>>(w.dysino, P[5], nsper); note();
+        launch_k(sumsq_kernel, vg, kVecThreads, 0, s, w.dysino, P[5], nsper); note();
     }
-    regsq_kernel<<<vg, kVecThreads, 0, s>>>(s_lam, s_mu, P[6], N); note();
-    if (has_prior) priorsq_kernel<<<vg, kVecThreads, 0, s>>>(s_lam, s_mu, pr, Pp, N); note();
-    dot2_kernel<<<vg, kVecThreads, 0, s>>>(w.bl, w.bm, s_lam, s_mu, P[7], n2); note();
-    scalar_kernel<<<sgrid, 128, 0, s>>>(SC_PRED, 0, P[5], P[6], P[7], kNblk, w.cg, stats, B, alpha, beta, betav, Pp); note();
+    launch_k(regsq_kernel, vg, kVecThreads, 0, s, s_lam, s_mu, P[6], N); note();
+    if (has_prior) launch_k(priorsq_kernel, vg, kVecThreads, 0, s, s_lam, s_mu, pr, Pp, N); note();
+    launch_k(dot2_kernel, vg, kVecThreads, 0, s, w.bl, w.bm, s_lam, s_mu, P[7], n2); note();
+    launch_k(scalar_kernel, sgrid, 128, 0, s, SC_PRED, 0, P[5], P[6], P[7], kNblk, w.cg, stats, B, alpha, beta, betav, Pp); note();
     CK(cudaGetLastError());
     // 7-8: f(u+s), rho, accept, beta_next
     if (flags & PGET_GN_EVAL_TRIAL) {
         if ((st = pack2(g, w, lam, mu, s_lam, s_mu, w.ul, w.um, s, box))) return st;
         if ((st = fwd_out(g, w, w.ysino, s))) return st;
-        residual_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, y_meas, P[0], nsper); note();
-        regsq_kernel<<<vg, kVecThreads, 0, s>>>(w.ul, w.um, P[1], N); note();
-        if (has_prior) priorsq_kernel<<<vg, kVecThreads, 0, s>>>(w.ul, w.um, pr, Pp, N); note();
-        scalar_kernel<<<sgrid, 128, 0, s>>>(SC_TRIAL, 0, P[0], P[1], nullptr, kNblk, w.cg, stats, B, alpha, beta, betav, Pp); note();
+        launch_k(residual_kernel, vg, kVecThreads, 0, s, w.ysino, y_meas, P[0], nsper); note();
+        launch_k(regsq_kernel, vg, kVecThreads, 0, s, w.ul, w.um, P[1], N); note();
+        if (has_prior) launch_k(priorsq_kernel, vg, kVecThreads, 0, s, w.ul, w.um, pr, Pp, N); note();
+        launch_k(scalar_kernel, sgrid, 128, 0, s, SC_TRIAL, 0, P[0], P[1], nullptr, kNblk, w.cg, stats, B, alpha, beta, betav, Pp); note();
         CK(cudaGetLastError());
     }
     return PGET_OK;
@@ -1321,6 +1337,7 @@ pget_status pget_gn_cg_step(pget_geometry h, const float* lam, const float* mu, 
                             float beta, int32_t n_cg, uint32_t flags, float* s_lam, float* s_mu,
                             pget_gn_stats* stats, void* ws, size_t ws_bytes, pget_stream_t stream)
 {
+    NvtxRange nvtx_("pget_gn_cg_step");
     WS w;
     pget_status st = check_common(h, PGET_OP_GN_CG_STEP, ws, ws_bytes, &w);
     if (st) return st;
@@ -1337,6 +1354,7 @@ pget_status pget_gn_cg_step(pget_geometry h, const float* lam, const float* mu, 
 pget_status pget_lm_solve(pget_geometry h, float* lam, float* mu, const float* y_meas, const pget_lm_params* prm,
                           pget_gn_stats* stats, void* ws, size_t ws_bytes, pget_stream_t stream)
 {
+    NvtxRange nvtx_("pget_lm_solve");
     WS w;
     pget_status st = check_common(h, PGET_OP_LM_SOLVE, ws, ws_bytes, &w);
     if (st) return st;
@@ -1362,11 +1380,11 @@ pget_status pget_lm_solve(pget_geometry h, float* lam, float* mu, const float* y
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int N = g.desc.n_px, B = g.desc.batch, n2 = N * N;
     const BoxK box{make_float4(p.lam_lo, p.lam_hi, p.mu_lo, p.mu_hi), p.lam_per_mu};
-    fill_kernel<<<(B + 127) / 128, 128, 0, s>>>(w.beta, p.beta0, B); note();
+    launch_k(fill_kernel, (B + 127) / 128, 128, 0, s, w.beta, p.beta0, B); note();
     CK(cudaGetLastError());
     if (use_box) {   // the initial guess itself is projected onto the box
         const size_t n = static_cast<size_t>(B) * n2;
-        clamp_kernel<<<vec_grid(n), kVecThreads, 0, s>>>(lam, mu, n, box); note();
+        launch_k(clamp_kernel, vec_grid(n), kVecThreads, 0, s, lam, mu, n, box); note();
         CK(cudaGetLastError());
     }
     double alpha = p.alpha0, pscale = 1.0;
@@ -1380,7 +1398,7 @@ pget_status pget_lm_solve(pget_geometry h, float* lam, float* mu, const float* y
                              PGET_GN_EVAL_TRIAL, w.sl, w.sm, sk, use_box ? &box : nullptr, s,
                              static_cast<float>(pscale), use_sgp)))
             return st;
-        lm_update_kernel<<<dim3(vec_grid(n2), B), kVecThreads, 0, s>>>(lam, mu, w.ul, w.um, sk, w.beta, n2); note();
+        launch_k(lm_update_kernel, dim3(vec_grid(n2), B), kVecThreads, 0, s, lam, mu, w.ul, w.um, sk, w.beta, n2); note();
         CK(cudaGetLastError());
     }
     return PGET_OK;
@@ -1392,6 +1410,7 @@ pget_status pget_safeguard(pget_geometry h, const float* lam, const float* mu, c
                            float* u_next_lam, float* u_next_mu, pget_safeguard_stats* stats, void* ws,
                            size_t ws_bytes, pget_stream_t stream)
 {
+    NvtxRange nvtx_("pget_safeguard");
     WS w;
     pget_status st = check_common(h, PGET_OP_SAFEGUARD, ws, ws_bytes, &w);
     if (st) return st;
@@ -1412,37 +1431,37 @@ pget_status pget_safeguard(pget_geometry h, const float* lam, const float* mu, c
     for (int k = 0; k < 18; ++k) P[k] = w.part + static_cast<size_t>(k) * B * kNblk;
     const size_t nimg = static_cast<size_t>(B) * n2;
     // s~ = u~ - u;  F(u) and J s~ in one JVP launch
-    diff2_kernel<<<vec_grid(nimg), kVecThreads, 0, s>>>(cand_lam, cand_mu, lam, mu, w.zl, w.zm, nimg); note();
+    launch_k(diff2_kernel, vec_grid(nimg), kVecThreads, 0, s, cand_lam, cand_mu, lam, mu, w.zl, w.zm, nimg); note();
     CK(cudaGetLastError());
     if ((st = pack4(g, w, lam, mu, w.zl, w.zm, s))) return st;
     if ((st = jvp_out(g, w, w.ysino, w.dysino, s))) return st;
-    residual_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, y_meas, P[0], nsper); note();
-    regsq_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, P[1], N); note();
-    dotsq_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, w.dysino, P[2], P[3], nsper); note();
-    lapdot_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, w.zl, w.zm, P[4], P[5], N); note();
+    launch_k(residual_kernel, vg, kVecThreads, 0, s, w.ysino, y_meas, P[0], nsper); note();
+    launch_k(regsq_kernel, vg, kVecThreads, 0, s, lam, mu, P[1], N); note();
+    launch_k(dotsq_kernel, vg, kVecThreads, 0, s, w.ysino, w.dysino, P[2], P[3], nsper); note();
+    launch_k(lapdot_kernel, vg, kVecThreads, 0, s, lam, mu, w.zl, w.zm, P[4], P[5], N); note();
     CK(cudaGetLastError());
     // J s_k
     if ((st = pack4(g, w, lam, mu, s_lam, s_mu, s))) return st;
     if ((st = jvp_out(g, w, nullptr, w.dysino, s))) return st;
-    dotsq_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, w.dysino, P[6], P[7], nsper); note();
-    lapdot_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, s_lam, s_mu, P[8], P[9], N); note();
+    launch_k(dotsq_kernel, vg, kVecThreads, 0, s, w.ysino, w.dysino, P[6], P[7], nsper); note();
+    launch_k(lapdot_kernel, vg, kVecThreads, 0, s, lam, mu, s_lam, s_mu, P[8], P[9], N); note();
     CK(cudaGetLastError());
     // f(u~)
     if ((st = pack2(g, w, cand_lam, cand_mu, nullptr, nullptr, nullptr, nullptr, s))) return st;
     if ((st = fwd_out(g, w, w.ysino, s))) return st;
-    residual_kernel<<<vg, kVecThreads, 0, s>>>(w.ysino, y_meas, P[10], nsper); note();
-    regsq_kernel<<<vg, kVecThreads, 0, s>>>(cand_lam, cand_mu, P[11], N); note();
+    launch_k(residual_kernel, vg, kVecThreads, 0, s, w.ysino, y_meas, P[10], nsper); note();
+    launch_k(regsq_kernel, vg, kVecThreads, 0, s, cand_lam, cand_mu, P[11], N); note();
     // priors (pget_set_prior): the rows sqrt(a1) P1 lam, sqrt(a2) P2 mu of F~ in f, m_k(s~), m_k(s_k), f(u~)
     const PriorArgs pr = prior_args(g, 1.f);
     const bool has_prior = pr.m1 || pr.m2;
     if (has_prior) {
-        priorsq_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, pr, P[12], N); note();
-        priordot_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, w.zl, w.zm, pr, P[13], P[14], N); note();
-        priordot_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, s_lam, s_mu, pr, P[15], P[16], N); note();
-        priorsq_kernel<<<vg, kVecThreads, 0, s>>>(cand_lam, cand_mu, pr, P[17], N); note();
+        launch_k(priorsq_kernel, vg, kVecThreads, 0, s, lam, mu, pr, P[12], N); note();
+        launch_k(priordot_kernel, vg, kVecThreads, 0, s, lam, mu, w.zl, w.zm, pr, P[13], P[14], N); note();
+        launch_k(priordot_kernel, vg, kVecThreads, 0, s, lam, mu, s_lam, s_mu, pr, P[15], P[16], N); note();
+        launch_k(priorsq_kernel, vg, kVecThreads, 0, s, cand_lam, cand_mu, pr, P[17], N); note();
     }
-    guard_scalar_kernel<<<(B + 127) / 128, 128, 0, s>>>(w.part, kNblk, B, alpha, kappa, stats, has_prior ? 1 : 0); note();
-    guard_select_kernel<<<vg, kVecThreads, 0, s>>>(lam, mu, s_lam, s_mu, cand_lam, cand_mu, stats, u_next_lam,
+    launch_k(guard_scalar_kernel, (B + 127) / 128, 128, 0, s, w.part, kNblk, B, alpha, kappa, stats, has_prior ? 1 : 0); note();
+    launch_k(guard_select_kernel, vg, kVecThreads, 0, s, lam, mu, s_lam, s_mu, cand_lam, cand_mu, stats, u_next_lam,
                                                   u_next_mu, n2); note();
     CK(cudaGetLastError());
     return PGET_OK;
@@ -1597,6 +1616,22 @@ pget_status pget_workspace_region(pget_geometry h, int op, int region, size_t* o
     }
     *offset = static_cast<size_t>(reinterpret_cast<uintptr_t>(p) - (uintptr_t(1) << 40));
     *bytes = static_cast<size_t>(h->g.desc.batch) * h->g.desc.n_px * h->g.desc.n_px * sizeof(float);
+    return PGET_OK;
+}
+
+pget_status pget_check_finite(const float* x, size_t n, int32_t* flag_dev, pget_stream_t stream)
+{
+    NvtxRange nvtx_("pget_check_finite");
+    if (n == 0) return PGET_OK;
+    if (!x || !flag_dev) return fail(PGET_ERR_INVALID_ARGUMENT, "pget_check_finite: NULL pointer");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    CK(cudaMemsetAsync(flag_dev, 0, sizeof(int32_t), s));
+    launch_k(finite_scan_kernel, vec_grid(n), kVecThreads, 0, s, x, n, flag_dev); note();
+    CK(cudaGetLastError());
+    int32_t h = 0;
+    CK(cudaMemcpyAsync(&h, flag_dev, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (h) return fail(PGET_ERR_NOT_FINITE, "pget_check_finite: the array holds a NaN or an infinity");
     return PGET_OK;
 }
 

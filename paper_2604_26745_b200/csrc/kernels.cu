@@ -7,6 +7,8 @@
 #include <stdint.h>
 
 #include "internal.h"
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace pget {
@@ -34,6 +36,7 @@ __global__ void pack2_kernel(const float* __restrict__ lam, const float* __restr
                              float2* outT, float* ut_lam, float* ut_mu, int N, int P, int B, int has_box,
                              BoxK box)
 {
+    pdl_entry();
     // has_box: box = (lam_lo, lam_hi, mu_lo, mu_hi) clamps the trial point u + s
     const size_t total = static_cast<size_t>(B) * P * P;
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
@@ -63,6 +66,7 @@ __global__ void pack4_kernel(const float* __restrict__ lam, const float* __restr
                              const float* __restrict__ dl, const float* __restrict__ dm, float4* out, float4* outT,
                              int N, int P, int B)
 {
+    pdl_entry();
     const size_t total = static_cast<size_t>(B) * P * P;
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < total;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -133,6 +137,7 @@ __global__ void finish_kernel(const double2* __restrict__ part, int G, const flo
                               float* copy2l, float* copy2m, float* zerol, float* zerom, int N, PriorArgs pr,
                               const float* betav)
 {
+    pdl_entry();
     __shared__ double sh[32];
     const int m = blockIdx.y;
     const size_t n2 = static_cast<size_t>(N) * N;
@@ -182,6 +187,7 @@ __global__ void finish_kernel(const double2* __restrict__ part, int G, const flo
 // r = y - ymeas (in place into y), partial 1/2||r||^2
 __global__ void residual_kernel(float* y, const float* __restrict__ ymeas, double* partial, int nper)
 {
+    pdl_entry();
     __shared__ double sh[32];
     const int m = blockIdx.y;
     double s = 0.0;
@@ -198,6 +204,7 @@ __global__ void residual_kernel(float* y, const float* __restrict__ ymeas, doubl
 // partial sum of squares of a per-member vector
 __global__ void sumsq_kernel(const float* __restrict__ x, double* partial, int nper)
 {
+    pdl_entry();
     __shared__ double sh[32];
     const int m = blockIdx.y;
     double s = 0.0;
@@ -212,6 +219,7 @@ __global__ void sumsq_kernel(const float* __restrict__ x, double* partial, int n
 // partial ||L xl||^2 + ||L xm||^2
 __global__ void regsq_kernel(const float* __restrict__ xl, const float* __restrict__ xm, double* partial, int N)
 {
+    pdl_entry();
     __shared__ double sh[32];
     const int m = blockIdx.y;
     const size_t n2 = static_cast<size_t>(N) * N;
@@ -230,6 +238,7 @@ __global__ void regsq_kernel(const float* __restrict__ xl, const float* __restri
 __global__ void priorsq_kernel(const float* __restrict__ xl, const float* __restrict__ xm, PriorArgs pr,
                                double* partial, int N)
 {
+    pdl_entry();
     __shared__ double sh[32];
     const int m = blockIdx.y;
     const size_t n2 = static_cast<size_t>(N) * N;
@@ -249,6 +258,7 @@ __global__ void priordot_kernel(const float* __restrict__ ul, const float* __res
                                 const float* __restrict__ sl, const float* __restrict__ sm, PriorArgs pr,
                                 double* pdot, double* psq, int N)
 {
+    pdl_entry();
     __shared__ double sh[32];
     const int m = blockIdx.y;
     const size_t n2 = static_cast<size_t>(N) * N;
@@ -277,6 +287,7 @@ __global__ void priordot_kernel(const float* __restrict__ ul, const float* __res
 __global__ void dot2_kernel(const float* __restrict__ al, const float* __restrict__ am,
                             const float* __restrict__ bl, const float* __restrict__ bm, double* partial, int n2)
 {
+    pdl_entry();
     __shared__ double sh[32];
     const int m = blockIdx.y;
     const size_t base = static_cast<size_t>(m) * n2;
@@ -293,6 +304,7 @@ __global__ void cg_update1_kernel(float* sl, float* sm, float* zl, float* zm, co
                                   const float* __restrict__ pm, const float* __restrict__ ql,
                                   const float* __restrict__ qm, const CGState* st, double* partial, int n2)
 {
+    pdl_entry();
     __shared__ double sh[32];
     const int m = blockIdx.y;
     const CGState c = st[m];
@@ -319,6 +331,7 @@ __global__ void cg_update1_kernel(float* sl, float* sm, float* zl, float* zm, co
 __global__ void cg_update2_kernel(const float* __restrict__ zl, const float* __restrict__ zm, float* pl,
                                   float* pm, const CGState* st, int n2)
 {
+    pdl_entry();
     const int m = blockIdx.y;
     const CGState c = st[m];
     if (c.stop) return;
@@ -343,6 +356,7 @@ __device__ __forceinline__ double psum(const double* partial, int m, int nblk)
 __global__ void dotsq_kernel(const float* __restrict__ a, const float* __restrict__ b, double* pdot, double* psq,
                              int nper)
 {
+    pdl_entry();
     __shared__ double sh[32];
     const int m = blockIdx.y;
     double d = 0.0, q = 0.0;
@@ -362,6 +376,7 @@ __global__ void dotsq_kernel(const float* __restrict__ a, const float* __restric
 __global__ void lapdot_kernel(const float* __restrict__ ul, const float* __restrict__ um, const float* __restrict__ sl,
                               const float* __restrict__ sm, double* pdot, double* psq, int N)
 {
+    pdl_entry();
     __shared__ double sh[32];
     const int m = blockIdx.y;
     const size_t n2 = static_cast<size_t>(N) * N;
@@ -384,6 +399,7 @@ __global__ void lapdot_kernel(const float* __restrict__ ul, const float* __restr
 __global__ void diff2_kernel(const float* __restrict__ al, const float* __restrict__ am, const float* __restrict__ bl,
                              const float* __restrict__ bm, float* ol, float* om, size_t n)
 {
+    pdl_entry();
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
         ol[e] = al[e] - bl[e];
@@ -396,6 +412,7 @@ __global__ void diff2_kernel(const float* __restrict__ al, const float* __restri
 __global__ void guard_scalar_kernel(const double* P, int nblk, int B, double alpha, double kappa,
                                     pget_safeguard_stats* out, int has_prior)
 {
+    pdl_entry();
     const int m = blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= B) return;
     auto v = [&](int k) { return psum(P + static_cast<size_t>(k) * B * nblk, m, nblk); };
@@ -421,6 +438,7 @@ __global__ void guard_select_kernel(const float* __restrict__ ul, const float* _
                                     const float* __restrict__ sl, const float* __restrict__ sm, const float* cl,
                                     const float* cm, const pget_safeguard_stats* st, float* ol, float* om, int n2)
 {
+    pdl_entry();
     const int m = blockIdx.y;
     const bool acc = st[m].accepted != 0;
     const size_t base = static_cast<size_t>(m) * n2;
@@ -438,6 +456,7 @@ __global__ void guard_select_kernel(const float* __restrict__ ul, const float* _
 __global__ void project_step_kernel(const float* __restrict__ ul, const float* __restrict__ um, float* sl, float* sm,
                                     size_t n, BoxK box)
 {
+    pdl_entry();
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
         float a = ul[e] + sl[e], b = um[e] + sm[e];
@@ -452,6 +471,7 @@ __global__ void project_step_kernel(const float* __restrict__ ul, const float* _
 __global__ void lm_update_kernel(float* ul, float* um, const float* __restrict__ tl, const float* __restrict__ tm,
                                  const pget_gn_stats* stats, float* betav, int n2)
 {
+    pdl_entry();
     const int m = blockIdx.y;
     const bool acc = stats[m].accepted != 0;
     const size_t base = static_cast<size_t>(m) * n2;
@@ -465,6 +485,7 @@ __global__ void lm_update_kernel(float* ul, float* um, const float* __restrict__
 
 __global__ void clamp_kernel(float* ul, float* um, size_t n, BoxK box)
 {
+    pdl_entry();
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
         float a = ul[e], b = um[e];
@@ -476,6 +497,7 @@ __global__ void clamp_kernel(float* ul, float* um, size_t n, BoxK box)
 
 __global__ void fill_kernel(float* x, float v, int n)
 {
+    pdl_entry();
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e < n) x[e] = v;
 }
@@ -485,6 +507,7 @@ __global__ void scalar_kernel(int op, int k, const double* p0, const double* p1,
                               CGState* st, pget_gn_stats* stats, int B, double alpha, double beta_h,
                               const float* betav, const double* pp)
 {
+    pdl_entry();
     const int m = blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= B) return;
     const double beta = betav ? static_cast<double>(betav[m]) : beta_h;   // per-member LM parameter
@@ -549,6 +572,7 @@ __global__ void scalar_kernel(int op, int k, const double* p0, const double* p1,
 __global__ void sgp_init_kernel(const float* __restrict__ bl, const float* __restrict__ bm, float* gl, float* gm,
                                 CGState* st, int n2, int B)
 {
+    pdl_entry();
     const size_t n = static_cast<size_t>(B) * n2;
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -565,6 +589,7 @@ __global__ void sgp_dir_kernel(const float* __restrict__ ul, const float* __rest
                                const float* __restrict__ gl, const float* __restrict__ gm, const CGState* st,
                                BoxK box, float* dl, float* dm, double* pgd, double* pdd, int n2)
 {
+    pdl_entry();
     __shared__ double sh[32];
     const int m = blockIdx.y;
     const size_t base = static_cast<size_t>(m) * n2;
@@ -597,6 +622,7 @@ __global__ void sgp_dir_kernel(const float* __restrict__ ul, const float* __rest
 __global__ void sgp_scalar_kernel(int k, int final_, const double* pgd, const double* pdd, const double* pdhd,
                                   const double* pqq, int nblk, CGState* st, pget_gn_stats* stats, int B)
 {
+    pdl_entry();
     const int m = blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= B) return;
     CGState& c = st[m];
@@ -626,6 +652,7 @@ __global__ void sgp_update_kernel(float* sl, float* sm, float* gl, float* gm, co
                                   const float* __restrict__ dm, const float* __restrict__ ql,
                                   const float* __restrict__ qm, const CGState* st, int n2)
 {
+    pdl_entry();
     const int m = blockIdx.y;
     if (st[m].stop) return;
     const float lam = static_cast<float>(st[m].bcg);
@@ -651,6 +678,7 @@ __global__ void cg_fused_kernel(const double2* __restrict__ part, int G, float a
                                 pget_gn_stats* stats, int k, int N, int B, int nblk, float4* img4n, float4* img4t,
                                 int P, PriorArgs pr)
 {
+    pdl_entry();
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
     __shared__ double sh[32];
@@ -771,4 +799,26 @@ __global__ void cg_fused_kernel(const double2* __restrict__ part, int G, float a
     }
 }
 
+}  // namespace pget
+
+namespace pget {
+bool pdl_enabled()
+{
+    static const bool on = [] {
+        const char* ev = std::getenv("PGET_PDL");
+        return !(ev && std::atoi(ev) == 0);
+    }();
+    return on;
+}
+
+// flag = 1 if any element is NaN or +-inf (pget_check_finite)
+__global__ void finite_scan_kernel(const float* __restrict__ x, size_t n, int32_t* flag)
+{
+    pdl_entry();
+    bool bad = false;
+    for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x)
+        bad |= !isfinite(x[e]);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicExch(flag, 1);
+}
 }  // namespace pget

@@ -1,10 +1,40 @@
 // kernels.cuh -- kernel argument blocks and declarations (library-private).
 #pragma once
+#include <utility>
 #include <cuda_runtime.h>
 
 #include "internal.h"
 
 namespace pget {
+
+// ---- programmatic dependent launch (PDL).  Every library kernel is launched with programmatic stream
+// serialisation (launch_k; env PGET_PDL=0 turns it off) and starts with pdl_entry(): it lets its own
+// dependent grid be scheduled at once, then waits until its predecessor grid has completed and its
+// memory is visible -- stream order is unchanged, but the next kernel's launch overlaps the tail of
+// the previous one (both in direct launches and in captured CUDA graphs).
+__device__ __forceinline__ void pdl_entry()
+{
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args)
+{
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    if (pdl_enabled()) {
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+    }
+    return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 enum { MODE_FWD = 0, MODE_JVP = 1, MODE_VJP = 2, MODE_GN = 3 };
 enum { SC_INIT = 0, SC_GAMMA = 1, SC_ZETA = 2, SC_PRED = 3, SC_TRIAL = 4 };
@@ -153,6 +183,7 @@ cudaError_t launch_fwd_combine(bool paired, const ProjArgs& A, const int32_t* ta
 cudaError_t launch_gnw(bool paired, const ProjArgs& A, const int32_t* tabs, int ntab, int B, cudaStream_t s);
 cudaError_t launch_jsq(bool paired, const ProjArgs& A, double* sq, int grid, int block, size_t smem, cudaStream_t s);
 cudaError_t launch_jsq_member(const double* sq, int ntab, int B, int nblk, double* partial, cudaStream_t s);
+__global__ void finite_scan_kernel(const float* __restrict__ x, size_t n, int32_t* flag);
 int proj_warps(int mode);
 int proj_ctas_per_sm(int mode);
 }  // namespace pget

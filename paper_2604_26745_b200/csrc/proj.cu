@@ -573,6 +573,7 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
 template <int MODE, int MAXG, bool PAIRED, bool VAR = false>
 __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MINB) proj_kernel(ProjArgs A)
 {
+    pdl_entry();
     using TR = ModeTraits<MODE>;
     const int W = blockDim.x >> 5;   // warps of this launch (<= TR::W, chosen per geometry: proj_cfg)
     const int NT = blockDim.x;
@@ -904,6 +905,7 @@ __device__ void issue_seg_stage(const ProjArgs& A, int Rb, int64_t sidx, void* d
 template <int MODE, int MAXG, bool PAIRED>
 __global__ void __launch_bounds__(512, 1) seg_a_kernel(ProjArgs A)   // W consumer warps + 1 producer warp
 {
+    pdl_entry();
     using TR = ModeTraits<MODE>;
     const int W = (blockDim.x >> 5) - 1;   // consumer warps
     extern __shared__ __align__(128) unsigned char smem[];
@@ -1008,6 +1010,7 @@ __global__ void __launch_bounds__(512, 1) seg_a_kernel(ProjArgs A)   // W consum
 // (t, m): traced angle-bank t of member m.
 __global__ void __launch_bounds__(256) jvp_combine_kernel(ProjArgs A, const int32_t* __restrict__ tabs, int ntab)
 {
+    pdl_entry();
     extern __shared__ __align__(128) unsigned char smem[];
     float* ry = reinterpret_cast<float*>(smem);          // [R]
     float* rdy = ry + A.R;                                // [R]
@@ -1055,6 +1058,7 @@ __global__ void __launch_bounds__(256) jvp_combine_kernel(ProjArgs A, const int3
 template <bool PAIRED>
 __global__ void __launch_bounds__(256) fwd_combine_kernel(ProjArgs A, const int32_t* __restrict__ tabs, int ntab)
 {
+    pdl_entry();
     extern __shared__ __align__(128) unsigned char smem[];
     float* ry = reinterpret_cast<float*>(smem);   // [2R]
     const int t = blockIdx.x, m = blockIdx.y;
@@ -1096,14 +1100,14 @@ __global__ void __launch_bounds__(256) fwd_combine_kernel(ProjArgs A, const int3
 
 cudaError_t launch_fwd_combine(bool paired, const ProjArgs& A, const int32_t* tabs, int ntab, int B, cudaStream_t s)
 {
-    if (paired) fwd_combine_kernel<true><<<dim3(ntab, B), 256, 2 * A.R * sizeof(float), s>>>(A, tabs, ntab);
-    else fwd_combine_kernel<false><<<dim3(ntab, B), 256, 2 * A.R * sizeof(float), s>>>(A, tabs, ntab);
+    if (paired) launch_k(fwd_combine_kernel<true>, dim3(ntab, B), 256, 2 * A.R * sizeof(float), s, A, tabs, ntab);
+    else launch_k(fwd_combine_kernel<false>, dim3(ntab, B), 256, 2 * A.R * sizeof(float), s, A, tabs, ntab);
     return cudaGetLastError();
 }
 
 cudaError_t launch_jvp_combine(const ProjArgs& A, const int32_t* tabs, int ntab, int B, cudaStream_t s)
 {
-    jvp_combine_kernel<<<dim3(ntab, B), 256, 2 * A.R * sizeof(float), s>>>(A, tabs, ntab);
+    launch_k(jvp_combine_kernel, dim3(ntab, B), 256, 2 * A.R * sizeof(float), s, A, tabs, ntab);
     return cudaGetLastError();
 }
 
@@ -1132,6 +1136,7 @@ __device__ __forceinline__ void entry_bounds(const ProjArgs& A, const UnitInfo& 
 template <int MODE, bool PAIRED, bool CACHE>
 __global__ void __launch_bounds__(512, 1) seg_b_kernel(ProjArgs A)
 {
+    pdl_entry();
     const int W = blockDim.x >> 5;
     const int NT = blockDim.x;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -1695,6 +1700,7 @@ __device__ __forceinline__ bool lane_ray(const ProjArgs& A, const UnitInfo& ui, 
 template <bool PAIRED>
 __global__ void __launch_bounds__(512, 1) lin_kernel(ProjArgs A)
 {
+    pdl_entry();
     const int W = blockDim.x >> 5;
     const int NT = blockDim.x;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -1767,6 +1773,7 @@ __global__ void __launch_bounds__(512, 1) lin_kernel(ProjArgs A)
 // (dlam, dmu), the same stage list) and the cache.
 __global__ void __launch_bounds__(512, 1) jvpc_kernel(ProjArgs A)
 {
+    pdl_entry();
     const int W = blockDim.x >> 5;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
@@ -1841,6 +1848,7 @@ __device__ __forceinline__ void gn_weights(const ProjArgs& A, const float* rout,
 template <bool PAIRED>
 __global__ void __launch_bounds__(256) gnw_kernel(ProjArgs A, const int32_t* __restrict__ tabs, int ntab)
 {
+    pdl_entry();
     extern __shared__ __align__(128) unsigned char smem[];
     float* rout = reinterpret_cast<float*>(smem);   // [2R]
     const int t = blockIdx.x, m = blockIdx.y;
@@ -1882,8 +1890,8 @@ __global__ void __launch_bounds__(256) gnw_kernel(ProjArgs A, const int32_t* __r
 
 cudaError_t launch_gnw(bool paired, const ProjArgs& A, const int32_t* tabs, int ntab, int B, cudaStream_t s)
 {
-    if (paired) gnw_kernel<true><<<dim3(ntab, B), 256, 2 * A.R * sizeof(float), s>>>(A, tabs, ntab);
-    else gnw_kernel<false><<<dim3(ntab, B), 256, 2 * A.R * sizeof(float), s>>>(A, tabs, ntab);
+    if (paired) launch_k(gnw_kernel<true>, dim3(ntab, B), 256, 2 * A.R * sizeof(float), s, A, tabs, ntab);
+    else launch_k(gnw_kernel<false>, dim3(ntab, B), 256, 2 * A.R * sizeof(float), s, A, tabs, ntab);
     return cudaGetLastError();
 }
 
@@ -1892,6 +1900,7 @@ cudaError_t launch_gnw(bool paired, const ProjArgs& A, const int32_t* tabs, int 
 template <bool PAIRED, bool INTACC>
 __global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
 {
+    pdl_entry();
     const int W = blockDim.x >> 5;
     const int NT = blockDim.x;
     extern __shared__ __align__(128) unsigned char smem[];
@@ -2037,6 +2046,7 @@ __global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
 template <bool PAIRED>
 __global__ void __launch_bounds__(512, 1) jsq_kernel(ProjArgs A, double* sq)
 {
+    pdl_entry();
     extern __shared__ __align__(128) unsigned char smem[];
     float* rout = reinterpret_cast<float*>(smem + A.off_rout);
     __shared__ double red[32];
@@ -2074,6 +2084,7 @@ __global__ void __launch_bounds__(512, 1) jsq_kernel(ProjArgs A, double* sq)
 // per member: the angle-banks' sums in order into partial[m * nblk] (the other nblk - 1 partials 0)
 __global__ void jsq_member_kernel(const double* __restrict__ sq, int ntab, int B, int nblk, double* partial)
 {
+    pdl_entry();
     const int m = blockIdx.x * blockDim.x + threadIdx.x;
     if (m >= B) return;
     double t = 0.0;
@@ -2084,31 +2095,31 @@ __global__ void jsq_member_kernel(const double* __restrict__ sq, int ntab, int B
 
 cudaError_t launch_jsq(bool paired, const ProjArgs& A, double* sq, int grid, int block, size_t smem, cudaStream_t s)
 {
-    if (paired) jsq_kernel<true><<<grid, block, smem, s>>>(A, sq);
-    else jsq_kernel<false><<<grid, block, smem, s>>>(A, sq);
+    if (paired) launch_k(jsq_kernel<true>, grid, block, smem, s, A, sq);
+    else launch_k(jsq_kernel<false>, grid, block, smem, s, A, sq);
     return cudaGetLastError();
 }
 
 cudaError_t launch_jsq_member(const double* sq, int ntab, int B, int nblk, double* partial, cudaStream_t s)
 {
-    jsq_member_kernel<<<(B + 127) / 128, 128, 0, s>>>(sq, ntab, B, nblk, partial);
+    launch_k(jsq_member_kernel, (B + 127) / 128, 128, 0, s, sq, ntab, B, nblk, partial);
     return cudaGetLastError();
 }
 
 cudaError_t launch_gnc(int phase, bool paired, const ProjArgs& A, int grid, int block, size_t smem, cudaStream_t s)
 {
     if (phase == 0) {
-        if (paired) lin_kernel<true><<<grid, block, smem, s>>>(A);
-        else lin_kernel<false><<<grid, block, smem, s>>>(A);
+        if (paired) launch_k(lin_kernel<true>, grid, block, smem, s, A);
+        else launch_k(lin_kernel<false>, grid, block, smem, s, A);
     } else if (phase == 1) {
-        jvpc_kernel<<<grid, block, smem, s>>>(A);
+        launch_k(jvpc_kernel, grid, block, smem, s, A);
     } else {
         if (A.gscale) {
-            if (paired) gnb_kernel<true, true><<<grid, block, smem, s>>>(A);
-            else gnb_kernel<false, true><<<grid, block, smem, s>>>(A);
+            if (paired) launch_k(gnb_kernel<true, true>, grid, block, smem, s, A);
+            else launch_k(gnb_kernel<false, true>, grid, block, smem, s, A);
         } else {
-            if (paired) gnb_kernel<true, false><<<grid, block, smem, s>>>(A);
-            else gnb_kernel<false, false><<<grid, block, smem, s>>>(A);
+            if (paired) launch_k(gnb_kernel<true, false>, grid, block, smem, s, A);
+            else launch_k(gnb_kernel<false, false>, grid, block, smem, s, A);
         }
     }
     return cudaGetLastError();
@@ -2158,6 +2169,7 @@ __global__ void reduce_slots_kernel(const float2* __restrict__ slots, double2* _
                                     const int32_t* __restrict__ red_slot, const int32_t* __restrict__ slot_lo,
                                     const int32_t* __restrict__ slot_hi)
 {
+    pdl_entry();
     __shared__ double2 tile[32][33];
     const int m = blockIdx.z / G, gq = blockIdx.z - m * G;
     const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
@@ -2228,14 +2240,14 @@ static cudaError_t launch_mode(int maxg, bool paired, const ProjArgs& A, int gri
 {
     constexpr bool CP = MODE != MODE_JVP;   // the JVP is never line-paired
     if (A.var_cw) {   // model variant (N3): unpaired only
-        if (maxg == 1) proj_kernel<MODE, 1, false, true><<<grid, block, smem, s>>>(A);
-        else proj_kernel<MODE, 2, false, true><<<grid, block, smem, s>>>(A);
+        if (maxg == 1) launch_k(proj_kernel<MODE, 1, false, true>, grid, block, smem, s, A);
+        else launch_k(proj_kernel<MODE, 2, false, true>, grid, block, smem, s, A);
     } else if (paired && CP) {
-        if (maxg == 1) proj_kernel<MODE, 1, CP><<<grid, block, smem, s>>>(A);
-        else proj_kernel<MODE, 2, CP><<<grid, block, smem, s>>>(A);
+        if (maxg == 1) launch_k(proj_kernel<MODE, 1, CP>, grid, block, smem, s, A);
+        else launch_k(proj_kernel<MODE, 2, CP>, grid, block, smem, s, A);
     } else {
-        if (maxg == 1) proj_kernel<MODE, 1, false><<<grid, block, smem, s>>>(A);
-        else proj_kernel<MODE, 2, false><<<grid, block, smem, s>>>(A);
+        if (maxg == 1) launch_k(proj_kernel<MODE, 1, false>, grid, block, smem, s, A);
+        else launch_k(proj_kernel<MODE, 2, false>, grid, block, smem, s, A);
     }
     return cudaGetLastError();
 }
@@ -2259,20 +2271,20 @@ static cudaError_t launch_seg_mode(int phase, int maxg, bool paired, const ProjA
 {
     if (phase == 0) {
         if (paired) {
-            if (maxg == 1) seg_a_kernel<MODE, 1, true><<<grid, block, smem, s>>>(A);
-            else seg_a_kernel<MODE, 2, true><<<grid, block, smem, s>>>(A);
+            if (maxg == 1) launch_k(seg_a_kernel<MODE, 1, true>, grid, block, smem, s, A);
+            else launch_k(seg_a_kernel<MODE, 2, true>, grid, block, smem, s, A);
         } else {
-            if (maxg == 1) seg_a_kernel<MODE, 1, false><<<grid, block, smem, s>>>(A);
-            else seg_a_kernel<MODE, 2, false><<<grid, block, smem, s>>>(A);
+            if (maxg == 1) launch_k(seg_a_kernel<MODE, 1, false>, grid, block, smem, s, A);
+            else launch_k(seg_a_kernel<MODE, 2, false>, grid, block, smem, s, A);
         }
     } else {
         const bool cache = MODE == MODE_VJP && A.cache != nullptr;   // fused cache build (LM wrap)
         if (cache) {
-            if (paired) seg_b_kernel<MODE, true, MODE == MODE_VJP><<<grid, block, smem, s>>>(A);
-            else seg_b_kernel<MODE, false, MODE == MODE_VJP><<<grid, block, smem, s>>>(A);
+            if (paired) launch_k(seg_b_kernel<MODE, true, MODE == MODE_VJP>, grid, block, smem, s, A);
+            else launch_k(seg_b_kernel<MODE, false, MODE == MODE_VJP>, grid, block, smem, s, A);
         } else {
-            if (paired) seg_b_kernel<MODE, true, false><<<grid, block, smem, s>>>(A);
-            else seg_b_kernel<MODE, false, false><<<grid, block, smem, s>>>(A);
+            if (paired) launch_k(seg_b_kernel<MODE, true, false>, grid, block, smem, s, A);
+            else launch_k(seg_b_kernel<MODE, false, false>, grid, block, smem, s, A);
         }
     }
     return cudaGetLastError();
@@ -2283,8 +2295,8 @@ cudaError_t launch_seg(int phase, int mode, int maxg, bool paired, const ProjArg
 {
     if (maxg != 1 && maxg != 2) return cudaErrorInvalidValue;
     if (mode == MODE_JVP && phase == 0) {   // the standalone JVP: phase A only, unpaired
-        if (maxg == 1) seg_a_kernel<MODE_JVP, 1, false><<<grid, block, smem, s>>>(A);
-        else seg_a_kernel<MODE_JVP, 2, false><<<grid, block, smem, s>>>(A);
+        if (maxg == 1) launch_k(seg_a_kernel<MODE_JVP, 1, false>, grid, block, smem, s, A);
+        else launch_k(seg_a_kernel<MODE_JVP, 2, false>, grid, block, smem, s, A);
         return cudaGetLastError();
     }
     if (mode == MODE_VJP) return launch_seg_mode<MODE_VJP>(phase, maxg, paired, A, grid, block, smem, s);

@@ -499,3 +499,21 @@ def test_high_optical_depth(pg, scale):
         x = np.concatenate([host(ql).ravel(), host(qm).ravel()])
         assert np.isfinite(x).all()
         assert rel_l2(x, o) <= TOL_L2, (cached, rel_l2(x, o))
+
+
+def test_check_finite(pg):
+    """SURVEY.md §5 failure detection: pget_check_finite passes finite outputs and reports a NaN or an
+    infinity as PGET_ERR_NOT_FINITE, e.g. the forward of an image holding a NaN."""
+    gd = EDGE[2]
+    g = pg.Geometry(gd)
+    lam, mu, _, _ = rand_inputs(gd, 3)
+    y = pg.forward(g, dev(lam), dev(mu))
+    pg.check_finite(y)
+    lam[0, 5, 7] = np.nan
+    y = pg.forward(g, dev(lam), dev(mu))
+    with pytest.raises(RuntimeError, match="NOT_FINITE"):
+        pg.check_finite(y)
+    x = torch.zeros(1000, device="cuda")
+    x[999] = float("inf")
+    with pytest.raises(RuntimeError, match="NOT_FINITE"):
+        pg.check_finite(x)
