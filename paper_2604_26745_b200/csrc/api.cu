@@ -172,6 +172,7 @@ struct SegCfg {
     size_t smemA;
     int WB, passesB, RbB, gridB, stageB, off_wacc, off_rout, off_gsh, off_rsc, off_q1;
     int RbG, off_waccG, off_routG;   // gnb_kernel: no stage buffers, so taller bands
+    int WG, passesG;                 // gnb_kernel warps (one shared accumulator: up to 26, one pass) and passes
     size_t smemG;
     size_t smemB;
 };
@@ -255,6 +256,14 @@ SegCfg seg_cfg(const Geometry& g)
                 c.off_waccG = 128;
                 c.off_routG = static_cast<int>(128 + wi);
                 c.smemG = 128 + wi + rout_b;
+            }
+            // the fixed-point scatter keeps one accumulator whatever the warp count: with 17-26 comb
+            // groups every group gets its own warp (one pass) in the 26-warp build of gnb_kernel
+            c.WG = c.WB;
+            c.passesG = c.passesB;
+            if (g.gnb_int && g.gn_hybrid && g.gnb_wide && ngB > 16 && ngB <= 26) {
+                c.WG = ngB;
+                c.passesG = 1;
             }
         }
     }
@@ -645,6 +654,7 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     g.gnb_tall = g.P >= 200;   // measured: config 4 -3.6 % LM, config 2 +0.8 %
     if (const char* ev = std::getenv("PGET_GNB_TALL")) g.gnb_tall = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_GNB_INT")) g.gnb_int = g.gnb_int && std::atoi(ev) != 0;
+    if (const char* ev = std::getenv("PGET_GNB_WIDE")) g.gnb_wide = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_GN_APPLY_CACHED")) g.gn_apply_cached = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_GN_CACHE_MAX_GB")) g.cache_max_gb = std::atof(ev);
     if (const char* ev = std::getenv("PGET_GN_CACHE")) {   // 0: recompute, 1: hybrid, 2: fully cached
@@ -998,7 +1008,8 @@ static pget_status gnc_product(const Geometry& g, const WS& w, const float* lam,
         Ag.RbB = c.RbG;
         Ag.off_wacc = c.off_waccG;
         Ag.off_rout = c.off_routG;
-        e = launch_gnc(2, g.pair, Ag, c.gridB, c.WB * 32, c.smemG, s);
+        Ag.passesB = c.passesG;
+        e = launch_gnc(2, g.pair, Ag, c.gridB, c.WG * 32, c.smemG, s);
     }
     if (eb) cudaEventRecord(eb, s);
     if (e != cudaSuccess) return cuda_fail(e, "cached GN launch");

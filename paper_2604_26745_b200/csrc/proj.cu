@@ -1897,8 +1897,9 @@ cudaError_t launch_gnw(bool paired, const ProjArgs& A, const int32_t* tabs, int 
 
 // gnb_kernel: per CG step, w_r from the (J p) partials, then the cached scatter into slots (as
 // seg_b_kernel; no image staging).
-template <bool PAIRED, bool INTACC>
-__global__ void __launch_bounds__(512, 1) gnb_kernel(ProjArgs A)
+// WIDE: up to 26 warps (one pass over 26 comb groups, configs 3-4) at <= 72 registers; else <= 16 warps
+template <bool PAIRED, bool INTACC, bool WIDE = false>
+__global__ void __launch_bounds__(WIDE ? 832 : 512, 1) gnb_kernel(ProjArgs A)
 {
     pdl_entry();
     const int W = blockDim.x >> 5;
@@ -2115,8 +2116,13 @@ cudaError_t launch_gnc(int phase, bool paired, const ProjArgs& A, int grid, int 
         launch_k(jvpc_kernel, grid, block, smem, s, A);
     } else {
         if (A.gscale) {
-            if (paired) launch_k(gnb_kernel<true, true>, grid, block, smem, s, A);
-            else launch_k(gnb_kernel<false, true>, grid, block, smem, s, A);
+            if (block > 512) {
+                if (paired) launch_k(gnb_kernel<true, true, true>, grid, block, smem, s, A);
+                else launch_k(gnb_kernel<false, true, true>, grid, block, smem, s, A);
+            } else {
+                if (paired) launch_k(gnb_kernel<true, true>, grid, block, smem, s, A);
+                else launch_k(gnb_kernel<false, true>, grid, block, smem, s, A);
+            }
         } else {
             if (paired) launch_k(gnb_kernel<true, false>, grid, block, smem, s, A);
             else launch_k(gnb_kernel<false, false>, grid, block, smem, s, A);
@@ -2154,6 +2160,8 @@ cudaError_t set_gnc_smem_limit(size_t smem)
     if ((e = raise_smem(gnb_kernel<true, false>, v))) return e;
     if ((e = raise_smem(gnb_kernel<true, true>, v))) return e;
     if ((e = raise_smem(gnb_kernel<false, true>, v))) return e;
+    if ((e = raise_smem(gnb_kernel<true, true, true>, v))) return e;
+    if ((e = raise_smem(gnb_kernel<false, true, true>, v))) return e;
     if ((e = raise_smem(jsq_kernel<true>, v))) return e;
     if ((e = raise_smem(jsq_kernel<false>, v))) return e;
     return raise_smem(gnb_kernel<false, false>, v);
