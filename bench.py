@@ -568,7 +568,7 @@ def main():
                 "projector_ms_per_launch": {k: (prof["ms"][k] / prof["launches"][k] if prof["launches"][k] else None)
                                             for k in prof["ms"]},
             },
-            "roofline": {"bound": "alu", "pipe": "shared-memory crossbar (128 B/clk/SM)", "kernel": ({"gn": "gn: seg_a_kernel<GN> + gnw_kernel + gnb_kernel (recomputed J p, scatter weights, cached fixed-point scatter; per CG step, timed together)",
+            "roofline": {"bound": "alu", "pipe": f"shared-memory data path ({bpc:.1f} B/clk/SM)", "kernel": ({"gn": "gn: seg_a_kernel<GN> + gnw_kernel + gnb_kernel (recomputed J p, scatter weights, cached fixed-point scatter; per CG step, timed together)",
                                     "vjp": "vjp: seg_a_kernel + seg_b_kernel (segmented adjoint, one launch pair)"}.get(dom, f"proj_kernel<{dom}>")),
                          "achieved": achieved_gbs, "peak": peak_gbs, "unit": "GB/s", "frac": achieved_gbs / peak_gbs,
                          "traffic": traffic,

@@ -183,6 +183,7 @@ SegCfg seg_cfg(const Geometry& g)
     SegCfg c;
     const int ngA = (g.R + 31) / 32;
     c.WA = g.segA_W;   // consumer warps (the kernel adds one producer warp)
+    if (g.segA_wide && ngA > c.WA && ngA <= 26) c.WA = ngA;   // the 26-warp build: one group per warp
     c.maxgA = ngA > c.WA ? 2 : 1;
     c.passesA = std::max(1, (ngA + c.WA * c.maxgA - 1) / (c.WA * c.maxgA));
     const size_t per_sm = 233472;
@@ -655,6 +656,7 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     if (const char* ev = std::getenv("PGET_GNB_TALL")) g.gnb_tall = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_GNB_INT")) g.gnb_int = g.gnb_int && std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_GNB_WIDE")) g.gnb_wide = std::atoi(ev) != 0;
+    if (const char* ev = std::getenv("PGET_SEGA_WIDE")) g.segA_wide = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_GN_APPLY_CACHED")) g.gn_apply_cached = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_GN_CACHE_MAX_GB")) g.cache_max_gb = std::atof(ev);
     if (const char* ev = std::getenv("PGET_GN_CACHE")) {   // 0: recompute, 1: hybrid, 2: fully cached

@@ -902,8 +902,9 @@ __device__ void issue_seg_stage(const ProjArgs& A, int Rb, int64_t sidx, void* d
 // every consumer warp arrives when done with it), so consumer warps never wait for one another.
 
 
-template <int MODE, int MAXG, bool PAIRED>
-__global__ void __launch_bounds__(512, 1) seg_a_kernel(ProjArgs A)   // W consumer warps + 1 producer warp
+// WIDE: up to 26 consumer warps (one 32-ray group each, configs 3-4) at <= 72 registers; else <= 15
+template <int MODE, int MAXG, bool PAIRED, bool WIDE = false>
+__global__ void __launch_bounds__(WIDE ? 864 : 512, 1) seg_a_kernel(ProjArgs A)   // W consumer warps + 1 producer warp
 {
     pdl_entry();
     using TR = ModeTraits<MODE>;
@@ -2279,10 +2280,12 @@ static cudaError_t launch_seg_mode(int phase, int maxg, bool paired, const ProjA
 {
     if (phase == 0) {
         if (paired) {
-            if (maxg == 1) launch_k(seg_a_kernel<MODE, 1, true>, grid, block, smem, s, A);
+            if (block > 512) launch_k(seg_a_kernel<MODE, 1, true, true>, grid, block, smem, s, A);
+            else if (maxg == 1) launch_k(seg_a_kernel<MODE, 1, true>, grid, block, smem, s, A);
             else launch_k(seg_a_kernel<MODE, 2, true>, grid, block, smem, s, A);
         } else {
-            if (maxg == 1) launch_k(seg_a_kernel<MODE, 1, false>, grid, block, smem, s, A);
+            if (block > 512) launch_k(seg_a_kernel<MODE, 1, false, true>, grid, block, smem, s, A);
+            else if (maxg == 1) launch_k(seg_a_kernel<MODE, 1, false>, grid, block, smem, s, A);
             else launch_k(seg_a_kernel<MODE, 2, false>, grid, block, smem, s, A);
         }
     } else {
@@ -2303,7 +2306,8 @@ cudaError_t launch_seg(int phase, int mode, int maxg, bool paired, const ProjArg
 {
     if (maxg != 1 && maxg != 2) return cudaErrorInvalidValue;
     if (mode == MODE_JVP && phase == 0) {   // the standalone JVP: phase A only, unpaired
-        if (maxg == 1) launch_k(seg_a_kernel<MODE_JVP, 1, false>, grid, block, smem, s, A);
+        if (block > 512) launch_k(seg_a_kernel<MODE_JVP, 1, false, true>, grid, block, smem, s, A);
+        else if (maxg == 1) launch_k(seg_a_kernel<MODE_JVP, 1, false>, grid, block, smem, s, A);
         else launch_k(seg_a_kernel<MODE_JVP, 2, false>, grid, block, smem, s, A);
         return cudaGetLastError();
     }
@@ -2320,6 +2324,8 @@ static cudaError_t seg_attr_mode(int phase, size_t smem)
     if (phase == 0) {
         if ((e = raise_smem(seg_a_kernel<MODE, 1, true>, v))) return e;
         if ((e = raise_smem(seg_a_kernel<MODE, 2, true>, v))) return e;
+        if ((e = raise_smem(seg_a_kernel<MODE, 1, true, true>, v))) return e;
+        if ((e = raise_smem(seg_a_kernel<MODE, 1, false, true>, v))) return e;
         if ((e = raise_smem(seg_a_kernel<MODE, 1, false>, v))) return e;
         return raise_smem(seg_a_kernel<MODE, 2, false>, v);
     }
@@ -2334,6 +2340,8 @@ cudaError_t set_seg_smem_limit(int phase, int mode, size_t smem)
     if (mode == MODE_JVP) {
         const int v = static_cast<int>(smem);
         cudaError_t e = raise_smem(seg_a_kernel<MODE_JVP, 1, false>, v);
+        if (e) return e;
+        e = raise_smem(seg_a_kernel<MODE_JVP, 1, false, true>, v);
         if (e) return e;
         return raise_smem(seg_a_kernel<MODE_JVP, 2, false>, v);
     }

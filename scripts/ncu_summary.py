@@ -124,11 +124,14 @@ def main():
     # ncu speed-of-light fractions per kernel (the north star's "FP32/SFU issue" roofline as ncu
     # measures it), for bench.py's roofline_ncu
     sol = {}
+    tscale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
     for mode, name, v in res:
         def num(lab):
             x = v.get(lab)
             return float(x[0].replace(",", "")) if x else None
-        sol[mode] = {"kernel": name.split("(")[0].replace("void ", ""), "duration_us": num("duration"),
+        dur = v.get("duration")
+        dur_us = float(dur[0].replace(",", "")) * tscale.get(dur[1], 1.0) if dur else None
+        sol[mode] = {"kernel": name.split("(")[0].replace("void ", ""), "duration_us": dur_us,
                      "sm_sol_pct": num("SM SOL %"), "issue_active_pct": num("issue active %"),
                      "l1_smem_pct": num("L1/smem throughput %"), "fma_pipe_pct": num("FMA pipe %"),
                      "xu_pipe_pct": num("XU (MUFU) %")}
