@@ -37,7 +37,8 @@ class _Desc(C.Structure):
     _fields_ = [("n_px", C.c_int), ("n_angles", C.c_int), ("n_banks", C.c_int),
                 ("n_det", C.c_int), ("n_subrays", C.c_int), ("subray_sigma", C.c_double),
                 ("step_px", C.c_double), ("bank1_shift", C.c_double), ("batch", C.c_int),
-                ("det_radius", C.c_double), ("c_slope", C.c_double), ("r_slope", C.c_double)]
+                ("det_radius", C.c_double), ("c_slope", C.c_double), ("r_slope", C.c_double),
+                ("pixel_basis", C.c_int)]
 
 
 def _load():
@@ -66,6 +67,8 @@ def _load():
         _lib.orc_ray_adjoint.argtypes = [C.c_int, P, P, C.c_double, P, P]
         _lib.orc_ray_adjoint.restype = None
         _lib.orc_threads.restype = C.c_int
+        _lib.orc_pb_crossings.argtypes = [C.c_int, C.c_double, C.c_double, C.c_double, P, P, P]
+        _lib.orc_pb_crossings.restype = C.c_int
         _lib.orc_set_prior.argtypes = [P, P, C.c_double, C.c_double]
         _lib.orc_project.argtypes = [P, P, C.c_size_t, P]
         _lib.orc_project.restype = None
@@ -105,7 +108,8 @@ def _desc(g: dict) -> _Desc:
     return _Desc(int(g["n_px"]), int(g["n_angles"]), int(g.get("n_banks", 2)), int(g.get("n_det", 91)),
                  int(g.get("n_subrays", 1)), float(g.get("subray_sigma", 0.4)),
                  float(g.get("step_px", 0.5)), float(g.get("bank1_shift", 0.0)), int(g.get("batch", 1)),
-                 float(g.get("det_radius", 0.0)), float(g.get("c_slope", 0.0)), float(g.get("r_slope", 0.0)))
+                 float(g.get("det_radius", 0.0)), float(g.get("c_slope", 0.0)), float(g.get("r_slope", 0.0)),
+                 int(g.get("pixel_basis", 0)))
 
 
 def _f64(a):
@@ -126,6 +130,20 @@ def variant_tables(g: dict) -> dict:
     rc = lib.orc_variant_tables(C.byref(d), _p(Cv), _p(W))
     assert rc == 0, rc
     return {"c": Cv, "w": W}
+
+
+def pb_crossings(n_px, c, s, sigma):
+    """O14: the pixels (row * N + col) the line sigma omega_perp + t omega, omega = (c, s), crosses in
+    [-1,1]^2 in order of increasing t, with the intersection lengths and the chord midpoints' t."""
+    lib = _load()
+    n = 2 * int(n_px) + 4
+    pix = np.zeros(n, np.int32)
+    ln = np.zeros(n)
+    tm = np.zeros(n)
+    M = lib.orc_pb_crossings(int(n_px), float(c), float(s), float(sigma), _p(pix), _p(ln), _p(tm))
+    if M < 0:
+        raise MemoryError("orc_pb_crossings")
+    return pix[:M].copy(), ln[:M].copy(), tm[:M].copy()
 
 
 def threads() -> int:

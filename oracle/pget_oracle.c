@@ -35,6 +35,12 @@
  *         y = sum_j sum_i W_j(d_i) Delta lam_i exp(-c_i A_i),  c_i = 1 + c_slope d_i,
  *         W_j(d) = exp(-delta_j^2 / (2 sigma(d)^2)) / sum_k exp(-delta_k^2 / (2 sigma(d)^2)),
  *         sigma(d) = subray_sigma * pitch * (1 + r_slope d);   on iff det_radius > 0
+ *   pixel basis (O14, N3): the exact intersection lengths d_{m,n,k} of eq:d_fwd_model (
+ *       reading R-pb): lam, mu constant on each pixel; a ray crosses pixels k_1..k_M (increasing t, the
+ *       detector at +t) with lengths l_q; the ray from pixel k_q starts at the midpoint of its chord:
+ *         A_q = 1/2 l_q mu_q + sum_{p>q} l_p mu_p,   g_ray = sum_q r_q lam_q exp(-c_q A_q),
+ *         r_q = l_q (W_j(d_q) with the O13 variant), d_q = det_radius - t_q at the chord midpoint;
+ *       y = sum_j w_j g_ray (base weights) as for the sampled model.  on iff pixel_basis != 0
  *
  * Parity pins: tests/test_oracle.py (P1-P12 of SURVEY.md §8(c.4)); DESIGN.md "Oracle".
  * Compile: gcc -O2 -fopenmp -ffp-contract=off -fPIC -shared (no fast-math).
@@ -51,6 +57,7 @@ typedef struct {
     double subray_sigma, step_px, bank1_shift;
     int batch;
     double det_radius, c_slope, r_slope;   /* O13 model variant (N3); det_radius <= 0: off */
+    int pixel_basis;                       /* O14 pixel basis (N3): exact intersection lengths  */
 } orc_desc;
 
 /* ------------------------------------------------------------------ O1 geometry */
@@ -364,6 +371,158 @@ static void ray_vjp(const orc_lattice* L, int N, const double* lam, const double
     }
 }
 
+/* ------------------------------------------------------------------ O14 pixel basis */
+static int cmp_double(const void* a, const void* b)
+{
+    double x = *(const double*)a, y = *(const double*)b;
+    return x < y ? -1 : (x > y ? 1 : 0);
+}
+
+/* The pixels a line x(t) = sigma omega_perp + t omega crosses in the image square [-1,1]^2, in order of
+ * increasing t, with the length of the line inside each.  In pixel units (X = (x + 1) N/2, the pixel
+ * edges at the integers 0..N): X(t) = X0 + t wX with X0 = (-sigma s + 1) N/2, wX = c N/2 (Y likewise,
+ * from sigma c and s); every crossing t = (k - X0) / wX of an edge strictly between the line's entry
+ * and exit of the square (slab clipping against [0, N]^2), plus the entry and exit, sorted; each
+ * interval of positive length lies in one pixel, found from its midpoint: floor(X0 + t_mid wX).
+ * (1/w is formed once per line and multiplied; a line exactly on the square's edge is outside.)
+ * pix[q] = row * N + col, len[q] = interval length (domain units: omega is a unit vector),
+ * tmid[q] = its midpoint t.  Returns M (<= 2N + 2). */
+static int o14_cross(int N, double c, double s, double sigma, int* pix, double* len, double* tmid, double* ts)
+{
+    double hN = 0.5 * N;
+    double X0[2] = {(-sigma * s + 1.0) * hN, (sigma * c + 1.0) * hN};
+    double w[2] = {c * hN, s * hN};
+    double inv[2] = {0.0, 0.0};
+    double tin = -INFINITY, tout = INFINITY;
+    for (int k = 0; k < 2; ++k) {
+        if (w[k] == 0.0) {
+            if (!(X0[k] > 0.0 && X0[k] < (double)N)) return 0;
+        } else {
+            inv[k] = 1.0 / w[k];
+            double t1 = (0.0 - X0[k]) * inv[k], t2 = ((double)N - X0[k]) * inv[k];
+            double lo = t1 < t2 ? t1 : t2, hi = t1 < t2 ? t2 : t1;
+            if (lo > tin) tin = lo;
+            if (hi < tout) tout = hi;
+        }
+    }
+    if (!(tin < tout)) return 0;
+    int n = 0;
+    ts[n++] = tin;
+    ts[n++] = tout;
+    for (int k = 0; k < 2; ++k) {
+        if (w[k] == 0.0) continue;
+        for (int e = 0; e <= N; ++e) {
+            double t = ((double)e - X0[k]) * inv[k];
+            if (t > tin && t < tout) ts[n++] = t;
+        }
+    }
+    qsort(ts, (size_t)n, sizeof(double), cmp_double);
+    int M = 0;
+    for (int q = 0; q + 1 < n; ++q) {
+        double l = ts[q + 1] - ts[q];
+        if (!(l > 0.0)) continue;
+        double tm = 0.5 * (ts[q] + ts[q + 1]);
+        int col = (int)floor(X0[0] + tm * w[0]);
+        int row = (int)floor(X0[1] + tm * w[1]);
+        if (col < 0) col = 0;
+        if (col > N - 1) col = N - 1;
+        if (row < 0) row = 0;
+        if (row > N - 1) row = N - 1;
+        pix[M] = row * N + col;
+        len[M] = l;
+        tmid[M] = tm;
+        ++M;
+    }
+    return M;
+}
+
+/* O13 response at distance d to the detector, for sub-ray j: c(d) = 1 + c_slope d and the normalised
+ * Gaussian W_j(d) of width subray_sigma * pitch * (1 + r_slope d) (the same functions as o13_tables) */
+static void o14_resp(const orc_desc* g, double d, int j, double* C, double* W)
+{
+    int J = g->n_subrays;
+    double p = 2.0 / (g->n_det - 1);
+    double sp = g->subray_sigma * p * (1.0 + g->r_slope * d);
+    double sum = 0.0, wj = 0.0;
+    for (int k = 0; k < J; ++k) {
+        double dk = (double)(2 * k + 1 - J) / (double)(2 * J) * p;
+        double e = exp(-(dk * dk) / (2.0 * sp * sp));
+        sum += e;
+        if (k == j) wj = e;
+    }
+    *C = 1.0 + g->c_slope * d;
+    *W = wj / sum;
+}
+
+/* one ray of the pixel basis: g = sum_q r_q lam_q E_q, E_q = exp(-c_q A_q),
+ * A_q = l_q mu_q / 2 + sum_{p>q} l_p mu_p;  JVP dg = sum_q r_q (dlam_q - lam_q c_q dA_q) E_q  (eq:frechet) */
+static double ray_fwd_pb(const orc_desc* g, int var, int j, int M, const int* pix, const double* len,
+                         const double* tmid, const double* lam, const double* mu, const double* dlam,
+                         const double* dmu, double* dg_ray)
+{
+    double gs = 0.0, dg = 0.0, sum_mu = 0.0, sum_dmu = 0.0;
+    for (int q = M - 1; q >= 0; --q) {
+        double l = len[q], cq = 1.0, rq = l;
+        if (var) {
+            double W;
+            o14_resp(g, g->det_radius - tmid[q], j, &cq, &W);
+            rq = W * l;
+        }
+        double A = 0.5 * l * mu[pix[q]] + sum_mu;
+        double E = exp(-cq * A);
+        gs += rq * lam[pix[q]] * E;
+        if (dlam) {
+            double dA = 0.5 * l * dmu[pix[q]] + sum_dmu;
+            dg += rq * (dlam[pix[q]] - lam[pix[q]] * cq * dA) * E;
+            sum_dmu += l * dmu[pix[q]];
+        }
+        sum_mu += l * mu[pix[q]];
+    }
+    if (dg_ray) *dg_ray = dg;
+    return gs;
+}
+
+/* its transpose with weight wr: a_lam(q) = wr r_q E_q,
+ * a_mu(q) = -wr l_q (sum_{p<q} r_p lam_p c_p E_p + 1/2 r_q lam_q c_q E_q) */
+static void ray_vjp_pb(const orc_desc* g, int var, int j, int M, const int* pix, const double* len,
+                       const double* tmid, const double* lam, const double* mu, double wr, double* glam,
+                       double* gmu, double* buf)
+{
+    double* E = buf;
+    double* R = buf + M;
+    double* Cq = buf + 2 * M;
+    double sum_mu = 0.0;
+    for (int q = M - 1; q >= 0; --q) {
+        double l = len[q], cq = 1.0, rq = l;
+        if (var) {
+            double W;
+            o14_resp(g, g->det_radius - tmid[q], j, &cq, &W);
+            rq = W * l;
+        }
+        E[q] = exp(-cq * (0.5 * l * mu[pix[q]] + sum_mu));
+        R[q] = rq;
+        Cq[q] = cq;
+        sum_mu += l * mu[pix[q]];
+    }
+    double prefix = 0.0;   /* sum_{p<q} r_p lam_p c_p E_p (farther from the detector) */
+    for (int q = 0; q < M; ++q) {
+        double le = R[q] * lam[pix[q]] * Cq[q] * E[q];
+        glam[pix[q]] += wr * R[q] * E[q];
+        gmu[pix[q]] += -wr * len[q] * (prefix + 0.5 * le);
+        prefix += le;
+    }
+}
+
+/* Export one ray's crossings (pin P19: traversal against per-pixel clipping). */
+int orc_pb_crossings(int N, double c, double s, double sigma, int* pix, double* len, double* tmid)
+{
+    double* ts = (double*)malloc(sizeof(double) * (2 * (N + 1) + 2));
+    if (!ts) return -2;
+    int M = o14_cross(N, c, s, sigma, pix, len, tmid, ts);
+    free(ts);
+    return M;
+}
+
 static int num_threads(void)
 {
 #ifdef _OPENMP
@@ -383,7 +542,7 @@ static int fwd_impl(const orc_desc* g, const double* lam, const double* mu, cons
 {
     orc_ctx cx;
     if (ctx_init(g, &cx)) return -1;
-    if (naive && cx.var) { ctx_free(&cx); return -1; }
+    if (naive && (cx.var || g->pixel_basis)) { ctx_free(&cx); return -1; }
     int N = g->n_px, nA = g->n_angles, nB = g->n_banks, nd = g->n_det, J = g->n_subrays;
     long n_ab = (long)g->batch * nA * nB;
     size_t npx = (size_t)N * N;
@@ -397,6 +556,14 @@ static int fwd_impl(const orc_desc* g, const double* lam, const double* mu, cons
         const double* du = dmu ? dmu + m * npx : NULL;
         double c, s;
         o1_dir(g, a, b, &c, &s);
+        int* pix = NULL;
+        double *len = NULL, *tmid = NULL, *ts = NULL;
+        if (g->pixel_basis) {   /* O14 crossing buffers */
+            pix = (int*)malloc(sizeof(int) * (2 * N + 4));
+            len = (double*)malloc(sizeof(double) * (2 * N + 4) * 3 + sizeof(double) * 2);
+            tmid = len + (2 * N + 4);
+            ts = tmid + (2 * N + 4);
+        }
         for (int d = 0; d < nd; ++d) {
             double acc = 0.0, dacc = 0.0;
             for (int j = 0; j < J; ++j) {
@@ -404,7 +571,10 @@ static int fwd_impl(const orc_desc* g, const double* lam, const double* mu, cons
                 int ilo, ihi;
                 o1_clip(g, &cx.L, c, s, sigma, &ilo, &ihi);
                 double gj, dgj = 0.0;
-                if (naive)
+                if (g->pixel_basis) {
+                    int M = o14_cross(N, c, s, sigma, pix, len, tmid, ts);
+                    gj = ray_fwd_pb(g, cx.var, j, M, pix, len, tmid, l, u, dl, du, dl ? &dgj : NULL);
+                } else if (naive)
                     gj = ray_fwd_naive(&cx.L, N, l, u, c, s, sigma, ilo, ihi);
                 else
                     gj = ray_fwd(&cx.L, N, l, u, dl, du, c, s, sigma, ilo, ihi, dl ? &dgj : NULL,
@@ -420,6 +590,8 @@ static int fwd_impl(const orc_desc* g, const double* lam, const double* mu, cons
             if (y) y[q * nd + d] = acc;
             if (dy) dy[q * nd + d] = dacc;
         }
+        free(pix);
+        free(len);
     }
     ctx_free(&cx);
     return 0;
@@ -466,6 +638,11 @@ int orc_vjp(const orc_desc* g, const double* lam, const double* mu, const double
             double* gl = priv + (size_t)tid * 2 * npx;
             double* gm = gl + npx;
             double* buf = (double*)malloc(sizeof(double) * 2 * (cx.L.n_t + 1));
+            int* pix = (int*)malloc(sizeof(int) * (2 * N + 4));       /* O14 crossing buffers */
+            double* len = (double*)malloc(sizeof(double) * (2 * N + 4) * 6 + sizeof(double) * 2);
+            double* tmid = len + (2 * N + 4);
+            double* pbuf = tmid + (2 * N + 4);
+            double* ts = pbuf + 3 * (2 * N + 4);
 #pragma omp for schedule(static)
             for (int q = 0; q < nA * nB; ++q) {
                 int b = q % nB, a = q / nB;
@@ -477,7 +654,10 @@ int orc_vjp(const orc_desc* g, const double* lam, const double* mu, const double
                         double sigma = o1_offset(g, b, d, j);
                         int ilo, ihi;
                         o1_clip(g, &cx.L, c, s, sigma, &ilo, &ihi);
-                        if (cx.var)   /* O13: the response W_j(d_i) is inside the ray sum */
+                        if (g->pixel_basis) {   /* O14 (with the O13 response W_j inside the ray sum) */
+                            int M = o14_cross(N, c, s, sigma, pix, len, tmid, ts);
+                            ray_vjp_pb(g, cx.var, j, M, pix, len, tmid, l, u, cx.var ? wd : cx.w[j] * wd, gl, gm, pbuf);
+                        } else if (cx.var)   /* O13: the response W_j(d_i) is inside the ray sum */
                             ray_vjp(&cx.L, N, l, u, wd, c, s, sigma, ilo, ihi, gl, gm, buf, cx.C,
                                     cx.W + (size_t)j * cx.L.n_t);
                         else
@@ -486,6 +666,8 @@ int orc_vjp(const orc_desc* g, const double* lam, const double* mu, const double
                 }
             }
             free(buf);
+            free(pix);
+            free(len);
         }
         for (int t = 0; t < nth; ++t)
             for (size_t k = 0; k < npx; ++k) {

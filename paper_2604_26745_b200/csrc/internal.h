@@ -187,8 +187,8 @@ struct Geometry {
     // requires every pixel's per-unit sum below 2^31 at the scale that keeps a pending cell below
     // 2^22, i.e. (samples near a pixel) / cellmax < 512 (geometry.cpp)
     bool gnb_int = true;
-    bool gnb_wide = true;
-    bool segA_wide = true;  // phase A with one consumer warp per 32-ray group for 16-26 groups (PGET_SEGA_WIDE=0: 15 warps)   // cached scatter with one warp per comb group for 17-26 groups (PGET_GNB_WIDE=0: <= 16)
+    bool gnb_wide = true;   // cached scatter with one warp per comb group for 17-26 groups (PGET_GNB_WIDE=0: <= 16)
+    bool segA_wide = true;  // phase A with one consumer warp per 32-ray group for 16-26 groups (PGET_SEGA_WIDE=0: 15 warps)
     // pget_gn_apply through the cache too (one product per call: building the cache costs more than
     // it saves; tests set PGET_GN_APPLY_CACHED=1 to pin the cached product at the operator tolerance)
     bool gn_apply_cached = false;

@@ -1056,3 +1056,225 @@ def test_p18_adjoint_identity_and_dense_transpose():
     JT = np.stack([np.concatenate([x.ravel() for x in O.vjp(g, lam, mu, e.reshape(O.sino_shape(g)))])
                    for e in np.eye(ns)], axis=0)
     assert np.abs(JT - Jd).max() <= 1e-12 * np.abs(Jd).max()
+
+
+# ----------------------------------------------------------------------------- P19 pixel basis (O14, R-pb)
+PB = dict(pixel_basis=1)
+
+
+def _clip_len(x0, x1, y0, y1, p0, om):
+    """length of the line p0 + t om inside the closed box [x0,x1] x [y0,y1] (slab clipping)"""
+    tin, tout = -np.inf, np.inf
+    for k, (a, b) in enumerate(((x0, x1), (y0, y1))):
+        if om[k] == 0.0:
+            if not (a <= p0[k] <= b):
+                return 0.0
+            continue
+        t1, t2 = (a - p0[k]) / om[k], (b - p0[k]) / om[k]
+        tin, tout = max(tin, min(t1, t2)), min(tout, max(t1, t2))
+    return max(0.0, tout - tin)
+
+
+@pytest.mark.parametrize("N", [7, 8, 13])
+def test_p19_crossings_match_per_pixel_clipping(N):
+    """The traversal's pixels and lengths equal, pixel by pixel, the clipped length of the line in each
+    pixel box (brute force over all N^2 pixels, eq:d_fwd_model's d_{m,n,k} as 'the distances a ray
+    covers within pixel k'); the pixels come in order of t and each is an edge or corner
+    neighbour of the previous one; the lengths sum to the chord of the square."""
+    h = 2.0 / N
+    rng = np.random.default_rng(N)
+    for k in range(60):
+        phi = rng.uniform(0, 2 * np.pi) if k > 3 else k * np.pi / 2 + 0.1
+        c, s = math.cos(phi), math.sin(phi)
+        sigma = rng.uniform(-1.3, 1.3)
+        pix, ln, tm = O.pb_crossings(N, c, s, sigma)
+        p0, om = (-sigma * s, sigma * c), (c, s)
+        ref = np.zeros(N * N)
+        for r in range(N):
+            for q in range(N):
+                ref[r * N + q] = _clip_len(-1 + q * h, -1 + (q + 1) * h, -1 + r * h, -1 + (r + 1) * h, p0, om)
+        got = np.zeros(N * N)
+        np.add.at(got, pix, ln)
+        assert len(set(pix.tolist())) == len(pix)
+        assert np.abs(got - ref).max() <= 1e-12
+        assert np.all(np.diff(tm) > 0)
+        rows, cols = pix // N, pix % N
+        assert np.all(np.maximum(np.abs(np.diff(rows)), np.abs(np.diff(cols))) == 1)
+        chord = _clip_len(-1, 1, -1, 1, p0, om)
+        assert abs(ln.sum() - chord) <= 1e-12
+
+
+def test_p19_uniform_square_is_the_chord():
+    """mu = 0, lam = 1 on the whole grid: every ray reads the chord of the square [-1,1]^2, in closed
+    form 2 at theta = 0, pi/2 (|s| < 1) and 2 sqrt2 - 2|s| at theta = pi/4 (|s| < sqrt2); y = sum_j w_j chord.
+    (J = 2: no sub-ray runs exactly along the square's edge, a measure-zero case either reading allows.)"""
+    g = small(n_px=16, n_angles=8, J=2, n_det=21, **PB)
+    lam, mu = np.ones(O.img_shape(g)), np.zeros(O.img_shape(g))
+    y = O.forward(g, lam, mu)[0]
+    T = O.tables(g)
+    w, off = T["weights"], T["offsets"]
+    for a, chord in ((0, lambda s: np.where(np.abs(s) < 1, 2.0, 0.0)),
+                     (2, lambda s: np.where(np.abs(s) < 1, 2.0, 0.0)),
+                     (1, lambda s: np.maximum(2 * math.sqrt(2) - 2 * np.abs(s), 0.0))):
+        for b in range(2):
+            ref = (chord(off[b]) * w[None, :]).sum(axis=1)
+            assert np.abs(y[a, b] - ref).max() <= 1e-12
+
+
+def test_p19_mu0_is_the_line_integral_of_the_pixel_field():
+    """mu = 0: the reading is the line integral of the piecewise-constant emission field, checked
+    against brute-force sampling of that field along each sub-ray (step 2e-5: error <= 2N jumps x step
+    x max), weighted by w_j.  (J = 2 and 5 angles: no ray runs along a pixel edge, where the two
+    readings may pick either side.)"""
+    g = small(n_px=10, n_angles=5, J=2, n_det=8, **PB)
+    N = 10
+    h = 2.0 / N
+    lam = rand_img(g, 19, 0.2, 1.5)
+    y = O.forward(g, lam, np.zeros_like(lam))[0]
+    T = O.tables(g)
+    dt = 2e-5
+    t = np.arange(-1.5, 1.5, dt) + dt / 2
+    for a in range(5):
+        for b in range(2):
+            c, s = T["dirs"][a, b]
+            for d in range(8):
+                ref = 0.0
+                for j in range(2):
+                    sig = T["offsets"][b, d, j]
+                    x, yy = -sig * s + t * c, sig * c + t * s
+                    ins = (np.abs(x) < 1) & (np.abs(yy) < 1)
+                    col = np.clip(np.floor((x[ins] + 1) / h).astype(int), 0, N - 1)
+                    row = np.clip(np.floor((yy[ins] + 1) / h).astype(int), 0, N - 1)
+                    ref += T["weights"][j] * lam[0, row, col].sum() * dt
+                assert abs(y[a, b, d] - ref) <= 2 * (2 * N + 2) * dt * lam.max()
+
+
+@pytest.mark.parametrize("mu0", [0.7, 3.0])
+def test_p19_attenuated_square_bracketed_by_the_exact_integral(mu0):
+    """lam = 1 on the square, mu = mu0 on its left half (x < 0): the exact attenuated transform along
+    theta = 0 (detector at +x) is 1 + (1 - e^{-mu0})/mu0 for |s| < 1, along theta = pi (detector at
+    -x) e^{-mu0} + (1 - e^{-mu0})/mu0.  Per pixel the midpoint reading l e^{-mu (A + l/2)} and the exact
+    e^{-mu A} (1 - e^{-mu l})/mu differ by the factor sinh(x/2)/(x/2), x = mu l, so
+    y <= exact <= y sinh(x/2)/(x/2) at x = mu0 h (a dropped 1/2, a reversed direction or a missing term
+    leaves the bracket); the readings also equal the geometric series of the midpoint terms."""
+    N = 16
+    h = 2.0 / N
+    g = small(n_px=N, n_angles=2, J=1, n_det=15, **PB)
+    lam = np.ones(O.img_shape(g))
+    mu = np.zeros(O.img_shape(g))
+    mu[0, :, : N // 2] = mu0
+    y = O.forward(g, lam, mu)[0]
+    s = O.tables(g)["offsets"][0, :, 0]
+    sel = np.abs(s) < 1 - 1e-9
+    x = mu0 * h
+    fac = math.sinh(x / 2) / (x / 2)
+    e0 = 1 + (1 - math.exp(-mu0)) / mu0
+    e1 = math.exp(-mu0) + (1 - math.exp(-mu0)) / mu0
+    assert abs(e0 - e1) > 0.05
+    for a, b, ex in ((0, 0, e0), (0, 1, e1), (1, 0, e1), (1, 1, e0)):
+        yy = y[a, b, sel]
+        assert np.all(yy <= ex * (1 + 1e-12))
+        assert np.all(ex <= yy * fac * (1 + 1e-12))
+        # and exactly: the N/2 attenuating pixels of length h form a geometric series
+        geo = h * math.exp(-x / 2) * math.expm1(-N // 2 * x) / math.expm1(-x)
+        mid = (1.0 if ex == e0 else math.exp(-mu0)) + geo
+        assert np.abs(yy - mid).max() <= 1e-13
+
+
+def test_p19_rotation_invariance():
+    """90 and 180 degree rotations of the images shift the sinogram by nA/4, nA/2 angles (J = 2: no ray
+    on a pixel edge, where the midpoint rule picks the upper / right pixel and the symmetry is lost)."""
+    g = small(n_px=14, n_angles=8, J=2, n_det=13, **PB)
+    lam, mu = rand_img(g, 31), rand_img(g, 32, 0, 0.8)
+    nA = 8
+    y = O.forward(g, lam, mu)
+    r90 = lambda im: np.transpose(im, (0, 2, 1))[:, :, ::-1]
+    assert rel_l2(O.forward(g, r90(lam), r90(mu)), np.roll(y, nA // 4, axis=1)) <= 1e-12
+    assert rel_l2(O.forward(g, lam[:, ::-1, ::-1], mu[:, ::-1, ::-1]), np.roll(y, nA // 2, axis=1)) <= 1e-12
+
+
+@pytest.mark.parametrize("var", [False, True])
+def test_p19_jvp_central_differences(var):
+    g = small(n_px=20, n_angles=10, J=3, n_det=11, **PB, **(VAR if var else {}))
+    lam, mu = rand_img(g, 40, 0, 1.5), rand_img(g, 41, 0, 0.6)
+    un = math.sqrt(np.sum(lam ** 2) + np.sum(mu ** 2))
+    for k in range(10):
+        rng = np.random.default_rng(400 + k)
+        dl = rng.uniform(-1, 1, lam.shape)
+        dm = rng.uniform(-0.1, 0.1, mu.shape)
+        eps = 1e-6 * un / math.sqrt(np.sum(dl ** 2) + np.sum(dm ** 2))
+        fd = (O.forward(g, lam + eps * dl, mu + eps * dm) - O.forward(g, lam - eps * dl, mu - eps * dm)) / (2 * eps)
+        assert rel_l2(O.jvp(g, lam, mu, dl, dm), fd) <= 1e-7
+    # the lambda part of the JVP is the forward of dlam (linear in lambda)
+    dl = rand_img(g, 42, -1, 1)
+    assert rel_l2(O.jvp(g, lam, mu, dl, np.zeros_like(mu)), O.forward(g, dl, mu)) <= 1e-13
+
+
+@pytest.mark.parametrize("var", [False, True])
+def test_p19_adjoint_identity_and_dense_transpose(var):
+    g = small(n_px=12, n_angles=6, J=2, n_det=9, **PB, **(VAR if var else {}))
+    for k in range(50):
+        rng = np.random.default_rng(5000 + k)
+        lam = rng.uniform(0, 1.5, O.img_shape(g))
+        mu = rng.uniform(0, 0.6, O.img_shape(g))
+        vl, vm = rng.standard_normal(O.img_shape(g)), rng.standard_normal(O.img_shape(g))
+        w = rng.standard_normal(O.sino_shape(g))
+        jv = O.jvp(g, lam, mu, vl, vm)
+        gl, gm = O.vjp(g, lam, mu, w)
+        assert abs(np.sum(jv * w) - np.sum(vl * gl) - np.sum(vm * gm)) <= 1e-10 * np.linalg.norm(jv) * np.linalg.norm(w)
+    g = dict(n_px=6, n_angles=4, n_banks=2, n_det=5, n_subrays=2, subray_sigma=0.4, step_px=0.5,
+             bank1_shift=0.0, batch=1, **PB, **(dict(VAR, det_radius=2.5) if var else {}))
+    rng = np.random.default_rng(7)
+    lam, mu = rng.uniform(0.2, 1.5, (1, 6, 6)), rng.uniform(0.1, 0.6, (1, 6, 6))
+    npx = 36
+    Jd = np.stack([O.jvp(g, lam, mu, e[:npx].reshape(1, 6, 6), e[npx:].reshape(1, 6, 6)).ravel()
+                   for e in np.eye(2 * npx)], axis=1)
+    JT = np.stack([np.concatenate([x.ravel() for x in O.vjp(g, lam, mu, e.reshape(O.sino_shape(g)))])
+                   for e in np.eye(Jd.shape[0])], axis=0)
+    assert np.abs(JT - Jd).max() <= 1e-12 * np.abs(Jd).max()
+
+
+def test_p19_variant_reduces_and_changes():
+    """With the O13 response at zero slopes the pixel basis is unchanged (sum_j W_j = 1 and w_j = W_j(d)
+    at r_slope 0, c = 1); the variant alone at nonzero c lowers every reading (c >= 1 in the exponent)."""
+    g = small(n_px=16, n_angles=6, J=3, n_det=11, **PB)
+    lam, mu = rand_img(g, 50, 0.1, 1.2), rand_img(g, 51, 0.05, 0.6)
+    y0 = O.forward(g, lam, mu)
+    y1 = O.forward(dict(g, det_radius=1.6, c_slope=0.0, r_slope=0.0), lam, mu)
+    assert np.abs(y1 - y0).max() <= 1e-13 * np.abs(y0).max()
+    yc = O.forward(dict(g, det_radius=1.6, c_slope=0.1, r_slope=0.0), lam, mu)
+    assert np.all(yc[y0 > 0] < y0[y0 > 0])
+
+
+def test_p19_attenuated_disk_converges():
+    """The north star's disk closed form g(s) = (1 - e^{-mu0 2 sqrt(R^2 - s^2)})/mu0 for the pixelated
+    (area-fraction) disk: the pixel-basis readings converge to it at first order in h."""
+    means = []
+    for N in (64, 128, 256):
+        g = dict(_disk_geom(N), **PB)
+        lam, mu = P.disk_phantom(N, 0.5, 1.0, 0.5)
+        y = O.forward(g, lam, mu)[0]
+        s = O.tables(g)["offsets"][0, :, 0]
+        sel = np.abs(s) <= 0.9 * 0.5
+        chord = 2 * np.sqrt(np.maximum(0.25 - s ** 2, 0))
+        ref = (1 - np.exp(-0.5 * chord)) / 0.5
+        err = np.abs(y[:, 0, sel] - ref[sel]) / ref[sel]
+        assert err.max() <= 0.3 * 64 / N
+        means.append(err.mean())
+    assert means[0] / means[1] >= 1.5 and means[1] / means[2] >= 1.5
+
+
+def test_p19_cg_equals_dense_solve():
+    N = 6
+    g = dict(n_px=N, n_angles=6, n_banks=2, n_det=9, n_subrays=2, subray_sigma=0.4, step_px=0.5,
+             bank1_shift=0.0, batch=1, **PB)
+    rng = np.random.default_rng(12)
+    lam, mu = rng.uniform(0.3, 1.2, (1, N, N)), rng.uniform(0.1, 0.5, (1, N, N))
+    y = O.forward(g, rng.uniform(0.3, 1.2, (1, N, N)), rng.uniform(0.1, 0.5, (1, N, N)))
+    alpha, beta = 1e-2, 0.05
+    Jd, Ld, H = _dense_H(g, lam, mu, alpha, beta)
+    r = (O.forward(g, lam, mu) - y).ravel()
+    u = np.concatenate([lam.ravel(), mu.ravel()])
+    b = -(Jd.T @ r + alpha * Ld.T @ (Ld @ u))
+    sl, sm, st = O.gn_cg_step(g, lam, mu, y, alpha, beta, 200)
+    assert rel_l2(np.concatenate([sl.ravel(), sm.ravel()]), np.linalg.solve(H, b)) <= 1e-8
