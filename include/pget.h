@@ -95,6 +95,16 @@ typedef struct {
     double det_radius;    /* distance from the rotation centre to the detector face (domain units) */
     double c_slope;       /* c_i = 1 + c_slope d_i                                          */
     double r_slope;       /* sigma(d) = sigma_0 (1 + r_slope d)                              */
+    /* Pixel basis (eq:d_fwd_model's d_{m,n,k}, "the distances a ray from m to n
+     * covers within pixel k"; reading R-pb): 1 = lam, mu constant on each pixel, a ray
+     * crosses pixels k_1..k_M (increasing t) with exact intersection lengths l_q and
+     *     A_q = l_q mu_q / 2 + sum_{p>q} l_p mu_p,   g_ray = sum_q r_q lam_q exp(-c_q A_q),
+     * r_q = l_q (times W_j(d_q), c_q = 1 + c_slope d_q with the variant above, d_q at the chord
+     * midpoint), y = sum_j w_j g_ray (w_j inside r_q with the variant); step_px is unused.
+     * 0 = the sampled model above.  Runs unpaired, unsegmented, every angle-bank traced, with the
+     * recomputed GN product (sid.cu). */
+    int32_t pixel_basis;
+    int32_t pad_;
 } pget_geometry_desc;
 
 typedef struct {

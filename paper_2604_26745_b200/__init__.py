@@ -36,7 +36,8 @@ class _Desc(C.Structure):
     _fields_ = [("n_px", C.c_int32), ("n_angles", C.c_int32), ("n_banks", C.c_int32), ("n_det", C.c_int32),
                 ("n_subrays", C.c_int32), ("subray_sigma", C.c_double), ("step_px", C.c_double),
                 ("bank1_shift", C.c_double), ("batch", C.c_int32), ("det_radius", C.c_double),
-                ("c_slope", C.c_double), ("r_slope", C.c_double)]
+                ("c_slope", C.c_double), ("r_slope", C.c_double), ("pixel_basis", C.c_int32),
+                ("pad_", C.c_int32)]
 
 
 class _Info(C.Structure):
@@ -160,7 +161,8 @@ class Geometry:
         d = _Desc(int(desc["n_px"]), int(desc["n_angles"]), int(desc.get("n_banks", 2)), int(desc.get("n_det", 91)),
                   int(desc.get("n_subrays", 1)), float(desc.get("subray_sigma", 0.4)),
                   float(desc.get("step_px", 0.5)), float(desc.get("bank1_shift", 0.0)), int(desc.get("batch", 1)),
-                  float(desc.get("det_radius", 0.0)), float(desc.get("c_slope", 0.0)), float(desc.get("r_slope", 0.0)))
+                  float(desc.get("det_radius", 0.0)), float(desc.get("c_slope", 0.0)), float(desc.get("r_slope", 0.0)),
+                  int(desc.get("pixel_basis", 0)), 0)
         h = C.c_void_p()
         _check(lib().pget_geometry_create(C.byref(d), self.device, C.byref(h)), "pget_geometry_create")
         self._h = h

@@ -3,7 +3,7 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SRC = [os.path.join(HERE, "csrc", f) for f in ("api.cu", "proj.cu", "kernels.cu", "geometry.cpp", "schedule.cpp")]
+SRC = [os.path.join(HERE, "csrc", f) for f in ("api.cu", "proj.cu", "sid.cu", "kernels.cu", "geometry.cpp", "schedule.cpp")]
 DEPS = SRC + [os.path.join(HERE, "csrc", f) for f in ("internal.h", "kernels.cuh")] + [
     os.path.join(os.path.dirname(HERE), "include", "pget.h")]
 LIB = os.path.join(HERE, "libpget.so")

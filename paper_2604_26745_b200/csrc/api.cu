@@ -156,6 +156,7 @@ ProjCfg proj_cfg(const Geometry& g, int mode)
         int64_t wg = want;
         if (const char* ev = std::getenv("PGET_RED_G")) wg = std::max(1, std::atoi(ev));   // experiment
         c.G = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(wg, std::max(1, S.max_slots_member))));
+        if (g.sid) c.G = 1;   // the pixel basis writes one fp64 partial (sid.cu)
     }
     return c;
 }
@@ -309,6 +310,37 @@ ProjArgs base_args(const Geometry& g, const ProjCfg& c)
     return A;
 }
 
+// the pixel basis (N3, R-pb): kernel arguments from the packed images (and outputs) of A
+SidArgs sid_args(const Geometry& g, const ProjArgs& A)
+{
+    SidArgs S;
+    std::memset(&S, 0, sizeof S);
+    S.dir = g.d_sdir;
+    S.off = g.d_soff;
+    S.img2 = A.img2[0];
+    S.img4 = A.img4[0];
+    S.wj = g.var ? g.d_ones : g.d_w;
+    S.dj2 = g.d_sdj2;
+    S.y = A.y;
+    S.dy = A.dy;
+    S.win = A.win;
+    S.nhits = g.sid_nhits;
+    S.det_radius = g.desc.det_radius;
+    S.c_slope = static_cast<float>(g.desc.c_slope);
+    S.r_slope = static_cast<float>(g.desc.r_slope);
+    S.sig0 = static_cast<float>(g.desc.subray_sigma * 2.0 / static_cast<double>(g.desc.n_det - 1));
+    S.lmax = static_cast<float>(std::sqrt(2.0) * g.h * (1.0 + 1e-6));
+    S.N = g.desc.n_px;
+    S.P = g.P;
+    S.R = g.R;
+    S.J = g.desc.n_subrays;
+    S.n_det = g.desc.n_det;
+    S.n_ab = g.n_ab;
+    S.nB = g.desc.n_banks;
+    S.B = g.desc.batch;
+    return S;
+}
+
 pget_status run_proj(const Geometry& g, int mode, const ProjCfg& c, const ProjArgs& A, cudaStream_t s)
 {
     cudaEvent_t ea = nullptr, eb = nullptr;
@@ -323,7 +355,8 @@ pget_status run_proj(const Geometry& g, int mode, const ProjCfg& c, const ProjAr
         }
     }
     if (ea) cudaEventRecord(ea, s);
-    cudaError_t e = launch_proj(mode, c.maxg, c.paired, A, c.grid, c.W * 32, c.smem, s);
+    cudaError_t e = g.sid ? launch_sid_proj(mode, g.var, sid_args(g, A), s)
+                          : launch_proj(mode, c.maxg, c.paired, A, c.grid, c.W * 32, c.smem, s);
     if (eb) cudaEventRecord(eb, s);
     if (e != cudaSuccess) return cuda_fail(e, "projector launch");
     return PGET_OK;
@@ -431,6 +464,11 @@ struct WS {
     float *sl = nullptr, *sm = nullptr, *beta = nullptr;   // pget_lm_solve
     double* part = nullptr;   // [8][B][kNblk]
     CGState* cg = nullptr;
+    // pixel basis (sid.cu): per-ray adjoint weights and sums, bounds, 64-bit fixed-point accumulator
+    float4* sray = nullptr;
+    float2* sraybd = nullptr;
+    unsigned* sbound = nullptr;
+    unsigned long long* sacc = nullptr;
     size_t bytes = 0;
 };
 
@@ -462,6 +500,13 @@ WS carve(const Geometry& g, int op, char* base)
         w.slots = reinterpret_cast<float2*>(take(static_cast<size_t>(std::max(1, g.sch[kSchedAdj].n_slots)) * plane *
                                                  sizeof(float2)));
         w.gacc = reinterpret_cast<double2*>(take(static_cast<size_t>(c.G) * n2 * sizeof(double2)));
+        if (g.sid) {
+            const size_t nr = B * g.n_ab * static_cast<size_t>(g.R);
+            w.sray = reinterpret_cast<float4*>(take(nr * sizeof(float4)));
+            w.sraybd = reinterpret_cast<float2*>(take(nr * sizeof(float2)));
+            w.sbound = reinterpret_cast<unsigned*>(take(2 * B * sizeof(unsigned)));
+            w.sacc = reinterpret_cast<unsigned long long*>(take(2 * n2 * sizeof(unsigned long long)));
+        }
         if (g.adj_seg)
             w.segp = reinterpret_cast<float*>(take(static_cast<size_t>(g.sch[kSchedAdj].n_canon) * kSegFields *
                                                    g.R * sizeof(float)));
@@ -560,6 +605,11 @@ void free_device_tables(Geometry* g)
     g->d_w = nullptr;
     g->d_ones = nullptr;
     g->d_var_cw = nullptr;
+    cudaFree(g->d_sdir);
+    cudaFree(g->d_soff);
+    cudaFree(g->d_sdj2);
+    g->d_sdir = g->d_soff = nullptr;
+    g->d_sdj2 = nullptr;
     for (Schedule& S : g->sch) {
         cudaFree(S.d_cta_begin); cudaFree(S.d_tasks); cudaFree(S.d_groups); cudaFree(S.d_red_off); cudaFree(S.d_red_slot);
         S.d_cta_begin = nullptr; S.d_tasks = nullptr; S.d_groups = nullptr; S.d_red_off = nullptr; S.d_red_slot = nullptr;
@@ -621,7 +671,7 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     // the model variant (N3): its attenuation exp(-c_i A_i) does not factor along a ray, so it runs the
     // whole-ray (fused) projectors, unpaired, with the recomputed GN product
     auto variant_paths = [&g]() {
-        if (!g.var) return;
+        if (!g.var && !g.sid) return;   // the pixel basis (R-pb) likewise: whole rays, sid.cu
         g.adj_seg = g.jvp_seg = g.fwd_seg = false;
         g.gn_cached = false;
         g.pair = false;
@@ -731,6 +781,23 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
         if (e == cudaSuccess) e = cudaMemcpy(g.d_var_cw, cw.data(), cw.size() * sizeof(float2), cudaMemcpyHostToDevice);
         if (e == cudaSuccess) e = cudaMalloc(&g.d_ones, ones.size() * sizeof(float));
         if (e == cudaSuccess) e = cudaMemcpy(g.d_ones, ones.data(), ones.size() * sizeof(float), cudaMemcpyHostToDevice);
+    }
+    if (e == cudaSuccess && g.sid) {   // the pixel basis: fp64 O1 dirs and offsets, delta_j^2 log2(e)
+        const int J = g.desc.n_subrays;
+        const double p = 2.0 / static_cast<double>(g.desc.n_det - 1);
+        std::vector<float> dj2(J);
+        for (int j = 0; j < J; ++j) {
+            const double dj = static_cast<double>(2 * j + 1 - J) / static_cast<double>(2 * J) * p;
+            dj2[j] = static_cast<float>(dj * dj * 1.4426950408889634);
+        }
+        e = cudaMalloc(&g.d_sdir, g.dirs.size() * sizeof(double));
+        if (e == cudaSuccess) e = cudaMemcpy(g.d_sdir, g.dirs.data(), g.dirs.size() * sizeof(double), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMalloc(&g.d_soff, g.offsets.size() * sizeof(double));
+        if (e == cudaSuccess) e = cudaMemcpy(g.d_soff, g.offsets.data(), g.offsets.size() * sizeof(double), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMalloc(&g.d_sdj2, dj2.size() * sizeof(float));
+        if (e == cudaSuccess) e = cudaMemcpy(g.d_sdj2, dj2.data(), dj2.size() * sizeof(float), cudaMemcpyHostToDevice);
+        if (e == cudaSuccess && 2 * sizeof(float) * g.R + 1024 > g.smem_optin) e = cudaErrorInvalidConfiguration;
+        if (e == cudaSuccess) e = set_sid_smem_limit(2 * sizeof(float) * g.R);
     }
     if (e == cudaSuccess) e = cudaMemcpy(g.d_rays, rays.data(), rays.size() * sizeof(RayP), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(g.d_w, g.wf.data(), g.wf.size() * sizeof(float), cudaMemcpyHostToDevice);
@@ -887,6 +954,29 @@ static pget_status proj_adjoint(const Geometry& g, const WS& w, int mode, const 
     for (int k = 0; k < 2; ++k) { A.img2[k] = w.img2[k]; A.img4[k] = w.img4[k]; }
     A.slots = w.slots;
     A.win = win;
+    if (g.sid) {   // pixel basis: bounds, scatter into the fixed-point accumulator, fp64 partials
+        SidArgs S = sid_args(g, A);
+        S.ray = w.sray;
+        S.raybd = w.sraybd;
+        S.bound = w.sbound;
+        S.acc = w.sacc;
+        cudaEvent_t ea = nullptr, eb = nullptr;
+        if (g_prof.on.load(std::memory_order_relaxed)) {
+            std::lock_guard<std::mutex> lk(g_prof.mu);
+            g_prof.total += 3;
+            g_prof.mode_launches[mode]++;
+            if (g_prof.used + 2 <= g_prof.pool.size()) {
+                ea = g_prof.pool[g_prof.used++];
+                eb = g_prof.pool[g_prof.used++];
+                g_prof.recs.push_back({mode, ea, eb});
+            }
+        }
+        if (ea) cudaEventRecord(ea, s);
+        const cudaError_t e = launch_sid_adj(mode, g.var, S, w.gacc, s);
+        if (eb) cudaEventRecord(eb, s);
+        if (e != cudaSuccess) return cuda_fail(e, "pixel-basis adjoint launch");
+        return PGET_OK;
+    }
     if (build_cache && w.gscale)   // the builder's entry bounds start from 0 (atomicMax)
         CK(cudaMemsetAsync(w.gscale, 0, static_cast<size_t>(g.desc.batch) * g.sch[kSchedAdj].ntab * 8 * sizeof(float), s));
     pget_status st = g.adj_seg ? run_seg(g, mode, A, w.segp, s, build_cache ? w.cache : nullptr, have_a, w.gscale)

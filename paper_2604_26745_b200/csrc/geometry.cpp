@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <vector>
 
 #include "internal.h"
 
@@ -40,7 +41,12 @@ pget_status build_geometry(const pget_geometry_desc* d, Geometry* g, std::string
         *err = "invalid model variant (det_radius, c_slope, r_slope must be finite; slopes >= 0)";
         return PGET_ERR_INVALID_ARGUMENT;
     }
+    if (d->pixel_basis != 0 && d->pixel_basis != 1) {
+        *err = "pixel_basis must be 0 or 1";
+        return PGET_ERR_INVALID_ARGUMENT;
+    }
     g->desc = *d;
+    g->sid = d->pixel_basis == 1;
     const int N = d->n_px, nA = d->n_angles, nB = d->n_banks, nd = d->n_det, J = d->n_subrays;
 
     // t-lattice: h = 2/N, Delta = step_px h, T = Delta ceil((sqrt2 + h)/Delta), n_t = 2T/Delta
@@ -174,7 +180,7 @@ pget_status build_geometry(const pget_geometry_desc* d, Geometry* g, std::string
         const double s = g->dirs[static_cast<size_t>(ab) * 2 + 1];
         g->orient[ab] = std::fabs(c) > std::fabs(s) ? 1 : 0;
     }
-    g->dup = (nA % 2 == 0) && nB == 2 && d->bank1_shift == 0.0;
+    g->dup = (nA % 2 == 0) && nB == 2 && d->bank1_shift == 0.0 && !g->sid;   // pixel basis: every angle-bank
     g->pair = g->dup && !g->var;   // the variant's opposite-direction attenuation does not factor
     auto traced = [&](int ab) { return !g->dup || (ab / nB) < nA / 2; };
     for (int cls = 0; cls < 2; ++cls)
@@ -220,6 +226,53 @@ pget_status build_geometry(const pget_geometry_desc* d, Geometry* g, std::string
         const double n_near = (std::floor(2.0 * std::sqrt(2.0) / a) + 2.0) * (std::floor(2.0 * std::sqrt(2.0) / st) + 2.0);
         g->cellmax = static_cast<int>(std::floor(std::sqrt(2.0) / st)) + 1;
         g->gnb_int = n_near < 512.0 * g->cellmax;
+    }
+    if (g->sid) {
+        // crossings per ray (interior pixel edges of both axes + 1: the pixel-basis "samples") and the
+        // most rays through one pixel: per bank, the most offsets inside any window of the width of a
+        // pixel's projection (<= sqrt2 h), summed over the angle-banks (the fixed-point scale, sid.cu)
+        const double hN = 0.5 * N;
+        int64_t cross = 0;
+        for (int ab = 0; ab < g->n_ab; ++ab) {
+            const int b = ab % nB;
+            const double c = g->dirs[static_cast<size_t>(ab) * 2], s = g->dirs[static_cast<size_t>(ab) * 2 + 1];
+            for (int r = 0; r < g->R; ++r) {
+                const double sigma = g->offsets[static_cast<size_t>(b) * g->R + r];
+                const double X0[2] = {(-sigma * s + 1.0) * hN, (sigma * c + 1.0) * hN}, w[2] = {c * hN, s * hN};
+                double tin = -INFINITY, tout = INFINITY;
+                bool ok = true;
+                for (int k = 0; k < 2; ++k) {
+                    if (w[k] == 0.0) { ok = ok && X0[k] > 0.0 && X0[k] < N; continue; }
+                    const double t1 = -X0[k] / w[k], t2 = (N - X0[k]) / w[k];
+                    tin = std::max(tin, std::min(t1, t2));
+                    tout = std::min(tout, std::max(t1, t2));
+                }
+                if (!ok || !(tin < tout)) continue;
+                int64_t n = 1;
+                for (int k = 0; k < 2; ++k) {
+                    const double a = X0[k] + tin * w[k], e = X0[k] + tout * w[k];
+                    const double lo = std::min(a, e), hi = std::max(a, e);
+                    n += std::max<int64_t>(0, static_cast<int64_t>(std::ceil(hi)) - static_cast<int64_t>(std::floor(lo)) - 1);
+                }
+                cross += n;
+            }
+        }
+        g->n_samples_nominal = cross * d->batch;
+        g->n_samples_traced = g->n_samples_nominal;
+        const double win = std::sqrt(2.0) * g->h * (1.0 + 1e-9);
+        double nh = 0.0;
+        for (int b = 0; b < nB; ++b) {
+            std::vector<double> o(g->offsets.begin() + static_cast<size_t>(b) * g->R,
+                                  g->offsets.begin() + static_cast<size_t>(b + 1) * g->R);
+            std::sort(o.begin(), o.end());
+            int best = 0;
+            for (size_t i = 0, k = 0; i < o.size(); ++i) {
+                while (o[i] - o[k] > win) ++k;
+                best = std::max(best, static_cast<int>(i - k + 1));
+            }
+            nh += best;
+        }
+        g->sid_nhits = nh * nA;
     }
     return PGET_OK;
 }

@@ -138,6 +138,13 @@ struct Geometry {
     // model variant (N3, reading R-N3; desc.det_radius > 0): c_i [n_t], W_j(d_i) [J][n_t]
     bool var = false;
     std::vector<double> var_c, var_w;
+    // pixel basis (N3, reading R-pb; desc.pixel_basis): exact intersection lengths (sid.cu), unpaired,
+    // every angle-bank traced; sid_nhits bounds the rays through one pixel (the fixed-point scale)
+    bool sid = false;
+    double sid_nhits = 0.0;
+    double* d_sdir = nullptr;     // [n_ab][2] dirs
+    double* d_soff = nullptr;     // [n_banks][R] offsets
+    float* d_sdj2 = nullptr;      // [J] delta_j^2 log2(e)
     int64_t n_samples_nominal;
     int64_t n_samples_traced = 0;
     // launch geometry

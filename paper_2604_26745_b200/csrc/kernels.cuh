@@ -81,6 +81,30 @@ struct ProjArgs {
     int n_t;
 };
 
+// pixel-basis model variant (N3, reading R-pb; sid.cu): one CTA per (angle-bank, member)
+struct SidArgs {
+    const double* dir;      // [n_ab][2] (cos phi, sin phi), the O1 table
+    const double* off;      // [n_banks][R] offsets sigma, the O1 table
+    const float2* img2;     // [B][P][P] (lam, mu), normal orientation, zero halo
+    const float4* img4;     // [B][P][P] (lam, mu, dlam, dmu)
+    const float* wj;        // [J] sub-ray weights outside the ray sums (ones with the response)
+    const float* dj2;       // [J] delta_j^2 log2(e) (response)
+    float* y;               // [B][n_ab][n_det]
+    float* dy;
+    const float* win;       // VJP weights [B][n_ab][n_det]
+    float4* ray;            // [B][n_ab][R] adjoint pass 1: (w_r, G, Gc, -)
+    float2* raybd;          // [B][n_ab][R] (sum r E, sum r |lam| c E)
+    unsigned* bound;        // [B][2] float bits: per-member magnitude bounds (lam, mu planes)
+    unsigned long long* acc;   // [B][2][N][N] 64-bit fixed-point adjoint (lam plane, mu plane)
+    double nhits;           // rays through one pixel, at most (all angle-banks)
+    double det_radius;
+    float c_slope, r_slope, sig0, lmax;
+    int N, P, R, J, n_det, n_ab, nB, B;
+};
+cudaError_t launch_sid_proj(int mode, bool var, const SidArgs& A, cudaStream_t s);
+cudaError_t launch_sid_adj(int mode, bool var, const SidArgs& A, double2* gacc, cudaStream_t s);
+cudaError_t set_sid_smem_limit(size_t bytes);
+
 constexpr int kSegFields = 9;
 // rows of 32 entries allocated past the end of the GN coefficient cache: gnb_kernel's entry ring and
 // L2 prefetch read ahead of a lane's last sample without bounds checks (the values are never used)

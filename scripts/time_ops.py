@@ -13,6 +13,10 @@ import pget_data as P  # noqa: E402
 cid = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 reps = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 20
 gd = P.geometry_desc(cid)
+if "--pb" in sys.argv:    # the pixel basis (N3, reading R-pb)
+    gd["pixel_basis"] = 1
+if "--var" in sys.argv:   # the response of reading R-N3
+    gd.update(det_radius=1.6, c_slope=0.05, r_slope=0.35)
 g = pg.Geometry(gd)
 dev = lambda x: torch.from_numpy(np.ascontiguousarray(x, np.float32)).cuda()
 lam, mu = map(dev, P.make_phantom(cid))
@@ -56,4 +60,4 @@ for name, f in ops.items():
         b.synchronize()
         ts.append(a.elapsed_time(b))
     out[name] = float(np.median(ts))
-print(f"cfg{cid}", " ".join(f"{k}={v:.4f}ms({nom / v / 1e6:.3g}Gs/s)" for k, v in out.items()), flush=True)
+print(f"cfg{cid}" + ("-pb" if "--pb" in sys.argv else "") + ("-var" if "--var" in sys.argv else ""), " ".join(f"{k}={v:.4f}ms({nom / v / 1e6:.3g}Gs/s)" for k, v in out.items()), flush=True)

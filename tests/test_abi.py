@@ -171,3 +171,32 @@ def test_variant_desc_validation():
     for gd in bad:
         with pytest.raises(RuntimeError, match="INVALID_ARGUMENT"):
             pg.Geometry(gd, device=-1)
+
+
+def test_pixel_basis_host_handle():
+    """Pixel basis (N3, reading R-pb): the descriptor carries pixel_basis (88-byte struct), the handle
+    traces every angle-bank (no merging), its sample count is the crossing count of the oracle's O14
+    traversal up to corner coincidences (an edge pair crossed at one t counts once there), and values
+    other than 0 / 1 are rejected."""
+    import ctypes as C
+    assert C.sizeof(pg._Desc) == 88
+    gd = dict(n_px=12, n_angles=6, n_banks=2, n_det=9, n_subrays=3, subray_sigma=0.4, step_px=0.5,
+              bank1_shift=0.0, batch=2, pixel_basis=1)
+    g = pg.Geometry(gd, device=-1)
+    assert g.info["angle_banks_merged"] == 0
+    T = O.tables(gd)
+    ref = 0
+    for a in range(6):
+        for b in range(2):
+            c, s = T["dirs"][a, b]
+            for d in range(9):
+                for j in range(3):
+                    ref += len(O.pb_crossings(12, c, s, T["offsets"][b, d, j])[0])
+    n_rays = 6 * 2 * 9 * 3
+    assert 2 * ref <= g.info["n_samples_nominal"] <= 2 * (ref + n_rays)
+    assert g.info["n_samples_traced"] == g.info["n_samples_nominal"]
+    for c in (2, 4):
+        h = pg.Geometry(dict(P.geometry_desc(c), pixel_basis=1), device=-1)
+        assert h.info["angle_banks_merged"] == 0
+    with pytest.raises(RuntimeError, match="INVALID_ARGUMENT"):
+        pg.Geometry(dict(gd, pixel_basis=2), device=-1)
