@@ -1604,20 +1604,25 @@ __device__ __forceinline__ void red_s32(uint32_t addr, int v)
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
 template <bool INTACC>
-__device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0, int r1, int abase, int sP, int ilo,
+__device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0, int r1, int ilo,
                                          int64_t dU, int64_t dV, float wr, float wr1, int& i, int64_t& u, int64_t& v,
                                          const float4*& ck, const float4* cend, float2 S, uint32_t planeB)
 {
+    const int sP = P;   // accumulator row of sample row iv: iv - r0
     const int iv0 = hi32(v);
     if (i < ilo || iv0 < r0 || iv0 >= r1) return;
     int n = band_steps(i, ilo, v, dV, r0, r1);
-    const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(acc));
-    auto rmw = [&](int off, float2 a, float2 b, float2 c, float2 d) {
+    // byte address of a sample's cell in the shared accumulator: org + iv * sP4 + iu * 4 (INTACC), with
+    // org the address of (row 0, col 0) for this band's row mapping (abase + (iv - r0) sP + iu)
+    const int sP4 = sP * 4;
+    const uint32_t org = static_cast<uint32_t>(__cvta_generic_to_shared(acc)) - static_cast<uint32_t>(r0 * sP * 4);
+    auto cell = [&](int ivv, int iuu) -> uint32_t { return org + static_cast<uint32_t>(ivv * sP4 + iuu * 4); };
+    auto rmw = [&](uint32_t a0, float2 a, float2 b, float2 c, float2 d) {
         if constexpr (INTACC) {
             const float2 mg = make_float2(12582912.f, 12582912.f);   // 1.5 * 2^23
             const float2 ta = __ffma2_rn(a, S, mg), tb = __ffma2_rn(b, S, mg);
             const float2 tc = __ffma2_rn(c, S, mg), td = __ffma2_rn(d, S, mg);
-            const uint32_t a0 = sbase + static_cast<uint32_t>(off * 4), a1 = sbase + static_cast<uint32_t>((off + sP) * 4);
+            const uint32_t a1 = a0 + static_cast<uint32_t>(sP4);
             red_s32(a0, __float_as_int(ta.x) - 0x4B400000);
             red_s32(a0 + planeB, __float_as_int(ta.y) - 0x4B400000);
             red_s32(a0 + 4, __float_as_int(tb.x) - 0x4B400000);
@@ -1627,7 +1632,8 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
             red_s32(a1 + 4, __float_as_int(td.x) - 0x4B400000);
             red_s32(a1 + 4 + planeB, __float_as_int(td.y) - 0x4B400000);
         } else {
-            float2* pa = acc + off;
+            // element index: cell() counts 4 bytes per element in both layouts
+            float2* pa = acc + (static_cast<int>(a0 - static_cast<uint32_t>(__cvta_generic_to_shared(acc))) >> 2);
             const float2 t00 = pa[0], t01 = pa[1], t10 = pa[sP], t11 = pa[sP + 1];
             pa[0] = make_float2(t00.x + a.x, t00.y + a.y);
             pa[1] = make_float2(t01.x + b.x, t01.y + b.y);
@@ -1636,8 +1642,7 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
         }
     };
     // the pending cell starts as the first sample's (valid address, zero sums): no first-time test
-    int iv = iv0;
-    int poff = abase + (iv - r0) * sP + hi32(u);
+    uint32_t pa = cell(iv0, hi32(u));
     const float2 z2 = make_float2(0.f, 0.f);
     float2 p00 = z2, p01 = z2, p10 = z2, p11 = z2;
     const float4* const p0 = ck;
@@ -1645,7 +1650,8 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
     float4 c0 = __ldg(p0), c1 = __ldg(p0 + 32), c2 = __ldg(p0 + 64), c3 = __ldg(p0 + 96);
     const float2 w2 = make_float2(wr, wr), w12 = make_float2(wr1, wr1);
     auto step = [&](float4& c) -> bool {
-        const int aoff = abase + (iv - r0) * sP + hi32(u);
+        const int iv = hi32(v);
+        const uint32_t aa = cell(iv, hi32(u));
         PGET_CHECK(hi32(u) >= 0 && hi32(u) + 1 < P && iv >= r0 && iv < r1 && p0 + k * 32 < cend);
         const float fu = frac23(u), fv = frac23(v);
         const float2 av = __ffma2_rn(w2, make_float2(c.x, c.y), __fmul2_rn(w12, make_float2(c.z, c.w)));
@@ -1658,9 +1664,9 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
         const float2 c10 = __ffma2_rn(c11, make_float2(-1.f, -1.f), tv);
         const float2 c01 = __fmul2_rn(bv, make_float2(fu, fu));
         const float2 c00 = __ffma2_rn(c01, make_float2(-1.f, -1.f), bv);
-        if (aoff != poff) {
-            if (PGET_ABLATE != 1 || p00.x == 12345.f) rmw(poff, p00, p01, p10, p11);   // ABLATE 1: no scatter
-            poff = aoff;
+        if (aa != pa) {
+            if (PGET_ABLATE != 1 || p00.x == 12345.f) rmw(pa, p00, p01, p10, p11);   // ABLATE 1: no scatter
+            pa = aa;
             p00 = c00; p01 = c01; p10 = c10; p11 = c11;
         } else {
             p00 = __fadd2_rn(p00, c00);
@@ -1670,12 +1676,11 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
         }
         u -= dU;
         v -= dV;
-        iv = hi32(v);
         return --n != 0;
     };
     while (step(c0) && step(c1) && step(c2) && step(c3)) {
     }
-    rmw(poff, p00, p01, p10, p11);
+    rmw(pa, p00, p01, p10, p11);
     i -= k;
     ck = p0 + (k << 5);
 }
@@ -1989,14 +1994,13 @@ __global__ void __launch_bounds__(WIDE ? 832 : 512, 1) gnb_kernel(ProjArgs A)
             for (int j = 0; j < ui.nb; ++j) {
                 int r0, r1;
                 seg_band(ui, j, Rb, r0, r1);
-                const bool flip = j & 1;
-                const int abase = flip ? Rb * P : 0, sP = flip ? -P : P;
+                // the band's accumulator rows are r - r0 (no flipping): the row it shares with the next
+                // band is flushed with it, zeroed, and collects the next band's part (slot adds twice)
                 if (PGET_ABLATE != 3)   // 3: no walk
-                    walk_gnb<INTACC>(wacc, P, r0, r1, abase, sP, ilo, dU, dV, wr, wr1, ii, uu, vv, cl, cend, S,
+                    walk_gnb<INTACC>(wacc, P, r0, r1, ilo, dU, dV, wr, wr1, ii, uu, vv, cl, cend, S,
                                      static_cast<uint32_t>(RB1 * P * 4));
                 __syncthreads();   // every warp ring complete
-                const bool last = j == ui.nb - 1;
-                const int carry = last ? -1 : (ui.dir > 0 ? r0 : r1);
+                const int carry = -1;
                 int qlo, qhi;
                 {
                     const double a0 = ucol(rfirst, r0 - 1.0), a1 = ucol(rfirst, r1 + 1.0);
@@ -2011,7 +2015,7 @@ __global__ void __launch_bounds__(WIDE ? 832 : 512, 1) gnb_kernel(ProjArgs A)
                     int q = e - rw * npairs;
                     if (q < 0) { --rw; q += npairs; } else if (q >= npairs) { ++rw; q -= npairs; }
                     if (rw == carry || q < qlo || q > qhi || PGET_ABLATE == 2) continue;   // 2: no flush
-                    const int lr = flip ? r0 + Rb - rw : rw - r0;
+                    const int lr = rw - r0;
                     PGET_CHECK(lr >= 0 && lr < RB1);
                     float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
                     if constexpr (INTACC) {
