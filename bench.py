@@ -169,7 +169,7 @@ def reference_arm(args, rank, world):
         "config": {"workload": workload(cfg), "sample": sample["desc"]},
         "cpu_baseline": {"value": value, "unit": "ray-samples/s", "cores": O.threads(), "kind": "oracle",
                          "sample": sample["desc"], "cpu_model": cpu_model(),
-                         "omp_num_threads": os.environ.get("OMP_NUM_THREADS")},
+                         "omp_num_threads": os.environ.get("OMP_NUM_THREADS", f"unset (OpenMP default: {O.threads()} threads)")},
         "e2e": {"value": value, "unit": "ray-samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -529,7 +529,7 @@ def main():
         s = cpu_sample(cfg, args.ref_angles or REF_ANGLES[cfg.cid])
         dt, n = run_oracle_step(O, P, cfg, s)
         cpu = {"value": n / dt, "unit": "ray-samples/s", "cores": O.threads(), "kind": "oracle",
-               "sample": s["desc"], "cpu_model": cpu_model(), "omp_num_threads": os.environ.get("OMP_NUM_THREADS")}
+               "sample": s["desc"], "cpu_model": cpu_model(), "omp_num_threads": os.environ.get("OMP_NUM_THREADS", f"unset (OpenMP default: {O.threads()} threads)")}
 
     per_config = None
     if rank == 0 and world == 1 and not args.no_per_config:
