@@ -1925,8 +1925,6 @@ __global__ void __launch_bounds__(WIDE ? 832 : 512, 1) gnb_kernel(ProjArgs A)
         const int n4 = NACC * RB1 * P / 2;
         for (int k = tid; k < n4; k += NT) z[k] = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-    const int npairs = P >> 1;
-    const float inv_np = 1.0f / static_cast<float>(npairs);
     const size_t plane = static_cast<size_t>(A.N) * A.Ns;
     for (int u = A.u_begin[c]; u < A.u_begin[c + 1]; ++u) {
         const UnitInfo ui = unit_info(A, u, Rb);
@@ -2000,7 +1998,6 @@ __global__ void __launch_bounds__(WIDE ? 832 : 512, 1) gnb_kernel(ProjArgs A)
                     walk_gnb<INTACC>(wacc, P, r0, r1, ilo, dU, dV, wr, wr1, ii, uu, vv, cl, cend, S,
                                      static_cast<uint32_t>(RB1 * P * 4));
                 __syncthreads();   // every warp ring complete
-                const int carry = -1;
                 int qlo, qhi;
                 {
                     const double a0 = ucol(rfirst, r0 - 1.0), a1 = ucol(rfirst, r1 + 1.0);
@@ -2009,35 +2006,39 @@ __global__ void __launch_bounds__(WIDE ? 832 : 512, 1) gnb_kernel(ProjArgs A)
                     qlo = max(0, static_cast<int>(floor(umin)) - 2) >> 1;
                     qhi = min(P - 1, static_cast<int>(floor(umax)) + 3) >> 1;
                 }
-                const int e_beg = r0 * npairs, e_end = (r1 + 1) * npairs;
-                for (int e = e_beg + (tid - e_beg % NT + NT) % NT; e < e_end; e += NT) {
-                    int rw = __float2int_rd(static_cast<float>(e) * inv_np);
-                    int q = e - rw * npairs;
-                    if (q < 0) { --rw; q += npairs; } else if (q >= npairs) { ++rw; q -= npairs; }
-                    if (rw == carry || q < qlo || q > qhi || PGET_ABLATE == 2) continue;   // 2: no flush
+                // element (row rw, pair q) is flushed by warp rw mod W, lane q mod 32 in every band: each
+                // slot element always by the same thread, in program order (deterministic), without the
+                // flat index's division; only the pairs [qlo, qhi] the band's rays can reach
+                int rw = r0 + ((warp - r0 % W) % W + W) % W;
+                const int qs = qlo + ((lane - qlo % 32) % 32 + 32) % 32;
+                for (; rw <= r1 && PGET_ABLATE != 2; rw += W) {   // 2: no flush
                     const int lr = rw - r0;
                     PGET_CHECK(lr >= 0 && lr < RB1);
-                    float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
-                    if constexpr (INTACC) {
-                        int2* el = reinterpret_cast<int2*>(wacc_all) + static_cast<size_t>(lr) * (P / 2) + q;
-                        int2* em = el + static_cast<size_t>(RB1) * (P / 2);   // mu plane
-                        const int2 xl = *el, xm = *em;
-                        *el = make_int2(0, 0);
-                        *em = make_int2(0, 0);
-                        sum = make_float4(static_cast<float>(xl.x) * iS.x, static_cast<float>(xm.x) * iS.y,
-                                          static_cast<float>(xl.y) * iS.x, static_cast<float>(xm.y) * iS.y);
-                    } else {
+                    const int ir = rw - kHalo;
+                    const bool inrow = ir >= 0 && ir < A.N;
+                    for (int q = qs; q <= qhi; q += 32) {
+                        float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+                        if constexpr (INTACC) {
+                            int2* el = reinterpret_cast<int2*>(wacc_all) + static_cast<size_t>(lr) * (P / 2) + q;
+                            int2* em = el + static_cast<size_t>(RB1) * (P / 2);   // mu plane
+                            const int2 xl = *el, xm = *em;
+                            *el = make_int2(0, 0);
+                            *em = make_int2(0, 0);
+                            sum = make_float4(static_cast<float>(xl.x) * iS.x, static_cast<float>(xm.x) * iS.y,
+                                              static_cast<float>(xl.y) * iS.x, static_cast<float>(xm.y) * iS.y);
+                        } else {
 #pragma unroll 4
-                        for (int w = 0; w < W; ++w) {
-                            float4* el = reinterpret_cast<float4*>(wacc_all + (static_cast<size_t>(w) * RB1 + lr) * P) + q;
-                            const float4 x = *el;
-                            sum.x += x.x; sum.y += x.y; sum.z += x.z; sum.w += x.w;
-                            *el = make_float4(0.f, 0.f, 0.f, 0.f);
+                            for (int w = 0; w < W; ++w) {
+                                float4* el = reinterpret_cast<float4*>(wacc_all + (static_cast<size_t>(w) * RB1 + lr) * P) + q;
+                                const float4 x = *el;
+                                sum.x += x.x; sum.y += x.y; sum.z += x.z; sum.w += x.w;
+                                *el = make_float4(0.f, 0.f, 0.f, 0.f);
+                            }
                         }
+                        const int ic = 2 * q - kHalo;
+                        if (inrow && ic >= 0 && ic < A.Ns)
+                            atomicAdd(reinterpret_cast<float4*>(slot + static_cast<size_t>(ir) * A.Ns + ic), sum);
                     }
-                    const int ir = rw - kHalo, ic = 2 * q - kHalo;
-                    if (ir >= 0 && ir < A.N && ic >= 0 && ic < A.Ns)
-                        atomicAdd(reinterpret_cast<float4*>(slot + static_cast<size_t>(ir) * A.Ns + ic), sum);
                 }
                 __syncthreads();   // rings zeroed before the next band's scatter
             }

@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "kernels.cuh"
@@ -214,7 +215,7 @@ __device__ __forceinline__ RayState ray_sums(const SidArgs& A, int m, int ab, in
 
 // ---- forward / JVP: per-ray sums, then the sub-ray weighting into the detector readings
 template <int MODE, bool VAR>
-__global__ void __launch_bounds__(256, 1) sid_proj_kernel(SidArgs A)
+__global__ void __launch_bounds__(512, 1) sid_proj_kernel(SidArgs A)
 {
     pdl_entry();
     extern __shared__ float rout[];   // [2R]
@@ -240,11 +241,11 @@ __global__ void __launch_bounds__(256, 1) sid_proj_kernel(SidArgs A)
 // ---- adjoint pass 1 (VJP: weights from A.win; GN: the (J p) of A.img4's p): per ray the weight w_r,
 // G (compensated) into A.ray, and the member's magnitude bounds max|w| sum r E, max|w| l_max sum r|lam|cE
 template <int MODE, bool VAR>
-__global__ void __launch_bounds__(256, 1) sid_adj_a_kernel(SidArgs A)
+__global__ void __launch_bounds__(512, 1) sid_adj_a_kernel(SidArgs A)
 {
     pdl_entry();
     extern __shared__ float rout[];   // [R]: GN (J p) per ray
-    __shared__ float red[2][8];
+    __shared__ float red[2][16];
     const int ab = blockIdx.x, m = blockIdx.y, R = A.R, J = A.J;
     const size_t rb = (static_cast<size_t>(m) * A.n_ab + ab) * R;
     for (int r = threadIdx.x; r < R; r += blockDim.x) {
@@ -310,7 +311,7 @@ __device__ __forceinline__ void red_u64(unsigned long long* p, double v)
 
 // ---- adjoint pass 2: walk again (the same E bit for bit) and scatter the adjoint weights
 template <bool VAR>
-__global__ void __launch_bounds__(256, 1) sid_adj_b_kernel(SidArgs A, bool f4)
+__global__ void __launch_bounds__(512, 1) sid_adj_b_kernel(SidArgs A, bool f4)
 {
     pdl_entry();
     const int ab = blockIdx.x, m = blockIdx.y, R = A.R;
@@ -379,36 +380,47 @@ __global__ void __launch_bounds__(256, 1) sid_adj_fin_kernel(SidArgs A, double2*
 
 }  // namespace
 
+// threads per CTA: the angle-bank's rays in as few equal rounds of <= 512 threads as possible (a ray
+// per thread per round), so the last round is not a ragged tail (config 4: 819 rays = 2 x 416)
+static int sid_block(int R)
+{
+    const int rounds = (R + 511) / 512;
+    const int per = (R + rounds - 1) / rounds;
+    return std::max(32, std::min(512, (per + 31) / 32 * 32));
+}
+
 cudaError_t launch_sid_proj(int mode, bool var, const SidArgs& A, cudaStream_t s)
 {
     const dim3 grid(A.n_ab, A.B);
+    const int nt = sid_block(A.R);
     const size_t sm = 2 * sizeof(float) * A.R;
     if (mode == MODE_FWD)
-        return var ? launch_k(sid_proj_kernel<MODE_FWD, true>, grid, 256, sm, s, A)
-                   : launch_k(sid_proj_kernel<MODE_FWD, false>, grid, 256, sm, s, A);
-    return var ? launch_k(sid_proj_kernel<MODE_JVP, true>, grid, 256, sm, s, A)
-               : launch_k(sid_proj_kernel<MODE_JVP, false>, grid, 256, sm, s, A);
+        return var ? launch_k(sid_proj_kernel<MODE_FWD, true>, grid, nt, sm, s, A)
+                   : launch_k(sid_proj_kernel<MODE_FWD, false>, grid, nt, sm, s, A);
+    return var ? launch_k(sid_proj_kernel<MODE_JVP, true>, grid, nt, sm, s, A)
+               : launch_k(sid_proj_kernel<MODE_JVP, false>, grid, nt, sm, s, A);
 }
 
 cudaError_t launch_sid_adj(int mode, bool var, const SidArgs& A, double2* gacc, cudaStream_t s)
 {
     const dim3 grid(A.n_ab, A.B);
+    const int nt = sid_block(A.R);
     const size_t n2 = static_cast<size_t>(A.N) * A.N;
     cudaError_t e = cudaMemsetAsync(A.bound, 0, 2 * sizeof(unsigned) * A.B, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(A.acc, 0, 2 * n2 * sizeof(unsigned long long) * A.B, s);
     const size_t sm = sizeof(float) * A.R;
     if (e == cudaSuccess) {
         if (mode == MODE_GN)
-            e = var ? launch_k(sid_adj_a_kernel<MODE_GN, true>, grid, 256, sm, s, A)
-                    : launch_k(sid_adj_a_kernel<MODE_GN, false>, grid, 256, sm, s, A);
+            e = var ? launch_k(sid_adj_a_kernel<MODE_GN, true>, grid, nt, sm, s, A)
+                    : launch_k(sid_adj_a_kernel<MODE_GN, false>, grid, nt, sm, s, A);
         else
-            e = var ? launch_k(sid_adj_a_kernel<MODE_VJP, true>, grid, 256, sm, s, A)
-                    : launch_k(sid_adj_a_kernel<MODE_VJP, false>, grid, 256, sm, s, A);
+            e = var ? launch_k(sid_adj_a_kernel<MODE_VJP, true>, grid, nt, sm, s, A)
+                    : launch_k(sid_adj_a_kernel<MODE_VJP, false>, grid, nt, sm, s, A);
     }
     const bool f4 = mode == MODE_GN;
     if (e == cudaSuccess)
-        e = var ? launch_k(sid_adj_b_kernel<true>, grid, 256, 0, s, A, f4)
-                : launch_k(sid_adj_b_kernel<false>, grid, 256, 0, s, A, f4);
+        e = var ? launch_k(sid_adj_b_kernel<true>, grid, nt, 0, s, A, f4)
+                : launch_k(sid_adj_b_kernel<false>, grid, nt, 0, s, A, f4);
     if (e == cudaSuccess) {
         const int nb = static_cast<int>(std::min<size_t>((n2 + 255) / 256, 1024));
         e = launch_k(sid_adj_fin_kernel, dim3(nb, A.B), 256, 0, s, A, gacc);
