@@ -48,6 +48,14 @@ def smem_peak():
         return float(SMEM_B_PER_CLK_SM), "nominal 128 B/clk/SM (B200_PROFILING guide)"
 
 
+def measured_hbm():
+    """The pool's measured HBM copy bandwidth (GB/s, MEASURED_PEAKS.json, driver-written), else None."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return None
+
+
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -316,6 +324,19 @@ def measure_config(pg, P, cid, flush, sm_mhz, reps=5, **desc_over):
         t = (ms["forward"] + ms["jvp"] + ms["vjp"]) * 1e-3
         out["hbm"] = {"alg_bytes_fwd_jvp_vjp": tot, "GBps": tot / t / 1e9,
                       "basis": "inputs read + outputs written once per op (lam, mu, dlam, dmu, w; y, dy, g_lam, g_mu)"}
+        # the batched LM's HBM-bound kernel: the GN product streams the coefficient cache (DRAM bytes per
+        # launch from the committed ncu capture, profiles/traffic.json) in the launch time measured here
+        try:
+            tb = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(f"cfg{cid}", {}).get("gn")
+        except (OSError, ValueError):
+            tb = None
+        if tb and "gn" in kern:
+            gbs = tb / (kern["gn"]["launch_ms"] * 1e-3) / 1e9
+            peak_hbm = measured_hbm()
+            out["hbm"]["gn_product"] = {"dram_bytes_per_launch": tb, "launch_ms": kern["gn"]["launch_ms"], "GBps": gbs,
+                                        "peak_GBps": peak_hbm, "frac": gbs / peak_hbm if peak_hbm else None,
+                                        "basis": "ncu dram read+write per GN launch pair (profiles/traffic.json) / "
+                                                 "CUDA-event launch time; peak = MEASURED_PEAKS.json hbm_gbs"}
     del g
     return out
 
