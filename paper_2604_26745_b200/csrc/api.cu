@@ -383,8 +383,9 @@ pget_status run_seg(const Geometry& g, int mode, ProjArgs A, float* segp, cudaSt
     A.cache = cache;   // VJP: also write the GN Jacobian-entry cache (fused lin_kernel)
     A.gscale = cache ? gscale : nullptr;
     A.cellmax = g.cellmax;
-    A.cache_off = S.d_cache_off;
+    A.cache_off = S.d_cache_off;   // the fused builder writes the comb-group layout of its own scatter
     A.cache_rows_member = S.cache_rows_member;
+    A.cache_ng = S.max_gB;
     A.ntab = S.ntab;
     A.slot_lo = S.d_slot_lo;
     A.slot_hi = S.d_slot_hi;
@@ -434,7 +435,8 @@ void build_host_schedules(Geometry& g, const std::vector<RayP>& rays)
             build_adj_schedule(g, rays, g.segA_cps * g.sm_count, g.sm_count, &S);
             const SegCfg sc = seg_cfg(g);
             build_adj_stages(sc.RbA, sc.passesA, sc.RbB, sc.passesB, &S);
-            const double cache_gb = static_cast<double>(g.desc.batch) * S.cache_rows_member * 32 * sizeof(float4) / 1e9;
+            const double cache_gb = static_cast<double>(g.desc.batch) * std::max(S.cache_rows_member, S.cache_rows_memberC) *
+                                    32 * sizeof(float4) / 1e9;
             if (cache_gb > g.cache_max_gb) g.gn_cached = false;
         } else {
             build_schedule(g, k, g.sm_count * proj_ctas_per_sm(mode), &S);
@@ -515,7 +517,8 @@ WS carve(const Geometry& g, int op, char* base)
         if (g.adj_seg && g.gn_cached && uses_cache) {
             const Schedule& S = g.sch[kSchedAdj];
             w.cache = reinterpret_cast<float4*>(
-                take((static_cast<size_t>(B) * S.cache_rows_member + kCachePadRows) * 32 * sizeof(float4)));
+                take((static_cast<size_t>(B) * std::max(S.cache_rows_member, S.cache_rows_memberC) + kCachePadRows) *
+                     32 * sizeof(float4)));
             w.jp = reinterpret_cast<float*>(take(static_cast<size_t>(S.n_canon) * 2 * g.R * sizeof(float)));
             if (g.gnb_int && g.gn_hybrid)
                 w.gscale = reinterpret_cast<float*>(take(static_cast<size_t>(B) * S.ntab * 8 * sizeof(float)));
@@ -619,6 +622,10 @@ void free_device_tables(Geometry* g)
         cudaFree(S.d_sa_begin); cudaFree(S.d_sb_begin); cudaFree(S.d_stA); cudaFree(S.d_stB); cudaFree(S.d_seg_rows);
         cudaFree(S.d_cache_off);
         S.d_cache_off = nullptr;
+        cudaFree(S.d_groupsC);
+        cudaFree(S.d_cache_offC);
+        S.d_groupsC = nullptr;
+        S.d_cache_offC = nullptr;
     }
     {
         Schedule& S = g->schJ;
@@ -706,6 +713,11 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     if (const char* ev = std::getenv("PGET_GNB_TALL")) g.gnb_tall = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_GNB_INT")) g.gnb_int = g.gnb_int && std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_GNB_WIDE")) g.gnb_wide = std::atoi(ev) != 0;
+    // the cached GN path over consecutive-ray groups for single assemblies (measured: LM config 2 -0.6 %,
+    // config 3 -3 %, config 4 -1 %; config 5's 64 members +3.5 %: the separate cache build costs more
+    // there than the scatter gains); PGET_GNB_ADJ=0/1 overrides
+    g.gnb_adj = g.desc.batch == 1;
+    if (const char* ev = std::getenv("PGET_GNB_ADJ")) g.gnb_adj = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_SEGA_WIDE")) g.segA_wide = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_GN_APPLY_CACHED")) g.gn_apply_cached = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_GN_CACHE_MAX_GB")) g.cache_max_gb = std::atof(ev);
@@ -719,6 +731,7 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     if (const char* ev = std::getenv("PGET_SEGA_CPS")) g.segA_cps = std::max(1, std::min(4, std::atoi(ev)));
     if ((g.segA_W + 1) * 32 * g.segA_cps > 2048) g.segA_cps = 2048 / ((g.segA_W + 1) * 32);
     variant_paths();
+    g.gnb_adj = g.gnb_adj && g.gnb_int && g.gn_hybrid;   // the float accumulators need comb lanes
     // the coefficient cache while it stays well inside HBM (config 2: 0.4 GB, config 4: 2.7 GB,
     // config 5's 64 assemblies: 25 GB of 180; measured: config 5 LM iteration 307 -> 210 ms)
     build_host_schedules(g, rays);
@@ -747,6 +760,8 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
             up(&S.d_sb_begin, S.sb_begin);
             up(&S.d_seg_rows, S.seg_rows);
             up(&S.d_cache_off, S.cache_off);
+            up(&S.d_groupsC, S.groupsC);
+            up(&S.d_cache_offC, S.cache_offC);
         }
     }
     if (g.adj_seg && g.jvp_seg) {
@@ -1016,8 +1031,8 @@ static ProjArgs gnc_args(const Geometry& g, const WS& w)
     A.slot_hi = S.d_slot_hi;
     A.K = S.K;
     A.seg_rows = S.d_seg_rows;
-    A.n_groups = S.max_gB;
-    A.groups = S.d_groups;
+    A.n_groups = g.gnb_adj ? S.max_gC : S.max_gB;
+    A.groups = g.gnb_adj ? S.d_groupsC : S.d_groups;
     A.units = S.d_unitsB;
     A.u_begin = S.d_ub_begin;
     A.stages = S.d_stB;
@@ -1031,8 +1046,9 @@ static ProjArgs gnc_args(const Geometry& g, const WS& w)
     A.off_rsc = c.off_rsc;
     A.off_q1 = c.off_q1;
     A.cache = w.cache;
-    A.cache_off = S.d_cache_off;
-    A.cache_rows_member = S.cache_rows_member;
+    A.cache_off = g.gnb_adj ? S.d_cache_offC : S.d_cache_off;
+    A.cache_rows_member = g.gnb_adj ? S.cache_rows_memberC : S.cache_rows_member;
+    A.cache_ng = g.gnb_adj ? S.max_gC : S.max_gB;
     A.ntab = S.ntab;
     A.jp = w.jp;
     A.gscale = w.gscale;
@@ -1111,6 +1127,49 @@ static pget_status gnc_product(const Geometry& g, const WS& w, const float* lam,
     launch_k(reduce_slots_kernel, grid, dim3(32, 8), 0, s, w.slots, w.gacc, N, slot_pitch(g), g.desc.batch, pc.G,
                                                     g.sch[kSchedAdj].d_red_off, g.sch[kSchedAdj].d_red_slot,
                                                     g.sch[kSchedAdj].d_slot_lo, g.sch[kSchedAdj].d_slot_hi); note();
+    CK(cudaGetLastError());
+    return PGET_OK;
+}
+
+// the LM iteration's gradient J^T win through the coefficient cache (consecutive-ray layout, built by
+// gnc_build from u's phase-A partials): the VJP's per-ray weights from the sinogram (gnw_kernel SINO),
+// the cached scatter and the slot reduction into w.gacc -- the VJP without re-walking the image
+static pget_status gnc_gradient(const Geometry& g, const WS& w, const float* win, cudaStream_t s)
+{
+    const SegCfg c = seg_cfg(g);
+    const Schedule& S = g.sch[kSchedAdj];
+    ProjArgs A = gnc_args(g, w);
+    A.jp = nullptr;
+    A.gw = w.jp;
+    A.win = win;
+    cudaEvent_t ea = nullptr, eb = nullptr;
+    if (g_prof.on.load(std::memory_order_relaxed)) {
+        std::lock_guard<std::mutex> lk(g_prof.mu);
+        g_prof.total += 2;
+        g_prof.mode_launches[MODE_VJP]++;
+        if (g_prof.used + 2 <= g_prof.pool.size()) {
+            ea = g_prof.pool[g_prof.used++];
+            eb = g_prof.pool[g_prof.used++];
+            g_prof.recs.push_back({MODE_VJP, ea, eb});
+        }
+    }
+    if (ea) cudaEventRecord(ea, s);
+    cudaError_t e = launch_gnw(g.pair, A, g.d_tabsA, S.ntab, g.desc.batch, s, true);
+    if (e == cudaSuccess) {
+        ProjArgs Ag = A;
+        Ag.RbB = c.RbG;
+        Ag.off_wacc = c.off_waccG;
+        Ag.off_rout = c.off_routG;
+        Ag.passesB = c.passesG;
+        e = launch_gnc(2, g.pair, Ag, c.gridB, c.WG * 32, c.smemG, s);
+    }
+    if (eb) cudaEventRecord(eb, s);
+    if (e != cudaSuccess) return cuda_fail(e, "cached gradient launch");
+    const ProjCfg pc = proj_cfg(g, MODE_VJP);
+    const int N = g.desc.n_px;
+    const dim3 grid((N + 31) / 32, (N + 31) / 32, g.desc.batch * pc.G);
+    launch_k(reduce_slots_kernel, grid, dim3(32, 8), 0, s, w.slots, w.gacc, N, slot_pitch(g), g.desc.batch, pc.G,
+                                                    S.d_red_off, S.d_red_slot, S.d_slot_lo, S.d_slot_hi); note();
     CK(cudaGetLastError());
     return PGET_OK;
 }
@@ -1320,7 +1379,15 @@ static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const f
     const bool cached = g.adj_seg && g.gn_cached;
     // the gradient VJP also writes the GN Jacobian-entry cache (fused cache build)
     // F(u) above was the segmented forward: its phase-A partials of u are the VJP's phase A
-    if ((st = proj_adjoint(g, w, MODE_VJP, w.ysino, s, cached && n_cg > 0, g.adj_seg && g.fwd_seg))) return st;
+    if (cached && n_cg > 0 && g.gnb_adj) {
+        // the cache over consecutive-ray groups, built by lin_kernel from the phase-A partials of u that
+        // F(u) left (the fused builder of the VJP writes the comb layout of its own scatter); the
+        // gradient then comes from the cache like every GN product
+        if ((st = gnc_build(g, w, s))) return st;
+        if ((st = gnc_gradient(g, w, w.ysino, s))) return st;
+    } else if ((st = proj_adjoint(g, w, MODE_VJP, w.ysino, s, cached && n_cg > 0, g.adj_seg && g.fwd_seg))) {
+        return st;
+    }
     launch_k(finish_kernel, vg, kVecThreads, 0, s, w.gacc, Gv, lam, mu, alpha, 0.f, -1.f, w.bl, w.bm, w.bl, w.bm, P[2], w.zl,
                                             w.zm, w.pl, w.pm, s_lam, s_mu, N, pr, nullptr); note();
     CK(cudaGetLastError());
@@ -1686,6 +1753,32 @@ pget_status pget_schedule_check(pget_geometry h)
                     if (n > rows) return bad("cache block shorter than a lane");
                 }
             }
+    // the consecutive-ray layout (PGET_GNB_ADJ): every ray once, blocks cover the longest lane
+    {
+        const int ngC = S.max_gC;
+        std::vector<int> cseen(R, 0);
+        for (int gi = 0; gi < ngC; ++gi)
+            for (int l = 0; l < 32; ++l) {
+                const int r = S.groupsC[static_cast<size_t>(gi) * 32 + l];
+                if (r >= 0) ++cseen[r];
+            }
+        for (int c : cseen)
+            if (c != 1) return bad("consecutive-ray groups");
+        for (int t = 0; t < ntab; ++t)
+            for (int k = 0; k < K; ++k)
+                for (int gi = 0; gi < ngC; ++gi) {
+                    const size_t idx = (static_cast<size_t>(t) * K + k) * ngC + gi;
+                    const int64_t rows = S.cache_offC[idx + 1] - S.cache_offC[idx];
+                    for (int l = 0; l < 32; ++l) {
+                        const int r = S.groupsC[static_cast<size_t>(gi) * 32 + l];
+                        if (r < 0) continue;
+                        const RayP& rp = rays[static_cast<size_t>(list[t]) * R + r];
+                        const int n = rp.dV > 0 ? seg_entry(rp, S.seg_rows[k + 1]) - seg_entry(rp, S.seg_rows[k])
+                                                : seg_entry(rp, S.seg_rows[k]) - seg_entry(rp, S.seg_rows[k + 1]);
+                        if (n > rows) return bad("consecutive-ray cache block shorter than a lane");
+                    }
+                }
+    }
     // comb groups: every ray once, lanes of a group >= comb_S rays apart
     std::vector<int> rseen(R, 0);
     for (int gi = 0; gi < ngB; ++gi)

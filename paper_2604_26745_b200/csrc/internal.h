@@ -118,6 +118,14 @@ struct Schedule {
     std::vector<int64_t> cache_off;
     int64_t cache_rows_member = 0;
     int64_t* d_cache_off = nullptr;
+    // the same cache over groups of 32 consecutive rays (the cached GN path's builder and scatter:
+    // integer atomics need no comb spacing, and neighbouring rays have similar chords)
+    std::vector<int32_t> groupsC;
+    int max_gC = 1;
+    std::vector<int64_t> cache_offC;
+    int64_t cache_rows_memberC = 0;
+    int32_t* d_groupsC = nullptr;
+    int64_t* d_cache_offC = nullptr;
     int32_t* d_cta_begin = nullptr;
     TaskD* d_tasks = nullptr;
     int32_t* d_groups = nullptr;
@@ -195,6 +203,7 @@ struct Geometry {
     // 2^22, i.e. (samples near a pixel) / cellmax < 512 (geometry.cpp)
     bool gnb_int = true;
     bool gnb_wide = true;   // cached scatter with one warp per comb group for 17-26 groups (PGET_GNB_WIDE=0: <= 16)
+    bool gnb_adj = false;   // cached GN path over consecutive-ray groups (lin_kernel builds the cache; batch 1, PGET_GNB_ADJ)
     bool segA_wide = true;  // phase A with one consumer warp per 32-ray group for 16-26 groups (PGET_SEGA_WIDE=0: 15 warps)
     // pget_gn_apply through the cache too (one product per call: building the cache costs more than
     // it saves; tests set PGET_GN_APPLY_CACHED=1 to pin the cached product at the operator tolerance)

@@ -71,6 +71,7 @@ struct ProjArgs {
     float4* cache;           // rows of 32 lanes: (alpha, beta, alpha', beta') per sample
     const int64_t* cache_off;
     int64_t cache_rows_member;
+    int cache_ng;            // groups per (angle-bank, segment) of the cache layout (comb or consecutive-ray groups)
     int ntab;
     float* jp;               // [n_canon][2][R] per-ray JVP partials of a segment (both directions)
     float* segp;            // [n_canon][kSegFields][R]
@@ -204,7 +205,8 @@ cudaError_t launch_gnc(int phase, bool paired, const ProjArgs& A, int grid, int 
 cudaError_t set_gnc_smem_limit(size_t smem);
 cudaError_t launch_jvp_combine(const ProjArgs& A, const int32_t* tabs, int ntab, int B, cudaStream_t s);
 cudaError_t launch_fwd_combine(bool paired, const ProjArgs& A, const int32_t* tabs, int ntab, int B, cudaStream_t s);
-cudaError_t launch_gnw(bool paired, const ProjArgs& A, const int32_t* tabs, int ntab, int B, cudaStream_t s);
+cudaError_t launch_gnw(bool paired, const ProjArgs& A, const int32_t* tabs, int ntab, int B, cudaStream_t s,
+                       bool sino = false);
 cudaError_t launch_jsq(bool paired, const ProjArgs& A, double* sq, int grid, int block, size_t smem, cudaStream_t s);
 cudaError_t launch_jsq_member(const double* sq, int ntab, int B, int nblk, double* partial, cudaStream_t s);
 __global__ void finite_scan_kernel(const float* __restrict__ x, size_t n, int32_t* flag);

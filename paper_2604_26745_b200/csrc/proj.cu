@@ -1380,7 +1380,7 @@ __global__ void __launch_bounds__(512, 1) seg_b_kernel(ProjArgs A)
 __device__ __forceinline__ float4* cache_lane(const ProjArgs& A, const UnitInfo& ui, int grp, int lane, int* kend)
 {
     const int t = (ui.canon / A.K) % A.ntab;
-    const int64_t idx = (static_cast<int64_t>(t) * A.K + ui.seg) * A.n_groups + grp;
+    const int64_t idx = (static_cast<int64_t>(t) * A.K + ui.seg) * A.cache_ng + grp;
     const int64_t off = A.cache_off[idx];
     *kend = static_cast<int>(A.cache_off[idx + 1] - off);   // rows of the block
     const int64_t row = static_cast<int64_t>(ui.m) * A.cache_rows_member + off;
@@ -1851,7 +1851,10 @@ __device__ __forceinline__ void gn_weights(const ProjArgs& A, const float* rout,
 
 // gnw_kernel: per CG step and (member, traced angle-bank), the whole-ray (J p) of the GN-mode phase-A
 // partials (once, instead of once per segment unit inside gnb_kernel) and the scatter weights, to A.gw
-template <bool PAIRED>
+// SINO: the VJP's weights instead, from the sinogram A.win (w_r = w_j (win[d] + win of the duplicate
+// angle-bank), w'_r from bank 1 mirrored, as seg_b_kernel forms them): the cached scatter then computes
+// the gradient J^T r of the LM iteration from the coefficient cache
+template <bool PAIRED, bool SINO = false>
 __global__ void __launch_bounds__(256) gnw_kernel(ProjArgs A, const int32_t* __restrict__ tabs, int ntab)
 {
     pdl_entry();
@@ -1862,13 +1865,27 @@ __global__ void __launch_bounds__(256) gnw_kernel(ProjArgs A, const int32_t* __r
     const int ab = tabs[t];
     const int dir = A.rays[static_cast<size_t>(ab) * R].dV > 0 ? 1 : -1;
     const int ct = m * ntab + t;
-    for (int r = threadIdx.x; r < R; r += blockDim.x) gn_rout_from_seg<PAIRED>(A, ct * A.K, dir, r, rout);
+    if (!SINO)
+        for (int r = threadIdx.x; r < R; r += blockDim.x) gn_rout_from_seg<PAIRED>(A, ct * A.K, dir, r, rout);
     __syncthreads();
     float* gw = A.gw + static_cast<size_t>(ct) * 2 * R;
     float wm = 0.f, wm1 = 0.f;
+    const size_t wbase = (static_cast<size_t>(m) * A.n_ab + ab) * A.n_det;
+    const size_t wbase2 = (static_cast<size_t>(m) * A.n_ab + dup_of(A, ab)) * A.n_det;
+    const size_t wpbase = (static_cast<size_t>(m) * A.n_ab + ab + 1) * A.n_det;
+    const size_t wpbase2 = (static_cast<size_t>(m) * A.n_ab + dup_of(A, ab + 1)) * A.n_det;
     for (int r = threadIdx.x; r < R; r += blockDim.x) {
         float wr, wr1;
-        gn_weights(A, rout, r, wr, wr1);
+        if constexpr (SINO) {
+            const int d = r / A.J, j = r - d * A.J;
+            float wd = A.win[wbase + d], wd1 = 0.f;
+            if (A.dup_half) wd += A.win[wbase2 + d];
+            if (PAIRED) wd1 = A.win[wpbase + A.n_det - 1 - d] + A.win[wpbase2 + A.n_det - 1 - d];
+            wr = A.w[j] * wd;
+            wr1 = A.w[j] * wd1;
+        } else {
+            gn_weights(A, rout, r, wr, wr1);
+        }
         gw[r] = wr;
         gw[R + r] = wr1;
         wm = fmaxf(wm, fabsf(wr));
@@ -1894,10 +1911,17 @@ __global__ void __launch_bounds__(256) gnw_kernel(ProjArgs A, const int32_t* __r
     }
 }
 
-cudaError_t launch_gnw(bool paired, const ProjArgs& A, const int32_t* tabs, int ntab, int B, cudaStream_t s)
+cudaError_t launch_gnw(bool paired, const ProjArgs& A, const int32_t* tabs, int ntab, int B, cudaStream_t s,
+                       bool sino)
 {
-    if (paired) launch_k(gnw_kernel<true>, dim3(ntab, B), 256, 2 * A.R * sizeof(float), s, A, tabs, ntab);
-    else launch_k(gnw_kernel<false>, dim3(ntab, B), 256, 2 * A.R * sizeof(float), s, A, tabs, ntab);
+    const size_t sm = 2 * A.R * sizeof(float);
+    if (sino) {
+        if (paired) launch_k(gnw_kernel<true, true>, dim3(ntab, B), 256, sm, s, A, tabs, ntab);
+        else launch_k(gnw_kernel<false, true>, dim3(ntab, B), 256, sm, s, A, tabs, ntab);
+    } else {
+        if (paired) launch_k(gnw_kernel<true>, dim3(ntab, B), 256, sm, s, A, tabs, ntab);
+        else launch_k(gnw_kernel<false>, dim3(ntab, B), 256, sm, s, A, tabs, ntab);
+    }
     return cudaGetLastError();
 }
 
