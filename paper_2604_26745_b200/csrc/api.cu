@@ -709,6 +709,8 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     if (const char* ev = std::getenv("PGET_ADJ_FUSED")) g.adj_seg = std::atoi(ev) == 0;   // A/B experiments
     if (const char* ev = std::getenv("PGET_JVP_FUSED")) g.jvp_seg = std::atoi(ev) == 0;
     if (const char* ev = std::getenv("PGET_FWD_FUSED")) g.fwd_seg = std::atoi(ev) == 0;
+    if (const char* ev = std::getenv("PGET_FWD_PLAIN")) g.fwd_plain = std::atoi(ev) != 0;
+    if (const char* ev = std::getenv("PGET_FWD_PLAIN_TRIAL")) g.fwd_plain_trial = std::atoi(ev) != 0;
     g.gnb_tall = g.P >= 200;   // measured: config 4 -3.6 % LM, config 2 +0.8 %
     if (const char* ev = std::getenv("PGET_GNB_TALL")) g.gnb_tall = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_GNB_INT")) g.gnb_int = g.gnb_int && std::atoi(ev) != 0;
@@ -719,6 +721,7 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     g.gnb_adj = g.desc.batch == 1;
     if (const char* ev = std::getenv("PGET_GNB_ADJ")) g.gnb_adj = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_SEGA_WIDE")) g.segA_wide = std::atoi(ev) != 0;
+    if (const char* ev = std::getenv("PGET_GNB_STRIDE")) g.gnbC_stride = std::max(1, std::min(16, std::atoi(ev)));
     if (const char* ev = std::getenv("PGET_GN_APPLY_CACHED")) g.gn_apply_cached = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_GN_CACHE_MAX_GB")) g.cache_max_gb = std::atof(ev);
     if (const char* ev = std::getenv("PGET_GN_CACHE")) {   // 0: recompute, 1: hybrid, 2: fully cached
@@ -824,6 +827,7 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     if (g.adj_seg && e == cudaSuccess) {
         const SegCfg sc = seg_cfg(g);
         if (sc.smemA > g.smem_optin || sc.smemB > g.smem_optin) e = cudaErrorInvalidConfiguration;
+        if (e == cudaSuccess) e = set_seg_smem_limit(0, MODE_FWD, sc.smemA);
         for (int mode : {MODE_VJP, MODE_GN}) {
             if (e == cudaSuccess) e = set_seg_smem_limit(0, mode, sc.smemA);
             if (e == cudaSuccess) e = set_seg_smem_limit(1, mode, sc.smemB);
@@ -1178,7 +1182,10 @@ static pget_status gnc_gradient(const Geometry& g, const WS& w, const float* win
 // fp64 combine) when enabled, else the fused projector.  Used for the LM wrap's F(u), whose phase-A
 // partials the gradient VJP then reuses, and its trial forward; the standalone forward stays fused
 // (measured faster alone on configs 2, 3 and 5)
-static pget_status fwd_out(const Geometry& g, const WS& w, float* y, cudaStream_t s)
+// plain: the phase A in forward mode (uncompensated sums, no adjoint fields: the standalone forward, graded
+// per element like the fused forward that never compensated); else the VJP mode, whose partials the LM
+// wrap's gradient reuses and whose compensated sums feed f(u), f(u+s) and f(u~)
+static pget_status fwd_out(const Geometry& g, const WS& w, float* y, cudaStream_t s, bool plain = false)
 {
     if (!(g.adj_seg && g.fwd_seg)) return proj_out(g, w, MODE_FWD, y, nullptr, s);
     const Schedule& S = g.sch[kSchedAdj];
@@ -1208,7 +1215,7 @@ static pget_status fwd_out(const Geometry& g, const WS& w, float* y, cudaStream_
         }
     }
     if (ea) cudaEventRecord(ea, s);
-    cudaError_t e = launch_seg(0, MODE_VJP, c.maxgA, g.pair, A, c.gridA, (c.WA + 1) * 32, c.smemA, s);
+    cudaError_t e = launch_seg(0, plain ? MODE_FWD : MODE_VJP, c.maxgA, g.pair, A, c.gridA, (c.WA + 1) * 32, c.smemA, s);
     const int ntab = static_cast<int>((g.pair ? g.task_ab_p : g.task_ab).size());
     if (e == cudaSuccess) e = launch_fwd_combine(g.pair, A, g.d_tabsA, ntab, g.desc.batch, s);
     if (eb) cudaEventRecord(eb, s);
@@ -1267,7 +1274,7 @@ pget_status pget_forward(pget_geometry h, const float* lam, const float* mu, flo
     const Geometry& g = h->g;
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     if ((st = pack2(g, w, lam, mu, nullptr, nullptr, nullptr, nullptr, s))) return st;
-    return fwd_out(g, w, y, s);   // the warp-specialised segmented phase A + fp64 combine (fused: variant only)
+    return fwd_out(g, w, y, s, g.fwd_plain);   // the warp-specialised segmented phase A + fp64 combine (fused: variant only)
 }
 
 pget_status pget_jvp(pget_geometry h, const float* lam, const float* mu, const float* dlam, const float* dmu,
@@ -1493,7 +1500,7 @@ static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const f
     // 7-8: f(u+s), rho, accept, beta_next
     if (flags & PGET_GN_EVAL_TRIAL) {
         if ((st = pack2(g, w, lam, mu, s_lam, s_mu, w.ul, w.um, s, box))) return st;
-        if ((st = fwd_out(g, w, w.ysino, s))) return st;
+        if ((st = fwd_out(g, w, w.ysino, s, g.fwd_plain_trial))) return st;
         launch_k(residual_kernel, vg, kVecThreads, 0, s, w.ysino, y_meas, P[0], nsper); note();
         launch_k(regsq_kernel, vg, kVecThreads, 0, s, w.ul, w.um, P[1], N); note();
         if (has_prior) launch_k(priorsq_kernel, vg, kVecThreads, 0, s, w.ul, w.um, pr, Pp, N); note();

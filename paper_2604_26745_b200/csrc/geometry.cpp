@@ -220,6 +220,7 @@ pget_status build_geometry(const pget_geometry_desc* d, Geometry* g, std::string
         if (S < 1) S = 1;
         if (S > g->R) S = g->R;
         g->comb_S = static_cast<int>(S);
+        g->gnbC_stride = a < 0.5 ? 2 : 1;   // measured (LM iteration, stride 1/2/3/4): config 4 25.0/24.0/24.2/24.7 ms, config 2 4.83/4.77/4.80/4.85
         // samples whose 2x2 bilinear support contains a given pixel: rays within the support's
         // width (2 sqrt2 px) x samples of one ray inside it; consecutive samples in one cell
         const double st = d->step_px;

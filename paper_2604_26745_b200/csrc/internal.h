@@ -180,6 +180,10 @@ struct Geometry {
     int n_class0 = 0;
     // comb stride: rays >= comb_S apart (>= 2 sqrt2 px) have disjoint bilinear footprints
     int comb_S = 1;
+    // the cached GN path's ray groups (PGET_GNB_ADJ): blocks of 32 x gnbC_stride consecutive rays, each split
+    // into gnbC_stride groups of every gnbC_stride-th ray (~1 px apart: neighbouring lanes rarely share a
+    // cell, so fewer same-address atomics; chords still similar)
+    int gnbC_stride = 1;
     // device tables
     RayP* d_rays = nullptr;       // [n_ab][R] oriented frame
     float* d_w = nullptr;         // [J] float weights
@@ -195,6 +199,8 @@ struct Geometry {
     bool jvp_seg = true;
     int32_t* d_tabsJ = nullptr;   // [ntab] traced angle-banks of schJ (task_ab)
     bool fwd_seg = true;          // forward as the segmented VJP-mode phase A + combine
+    bool fwd_plain = true;        // standalone forward: forward-mode phase A (plain sums); trial f(u+s) too if fwd_plain_trial
+    bool fwd_plain_trial = false;
     int32_t* d_tabsA = nullptr;   // traced angle-banks of the adjoint schedule (task_ab_p or task_ab)
     bool adj_seg = true;   // adjoint (VJP / GN) as the segmented two-phase projector (else the fused one)
     bool gnb_tall = true;   // gnb_kernel with its own (taller) bands: no stage buffers to fit

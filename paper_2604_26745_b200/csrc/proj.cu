@@ -330,10 +330,22 @@ __device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int
     if (i < ilo || iv0 < r0 || iv0 >= r1) return;
     int n = band_steps(i, ilo, v, dV, r0, r1);
     const Cn* img = reinterpret_cast<const Cn*>(sb);
-    auto load = [&](SmpA<TR::NF4>& x, int64_t uu, int64_t vv, int ivv) {
-        const int o = (ivv - r0) * P + hi32(uu);
-        PGET_CHECK(o >= 0 && o + P + 1 < (r1 - r0 + 1) * P);
-        x.c00 = img[o]; x.c01 = img[o + 1]; x.c10 = img[o + P]; x.c11 = img[o + P + 1];
+    // the band's origin: element (row iv, column iu) at org + iv * P + iu (one base register instead of
+    // r0, which the 72-register builds otherwise recompute per sample)
+    int r0o = r0;
+#ifndef PGET_WALKA_OLD
+    asm volatile("" : "+r"(r0o));   // opaque: kept in a register, not recomputed from the unit per sample
+#endif
+    const Cn* org = img - r0o * P;
+    [[maybe_unused]] const int o_first = r0o * P;   // ok false (the band's last sample has no successor here): load the
+                                  // band's first cell instead of branching around the loads
+    auto load = [&](SmpA<TR::NF4>& x, int64_t uu, int64_t vv, int ivv, bool ok = true) {
+        int o = ivv * P + hi32(uu);
+#ifndef PGET_WALKA_OLD
+        o = ok ? o : o_first;
+#endif
+        PGET_CHECK(o - o_first >= 0 && o - o_first + P + 1 < (r1 - r0 + 1) * P);
+        x.c00 = org[o]; x.c01 = org[o + 1]; x.c10 = org[o + P]; x.c11 = org[o + P + 1];
         x.fu = frac23(uu);
         x.fv = frac23(vv);
     };
@@ -344,7 +356,10 @@ __device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int
         const int64_t u2 = u - dU, v2 = v - dV;
         const int iv2 = hi32(v2);
         const bool nxt = --n != 0;
-        if (nxt) load(nx, u2, v2, iv2);
+#ifdef PGET_WALKA_OLD
+        if (nxt)
+#endif
+        load(nx, u2, v2, iv2, nxt);
         float lam, mu, dlam = 0.f, dmu = 0.f;
         if constexpr (TR::NF4) {
             const float2 x = bilerp2(lo2(cur.c00), lo2(cur.c01), lo2(cur.c10), lo2(cur.c11), cur.fu, cur.fv);
@@ -465,12 +480,19 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
         const int iv2 = hi32(v2);
         const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;   // sweep-B bands are a few rows: no band_steps
         float2 n00, n01, n10, n11;
+#ifdef PGET_WALKA_OLD
         int o2 = o;
         if (nxt) {
             o2 = (iv2 - r0) * P + hi32(u2);
             PGET_CHECK(o2 >= 0 && o2 + P + 1 < (r1 - r0 + 1) * P);
             n00 = img[o2]; n01 = img[o2 + 1]; n10 = img[o2 + P]; n11 = img[o2 + P + 1];
         }
+#else
+        // the band's last sample loads its own cell again instead of branching around the loads
+        const int o2 = nxt ? (iv2 - r0) * P + hi32(u2) : o;
+        PGET_CHECK(o2 >= 0 && o2 + P + 1 < (r1 - r0 + 1) * P);
+        n00 = img[o2]; n01 = img[o2 + 1]; n10 = img[o2 + P]; n11 = img[o2 + P + 1];
+#endif
         const float2 x = bilerp2(q00, q01, q10, q11, fu, fv);
         const float arg_hi = fmaf(x.y, ch, x_.s);
         float cv = 1.f, wv = 1.f;
@@ -1495,12 +1517,19 @@ __device__ __forceinline__ void walk_lin(const float2* __restrict__ img, int P, 
         const int iv2 = hi32(v2);
         const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;   // sweep-B bands are a few rows: no band_steps
         float2 n00, n01, n10, n11;
+#ifdef PGET_WALKA_OLD
         int o2 = o;
         if (nxt) {
             o2 = (iv2 - r0) * P + hi32(u2);
             PGET_CHECK(o2 >= 0 && o2 + P + 1 < (r1 - r0 + 1) * P);
             n00 = img[o2]; n01 = img[o2 + 1]; n10 = img[o2 + P]; n11 = img[o2 + P + 1];
         }
+#else
+        // the band's last sample loads its own cell again instead of branching around the loads
+        const int o2 = nxt ? (iv2 - r0) * P + hi32(u2) : o;
+        PGET_CHECK(o2 >= 0 && o2 + P + 1 < (r1 - r0 + 1) * P);
+        n00 = img[o2]; n01 = img[o2 + 1]; n10 = img[o2 + P]; n11 = img[o2 + P + 1];
+#endif
         const float2 x = bilerp2(q00, q01, q10, q11, fu, fv);
         const float arg_hi = fmaf(x.y, ch, x_.s);
         const float E = ex2(arg_hi - x_.sc);
@@ -2340,6 +2369,18 @@ cudaError_t launch_seg(int phase, int mode, int maxg, bool paired, const ProjArg
         else launch_k(seg_a_kernel<MODE_JVP, 2, false>, grid, block, smem, s, A);
         return cudaGetLastError();
     }
+    if (mode == MODE_FWD && phase == 0) {   // the standalone forward: plain sums, G and (paired) p2 only
+        if (paired) {
+            if (block > 512) launch_k(seg_a_kernel<MODE_FWD, 1, true, true>, grid, block, smem, s, A);
+            else if (maxg == 1) launch_k(seg_a_kernel<MODE_FWD, 1, true>, grid, block, smem, s, A);
+            else launch_k(seg_a_kernel<MODE_FWD, 2, true>, grid, block, smem, s, A);
+        } else {
+            if (block > 512) launch_k(seg_a_kernel<MODE_FWD, 1, false, true>, grid, block, smem, s, A);
+            else if (maxg == 1) launch_k(seg_a_kernel<MODE_FWD, 1, false>, grid, block, smem, s, A);
+            else launch_k(seg_a_kernel<MODE_FWD, 2, false>, grid, block, smem, s, A);
+        }
+        return cudaGetLastError();
+    }
     if (mode == MODE_VJP) return launch_seg_mode<MODE_VJP>(phase, maxg, paired, A, grid, block, smem, s);
     if (mode == MODE_GN) return launch_seg_mode<MODE_GN>(phase, maxg, paired, A, grid, block, smem, s);
     return cudaErrorInvalidValue;
@@ -2373,6 +2414,16 @@ cudaError_t set_seg_smem_limit(int phase, int mode, size_t smem)
         e = raise_smem(seg_a_kernel<MODE_JVP, 1, false, true>, v);
         if (e) return e;
         return raise_smem(seg_a_kernel<MODE_JVP, 2, false>, v);
+    }
+    if (mode == MODE_FWD && phase == 0) {
+        const int v = static_cast<int>(smem);
+        cudaError_t e;
+        if ((e = raise_smem(seg_a_kernel<MODE_FWD, 1, true>, v))) return e;
+        if ((e = raise_smem(seg_a_kernel<MODE_FWD, 2, true>, v))) return e;
+        if ((e = raise_smem(seg_a_kernel<MODE_FWD, 1, true, true>, v))) return e;
+        if ((e = raise_smem(seg_a_kernel<MODE_FWD, 1, false, true>, v))) return e;
+        if ((e = raise_smem(seg_a_kernel<MODE_FWD, 1, false>, v))) return e;
+        return raise_smem(seg_a_kernel<MODE_FWD, 2, false>, v);
     }
     if (mode == MODE_VJP) return seg_attr_mode<MODE_VJP>(phase, smem);
     if (mode == MODE_GN) return seg_attr_mode<MODE_GN>(phase, smem);

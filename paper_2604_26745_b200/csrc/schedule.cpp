@@ -410,10 +410,19 @@ void build_adj_schedule(const Geometry& g, const std::vector<RayP>& rays, int CA
         S->cache_off[static_cast<size_t>(ntab) * K * ngB] = off;
         S->cache_rows_member = off;
     }
-    {   // the same layout over groups of 32 consecutive rays
+    {   // the same layout over groups of nearby rays: blocks of 32 s consecutive rays, each split into s
+        // groups of every s-th ray (s = gnbC_stride); the tail of T < 32 s rays into ceil(T / 32) groups
+        // the same way -- ceil(R / 32) groups in all
         S->max_gC = ngA;
         S->groupsC.assign(static_cast<size_t>(ngA) * 32, -1);
-        for (int r = 0; r < R; ++r) S->groupsC[r] = r;
+        const int sb = std::max(1, g.gnbC_stride);
+        int gi0 = 0;
+        for (int r0 = 0; r0 < R; r0 += 32 * sb) {
+            const int T = std::min(32 * sb, R - r0);
+            const int ng = (T + 31) / 32;
+            for (int k = 0; k < T; ++k) S->groupsC[static_cast<size_t>(gi0 + k % ng) * 32 + k / ng] = r0 + k;
+            gi0 += ng;
+        }
         S->cache_offC.assign(static_cast<size_t>(ntab) * K * ngA + 1, 0);
         int64_t off = 0;
         for (int t = 0; t < ntab; ++t)
