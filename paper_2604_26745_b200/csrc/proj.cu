@@ -451,7 +451,7 @@ struct RayB {   // per-ray constants of sweep B
 // VAR (model variant N3): cw is the lane's row of (W_j(d_i), c_i): a_lam(i) = w_r Delta W_i E_i,
 // a_mu(i) = -w_r Delta^2 (sum_{k<i} W_k lam_k c_k E_k + W_i lam_i c_i E_i / 2), E_i = e^{-c_i A_i}
 template <bool PAIRED, bool COMP, bool CACHE = false, bool VAR = false>
-__device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* __restrict__ acc, int P, int r0,
+__device__ __forceinline__ void walk_b_old(const float2* __restrict__ img, float2* __restrict__ acc, int P, int r0,
                                        int r1, int abase, int sP, int ilo, int64_t dU, int64_t dV, float cf, float ch,
                                        const RayB& rb, int& i, int64_t& u, int64_t& v, StateB& st,
                                        float wr = 0.f, float wr1 = 0.f, float4* cl = nullptr, int* kp = nullptr,
@@ -589,6 +589,138 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
     }
 #endif
     st = x_;
+}
+
+// Sweep B, unrolled by two with alternating register roles (as walk_a: the corners of the next sample
+// load into the other SmpB, no register rotation), the next sample's loads issued unconditionally,
+// and the pending cell sums updated by one packed FMA per corner pair: p = p * keep + c (keep 0 when
+// the lane enters a new cell, after the old cell's read-modify-write) -- bitwise the same sums as
+// "p = c" / "p += c", without the copies a two-way join needs.
+struct SmpB {
+    float2 c00, c01, c10, c11;
+    float fu, fv;
+};
+template <bool PAIRED, bool COMP, bool CACHE = false, bool VAR = false>
+__device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* __restrict__ acc, int P, int r0,
+                                       int r1, int abase, int sP, int ilo, int64_t dU, int64_t dV, float cf, float ch,
+                                       const RayB& rb, int& i, int64_t& u, int64_t& v, StateB& st,
+                                       float wr = 0.f, float wr1 = 0.f, float4* cl = nullptr, int* kp = nullptr,
+                                       float2* emax = nullptr, const float2* __restrict__ cw = nullptr)
+{
+#if PGET_SCATTER == 0 || defined(PGET_WALKB_OLD)
+    walk_b_old<PAIRED, COMP, CACHE, VAR>(img, acc, P, r0, r1, abase, sP, ilo, dU, dV, cf, ch, rb, i, u, v, st, wr, wr1,
+                                         cl, kp, emax, cw);
+#else
+    if constexpr (!COMP) {   // the GN mode (plain sums) keeps the rolled loop: 128 registers and a spill unrolled
+        walk_b_old<PAIRED, COMP, CACHE, VAR>(img, acc, P, r0, r1, abase, sP, ilo, dU, dV, cf, ch, rb, i, u, v, st, wr,
+                                             wr1, cl, kp, emax, cw);
+        return;
+    }
+    {
+        const int iv = hi32(v);
+        if (i < ilo || iv < r0 || iv >= r1) return;
+    }
+    auto load = [&](SmpB& x, int64_t uu, int64_t vv, bool ok) {
+        int o = (hi32(vv) - r0) * P + hi32(uu);
+        o = ok ? o : 0;   // the band's last sample: a valid cell instead of a branch around the loads
+        PGET_CHECK(o >= 0 && o + P + 1 < (r1 - r0 + 1) * P);
+        x.c00 = img[o]; x.c01 = img[o + 1]; x.c10 = img[o + P]; x.c11 = img[o + P + 1];
+        x.fu = frac23(uu);
+        x.fv = frac23(vv);
+    };
+    auto cell = [&](int64_t uu, int64_t vv) { return abase + (hi32(vv) - r0) * sP + hi32(uu); };
+    StateB x_ = st;
+    int poff = cell(u, v);   // the pending cell starts as the first sample's, with zero sums
+    float2 p00 = make_float2(0.f, 0.f), p01 = p00, p10 = p00, p11 = p00;
+    auto rmw = [&](int off) {
+        float2* pa = acc + off;
+        const float2 t00 = pa[0], t01 = pa[1], t10 = pa[sP], t11 = pa[sP + 1];
+        pa[0] = __fadd2_rn(t00, p00);
+        pa[1] = __fadd2_rn(t01, p01);
+        pa[sP] = __fadd2_rn(t10, p10);
+        pa[sP + 1] = __fadd2_rn(t11, p11);
+    };
+    auto step = [&](const SmpB& cur, SmpB& nx) -> bool {
+        PGET_CHECK(hi32(u) >= 0 && hi32(u) + 1 < P && hi32(v) >= r0 && hi32(v) < r1);
+        const int aoff = cell(u, v);
+        const int i2 = i - 1;
+        const int64_t u2 = u - dU, v2 = v - dV;
+        const int iv2 = hi32(v2);
+        const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;   // sweep-B bands are a few rows: no band_steps
+        load(nx, u2, v2, nxt);
+        const float2 x = bilerp2(cur.c00, cur.c01, cur.c10, cur.c11, cur.fu, cur.fv);
+        const float arg_hi = fmaf(x.y, ch, x_.s);
+        float cv = 1.f, wv = 1.f;
+        if constexpr (VAR) {
+            const float2 t = __ldg(cw + i);
+            wv = t.x;
+            cv = t.y;
+        }
+        const float E = VAR ? ex2(cv * (arg_hi - x_.sc)) : ex2(arg_hi - x_.sc);
+        const float le = VAR ? x.x * (wv * cv) * E : x.x * E;
+        float al = VAR ? rb.kl * (wv * E) : rb.kl * E;
+        float am = rb.km * (((rb.G - x_.q) - (rb.Gc - x_.qc)) - 0.5f * le);
+        if constexpr (CACHE) {   // unit-weight entries: store, then weight
+            float4 ce = make_float4(al, am, 0.f, 0.f);
+            if constexpr (PAIRED) {
+                const float E1 = ex2((rb.Sl - arg_hi) - (rb.Slc - x_.sc));
+                const float le1 = x.x * E1;
+                ce.z = rb.kl1 * E1;
+                ce.w = rb.km1 * ((x_.q1 - x_.q1c) + 0.5f * le1);
+                if (COMP) kahan(x_.q1, x_.q1c, le1);
+                else x_.q1 += le1;
+            }
+            __stcs(cl + static_cast<int64_t>(*kp) * 32, ce);
+            ++*kp;
+            emax->x = fmaxf(emax->x, fmaxf(fabsf(ce.x), fabsf(ce.z)));   // magnitude bounds of the entries
+            emax->y = fmaxf(emax->y, fmaxf(fabsf(ce.y), fabsf(ce.w)));   // (gnb_kernel's fixed-point scale)
+            al = fmaf(wr, ce.x, wr1 * ce.z);
+            am = fmaf(wr, ce.y, wr1 * ce.w);
+        } else if constexpr (PAIRED) {
+            const float E1 = ex2((rb.Sl - arg_hi) - (rb.Slc - x_.sc));   // e^{-(S - A_i)}
+            const float le1 = x.x * E1;
+            al = fmaf(rb.kl1, E1, al);
+            am = fmaf(rb.km1, (x_.q1 - x_.q1c) + 0.5f * le1, am);
+            if (COMP) kahan(x_.q1, x_.q1c, le1);
+            else x_.q1 += le1;
+        }
+        if (COMP) {
+            kahan(x_.q, x_.qc, le);
+            kahan(x_.s, x_.sc, x.y * cf);
+        } else {
+            x_.q += le;
+            x_.s = fmaf(x.y, cf, x_.s);
+        }
+        const float2 av = make_float2(al, am);
+        const float2 tv = __fmul2_rn(av, make_float2(cur.fv, cur.fv));   // row j0+1
+        const float2 bv = __ffma2_rn(tv, make_float2(-1.f, -1.f), av);   // row j0
+        const float2 c11 = __fmul2_rn(tv, make_float2(cur.fu, cur.fu));
+        const float2 c10 = __ffma2_rn(c11, make_float2(-1.f, -1.f), tv);
+        const float2 c01 = __fmul2_rn(bv, make_float2(cur.fu, cur.fu));
+        const float2 c00 = __ffma2_rn(c01, make_float2(-1.f, -1.f), bv);
+        const bool chg = aoff != poff;
+        if (chg) {
+            if (PGET_ABLATE != 1 || p00.x == 12345.f) rmw(poff);   // ABLATE 1: no scatter
+            poff = aoff;
+        }
+        const float kk = chg ? 0.f : 1.f;
+        const float2 k2 = make_float2(kk, kk);
+        p00 = __ffma2_rn(p00, k2, c00);
+        p01 = __ffma2_rn(p01, k2, c01);
+        p10 = __ffma2_rn(p10, k2, c10);
+        p11 = __ffma2_rn(p11, k2, c11);
+        i = i2;
+        u = u2;
+        v = v2;
+        return nxt;
+    };
+    SmpB sa, sb;
+    load(sa, u, v, true);
+    while (step(sa, sb) && step(sb, sa)) {
+    }
+    rmw(poff);   // the last cell
+    st = x_;
+#endif
 }
 
 // ------------------------------------------------------------------------------------------ kernel
@@ -1501,7 +1633,7 @@ __device__ __forceinline__ void gn_rout_from_seg(const ProjArgs& A, int canon0, 
 
 // lin walk: the Jacobian entries of every sample of the band into the lane's cache block
 template <bool PAIRED>
-__device__ __forceinline__ void walk_lin(const float2* __restrict__ img, int P, int r0, int r1, int ilo, int64_t dU,
+__device__ __forceinline__ void walk_lin_old(const float2* __restrict__ img, int P, int r0, int r1, int ilo, int64_t dU,
                                          int64_t dV, float cf, float ch, const RayB& rb, int& i, int64_t& u,
                                          int64_t& v, StateB& st, float4* cl, int& k, float2& am)
 {
@@ -1562,6 +1694,69 @@ __device__ __forceinline__ void walk_lin(const float2* __restrict__ img, int P, 
         fv = frac23(v);
     }
     st = x_;
+}
+
+// walk_lin, unrolled by two with alternating register roles and unconditional next-sample loads (walk_b)
+template <bool PAIRED>
+__device__ __forceinline__ void walk_lin(const float2* __restrict__ img, int P, int r0, int r1, int ilo, int64_t dU,
+                                         int64_t dV, float cf, float ch, const RayB& rb, int& i, int64_t& u,
+                                         int64_t& v, StateB& st, float4* cl, int& k, float2& am)
+{
+#ifdef PGET_WALKB_OLD
+    walk_lin_old<PAIRED>(img, P, r0, r1, ilo, dU, dV, cf, ch, rb, i, u, v, st, cl, k, am);
+#else
+    {
+        const int iv = hi32(v);
+        if (i < ilo || iv < r0 || iv >= r1) return;
+    }
+    auto load = [&](SmpB& x, int64_t uu, int64_t vv, bool ok) {
+        int o = (hi32(vv) - r0) * P + hi32(uu);
+        o = ok ? o : 0;
+        PGET_CHECK(o >= 0 && o + P + 1 < (r1 - r0 + 1) * P);
+        x.c00 = img[o]; x.c01 = img[o + 1]; x.c10 = img[o + P]; x.c11 = img[o + P + 1];
+        x.fu = frac23(uu);
+        x.fv = frac23(vv);
+    };
+    StateB x_ = st;
+    auto step = [&](const SmpB& cur, SmpB& nx) -> bool {
+        const int i2 = i - 1;
+        const int64_t u2 = u - dU, v2 = v - dV;
+        const int iv2 = hi32(v2);
+        const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;   // sweep-B bands are a few rows: no band_steps
+        load(nx, u2, v2, nxt);
+        const float2 x = bilerp2(cur.c00, cur.c01, cur.c10, cur.c11, cur.fu, cur.fv);
+        const float arg_hi = fmaf(x.y, ch, x_.s);
+        const float E = ex2(arg_hi - x_.sc);
+        const float le = x.x * E;
+        float4 cv;
+        cv.x = rb.kl * E;
+        cv.y = rb.km * (((rb.G - x_.q) - (rb.Gc - x_.qc)) - 0.5f * le);
+        cv.z = 0.f;
+        cv.w = 0.f;
+        if constexpr (PAIRED) {
+            const float E1 = ex2((rb.Sl - arg_hi) - (rb.Slc - x_.sc));
+            const float le1 = x.x * E1;
+            cv.z = rb.kl1 * E1;
+            cv.w = rb.km1 * ((x_.q1 - x_.q1c) + 0.5f * le1);
+            kahan(x_.q1, x_.q1c, le1);
+        }
+        kahan(x_.q, x_.qc, le);
+        kahan(x_.s, x_.sc, x.y * cf);
+        __stcs(cl + static_cast<int64_t>(k) * 32, cv);   // streaming store: written once, read 2 x n_cg times
+        am.x = fmaxf(am.x, fmaxf(fabsf(cv.x), fabsf(cv.z)));
+        am.y = fmaxf(am.y, fmaxf(fabsf(cv.y), fabsf(cv.w)));
+        ++k;
+        i = i2;
+        u = u2;
+        v = v2;
+        return nxt;
+    };
+    SmpB sa, sb;
+    load(sa, u, v, true);
+    while (step(sa, sb) && step(sb, sa)) {
+    }
+    st = x_;
+#endif
 }
 
 // Cached entries are streamed from HBM: a 4-slot register ring (the entry of sample k+4 is loaded

@@ -517,3 +517,33 @@ def test_check_finite(pg):
     x[999] = float("inf")
     with pytest.raises(RuntimeError, match="NOT_FINITE"):
         pg.check_finite(x)
+
+
+@pytest.mark.parametrize("cid", [2, 4])
+def test_gnb_group_stride_is_bitwise_neutral(pg, cid, monkeypatch):
+    """The cached scatter's ray groups (blocks of 32 s consecutive rays split into s interleaved groups,
+    DESIGN.md 7.1.3) only decide which lanes share a warp: every lane still walks its own ray with the
+    same pending-cell sums, the shared accumulator's integer sums do not depend on the order of the adds,
+    and the flush and slot order are per unit.  So the cached GN product and a whole LM iteration (cache
+    build, cached gradient, 20 cached products) must be bitwise identical for every stride."""
+    cfg = P.CONFIGS[cid]
+    gd = P.geometry_desc(cid)
+    lam, mu = P.initial_guess(gd["n_px"])
+    pl, pm = P.rod_directions(cid)
+    lt, mt = P.make_phantom(cid)
+    y = P.poisson_noise(O.forward(gd, lt, mt), cfg.noise_peak, cfg.seed)
+    monkeypatch.setenv("PGET_GN_APPLY_CACHED", "1")
+    res = {}
+    for stride in ("1", "2", "3"):
+        monkeypatch.setenv("PGET_GNB_STRIDE", stride)
+        g = pg.Geometry(gd)
+        q = [host(x) for x in pg.gn_apply(g, dev(lam), dev(mu), dev(pl), dev(pm), cfg.alpha, 0.25)]
+        sl, sm, st = pg.gn_cg_step(g, dev(lam), dev(mu), dev(y), cfg.alpha, 0.0, cfg.n_cg)
+        torch.cuda.synchronize()
+        S = pg.read_stats(st, 1, cfg.n_cg)[0]
+        res[stride] = (q, host(sl), host(sm), S["pred"], S["f_trial"])
+    for stride in ("2", "3"):
+        a, b = res["1"], res[stride]
+        assert all(np.array_equal(x, y) for x, y in zip(a[0], b[0])), stride
+        assert np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2]), stride
+        assert a[3] == b[3] and a[4] == b[4], stride
