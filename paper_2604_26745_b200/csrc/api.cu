@@ -715,10 +715,10 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     if (const char* ev = std::getenv("PGET_GNB_TALL")) g.gnb_tall = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_GNB_INT")) g.gnb_int = g.gnb_int && std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_GNB_WIDE")) g.gnb_wide = std::atoi(ev) != 0;
-    // the cached GN path over consecutive-ray groups for single assemblies (measured: LM config 2 -0.6 %,
-    // config 3 -3 %, config 4 -1 %; config 5's 64 members +3.5 %: the separate cache build costs more
-    // there than the scatter gains); PGET_GNB_ADJ=0/1 overrides
-    g.gnb_adj = g.desc.batch == 1;
+    // the cached GN path over consecutive-ray groups (measured: LM config 2 -0.6 %, config 3 -3 %, config
+    // 4 -1 %; config 5's 64 members: +3.5 % with groups of 32 consecutive rays, -3.4 % (206.8 -> 199.7 ms)
+    // with the interleaved groups of stride 2); PGET_GNB_ADJ=0/1 overrides
+    g.gnb_adj = true;
     if (const char* ev = std::getenv("PGET_GNB_ADJ")) g.gnb_adj = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_SEGA_WIDE")) g.segA_wide = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_GNB_STRIDE")) g.gnbC_stride = std::max(1, std::min(16, std::atoi(ev)));
