@@ -145,7 +145,8 @@ __global__ void finish_kernel(const double2* __restrict__ part, int G, const flo
     double dsum = 0.0;
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n2;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int i = static_cast<int>(e % N), j = static_cast<int>(e / N);
+        const int i = static_cast<int>(static_cast<unsigned>(e) % static_cast<unsigned>(N)),   // e < N^2 < 2^32
+                  j = static_cast<int>(static_cast<unsigned>(e) / static_cast<unsigned>(N));
         double2 a = part[base + e];   // the G fp64 partials of reduce_slots_kernel, in order
         for (int g0 = 1; g0 < G; g0 += 8) {
             double2 b[8];
@@ -226,7 +227,8 @@ __global__ void regsq_kernel(const float* __restrict__ xl, const float* __restri
     double s = 0.0;
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n2;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int i = static_cast<int>(e % N), j = static_cast<int>(e / N);
+        const int i = static_cast<int>(static_cast<unsigned>(e) % static_cast<unsigned>(N)),   // e < N^2 < 2^32
+                  j = static_cast<int>(static_cast<unsigned>(e) / static_cast<unsigned>(N));
         const double a = lap_at(xl + m * n2, N, j, i), b = lap_at(xm + m * n2, N, j, i);
         s += a * a + b * b;
     }
@@ -383,7 +385,8 @@ __global__ void lapdot_kernel(const float* __restrict__ ul, const float* __restr
     double d = 0.0, q = 0.0;
     for (size_t e = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; e < n2;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int i = static_cast<int>(e % N), j = static_cast<int>(e / N);
+        const int i = static_cast<int>(static_cast<unsigned>(e) % static_cast<unsigned>(N)),   // e < N^2 < 2^32
+                  j = static_cast<int>(static_cast<unsigned>(e) / static_cast<unsigned>(N));
         const double a1 = lap_at(ul + m * n2, N, j, i), b1 = lap_at(sl + m * n2, N, j, i);
         const double a2 = lap_at(um + m * n2, N, j, i), b2 = lap_at(sm + m * n2, N, j, i);
         d += a1 * b1 + a2 * b2;
@@ -698,7 +701,8 @@ __global__ void cg_fused_kernel(const double2* __restrict__ part, int G, float a
         const float beta = betav ? betav[m] : beta_h;
         if (!st[m].stop) {
             for (size_t e = static_cast<size_t>(j) * blockDim.x + threadIdx.x; e < n2; e += stride) {
-                const int i = static_cast<int>(e % N), jj = static_cast<int>(e / N);
+                const int i = static_cast<int>(static_cast<unsigned>(e) % static_cast<unsigned>(N)),   // e < N^2 < 2^32
+                          jj = static_cast<int>(static_cast<unsigned>(e) / static_cast<unsigned>(N));
                 double2 a = part[base + e];
                 // the G partials in order; eight loads issued before their additions (latency-bound)
                 for (int g0 = 1; g0 < G; g0 += 8) {
@@ -773,7 +777,8 @@ __global__ void cg_fused_kernel(const double2* __restrict__ part, int G, float a
                 pl[q] = p1;
                 pm[q] = p2;
                 if (img4n) {   // the next GN product's packed (dlam, dmu) halves, both orientations (pack4)
-                    const int i = static_cast<int>(e % N) + kHalo, jj = static_cast<int>(e / N) + kHalo;
+                    const int i = static_cast<int>(static_cast<unsigned>(e) % static_cast<unsigned>(N)) + kHalo,
+                              jj = static_cast<int>(static_cast<unsigned>(e) / static_cast<unsigned>(N)) + kHalo;
                     reinterpret_cast<float2*>(img4n + (static_cast<size_t>(m) * P + jj) * P + i)[1] = make_float2(p1, p2);
                     reinterpret_cast<float2*>(img4t + (static_cast<size_t>(m) * P + i) * P + jj)[1] = make_float2(p1, p2);
                 }

@@ -333,17 +333,13 @@ __device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int
     // the band's origin: element (row iv, column iu) at org + iv * P + iu (one base register instead of
     // r0, which the 72-register builds otherwise recompute per sample)
     int r0o = r0;
-#ifndef PGET_WALKA_OLD
     asm volatile("" : "+r"(r0o));   // opaque: kept in a register, not recomputed from the unit per sample
-#endif
     const Cn* org = img - r0o * P;
     [[maybe_unused]] const int o_first = r0o * P;   // ok false (the band's last sample has no successor here): load the
                                   // band's first cell instead of branching around the loads
     auto load = [&](SmpA<TR::NF4>& x, int64_t uu, int64_t vv, int ivv, bool ok = true) {
         int o = ivv * P + hi32(uu);
-#ifndef PGET_WALKA_OLD
         o = ok ? o : o_first;
-#endif
         PGET_CHECK(o - o_first >= 0 && o - o_first + P + 1 < (r1 - r0 + 1) * P);
         x.c00 = org[o]; x.c01 = org[o + 1]; x.c10 = org[o + P]; x.c11 = org[o + P + 1];
         x.fu = frac23(uu);
@@ -356,9 +352,6 @@ __device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int
         const int64_t u2 = u - dU, v2 = v - dV;
         const int iv2 = hi32(v2);
         const bool nxt = --n != 0;
-#ifdef PGET_WALKA_OLD
-        if (nxt)
-#endif
         load(nx, u2, v2, iv2, nxt);
         float lam, mu, dlam = 0.f, dmu = 0.f;
         if constexpr (TR::NF4) {
@@ -451,7 +444,7 @@ struct RayB {   // per-ray constants of sweep B
 // VAR (model variant N3): cw is the lane's row of (W_j(d_i), c_i): a_lam(i) = w_r Delta W_i E_i,
 // a_mu(i) = -w_r Delta^2 (sum_{k<i} W_k lam_k c_k E_k + W_i lam_i c_i E_i / 2), E_i = e^{-c_i A_i}
 template <bool PAIRED, bool COMP, bool CACHE = false, bool VAR = false>
-__device__ __forceinline__ void walk_b_old(const float2* __restrict__ img, float2* __restrict__ acc, int P, int r0,
+__device__ __forceinline__ void walk_b_rolled(const float2* __restrict__ img, float2* __restrict__ acc, int P, int r0,
                                        int r1, int abase, int sP, int ilo, int64_t dU, int64_t dV, float cf, float ch,
                                        const RayB& rb, int& i, int64_t& u, int64_t& v, StateB& st,
                                        float wr = 0.f, float wr1 = 0.f, float4* cl = nullptr, int* kp = nullptr,
@@ -480,19 +473,10 @@ __device__ __forceinline__ void walk_b_old(const float2* __restrict__ img, float
         const int iv2 = hi32(v2);
         const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;   // sweep-B bands are a few rows: no band_steps
         float2 n00, n01, n10, n11;
-#ifdef PGET_WALKA_OLD
-        int o2 = o;
-        if (nxt) {
-            o2 = (iv2 - r0) * P + hi32(u2);
-            PGET_CHECK(o2 >= 0 && o2 + P + 1 < (r1 - r0 + 1) * P);
-            n00 = img[o2]; n01 = img[o2 + 1]; n10 = img[o2 + P]; n11 = img[o2 + P + 1];
-        }
-#else
         // the band's last sample loads its own cell again instead of branching around the loads
         const int o2 = nxt ? (iv2 - r0) * P + hi32(u2) : o;
         PGET_CHECK(o2 >= 0 && o2 + P + 1 < (r1 - r0 + 1) * P);
         n00 = img[o2]; n01 = img[o2 + 1]; n10 = img[o2 + P]; n11 = img[o2 + P + 1];
-#endif
         const float2 x = bilerp2(q00, q01, q10, q11, fu, fv);
         const float arg_hi = fmaf(x.y, ch, x_.s);
         float cv = 1.f, wv = 1.f;
@@ -607,12 +591,12 @@ __device__ __forceinline__ void walk_b(const float2* __restrict__ img, float2* _
                                        float wr = 0.f, float wr1 = 0.f, float4* cl = nullptr, int* kp = nullptr,
                                        float2* emax = nullptr, const float2* __restrict__ cw = nullptr)
 {
-#if PGET_SCATTER == 0 || defined(PGET_WALKB_OLD)
-    walk_b_old<PAIRED, COMP, CACHE, VAR>(img, acc, P, r0, r1, abase, sP, ilo, dU, dV, cf, ch, rb, i, u, v, st, wr, wr1,
+#if PGET_SCATTER == 0
+    walk_b_rolled<PAIRED, COMP, CACHE, VAR>(img, acc, P, r0, r1, abase, sP, ilo, dU, dV, cf, ch, rb, i, u, v, st, wr, wr1,
                                          cl, kp, emax, cw);
 #else
     if constexpr (!COMP) {   // the GN mode (plain sums) keeps the rolled loop: 128 registers and a spill unrolled
-        walk_b_old<PAIRED, COMP, CACHE, VAR>(img, acc, P, r0, r1, abase, sP, ilo, dU, dV, cf, ch, rb, i, u, v, st, wr,
+        walk_b_rolled<PAIRED, COMP, CACHE, VAR>(img, acc, P, r0, r1, abase, sP, ilo, dU, dV, cf, ch, rb, i, u, v, st, wr,
                                              wr1, cl, kp, emax, cw);
         return;
     }
@@ -1632,79 +1616,12 @@ __device__ __forceinline__ void gn_rout_from_seg(const ProjArgs& A, int canon0, 
 }
 
 // lin walk: the Jacobian entries of every sample of the band into the lane's cache block
-template <bool PAIRED>
-__device__ __forceinline__ void walk_lin_old(const float2* __restrict__ img, int P, int r0, int r1, int ilo, int64_t dU,
-                                         int64_t dV, float cf, float ch, const RayB& rb, int& i, int64_t& u,
-                                         int64_t& v, StateB& st, float4* cl, int& k, float2& am)
-{
-    int iv = hi32(v), iu = hi32(u);
-    if (i < ilo || iv < r0 || iv >= r1) return;
-    int o = (iv - r0) * P + iu;
-    float2 q00 = img[o], q01 = img[o + 1], q10 = img[o + P], q11 = img[o + P + 1];
-    float fu = frac23(u), fv = frac23(v);
-    StateB x_ = st;
-    while (true) {
-        const int i2 = i - 1;
-        const int64_t u2 = u - dU, v2 = v - dV;
-        const int iv2 = hi32(v2);
-        const bool nxt = i2 >= ilo && iv2 >= r0 && iv2 < r1;   // sweep-B bands are a few rows: no band_steps
-        float2 n00, n01, n10, n11;
-#ifdef PGET_WALKA_OLD
-        int o2 = o;
-        if (nxt) {
-            o2 = (iv2 - r0) * P + hi32(u2);
-            PGET_CHECK(o2 >= 0 && o2 + P + 1 < (r1 - r0 + 1) * P);
-            n00 = img[o2]; n01 = img[o2 + 1]; n10 = img[o2 + P]; n11 = img[o2 + P + 1];
-        }
-#else
-        // the band's last sample loads its own cell again instead of branching around the loads
-        const int o2 = nxt ? (iv2 - r0) * P + hi32(u2) : o;
-        PGET_CHECK(o2 >= 0 && o2 + P + 1 < (r1 - r0 + 1) * P);
-        n00 = img[o2]; n01 = img[o2 + 1]; n10 = img[o2 + P]; n11 = img[o2 + P + 1];
-#endif
-        const float2 x = bilerp2(q00, q01, q10, q11, fu, fv);
-        const float arg_hi = fmaf(x.y, ch, x_.s);
-        const float E = ex2(arg_hi - x_.sc);
-        const float le = x.x * E;
-        float4 cv;
-        cv.x = rb.kl * E;
-        cv.y = rb.km * (((rb.G - x_.q) - (rb.Gc - x_.qc)) - 0.5f * le);
-        cv.z = 0.f;
-        cv.w = 0.f;
-        if constexpr (PAIRED) {
-            const float E1 = ex2((rb.Sl - arg_hi) - (rb.Slc - x_.sc));
-            const float le1 = x.x * E1;
-            cv.z = rb.kl1 * E1;
-            cv.w = rb.km1 * ((x_.q1 - x_.q1c) + 0.5f * le1);
-            kahan(x_.q1, x_.q1c, le1);
-        }
-        kahan(x_.q, x_.qc, le);
-        kahan(x_.s, x_.sc, x.y * cf);
-        __stcs(cl + static_cast<int64_t>(k) * 32, cv);   // streaming store: written once, read 2 x n_cg times
-        am.x = fmaxf(am.x, fmaxf(fabsf(cv.x), fabsf(cv.z)));
-        am.y = fmaxf(am.y, fmaxf(fabsf(cv.y), fabsf(cv.w)));
-        ++k;
-        i = i2;
-        u = u2;
-        v = v2;
-        if (!nxt) break;
-        q00 = n00; q01 = n01; q10 = n10; q11 = n11;
-        o = o2;
-        fu = frac23(u);
-        fv = frac23(v);
-    }
-    st = x_;
-}
-
 // walk_lin, unrolled by two with alternating register roles and unconditional next-sample loads (walk_b)
 template <bool PAIRED>
 __device__ __forceinline__ void walk_lin(const float2* __restrict__ img, int P, int r0, int r1, int ilo, int64_t dU,
                                          int64_t dV, float cf, float ch, const RayB& rb, int& i, int64_t& u,
                                          int64_t& v, StateB& st, float4* cl, int& k, float2& am)
 {
-#ifdef PGET_WALKB_OLD
-    walk_lin_old<PAIRED>(img, P, r0, r1, ilo, dU, dV, cf, ch, rb, i, u, v, st, cl, k, am);
-#else
     {
         const int iv = hi32(v);
         if (i < ilo || iv < r0 || iv >= r1) return;
@@ -1756,7 +1673,6 @@ __device__ __forceinline__ void walk_lin(const float2* __restrict__ img, int P, 
     while (step(sa, sb) && step(sb, sa)) {
     }
     st = x_;
-#endif
 }
 
 // Cached entries are streamed from HBM: a 4-slot register ring (the entry of sample k+4 is loaded
