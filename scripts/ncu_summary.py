@@ -89,8 +89,11 @@ def main():
              "Launch list: `ncu --metrics gpu__time_duration.sum --clock-control none` of "
              f"`python bench.py --config {cid} --steps 1 --warmup 3 --no-cpu-baseline --no-e2e --no-per-config` "
              f"(config {cid}; cold-cache, serialised launches: compare shares, not absolute times).", ""]
-    tab, n, T = launches(lst)
-    lines += [f"{n} launches, {T / 1e3:.2f} ms total.", ""] + tab + [""]
+    if lst == "-":   # no launch list for this capture
+        lines = [f"# ncu summary, round {tag}", ""]
+    else:
+        tab, n, T = launches(lst)
+        lines += [f"{n} launches, {T / 1e3:.2f} ms total.", ""] + tab + [""]
     if rep == "-":
         out = os.path.join(ROOT, "profiles", f"ncu_summary_{tag}.md")
         open(out, "w").write("\n".join(lines) + "\n")
