@@ -240,6 +240,34 @@ def test_lm_iteration(pg, cid):
     assert rel_l2(s, so) <= 0.1
 
 
+def test_lm_iteration_comb_layout(pg, monkeypatch):
+    """The LM iteration with the comb-lane cache layout (PGET_GNB_ADJ=0): the gradient VJP's fused cache
+    builder (seg_b_kernel<VJP, CACHE>, the unrolled sweep B with cache stores) and the scatter over comb
+    groups -- the default since round 2 is the interleaved layout built by lin_kernel, so this keeps the
+    alternative path pinned to the oracle with test_lm_iteration's tolerances (config 2)."""
+    monkeypatch.setenv("PGET_GNB_ADJ", "0")
+    cid = 2
+    cfg = P.CONFIGS[cid]
+    gd = P.geometry_desc(cid)
+    g = pg.Geometry(gd)
+    lt, mt = P.make_phantom(cid)
+    y = P.poisson_noise(O.forward(gd, lt, mt), cfg.noise_peak, cfg.seed)
+    l0, m0 = P.initial_guess(gd["n_px"])
+    sl, sm, st = pg.gn_cg_step(g, dev(l0), dev(m0), dev(y), cfg.alpha, 0.0, cfg.n_cg)
+    torch.cuda.synchronize()
+    S = pg.read_stats(st, 1, cfg.n_cg)[0]
+    sl_o, sm_o, So = O.gn_cg_step(gd, l0, m0, y, cfg.alpha, 0.0, cfg.n_cg)
+    s = np.concatenate([host(sl).ravel(), host(sm).ravel()])
+    so = np.concatenate([sl_o.ravel(), sm_o.ravel()])
+    for k in ("f", "misfit", "reg", "grad_norm"):
+        assert abs(S[k] - So[k]) <= 1e-5 * abs(So[k]), k
+    assert abs(S["cg_res"][1] - So["cg_res"][1]) <= 1e-4 * So["cg_res"][1]
+    assert abs(S["pred"] - So["pred"]) <= 1e-3 * abs(So["pred"])
+    assert abs(S["rho"] - So["rho"]) <= rho_tol(So)
+    assert S["accepted"] == So["accepted"]
+    assert rel_l2(s, so) <= 0.1
+
+
 def test_lm_iteration_small_batched(pg):
     gd = dict(n_px=24, n_angles=16, n_banks=2, n_det=21, n_subrays=3, subray_sigma=0.4, step_px=0.5,
               bank1_shift=0.0, batch=3)
