@@ -710,6 +710,7 @@ pget_status pget_geometry_create(const pget_geometry_desc* desc, int device, pge
     if (const char* ev = std::getenv("PGET_JVP_FUSED")) g.jvp_seg = std::atoi(ev) == 0;
     if (const char* ev = std::getenv("PGET_FWD_FUSED")) g.fwd_seg = std::atoi(ev) == 0;
     if (const char* ev = std::getenv("PGET_FWD_PLAIN")) g.fwd_plain = std::atoi(ev) != 0;
+    if (const char* ev = std::getenv("PGET_CG_PDL")) g.cg_pdl = std::atoi(ev) != 0;
     if (const char* ev = std::getenv("PGET_FWD_PLAIN_TRIAL")) g.fwd_plain_trial = std::atoi(ev) != 0;
     g.gnb_tall = g.P >= 200;   // measured: config 4 -3.6 % LM, config 2 +0.8 %
     if (const char* ev = std::getenv("PGET_GNB_TALL")) g.gnb_tall = std::atoi(ev) != 0;
@@ -1453,8 +1454,23 @@ static pget_status gn_cg_impl(const Geometry& g, WS w, const float* lam, const f
             void* args[] = {&w.gacc, &GG, &al, &be, &bv, &s_lam, &s_mu, &w.zl, &w.zm, &w.pl, &w.pm, &w.ql, &w.qm,
                             &pg, &pz, &cgs, &stats, &kk, &NN, &BB, &nb, &i4n, &i4t, &PP, &prv};
             const int grid = std::min(B * kNblk, g.cg_coop_blocks);
-            CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cg_fused_kernel), dim3(grid), dim3(kVecThreads),
-                                           args, 0, s));
+            if (g.cg_pdl) {   // cooperative + programmatic serialisation: overlaps the slot reduction's tail
+                cudaLaunchConfig_t cfg = {};
+                cfg.gridDim = dim3(grid);
+                cfg.blockDim = dim3(kVecThreads);
+                cfg.stream = s;
+                cudaLaunchAttribute at[2];
+                at[0].id = cudaLaunchAttributeCooperative;
+                at[0].val.cooperative = 1;
+                at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+                at[1].val.programmaticStreamSerializationAllowed = 1;
+                cfg.attrs = at;
+                cfg.numAttrs = pdl_enabled() ? 2 : 1;
+                CK(cudaLaunchKernelExC(&cfg, reinterpret_cast<const void*>(cg_fused_kernel), args));
+            } else {
+                CK(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(cg_fused_kernel), dim3(grid), dim3(kVecThreads),
+                                               args, 0, s));
+            }
             note();
         }
         CK(cudaGetLastError());

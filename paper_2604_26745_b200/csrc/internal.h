@@ -201,6 +201,7 @@ struct Geometry {
     bool fwd_seg = true;          // forward as the segmented VJP-mode phase A + combine
     bool fwd_plain = true;        // standalone forward: forward-mode phase A (plain sums); trial f(u+s) too if fwd_plain_trial
     bool fwd_plain_trial = false;
+    bool cg_pdl = true;           // the fused CG kernel launched cooperative + programmatic (PGET_CG_PDL=0: plain cooperative)
     int32_t* d_tabsA = nullptr;   // traced angle-banks of the adjoint schedule (task_ab_p or task_ab)
     bool adj_seg = true;   // adjoint (VJP / GN) as the segmented two-phase projector (else the fused one)
     bool gnb_tall = true;   // gnb_kernel with its own (taller) bands: no stage buffers to fit
