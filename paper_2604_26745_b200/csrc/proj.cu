@@ -1795,8 +1795,12 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
         PGET_CHECK(hi32(u) >= 0 && hi32(u) + 1 < P && iv >= r0 && iv < r1 && p0 + k * 32 < cend);
         const float fu = frac23(u), fv = frac23(v);
         const float2 av = __ffma2_rn(w2, make_float2(c.x, c.y), __fmul2_rn(w12, make_float2(c.z, c.w)));
+#if PGET_ABLATE == 4   // 4: no entry stream (the first four rows again: cache hits; wrong values, timing only)
+        c = __ldg(p0 + (((k + 4) & 3) << 5));
+#else
         asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + ((k + PGET_PF_DIST) << 5)));
         c = __ldg(p0 + ((k + 4) << 5));
+#endif
         ++k;
         const float2 tv = __fmul2_rn(av, make_float2(fv, fv));         // row j0+1
         const float2 bv = __ffma2_rn(tv, make_float2(-1.f, -1.f), av); // row j0
