@@ -58,6 +58,12 @@ __device__ __forceinline__ float frac23(int64_t x)
     return __uint_as_float((static_cast<uint32_t>(x) >> 9) | 0x3f800000u) - 1.0f;
 }
 
+// 1 + frac23(x), exactly (the float in [1, 2) whose mantissa is the rounded fraction)
+__device__ __forceinline__ float frac23p1(int64_t x)
+{
+    return __uint_as_float((static_cast<uint32_t>(x) >> 9) | 0x3f800000u);
+}
+
 __device__ __forceinline__ int hi32(int64_t x) { return static_cast<int>(x >> 32); }
 
 __device__ __forceinline__ float ex2(float x)
@@ -1793,7 +1799,9 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
         const int iv = hi32(v);
         const uint32_t aa = cell(iv, hi32(u));
         PGET_CHECK(hi32(u) >= 0 && hi32(u) + 1 < P && iv >= r0 && iv < r1 && p0 + k * 32 < cend);
-        const float fu = frac23(u), fv = frac23(v);
+        // 1 + the bilinear fractions (exactly): x * f = x * (1 + f) - x in one FMA, bit for bit the
+        // product of walk_b, without the two subtractions of 1
+        const float gu = frac23p1(u), gv = frac23p1(v);
         const float2 av = __ffma2_rn(w2, make_float2(c.x, c.y), __fmul2_rn(w12, make_float2(c.z, c.w)));
 #if PGET_ABLATE == 4   // 4: no entry stream (the first four rows again: cache hits; wrong values, timing only)
         c = __ldg(p0 + (((k + 4) & 3) << 5));
@@ -1802,11 +1810,12 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
         c = __ldg(p0 + ((k + 4) << 5));
 #endif
         ++k;
-        const float2 tv = __fmul2_rn(av, make_float2(fv, fv));         // row j0+1
+        const float2 nav = make_float2(-av.x, -av.y);
+        const float2 tv = __ffma2_rn(av, make_float2(gv, gv), nav);     // row j0+1: av * fv
         const float2 bv = __ffma2_rn(tv, make_float2(-1.f, -1.f), av); // row j0
-        const float2 c11 = __fmul2_rn(tv, make_float2(fu, fu));
+        const float2 c11 = __ffma2_rn(tv, make_float2(gu, gu), make_float2(-tv.x, -tv.y));
         const float2 c10 = __ffma2_rn(c11, make_float2(-1.f, -1.f), tv);
-        const float2 c01 = __fmul2_rn(bv, make_float2(fu, fu));
+        const float2 c01 = __ffma2_rn(bv, make_float2(gu, gu), make_float2(-bv.x, -bv.y));
         const float2 c00 = __ffma2_rn(c01, make_float2(-1.f, -1.f), bv);
         if (aa != pa) {
             if (PGET_ABLATE != 1 || p00.x == 12345.f) rmw(pa, p00, p01, p10, p11);   // ABLATE 1: no scatter

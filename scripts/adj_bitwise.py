@@ -25,6 +25,12 @@ if sys.argv[1] == "save":
         ql, qm = pg.gn_apply(g, dev(lam), dev(mu), dev(dl), dev(dm), 1e-3, 0.25)
         for k, v in (("gl", gl), ("gm", gm), ("ql", ql), ("qm", qm)):
             res[f"cfg{cid}_{k}"] = v.cpu().numpy()
+        # one LM iteration (cache build, cached gradient, 20 cached GN products)
+        l0, m0 = P.initial_guess(gd["n_px"])
+        y = pg.forward(g, dev(lam), dev(mu)).contiguous()
+        sl, sm, st = pg.gn_cg_step(g, dev(l0), dev(m0), y, 1e-3, 0.0, 20)
+        res[f"cfg{cid}_lm_sl"] = sl.cpu().numpy()
+        res[f"cfg{cid}_lm_sm"] = sm.cpu().numpy()
     np.savez(os.path.join(out, f"adj_{sys.argv[2]}.npz"), **res)
     print("saved", sys.argv[2])
 else:
