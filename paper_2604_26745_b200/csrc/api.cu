@@ -303,6 +303,8 @@ ProjArgs base_args(const Geometry& g, const ProjCfg& c)
     A.off_wacc = c.off_wacc;
     A.off_rout = c.off_rout;
     A.off_gsh = c.off_gsh;
+    A.P4 = 4 * g.P;
+    A.planeB4 = 4 * (A.RbB + 1) * g.P;
     A.delta = static_cast<float>(g.delta);
     const double cf = -g.delta * 1.4426950408889634;   // -Delta log2(e)
     A.cf = static_cast<float>(cf);
@@ -1119,6 +1121,7 @@ static pget_status gnc_product(const Geometry& g, const WS& w, const float* lam,
     if (e == cudaSuccess) {
         ProjArgs Ag = A;
         Ag.RbB = c.RbG;
+        Ag.planeB4 = 4 * (c.RbG + 1) * g.P;
         Ag.off_wacc = c.off_waccG;
         Ag.off_rout = c.off_routG;
         Ag.passesB = c.passesG;
@@ -1163,6 +1166,7 @@ static pget_status gnc_gradient(const Geometry& g, const WS& w, const float* win
     if (e == cudaSuccess) {
         ProjArgs Ag = A;
         Ag.RbB = c.RbG;
+        Ag.planeB4 = 4 * (c.RbG + 1) * g.P;
         Ag.off_wacc = c.off_waccG;
         Ag.off_rout = c.off_routG;
         Ag.passesB = c.passesG;

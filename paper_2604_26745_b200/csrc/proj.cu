@@ -1752,15 +1752,15 @@ __device__ __forceinline__ void red_s32(uint32_t addr, int v)
 template <bool INTACC>
 __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0, int r1, int ilo,
                                          int64_t dU, int64_t dV, float wr, float wr1, int& i, int64_t& u, int64_t& v,
-                                         const float4*& ck, const float4* cend, float2 S, uint32_t planeB)
+                                         const float4*& ck, const float4* cend, float2 S, uint32_t planeB, int sP4)
 {
     const int sP = P;   // accumulator row of sample row iv: iv - r0
     const int iv0 = hi32(v);
     if (i < ilo || iv0 < r0 || iv0 >= r1) return;
     int n = band_steps(i, ilo, v, dV, r0, r1);
     // byte address of a sample's cell in the shared accumulator: org + iv * sP4 + iu * 4 (INTACC), with
-    // org the address of (row 0, col 0) for this band's row mapping (abase + (iv - r0) sP + iu)
-    const int sP4 = sP * 4;
+    // org the address of (row 0, col 0) for this band's row mapping (abase + (iv - r0) sP + iu); sP4 =
+    // 4 P and planeB come from the kernel parameters (constant-bank operands, nothing rematerialised)
     const uint32_t org = static_cast<uint32_t>(__cvta_generic_to_shared(acc)) - static_cast<uint32_t>(r0 * sP * 4);
     auto cell = [&](int ivv, int iuu) -> uint32_t { return org + static_cast<uint32_t>(ivv * sP4 + iuu * 4); };
     auto rmw = [&](uint32_t a0, float2 a, float2 b, float2 c, float2 d) {
@@ -2173,7 +2173,7 @@ __global__ void __launch_bounds__(WIDE ? 832 : 512, 1) gnb_kernel(ProjArgs A)
                 // band is flushed with it, zeroed, and collects the next band's part (slot adds twice)
                 if (PGET_ABLATE != 3)   // 3: no walk
                     walk_gnb<INTACC>(wacc, P, r0, r1, ilo, dU, dV, wr, wr1, ii, uu, vv, cl, cend, S,
-                                     static_cast<uint32_t>(RB1 * P * 4));
+                                     static_cast<uint32_t>(A.planeB4), A.P4);
                 __syncthreads();   // every warp ring complete
                 int qlo, qhi;
                 {
