@@ -65,6 +65,14 @@ __device__ __forceinline__ float frac23p1(int64_t x)
 }
 
 __device__ __forceinline__ int hi32(int64_t x) { return static_cast<int>(x >> 32); }
+// the high word as the register it is (the compiler otherwise folds ">> 32, * 4" into a funnel shift
+// by 30 plus a mask)
+__device__ __forceinline__ int hi32r(int64_t x)
+{
+    int lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(x));
+    return hi;
+}
 
 __device__ __forceinline__ float ex2(float x)
 {
@@ -1797,7 +1805,7 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
     const float2 w2 = make_float2(wr, wr), w12 = make_float2(wr1, wr1);
     auto step = [&](float4& c) -> bool {
         const int iv = hi32(v);
-        const uint32_t aa = cell(iv, hi32(u));
+        const uint32_t aa = cell(iv, hi32r(u));
         PGET_CHECK(hi32(u) >= 0 && hi32(u) + 1 < P && iv >= r0 && iv < r1 && p0 + k * 32 < cend);
         // 1 + the bilinear fractions (exactly): x * f = x * (1 + f) - x in one FMA, bit for bit the
         // product of walk_b, without the two subtractions of 1
@@ -1829,9 +1837,21 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
         }
         u -= dU;
         v -= dV;
-        return --n != 0;
+        return true;
     };
-    while (step(c0) && step(c1) && step(c2) && step(c3)) {
+    // full rounds of the 4-entry ring without per-sample exit tests, then the 0-3 remaining samples
+    for (; n >= 4; n -= 4) {
+        step(c0);
+        step(c1);
+        step(c2);
+        step(c3);
+    }
+    if (n > 0) {
+        step(c0);
+        if (n > 1) {
+            step(c1);
+            if (n > 2) step(c2);
+        }
     }
     rmw(pa, p00, p01, p10, p11);
     i -= k;
