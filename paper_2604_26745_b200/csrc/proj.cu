@@ -69,8 +69,8 @@ __device__ __forceinline__ int hi32(int64_t x) { return static_cast<int>(x >> 32
 // by 30 plus a mask)
 __device__ __forceinline__ int hi32r(int64_t x)
 {
-    int lo, hi;
-    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(x));
+    int hi;
+    asm("{\n\t.reg .b32 lo;\n\tmov.b64 {lo, %0}, %1;\n\t}" : "=r"(hi) : "l"(x));
     return hi;
 }
 
