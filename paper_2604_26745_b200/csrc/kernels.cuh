@@ -102,6 +102,7 @@ struct SidArgs {
     double det_radius;
     float c_slope, r_slope, sig0, lmax;
     int N, P, R, J, n_det, n_ab, nB, B;
+    int dpc, nch;           // detectors per CTA, CTAs per angle-bank (set by the launchers)
 };
 cudaError_t launch_sid_proj(int mode, bool var, const SidArgs& A, cudaStream_t s);
 cudaError_t launch_sid_adj(int mode, bool var, const SidArgs& A, double2* gacc, cudaStream_t s);

@@ -10,8 +10,8 @@
 // JVP: dg = sum_q r_q (dlam_q - lam_q c_q dA_q) E_q;  VJP: a_lam(q) = w r_q E_q,
 // a_mu(q) = -w l_q (sum_{p<q} r_p lam_p c_p E_p + r_q lam_q c_q E_q / 2).
 //
-// Design.  One CTA per (angle-bank, member), one thread per ray, images read through
-// L1/L2 from the packed padded float2 / float4 images (a ray reads one pixel per crossing; adjacent
+// Design.  A CTA per (angle-bank, chunk of whole detectors, member), ~128 rays, one
+// thread per ray, images read through L1/L2 from the packed padded float2 / float4 images (a ray reads one pixel per crossing; adjacent
 // lanes trace adjacent rays, so a warp's reads fall on a few neighbouring pixels).  The traversal
 // (Siddon's crossing merge, walked from the detector end so the optical depth accumulates) is fp64
 // with the oracle's exact operation order (explicit _rn intrinsics, no contraction): every pixel
@@ -26,8 +26,16 @@
 
 #include <algorithm>
 #include <mutex>
+#include <type_traits>
 
 #include "kernels.cuh"
+
+#ifndef PGET_SID_CHUNK
+#define PGET_SID_CHUNK 1   // CTAs of whole detectors, ~128 rays (0: one CTA per angle-bank; experiment switch)
+#endif
+#ifndef PGET_SID_MINB
+#define PGET_SID_MINB 1   // CTAs per SM the register allocation targets (experiment switch)
+#endif
 
 namespace pget {
 
@@ -109,10 +117,11 @@ struct Edges {
     __device__ __forceinline__ void step() { e += de; set(); }
 };
 
-// Walk the crossings of a line from the detector end: visit(row, col, l, tm) per interval of positive
-// length, in order of decreasing t.
-template <class F>
-__device__ __forceinline__ void walk(const Line& L, int N, F&& visit)
+// Walk the crossings of a line from the detector end: visit(fetch(row, col), row, col, l, tm) per
+// interval of positive length, in order of decreasing t.  (Measured: issuing each pixel load one
+// interval ahead of its use, with the traversal as a generator, made every mode 5-15 % slower.)
+template <class Fe, class F>
+__device__ __forceinline__ void walk(const Line& L, int N, Fe&& fetch, F&& visit)
 {
     Edges ex, ey;
     ex.init(L.X0, L.wX, L.iX, L.tin, L.tout, N);
@@ -127,7 +136,7 @@ __device__ __forceinline__ void walk(const Line& L, int N, F&& visit)
             int row = static_cast<int>(floor(__dadd_rn(L.Y0, __dmul_rn(tm, L.wY))));
             col = max(0, min(N - 1, col));
             row = max(0, min(N - 1, row));
-            visit(row, col, l, tm);
+            visit(fetch(row, col), row, col, l, tm);
         }
         if (!(tn > L.tin)) break;
         const bool sx = ex.t == tn, sy = ey.t == tn;
@@ -172,15 +181,17 @@ __device__ __forceinline__ RayState ray_sums(const SidArgs& A, int m, int ab, in
     const int j = r % A.J;
     const size_t base = static_cast<size_t>(m) * A.P * A.P;
     constexpr bool F4 = MODE == MODE_JVP || MODE == MODE_GN;
-    walk(L, A.N, [&](int row, int col, double l, double tm) {
+    using Px = typename std::conditional<F4, float4, float2>::type;
+    auto fetch = [&](int row, int col) -> Px {
         const size_t o = base + static_cast<size_t>(row + kHalo) * A.P + (col + kHalo);
-        float lam, mu, dlam = 0.f, dmu = 0.f;
+        if constexpr (F4) return __ldg(A.img4 + o);
+        else return __ldg(A.img2 + o);
+    };
+    walk(L, A.N, fetch, [&](const Px& x, int, int, double l, double tm) {
+        float lam = x.x, mu = x.y, dlam = 0.f, dmu = 0.f;
         if constexpr (F4) {
-            const float4 x = __ldg(A.img4 + o);
-            lam = x.x; mu = x.y; dlam = x.z; dmu = x.w;
-        } else {
-            const float2 x = __ldg(A.img2 + o);
-            lam = x.x; mu = x.y;
+            dlam = x.z;
+            dmu = x.w;
         }
         const float lf = static_cast<float>(l);
         float cq = 1.f, rq = lf;
@@ -215,23 +226,24 @@ __device__ __forceinline__ RayState ray_sums(const SidArgs& A, int m, int ab, in
 
 // ---- forward / JVP: per-ray sums, then the sub-ray weighting into the detector readings
 template <int MODE, bool VAR>
-__global__ void __launch_bounds__(256, 1) sid_proj_kernel(SidArgs A)
+__global__ void __launch_bounds__(256, PGET_SID_MINB) sid_proj_kernel(SidArgs A)
 {
     pdl_entry();
-    extern __shared__ float rout[];   // [2R]
-    const int ab = blockIdx.x, m = blockIdx.y, R = A.R;
-    for (int r = threadIdx.x; r < R; r += blockDim.x) {
-        const RayState st = ray_sums<MODE, VAR>(A, m, ab, r);
-        rout[r] = st.g - st.gc;
-        if (MODE == MODE_JVP) rout[R + r] = st.dg - st.dgc;
+    extern __shared__ float rout[];   // [2 dpc J]: the CTA's rays
+    const int ab = blockIdx.x / A.nch, ch = blockIdx.x - ab * A.nch, m = blockIdx.y;
+    const int d0 = ch * A.dpc, d1 = min(A.n_det, d0 + A.dpc), ra = d0 * A.J, nr = (d1 - d0) * A.J;
+    for (int t = threadIdx.x; t < nr; t += blockDim.x) {
+        const RayState st = ray_sums<MODE, VAR>(A, m, ab, ra + t);
+        rout[t] = st.g - st.gc;
+        if (MODE == MODE_JVP) rout[nr + t] = st.dg - st.dgc;
     }
     __syncthreads();
     const size_t ob = (static_cast<size_t>(m) * A.n_ab + ab) * A.n_det;
-    for (int d = threadIdx.x; d < A.n_det; d += blockDim.x) {
+    for (int d = d0 + threadIdx.x; d < d1; d += blockDim.x) {
         float acc = 0.f, dacc = 0.f;
         for (int j = 0; j < A.J; ++j) {
-            acc = fmaf(A.wj[j], rout[d * A.J + j], acc);
-            if (MODE == MODE_JVP) dacc = fmaf(A.wj[j], rout[R + d * A.J + j], dacc);
+            acc = fmaf(A.wj[j], rout[(d - d0) * A.J + j], acc);
+            if (MODE == MODE_JVP) dacc = fmaf(A.wj[j], rout[nr + (d - d0) * A.J + j], dacc);
         }
         if (A.y) A.y[ob + d] = acc;
         if (MODE == MODE_JVP) A.dy[ob + d] = dacc;
@@ -241,28 +253,29 @@ __global__ void __launch_bounds__(256, 1) sid_proj_kernel(SidArgs A)
 // ---- adjoint pass 1 (VJP: weights from A.win; GN: the (J p) of A.img4's p): per ray the weight w_r,
 // G (compensated) into A.ray, and the member's magnitude bounds max|w| sum r E, max|w| l_max sum r|lam|cE
 template <int MODE, bool VAR>
-__global__ void __launch_bounds__(256, 1) sid_adj_a_kernel(SidArgs A)
+__global__ void __launch_bounds__(256, PGET_SID_MINB) sid_adj_a_kernel(SidArgs A)
 {
     pdl_entry();
-    extern __shared__ float rout[];   // [R]: GN (J p) per ray
-    __shared__ float red[2][16];
-    const int ab = blockIdx.x, m = blockIdx.y, R = A.R, J = A.J;
+    extern __shared__ float rout[];   // [dpc J]: GN (J p) per ray of the CTA
+    __shared__ float red[2][32];
+    const int ab = blockIdx.x / A.nch, ch = blockIdx.x - ab * A.nch, m = blockIdx.y, R = A.R, J = A.J;
+    const int d0 = ch * A.dpc, d1 = min(A.n_det, d0 + A.dpc), ra = d0 * J, re = d1 * J;
     const size_t rb = (static_cast<size_t>(m) * A.n_ab + ab) * R;
-    for (int r = threadIdx.x; r < R; r += blockDim.x) {
+    for (int r = ra + threadIdx.x; r < re; r += blockDim.x) {
         const RayState st = ray_sums<MODE, VAR>(A, m, ab, r);
         A.ray[rb + r] = make_float4(0.f, st.g, st.gc, 0.f);
         A.raybd[rb + r] = make_float2(st.lsum, st.gabs);
-        if (MODE == MODE_GN) rout[r] = st.dg - st.dgc;
+        if (MODE == MODE_GN) rout[r - ra] = st.dg - st.dgc;
     }
     __syncthreads();
     float bl = 0.f, bm = 0.f;
     const size_t ob = (static_cast<size_t>(m) * A.n_ab + ab) * A.n_det;
-    for (int r = threadIdx.x; r < R; r += blockDim.x) {
+    for (int r = ra + threadIdx.x; r < re; r += blockDim.x) {
         const int d = r / J, j = r - d * J;
         float wd;
         if (MODE == MODE_GN) {
             wd = 0.f;
-            for (int q = 0; q < J; ++q) wd = fmaf(A.wj[q], rout[d * J + q], wd);
+            for (int q = 0; q < J; ++q) wd = fmaf(A.wj[q], rout[(d - d0) * J + q], wd);
         } else {
             wd = A.win[ob + d];
         }
@@ -311,17 +324,18 @@ __device__ __forceinline__ void red_u64(unsigned long long* p, double v)
 
 // ---- adjoint pass 2: walk again (the same E bit for bit) and scatter the adjoint weights
 template <bool VAR>
-__global__ void __launch_bounds__(256, 1) sid_adj_b_kernel(SidArgs A, bool f4)
+__global__ void __launch_bounds__(256, PGET_SID_MINB) sid_adj_b_kernel(SidArgs A, bool f4)
 {
     pdl_entry();
-    const int ab = blockIdx.x, m = blockIdx.y, R = A.R;
+    const int ab = blockIdx.x / A.nch, ch = blockIdx.x - ab * A.nch, m = blockIdx.y, R = A.R;
+    const int d0 = ch * A.dpc, d1 = min(A.n_det, d0 + A.dpc);
     const size_t rb = (static_cast<size_t>(m) * A.n_ab + ab) * R;
     const double Sl = fx_scale(A.bound[2 * m], A.nhits), Sm = fx_scale(A.bound[2 * m + 1], A.nhits);
     const size_t n2 = static_cast<size_t>(A.N) * A.N;
     unsigned long long* accl = A.acc + static_cast<size_t>(m) * 2 * n2;
     unsigned long long* accm = accl + n2;
     const size_t base = static_cast<size_t>(m) * A.P * A.P;
-    for (int r = threadIdx.x; r < R; r += blockDim.x) {
+    for (int r = d0 * A.J + threadIdx.x; r < d1 * A.J; r += blockDim.x) {
         const float4 rv = A.ray[rb + r];
         const float w = rv.x, G = rv.y, Gc = rv.z;
         if (w == 0.f) continue;
@@ -329,16 +343,16 @@ __global__ void __launch_bounds__(256, 1) sid_adj_b_kernel(SidArgs A, bool f4)
         if (!line_of(A, ab, r, L)) continue;
         const int j = r % A.J;
         float s = 0.f, sc = 0.f, Q = 0.f, Qc = 0.f;
-        walk(L, A.N, [&](int row, int col, double l, double tm) {
+        auto fetch = [&](int row, int col) -> float2 {
             const size_t o = base + static_cast<size_t>(row + kHalo) * A.P + (col + kHalo);
-            float lam, mu;
             if (f4) {
                 const float4 x = __ldg(A.img4 + o);
-                lam = x.x; mu = x.y;
-            } else {
-                const float2 x = __ldg(A.img2 + o);
-                lam = x.x; mu = x.y;
+                return make_float2(x.x, x.y);
             }
+            return __ldg(A.img2 + o);
+        };
+        walk(L, A.N, fetch, [&](const float2& x, int row, int col, double l, double tm) {
+            const float lam = x.x, mu = x.y;
             const float lf = static_cast<float>(l);
             float cq = 1.f, rq = lf;
             if constexpr (VAR) {
@@ -362,7 +376,7 @@ __global__ void __launch_bounds__(256, 1) sid_adj_b_kernel(SidArgs A, bool f4)
 }
 
 // ---- adjoint pass 3: fixed point -> the fp64 partials (G = 1) of the finish / CG kernels
-__global__ void __launch_bounds__(256, 1) sid_adj_fin_kernel(SidArgs A, double2* gacc)
+__global__ void __launch_bounds__(256, PGET_SID_MINB) sid_adj_fin_kernel(SidArgs A, double2* gacc)
 {
     pdl_entry();
     const int m = blockIdx.y;
@@ -380,15 +394,31 @@ __global__ void __launch_bounds__(256, 1) sid_adj_fin_kernel(SidArgs A, double2*
 
 }  // namespace
 
-// 256 threads per CTA, a ray per thread per round (equal-round blocks of up to 512 threads measured
-// mixed: forward -3 %, JVP on config 2 +20 %, VJP on config 4 +8 %)
-static int sid_block(int) { return 256; }
-
-cudaError_t launch_sid_proj(int mode, bool var, const SidArgs& A, cudaStream_t s)
+// CTAs of whole detectors (the sub-ray weighting stays in shared memory), about 128 rays each, one ray
+// per thread: (angle-bank, detector chunk, member) -- thousands of small CTAs instead of one CTA per
+// angle-bank looping over its rays in rounds of 256 (whose last round and last wave ran mostly idle)
+static SidArgs sid_chunks(const SidArgs& A0, int& nt)
 {
-    const dim3 grid(A.n_ab, A.B);
-    const int nt = sid_block(A.R);
-    const size_t sm = 2 * sizeof(float) * A.R;
+    SidArgs A = A0;
+    if (!PGET_SID_CHUNK) {   // one CTA of 256 threads per angle-bank (the first design)
+        A.dpc = A.n_det;
+        A.nch = 1;
+        nt = 256;
+        return A;
+    }
+    const int nch0 = std::max(1, (A.R + 127) / 128);
+    A.dpc = std::max(1, (A.n_det + nch0 - 1) / nch0);
+    A.nch = (A.n_det + A.dpc - 1) / A.dpc;
+    nt = std::min(256, std::max(32, (A.dpc * A.J + 31) / 32 * 32));
+    return A;
+}
+
+cudaError_t launch_sid_proj(int mode, bool var, const SidArgs& A0, cudaStream_t s)
+{
+    int nt;
+    const SidArgs A = sid_chunks(A0, nt);
+    const dim3 grid(A.n_ab * A.nch, A.B);
+    const size_t sm = 2 * sizeof(float) * A.dpc * A.J;
     if (mode == MODE_FWD)
         return var ? launch_k(sid_proj_kernel<MODE_FWD, true>, grid, nt, sm, s, A)
                    : launch_k(sid_proj_kernel<MODE_FWD, false>, grid, nt, sm, s, A);
@@ -396,14 +426,15 @@ cudaError_t launch_sid_proj(int mode, bool var, const SidArgs& A, cudaStream_t s
                : launch_k(sid_proj_kernel<MODE_JVP, false>, grid, nt, sm, s, A);
 }
 
-cudaError_t launch_sid_adj(int mode, bool var, const SidArgs& A, double2* gacc, cudaStream_t s)
+cudaError_t launch_sid_adj(int mode, bool var, const SidArgs& A0, double2* gacc, cudaStream_t s)
 {
-    const dim3 grid(A.n_ab, A.B);
-    const int nt = sid_block(A.R);
+    int nt;
+    const SidArgs A = sid_chunks(A0, nt);
+    const dim3 grid(A.n_ab * A.nch, A.B);
     const size_t n2 = static_cast<size_t>(A.N) * A.N;
     cudaError_t e = cudaMemsetAsync(A.bound, 0, 2 * sizeof(unsigned) * A.B, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(A.acc, 0, 2 * n2 * sizeof(unsigned long long) * A.B, s);
-    const size_t sm = sizeof(float) * A.R;
+    const size_t sm = sizeof(float) * A.dpc * A.J;
     if (e == cudaSuccess) {
         if (mode == MODE_GN)
             e = var ? launch_k(sid_adj_a_kernel<MODE_GN, true>, grid, nt, sm, s, A)
