@@ -304,6 +304,8 @@ ProjArgs base_args(const Geometry& g, const ProjCfg& c)
     A.off_rout = c.off_rout;
     A.off_gsh = c.off_gsh;
     A.P4 = 4 * g.P;
+    A.P8 = 8 * g.P;
+    A.P16 = 16 * g.P;
     A.planeB4 = 4 * (A.RbB + 1) * g.P;
     A.delta = static_cast<float>(g.delta);
     const double cf = -g.delta * 1.4426950408889634;   // -Delta log2(e)

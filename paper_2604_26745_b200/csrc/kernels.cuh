@@ -52,6 +52,7 @@ struct ProjArgs {
     float* y;               // [B][n_ab][n_det]
     float* dy;              // [B][n_ab][n_det]
     int N, Ns, P, n_det, J, R, n_ab, B;
+    int P8, P16;            // 8 P and 16 P: byte row pitches of the staged float2 / float4 bands (walk_a; constant-bank operands)
     int P4, planeB4;        // 4 P and 4 (RbB + 1) P: byte strides of the cached scatter's accumulator (constant-bank operands)
     int dup_half;           // n_angles / 2 when duplicate angle-banks are merged (geometry dup), else 0
     int RbA, RbB, nbA, nbB, passesA, passesB;   // sweep A: 32 adjacent rays per warp; sweep B: comb groups

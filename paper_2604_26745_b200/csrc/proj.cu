@@ -277,6 +277,21 @@ struct CornerT<false> {
     using T = float2;
 };
 
+// explicit shared-memory corner loads from a 32-bit shared-space address (+ an immediate byte offset)
+template <int OFF>
+__device__ __forceinline__ void lds_c(float4& v, uint32_t a)
+{
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4+%5];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(a), "n"(OFF)
+                 : "memory");
+}
+template <int OFF>
+__device__ __forceinline__ void lds_c(float2& v, uint32_t a)
+{
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2+%3];" : "=f"(v.x), "=f"(v.y) : "r"(a), "n"(OFF) : "memory");
+}
+
 struct StateA {
     float s, sc, g, gc, ds, dg, dgc;
     float p1, p1c, p2, p2c, p3, p3c;   // PAIRED: sums over e^{+A_i} for the reverse-direction ray
@@ -334,7 +349,7 @@ __device__ __forceinline__ int band_steps(int i, int ilo, int64_t v, int64_t dV,
 // VAR (model variant N3, reading R-N3): cw is the lane's row [n_t] of (W_j(d_i), c_i); E_i = e^{-c_i A_i},
 // the forward / JVP sums carry W_j(d_i), the adjoint's G carries W c (G_c = sum W lam c E).
 template <int MODE, bool PAIRED, bool VAR = false>
-__device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int P, int r0, int r1, int ilo,
+__device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int Pb, int r0, int r1, int ilo,
                                        int64_t dU, int64_t dV, float cf, float ch, float dl, float dlh, int& i,
                                        int64_t& u, int64_t& v, StateA& st, const float2* __restrict__ cw = nullptr)
 {
@@ -343,19 +358,28 @@ __device__ __forceinline__ void walk_a(const unsigned char* __restrict__ sb, int
     const int iv0 = hi32(v);
     if (i < ilo || iv0 < r0 || iv0 >= r1) return;
     int n = band_steps(i, ilo, v, dV, r0, r1);
-    const Cn* img = reinterpret_cast<const Cn*>(sb);
-    // the band's origin: element (row iv, column iu) at org + iv * P + iu (one base register instead of
-    // r0, which the 72-register builds otherwise recompute per sample)
-    int r0o = r0;
-    asm volatile("" : "+r"(r0o));   // opaque: kept in a register, not recomputed from the unit per sample
-    const Cn* org = img - r0o * P;
-    [[maybe_unused]] const int o_first = r0o * P;   // ok false (the band's last sample has no successor here): load the
-                                  // band's first cell instead of branching around the loads
+    // byte addressing from the band's origin (as the cached scatter's P4/planeB4): element (row iv, column iu) at
+    // orgb + iv * Pb + iu * sizeof(Cn), Pb = P * sizeof(Cn) a constant-bank operand, the origin one opaque
+    // register -- one IMAD (the FMA pipe, which bounds these kernels) per sample address instead of four
+    constexpr int SH = TR::NF4 ? 4 : 3;
+    static_assert(sizeof(Cn) == (1 << SH), "corner size");
+    // the band's origin as a shared-space address in one opaque register (not re-associated, not recomputed
+    // from the unit per sample); the loads are explicit ld.shared from 32-bit addresses
+    const uint32_t sba = smem_u32(sb);
+    uint32_t orga = sba - static_cast<uint32_t>(r0 * Pb);
+    asm volatile("" : "+r"(orga));
+    // ok false (the band's last sample has no successor here): load the band's first cell instead of branching
+    // around the loads
     auto load = [&](SmpA<TR::NF4>& x, int64_t uu, int64_t vv, int ivv, bool ok = true) {
-        int o = ivv * P + hi32(uu);
-        o = ok ? o : o_first;
-        PGET_CHECK(o - o_first >= 0 && o - o_first + P + 1 < (r1 - r0 + 1) * P);
-        x.c00 = org[o]; x.c01 = org[o + 1]; x.c10 = org[o + P]; x.c11 = org[o + P + 1];
+        uint32_t q = static_cast<uint32_t>(ivv * Pb) + orga;
+        q += static_cast<uint32_t>(hi32r(uu)) << SH;
+        q = ok ? q : sba;
+        PGET_CHECK(q >= sba && (q - sba) + Pb + (1 << SH) < static_cast<uint32_t>((r1 - r0 + 1) * Pb));
+        const uint32_t q1 = q + static_cast<uint32_t>(Pb);
+        lds_c<0>(x.c00, q);
+        lds_c<(1 << SH)>(x.c01, q);
+        lds_c<0>(x.c10, q1);
+        lds_c<(1 << SH)>(x.c11, q1);
         x.fu = frac23(uu);
         x.fv = frac23(vv);
     };
@@ -802,7 +826,7 @@ __global__ void __launch_bounds__(ModeTraits<MODE>::W * 32, ModeTraits<MODE>::MI
                 const unsigned char* sb = stage0 + b * A.stage_bytes;
 #pragma unroll
                 for (int k = 0; k < MAXG; ++k) {
-                    walk_a<MODE, PAIRED, VAR>(sb, P, r0, r1, ilo[k], dU, dV, cf, ch, dl, dlh, ii[k], uu[k], vv[k], st[k],
+                    walk_a<MODE, PAIRED, VAR>(sb, TR::NF4 ? A.P16 : A.P8, r0, r1, ilo[k], dU, dV, cf, ch, dl, dlh, ii[k], uu[k], vv[k], st[k],
                                               cwa[k]);
                     if (PAIRED) fold_a(st[k]);
                 }
@@ -1070,7 +1094,7 @@ __global__ void __launch_bounds__(WIDE ? 864 : 512, 1) seg_a_kernel(ProjArgs A) 
     const int64_t sb0 = A.s_begin[c];
     const int64_t n_stages = A.s_begin[c + 1] - sb0;
     if (n_stages == 0) return;
-    const int P = A.P, R = A.R, Rb = A.RbA;
+    const int R = A.R, Rb = A.RbA;
     if (tid == 0) {
         for (int b = 0; b < kSegAStages; ++b) {
             mbar_init(&full[b], 1);
@@ -1122,7 +1146,7 @@ __global__ void __launch_bounds__(WIDE ? 864 : 512, 1) seg_a_kernel(ProjArgs A) 
                 const unsigned char* sbuf = stage0 + b * A.stage_bytes;
 #pragma unroll
                 for (int k = 0; k < MAXG; ++k) {
-                    walk_a<MODE, PAIRED>(sbuf, P, r0, r1, ilo[k], dU, dV, cf, ch, dl, dlh, ii[k], uu[k], vv[k], st[k]);
+                    walk_a<MODE, PAIRED>(sbuf, TR::NF4 ? A.P16 : A.P8, r0, r1, ilo[k], dU, dV, cf, ch, dl, dlh, ii[k], uu[k], vv[k], st[k]);
                     if (PAIRED) fold_a(st[k]);
                 }
                 __syncwarp();
