@@ -337,11 +337,16 @@ __device__ __forceinline__ int band_steps(int i, int ilo, int64_t v, int64_t dV,
     const int64_t num = dV > 0 ? v - (static_cast<int64_t>(r0) << 32)
                                : ((static_cast<int64_t>(r1) << 32) - 1) - v;   // >= 0: v is inside
     const int64_t adV = dV > 0 ? dV : -dV;
-    // further steps inside = floor(num / |dV|): a double quotient (both exact below 2^53), fixed up
-    // exactly (a 64-bit integer division is a long subroutine, and a band is only tens of samples)
-    int64_t k = static_cast<int64_t>(__ddiv_rz(static_cast<double>(num), static_cast<double>(adV)));
+    // further steps inside = floor(num / |dV|): an fp32 estimate (relative error < 2^-21; a band is at most a
+    // few hundred samples, so the estimate is within one of the quotient), fixed up exactly in 64-bit integers
+    // -- the fp64 division it replaces was a ~45-instruction subroutine plus 64-bit int <-> double conversions
+    // per band and lane; a 64-bit integer division is longer still
+    float rcp;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rcp) : "f"(__ll2float_rn(adV)));
+    int64_t k = static_cast<int64_t>(static_cast<int>(__ll2float_rn(num) * rcp));
     if ((k + 1) * adV <= num) ++k;
     else if (k * adV > num) --k;
+    PGET_CHECK(k >= 0 && k * adV <= num && (k + 1) * adV > num);
     const int64_t n = i - ilo + 1;
     return static_cast<int>(k + 1 < n ? k + 1 : n);
 }
