@@ -113,10 +113,14 @@ constexpr int kSegFields = 9;
 // rows of 32 entries allocated past the end of the GN coefficient cache: gnb_kernel's entry ring and
 // L2 prefetch read ahead of a lane's last sample without bounds checks (the values are never used)
 constexpr int kCachePadRows = 16;
+// stage buffers of the warp-specialised phase A.  Two (double buffering) leave bands half again as tall as three
+// in the same shared memory (config 4: 26 rows instead of 17), and the per-band costs (band_steps, fold_a, the
+// barrier hand-over) weigh more than the third buffer's slack: config 4 forward 0.252 -> 0.242 ms, JVP 0.689 ->
+// 0.663 ms, LM 22.16 -> 21.87 ms; four: 0.256 / 0.696 / 22.24 ms (profiles/ab_r02nn_stages.txt)
 #ifndef PGET_SEGA_STAGES
-#define PGET_SEGA_STAGES 3
+#define PGET_SEGA_STAGES 2
 #endif
-constexpr int kSegAStages = PGET_SEGA_STAGES;   // stage buffers of the warp-specialised phase A   // s, sc, g, gc, ds, dg, p1, p2, p3 (see seg_a_kernel)
+constexpr int kSegAStages = PGET_SEGA_STAGES;   // kSegFields: s, sc, g, gc, ds, dg, p1, p2, p3 (see seg_a_kernel)
 
 struct CGState {
     double zeta, a, bcg;
