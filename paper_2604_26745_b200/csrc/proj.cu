@@ -1786,6 +1786,26 @@ __device__ __forceinline__ void red_s32(uint32_t addr, int v)
 {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
+// The cached scatter's entry stream is read once per product: with PGET_GNB_EF its loads carry an L2 evict-first
+// policy, so the stream does not push the CTA-private slot partials (re-read and re-written by every unit's
+// flush, then read by the slot reduction) out of L2.
+#ifndef PGET_GNB_EF
+#define PGET_GNB_EF 0
+#endif
+__device__ __forceinline__ float4 ldg_entry(const float4* p)
+{
+#if PGET_GNB_EF
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    float4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
 template <bool INTACC>
 __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0, int r1, int ilo,
                                          int64_t dU, int64_t dV, float wr, float wr1, int& i, int64_t& u, int64_t& v,
@@ -1830,7 +1850,7 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
     float2 p00 = z2, p01 = z2, p10 = z2, p11 = z2;
     const float4* const p0 = ck;
     int k = 0;   // entry row of the current sample, relative to p0
-    float4 c0 = __ldg(p0), c1 = __ldg(p0 + 32), c2 = __ldg(p0 + 64), c3 = __ldg(p0 + 96);
+    float4 c0 = ldg_entry(p0), c1 = ldg_entry(p0 + 32), c2 = ldg_entry(p0 + 64), c3 = ldg_entry(p0 + 96);
     const float2 w2 = make_float2(wr, wr), w12 = make_float2(wr1, wr1);
     auto step = [&](float4& c) -> bool {
         const int iv = hi32(v);
@@ -1844,7 +1864,7 @@ __device__ __forceinline__ void walk_gnb(float2* __restrict__ acc, int P, int r0
         c = __ldg(p0 + (((k + 4) & 3) << 5));
 #else
         asm volatile("prefetch.global.L2 [%0];" ::"l"(p0 + ((k + PGET_PF_DIST) << 5)));
-        c = __ldg(p0 + ((k + 4) << 5));
+        c = ldg_entry(p0 + ((k + 4) << 5));
 #endif
         ++k;
         const float2 nav = make_float2(-av.x, -av.y);
